@@ -1,0 +1,131 @@
+"""CPU oracle for the MRA log-likelihood -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / `--impl reference`
+leg may import this package. The product (paper_1905_00141_b200) never imports it and
+shares no code with it.
+
+  oracle.run(...)       -> the recursion (oracle/mra_oracle.c, plain C + OpenMP)
+  oracle.plan(...)      -> the oracle's own partition / knots / leaf assignment
+  oracle.dense          -> the dense definition of Sigma_MRA, tiny inputs
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "mra_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+E_OVER_100 = math.e / 100.0
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle (gcc, -O2, OpenMP, no FMA contraction so the plan formulas are
+    evaluated exactly as written)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-shared", "-fPIC",
+               "-o", _LIB + ".tmp", _SRC, "-lm"]
+        subprocess.check_call(cmd)
+        os.replace(_LIB + ".tmp", _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB)
+        D = ctypes.POINTER(ctypes.c_double)
+        I64 = ctypes.POINTER(ctypes.c_int64)
+        lib.oracle_run.restype = ctypes.c_int
+        lib.oracle_run.argtypes = [D, D, D, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                   ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int,
+                                   ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int,
+                                   ctypes.c_int64, D, D, D, D, D, D, D, D, I64, ctypes.c_int]
+        lib.oracle_plan.restype = ctypes.c_int
+        lib.oracle_plan.argtypes = [D, D, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                    ctypes.c_double, ctypes.POINTER(ctypes.c_int), I64, I64, D, D, D]
+        lib.oracle_threads.restype = ctypes.c_int
+        _lib = lib
+    return _lib
+
+
+def _p(a):
+    if a is None:
+        return None
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double if a.dtype == np.float64 else ctypes.c_int64))
+
+
+def threads() -> int:
+    return int(_load().oracle_threads())
+
+
+class OracleError(RuntimeError):
+    pass
+
+
+def plan(x, y, M, J, r, offset=E_OVER_100):
+    lib = _load()
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    n = x.shape[0]
+    nreg = (J ** M - 1) // (J - 1)
+    nint = (J ** (M - 1) - 1) // (J - 1)
+    rh = ctypes.c_int()
+    nr = ctypes.c_int64()
+    leaf = np.empty(n, dtype=np.int64)
+    boxes = np.empty(4 * nreg)
+    # rh <= r
+    kx = np.empty(max(1, nint * r))
+    ky = np.empty(max(1, nint * r))
+    rc = lib.oracle_plan(_p(x), _p(y), n, M, J, r, offset, ctypes.byref(rh), ctypes.byref(nr),
+                         _p(leaf), _p(boxes), _p(kx), _p(ky))
+    if rc not in (0, -3):
+        raise OracleError(f"oracle_plan failed: {rc}")
+    rh = rh.value
+    return dict(r_hat=rh, n_regions=nr.value, leaf=leaf, boxes=boxes.reshape(nreg, 4),
+                knots_x=kx[: nint * rh].reshape(nint, rh), knots_y=ky[: nint * rh].reshape(nint, rh))
+
+
+def run(x, y, z, M, J, r, theta, offset=E_OVER_100, xscale=1.0, yscale=1.0, target=None,
+        regions=False, posterior=False, nthreads=0):
+    """Run the recursion. theta = (cov, sigma2, rho, tau2). target = (level, index) evaluates
+    one subtree only (its d, u). Returns a dict with loglik, d, u, n_retained and optional
+    per-region d/u, mu, xq (E[X(q)|y] at knots) and smooth (E[X(s_i)|y])."""
+    lib = _load()
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    z = np.ascontiguousarray(z, dtype=np.float64)
+    n = x.shape[0]
+    cov, s2, rho, t2 = theta
+    nreg = (J ** M - 1) // (J - 1)
+    nint = (J ** (M - 1) - 1) // (J - 1)
+    nx = math.isqrt(r - 1) + 1 if r > 1 else 1
+    rh = nx * (r // nx)
+    ll, d, u = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    nret = ctypes.c_int64()
+    rd = np.empty(nreg) if regions else None
+    ru = np.empty(nreg) if regions else None
+    mu = np.empty(max(1, nint * rh)) if posterior else None
+    xq = np.empty(max(1, nint * rh)) if posterior else None
+    sm = np.empty(n) if posterior else None
+    tl, tt = (0, 0) if target is None else target
+    rc = lib.oracle_run(_p(x), _p(y), _p(z), n, M, J, r, offset, xscale, yscale, int(cov), float(s2),
+                        float(rho), float(t2), int(tl), int(tt), ctypes.byref(ll), ctypes.byref(d),
+                        ctypes.byref(u), _p(rd), _p(ru), _p(mu), _p(xq), _p(sm), ctypes.byref(nret),
+                        int(nthreads))
+    if rc != 0:
+        raise OracleError(f"oracle_run failed: {rc}")
+    out = dict(loglik=ll.value, d=d.value, u=u.value, n_retained=nret.value, r_hat=rh)
+    if regions:
+        out["region_d"], out["region_u"] = rd, ru
+    if posterior:
+        out["mu"] = mu[: nint * rh].reshape(nint, rh)
+        out["xq"] = xq[: nint * rh].reshape(nint, rh)
+        out["smooth"] = sm
+    return out
