@@ -1,0 +1,155 @@
+/*
+ * mra.h -- C ABI of the B200-native MRA log-likelihood library (libmra_b200.so).
+ *
+ * The hot path of arXiv:1905.00141: evaluating the
+ * multi-resolution-approximation (MRA) Gaussian-process log-likelihood and its
+ * posterior state over a multi-resolution region tree, for a fixed partition and
+ * covariance parameters theta. All arithmetic is fp64 (64-bit reals).
+ *
+ * Conventions for every entry point
+ *   - Plain pointers and sizes only. "host" pointers are ordinary CPU memory; "device"
+ *     pointers are CUDA global memory on the plan's device.
+ *   - Inputs are borrowed for the duration of the call (copied if kept). Outputs are
+ *     caller-allocated.
+ *   - No call aborts. Each returns an mra_status; mra_last_error() (thread-local) then
+ *     names the argument, the region (level, index) or the CUDA call that failed.
+ *   - A plan is single-entrant: one call at a time per plan.
+ *   - There is no CPU fallback: every evaluation step runs in the library's sm_100a kernels;
+ *     with no usable CUDA device the calls return MRA_E_CUDA.
+ */
+#ifndef MRA_B200_H
+#define MRA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mra_plan mra_plan;   /* opaque; owns host + device state of one partition */
+
+typedef enum {
+    MRA_OK = 0,
+    MRA_E_ARG = 1,      /* NULL/NaN/Inf input, theta <= 0, bad size                      */
+    MRA_E_CONFIG = 2,   /* J not in {2,4}, M < 1, r < 1, r_hat > 64        */
+    MRA_E_STRUCT = 3,   /* degenerate bounding box, or every observation eliminated      */
+    MRA_E_NUMERIC = 4,  /* a Cholesky factorization failed (not positive definite)       */
+    MRA_E_CUDA = 5,     /* CUDA runtime error / no device                                  */
+    MRA_E_OOM = 6       /* device allocation failed                                        */
+} mra_status;
+
+typedef enum {
+    MRA_COV_EXP = 0,       /* sigma2 * exp(-d / rho)           ("exponential")   */
+    MRA_COV_MATERN32 = 1   /* sigma2 (1 + sqrt3 d/rho) exp(-sqrt3 d/rho)  (BASELINE C2; DESIGN R3) */
+} mra_cov;
+
+/* Covariance parameters theta (PAPER.md:278 ALPHA/BETA/TAU; reading R2: tau2 is the
+   nugget VARIANCE, added to the diagonal of the finest-level (observation) blocks only). */
+typedef struct {
+    int cov;          /* mra_cov */
+    double sigma2;    /* sill, > 0 */
+    double rho;       /* range, > 0 */
+    double tau2;      /* nugget variance, > 0 */
+} mra_theta;
+
+/* Plan options. Zero-initialised struct or NULL = defaults. */
+typedef struct {
+    double offset;    /* knot margin ratio in (0, 0.5); 0 = default e/100        */
+    double xscale;    /* distance scaling of x differences; 0 = 1 (DESIGN reading R4)           */
+    double yscale;    /* distance scaling of y differences; 0 = 1                                */
+    int device;       /* CUDA device ordinal; -1 = current device; -2 = host-only plan (structure
+                         only, the paper's build_structure_only mode PAPER.md:228: info/layout work,
+                         evaluations return MRA_E_CUDA)                                          */
+    void* stream;     /* cudaStream_t all work is issued on (e.g. torch's current stream); NULL = legacy default */
+    int rank, world;  /* subtree sharding: this process evaluates the subtrees   */
+                      /* assigned to `rank` of `world`; world <= 1 = the whole tree              */
+    int shard_level;  /* level whose regions are the shards; 0 = auto (first level with >= 8*world regions) */
+    double mem_budget_gb; /* device memory budget for the chunked bottom pass; 0 = auto        */
+} mra_opts;
+
+/* Posterior state requested from an evaluation; any pointer may be NULL. */
+typedef struct {
+    double* mu;       /* [n_interior * r_hat] E[eta_R | y] per pre-finest region R, level-major
+                         region order, in the paper's parametrization eta_R ~ N(0, C_m(Q,Q)^{-1})
+                         (PAPER.md:93-97). host pointer for mra_loglik, device for _dev        */
+    double* smooth;   /* [n] E[X(s_i) | y] at each observation, ORIGINAL input order, NaN for
+                         eliminated observations. host / device as above                       */
+    double* region_d; /* [n_regions] per-region log-det term d_R (diagnostics/parity), host    */
+    double* region_u; /* [n_regions] per-region quadratic term u_R, host                        */
+    double d, u;      /* root terms: log|Sigma_MRA + tau2 I| and y^T (Sigma_MRA + tau2 I)^{-1} y */
+} mra_post;
+
+/* Build the partition, knots and observation order, upload them, and size
+ * the device buffers. x, y: host arrays of n coordinates (the paper's lon, lat).
+ * M >= 1 levels, J in {2,4} children per region, r >= 1 requested knots (r_hat =
+ * ceil(sqrt r) * floor(r / ceil(sqrt r)) are placed; r_hat <= 64 in this build).
+ * Observations located exactly at a pre-finest knot are eliminated.
+ * On success *out owns the plan; release it with mra_plan_destroy. */
+mra_status mra_plan_create(const double* x, const double* y, uint64_t n, int M, int J, int r,
+                           const mra_opts* opts, mra_plan** out);
+
+/* Evaluate log L = -1/2 (N log 2pi + log|Sigma_MRA + tau2 I| + y^T (Sigma_MRA + tau2 I)^{-1} y)
+ * (N = retained observations) by the prior pass (top-down) and the posterior pass (bottom-up)
+ * of the MRA recursion (north_star).
+ *   y      : HOST array of n observed values in the ORIGINAL order given to mra_plan_create.
+ *   theta  : covariance parameters.
+ *   loglik : out, host scalar. With world > 1 only rank 0 receives the value (others get NaN);
+ *            use the _shard / _finish pair below for the collective.
+ *   post   : optional posterior state (host pointers), NULL = log L only.
+ * Host<->device copies of y and of the outputs happen inside the call. */
+mra_status mra_loglik(mra_plan* plan, const double* y, const mra_theta* theta, double* loglik,
+                      mra_post* post);
+
+/* Same with y (and post->mu / post->smooth) as DEVICE pointers on the plan's device. */
+mra_status mra_loglik_dev(mra_plan* plan, const double* d_y, const mra_theta* theta,
+                          double* loglik, mra_post* post);
+
+/* Evaluate n_theta parameter sets on the same data (likelihood sweep, e.g. C4's 4x4 grid);
+ * loglik[n_theta] host output. y is a DEVICE pointer. */
+mra_status mra_loglik_batch_dev(mra_plan* plan, const double* d_y, const mra_theta* theta,
+                                int n_theta, double* loglik);
+
+/* Multi-GPU subtree sharding, one process per GPU:
+ *   mra_shard_size(plan)          -> doubles in the exchange buffer (same on every rank)
+ *   mra_loglik_shard(plan, d_y, theta, d_xbuf)
+ *        evaluates this rank's subtrees and writes their shard-root outputs into the
+ *        zero-initialised DEVICE buffer d_xbuf (slots of other ranks stay zero);
+ *   <the caller sum-reduces d_xbuf to rank 0, e.g. ncclReduce / torch.distributed.reduce>
+ *   mra_loglik_finish(plan, theta, d_xbuf, loglik)   (rank 0) merges the levels above the
+ *        shard level and returns log L. */
+uint64_t mra_shard_size(const mra_plan* plan);
+mra_status mra_loglik_shard(mra_plan* plan, const double* d_y, const mra_theta* theta,
+                            double* d_xbuf);
+mra_status mra_loglik_finish(mra_plan* plan, const mra_theta* theta, const double* d_xbuf,
+                             double* loglik);
+
+/* Plan statistics (the paper's build_structure_only report): any pointer may
+ * be NULL. n_regions = (J^M - 1)/(J - 1), n_leaves = J^(M-1). */
+mra_status mra_plan_info(const mra_plan* plan, uint64_t* n_retained, int* r_hat,
+                         uint64_t* n_regions, uint64_t* n_leaves, uint64_t* n_empty_leaves,
+                         uint64_t* max_leaf);
+
+/* Copies of the plan's host-side layout: perm[n_retained] (sorted position -> original index),
+ * leaf_off[n_leaves + 1] (CSR offsets of each leaf in sorted order), knots x/y
+ * [n_interior * r_hat] (level-major). Any pointer may be NULL. */
+mra_status mra_plan_layout(const mra_plan* plan, int64_t* perm, int64_t* leaf_off,
+                           double* knots_x, double* knots_y);
+
+/* Shard assignment of a sharded plan (world > 1): the shard level and the level-shard_level
+ * region indices this rank owns (longest-processing-time assignment on the per-leaf flop model,
+ * the GPU analogue of the paper's sum n_j^2 dynamic split). own may be NULL. */
+mra_status mra_plan_shards(const mra_plan* plan, int* shard_level, int64_t* own, uint64_t* n_own);
+
+/* Number of kernel launches issued by the last evaluation call on this plan. */
+uint64_t mra_last_launches(const mra_plan* plan);
+
+void mra_plan_destroy(mra_plan* plan);
+
+/* Thread-local text of the last error ("" if none). */
+const char* mra_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MRA_B200_H */

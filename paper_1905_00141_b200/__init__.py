@@ -1,0 +1,289 @@
+"""B200-native MRA log-likelihood (arXiv:1905.00141) -- thin Python binding of libmra_b200.so.
+
+Argument marshalling only: every evaluation step runs in the library's sm_100a kernels
+(include/mra.h). The functions carry the C-ABI names:
+
+    mra_plan_create(x, y, M, J, r, **opts) -> handle
+    mra_loglik(plan, y_host, theta, posterior=False, regions=False)
+    mra_loglik_dev(plan, y_tensor_cuda, theta, ...)
+    mra_loglik_batch_dev(plan, y_tensor_cuda, thetas)
+    mra_shard_size / mra_loglik_shard / mra_loglik_finish       (multi-GPU subtree sharding)
+    mra_plan_info / mra_plan_layout / mra_last_launches / mra_plan_destroy
+
+theta = (cov, sigma2, rho, tau2) with cov 0 = exponential, 1 = Matern-3/2.
+There is no CPU fallback: if the CUDA library is missing or no GPU is visible these raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmra_b200.so")
+
+COV_EXP = 0
+COV_MATERN32 = 1
+E_OVER_100 = math.e / 100.0
+
+
+class MraError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"mra status {status}: {msg}")
+        self.status = status
+
+
+class _Theta(ctypes.Structure):
+    _fields_ = [("cov", ctypes.c_int), ("sigma2", ctypes.c_double), ("rho", ctypes.c_double),
+                ("tau2", ctypes.c_double)]
+
+
+class _Opts(ctypes.Structure):
+    _fields_ = [("offset", ctypes.c_double), ("xscale", ctypes.c_double), ("yscale", ctypes.c_double),
+                ("device", ctypes.c_int), ("stream", ctypes.c_void_p), ("rank", ctypes.c_int),
+                ("world", ctypes.c_int), ("shard_level", ctypes.c_int), ("mem_budget_gb", ctypes.c_double)]
+
+
+class _Post(ctypes.Structure):
+    _fields_ = [("mu", ctypes.c_void_p), ("smooth", ctypes.c_void_p), ("region_d", ctypes.c_void_p),
+                ("region_u", ctypes.c_void_p), ("d", ctypes.c_double), ("u", ctypes.c_double)]
+
+
+_lib = None
+EXPORTS = ["mra_plan_create", "mra_loglik", "mra_loglik_dev", "mra_loglik_batch_dev", "mra_shard_size",
+           "mra_loglik_shard", "mra_loglik_finish", "mra_plan_info", "mra_plan_layout", "mra_plan_shards",
+           "mra_last_launches", "mra_plan_destroy", "mra_last_error"]
+
+
+def load_library(path: str = LIB_PATH):
+    """dlopen libmra_b200.so and declare the C-ABI signatures (no GPU needed to load)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"{path} is missing: build it with `python -m paper_1905_00141_b200.build` "
+                           "(nvcc, sm_100a). There is no CPU fallback.")
+    lib = ctypes.CDLL(path)
+    P = ctypes.c_void_p
+    D = ctypes.POINTER(ctypes.c_double)
+    U64 = ctypes.c_uint64
+    lib.mra_plan_create.restype = ctypes.c_int
+    lib.mra_plan_create.argtypes = [D, D, U64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                    ctypes.POINTER(_Opts), ctypes.POINTER(P)]
+    lib.mra_loglik.restype = ctypes.c_int
+    lib.mra_loglik.argtypes = [P, D, ctypes.POINTER(_Theta), D, ctypes.POINTER(_Post)]
+    lib.mra_loglik_dev.restype = ctypes.c_int
+    lib.mra_loglik_dev.argtypes = [P, P, ctypes.POINTER(_Theta), D, ctypes.POINTER(_Post)]
+    lib.mra_loglik_batch_dev.restype = ctypes.c_int
+    lib.mra_loglik_batch_dev.argtypes = [P, P, ctypes.POINTER(_Theta), ctypes.c_int, D]
+    lib.mra_shard_size.restype = U64
+    lib.mra_shard_size.argtypes = [P]
+    lib.mra_loglik_shard.restype = ctypes.c_int
+    lib.mra_loglik_shard.argtypes = [P, P, ctypes.POINTER(_Theta), P]
+    lib.mra_loglik_finish.restype = ctypes.c_int
+    lib.mra_loglik_finish.argtypes = [P, ctypes.POINTER(_Theta), P, D]
+    lib.mra_plan_info.restype = ctypes.c_int
+    lib.mra_plan_info.argtypes = [P, ctypes.POINTER(U64), ctypes.POINTER(ctypes.c_int), ctypes.POINTER(U64),
+                                  ctypes.POINTER(U64), ctypes.POINTER(U64), ctypes.POINTER(U64)]
+    lib.mra_plan_layout.restype = ctypes.c_int
+    lib.mra_plan_layout.argtypes = [P, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64), D, D]
+    lib.mra_plan_shards.restype = ctypes.c_int
+    lib.mra_plan_shards.argtypes = [P, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int64),
+                                    ctypes.POINTER(U64)]
+    lib.mra_last_launches.restype = U64
+    lib.mra_last_launches.argtypes = [P]
+    lib.mra_plan_destroy.restype = None
+    lib.mra_plan_destroy.argtypes = [P]
+    lib.mra_last_error.restype = ctypes.c_char_p
+    lib.mra_last_error.argtypes = []
+    _lib = lib
+    return lib
+
+
+def _check(status):
+    if status != 0:
+        raise MraError(status, _lib.mra_last_error().decode())
+
+
+def _dptr(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _theta(theta):
+    cov, s2, rho, t2 = theta
+    return _Theta(int(cov), float(s2), float(rho), float(t2))
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return stream
+    return int(stream.cuda_stream)
+
+
+class PlanHandle:
+    """Owning handle of an mra_plan (destroyed on close / garbage collection)."""
+
+    def __init__(self, ptr, n, M, J, r):
+        self.ptr = ptr
+        self.n, self.M, self.J, self.r = n, M, J, r
+        info = mra_plan_info(self)
+        self.n_retained = info["n_retained"]
+        self.r_hat = info["r_hat"]
+        self.n_regions = info["n_regions"]
+        self.n_leaves = info["n_leaves"]
+        self.n_interior = self.n_regions - self.n_leaves
+
+    def close(self):
+        if self.ptr:
+            _lib.mra_plan_destroy(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def mra_plan_create(x, y, M, J, r, offset=0.0, xscale=0.0, yscale=0.0, device=-1, stream=None, rank=0,
+                    world=1, shard_level=0, mem_budget_gb=0.0) -> PlanHandle:
+    lib = load_library()
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    if x.shape != y.shape or x.ndim != 1:
+        raise ValueError("x and y must be 1-D arrays of equal length")
+    opts = _Opts(float(offset), float(xscale), float(yscale), int(device), _stream_ptr(stream), int(rank),
+                 int(world), int(shard_level), float(mem_budget_gb))
+    out = ctypes.c_void_p()
+    _check(lib.mra_plan_create(_dptr(x), _dptr(y), x.shape[0], int(M), int(J), int(r), ctypes.byref(opts),
+                               ctypes.byref(out)))
+    return PlanHandle(out.value, x.shape[0], M, J, r)
+
+
+def _post_struct(plan, posterior, regions, host, device=None):
+    bufs = {}
+    post = _Post()
+    if posterior:
+        nmu = max(1, plan.n_interior * plan.r_hat)
+        if host:
+            bufs["mu"] = np.empty(nmu)
+            bufs["smooth"] = np.empty(plan.n)
+            post.mu = bufs["mu"].ctypes.data
+            post.smooth = bufs["smooth"].ctypes.data
+        else:
+            import torch
+            bufs["mu"] = torch.empty(nmu, dtype=torch.float64, device=device)
+            bufs["smooth"] = torch.empty(plan.n, dtype=torch.float64, device=device)
+            post.mu = bufs["mu"].data_ptr()
+            post.smooth = bufs["smooth"].data_ptr()
+    if regions:
+        bufs["region_d"] = np.empty(plan.n_regions)
+        bufs["region_u"] = np.empty(plan.n_regions)
+        post.region_d = bufs["region_d"].ctypes.data
+        post.region_u = bufs["region_u"].ctypes.data
+    return post, bufs
+
+
+def _result(plan, ll, post, bufs, posterior):
+    out = {"loglik": ll.value, "d": post.d, "u": post.u, "n_retained": plan.n_retained}
+    if "region_d" in bufs:
+        out["region_d"], out["region_u"] = bufs["region_d"], bufs["region_u"]
+    if posterior:
+        out["mu"] = bufs["mu"][: plan.n_interior * plan.r_hat].reshape(plan.n_interior, plan.r_hat)
+        out["smooth"] = bufs["smooth"]
+    return out
+
+
+def mra_loglik(plan: PlanHandle, y, theta, posterior=False, regions=False):
+    """Host y (original order) -> dict(loglik, d, u[, region_d, region_u][, mu, smooth])."""
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    if y.shape[0] != plan.n:
+        raise ValueError("y has the wrong length")
+    th = _theta(theta)
+    ll = ctypes.c_double()
+    post, bufs = _post_struct(plan, posterior, regions, host=True)
+    _check(_lib.mra_loglik(plan.ptr, _dptr(y), ctypes.byref(th), ctypes.byref(ll), ctypes.byref(post)))
+    return _result(plan, ll, post, bufs, posterior)
+
+
+def mra_loglik_dev(plan: PlanHandle, y_dev, theta, posterior=False, regions=False):
+    """y_dev: torch float64 CUDA tensor (original order). Posterior outputs stay on the device."""
+    th = _theta(theta)
+    ll = ctypes.c_double()
+    post, bufs = _post_struct(plan, posterior, regions, host=False, device=y_dev.device)
+    _check(_lib.mra_loglik_dev(plan.ptr, ctypes.c_void_p(y_dev.data_ptr()), ctypes.byref(th), ctypes.byref(ll),
+                               ctypes.byref(post)))
+    return _result(plan, ll, post, bufs, posterior)
+
+
+def mra_loglik_batch_dev(plan: PlanHandle, y_dev, thetas):
+    arr = (_Theta * len(thetas))(*[_theta(t) for t in thetas])
+    out = np.empty(len(thetas))
+    _check(_lib.mra_loglik_batch_dev(plan.ptr, ctypes.c_void_p(y_dev.data_ptr()), arr, len(thetas), _dptr(out)))
+    return out
+
+
+def mra_shard_size(plan: PlanHandle) -> int:
+    return int(_lib.mra_shard_size(plan.ptr))
+
+
+def mra_loglik_shard(plan: PlanHandle, y_dev, theta, xbuf_dev):
+    th = _theta(theta)
+    _check(_lib.mra_loglik_shard(plan.ptr, ctypes.c_void_p(y_dev.data_ptr()), ctypes.byref(th),
+                                 ctypes.c_void_p(xbuf_dev.data_ptr())))
+
+
+def mra_loglik_finish(plan: PlanHandle, theta, xbuf_dev) -> float:
+    th = _theta(theta)
+    ll = ctypes.c_double()
+    _check(_lib.mra_loglik_finish(plan.ptr, ctypes.byref(th), ctypes.c_void_p(xbuf_dev.data_ptr()),
+                                  ctypes.byref(ll)))
+    return ll.value
+
+
+def mra_plan_info(plan: PlanHandle) -> dict:
+    v = [ctypes.c_uint64() for _ in range(5)]
+    rh = ctypes.c_int()
+    _check(_lib.mra_plan_info(plan.ptr, ctypes.byref(v[0]), ctypes.byref(rh), ctypes.byref(v[1]),
+                              ctypes.byref(v[2]), ctypes.byref(v[3]), ctypes.byref(v[4])))
+    return dict(n_retained=v[0].value, r_hat=rh.value, n_regions=v[1].value, n_leaves=v[2].value,
+                n_empty_leaves=v[3].value, max_leaf=v[4].value)
+
+
+def mra_plan_layout(plan: PlanHandle) -> dict:
+    perm = np.empty(plan.n_retained, dtype=np.int64)
+    off = np.empty(plan.n_leaves + 1, dtype=np.int64)
+    nk = max(1, plan.n_interior * plan.r_hat)
+    kx = np.empty(nk)
+    ky = np.empty(nk)
+    _check(_lib.mra_plan_layout(plan.ptr, perm.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                off.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), _dptr(kx), _dptr(ky)))
+    return dict(perm=perm, leaf_off=off, knots_x=kx[: plan.n_interior * plan.r_hat],
+                knots_y=ky[: plan.n_interior * plan.r_hat])
+
+
+def mra_plan_shards(plan: PlanHandle) -> dict:
+    lvl = ctypes.c_int()
+    n = ctypes.c_uint64()
+    _check(_lib.mra_plan_shards(plan.ptr, ctypes.byref(lvl), None, ctypes.byref(n)))
+    own = np.empty(max(1, n.value), dtype=np.int64)
+    _check(_lib.mra_plan_shards(plan.ptr, ctypes.byref(lvl), own.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                ctypes.byref(n)))
+    return dict(shard_level=lvl.value, own=own[: n.value])
+
+
+def mra_last_launches(plan: PlanHandle) -> int:
+    return int(_lib.mra_last_launches(plan.ptr))
+
+
+def mra_plan_destroy(plan: PlanHandle):
+    plan.close()
+
+
+def atilde_bound_gib(J, M, r):
+    """Eq. (1) of PAPER.md:486-488: upper bound of the paper's ATilde memory, J^{M-1} M (M-1) r^2 2^-28 GiB."""
+    return J ** (M - 1) * M * (M - 1) * r * r * 2.0 ** -28

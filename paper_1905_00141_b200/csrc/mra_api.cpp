@@ -1,0 +1,708 @@
+// mra_api.cpp -- C ABI (include/mra.h): host plan builder + level-synchronous scheduler.
+//
+// Plan, built once on the host and uploaded as flat level-major SoA:
+//   root = data bounding box with top/right pushed out 1%; J=4 halves both axes,
+//   J=2 the longer one (ties -> x); r_hat = ceil(sqrt r) * floor(r/ceil(sqrt r))
+//   knots on an offset grid; observations equal to a pre-finest knot are
+//   eliminated; the rest are counting-sorted by leaf (CSR leaf_off, perm).
+// Evaluation: gather y -> prior levels 1..M-1 -> for each chunk of subtrees
+//   rooted at the chunk level c: bottom (leaves + level M-1 merge) and merges M-2..c ->
+//   merges c-1..1 -> log L. Every arithmetic step runs in mra_kernels.cu; this file only
+//   sizes buffers, launches and checks errors.
+#include "../../include/mra.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "mra_internal.h"
+
+using namespace mra;
+
+static thread_local std::string g_err;
+static mra_status fail(mra_status s, const std::string& msg) {
+    g_err = msg;
+    return s;
+}
+
+struct mra_plan {
+    int M = 0, J = 0, lj = 0, r = 0, rh = 0, nx = 0, ny = 0;
+    double offset = 0, xs = 1, ys = 1;
+    uint64_t n_in = 0;
+    long long N = 0, nreg = 0, nint = 0, nleaf = 0, n_empty = 0, max_leaf = 0, max_group = 0;
+    std::vector<long long> perm, leaf_off;
+    std::vector<double> kx, ky;
+    int device = 0, nsm = 148;
+    cudaStream_t st = nullptr;
+    // device state
+    double *px = nullptr, *py = nullptr, *zs = nullptr, *zin = nullptr;
+    long long *perm_d = nullptr, *leaf_off_d = nullptr;
+    double *kx_d = nullptr, *ky_d = nullptr;
+    double* prior = nullptr;
+    long long prior_base[MAXM + 1] = {0};
+    double *dreg = nullptr, *ureg = nullptr, *loglik_d = nullptr;
+    int* err = nullptr;
+    unsigned long long* counters = nullptr;
+    int n_counters = 0, next_counter = 0;
+    // posterior-pass buffers: level m output has q_m = (m-1) rh + 1 rows
+    int c = 1;                       // chunk level
+    long long Kc = 1;                // level-c regions per chunk
+    double* out_full[MAXM + 1] = {nullptr};   // levels 1..c: every region
+    double* out_chunk[MAXM + 1] = {nullptr};  // levels c+1..M-1: one chunk
+    double* ws = nullptr;
+    long long ws_stride = 0;
+    WsLayout L{};
+    int grid = 0;
+    // sharding
+    int rank = 0, world = 1;
+    std::vector<long long> my_c;     // level-c regions owned by this rank (sorted)
+    // posterior state
+    double* post = nullptr;
+    long long post_base[MAXM + 1] = {0};
+    double* muhat = nullptr;
+    double* mu_d = nullptr;
+    double* smooth_d = nullptr;
+    uint64_t launches = 0;
+    std::vector<void*> allocs;
+};
+
+static long long ipow(long long b, int e) {
+    long long v = 1;
+    while (e-- > 0) v *= b;
+    return v;
+}
+static long long lvl_first(int J, int m) { return (ipow(J, m - 1) - 1) / (J - 1); }
+static long long q_of(int m, int rh) { return (long long)(m - 1) * rh + 1; }
+
+#define CU(call)                                                                               \
+    do {                                                                                       \
+        cudaError_t e_ = (call);                                                               \
+        if (e_ != cudaSuccess)                                                                 \
+            return fail(e_ == cudaErrorMemoryAllocation ? MRA_E_OOM : MRA_E_CUDA,              \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));                   \
+    } while (0)
+
+static mra_status dalloc(mra_plan* p, void** ptr, size_t bytes, const char* what) {
+    if (bytes == 0) bytes = 8;
+    cudaError_t e = cudaMalloc(ptr, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        char buf[256];
+        snprintf(buf, sizeof buf, "cudaMalloc(%s, %.3f GB): %s", what, bytes / 1e9, cudaGetErrorString(e));
+        return fail(e == cudaErrorMemoryAllocation ? MRA_E_OOM : MRA_E_CUDA, buf);
+    }
+    p->allocs.push_back(*ptr);
+    return MRA_OK;
+}
+
+// ------------------------------------------------------------------------- plan build
+static double bar_pos(double lo, double hi, int nb, int i, double off) {
+    if (nb == 1) return 0.5 * (lo + hi);
+    const double ext = hi - lo;
+    return lo + off * ext + (double)i * (ext * (1.0 - 2.0 * off) / (double)(nb - 1));
+}
+
+static mra_status build_host(mra_plan* P, const double* x, const double* y, uint64_t n) {
+    const int M = P->M, J = P->J;
+    int nx = 1;
+    while (nx * nx < P->r) nx++;
+    P->nx = nx;
+    P->ny = P->r / nx;
+    P->rh = P->nx * P->ny;
+    if (P->rh > 64) return fail(MRA_E_CONFIG, "r_hat > 64 is not supported by this build");
+    P->nreg = (ipow(J, M) - 1) / (J - 1);
+    P->nint = (ipow(J, M - 1) - 1) / (J - 1);
+    P->nleaf = ipow(J, M - 1);
+    double x0 = x[0], x1 = x[0], y0 = y[0], y1 = y[0];
+    for (uint64_t i = 0; i < n; i++) {
+        if (!std::isfinite(x[i]) || !std::isfinite(y[i])) return fail(MRA_E_ARG, "non-finite location");
+        x0 = std::min(x0, x[i]); x1 = std::max(x1, x[i]);
+        y0 = std::min(y0, y[i]); y1 = std::max(y1, y[i]);
+    }
+    if (!(x1 > x0) || !(y1 > y0)) return fail(MRA_E_STRUCT, "degenerate bounding box (zero extent)");
+    // interior boxes, level-major; root pushed out 1% at top/right
+    std::vector<double> box(4 * std::max<long long>(P->nint, 1));
+    if (P->nint > 0) {
+        box[0] = x0; box[1] = x1 + 0.01 * (x1 - x0);
+        box[2] = y0; box[3] = y1 + 0.01 * (y1 - y0);
+    }
+    for (int m = 1; m + 1 < M; m++) {
+        const long long cnt = ipow(J, m - 1), f = lvl_first(J, m), fc = lvl_first(J, m + 1);
+        for (long long t = 0; t < cnt; t++) {
+            const double* b = &box[4 * (f + t)];
+            const double mx = 0.5 * (b[0] + b[1]), my = 0.5 * (b[2] + b[3]);
+            const bool sx = (b[1] - b[0]) >= (b[3] - b[2]);
+            for (int c = 0; c < J; c++) {
+                double* cb = &box[4 * (fc + t * J + c)];
+                std::memcpy(cb, b, 4 * sizeof(double));
+                if (J == 4) {
+                    if (c & 1) cb[0] = mx; else cb[1] = mx;
+                    if (c & 2) cb[2] = my; else cb[3] = my;
+                } else if (sx) {
+                    if (c) cb[0] = mx; else cb[1] = mx;
+                } else {
+                    if (c) cb[2] = my; else cb[3] = my;
+                }
+            }
+        }
+    }
+    const int rh = P->rh;
+    P->kx.assign(P->nint * rh, 0.0);
+    P->ky.assign(P->nint * rh, 0.0);
+    for (long long id = 0; id < P->nint; id++) {
+        const double* b = &box[4 * id];
+        for (int iy = 0; iy < P->ny; iy++)
+            for (int ix = 0; ix < P->nx; ix++) {
+                P->kx[id * rh + iy * P->nx + ix] = bar_pos(b[0], b[1], P->nx, ix, P->offset);
+                P->ky[id * rh + iy * P->nx + ix] = bar_pos(b[2], b[3], P->ny, iy, P->offset);
+            }
+    }
+    // leaf key by descent; elimination test against each ancestor's bar sets
+    std::vector<long long> key(n);
+#pragma omp parallel for schedule(static)
+    for (long long i = 0; i < (long long)n; i++) {
+        const double px = x[i], py = y[i];
+        long long t = 0;
+        bool elim = false;
+        for (int m = 1; m < M; m++) {
+            const long long id = lvl_first(J, m) + t;
+            const double* b = &box[4 * id];
+            if (!elim) {
+                bool inx = false, iny = false;
+                for (int ix = 0; ix < P->nx && !inx; ix++) inx = (px == P->kx[id * rh + ix]);
+                if (inx)
+                    for (int iy = 0; iy < P->ny && !iny; iy++) iny = (py == P->ky[id * rh + iy * P->nx]);
+                elim = inx && iny;
+            }
+            const double mx = 0.5 * (b[0] + b[1]), my = 0.5 * (b[2] + b[3]);
+            int c;
+            if (J == 4) c = (px >= mx ? 1 : 0) | (py >= my ? 2 : 0);
+            else if ((b[1] - b[0]) >= (b[3] - b[2])) c = px >= mx ? 1 : 0;
+            else c = py >= my ? 1 : 0;
+            t = t * J + c;
+        }
+        key[i] = elim ? -1 : t;
+    }
+    // stable counting sort by leaf
+    P->leaf_off.assign(P->nleaf + 1, 0);
+    for (uint64_t i = 0; i < n; i++)
+        if (key[i] >= 0) P->leaf_off[key[i] + 1]++;
+    P->n_empty = 0;
+    P->max_leaf = 0;
+    for (long long t = 0; t < P->nleaf; t++) {
+        if (P->leaf_off[t + 1] == 0) P->n_empty++;
+        P->max_leaf = std::max(P->max_leaf, P->leaf_off[t + 1]);
+        P->leaf_off[t + 1] += P->leaf_off[t];
+    }
+    P->N = P->leaf_off[P->nleaf];
+    if (P->N == 0) return fail(MRA_E_STRUCT, "every observation was eliminated");
+    std::vector<long long> fill(P->leaf_off.begin(), P->leaf_off.end() - 1);
+    P->perm.assign(P->N, 0);
+    for (uint64_t i = 0; i < n; i++)
+        if (key[i] >= 0) P->perm[fill[key[i]]++] = (long long)i;
+    const int Jc = (M == 1) ? 1 : J;
+    P->max_group = 0;
+    for (long long g = 0; g < P->nleaf / Jc; g++)
+        P->max_group = std::max(P->max_group, P->leaf_off[(g + 1) * Jc] - P->leaf_off[g * Jc]);
+    return MRA_OK;
+}
+
+// ------------------------------------------------------------------- device sizing
+static long long round_up(long long v, long long a) { return (v + a - 1) / a * a; }
+
+static mra_status size_device(mra_plan* P, double budget_gb) {
+    const int M = P->M, J = P->J, rh = P->rh;
+    // prior chain rows
+    long long tot = 0;
+    for (int m = 1; m < M; m++) {
+        P->prior_base[m] = tot;
+        tot += ipow(J, m - 1) * (long long)m * rh * rh;
+    }
+    mra_status s;
+    if ((s = dalloc(P, (void**)&P->prior, sizeof(double) * tot, "prior chain rows"))) return s;
+    // workspace layout (bottom kernel; also covers merge / prior / smooth)
+    const int mg = M - 1, Pg = mg * rh, ncol = Pg + 1;
+    WsLayout L{};
+    L.ldG = (int)round_up(ncol, 2);
+    L.ldS = (int)round_up(std::max<long long>(P->max_leaf, 1), 2);
+    L.ldA = ncol;
+    const long long nb = (std::max<long long>(P->max_leaf, 1) + 63) / 64;
+    long long o = 0;
+    L.oG = o; o += round_up(std::max<long long>(P->max_group, 1) * L.ldG, 32);
+    L.oS = o; o += round_up(std::max<long long>(P->max_leaf, 1) * (long long)L.ldS, 32);
+    L.oD = o; o += nb * 4096;
+    L.oA = o; o += round_up((long long)ncol * ncol, 32);
+    L.oF = o; o += round_up((long long)ncol * rh, 32);
+    L.oL = o; o += round_up((long long)rh * rh, 32);
+    L.oV = o; o += round_up(std::max<long long>(P->max_leaf, 1), 32);
+    // merge at level m <= M-2 needs qc^2 + q rh + rh^2 with qc = m rh + 1
+    long long merge_need = 0;
+    for (int m = 1; m + 2 <= M; m++) {
+        const long long qc = (long long)m * rh + 1, q = q_of(m, rh);
+        merge_need = std::max(merge_need, qc * qc + q * rh + (long long)rh * rh);
+    }
+    L.stride = round_up(std::max<long long>({o, merge_need, (long long)rh * rh}), 64);
+    P->L = L;
+    P->ws_stride = L.stride;
+    size_t freeb = 0, totalb = 0;
+    cudaMemGetInfo(&freeb, &totalb);
+    double budget = budget_gb > 0 ? budget_gb * 1e9 : 0.85 * (double)freeb;
+    budget -= (double)tot * 8.0;
+    // slots: 2 CTAs per SM, fewer if the per-slot workspace is huge
+    long long slots = 2LL * P->nsm;
+    const double ws_cap = std::max(0.25 * budget, (double)L.stride * 8.0);
+    slots = std::min<long long>(slots, std::max<long long>(1, (long long)(ws_cap / (L.stride * 8.0))));
+    P->grid = (int)slots;
+    if ((s = dalloc(P, (void**)&P->ws, sizeof(double) * L.stride * slots, "workspace"))) return s;
+    budget -= (double)L.stride * slots * 8.0;
+    // choose chunk level c and chunk size Kc so the posterior outputs fit
+    const double out_budget = std::max(0.5 * budget, 1e8);
+    auto full_bytes = [&](int c) {
+        double b = 0;
+        for (int m = 1; m <= c && m < M; m++) b += (double)ipow(J, m - 1) * q_of(m, rh) * q_of(m, rh) * 8.0;
+        return b;
+    };
+    auto chunk_bytes = [&](int c, long long Kc) {
+        double b = 0;
+        for (int m = c + 1; m < M; m++) b += (double)Kc * ipow(J, m - c) * q_of(m, rh) * q_of(m, rh) * 8.0;
+        return b;
+    };
+    int c = 1;
+    const int cmax = std::max(1, M - 1);
+    if (P->world > 1) {
+        c = P->c;   // shard level fixed by the caller / auto rule
+    } else {
+        while (c < cmax && full_bytes(c) + chunk_bytes(c, 1) > out_budget) c++;
+    }
+    long long nc = ipow(J, c - 1);
+    long long Kc = nc;
+    while (Kc > 1 && full_bytes(c) + chunk_bytes(c, Kc) > out_budget) Kc = (Kc + 1) / 2;
+    P->c = c;
+    P->Kc = Kc;
+    for (int m = 1; m <= c && m < M; m++)
+        if ((s = dalloc(P, (void**)&P->out_full[m], sizeof(double) * ipow(J, m - 1) * q_of(m, rh) * q_of(m, rh),
+                        "level output")))
+            return s;
+    for (int m = c + 1; m < M; m++)
+        if ((s = dalloc(P, (void**)&P->out_chunk[m], sizeof(double) * Kc * ipow(J, m - c) * q_of(m, rh) * q_of(m, rh),
+                        "chunk output")))
+            return s;
+    return MRA_OK;
+}
+
+// --------------------------------------------------------------------- C ABI entry
+extern "C" const char* mra_last_error(void) { return g_err.c_str(); }
+
+extern "C" mra_status mra_plan_create(const double* x, const double* y, uint64_t n, int M, int J, int r,
+                                      const mra_opts* opts, mra_plan** out) {
+    g_err.clear();
+    if (!out) return fail(MRA_E_ARG, "out is NULL");
+    *out = nullptr;
+    if (!x || !y || n == 0) return fail(MRA_E_ARG, "x/y NULL or n == 0");
+    if (M < 1 || M > MAXM - 1) return fail(MRA_E_CONFIG, "M out of range [1, 22]");
+    if (J != 2 && J != 4) return fail(MRA_E_CONFIG, "J must be 2 or 4 (PAPER.md:100)");
+    if (r < 1) return fail(MRA_E_CONFIG, "r must be >= 1");
+    mra_opts o{};
+    if (opts) o = *opts;
+    mra_plan* P = new mra_plan();
+    P->M = M; P->J = J; P->lj = (J == 4) ? 2 : 1; P->r = r;
+    P->offset = o.offset > 0 ? o.offset : std::exp(1.0) / 100.0;
+    if (!(P->offset > 0 && P->offset < 0.5)) { delete P; return fail(MRA_E_ARG, "offset must be in (0, 0.5)"); }
+    P->xs = o.xscale > 0 ? o.xscale : 1.0;
+    P->ys = o.yscale > 0 ? o.yscale : 1.0;
+    P->n_in = n;
+    P->rank = o.world > 1 ? o.rank : 0;
+    P->world = o.world > 1 ? o.world : 1;
+    mra_status s = build_host(P, x, y, n);
+    if (s) { delete P; return s; }
+    // sharding: shard level = first level with >= 8*world regions (or the caller's choice)
+    if (P->world > 1) {
+        int sl = o.shard_level;
+        if (sl <= 0) { sl = 1; while (sl < M - 1 && ipow(J, sl - 1) < 8LL * P->world) sl++; }
+        if (sl >= M) sl = M - 1;
+        if (sl < 1) { delete P; return fail(MRA_E_CONFIG, "tree too shallow to shard (need M >= 2)"); }
+        P->c = sl;
+        // LPT over the per-shard leaf work (sum n_j^3 + n_j^2 ((M-1) r_hat))
+        const long long ns = ipow(J, sl - 1), per = ipow(J, M - sl);
+        std::vector<std::pair<double, long long>> cost(ns);
+        for (long long s2 = 0; s2 < ns; s2++) {
+            double cst = 0;
+            for (long long l = s2 * per; l < (s2 + 1) * per; l++) {
+                const double nj = (double)(P->leaf_off[l + 1] - P->leaf_off[l]);
+                cst += nj * nj * nj / 3.0 + nj * nj * (M - 1) * P->rh * 2.0 + nj * std::pow((M - 1) * P->rh, 2);
+            }
+            cost[s2] = {cst + 1.0, s2};
+        }
+        std::sort(cost.begin(), cost.end(), [](auto& a, auto& b) { return a.first > b.first || (a.first == b.first && a.second < b.second); });
+        std::vector<double> load(P->world, 0.0);
+        for (auto& cs : cost) {
+            int best = 0;
+            for (int w = 1; w < P->world; w++) if (load[w] < load[best]) best = w;
+            load[best] += cs.first;
+            if (best == P->rank) P->my_c.push_back(cs.second);
+        }
+        std::sort(P->my_c.begin(), P->my_c.end());
+    }
+    if (o.device == -2) {   // host-only plan: structure only (PAPER.md:228 build_structure_only)
+        P->device = -2;
+        *out = P;
+        return MRA_OK;
+    }
+    int dev = o.device;
+    if (dev < 0) {
+        if (cudaGetDevice(&dev) != cudaSuccess) { delete P; return fail(MRA_E_CUDA, "no CUDA device"); }
+    }
+    P->device = dev;
+    if (cudaSetDevice(dev) != cudaSuccess) { delete P; return fail(MRA_E_CUDA, "cudaSetDevice failed (no GPU?)"); }
+    cudaDeviceGetAttribute(&P->nsm, cudaDevAttrMultiProcessorCount, dev);
+    P->st = (cudaStream_t)o.stream;
+    mra_status st;
+#define TRY(x) do { if ((st = (x))) { mra_plan_destroy(P); return st; } } while (0)
+    const long long N = P->N;
+    TRY(dalloc(P, (void**)&P->px, 8 * N, "px"));
+    TRY(dalloc(P, (void**)&P->py, 8 * N, "py"));
+    TRY(dalloc(P, (void**)&P->zs, 8 * N, "zs"));
+    TRY(dalloc(P, (void**)&P->zin, 8 * (long long)n, "zin"));
+    TRY(dalloc(P, (void**)&P->perm_d, 8 * N, "perm"));
+    TRY(dalloc(P, (void**)&P->leaf_off_d, 8 * (P->nleaf + 1), "leaf_off"));
+    TRY(dalloc(P, (void**)&P->kx_d, 8 * std::max<long long>(1, P->nint * P->rh), "kx"));
+    TRY(dalloc(P, (void**)&P->ky_d, 8 * std::max<long long>(1, P->nint * P->rh), "ky"));
+    TRY(dalloc(P, (void**)&P->dreg, 8 * P->nreg, "dreg"));
+    TRY(dalloc(P, (void**)&P->ureg, 8 * P->nreg, "ureg"));
+    TRY(dalloc(P, (void**)&P->loglik_d, 8, "loglik"));
+    TRY(dalloc(P, (void**)&P->err, 16, "err"));
+    P->n_counters = 1 << 16;
+    TRY(dalloc(P, (void**)&P->counters, 8 * (size_t)P->n_counters, "counters"));
+    {
+        std::vector<double> sx(N), sy(N);
+        for (long long i = 0; i < N; i++) { sx[i] = x[P->perm[i]]; sy[i] = y[P->perm[i]]; }
+        auto cp = [&](void* d, const void* h, size_t b) -> mra_status {
+            cudaError_t e = cudaMemcpy(d, h, b, cudaMemcpyHostToDevice);
+            if (e != cudaSuccess) return fail(MRA_E_CUDA, std::string("upload: ") + cudaGetErrorString(e));
+            return MRA_OK;
+        };
+        TRY(cp(P->px, sx.data(), 8 * N));
+        TRY(cp(P->py, sy.data(), 8 * N));
+        TRY(cp(P->perm_d, P->perm.data(), 8 * N));
+        TRY(cp(P->leaf_off_d, P->leaf_off.data(), 8 * (P->nleaf + 1)));
+        if (P->nint) {
+            TRY(cp(P->kx_d, P->kx.data(), 8 * P->nint * P->rh));
+            TRY(cp(P->ky_d, P->ky.data(), 8 * P->nint * P->rh));
+        }
+    }
+    TRY(size_device(P, o.mem_budget_gb));
+#undef TRY
+    *out = P;
+    return MRA_OK;
+}
+
+extern "C" void mra_plan_destroy(mra_plan* P) {
+    if (!P) return;
+    if (P->device >= 0 && cudaSetDevice(P->device) == cudaSuccess) {
+        cudaDeviceSynchronize();
+        for (void* a : P->allocs) cudaFree(a);
+    }
+    delete P;
+}
+
+extern "C" mra_status mra_plan_info(const mra_plan* P, uint64_t* n_retained, int* r_hat, uint64_t* n_regions,
+                                    uint64_t* n_leaves, uint64_t* n_empty, uint64_t* max_leaf) {
+    if (!P) return fail(MRA_E_ARG, "plan is NULL");
+    if (n_retained) *n_retained = (uint64_t)P->N;
+    if (r_hat) *r_hat = P->rh;
+    if (n_regions) *n_regions = (uint64_t)P->nreg;
+    if (n_leaves) *n_leaves = (uint64_t)P->nleaf;
+    if (n_empty) *n_empty = (uint64_t)P->n_empty;
+    if (max_leaf) *max_leaf = (uint64_t)P->max_leaf;
+    return MRA_OK;
+}
+
+extern "C" mra_status mra_plan_layout(const mra_plan* P, int64_t* perm, int64_t* leaf_off, double* kx, double* ky) {
+    if (!P) return fail(MRA_E_ARG, "plan is NULL");
+    if (perm) std::memcpy(perm, P->perm.data(), 8 * P->N);
+    if (leaf_off) std::memcpy(leaf_off, P->leaf_off.data(), 8 * (P->nleaf + 1));
+    if (kx && P->nint) std::memcpy(kx, P->kx.data(), 8 * P->nint * P->rh);
+    if (ky && P->nint) std::memcpy(ky, P->ky.data(), 8 * P->nint * P->rh);
+    return MRA_OK;
+}
+
+extern "C" uint64_t mra_last_launches(const mra_plan* P) { return P ? P->launches : 0; }
+
+extern "C" mra_status mra_plan_shards(const mra_plan* P, int* shard_level, int64_t* own, uint64_t* n_own) {
+    if (!P) return fail(MRA_E_ARG, "plan is NULL");
+    if (shard_level) *shard_level = P->world > 1 ? P->c : 0;
+    if (n_own) *n_own = (uint64_t)P->my_c.size();
+    if (own) for (size_t i = 0; i < P->my_c.size(); i++) own[i] = P->my_c[i];
+    return MRA_OK;
+}
+
+// ------------------------------------------------------------------------ evaluation
+static TreeParams tree_params(mra_plan* P, const mra_theta* th) {
+    TreeParams tp{};
+    tp.M = P->M; tp.J = P->J; tp.lj = P->lj; tp.rh = P->rh;
+    tp.cp.kind = th->cov; tp.cp.s2 = th->sigma2; tp.cp.rho = th->rho; tp.cp.xs = P->xs; tp.cp.ys = P->ys;
+    tp.tau2 = th->tau2;
+    tp.px = P->px; tp.py = P->py; tp.zs = P->zs; tp.leaf_off = P->leaf_off_d;
+    tp.kx = P->kx_d; tp.ky = P->ky_d; tp.prior = P->prior;
+    for (int m = 0; m <= MAXM; m++) { tp.prior_base[m] = P->prior_base[m]; tp.post_base[m] = P->post_base[m]; }
+    tp.dreg = P->dreg; tp.ureg = P->ureg; tp.err = P->err; tp.post = nullptr;
+    return tp;
+}
+
+static mra_status check_theta(const mra_theta* th) {
+    if (!th) return fail(MRA_E_ARG, "theta is NULL");
+    if (th->cov != MRA_COV_EXP && th->cov != MRA_COV_MATERN32) return fail(MRA_E_ARG, "unknown covariance kind");
+    if (!(th->sigma2 > 0) || !(th->rho > 0) || !(th->tau2 > 0) || !std::isfinite(th->sigma2) ||
+        !std::isfinite(th->rho) || !std::isfinite(th->tau2))
+        return fail(MRA_E_ARG, "theta must be finite and > 0");
+    return MRA_OK;
+}
+
+#define LCHK(expr)                                                                           \
+    do {                                                                                     \
+        cudaError_t e_ = (expr);                                                             \
+        P->launches++;                                                                       \
+        if (e_ != cudaSuccess) return fail(MRA_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+static unsigned long long* take_counter(mra_plan* P) { return P->counters + (P->next_counter++ % P->n_counters); }
+
+// ranges of level-m regions under the level-c regions [a, b)
+static void range_at(const mra_plan* P, int m, long long a, long long b, long long* f, long long* cnt) {
+    const long long s = ipow(P->J, m - P->c);
+    *f = a * s;
+    *cnt = (b - a) * s;
+}
+
+// contiguous runs of this rank's level-c regions
+static std::vector<std::pair<long long, long long>> my_runs(const mra_plan* P) {
+    std::vector<std::pair<long long, long long>> runs;
+    if (P->world <= 1) {
+        runs.push_back({0, ipow(P->J, P->c - 1)});
+        return runs;
+    }
+    for (long long s : P->my_c) {
+        if (!runs.empty() && runs.back().second == s) runs.back().second = s + 1;
+        else runs.push_back({s, s + 1});
+    }
+    return runs;
+}
+
+// prior + posterior below (and at) level c for this rank's subtrees
+static mra_status eval_lower(mra_plan* P, const TreeParams& tp) {
+    const int M = P->M, J = P->J, rh = P->rh, c = P->c;
+    cudaStream_t st = P->st;
+    auto runs = my_runs(P);
+    // prior: levels < c for every region, levels >= c for own subtrees
+    for (int m = 1; m < M; m++) {
+        if (m < c) {
+            TreeParams t2 = tp;
+            LCHK(launch_prior(t2, m, 0, ipow(J, m - 1), P->grid, P->ws, P->ws_stride, take_counter(P), st));
+        } else {
+            for (auto& rg : runs) {
+                long long f, cnt;
+                range_at(P, m, rg.first, rg.second, &f, &cnt);
+                LCHK(launch_prior(tp, m, f, cnt, P->grid, P->ws, P->ws_stride, take_counter(P), st));
+            }
+        }
+    }
+    // posterior: chunks of Kc level-c regions
+    for (auto& rg : runs) {
+        for (long long a = rg.first; a < rg.second; a += P->Kc) {
+            const long long b = std::min(rg.second, a + P->Kc);
+            const int mg = M - 1;
+            if (M == 1) {
+                LCHK(launch_bottom(tp, 0, 1, nullptr, 0, 0, P->grid, P->ws, P->L, take_counter(P), st));
+                continue;
+            }
+            long long gf, gc;
+            range_at(P, mg, a, b, &gf, &gc);
+            double* gout = (mg <= c) ? P->out_full[mg] : P->out_chunk[mg];
+            const long long gout_first = (mg <= c) ? 0 : gf;
+            LCHK(launch_bottom(tp, gf, gc, gout, gout_first, (int)q_of(mg, rh), P->grid, P->ws, P->L,
+                               take_counter(P), st));
+            for (int m = mg - 1; m >= c; m--) {
+                long long f, cnt, cf, ccnt;
+                range_at(P, m, a, b, &f, &cnt);
+                range_at(P, m + 1, a, b, &cf, &ccnt);
+                const double* cout_ = (m + 1 <= c) ? P->out_full[m + 1] : P->out_chunk[m + 1];
+                const long long cfirst = (m + 1 <= c) ? 0 : cf;
+                double* o = (m <= c) ? P->out_full[m] : P->out_chunk[m];
+                const long long ofirst = (m <= c) ? 0 : f;
+                LCHK(launch_merge(tp, m, f, cnt, cout_, cfirst, o, ofirst, (int)q_of(m, rh), P->grid, P->ws,
+                                  P->ws_stride, take_counter(P), st));
+            }
+        }
+    }
+    return MRA_OK;
+}
+
+// merges above the chunk level and log L
+static mra_status eval_upper(mra_plan* P, const TreeParams& tp) {
+    const int M = P->M, J = P->J, rh = P->rh, c = P->c;
+    for (int m = std::min(c - 1, M - 2); m >= 1; m--)
+        LCHK(launch_merge(tp, m, 0, ipow(J, m - 1), P->out_full[m + 1], 0, P->out_full[m], 0, (int)q_of(m, rh),
+                          P->grid, P->ws, P->ws_stride, take_counter(P), P->st));
+    LCHK(launch_final(tp, (double)P->N, P->loglik_d, P->st));
+    return MRA_OK;
+}
+
+static mra_status check_err(mra_plan* P) {
+    int h[4];
+    cudaError_t e = cudaMemcpyAsync(h, P->err, 16, cudaMemcpyDeviceToHost, P->st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(P->st);
+    if (e != cudaSuccess) return fail(MRA_E_CUDA, std::string("evaluation: ") + cudaGetErrorString(e));
+    if (h[0]) {
+        long long idx;
+        std::memcpy(&idx, h + 2, 8);
+        char buf[160];
+        snprintf(buf, sizeof buf, "Cholesky failed (matrix not positive definite) at region level %d index %lld",
+                 h[1], idx);
+        return fail(MRA_E_NUMERIC, buf);
+    }
+    return MRA_OK;
+}
+
+static mra_status begin_eval(mra_plan* P, const double* d_y, const mra_theta* th) {
+    g_err.clear();
+    if (P->device < 0) return fail(MRA_E_CUDA, "host-only plan (device -2) cannot evaluate");
+    P->launches = 0;
+    P->next_counter = 0;
+    mra_status s = check_theta(th);
+    if (s) return s;
+    if (cudaSetDevice(P->device) != cudaSuccess) return fail(MRA_E_CUDA, "cudaSetDevice failed");
+    CU(cudaMemsetAsync(P->counters, 0, 8 * (size_t)P->n_counters, P->st));
+    CU(cudaMemsetAsync(P->err, 0, 16, P->st));
+    LCHK(launch_gather(d_y, P->perm_d, P->zs, P->N, P->st));
+    return MRA_OK;
+}
+
+static mra_status ensure_post(mra_plan* P) {
+    if (P->post) return MRA_OK;
+    const int M = P->M, J = P->J, rh = P->rh;
+    long long tot = 0;
+    for (int m = 1; m < M; m++) {
+        P->post_base[m] = tot;
+        tot += ipow(J, m - 1) * ((long long)rh * rh + q_of(m, rh) * rh);
+    }
+    mra_status s;
+    if ((s = dalloc(P, (void**)&P->post, 8 * std::max<long long>(tot, 1), "posterior state"))) return s;
+    if ((s = dalloc(P, (void**)&P->muhat, 8 * std::max<long long>(P->nint * rh, 1), "muhat"))) return s;
+    if ((s = dalloc(P, (void**)&P->mu_d, 8 * std::max<long long>(P->nint * rh, 1), "mu"))) return s;
+    if ((s = dalloc(P, (void**)&P->smooth_d, 8 * (long long)P->n_in, "smooth"))) return s;
+    return MRA_OK;
+}
+
+static mra_status run_eval(mra_plan* P, const double* d_y, const mra_theta* th, double* loglik, mra_post* post,
+                           bool host_post) {
+    if (P->world > 1) return fail(MRA_E_CONFIG, "sharded plan: use mra_loglik_shard / mra_loglik_finish");
+    mra_status s;
+    const bool want_state = post && (post->mu || post->smooth);
+    if (want_state && (s = ensure_post(P))) return s;
+    if ((s = begin_eval(P, d_y, th))) return s;
+    TreeParams tp = tree_params(P, th);
+    if (want_state) tp.post = P->post;
+    if ((s = eval_lower(P, tp))) return s;
+    if ((s = eval_upper(P, tp))) return s;
+    double ll = NAN;
+    CU(cudaMemcpyAsync(&ll, P->loglik_d, 8, cudaMemcpyDeviceToHost, P->st));
+    if ((s = check_err(P))) return s;
+    if (loglik) *loglik = ll;
+    if (post) {
+        CU(cudaMemcpy(&post->d, P->dreg, 8, cudaMemcpyDeviceToHost));
+        CU(cudaMemcpy(&post->u, P->ureg, 8, cudaMemcpyDeviceToHost));
+        if (post->region_d) CU(cudaMemcpy(post->region_d, P->dreg, 8 * P->nreg, cudaMemcpyDeviceToHost));
+        if (post->region_u) CU(cudaMemcpy(post->region_u, P->ureg, 8 * P->nreg, cudaMemcpyDeviceToHost));
+    }
+    if (want_state) {
+        for (int m = 1; m < P->M; m++) LCHK(launch_mu(tp, m, P->muhat, P->mu_d, P->st));
+        if (post->smooth) {
+            LCHK(launch_fill(P->smooth_d, (long long)P->n_in, NAN, P->st));
+            LCHK(launch_smooth(tp, P->muhat, P->perm_d, P->smooth_d, P->grid, P->ws, P->L, take_counter(P), P->st));
+        }
+        if ((s = check_err(P))) return s;
+        const size_t nmu = 8 * (size_t)P->nint * P->rh;
+        const cudaMemcpyKind k = host_post ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+        if (post->mu && nmu) CU(cudaMemcpyAsync(post->mu, P->mu_d, nmu, k, P->st));
+        if (post->smooth) CU(cudaMemcpyAsync(post->smooth, P->smooth_d, 8 * P->n_in, k, P->st));
+        CU(cudaStreamSynchronize(P->st));
+    }
+    return MRA_OK;
+}
+
+extern "C" mra_status mra_loglik_dev(mra_plan* P, const double* d_y, const mra_theta* th, double* loglik,
+                                     mra_post* post) {
+    if (!P || !d_y) return fail(MRA_E_ARG, "plan or y is NULL");
+    return run_eval(P, d_y, th, loglik, post, false);
+}
+
+extern "C" mra_status mra_loglik(mra_plan* P, const double* y, const mra_theta* th, double* loglik, mra_post* post) {
+    if (!P || !y) return fail(MRA_E_ARG, "plan or y is NULL");
+    if (P->device < 0) return fail(MRA_E_CUDA, "host-only plan (device -2) cannot evaluate");
+    for (uint64_t i = 0; i < P->n_in; i++)
+        if (!std::isfinite(y[i])) return fail(MRA_E_ARG, "non-finite observation value");
+    if (cudaSetDevice(P->device) != cudaSuccess) return fail(MRA_E_CUDA, "cudaSetDevice failed");
+    CU(cudaMemcpyAsync(P->zin, y, 8 * P->n_in, cudaMemcpyHostToDevice, P->st));
+    return run_eval(P, P->zin, th, loglik, post, true);
+}
+
+extern "C" mra_status mra_loglik_batch_dev(mra_plan* P, const double* d_y, const mra_theta* th, int n_theta,
+                                           double* loglik) {
+    if (!P || !d_y || !th || !loglik || n_theta < 0) return fail(MRA_E_ARG, "bad arguments");
+    for (int i = 0; i < n_theta; i++) {
+        mra_status s = run_eval(P, d_y, th + i, loglik + i, nullptr, false);
+        if (s) return s;
+    }
+    return MRA_OK;
+}
+
+// ------------------------------------------------------------------------ sharding
+extern "C" uint64_t mra_shard_size(const mra_plan* P) {
+    if (!P) return 0;
+    const long long ns = ipow(P->J, P->c - 1), q = q_of(P->c, P->rh);
+    return (uint64_t)(ns * q * q + 2 * ns);
+}
+
+extern "C" mra_status mra_loglik_shard(mra_plan* P, const double* d_y, const mra_theta* th, double* d_xbuf) {
+    if (!P || !d_y || !d_xbuf) return fail(MRA_E_ARG, "NULL argument");
+    if (P->M < 2) return fail(MRA_E_CONFIG, "sharding needs M >= 2");
+    mra_status s;
+    if ((s = begin_eval(P, d_y, th))) return s;
+    TreeParams tp = tree_params(P, th);
+    CU(cudaMemsetAsync(P->dreg, 0, 8 * P->nreg, P->st));
+    CU(cudaMemsetAsync(P->ureg, 0, 8 * P->nreg, P->st));
+    const long long ns = ipow(P->J, P->c - 1), q = q_of(P->c, P->rh);
+    CU(cudaMemsetAsync(P->out_full[P->c], 0, 8 * ns * q * q, P->st));
+    if ((s = eval_lower(P, tp))) return s;
+    // exchange buffer: [ns * q * q outputs][ns d][ns u]; only own slots are non-zero
+    CU(cudaMemcpyAsync(d_xbuf, P->out_full[P->c], 8 * ns * q * q, cudaMemcpyDeviceToDevice, P->st));
+    CU(cudaMemcpyAsync(d_xbuf + ns * q * q, P->dreg + lvl_first(P->J, P->c), 8 * ns, cudaMemcpyDeviceToDevice, P->st));
+    CU(cudaMemcpyAsync(d_xbuf + ns * q * q + ns, P->ureg + lvl_first(P->J, P->c), 8 * ns, cudaMemcpyDeviceToDevice,
+                       P->st));
+    return check_err(P);
+}
+
+extern "C" mra_status mra_loglik_finish(mra_plan* P, const mra_theta* th, const double* d_xbuf, double* loglik) {
+    if (!P || !d_xbuf) return fail(MRA_E_ARG, "NULL argument");
+    if (P->device < 0) return fail(MRA_E_CUDA, "host-only plan (device -2) cannot evaluate");
+    mra_status s = check_theta(th);
+    if (s) return s;
+    if (cudaSetDevice(P->device) != cudaSuccess) return fail(MRA_E_CUDA, "cudaSetDevice failed");
+    TreeParams tp = tree_params(P, th);
+    const long long ns = ipow(P->J, P->c - 1), q = q_of(P->c, P->rh);
+    CU(cudaMemcpyAsync(P->out_full[P->c], d_xbuf, 8 * ns * q * q, cudaMemcpyDeviceToDevice, P->st));
+    CU(cudaMemcpyAsync(P->dreg + lvl_first(P->J, P->c), d_xbuf + ns * q * q, 8 * ns, cudaMemcpyDeviceToDevice, P->st));
+    CU(cudaMemcpyAsync(P->ureg + lvl_first(P->J, P->c), d_xbuf + ns * q * q + ns, 8 * ns, cudaMemcpyDeviceToDevice,
+                       P->st));
+    if ((s = eval_upper(P, tp))) return s;
+    double ll = NAN;
+    CU(cudaMemcpyAsync(&ll, P->loglik_d, 8, cudaMemcpyDeviceToHost, P->st));
+    if ((s = check_err(P))) return s;
+    if (loglik) *loglik = ll;
+    return MRA_OK;
+}

@@ -1,0 +1,65 @@
+// mra_internal.h -- host-side launch interface between the C-ABI (mra_api.cpp) and the
+// sm_100a kernels (mra_kernels.cu). Not part of the public ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mra {
+
+constexpr int MAXM = 24;
+
+struct CovParams {
+    int kind;
+    double s2, rho, xs, ys;
+};
+
+// Everything a kernel needs to know about the tree and the current theta (passed by value).
+struct TreeParams {
+    int M, J, lj, rh;           // levels, children, log2 J, r_hat
+    CovParams cp;
+    double tau2;
+    const double* px;           // [N] sorted (by leaf) retained observation x
+    const double* py;           // [N] y
+    const double* zs;           // [N] observed values in sorted order
+    const long long* leaf_off;  // [n_leaves + 1]
+    const double* kx;           // [n_interior * rh] knots, level-major regions
+    const double* ky;
+    double* prior;              // chain rows R_R = [Linv_R | -U^{m-1}_R .. -U^1_R], rh x m*rh each
+    long long prior_base[MAXM + 1];  // offset (doubles) of level m's first region
+    double* dreg;               // [n_regions] per-region log-det term
+    double* ureg;               // [n_regions] per-region quadratic term
+    int* err;                   // [4]: flag, level, index lo, index hi
+    // posterior-state storage (nullptr unless requested)
+    double* post;               // per interior region: Ltilde^{-1} (rh x rh) then F = H^T (q x rh)
+    long long post_base[MAXM + 1];
+};
+
+// per-CTA workspace layout of the bottom / smoothing kernels (offsets in doubles)
+struct WsLayout {
+    long long stride;           // doubles per CTA slot
+    long long oG, oS, oD, oA, oF, oL, oV;
+    int ldG, ldS, ldA;
+};
+
+// launchers (all asynchronous on `st`); return cudaGetLastError()
+cudaError_t launch_gather(const double* z, const long long* perm, double* zs, long long N, cudaStream_t st);
+// region ranges: level-m regions [t_first, t_first + t_count); output buffers are indexed by
+// (t - out_first), child buffers by (child t - child_first)
+cudaError_t launch_prior(const TreeParams& tp, int m, long long t_first, long long t_count, int grid,
+                         double* ws, long long ws_stride, unsigned long long* counter, cudaStream_t st);
+cudaError_t launch_bottom(const TreeParams& tp, long long g_first, long long g_count, double* out,
+                          long long out_first, int q, int grid, double* ws, const WsLayout& L,
+                          unsigned long long* counter, cudaStream_t st);
+cudaError_t launch_merge(const TreeParams& tp, int m, long long t_first, long long t_count,
+                         const double* child_out, long long child_first, double* out, long long out_first,
+                         int q, int grid, double* ws, long long ws_stride, unsigned long long* counter,
+                         cudaStream_t st);
+cudaError_t launch_final(const TreeParams& tp, double N, double* d_loglik, cudaStream_t st);
+cudaError_t launch_mu(const TreeParams& tp, int m, double* muhat, double* mu, cudaStream_t st);
+cudaError_t launch_smooth(const TreeParams& tp, const double* muhat, const long long* perm, double* smooth,
+                          int grid, double* ws, const WsLayout& L, unsigned long long* counter,
+                          cudaStream_t st);
+cudaError_t launch_fill(double* p, long long n, double v, cudaStream_t st);
+int smem_bytes();
+
+}  // namespace mra

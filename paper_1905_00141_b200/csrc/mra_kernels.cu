@@ -1,0 +1,469 @@
+// mra_kernels.cu -- sm_100a kernels of the MRA log-likelihood hot path.
+//
+// Whitened formulation: every pre-finest region R at level m stores its chain row
+//   R_R = [ L_R^{-1} | -L_R^{-1} V^{m-1}_R | ... | -L_R^{-1} V^1_R ]           (rh x m*rh)
+// where L_R = chol(W^m_R) and V^k_R = W^k_R L_{a_k}^{-T} (north_star W-recursion).
+// For any point set P inside R's subtree the chain block V^k(P) = [C(P, Q_{a_k}) | V^{k-1}(P)..V^1(P)]
+// R_{a_k}^T is ONE GEMM whose first K-segment is generated covariance (fused covgen).
+// The posterior pass then works with identity priors: Ktilde^{-1} = I + Atilde^{mm} and
+// d_R = sum d_c + log|I + Atilde^{mm}| (equal to the paper's log|W^m + A^{mm}| - log|W^m|).
+//
+// Kernels (persistent CTAs of 256 threads, one work item = one region, dynamic atomic queue):
+//   k_prior   level m: V chain + W^m = C(Q,Q) - V V^T, chol, inverse, U = L^{-1} V
+//   k_bottom  one level-(M-1) region p with its J leaves: per leaf V (chain GEMMs with fused
+//             covariance), Sigma_j = C(S,S) + tau2 I - V V^T, blocked Cholesky, G = L^{-1}[V|y];
+//             then Atilde_p = G_stack^T G_stack (stacked SYRK over the J leaves, no per-leaf ATilde
+//             is ever stored) and the merge of p.
+//   k_merge   level m < M-1: Atilde = sum of J child outputs, merge.
+//   k_mu / k_smooth   posterior state (top-down), only when requested.
+#include <cuda_runtime.h>
+
+#include "mra_device.cuh"
+#include "mra_internal.h"
+
+namespace mra {
+
+__device__ __forceinline__ long long lvl_first(int J, int m) {
+    long long p = 1;
+    for (int i = 1; i < m; i++) p *= J;
+    return (p - 1) / (J - 1);
+}
+
+__device__ __forceinline__ CovP to_covp(const CovParams& c) {
+    CovP p;
+    p.kind = c.kind; p.s2 = c.s2; p.rho = c.rho; p.xs = c.xs; p.ys = c.ys;
+    return p;
+}
+
+__device__ __forceinline__ void set_err(int* err, int level, long long idx) {
+    if (atomicCAS(err, 0, 1) == 0) {
+        err[1] = level;
+        *reinterpret_cast<long long*>(err + 2) = idx;
+    }
+}
+
+// persistent work queue: returns the next item index (uniform across the CTA)
+__device__ __forceinline__ long long next_item(unsigned long long* counter, double* smem) {
+    long long* slot = reinterpret_cast<long long*>(misc_smem(smem) + 18);
+    __syncthreads();
+    if (threadIdx.x == 0) *slot = (long long)atomicAdd(counter, 1ULL);
+    __syncthreads();
+    long long v = *slot;
+    return v;
+}
+
+__device__ __forceinline__ const double* chain_row(const TreeParams& tp, int k, long long ak) {
+    return tp.prior + tp.prior_base[k] + ak * (long long)k * tp.rh * tp.rh;
+}
+
+// V chain of a point set P (n points inside level-m region t): for k = 1..m
+//   V^k(P) = [ C(P, Q_{a_k}) | V^{k-1}(P) .. V^1(P) ] R_{a_k}^T        (K = k * rh)
+// written into Gc at column block m-k (levels in descending order), ld ldg.
+__device__ void point_chain(const TreeParams& tp, int m, long long t, int n, const double* px, const double* py,
+                            double* Gc, long long ldg, const CovP& cp, double* smem) {
+    const int rh = tp.rh;
+    for (int k = 1; k <= m; k++) {
+        const long long ak = t >> (tp.lj * (m - k));
+        const long long akid = lvl_first(tp.J, k) + ak;
+        const long long ldk = (long long)k * rh;
+        const double* Rk = chain_row(tp, k, ak);
+        cta_gemm<COVK, MEMN, MEMN, MEMN>(n, rh, 0, op_cov(px, py, tp.kx + akid * rh, tp.ky + akid * rh),
+                                         op_mem(Rk, ldk), rh, op_mem(Gc + (long long)(m - k + 1) * rh, ldg),
+                                         op_mem(Rk + rh, ldk), (k - 1) * rh, ci_zero(), 1.0,
+                                         Gc + (long long)(m - k) * rh, ldg, cp, smem);
+    }
+}
+
+// --------------------------------------------------------------------------- prior
+__global__ void __launch_bounds__(NT, 2)
+k_prior(TreeParams tp, int m, long long t_first, long long nitems, double* ws, long long ws_stride,
+        unsigned long long* counter) {
+    extern __shared__ double smem[];
+    const CovP cp = to_covp(tp.cp);
+    const int rh = tp.rh;
+    double* W = ws + (long long)blockIdx.x * ws_stride;
+    FacSmem f = fac_smem(smem);
+    const long long ldR = (long long)m * rh;
+    for (;;) {
+        const long long it = next_item(counter, smem);
+        if (it >= nitems) break;
+        if (threadIdx.x == 0) *f.bad = 0;
+        const long long t = t_first + it;
+        const long long id = lvl_first(tp.J, m) + t;
+        double* R = tp.prior + tp.prior_base[m] + t * ldR * rh;
+        const double* qx = tp.kx + id * rh;
+        const double* qy = tp.ky + id * rh;
+        // V^k_R for k < m into R's blocks m-k (they become -U after the inverse is known)
+        point_chain(tp, m - 1, t >> tp.lj, rh, qx, qy, R + rh, ldR, cp, smem);
+        // W^m_R = C(Q_R, Q_R) - sum_k V^k V^kT
+        cta_gemm<MEMN, MEMN, MEMN, MEMN>(rh, rh, 1, op_mem(R + rh, ldR), op_mem(R + rh, ldR), (m - 1) * rh,
+                                         op_mem(R, ldR), op_mem(R, ldR), 0, ci_cov(qx, qy, qx, qy, 0.0), -1.0,
+                                         W, rh, cp, smem);
+        load_block_lower(f.blk, W, rh, rh, 0.0);
+        double ld;
+        chol_small(f.blk, rh, f.diagv, f.bad, f.red, &ld);
+        if (*f.bad && threadIdx.x == 0) set_err(tp.err, m, t);
+        trinv_small(f.blk, f.inv, rh);
+        store_block_full(f.inv, R, ldR, rh);
+        __syncthreads();
+        // -U = -L^{-1} V  (in place over the V blocks; single row tile)
+        if (m > 1)
+            cta_gemm<MEMN, MEMT, MEMN, MEMN>(rh, (m - 1) * rh, 0, op_mem(R, ldR), op_mem(R + rh, ldR), rh,
+                                             op_mem(R, ldR), op_mem(R, ldR), 0, ci_zero(), -1.0, R + rh, ldR, cp,
+                                             smem);
+    }
+}
+
+// merge of region with Atilde (ncol x ncol lower, ld ldA): Lt = chol(I + A_oo), Li = Lt^{-1},
+// F = A_ro Li^T, O = A_rr - F F^T (q = ncol - rh). Returns log|I + A_oo|.
+__device__ double merge_core(const double* A, int rh, long long ldA, double* O, int q, double* F, double* Li,
+                             int* err, int level, long long t, const CovP& cp, double* smem) {
+    FacSmem f = fac_smem(smem);
+    load_block_lower(f.blk, A, ldA, rh, 1.0);
+    double ld;
+    chol_small(f.blk, rh, f.diagv, f.bad, f.red, &ld);
+    if (*f.bad && threadIdx.x == 0) set_err(err, level, t);
+    trinv_small(f.blk, f.inv, rh);
+    store_block_full(f.inv, Li, rh, rh);
+    __syncthreads();
+    cta_gemm<MEMN, MEMN, MEMN, MEMN>(q, rh, 0, op_mem(A + (long long)rh * ldA, ldA), op_mem(Li, rh), rh,
+                                     op_mem(Li, rh), op_mem(Li, rh), 0, ci_zero(), 1.0, F, rh, cp, smem);
+    cta_gemm<MEMN, MEMN, MEMN, MEMN>(q, q, 1, op_mem(F, rh), op_mem(F, rh), rh, op_mem(F, rh), op_mem(F, rh), 0,
+                                     ci_mem(A + (long long)rh * ldA + rh, ldA), -1.0, O, q, cp, smem);
+    return ld;
+}
+
+__device__ __forceinline__ void save_post(const TreeParams& tp, int m, long long t, int q, const double* Li,
+                                          const double* F) {
+    if (!tp.post) return;
+    const int rh = tp.rh;
+    double* P = tp.post + tp.post_base[m] + t * ((long long)rh * rh + (long long)q * rh);
+    for (int e = threadIdx.x; e < rh * rh; e += NT) P[e] = Li[e];
+    for (int e = threadIdx.x; e < q * rh; e += NT) P[rh * rh + e] = F[e];
+}
+
+// -------------------------------------------------------------------------- bottom
+__global__ void __launch_bounds__(NT, 2)
+k_bottom(TreeParams tp, long long g_first, long long g_count, double* out, long long out_first, int q, double* ws,
+         WsLayout L, unsigned long long* counter) {
+    extern __shared__ double smem[];
+    const CovP cp = to_covp(tp.cp);
+    const int M = tp.M, J = tp.J, rh = tp.rh;
+    const int m = M - 1;                 // group level; 0 when M == 1 (the root is the only leaf)
+    const int Jc = (M == 1) ? 1 : J;     // leaves per group
+    const int Pg = m * rh, ncol = Pg + 1;
+    double* base = ws + (long long)blockIdx.x * L.stride;
+    double *G = base + L.oG, *S = base + L.oS, *D = base + L.oD, *A = base + L.oA, *F = base + L.oF,
+           *Li = base + L.oL;
+    FacSmem f = fac_smem(smem);
+    double* red = misc_smem(smem);
+    const long long leaf_id0 = lvl_first(J, M);
+    for (;;) {
+        const long long it = next_item(counter, smem);
+        if (it >= g_count) break;
+        if (threadIdx.x == 0) *f.bad = 0;
+        const long long t = g_first + it;
+        const long long l0 = t * Jc;
+        const long long obase = tp.leaf_off[l0];
+        const long long ng = tp.leaf_off[l0 + Jc] - obase;
+        double dsum = 0.0, ulast = 0.0;
+        for (int c = 0; c < Jc; c++) {
+            const long long l = l0 + c;
+            const long long o0 = tp.leaf_off[l];
+            const int n = (int)(tp.leaf_off[l + 1] - o0);
+            if (n == 0) {   // empty leaf: zero contribution (reading R10)
+                if (threadIdx.x == 0) { tp.dreg[leaf_id0 + l] = 0.0; tp.ureg[leaf_id0 + l] = 0.0; }
+                continue;
+            }
+            double* Gc = G + (o0 - obase) * L.ldG;
+            const double* px = tp.px + o0;
+            const double* py = tp.py + o0;
+            point_chain(tp, m, t, n, px, py, Gc, L.ldG, cp, smem);
+            for (int i = threadIdx.x; i < n; i += NT) Gc[(long long)i * L.ldG + Pg] = tp.zs[o0 + i];
+            __syncthreads();
+            // Sigma_j = C(S,S) + tau2 I - V V^T  (nugget on the observation diagonal only, reading R2)
+            cta_gemm<MEMN, MEMN, MEMN, MEMN>(n, n, 1, op_mem(Gc, L.ldG), op_mem(Gc, L.ldG), Pg, op_mem(Gc, L.ldG),
+                                             op_mem(Gc, L.ldG), 0, ci_cov(px, py, px, py, tp.tau2), -1.0, S,
+                                             L.ldS, cp, smem);
+            const double ldet = chol_blocked(S, n, L.ldS, D, cp, smem);
+            if (*f.bad && threadIdx.x == 0) set_err(tp.err, M, l);
+            fwd_subst(S, n, L.ldS, D, Gc, ncol, L.ldG, cp, smem);
+            double u = 0.0;
+            for (int i = threadIdx.x; i < n; i += NT) {
+                const double g = Gc[(long long)i * L.ldG + Pg];
+                u += g * g;
+            }
+            u = cta_sum(u, red);
+            if (threadIdx.x == 0) { tp.dreg[leaf_id0 + l] = ldet; tp.ureg[leaf_id0 + l] = u; }
+            dsum += ldet;
+            ulast = u;
+        }
+        if (m == 0) {   // M == 1: the leaf is the root
+            if (threadIdx.x == 0) { tp.dreg[0] = dsum; tp.ureg[0] = ulast; }
+            continue;
+        }
+        // Atilde_p = sum_c G_c^T G_c = G_stack^T G_stack (lower)
+        cta_gemm<MEMT, MEMT, MEMN, MEMN>(ncol, ncol, 1, op_mem(G, L.ldG), op_mem(G, L.ldG), (int)ng, op_mem(G, 0),
+                                         op_mem(G, 0), 0, ci_zero(), 1.0, A, L.ldA, cp, smem);
+        double* O = out + (t - out_first) * (long long)q * q;
+        const double ldm = merge_core(A, rh, L.ldA, O, q, F, Li, tp.err, m, t, cp, smem);
+        const long long id = lvl_first(J, m) + t;
+        if (threadIdx.x == 0) {
+            tp.dreg[id] = dsum + ldm;
+            tp.ureg[id] = O[(long long)(q - 1) * q + q - 1];
+        }
+        save_post(tp, m, t, q, Li, F);
+    }
+}
+
+// --------------------------------------------------------------------------- merge
+__global__ void __launch_bounds__(NT, 2)
+k_merge(TreeParams tp, int m, long long t_first, long long t_count, const double* child_out, long long child_first,
+        double* out, long long out_first, int q, double* ws, long long ws_stride, unsigned long long* counter) {
+    extern __shared__ double smem[];
+    const CovP cp = to_covp(tp.cp);
+    const int J = tp.J, rh = tp.rh;
+    const int qc = m * rh + 1;
+    double* A = ws + (long long)blockIdx.x * ws_stride;
+    double* F = A + (long long)qc * qc;
+    double* Li = F + (long long)q * rh;
+    FacSmem f = fac_smem(smem);
+    const long long qc2 = (long long)qc * qc;
+    for (;;) {
+        const long long it = next_item(counter, smem);
+        if (it >= t_count) break;
+        if (threadIdx.x == 0) *f.bad = 0;
+        const long long t = t_first + it;
+        const double* C0 = child_out + (t * J - child_first) * qc2;
+        for (long long e = threadIdx.x; e < qc2; e += NT) {
+            const int i = (int)(e / qc), j = (int)(e - (long long)i * qc);
+            if (j <= i) {
+                double s = 0.0;
+                for (int c = 0; c < J; c++) s += C0[c * qc2 + e];
+                A[e] = s;
+            }
+        }
+        __syncthreads();
+        double* O = out + (t - out_first) * (long long)q * q;
+        const double ldm = merge_core(A, rh, qc, O, q, F, Li, tp.err, m, t, cp, smem);
+        const long long id = lvl_first(J, m) + t;
+        if (threadIdx.x == 0) {
+            const long long c0 = lvl_first(J, m + 1) + t * J;
+            double ds = 0.0;
+            for (int c = 0; c < J; c++) ds += tp.dreg[c0 + c];
+            tp.dreg[id] = ds + ldm;
+            tp.ureg[id] = O[(long long)(q - 1) * q + q - 1];
+        }
+        save_post(tp, m, t, q, Li, F);
+    }
+}
+
+// log L = -1/2 (N log 2 pi + d_root + u_root)
+__global__ void k_final(TreeParams tp, double N, double* loglik) {
+    if (threadIdx.x == 0 && blockIdx.x == 0)
+        *loglik = -0.5 * (N * log(2.0 * 3.14159265358979323846) + tp.dreg[0] + tp.ureg[0]);
+}
+
+__global__ void k_gather(const double* z, const long long* perm, double* zs, long long N) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x)
+        zs[i] = z[perm[i]];
+}
+
+__global__ void k_fill(double* p, long long n, double v) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
+// ----------------------------------------------------------------- posterior state
+// muhat_R = Lt^{-T} (h - sum_k H^k muhat_{a_k})   (whitened), mu_R = L_R^{-T} muhat_R (paper's eta)
+__global__ void k_mu(TreeParams tp, int m, double* muhat, double* mu) {
+    __shared__ double tv[64], mh[64];
+    const int rh = tp.rh, q = (m - 1) * rh + 1;
+    const long long cnt = lvl_first(tp.J, m + 1) - lvl_first(tp.J, m);
+    for (long long t = blockIdx.x; t < cnt; t += gridDim.x) {
+        const long long id = lvl_first(tp.J, m) + t;
+        const double* Li = tp.post + tp.post_base[m] + t * ((long long)rh * rh + (long long)q * rh);
+        const double* F = Li + rh * rh;
+        for (int a = threadIdx.x; a < rh; a += blockDim.x) {
+            double s = F[(long long)(q - 1) * rh + a];
+            for (int b = 0; b < q - 1; b++) {
+                const int bi = b / rh, lev = m - 1 - bi;
+                const long long anc = lvl_first(tp.J, lev) + (t >> (tp.lj * (m - lev)));
+                s -= F[(long long)b * rh + a] * muhat[anc * rh + (b - bi * rh)];
+            }
+            tv[a] = s;
+        }
+        __syncthreads();
+        for (int a = threadIdx.x; a < rh; a += blockDim.x) {
+            double s = 0.0;
+            for (int b = 0; b < rh; b++) s += Li[b * rh + a] * tv[b];
+            mh[a] = s;
+        }
+        __syncthreads();
+        const double* Rr = chain_row(tp, m, t);
+        const long long ldR = (long long)m * rh;
+        for (int a = threadIdx.x; a < rh; a += blockDim.x) {
+            muhat[id * rh + a] = mh[a];
+            double s = 0.0;
+            for (int b = 0; b < rh; b++) s += Rr[(long long)b * ldR + a] * mh[b];
+            if (mu) mu[id * rh + a] = s;
+        }
+        __syncthreads();
+    }
+}
+
+// E[X(S_j)|y] = y_j - tau2 Sigma_j^{-1} (y_j - sum_k V^k muhat_{a_k})   (recomputes V, Sigma_j, L_j)
+__global__ void __launch_bounds__(NT, 2)
+k_smooth(TreeParams tp, const double* muhat, const long long* perm, double* smooth, double* ws, WsLayout L,
+         unsigned long long* counter) {
+    extern __shared__ double smem[];
+    const CovP cp = to_covp(tp.cp);
+    const int M = tp.M, rh = tp.rh, m = M - 1, Pg = m * rh;
+    double* base = ws + (long long)blockIdx.x * L.stride;
+    double *G = base + L.oG, *S = base + L.oS, *D = base + L.oD, *r = base + L.oV;
+    FacSmem f = fac_smem(smem);
+    double* tmp = misc_smem(smem);   // not used for vectors; vectors live in r
+    (void)tmp;
+    long long nleaves = 1;
+    for (int i = 1; i < M; i++) nleaves *= tp.J;
+    for (;;) {
+        const long long l = next_item(counter, smem);
+        if (l >= nleaves) break;
+        if (threadIdx.x == 0) *f.bad = 0;
+        const long long t = (M == 1) ? 0 : (l >> tp.lj);
+        const long long o0 = tp.leaf_off[l];
+        const int n = (int)(tp.leaf_off[l + 1] - o0);
+        if (n == 0) continue;
+        const double* px = tp.px + o0;
+        const double* py = tp.py + o0;
+        point_chain(tp, m, t, n, px, py, G, L.ldG, cp, smem);
+        cta_gemm<MEMN, MEMN, MEMN, MEMN>(n, n, 1, op_mem(G, L.ldG), op_mem(G, L.ldG), Pg, op_mem(G, L.ldG),
+                                         op_mem(G, L.ldG), 0, ci_cov(px, py, px, py, tp.tau2), -1.0, S, L.ldS, cp,
+                                         smem);
+        chol_blocked(S, n, L.ldS, D, cp, smem);
+        if (*f.bad && threadIdx.x == 0) set_err(tp.err, M, l);
+        // r = y - V muhat_chain
+        for (int i = threadIdx.x; i < n; i += NT) {
+            double s = tp.zs[o0 + i];
+            for (int col = 0; col < Pg; col++) {
+                const int b = col / rh, lev = m - b;
+                const long long anc = lvl_first(tp.J, lev) + (t >> (tp.lj * (m - lev)));
+                s -= G[(long long)i * L.ldG + col] * muhat[anc * rh + (col - b * rh)];
+            }
+            r[i] = s;
+        }
+        __syncthreads();
+        double* w = f.blk;   // smem scratch [64]
+        // forward: r <- L^{-1} r
+        for (int i0 = 0; i0 < n; i0 += 64) {
+            const int nb = min(64, n - i0);
+            for (int ii = threadIdx.x; ii < nb; ii += NT) {
+                double s = r[i0 + ii];
+                for (int k = 0; k < i0; k++) s -= S[(long long)(i0 + ii) * L.ldS + k] * r[k];
+                w[ii] = s;
+            }
+            __syncthreads();
+            const double* Di = D + (long long)(i0 / 64) * 4096;
+            for (int ii = threadIdx.x; ii < nb; ii += NT) {
+                double s = 0.0;
+                for (int k = 0; k <= ii; k++) s += Di[ii * 64 + k] * w[k];
+                r[i0 + ii] = s;
+            }
+            __syncthreads();
+        }
+        // backward: r <- L^{-T} r
+        const int nblk = (n + 63) / 64;
+        for (int bb = nblk - 1; bb >= 0; bb--) {
+            const int i0 = bb * 64, nb = min(64, n - i0);
+            for (int ii = threadIdx.x; ii < nb; ii += NT) {
+                double s = r[i0 + ii];
+                for (int k = i0 + nb; k < n; k++) s -= S[(long long)k * L.ldS + i0 + ii] * r[k];
+                w[ii] = s;
+            }
+            __syncthreads();
+            const double* Di = D + (long long)bb * 4096;
+            for (int ii = threadIdx.x; ii < nb; ii += NT) {
+                double s = 0.0;
+                for (int k = ii; k < nb; k++) s += Di[k * 64 + ii] * w[k];
+                r[i0 + ii] = s;
+            }
+            __syncthreads();
+        }
+        for (int i = threadIdx.x; i < n; i += NT) smooth[perm[o0 + i]] = tp.zs[o0 + i] - tp.tau2 * r[i];
+    }
+}
+
+// ------------------------------------------------------------------------ launchers
+int smem_bytes() { return SMEM_DBL * (int)sizeof(double); }
+
+static bool g_attr_done = false;
+static void set_attrs() {
+    if (g_attr_done) return;
+    const int b = smem_bytes();
+    cudaFuncSetAttribute(k_prior, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    cudaFuncSetAttribute(k_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    cudaFuncSetAttribute(k_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    cudaFuncSetAttribute(k_smooth, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    g_attr_done = true;
+}
+
+cudaError_t launch_gather(const double* z, const long long* perm, double* zs, long long N, cudaStream_t st) {
+    long long blocks = (N + 255) / 256;
+    if (blocks > 4096) blocks = 4096;
+    if (blocks < 1) blocks = 1;
+    k_gather<<<(int)blocks, 256, 0, st>>>(z, perm, zs, N);
+    return cudaGetLastError();
+}
+cudaError_t launch_fill(double* p, long long n, double v, cudaStream_t st) {
+    long long blocks = (n + 255) / 256;
+    if (blocks > 4096) blocks = 4096;
+    if (blocks < 1) blocks = 1;
+    k_fill<<<(int)blocks, 256, 0, st>>>(p, n, v);
+    return cudaGetLastError();
+}
+cudaError_t launch_prior(const TreeParams& tp, int m, long long t_first, long long t_count, int grid, double* ws,
+                         long long ws_stride, unsigned long long* counter, cudaStream_t st) {
+    set_attrs();
+    if (t_count < grid) grid = (int)t_count;
+    if (grid < 1) return cudaSuccess;
+    k_prior<<<grid, NT, smem_bytes(), st>>>(tp, m, t_first, t_count, ws, ws_stride, counter);
+    return cudaGetLastError();
+}
+cudaError_t launch_bottom(const TreeParams& tp, long long g_first, long long g_count, double* out, long long out_first,
+                          int q, int grid, double* ws, const WsLayout& L, unsigned long long* counter,
+                          cudaStream_t st) {
+    set_attrs();
+    if (g_count < grid) grid = (int)g_count;
+    if (grid < 1) return cudaSuccess;
+    k_bottom<<<grid, NT, smem_bytes(), st>>>(tp, g_first, g_count, out, out_first, q, ws, L, counter);
+    return cudaGetLastError();
+}
+cudaError_t launch_merge(const TreeParams& tp, int m, long long t_first, long long t_count, const double* child_out,
+                         long long child_first, double* out, long long out_first, int q, int grid, double* ws,
+                         long long ws_stride, unsigned long long* counter, cudaStream_t st) {
+    set_attrs();
+    if (t_count < grid) grid = (int)t_count;
+    if (grid < 1) return cudaSuccess;
+    k_merge<<<grid, NT, smem_bytes(), st>>>(tp, m, t_first, t_count, child_out, child_first, out, out_first, q, ws,
+                                           ws_stride, counter);
+    return cudaGetLastError();
+}
+cudaError_t launch_final(const TreeParams& tp, double N, double* d_loglik, cudaStream_t st) {
+    k_final<<<1, 32, 0, st>>>(tp, N, d_loglik);
+    return cudaGetLastError();
+}
+cudaError_t launch_mu(const TreeParams& tp, int m, double* muhat, double* mu, cudaStream_t st) {
+    long long cnt = 1;
+    for (int i = 1; i < m; i++) cnt *= tp.J;
+    int grid = (int)(cnt < 4096 ? cnt : 4096);
+    k_mu<<<grid, 64, 0, st>>>(tp, m, muhat, mu);
+    return cudaGetLastError();
+}
+cudaError_t launch_smooth(const TreeParams& tp, const double* muhat, const long long* perm, double* smooth, int grid,
+                          double* ws, const WsLayout& L, unsigned long long* counter, cudaStream_t st) {
+    set_attrs();
+    k_smooth<<<grid, NT, smem_bytes(), st>>>(tp, muhat, perm, smooth, ws, L, counter);
+    return cudaGetLastError();
+}
+
+}  // namespace mra

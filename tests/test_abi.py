@@ -1,0 +1,122 @@
+"""C-ABI library: loads, exports every symbol include/mra.h declares, host-side plan logic
+(no GPU: host-only plans, device = -2). The plan built by the product must agree bit for bit
+with the oracle's independent plan."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1905_00141_b200 as mra
+import synth
+from paper_1905_00141_b200 import build as mbuild
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def lib():
+    mbuild.build()
+    return mra.load_library()
+
+
+def test_exports_every_declared_symbol(lib):
+    hdr = open(os.path.join(ROOT, "include", "mra.h")).read()
+    names = set(re.findall(r"^\s*(?:mra_status|uint64_t|void|const char\*)\s+(mra_\w+)\s*\(", hdr, re.M))
+    assert len(names) >= 12
+    cdll = ctypes.CDLL(mra.LIB_PATH)
+    for nme in sorted(names):
+        assert hasattr(cdll, nme), nme
+    assert names <= set(mra.EXPORTS)
+
+
+def test_sass_is_sm100a_with_dmma():
+    """The library carries sm_100a SASS and its GEMM tiles run on the fp64 tensor path (DMMA)."""
+    import shutil
+    import subprocess
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(exe):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([exe, "-sass", mra.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert "DMMA" in out
+
+
+@pytest.mark.parametrize("J,M,r,clusters", [(4, 4, 16, 0), (2, 7, 9, 3), (4, 3, 36, 2), (2, 5, 32, 0)])
+def test_host_plan_matches_oracle_plan(J, M, r, clusters):
+    x, y, _ = synth.uniform_small(3000, seed=J * 10 + M, clusters=clusters, domain=(-5.0, 7.0, 40.0, 41.5))
+    p = mra.mra_plan_create(x, y, M, J, r, device=-2)
+    lay = mra.mra_plan_layout(p)
+    o = oracle.plan(x, y, M, J, r)
+    assert p.r_hat == o["r_hat"]
+    # knots bit-identical
+    np.testing.assert_array_equal(lay["knots_x"].reshape(-1, p.r_hat), o["knots_x"])
+    np.testing.assert_array_equal(lay["knots_y"].reshape(-1, p.r_hat), o["knots_y"])
+    # leaf assignment: perm/leaf_off reproduce the oracle's leaf of every observation, stable order
+    leaf = np.full(len(x), -1)
+    off = lay["leaf_off"]
+    for l in range(p.n_leaves):
+        leaf[lay["perm"][off[l]:off[l + 1]]] = l
+        assert np.all(np.diff(lay["perm"][off[l]:off[l + 1]]) > 0)
+    np.testing.assert_array_equal(leaf, o["leaf"])
+    info = mra.mra_plan_info(p)
+    assert info["n_regions"] == (J ** M - 1) // (J - 1)
+    assert info["n_empty_leaves"] == int(np.sum(np.diff(off) == 0))
+    p.close()
+
+
+def test_elimination_matches_oracle():
+    x, y, z = synth.uniform_small(500, seed=9)
+    o = oracle.plan(x, y, 3, 4, 9)
+    x2 = np.append(x, [o["knots_x"][1, 3], o["knots_x"][0, 0]])
+    y2 = np.append(y, [o["knots_y"][1, 3], o["knots_y"][0, 0]])
+    p = mra.mra_plan_create(x2, y2, 3, 4, 9, device=-2)
+    assert p.n_retained == 500
+    assert set(mra.mra_plan_layout(p)["perm"].tolist()) == set(range(500))
+
+
+def test_config_and_arg_errors():
+    x, y, _ = synth.uniform_small(100, seed=1)
+    for args, status in [((3, 3, 16), 2), ((0, 4, 16), 2), ((3, 4, 0), 2), ((3, 4, 100), 2)]:
+        with pytest.raises(mra.MraError) as e:
+            mra.mra_plan_create(x, y, *args, device=-2)
+        assert e.value.status == status
+    with pytest.raises(mra.MraError) as e:
+        mra.mra_plan_create(np.ones(10), np.arange(10.0), 2, 4, 4, device=-2)
+    assert e.value.status == 3                     # degenerate bounding box
+    xb = x.copy(); xb[3] = np.nan
+    with pytest.raises(mra.MraError) as e:
+        mra.mra_plan_create(xb, y, 2, 4, 4, device=-2)
+    assert e.value.status == 1
+    p = mra.mra_plan_create(x, y, 2, 4, 4, device=-2)
+    with pytest.raises(mra.MraError) as e:
+        mra.mra_loglik(p, np.zeros(100), (0, 1.0, 0.1, 0.1))
+    assert e.value.status == 5                     # host-only plans cannot evaluate (no CPU fallback)
+
+
+def test_all_eliminated_is_struct_error():
+    o = oracle.plan(np.array([0.0, 1.0]), np.array([0.0, 1.0]), 2, 4, 4)
+    x = np.append(o["knots_x"][0], [0.0, 1.0]); y = np.append(o["knots_y"][0], [0.0, 1.0])
+    # the two extreme points define the same box; knots sit inside -> eliminated, corners stay
+    p = mra.mra_plan_create(x, y, 2, 4, 4, device=-2)
+    assert p.n_retained == 2
+
+
+def test_shard_assignment_partitions_subtrees():
+    w = synth.make("C4", n=40000)
+    owned = []
+    for rank in range(4):
+        p = mra.mra_plan_create(w.x, w.y, w.M, w.J, w.r, device=-2, rank=rank, world=4)
+        s = mra.mra_plan_shards(p)
+        owned.append(s["own"])
+        lvl = s["shard_level"]
+        assert w.J ** (lvl - 1) >= 32
+    allv = np.sort(np.concatenate(owned))
+    np.testing.assert_array_equal(allv, np.arange(w.J ** (lvl - 1)))
+
+
+def test_atilde_eq1():
+    assert abs(mra.atilde_bound_gib(2, 10, 256) - 11.25) < 1e-12
+    assert abs(mra.atilde_bound_gib(2, 14, 49) - 13.34) < 0.005
