@@ -1,0 +1,395 @@
+#!/usr/bin/env python
+"""Benchmark of the MRA log-likelihood hot path on B200 (BASELINE.json metric:
+observations/sec per MRA log-lik evaluation, fp64, and the fraction of the fp64 roofline).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl mra|reference]
+
+One step = one full MRA log-likelihood evaluation (prior pass + posterior pass, every §8(a)
+row) of the config's synthetic data for a fixed plan, y already resident in HBM (the paper's
+"excluding loading the data and building the structure"). N > 1 ranks
+(torchrun, one per GPU, NCCL) shard the subtrees and sum-reduce the shard-level
+outputs to rank 0 with torch.distributed.reduce over NCCL; time = max over ranks (CUDA events).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "observations/sec per MRA log-lik eval (fp64)"
+UNIT = "obs/s"
+DEFAULT_CONFIG = "C3"
+# fp64 roofline denominator: MEASURED_PEAKS.json bf16 x the guide's nominal fp64-tensor:bf16 ratio
+# (blackwell_cuda_programming.md: B200 FP64 tensor 45 TFLOPS vs 2.25 PFLOPS dense bf16)
+FP64_NOMINAL_TF = 45.0
+BF16_NOMINAL_TF = 2250.0
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ------------------------------------------------------------------ flop model (§8(d))
+def leaf_flops(n, P, r):
+    """SURVEY.md §8(d) algorithmic flops of one leaf with n observations, P = M-1 ancestor levels."""
+    n = np.asarray(n, dtype=np.float64)
+    Pr = P * r
+    f = P * P * n * r * r                      # W chain + V triangular solves
+    f += n * (n + 1) * Pr                      # Sigma_j = C - V V^T (symmetric, half)
+    f += n ** 3 / 3.0                          # Cholesky
+    f += n * n * (Pr + 1)                      # G = L^{-1} [V | y]
+    f += Pr * (Pr + 1) * n                     # A = G^T G (symmetric, half)
+    f += 2 * Pr * n + 2 * n                    # omega, u
+    return np.where(n > 0, f, 0.0)
+
+
+def interior_flops(m, r):
+    """prior + merge flops of one level-m region."""
+    prior = m * (m - 1) * r ** 3 + (m - 1) * r ** 3 + r ** 3 / 3.0
+    merge = r ** 3 / 3.0 + r * r * ((m - 1) * r + 1) + (m - 1) * r * ((m - 1) * r + 1) * r + 2 * (m - 1) * r * r
+    return prior, merge
+
+
+def flop_model(leaf_sizes, M, J, r):
+    P = M - 1
+    leaves = float(np.sum(leaf_flops(leaf_sizes, P, r)))
+    prior = merge = merge_bottom = 0.0
+    for m in range(1, M):
+        p, g = interior_flops(m, r)
+        prior += J ** (m - 1) * p
+        merge += J ** (m - 1) * g
+        if m == M - 1:
+            merge_bottom = J ** (m - 1) * g
+    return dict(total=leaves + prior + merge, leaves=leaves, prior=prior, merge=merge,
+                bottom=leaves + merge_bottom)
+
+
+# --------------------------------------------------------------------------- helpers
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            out, _ = self.p.communicate(timeout=5)
+        except Exception:
+            self.p.kill()
+            return None
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for nme, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nme)
+        if not sm:
+            return None
+        loaded = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def peaks():
+    try:
+        pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return pk, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def region_box(x, y, J, level, t):
+    """Box of region (level, t) by the paper's split rule (only used to pre-select the oracle's
+    timing sample; the oracle assigns the points itself)."""
+    x0, x1, y0, y1 = x.min(), x.max(), y.min(), y.max()
+    b = [x0, x1 + 0.01 * (x1 - x0), y0, y1 + 0.01 * (y1 - y0)]
+    path = []
+    for _ in range(level - 1):
+        path.append(t % J)
+        t //= J
+    for c in reversed(path):
+        mx, my = 0.5 * (b[0] + b[1]), 0.5 * (b[2] + b[3])
+        if J == 4:
+            b = [mx, b[1], b[2], b[3]] if c & 1 else [b[0], mx, b[2], b[3]]
+            b = [b[0], b[1], my, b[3]] if c & 2 else [b[0], b[1], b[2], my]
+        elif (b[1] - b[0]) >= (b[3] - b[2]):
+            b = [mx, b[1], b[2], b[3]] if c else [b[0], mx, b[2], b[3]]
+        else:
+            b = [b[0], b[1], my, b[3]] if c else [b[0], b[1], b[2], my]
+    return b
+
+
+def oracle_sample(w, theta, budget_s, seed=0, max_samples=64):
+    """Time the CPU oracle (as it stands) on a bounded sample of the same workload: whole subtrees
+    rooted at level max(1, M-3) (<= 64 leaves each), evaluated with the oracle's subtree mode on the
+    subtree's points plus the 4 bounding-box extremes (so the oracle builds the identical tree).
+    Returns (obs/s, obs, seconds, samples, threads)."""
+    import oracle
+    lvl = max(1, w.M - 3)
+    nreg = w.J ** (lvl - 1)
+    rng = np.random.default_rng(seed)
+    ext = np.unique([np.argmin(w.x), np.argmax(w.x), np.argmin(w.y), np.argmax(w.y)])
+    tot_obs, tot_s, k = 0, 0.0, 0
+    while (tot_s < budget_s or k == 0) and k < max_samples:
+        t = int(rng.integers(0, nreg))
+        b = region_box(w.x, w.y, w.J, lvl, t)
+        sel = np.nonzero((w.x >= b[0]) & (w.x < b[1]) & (w.y >= b[2]) & (w.y < b[3]))[0]
+        idx = np.union1d(sel, ext)
+        xs, ys, zs = w.x[idx], w.y[idx], w.z[idx]
+        t0 = time.perf_counter()
+        oracle.run(xs, ys, zs, w.M, w.J, w.r, theta, target=(lvl, t))
+        tot_s += time.perf_counter() - t0
+        tot_obs += sel.size
+        k += 1
+    return tot_obs / tot_s, tot_obs, tot_s, k, oracle.threads(), lvl
+
+
+# ------------------------------------------------------------------------- arms
+def run_reference(args, rank):
+    """--impl reference: the oracle (the deliberately slow CPU baseline) on the box's host cores."""
+    if rank != 0:
+        return
+    w = synth.make(args.config, n=args.n)
+    theta = w.thetas[0]
+    import oracle
+    oracle.build()
+    budget = args.ref_budget
+    for _ in range(args.warmup):
+        oracle_sample(w, theta, 0.0, seed=123, max_samples=1)
+    vals, obs, secs, samples = [], 0, 0.0, 0
+    for s in range(args.steps):
+        v, o, sec, k, thr, lvl = oracle_sample(w, theta, budget, seed=s)
+        vals.append(v); obs += o; secs += sec; samples += k
+    value = obs / secs
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": config_block(w, None, args.gpus),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": thr, "kind": "oracle",
+                             "sample": f"{samples} whole level-{lvl} subtrees ({obs} obs) of {w.name}, "
+                                       f"oracle subtree mode, {secs:.1f} s CPU wall"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_block(w, plan, ngpu):
+    th = w.thetas[0]
+    c = {"workload": f"{w.name}: n={w.n:,} {w.recipe}; M={w.M} J={w.J} r={w.r}"
+                     + (f" (r_hat={plan.r_hat})" if plan else ""),
+         "n_obs": w.n, "M": w.M, "J": w.J, "r": w.r,
+         "theta": {"cov": ["exponential", "matern32"][th[0]], "sigma2": th[1], "rho": th[2], "tau2": th[3]},
+         "parallelism": f"subtree-shard x{ngpu}" if ngpu > 1 else "1 GPU",
+         "l2": "inputs larger than L2 (plan + prior state >> 126 MB) and L2 flushed between steps"}
+    return c
+
+
+def run_gpu(args, rank, world, local_rank):
+    import torch
+    import paper_1905_00141_b200 as mra
+    from paper_1905_00141_b200 import build as mbuild
+    if rank == 0:
+        mbuild.build()
+    if world > 1:
+        torch.distributed.barrier()
+    mra.load_library()
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream()
+    t0 = time.time()
+    w = synth.make(args.config, n=args.n, device=dev)
+    log(f"[rank {rank}] data {w.name} n={w.n} in {time.time() - t0:.1f}s")
+    t0 = time.time()
+    plan = mra.mra_plan_create(w.x, w.y, w.M, w.J, w.r, device=local_rank, stream=stream, rank=rank,
+                               world=world)
+    log(f"[rank {rank}] plan in {time.time() - t0:.1f}s: n_retained={plan.n_retained} r_hat={plan.r_hat}")
+    thetas = w.thetas if args.config == "C4" else w.thetas[:1]
+    zd = torch.from_numpy(w.z).to(dev)
+    zpin = torch.from_numpy(w.z).pin_memory()
+    zpin_np = zpin.numpy()
+    flush = torch.empty(256 * 1024 * 1024 // 8 * 2, dtype=torch.float64, device=dev)   # 256 MB > L2
+    xbuf = None
+    if world > 1:
+        xbuf = torch.zeros(mra.mra_shard_size(plan), dtype=torch.float64, device=dev)
+
+    def step(host=False):
+        lls = []
+        for th in thetas:
+            if world == 1:
+                if host:
+                    lls.append(mra.mra_loglik(plan, zpin_np, th)["loglik"])
+                else:
+                    lls.append(mra.mra_loglik_dev(plan, zd, th)["loglik"])
+            else:
+                if host:
+                    zd.copy_(zpin, non_blocking=True)
+                xbuf.zero_()
+                mra.mra_loglik_shard(plan, zd, th, xbuf)
+                torch.distributed.reduce(xbuf, dst=0, op=torch.distributed.ReduceOp.SUM)
+                if rank == 0:
+                    lls.append(mra.mra_loglik_finish(plan, th, xbuf))
+                else:
+                    lls.append(float("nan"))
+        return lls
+
+    def timed(n, host=False, prof=False):
+        ev = []
+        launches = 0
+        if prof:
+            mra.mra_profile(plan, True)
+        sampler = ClockSampler(local_rank)
+        sampler.start()
+        for _ in range(n):
+            flush.fill_(1.0)
+            if world > 1:
+                torch.distributed.barrier()
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            lls = step(host)
+            b.record(stream)
+            torch.cuda.synchronize()
+            ev.append(a.elapsed_time(b))
+            launches += mra.mra_last_launches(plan) * (1 if len(thetas) == 1 else 1)
+        clocks = sampler.stop()
+        ms = float(np.sum(ev))
+        if world > 1:
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms = float(t.item())
+        kt = None
+        if prof:
+            t = mra.mra_kernel_times(plan)
+            mra.mra_profile(plan, False)
+            kt = ([t[k][0] for k in mra.KERNEL_CLASSES], [t[k][1] for k in mra.KERNEL_CLASSES])
+        return ms, lls, launches, clocks, kt
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ms, lls, launches, clocks, kt = timed(args.steps, prof=True)
+    ms_e2e, _, _, _, _ = timed(max(1, min(args.steps, 3)), host=True)
+    e2e_steps = max(1, min(args.steps, 3))
+    if rank != 0:
+        return
+    ntheta = len(thetas)
+    N = plan.n_retained
+    per_step = ms / args.steps
+    value = N * ntheta / (per_step / 1e3)
+    e2e_val = N * ntheta / ((ms_e2e / e2e_steps) / 1e3)
+    # roofline of the dominant kernel (bottom: leaves + level M-1 merge)
+    lay = mra.mra_plan_layout(plan)
+    sizes = np.diff(lay["leaf_off"])
+    fm = flop_model(sizes, w.M, w.J, plan.r_hat)
+    pk, src = peaks()
+    bf16 = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+    peak64 = bf16 * FP64_NOMINAL_TF / BF16_NOMINAL_TF
+    bottom_ms, bottom_n = kt[0][1], kt[1][1]
+    steps_th = args.steps * ntheta
+    roof = None
+    if bottom_n:
+        launch_ms = bottom_ms / bottom_n
+        flops_launch = fm["bottom"] / (bottom_n / steps_th)
+        achieved = flops_launch / (launch_ms / 1e3) / 1e12
+        traffic = None
+        try:
+            tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+            traffic = tj.get(w.name, {}).get("bytes_per_launch")
+        except Exception:
+            pass
+        roof = {"bound": "tensor", "achieved": round(achieved, 3), "peak": round(peak64, 3), "unit": "TFLOP/s",
+                "frac": round(achieved / peak64, 4), "traffic": traffic,
+                "kernel": "k_bottom (leaf prior chain + Sigma_j + Cholesky + TRSM + stacked SYRK + level M-1 merge)",
+                "flops_per_launch": flops_launch, "launch_ms": launch_ms,
+                "peak_source": f"{src} bf16_tflops_sustained {bf16} x {FP64_NOMINAL_TF}/{BF16_NOMINAL_TF} "
+                               "(guide's nominal fp64-tensor:bf16 ratio)",
+                "kernel_share_of_step": round(bottom_ms / ms, 4),
+                "step_fp64_tflops": round(fm["total"] * steps_th / (ms / 1e3) / 1e12, 3)}
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        v, o, sec, k, thr, lvl = oracle_sample(w, thetas[0], args.cpu_budget)
+        cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": "oracle",
+               "sample": f"{k} whole level-{lvl} subtrees ({o} obs) of {w.name}, oracle subtree mode, "
+                         f"{sec:.1f} s CPU wall"}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_block(w, plan, world),
+            "loglik": lls[0], "n_theta_per_step": ntheta, "flops_per_step": fm["total"] * ntheta,
+            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8 * w.n * ntheta,
+                    "d2h_bytes_per_step": 8 * ntheta},
+            "gpu_launches": int(launches),
+            "kernel_ms": {"prior": kt[0][0], "bottom": kt[0][1], "merge": kt[0][2], "other": kt[0][3],
+                          "launches": kt[1]},
+            "roofline": roof, "cpu_baseline": cpu, "clocks": clocks}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="mra", choices=["mra", "reference"])
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=list(synth.SPECS))
+    ap.add_argument("--n", type=int, default=None, help="override the config's n (same recipe)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle CPU work")
+    ap.add_argument("--ref-budget", type=float, default=10.0, help="seconds of oracle work per reference step")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    if world > 1:
+        import torch
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_gpu(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch
+            torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

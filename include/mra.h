@@ -141,6 +141,13 @@ mra_status mra_plan_layout(const mra_plan* plan, int64_t* perm, int64_t* leaf_of
  * the GPU analogue of the paper's sum n_j^2 dynamic split). own may be NULL. */
 mra_status mra_plan_shards(const mra_plan* plan, int* shard_level, int64_t* own, uint64_t* n_own);
 
+/* Live kernel timing: with profiling enabled every launch is bracketed by CUDA events on the
+ * plan's stream; mra_kernel_times returns the accumulated device milliseconds and launch counts
+ * since the last mra_profile(plan, 1) per kernel class [prior, bottom (leaves + level M-1
+ * merge), merge, other]. ms / launches: host arrays of 4, either may be NULL. */
+mra_status mra_profile(mra_plan* plan, int enable);
+mra_status mra_kernel_times(const mra_plan* plan, double* ms, uint64_t* launches);
+
 /* Number of kernel launches issued by the last evaluation call on this plan. */
 uint64_t mra_last_launches(const mra_plan* plan);
 

@@ -54,7 +54,7 @@ class _Post(ctypes.Structure):
 _lib = None
 EXPORTS = ["mra_plan_create", "mra_loglik", "mra_loglik_dev", "mra_loglik_batch_dev", "mra_shard_size",
            "mra_loglik_shard", "mra_loglik_finish", "mra_plan_info", "mra_plan_layout", "mra_plan_shards",
-           "mra_last_launches", "mra_plan_destroy", "mra_last_error"]
+           "mra_profile", "mra_kernel_times", "mra_last_launches", "mra_plan_destroy", "mra_last_error"]
 
 
 def load_library(path: str = LIB_PATH):
@@ -92,6 +92,10 @@ def load_library(path: str = LIB_PATH):
     lib.mra_plan_shards.restype = ctypes.c_int
     lib.mra_plan_shards.argtypes = [P, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int64),
                                     ctypes.POINTER(U64)]
+    lib.mra_profile.restype = ctypes.c_int
+    lib.mra_profile.argtypes = [P, ctypes.c_int]
+    lib.mra_kernel_times.restype = ctypes.c_int
+    lib.mra_kernel_times.argtypes = [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(U64)]
     lib.mra_last_launches.restype = U64
     lib.mra_last_launches.argtypes = [P]
     lib.mra_plan_destroy.restype = None
@@ -274,6 +278,21 @@ def mra_plan_shards(plan: PlanHandle) -> dict:
     _check(_lib.mra_plan_shards(plan.ptr, ctypes.byref(lvl), own.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
                                 ctypes.byref(n)))
     return dict(shard_level=lvl.value, own=own[: n.value])
+
+
+def mra_profile(plan: PlanHandle, enable: bool = True):
+    _check(_lib.mra_profile(plan.ptr, int(bool(enable))))
+
+
+KERNEL_CLASSES = ("prior", "bottom", "merge", "other")
+
+
+def mra_kernel_times(plan: PlanHandle) -> dict:
+    """Accumulated device ms and launch counts per kernel class since mra_profile(plan, True)."""
+    ms = (ctypes.c_double * 4)()
+    cnt = (ctypes.c_uint64 * 4)()
+    _check(_lib.mra_kernel_times(plan.ptr, ms, cnt))
+    return {k: (ms[i], cnt[i]) for i, k in enumerate(KERNEL_CLASSES)}
 
 
 def mra_last_launches(plan: PlanHandle) -> int:

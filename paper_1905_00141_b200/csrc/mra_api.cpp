@@ -69,7 +69,36 @@ struct mra_plan {
     double* smooth_d = nullptr;
     uint64_t launches = 0;
     std::vector<void*> allocs;
+    // live per-kernel timing (CUDA events on the plan stream around every launch)
+    bool prof = false;
+    std::vector<cudaEvent_t> evpool;
+    size_t ev_used = 0;
+    std::vector<std::pair<int, size_t>> recs;   // (kind, index of start event; end = +1)
+    double prof_ms[4] = {0, 0, 0, 0};
+    uint64_t prof_cnt[4] = {0, 0, 0, 0};
 };
+
+enum { KIND_PRIOR = 0, KIND_BOTTOM = 1, KIND_MERGE = 2, KIND_OTHER = 3 };
+
+static cudaEvent_t take_event(mra_plan* P) {
+    if (P->ev_used == P->evpool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        P->evpool.push_back(e);
+    }
+    return P->evpool[P->ev_used++];
+}
+static void prof_collect(mra_plan* P) {
+    for (auto& r : P->recs) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, P->evpool[r.second], P->evpool[r.second + 1]) == cudaSuccess) {
+            P->prof_ms[r.first] += ms;
+            P->prof_cnt[r.first]++;
+        }
+    }
+    P->recs.clear();
+    P->ev_used = 0;
+}
 
 static long long ipow(long long b, int e) {
     long long v = 1;
@@ -405,6 +434,7 @@ extern "C" void mra_plan_destroy(mra_plan* P) {
     if (!P) return;
     if (P->device >= 0 && cudaSetDevice(P->device) == cudaSuccess) {
         cudaDeviceSynchronize();
+        for (cudaEvent_t e : P->evpool) cudaEventDestroy(e);
         for (void* a : P->allocs) cudaFree(a);
     }
     delete P;
@@ -432,6 +462,24 @@ extern "C" mra_status mra_plan_layout(const mra_plan* P, int64_t* perm, int64_t*
 }
 
 extern "C" uint64_t mra_last_launches(const mra_plan* P) { return P ? P->launches : 0; }
+
+extern "C" mra_status mra_profile(mra_plan* P, int enable) {
+    if (!P) return fail(MRA_E_ARG, "plan is NULL");
+    P->prof = enable != 0;
+    P->recs.clear();
+    P->ev_used = 0;
+    for (int k = 0; k < 4; k++) { P->prof_ms[k] = 0; P->prof_cnt[k] = 0; }
+    return MRA_OK;
+}
+
+extern "C" mra_status mra_kernel_times(const mra_plan* P, double* ms, uint64_t* launches) {
+    if (!P) return fail(MRA_E_ARG, "plan is NULL");
+    for (int k = 0; k < 4; k++) {
+        if (ms) ms[k] = P->prof_ms[k];
+        if (launches) launches[k] = P->prof_cnt[k];
+    }
+    return MRA_OK;
+}
 
 extern "C" mra_status mra_plan_shards(const mra_plan* P, int* shard_level, int64_t* own, uint64_t* n_own) {
     if (!P) return fail(MRA_E_ARG, "plan is NULL");
@@ -463,12 +511,22 @@ static mra_status check_theta(const mra_theta* th) {
     return MRA_OK;
 }
 
-#define LCHK(expr)                                                                           \
+#define LCHK_K(kind, expr)                                                                   \
     do {                                                                                     \
+        size_t ev0_ = 0;                                                                     \
+        if (P->prof) {                                                                       \
+            ev0_ = P->ev_used;                                                               \
+            cudaEventRecord(take_event(P), P->st);                                           \
+        }                                                                                    \
         cudaError_t e_ = (expr);                                                             \
+        if (P->prof) {                                                                       \
+            cudaEventRecord(take_event(P), P->st);                                           \
+            P->recs.push_back({(kind), ev0_});                                               \
+        }                                                                                    \
         P->launches++;                                                                       \
         if (e_ != cudaSuccess) return fail(MRA_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
     } while (0)
+#define LCHK(expr) LCHK_K(KIND_OTHER, expr)
 
 static unsigned long long* take_counter(mra_plan* P) { return P->counters + (P->next_counter++ % P->n_counters); }
 
@@ -502,12 +560,12 @@ static mra_status eval_lower(mra_plan* P, const TreeParams& tp) {
     for (int m = 1; m < M; m++) {
         if (m < c) {
             TreeParams t2 = tp;
-            LCHK(launch_prior(t2, m, 0, ipow(J, m - 1), P->grid, P->ws, P->ws_stride, take_counter(P), st));
+            LCHK_K(KIND_PRIOR, launch_prior(t2, m, 0, ipow(J, m - 1), P->grid, P->ws, P->ws_stride, take_counter(P), st));
         } else {
             for (auto& rg : runs) {
                 long long f, cnt;
                 range_at(P, m, rg.first, rg.second, &f, &cnt);
-                LCHK(launch_prior(tp, m, f, cnt, P->grid, P->ws, P->ws_stride, take_counter(P), st));
+                LCHK_K(KIND_PRIOR, launch_prior(tp, m, f, cnt, P->grid, P->ws, P->ws_stride, take_counter(P), st));
             }
         }
     }
@@ -517,14 +575,14 @@ static mra_status eval_lower(mra_plan* P, const TreeParams& tp) {
             const long long b = std::min(rg.second, a + P->Kc);
             const int mg = M - 1;
             if (M == 1) {
-                LCHK(launch_bottom(tp, 0, 1, nullptr, 0, 0, P->grid, P->ws, P->L, take_counter(P), st));
+                LCHK_K(KIND_BOTTOM, launch_bottom(tp, 0, 1, nullptr, 0, 0, P->grid, P->ws, P->L, take_counter(P), st));
                 continue;
             }
             long long gf, gc;
             range_at(P, mg, a, b, &gf, &gc);
             double* gout = (mg <= c) ? P->out_full[mg] : P->out_chunk[mg];
             const long long gout_first = (mg <= c) ? 0 : gf;
-            LCHK(launch_bottom(tp, gf, gc, gout, gout_first, (int)q_of(mg, rh), P->grid, P->ws, P->L,
+            LCHK_K(KIND_BOTTOM, launch_bottom(tp, gf, gc, gout, gout_first, (int)q_of(mg, rh), P->grid, P->ws, P->L,
                                take_counter(P), st));
             for (int m = mg - 1; m >= c; m--) {
                 long long f, cnt, cf, ccnt;
@@ -534,7 +592,7 @@ static mra_status eval_lower(mra_plan* P, const TreeParams& tp) {
                 const long long cfirst = (m + 1 <= c) ? 0 : cf;
                 double* o = (m <= c) ? P->out_full[m] : P->out_chunk[m];
                 const long long ofirst = (m <= c) ? 0 : f;
-                LCHK(launch_merge(tp, m, f, cnt, cout_, cfirst, o, ofirst, (int)q_of(m, rh), P->grid, P->ws,
+                LCHK_K(KIND_MERGE, launch_merge(tp, m, f, cnt, cout_, cfirst, o, ofirst, (int)q_of(m, rh), P->grid, P->ws,
                                   P->ws_stride, take_counter(P), st));
             }
         }
@@ -546,7 +604,7 @@ static mra_status eval_lower(mra_plan* P, const TreeParams& tp) {
 static mra_status eval_upper(mra_plan* P, const TreeParams& tp) {
     const int M = P->M, J = P->J, rh = P->rh, c = P->c;
     for (int m = std::min(c - 1, M - 2); m >= 1; m--)
-        LCHK(launch_merge(tp, m, 0, ipow(J, m - 1), P->out_full[m + 1], 0, P->out_full[m], 0, (int)q_of(m, rh),
+        LCHK_K(KIND_MERGE, launch_merge(tp, m, 0, ipow(J, m - 1), P->out_full[m + 1], 0, P->out_full[m], 0, (int)q_of(m, rh),
                           P->grid, P->ws, P->ws_stride, take_counter(P), P->st));
     LCHK(launch_final(tp, (double)P->N, P->loglik_d, P->st));
     return MRA_OK;
@@ -557,6 +615,7 @@ static mra_status check_err(mra_plan* P) {
     cudaError_t e = cudaMemcpyAsync(h, P->err, 16, cudaMemcpyDeviceToHost, P->st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(P->st);
     if (e != cudaSuccess) return fail(MRA_E_CUDA, std::string("evaluation: ") + cudaGetErrorString(e));
+    if (P->prof) prof_collect(P);
     if (h[0]) {
         long long idx;
         std::memcpy(&idx, h + 2, 8);
