@@ -1,0 +1,29 @@
+"""Run a few MRA evaluations of a config on cuda:0 (for ncu / compute-sanitizer captures)."""
+import argparse
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_1905_00141_b200 as mra  # noqa: E402
+import synth  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="C2")
+ap.add_argument("--n", type=int, default=None)
+ap.add_argument("--evals", type=int, default=1)
+ap.add_argument("--M", type=int, default=None)
+a = ap.parse_args()
+w = synth.make(a.config, n=a.n, device="cuda")
+M = a.M or w.M
+plan = mra.mra_plan_create(w.x, w.y, M, w.J, w.r, stream=torch.cuda.current_stream())
+zd = torch.from_numpy(w.z).cuda()
+for i in range(a.evals):
+    t = time.time()
+    ll = mra.mra_loglik_dev(plan, zd, w.thetas[0])["loglik"]
+    torch.cuda.synchronize()
+    print(f"eval {i}: loglik={ll:.10f} {1e3 * (time.time() - t):.1f} ms launches={mra.mra_last_launches(plan)}")
