@@ -40,9 +40,9 @@ struct mra_plan {
     int device = 0, nsm = 148;
     cudaStream_t st = nullptr;
     // device state
-    double *px = nullptr, *py = nullptr, *zs = nullptr, *zin = nullptr;
+    double *pxy = nullptr, *zs = nullptr, *zin = nullptr;
     long long *perm_d = nullptr, *leaf_off_d = nullptr;
-    double *kx_d = nullptr, *ky_d = nullptr;
+    double* kxy_d = nullptr;
     double* prior = nullptr;
     long long prior_base[MAXM + 1] = {0};
     double *dreg = nullptr, *ureg = nullptr, *loglik_d = nullptr;
@@ -259,13 +259,13 @@ static mra_status size_device(mra_plan* P, double budget_gb) {
     WsLayout L{};
     L.ldG = (int)round_up(ncol, 2);
     L.ldS = (int)round_up(std::max<long long>(P->max_leaf, 1), 2);
-    L.ldA = ncol;
+    L.ldA = (int)round_up(ncol, 2);
     const long long nb = (std::max<long long>(P->max_leaf, 1) + 63) / 64;
     long long o = 0;
     L.oG = o; o += round_up(std::max<long long>(P->max_group, 1) * L.ldG, 32);
     L.oS = o; o += round_up(std::max<long long>(P->max_leaf, 1) * (long long)L.ldS, 32);
     L.oD = o; o += nb * 4096;
-    L.oA = o; o += round_up((long long)ncol * ncol, 32);
+    L.oA = o; o += round_up((long long)ncol * L.ldA, 32);
     L.oF = o; o += round_up((long long)ncol * rh, 32);
     L.oL = o; o += round_up((long long)rh * rh, 32);
     L.oV = o; o += round_up(std::max<long long>(P->max_leaf, 1), 32);
@@ -273,7 +273,7 @@ static mra_status size_device(mra_plan* P, double budget_gb) {
     long long merge_need = 0;
     for (int m = 1; m + 2 <= M; m++) {
         const long long qc = (long long)m * rh + 1, q = q_of(m, rh);
-        merge_need = std::max(merge_need, qc * qc + q * rh + (long long)rh * rh);
+        merge_need = std::max(merge_need, qc * (qc + 1) + q * rh + (long long)rh * rh + 64);
     }
     L.stride = round_up(std::max<long long>({o, merge_need, (long long)rh * rh}), 64);
     P->L = L;
@@ -393,14 +393,12 @@ extern "C" mra_status mra_plan_create(const double* x, const double* y, uint64_t
     mra_status st;
 #define TRY(x) do { if ((st = (x))) { mra_plan_destroy(P); return st; } } while (0)
     const long long N = P->N;
-    TRY(dalloc(P, (void**)&P->px, 8 * N, "px"));
-    TRY(dalloc(P, (void**)&P->py, 8 * N, "py"));
+    TRY(dalloc(P, (void**)&P->pxy, 16 * N, "pxy"));
     TRY(dalloc(P, (void**)&P->zs, 8 * N, "zs"));
     TRY(dalloc(P, (void**)&P->zin, 8 * (long long)n, "zin"));
     TRY(dalloc(P, (void**)&P->perm_d, 8 * N, "perm"));
     TRY(dalloc(P, (void**)&P->leaf_off_d, 8 * (P->nleaf + 1), "leaf_off"));
-    TRY(dalloc(P, (void**)&P->kx_d, 8 * std::max<long long>(1, P->nint * P->rh), "kx"));
-    TRY(dalloc(P, (void**)&P->ky_d, 8 * std::max<long long>(1, P->nint * P->rh), "ky"));
+    TRY(dalloc(P, (void**)&P->kxy_d, 16 * std::max<long long>(1, P->nint * P->rh), "kxy"));
     TRY(dalloc(P, (void**)&P->dreg, 8 * P->nreg, "dreg"));
     TRY(dalloc(P, (void**)&P->ureg, 8 * P->nreg, "ureg"));
     TRY(dalloc(P, (void**)&P->loglik_d, 8, "loglik"));
@@ -408,21 +406,18 @@ extern "C" mra_status mra_plan_create(const double* x, const double* y, uint64_t
     P->n_counters = 1 << 16;
     TRY(dalloc(P, (void**)&P->counters, 8 * (size_t)P->n_counters, "counters"));
     {
-        std::vector<double> sx(N), sy(N);
-        for (long long i = 0; i < N; i++) { sx[i] = x[P->perm[i]]; sy[i] = y[P->perm[i]]; }
+        std::vector<double> sxy(2 * N), kxy(2 * std::max<long long>(1, P->nint * P->rh));
+        for (long long i = 0; i < N; i++) { sxy[2 * i] = x[P->perm[i]]; sxy[2 * i + 1] = y[P->perm[i]]; }
+        for (long long i = 0; i < P->nint * P->rh; i++) { kxy[2 * i] = P->kx[i]; kxy[2 * i + 1] = P->ky[i]; }
         auto cp = [&](void* d, const void* h, size_t b) -> mra_status {
             cudaError_t e = cudaMemcpy(d, h, b, cudaMemcpyHostToDevice);
             if (e != cudaSuccess) return fail(MRA_E_CUDA, std::string("upload: ") + cudaGetErrorString(e));
             return MRA_OK;
         };
-        TRY(cp(P->px, sx.data(), 8 * N));
-        TRY(cp(P->py, sy.data(), 8 * N));
+        TRY(cp(P->pxy, sxy.data(), 16 * N));
         TRY(cp(P->perm_d, P->perm.data(), 8 * N));
         TRY(cp(P->leaf_off_d, P->leaf_off.data(), 8 * (P->nleaf + 1)));
-        if (P->nint) {
-            TRY(cp(P->kx_d, P->kx.data(), 8 * P->nint * P->rh));
-            TRY(cp(P->ky_d, P->ky.data(), 8 * P->nint * P->rh));
-        }
+        if (P->nint) TRY(cp(P->kxy_d, kxy.data(), 16 * P->nint * P->rh));
     }
     TRY(size_device(P, o.mem_budget_gb));
 #undef TRY
@@ -495,8 +490,8 @@ static TreeParams tree_params(mra_plan* P, const mra_theta* th) {
     tp.M = P->M; tp.J = P->J; tp.lj = P->lj; tp.rh = P->rh;
     tp.cp.kind = th->cov; tp.cp.s2 = th->sigma2; tp.cp.rho = th->rho; tp.cp.xs = P->xs; tp.cp.ys = P->ys;
     tp.tau2 = th->tau2;
-    tp.px = P->px; tp.py = P->py; tp.zs = P->zs; tp.leaf_off = P->leaf_off_d;
-    tp.kx = P->kx_d; tp.ky = P->ky_d; tp.prior = P->prior;
+    tp.pxy = P->pxy; tp.zs = P->zs; tp.leaf_off = P->leaf_off_d;
+    tp.kxy = P->kxy_d; tp.prior = P->prior;
     for (int m = 0; m <= MAXM; m++) { tp.prior_base[m] = P->prior_base[m]; tp.post_base[m] = P->post_base[m]; }
     tp.dreg = P->dreg; tp.ureg = P->ureg; tp.err = P->err; tp.post = nullptr;
     return tp;

@@ -35,38 +35,41 @@ struct CovP {
     double s2, rho, xs, ys;
 };
 
-// one logical operand of size rows x K:
+// one logical operand of size rows x K (points are interleaved (x, y) pairs):
 //   MEMN: X[i][k] = p[i*ld + k]     MEMT: X[i][k] = p[k*ld + i]
-//   COVK: X[i][k] = C((rx[i], ry[i]), (cx[k], cy[k]))
+//   COVK: X[i][k] = C(p[2i], p[2i+1]; q[2k], q[2k+1])
 struct Op {
     const double* p;
+    const double* q;
     long long ld;
-    const double *rx, *ry, *cx, *cy;
 };
 
-// epilogue initial value: ZERO, MEM (p[i*ld+j], may alias C), COV (+ diag on i == j)
+// epilogue initial value: ZERO, MEM (p[i*ld+j], may alias C), COV C(p_i, q_j) (+ diag on i == j)
 struct CInit {
     int kind;  // 0 zero, 1 mem, 2 cov
     const double* p;
+    const double* q;
     long long ld;
-    const double *rx, *ry, *cx, *cy;
     double diag;
 };
 
 __device__ __forceinline__ Op op_mem(const double* p, long long ld) {
-    Op o; o.p = p; o.ld = ld; o.rx = o.ry = o.cx = o.cy = nullptr; return o;
+    Op o; o.p = p; o.q = nullptr; o.ld = ld; return o;
 }
-__device__ __forceinline__ Op op_cov(const double* rx, const double* ry, const double* cx, const double* cy) {
-    Op o; o.p = nullptr; o.ld = 0; o.rx = rx; o.ry = ry; o.cx = cx; o.cy = cy; return o;
+__device__ __forceinline__ Op op_cov(const double* rowpts, const double* kpts) {
+    Op o; o.p = rowpts; o.q = kpts; o.ld = 0; return o;
 }
 __device__ __forceinline__ CInit ci_zero() {
-    CInit c; c.kind = 0; c.p = nullptr; c.ld = 0; c.rx = c.ry = c.cx = c.cy = nullptr; c.diag = 0; return c;
+    CInit c; c.kind = 0; c.p = nullptr; c.q = nullptr; c.ld = 0; c.diag = 0; return c;
 }
 __device__ __forceinline__ CInit ci_mem(const double* p, long long ld) {
     CInit c = ci_zero(); c.kind = 1; c.p = p; c.ld = ld; return c;
 }
-__device__ __forceinline__ CInit ci_cov(const double* rx, const double* ry, const double* cx, const double* cy, double diag) {
-    CInit c = ci_zero(); c.kind = 2; c.rx = rx; c.ry = ry; c.cx = cx; c.cy = cy; c.diag = diag; return c;
+__device__ __forceinline__ CInit ci_cov(const double* rowpts, const double* colpts, double diag) {
+    CInit c = ci_zero(); c.kind = 2; c.p = rowpts; c.q = colpts; c.diag = diag; return c;
+}
+__device__ __forceinline__ double2 ldpt(const double* pts, int i) {
+    return reinterpret_cast<const double2*>(pts)[i];
 }
 
 __device__ __forceinline__ double covf(const CovP& c, double x1, double y1, double x2, double y2) {
@@ -83,34 +86,82 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
-// stage rows [r0, r0+nr) x k [k0, k0+nk) of an operand into smem (zero-padded to 64 x 32)
+// ------------------------------------------------------------- async tile staging
+constexpr int NSTAGE = 3;                  // cp.async pipeline depth
+constexpr int STAGE_DBL = 2 * TILE_DBL;    // A tile + B tile
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+// 8-byte async copy global -> smem; src_bytes 0 zero-fills (the source is not read)
+__device__ __forceinline__ void cp_async8(double* s, const double* g, int src_bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(s)), "l"(g), "r"(src_bytes));
+}
+// 16-byte async copy (L2 only); src_bytes in {0, 8, 16}, the rest zero-filled
+__device__ __forceinline__ void cp_async16(double* s, const double* g, int src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(s)), "l"(g), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ bool op_aligned16(const Op& op) {
+    return ((reinterpret_cast<uintptr_t>(op.p) & 15) == 0) && ((op.ld & 1) == 0);
+}
+
+// stage rows [r0, r0+nr) x k [k0, k0+nk) of an operand into smem (zero-padded to 64 x 32).
+// Memory operands go through cp.async (16-byte copies when aligned); covariance operands are
+// generated in registers (fused covariance generation) and stored.
 template <int KIND>
-__device__ __forceinline__ void load_tile(double* s, const Op& op, int r0, int nr, int k0, int nk,
-                                          const CovP& cp) {
+__device__ __forceinline__ void load_tile_async(double* s, const Op& op, int r0, int nr, int k0, int nk,
+                                                const CovP& cp, bool al16) {
     const int tid = threadIdx.x;
-    if (KIND == MEMT) {
-#pragma unroll 4
-        for (int e = tid; e < TM * TK; e += NT) {
-            int kk = e >> 6, row = e & 63;
-            double v = 0.0;
-            if (row < nr && kk < nk) v = op.p[(long long)(k0 + kk) * op.ld + r0 + row];
-            s[kk * LDT + row] = v;
+    if (KIND == MEMN) {
+        if (al16) {
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                const int e = tid + NT * i, row = e >> 4, kk = (e & 15) * 2;
+                const int ok = (row < nr) ? min(2, max(0, nk - kk)) : 0;
+                const double* g = ok ? op.p + (long long)(r0 + row) * op.ld + k0 + kk : op.p;
+                cp_async16(s + row * LDN + kk, g, ok * 8);
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                const int e = tid + NT * i, row = e >> 5, kk = e & 31;
+                const bool ok = row < nr && kk < nk;
+                cp_async8(s + row * LDN + kk, ok ? op.p + (long long)(r0 + row) * op.ld + k0 + kk : op.p, ok ? 8 : 0);
+            }
         }
-    } else if (KIND == MEMN) {
-#pragma unroll 4
-        for (int e = tid; e < TM * TK; e += NT) {
-            int row = e >> 5, kk = e & 31;
-            double v = 0.0;
-            if (row < nr && kk < nk) v = op.p[(long long)(r0 + row) * op.ld + k0 + kk];
-            s[row * LDN + kk] = v;
+    } else if (KIND == MEMT) {
+        if (al16) {
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                const int e = tid + NT * i, kk = e >> 5, row = (e & 31) * 2;
+                const int ok = (kk < nk) ? min(2, max(0, nr - row)) : 0;
+                const double* g = ok ? op.p + (long long)(k0 + kk) * op.ld + r0 + row : op.p;
+                cp_async16(s + kk * LDT + row, g, ok * 8);
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                const int e = tid + NT * i, kk = e >> 6, row = e & 63;
+                const bool ok = row < nr && kk < nk;
+                cp_async8(s + kk * LDT + row, ok ? op.p + (long long)(k0 + kk) * op.ld + r0 + row : op.p, ok ? 8 : 0);
+            }
         }
     } else {
+        const int kk = tid & 31, rw = tid >> 5;
+        const bool kok = kk < nk;
+        const double2 qk = kok ? ldpt(op.q, k0 + kk) : make_double2(0.0, 0.0);
 #pragma unroll 2
-        for (int e = tid; e < TM * TK; e += NT) {
-            int row = e >> 5, kk = e & 31;
+        for (int i = 0; i < 8; i++) {
+            const int row = rw + 8 * i;
             double v = 0.0;
-            if (row < nr && kk < nk)
-                v = covf(cp, op.rx[r0 + row], op.ry[r0 + row], op.cx[k0 + kk], op.cy[k0 + kk]);
+            if (kok && row < nr) {
+                const double2 pr = ldpt(op.p, r0 + row);
+                v = covf(cp, pr.x, pr.y, qk.x, qk.y);
+            }
             s[row * LDN + kk] = v;
         }
     }
@@ -121,33 +172,69 @@ __device__ __forceinline__ double frag(const double* s, int row, int k) {
     return KIND == MEMT ? s[k * LDT + row] : s[row * LDN + k];
 }
 
-// accumulate one K-segment into the warp's 16x32 sub-tile of output tile (r0, c0)
+// 8 DMMAs per k-step of 4 on the warp's 16 x 32 sub-tile
 template <int KA, int KB>
-__device__ __forceinline__ void gemm_segment(double (&acc)[2][4][2], const Op& A, const Op& B, int K,
-                                             int r0, int nr, int c0, int nc, const CovP& cp,
-                                             double* As, double* Bs) {
+__device__ __forceinline__ void mma_ktile(double (&acc)[2][4][2], const double* As, const double* Bs, int nk) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
     const int wr = (warp >> 1) * 16, wc = (warp & 1) * 32;
-    for (int k0 = 0; k0 < K; k0 += TK) {
-        const int nk = min(TK, K - k0);
-        __syncthreads();
-        load_tile<KA>(As, A, r0, nr, k0, nk, cp);
-        load_tile<KB>(Bs, B, c0, nc, k0, nk, cp);
-        __syncthreads();
+    auto step = [&](int kk) {
+        double a[2], b[4];
+#pragma unroll
+        for (int mi = 0; mi < 2; mi++) a[mi] = frag<KA>(As, wr + mi * 8 + g, kk + t);
+#pragma unroll
+        for (int ni = 0; ni < 4; ni++) b[ni] = frag<KB>(Bs, wc + ni * 8 + g, kk + t);
+#pragma unroll
+        for (int mi = 0; mi < 2; mi++)
+#pragma unroll
+            for (int ni = 0; ni < 4; ni++) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+    };
+    if (nk == TK) {
+#pragma unroll
+        for (int kk = 0; kk < TK; kk += 4) step(kk);
+    } else {
         const int nk4 = (nk + 3) & ~3;
-        for (int kk = 0; kk < nk4; kk += 4) {
-            double a[2], b[4];
-#pragma unroll
-            for (int mi = 0; mi < 2; mi++) a[mi] = frag<KA>(As, wr + mi * 8 + g, kk + t);
-#pragma unroll
-            for (int ni = 0; ni < 4; ni++) b[ni] = frag<KB>(Bs, wc + ni * 8 + g, kk + t);
-#pragma unroll
-            for (int mi = 0; mi < 2; mi++)
-#pragma unroll
-                for (int ni = 0; ni < 4; ni++) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
-        }
+        for (int kk = 0; kk < nk4; kk += 4) step(kk);
     }
+}
+
+// accumulate both K-segments of one output tile through an NSTAGE-deep cp.async pipeline
+template <int KA0, int KB0, int KA1, int KB1>
+__device__ __forceinline__ void tile_pipeline(double (&acc)[2][4][2], const Op& A0, const Op& B0, int K0,
+                                              const Op& A1, const Op& B1, int K1, int r0, int nr, int c0, int nc,
+                                              const CovP& cp, double* smem) {
+    const int T0 = (K0 + TK - 1) / TK, T1 = (K1 + TK - 1) / TK, T = T0 + T1;
+    const bool a0 = op_aligned16(A0), b0 = op_aligned16(B0), a1 = op_aligned16(A1), b1 = op_aligned16(B1);
+    __syncthreads();   // the stage buffers (and any smem view aliasing them) are free
+    // single issue site: iterations kt < 0 only prefetch (pipeline prologue)
+#pragma unroll 1
+    for (int kt = -(NSTAGE - 1); kt < T; kt++) {
+        if (kt >= 0) {
+            cp_async_wait<NSTAGE - 2>();
+            __syncthreads();
+        }
+        const int ki = kt + NSTAGE - 1;
+        if (ki < T) {
+            double* As = smem + (ki % NSTAGE) * STAGE_DBL;
+            double* Bs = As + TILE_DBL;
+            if (ki < T0) {
+                const int k0 = ki * TK, nk = min(TK, K0 - k0);
+                load_tile_async<KA0>(As, A0, r0, nr, k0, nk, cp, a0);
+                load_tile_async<KB0>(Bs, B0, c0, nc, k0, nk, cp, b0);
+            } else {
+                const int k0 = (ki - T0) * TK, nk = min(TK, K1 - k0);
+                load_tile_async<KA1>(As, A1, r0, nr, k0, nk, cp, a1);
+                load_tile_async<KB1>(Bs, B1, c0, nc, k0, nk, cp, b1);
+            }
+        }
+        cp_async_commit();
+        if (kt < 0) continue;
+        const double* As = smem + (kt % NSTAGE) * STAGE_DBL;
+        const double* Bs = As + TILE_DBL;
+        if (kt < T0) mma_ktile<KA0, KB0>(acc, As, Bs, min(TK, K0 - kt * TK));
+        else mma_ktile<KA1, KB1>(acc, As, Bs, min(TK, K1 - (kt - T0) * TK));
+    }
+    cp_async_wait<0>();
 }
 
 // C[Mr x Nc] = init + alpha * (A0 B0^T [K0] + A1 B1^T [K1]); lower != 0 -> only i >= j written.
@@ -157,8 +244,6 @@ template <int KA0, int KB0, int KA1, int KB1>
 __device__ void cta_gemm(int Mr, int Nc, int lower, const Op& A0, const Op& B0, int K0, const Op& A1,
                          const Op& B1, int K1, const CInit& ci, double alpha, double* C, long long ldc,
                          const CovP& cp, double* smem) {
-    double* As = smem;
-    double* Bs = smem + TILE_DBL;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
     const int wr = (warp >> 1) * 16, wc = (warp & 1) * 32;
@@ -173,8 +258,7 @@ __device__ void cta_gemm(int Mr, int Nc, int lower, const Op& A0, const Op& B0, 
             for (int mi = 0; mi < 2; mi++)
 #pragma unroll
                 for (int ni = 0; ni < 4; ni++) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-            if (K0 > 0) gemm_segment<KA0, KB0>(acc, A0, B0, K0, r0, nr, c0, nc, cp, As, Bs);
-            if (K1 > 0) gemm_segment<KA1, KB1>(acc, A1, B1, K1, r0, nr, c0, nc, cp, As, Bs);
+            if (K0 + K1 > 0) tile_pipeline<KA0, KB0, KA1, KB1>(acc, A0, B0, K0, A1, B1, K1, r0, nr, c0, nc, cp, smem);
 #pragma unroll
             for (int mi = 0; mi < 2; mi++)
 #pragma unroll
@@ -186,7 +270,10 @@ __device__ void cta_gemm(int Mr, int Nc, int lower, const Op& A0, const Op& B0, 
                             double v;
                             if (ci.kind == 0) v = 0.0;
                             else if (ci.kind == 1) v = ci.p[(long long)i * ci.ld + j];
-                            else v = covf(cp, ci.rx[i], ci.ry[i], ci.cx[j], ci.cy[j]) + (i == j ? ci.diag : 0.0);
+                            else {
+                                const double2 pi = ldpt(ci.p, i), pj = ldpt(ci.q, j);
+                                v = covf(cp, pi.x, pi.y, pj.x, pj.y) + (i == j ? ci.diag : 0.0);
+                            }
                             C[(long long)i * ldc + j] = v + alpha * acc[mi][ni][e];
                         }
                     }
@@ -196,67 +283,140 @@ __device__ void cta_gemm(int Mr, int Nc, int lower, const Op& A0, const Op& B0, 
 }
 
 // ---------------------------------------------------------------- small factor blocks
-// a: smem n x n (ld LDB), lower Cholesky in place; returns log|A| in *logdet (all threads);
-// sets *bad (smem flag) if not positive definite. diagv: smem scratch [64].
-__device__ void chol_small(double* a, int n, double* diagv, int* bad, double* red, double* logdet) {
-    const int tid = threadIdx.x;
-    for (int j = 0; j < n; j++) {
-        const double ajj = a[j * LDB + j];
-        const double ljj = sqrt(ajj > 0.0 ? ajj : 1.0);
-        if (tid == 0) {
-            if (!(ajj > 0.0)) *bad = 1;
-            diagv[j] = ljj;
-        }
-        const double inv = 1.0 / ljj;
-        for (int i = j + 1 + tid; i < n; i += NT) a[i * LDB + j] *= inv;
-        __syncthreads();
-        const int m = n - j - 1;
-        for (int e = tid; e < m * m; e += NT) {
-            const int ii = e / m, kk = e - ii * m;
-            if (kk <= ii) a[(j + 1 + ii) * LDB + j + 1 + kk] -= a[(j + 1 + ii) * LDB + j] * a[(j + 1 + kk) * LDB + j];
-        }
-        __syncthreads();
+// In-smem Cholesky + triangular inverse of an n <= 64 block, blocked by 16 so that the CTA
+// synchronises ~20 times instead of twice per column:
+//   per 16-block: warp 0 factors and inverts the diagonal block (warp-synchronous), all threads
+//   form the panel L_ib = A_ib D_bb^{-T} and the trailing update A -= L_ib L_kb^T;
+//   then X = L^{-1} is assembled block-row by block-row: X_ij = -X_ii sum_k L_ik X_kj.
+// a: n x n (ld LDB), lower, overwritten by L. x: n x n (ld LDB) receives L^{-1} (upper part 0).
+// tmp: >= 3*256 doubles of smem scratch. Returns log|A| (all threads); *bad set if not PD.
+__device__ __noinline__ double chol_inv_small(double* a, double* x, int n, double* diagv, int* bad, double* red, double* tmp) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nbk = (n + 15) >> 4;
+    for (int e = tid; e < 64 * 64; e += NT) {
+        const int i = e >> 6, j = e & 63;
+        if (i < n && j < n) x[i * LDB + j] = 0.0;
     }
-    for (int j = tid; j < n; j += NT) a[j * LDB + j] = diagv[j];
-    // log-determinant: warp 0 reduces 2 sum log L_jj
-    if (tid < 32) {
-        double s = 0.0;
-        for (int j = tid; j < n; j += 32) s += log(diagv[j]);
+    __syncthreads();
+    for (int b = 0; b < nbk; b++) {
+        const int j0 = b * 16, nb = min(16, n - j0);
+        if (warp == 0) {
+            double* d = a + j0 * LDB + j0;
+            for (int j = 0; j < nb; j++) {
+                const double ajj = d[j * LDB + j];
+                const double ljj = sqrt(ajj > 0.0 ? ajj : 1.0);
+                if (lane == 0) {
+                    if (!(ajj > 0.0)) *bad = 1;
+                    diagv[j0 + j] = ljj;
+                }
+                __syncwarp();
+                if (lane > j && lane < nb) d[lane * LDB + j] /= ljj;
+                __syncwarp();
+                const int m = nb - j - 1;
+                for (int e = lane; e < m * m; e += 32) {
+                    const int ii = e / m, kk = e - ii * m;
+                    if (kk <= ii) d[(j + 1 + ii) * LDB + j + 1 + kk] -= d[(j + 1 + ii) * LDB + j] * d[(j + 1 + kk) * LDB + j];
+                }
+                __syncwarp();
+            }
+            if (lane < nb) d[lane * LDB + lane] = diagv[j0 + lane];
+            __syncwarp();
+            // inverse of the diagonal block, one column per lane
+            double* xd = x + j0 * LDB + j0;
+            if (lane < nb) {
+                const int c = lane;
+                xd[c * LDB + c] = 1.0 / d[c * LDB + c];
+                for (int i = c + 1; i < nb; i++) {
+                    double sacc = 0.0;
+                    for (int k = c; k < i; k++) sacc += d[i * LDB + k] * xd[k * LDB + c];
+                    xd[i * LDB + c] = -sacc / d[i * LDB + i];
+                }
+            }
+        }
+        __syncthreads();
+        const int r0 = j0 + nb, nr = n - r0;
+        if (nr > 0) {
+            // panel: L_ib = A_ib X_bb^T  (rows r0..n-1, cols j0..j0+nb-1)
+            const double* xd = x + j0 * LDB + j0;
+            double v[3];   // nr * nb <= 48 * 16 = 3 * NT
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (tid == 0) *red = 2.0 * s;
-    }
-    __syncthreads();
-    *logdet = *red;
-    __syncthreads();
-}
-
-// x = L^{-1} (lower triangular, n <= 64), both in smem with ld LDB; upper part of x zeroed
-__device__ void trinv_small(const double* L, double* x, int n) {
-    const int tid = threadIdx.x;
-    const int c = tid & 63, part = tid >> 6;  // 4 threads per column: part 0 computes, others zero-fill
-    if (part == 0 && c < n) {
-        for (int i = 0; i < c; i++) x[i * LDB + c] = 0.0;
-        x[c * LDB + c] = 1.0 / L[c * LDB + c];
-        for (int i = c + 1; i < n; i++) {
-            double s = 0.0;
-            for (int k = c; k < i; k++) s += L[i * LDB + k] * x[k * LDB + c];
-            x[i * LDB + c] = -s / L[i * LDB + i];
+            for (int c = 0; c < 3; c++) {
+                const int e = tid + c * NT;
+                double sacc = 0.0;
+                if (e < nr * nb) {
+                    const int i = r0 + e / nb, jj = e % nb;
+                    for (int kk = 0; kk <= jj; kk++) sacc += a[i * LDB + j0 + kk] * xd[jj * LDB + kk];
+                }
+                v[c] = sacc;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int c = 0; c < 3; c++) {
+                const int e = tid + c * NT;
+                if (e < nr * nb) a[(r0 + e / nb) * LDB + j0 + e % nb] = v[c];
+            }
+            __syncthreads();
+            // trailing update of the lower part
+            for (int e = tid; e < nr * nr; e += NT) {
+                const int ii = e / nr, kk = e - ii * nr;
+                if (kk <= ii) {
+                    const double* li = a + (r0 + ii) * LDB + j0;
+                    const double* lk = a + (r0 + kk) * LDB + j0;
+                    double sacc = 0.0;
+#pragma unroll 4
+                    for (int q = 0; q < nb; q++) sacc += li[q] * lk[q];
+                    a[(r0 + ii) * LDB + r0 + kk] -= sacc;
+                }
+            }
+            __syncthreads();
         }
     }
+    // off-diagonal blocks of X = L^{-1}, block row by block row
+    for (int bi = 1; bi < nbk; bi++) {
+        const int i0 = bi * 16, ni = min(16, n - i0);
+        // tmp[bj] (ni x 16) = sum_{k=j0}^{i0-1} L[i0+r][k] X[k][j0+c]
+        for (int e = tid; e < bi * 256; e += NT) {
+            const int bj = e >> 8, r = (e >> 4) & 15, c = e & 15;
+            double sacc = 0.0;
+            if (r < ni)
+                for (int k = bj * 16 + c; k < i0; k++) sacc += a[(i0 + r) * LDB + k] * x[k * LDB + bj * 16 + c];
+            tmp[e] = sacc;
+        }
+        __syncthreads();
+        for (int e = tid; e < bi * 256; e += NT) {
+            const int bj = e >> 8, r = (e >> 4) & 15, c = e & 15;
+            if (r < ni) {
+                double sacc = 0.0;
+                for (int k = 0; k <= r; k++) sacc += x[(i0 + r) * LDB + i0 + k] * tmp[(bj << 8) + (k << 4) + c];
+                x[(i0 + r) * LDB + bj * 16 + c] = -sacc;
+            }
+        }
+        __syncthreads();
+    }
+    if (tid < 32) {
+        double sacc = 0.0;
+        for (int j = tid; j < n; j += 32) sacc += log(diagv[j]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+        if (tid == 0) *red = 2.0 * sacc;
+    }
     __syncthreads();
+    const double ld = *red;
+    __syncthreads();
+    return ld;
 }
 
 // smem layout (doubles): [ main: GEMM tiles | factor blocks ] [ misc: 32 doubles ]
 //   factor view of main: blk[64*LDB] | inv[64*LDB] | diag[64]
 //   misc: red[0..15] (reductions) | bad flag (int) at misc+16 | work item at misc+18
-constexpr int FAC_DBL = 2 * 64 * LDB + 64;
-constexpr int MAIN_DBL = (FAC_DBL > 2 * TILE_DBL) ? FAC_DBL : 2 * TILE_DBL;
+constexpr int FAC_DBL = 2 * 64 * LDB + 64 + 768;
+constexpr int MAIN_DBL = (FAC_DBL > NSTAGE * STAGE_DBL) ? FAC_DBL : NSTAGE * STAGE_DBL;
 constexpr int SMEM_DBL = MAIN_DBL + 32;
 struct FacSmem {
     double* blk;
     double* inv;
     double* diagv;
+    double* tmp;
     double* red;
     int* bad;
 };
@@ -266,6 +426,7 @@ __device__ __forceinline__ FacSmem fac_smem(double* smem) {
     f.blk = smem;
     f.inv = smem + 64 * LDB;
     f.diagv = smem + 2 * 64 * LDB;
+    f.tmp = f.diagv + 64;
     f.red = misc_smem(smem);
     f.bad = reinterpret_cast<int*>(misc_smem(smem) + 16);
     return f;
@@ -302,10 +463,7 @@ __device__ double chol_blocked(double* S, int n, long long ld, double* Dinv, con
     for (int j0 = 0; j0 < n; j0 += 64) {
         const int nb = min(64, n - j0);
         load_block_lower(f.blk, S + (long long)j0 * ld + j0, ld, nb, 0.0);
-        double ldet;
-        chol_small(f.blk, nb, f.diagv, f.bad, f.red, &ldet);
-        total += ldet;
-        trinv_small(f.blk, f.inv, nb);
+        total += chol_inv_small(f.blk, f.inv, nb, f.diagv, f.bad, f.red, f.tmp);
         double* Di = Dinv + (long long)(j0 / 64) * 4096;
         store_block_lower(f.blk, S + (long long)j0 * ld + j0, ld, nb);
         store_block_full(f.inv, Di, 64, nb);

@@ -18,12 +18,10 @@ struct TreeParams {
     int M, J, lj, rh;           // levels, children, log2 J, r_hat
     CovParams cp;
     double tau2;
-    const double* px;           // [N] sorted (by leaf) retained observation x
-    const double* py;           // [N] y
+    const double* pxy;          // [2N] sorted (by leaf) retained observations, interleaved (x, y)
     const double* zs;           // [N] observed values in sorted order
     const long long* leaf_off;  // [n_leaves + 1]
-    const double* kx;           // [n_interior * rh] knots, level-major regions
-    const double* ky;
+    const double* kxy;          // [2 * n_interior * rh] knots, level-major regions, interleaved (x, y)
     double* prior;              // chain rows R_R = [Linv_R | -U^{m-1}_R .. -U^1_R], rh x m*rh each
     long long prior_base[MAXM + 1];  // offset (doubles) of level m's first region
     double* dreg;               // [n_regions] per-region log-det term

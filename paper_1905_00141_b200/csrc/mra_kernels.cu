@@ -21,6 +21,10 @@
 #include "mra_device.cuh"
 #include "mra_internal.h"
 
+#ifndef MRA_MINB
+#define MRA_MINB 2   // resident CTAs per SM the register allocation is sized for
+#endif
+
 namespace mra {
 
 __device__ __forceinline__ long long lvl_first(int J, int m) {
@@ -59,15 +63,15 @@ __device__ __forceinline__ const double* chain_row(const TreeParams& tp, int k, 
 // V chain of a point set P (n points inside level-m region t): for k = 1..m
 //   V^k(P) = [ C(P, Q_{a_k}) | V^{k-1}(P) .. V^1(P) ] R_{a_k}^T        (K = k * rh)
 // written into Gc at column block m-k (levels in descending order), ld ldg.
-__device__ void point_chain(const TreeParams& tp, int m, long long t, int n, const double* px, const double* py,
-                            double* Gc, long long ldg, const CovP& cp, double* smem) {
+__device__ void point_chain(const TreeParams& tp, int m, long long t, int n, const double* pts, double* Gc,
+                            long long ldg, const CovP& cp, double* smem) {
     const int rh = tp.rh;
     for (int k = 1; k <= m; k++) {
         const long long ak = t >> (tp.lj * (m - k));
         const long long akid = lvl_first(tp.J, k) + ak;
         const long long ldk = (long long)k * rh;
         const double* Rk = chain_row(tp, k, ak);
-        cta_gemm<COVK, MEMN, MEMN, MEMN>(n, rh, 0, op_cov(px, py, tp.kx + akid * rh, tp.ky + akid * rh),
+        cta_gemm<COVK, MEMN, MEMN, MEMN>(n, rh, 0, op_cov(pts, tp.kxy + 2 * akid * rh),
                                          op_mem(Rk, ldk), rh, op_mem(Gc + (long long)(m - k + 1) * rh, ldg),
                                          op_mem(Rk + rh, ldk), (k - 1) * rh, ci_zero(), 1.0,
                                          Gc + (long long)(m - k) * rh, ldg, cp, smem);
@@ -75,7 +79,7 @@ __device__ void point_chain(const TreeParams& tp, int m, long long t, int n, con
 }
 
 // --------------------------------------------------------------------------- prior
-__global__ void __launch_bounds__(NT, 2)
+__global__ void __launch_bounds__(NT, MRA_MINB)
 k_prior(TreeParams tp, int m, long long t_first, long long nitems, double* ws, long long ws_stride,
         unsigned long long* counter) {
     extern __shared__ double smem[];
@@ -91,19 +95,16 @@ k_prior(TreeParams tp, int m, long long t_first, long long nitems, double* ws, l
         const long long t = t_first + it;
         const long long id = lvl_first(tp.J, m) + t;
         double* R = tp.prior + tp.prior_base[m] + t * ldR * rh;
-        const double* qx = tp.kx + id * rh;
-        const double* qy = tp.ky + id * rh;
+        const double* q = tp.kxy + 2 * id * rh;
         // V^k_R for k < m into R's blocks m-k (they become -U after the inverse is known)
-        point_chain(tp, m - 1, t >> tp.lj, rh, qx, qy, R + rh, ldR, cp, smem);
+        point_chain(tp, m - 1, t >> tp.lj, rh, q, R + rh, ldR, cp, smem);
         // W^m_R = C(Q_R, Q_R) - sum_k V^k V^kT
         cta_gemm<MEMN, MEMN, MEMN, MEMN>(rh, rh, 1, op_mem(R + rh, ldR), op_mem(R + rh, ldR), (m - 1) * rh,
-                                         op_mem(R, ldR), op_mem(R, ldR), 0, ci_cov(qx, qy, qx, qy, 0.0), -1.0,
+                                         op_mem(R, ldR), op_mem(R, ldR), 0, ci_cov(q, q, 0.0), -1.0,
                                          W, rh, cp, smem);
         load_block_lower(f.blk, W, rh, rh, 0.0);
-        double ld;
-        chol_small(f.blk, rh, f.diagv, f.bad, f.red, &ld);
+        chol_inv_small(f.blk, f.inv, rh, f.diagv, f.bad, f.red, f.tmp);
         if (*f.bad && threadIdx.x == 0) set_err(tp.err, m, t);
-        trinv_small(f.blk, f.inv, rh);
         store_block_full(f.inv, R, ldR, rh);
         __syncthreads();
         // -U = -L^{-1} V  (in place over the V blocks; single row tile)
@@ -120,10 +121,8 @@ __device__ double merge_core(const double* A, int rh, long long ldA, double* O, 
                              int* err, int level, long long t, const CovP& cp, double* smem) {
     FacSmem f = fac_smem(smem);
     load_block_lower(f.blk, A, ldA, rh, 1.0);
-    double ld;
-    chol_small(f.blk, rh, f.diagv, f.bad, f.red, &ld);
+    const double ld = chol_inv_small(f.blk, f.inv, rh, f.diagv, f.bad, f.red, f.tmp);
     if (*f.bad && threadIdx.x == 0) set_err(err, level, t);
-    trinv_small(f.blk, f.inv, rh);
     store_block_full(f.inv, Li, rh, rh);
     __syncthreads();
     cta_gemm<MEMN, MEMN, MEMN, MEMN>(q, rh, 0, op_mem(A + (long long)rh * ldA, ldA), op_mem(Li, rh), rh,
@@ -143,7 +142,7 @@ __device__ __forceinline__ void save_post(const TreeParams& tp, int m, long long
 }
 
 // -------------------------------------------------------------------------- bottom
-__global__ void __launch_bounds__(NT, 2)
+__global__ void __launch_bounds__(NT, MRA_MINB)
 k_bottom(TreeParams tp, long long g_first, long long g_count, double* out, long long out_first, int q, double* ws,
          WsLayout L, unsigned long long* counter) {
     extern __shared__ double smem[];
@@ -176,14 +175,13 @@ k_bottom(TreeParams tp, long long g_first, long long g_count, double* out, long 
                 continue;
             }
             double* Gc = G + (o0 - obase) * L.ldG;
-            const double* px = tp.px + o0;
-            const double* py = tp.py + o0;
-            point_chain(tp, m, t, n, px, py, Gc, L.ldG, cp, smem);
+            const double* pts = tp.pxy + 2 * o0;
+            point_chain(tp, m, t, n, pts, Gc, L.ldG, cp, smem);
             for (int i = threadIdx.x; i < n; i += NT) Gc[(long long)i * L.ldG + Pg] = tp.zs[o0 + i];
             __syncthreads();
             // Sigma_j = C(S,S) + tau2 I - V V^T  (nugget on the observation diagonal only, reading R2)
             cta_gemm<MEMN, MEMN, MEMN, MEMN>(n, n, 1, op_mem(Gc, L.ldG), op_mem(Gc, L.ldG), Pg, op_mem(Gc, L.ldG),
-                                             op_mem(Gc, L.ldG), 0, ci_cov(px, py, px, py, tp.tau2), -1.0, S,
+                                             op_mem(Gc, L.ldG), 0, ci_cov(pts, pts, tp.tau2), -1.0, S,
                                              L.ldS, cp, smem);
             const double ldet = chol_blocked(S, n, L.ldS, D, cp, smem);
             if (*f.bad && threadIdx.x == 0) set_err(tp.err, M, l);
@@ -217,15 +215,16 @@ k_bottom(TreeParams tp, long long g_first, long long g_count, double* out, long 
 }
 
 // --------------------------------------------------------------------------- merge
-__global__ void __launch_bounds__(NT, 2)
+__global__ void __launch_bounds__(NT, MRA_MINB)
 k_merge(TreeParams tp, int m, long long t_first, long long t_count, const double* child_out, long long child_first,
         double* out, long long out_first, int q, double* ws, long long ws_stride, unsigned long long* counter) {
     extern __shared__ double smem[];
     const CovP cp = to_covp(tp.cp);
     const int J = tp.J, rh = tp.rh;
     const int qc = m * rh + 1;
+    const int ldA = qc + (qc & 1);   // even leading dimension -> 16-byte cp.async rows
     double* A = ws + (long long)blockIdx.x * ws_stride;
-    double* F = A + (long long)qc * qc;
+    double* F = A + (long long)qc * ldA;
     double* Li = F + (long long)q * rh;
     FacSmem f = fac_smem(smem);
     const long long qc2 = (long long)qc * qc;
@@ -240,12 +239,12 @@ k_merge(TreeParams tp, int m, long long t_first, long long t_count, const double
             if (j <= i) {
                 double s = 0.0;
                 for (int c = 0; c < J; c++) s += C0[c * qc2 + e];
-                A[e] = s;
+                A[(long long)i * ldA + j] = s;
             }
         }
         __syncthreads();
         double* O = out + (t - out_first) * (long long)q * q;
-        const double ldm = merge_core(A, rh, qc, O, q, F, Li, tp.err, m, t, cp, smem);
+        const double ldm = merge_core(A, rh, ldA, O, q, F, Li, tp.err, m, t, cp, smem);
         const long long id = lvl_first(J, m) + t;
         if (threadIdx.x == 0) {
             const long long c0 = lvl_first(J, m + 1) + t * J;
@@ -313,7 +312,7 @@ __global__ void k_mu(TreeParams tp, int m, double* muhat, double* mu) {
 }
 
 // E[X(S_j)|y] = y_j - tau2 Sigma_j^{-1} (y_j - sum_k V^k muhat_{a_k})   (recomputes V, Sigma_j, L_j)
-__global__ void __launch_bounds__(NT, 2)
+__global__ void __launch_bounds__(NT, MRA_MINB)
 k_smooth(TreeParams tp, const double* muhat, const long long* perm, double* smooth, double* ws, WsLayout L,
          unsigned long long* counter) {
     extern __shared__ double smem[];
@@ -334,11 +333,10 @@ k_smooth(TreeParams tp, const double* muhat, const long long* perm, double* smoo
         const long long o0 = tp.leaf_off[l];
         const int n = (int)(tp.leaf_off[l + 1] - o0);
         if (n == 0) continue;
-        const double* px = tp.px + o0;
-        const double* py = tp.py + o0;
-        point_chain(tp, m, t, n, px, py, G, L.ldG, cp, smem);
+        const double* pts = tp.pxy + 2 * o0;
+        point_chain(tp, m, t, n, pts, G, L.ldG, cp, smem);
         cta_gemm<MEMN, MEMN, MEMN, MEMN>(n, n, 1, op_mem(G, L.ldG), op_mem(G, L.ldG), Pg, op_mem(G, L.ldG),
-                                         op_mem(G, L.ldG), 0, ci_cov(px, py, px, py, tp.tau2), -1.0, S, L.ldS, cp,
+                                         op_mem(G, L.ldG), 0, ci_cov(pts, pts, tp.tau2), -1.0, S, L.ldS, cp,
                                          smem);
         chol_blocked(S, n, L.ldS, D, cp, smem);
         if (*f.bad && threadIdx.x == 0) set_err(tp.err, M, l);
@@ -397,14 +395,27 @@ k_smooth(TreeParams tp, const double* muhat, const long long* perm, double* smoo
 int smem_bytes() { return SMEM_DBL * (int)sizeof(double); }
 
 static bool g_attr_done = false;
+static int g_resident[4] = {1, 1, 1, 1};   // resident CTAs per SM x SM count, per persistent kernel
 static void set_attrs() {
     if (g_attr_done) return;
     const int b = smem_bytes();
-    cudaFuncSetAttribute(k_prior, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-    cudaFuncSetAttribute(k_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-    cudaFuncSetAttribute(k_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-    cudaFuncSetAttribute(k_smooth, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    const void* ks[4] = {(const void*)k_prior, (const void*)k_bottom, (const void*)k_merge, (const void*)k_smooth};
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    for (int i = 0; i < 4; i++) {
+        cudaFuncSetAttribute(ks[i], cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+        int per = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ks[i], NT, b);
+        g_resident[i] = (per > 0 ? per : 1) * nsm;
+    }
     g_attr_done = true;
+}
+// persistent grid: never more CTAs than can be resident at once (they pull work from a queue)
+static int clamp_grid(int grid, long long items, int kidx) {
+    if (grid > g_resident[kidx]) grid = g_resident[kidx];
+    if (items < grid) grid = (int)items;
+    return grid;
 }
 
 cudaError_t launch_gather(const double* z, const long long* perm, double* zs, long long N, cudaStream_t st) {
@@ -424,7 +435,7 @@ cudaError_t launch_fill(double* p, long long n, double v, cudaStream_t st) {
 cudaError_t launch_prior(const TreeParams& tp, int m, long long t_first, long long t_count, int grid, double* ws,
                          long long ws_stride, unsigned long long* counter, cudaStream_t st) {
     set_attrs();
-    if (t_count < grid) grid = (int)t_count;
+    grid = clamp_grid(grid, t_count, 0);
     if (grid < 1) return cudaSuccess;
     k_prior<<<grid, NT, smem_bytes(), st>>>(tp, m, t_first, t_count, ws, ws_stride, counter);
     return cudaGetLastError();
@@ -433,7 +444,7 @@ cudaError_t launch_bottom(const TreeParams& tp, long long g_first, long long g_c
                           int q, int grid, double* ws, const WsLayout& L, unsigned long long* counter,
                           cudaStream_t st) {
     set_attrs();
-    if (g_count < grid) grid = (int)g_count;
+    grid = clamp_grid(grid, g_count, 1);
     if (grid < 1) return cudaSuccess;
     k_bottom<<<grid, NT, smem_bytes(), st>>>(tp, g_first, g_count, out, out_first, q, ws, L, counter);
     return cudaGetLastError();
@@ -442,7 +453,7 @@ cudaError_t launch_merge(const TreeParams& tp, int m, long long t_first, long lo
                          long long child_first, double* out, long long out_first, int q, int grid, double* ws,
                          long long ws_stride, unsigned long long* counter, cudaStream_t st) {
     set_attrs();
-    if (t_count < grid) grid = (int)t_count;
+    grid = clamp_grid(grid, t_count, 2);
     if (grid < 1) return cudaSuccess;
     k_merge<<<grid, NT, smem_bytes(), st>>>(tp, m, t_first, t_count, child_out, child_first, out, out_first, q, ws,
                                            ws_stride, counter);
@@ -462,6 +473,7 @@ cudaError_t launch_mu(const TreeParams& tp, int m, double* muhat, double* mu, cu
 cudaError_t launch_smooth(const TreeParams& tp, const double* muhat, const long long* perm, double* smooth, int grid,
                           double* ws, const WsLayout& L, unsigned long long* counter, cudaStream_t st) {
     set_attrs();
+    grid = clamp_grid(grid, 1LL << 40, 3);
     k_smooth<<<grid, NT, smem_bytes(), st>>>(tp, muhat, perm, smooth, ws, L, counter);
     return cudaGetLastError();
 }

@@ -17,7 +17,10 @@ ap.add_argument("--config", default="C2")
 ap.add_argument("--n", type=int, default=None)
 ap.add_argument("--evals", type=int, default=1)
 ap.add_argument("--M", type=int, default=None)
+ap.add_argument("--lib", default=None)
 a = ap.parse_args()
+if a.lib:
+    mra.load_library(a.lib)
 w = synth.make(a.config, n=a.n, device="cuda")
 M = a.M or w.M
 plan = mra.mra_plan_create(w.x, w.y, M, w.J, w.r, stream=torch.cuda.current_stream())
