@@ -476,6 +476,13 @@ extern "C" mra_status mra_kernel_times(const mra_plan* P, double* ms, uint64_t* 
     return MRA_OK;
 }
 
+// diagnostics of -DMRA_PHASE_TIMING builds (zeros otherwise): CTA-cycles per bottom-kernel phase
+extern "C" void mra_debug_phase_cycles(uint64_t* out16, int reset) {
+    unsigned long long v[16];
+    phase_cycles(v, reset != 0);
+    for (int i = 0; i < 16; i++) out16[i] = v[i];
+}
+
 extern "C" mra_status mra_plan_shards(const mra_plan* P, int* shard_level, int64_t* own, uint64_t* n_own) {
     if (!P) return fail(MRA_E_ARG, "plan is NULL");
     if (shard_level) *shard_level = P->world > 1 ? P->c : 0;

@@ -237,13 +237,27 @@ __device__ __forceinline__ void tile_pipeline(double (&acc)[2][4][2], const Op& 
     cp_async_wait<0>();
 }
 
-// C[Mr x Nc] = init + alpha * (A0 B0^T [K0] + A1 B1^T [K1]); lower != 0 -> only i >= j written.
-// In-place use (C aliasing the operands / init) is safe when every output tile reads only its own
-// rows (A side) / columns (B side) of the aliased region -- see DESIGN.md §5.
+// GEMM call descriptor: written to shared memory by the (inlined) caller, read by the single
+// non-inlined implementation per operand-kind combination (keeps the kernels' SASS small enough
+// to stay instruction-cache resident).
+struct GemmDesc {
+    Op A0, B0, A1, B1;
+    CInit ci;
+    CovP cp;
+    double alpha;
+    double* C;
+    long long ldc;
+    int Mr, Nc, lower, K0, K1;
+};
+constexpr int MISC_DBL = 64;                 // misc smem: reductions, flags, work item, GemmDesc
+__device__ __forceinline__ GemmDesc* gemm_desc(double* smem);
+
 template <int KA0, int KB0, int KA1, int KB1>
-__device__ void cta_gemm(int Mr, int Nc, int lower, const Op& A0, const Op& B0, int K0, const Op& A1,
-                         const Op& B1, int K1, const CInit& ci, double alpha, double* C, long long ldc,
-                         const CovP& cp, double* smem) {
+__device__ __noinline__ void cta_gemm_impl(double* smem) {
+    const GemmDesc& d = *gemm_desc(smem);
+    const Op A0 = d.A0, B0 = d.B0, A1 = d.A1, B1 = d.B1;
+    const int Mr = d.Mr, Nc = d.Nc, lower = d.lower, K0 = d.K0, K1 = d.K1;
+    const CovP cp = d.cp;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
     const int wr = (warp >> 1) * 16, wc = (warp & 1) * 32;
@@ -259,6 +273,10 @@ __device__ void cta_gemm(int Mr, int Nc, int lower, const Op& A0, const Op& B0, 
 #pragma unroll
                 for (int ni = 0; ni < 4; ni++) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
             if (K0 + K1 > 0) tile_pipeline<KA0, KB0, KA1, KB1>(acc, A0, B0, K0, A1, B1, K1, r0, nr, c0, nc, cp, smem);
+            const CInit ci = d.ci;
+            const double alpha = d.alpha;
+            double* C = d.C;
+            const long long ldc = d.ldc;
 #pragma unroll
             for (int mi = 0; mi < 2; mi++)
 #pragma unroll
@@ -267,19 +285,44 @@ __device__ void cta_gemm(int Mr, int Nc, int lower, const Op& A0, const Op& B0, 
                     for (int e = 0; e < 2; e++) {
                         const int i = r0 + wr + mi * 8 + g, j = c0 + wc + ni * 8 + 2 * t + e;
                         if (i < Mr && j < Nc && (!lower || j <= i)) {
-                            double v;
-                            if (ci.kind == 0) v = 0.0;
-                            else if (ci.kind == 1) v = ci.p[(long long)i * ci.ld + j];
-                            else {
-                                const double2 pi = ldpt(ci.p, i), pj = ldpt(ci.q, j);
-                                v = covf(cp, pi.x, pi.y, pj.x, pj.y) + (i == j ? ci.diag : 0.0);
-                            }
+                            const double v = (ci.kind == 1) ? ci.p[(long long)i * ci.ld + j] : 0.0;
                             C[(long long)i * ldc + j] = v + alpha * acc[mi][ni][e];
                         }
                     }
+            if (ci.kind == 2) {
+                // covariance initial value, added by the thread that stored the element (rolled loop:
+                // one copy of the fp64 exp/sqrt sequence instead of sixteen)
+#pragma unroll 1
+                for (int q = 0; q < 16; q++) {
+                    const int mi = q >> 3, ni = (q >> 1) & 3, e = q & 1;
+                    const int i = r0 + wr + mi * 8 + g, j = c0 + wc + ni * 8 + 2 * t + e;
+                    if (i < Mr && j < Nc && (!lower || j <= i)) {
+                        const double2 pi = ldpt(ci.p, i), pj = ldpt(ci.q, j);
+                        C[(long long)i * ldc + j] += covf(cp, pi.x, pi.y, pj.x, pj.y) + (i == j ? ci.diag : 0.0);
+                    }
+                }
+            }
         }
     }
     __syncthreads();
+}
+
+// C[Mr x Nc] = init + alpha * (A0 B0^T [K0] + A1 B1^T [K1]); lower != 0 -> only i >= j written.
+// In-place use (C aliasing the operands / init) is safe when every output tile reads only its own
+// rows (A side) / columns (B side) of the aliased region -- see DESIGN.md §5.
+template <int KA0, int KB0, int KA1, int KB1>
+__device__ __forceinline__ void cta_gemm(int Mr, int Nc, int lower, const Op& A0, const Op& B0, int K0,
+                                         const Op& A1, const Op& B1, int K1, const CInit& ci, double alpha,
+                                         double* C, long long ldc, const CovP& cp, double* smem) {
+    GemmDesc* d = gemm_desc(smem);
+    __syncthreads();   // the previous descriptor is no longer read
+    if (threadIdx.x == 0) {
+        d->A0 = A0; d->B0 = B0; d->A1 = A1; d->B1 = B1;
+        d->ci = ci; d->cp = cp; d->alpha = alpha; d->C = C; d->ldc = ldc;
+        d->Mr = Mr; d->Nc = Nc; d->lower = lower; d->K0 = K0; d->K1 = K1;
+    }
+    __syncthreads();
+    cta_gemm_impl<KA0, KB0, KA1, KB1>(smem);
 }
 
 // ---------------------------------------------------------------- small factor blocks
@@ -290,128 +333,202 @@ __device__ void cta_gemm(int Mr, int Nc, int lower, const Op& A0, const Op& B0, 
 //   then X = L^{-1} is assembled block-row by block-row: X_ij = -X_ii sum_k L_ik X_kj.
 // a: n x n (ld LDB), lower, overwritten by L. x: n x n (ld LDB) receives L^{-1} (upper part 0).
 // tmp: >= 3*256 doubles of smem scratch. Returns log|A| (all threads); *bad set if not PD.
-__device__ __noinline__ double chol_inv_small(double* a, double* x, int n, double* diagv, int* bad, double* red, double* tmp) {
+#ifdef MRA_CHOL_DEBUG
+__device__ long long g_chol_dbg[16];
+#define CHK(k) do { if (threadIdx.x == 0 && blockIdx.x == 0) g_chol_dbg[k] += clock64(); } while (0)
+#else
+#define CHK(k)
+#endif
+__device__ __noinline__ double chol_inv_small(double* a, double* x, int n, double* diagv, int* bad, double* red,
+                                              double* tmp) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    CHK(0);
     const int nbk = (n + 15) >> 4;
     for (int e = tid; e < 64 * 64; e += NT) {
         const int i = e >> 6, j = e & 63;
         if (i < n && j < n) x[i * LDB + j] = 0.0;
     }
-    __syncthreads();
+    CHK(1);
     for (int b = 0; b < nbk; b++) {
         const int j0 = b * 16, nb = min(16, n - j0);
         if (warp == 0) {
+            // 16 x 16 diagonal block: lane i keeps row i in registers (rows >= nb padded with the
+            // identity); the pivot column is broadcast through shared memory (independent LDS, no
+            // shuffle chains).
+            const int i = lane & 15;
             double* d = a + j0 * LDB + j0;
-            for (int j = 0; j < nb; j++) {
-                const double ajj = d[j * LDB + j];
-                const double ljj = sqrt(ajj > 0.0 ? ajj : 1.0);
-                if (lane == 0) {
-                    if (!(ajj > 0.0)) *bad = 1;
-                    diagv[j0 + j] = ljj;
-                }
+            double r[16];
+#pragma unroll
+            for (int k = 0; k < 16; k++)
+                r[k] = (i < nb && k < nb && k <= i) ? d[i * LDB + k] : (i == k ? 1.0 : 0.0);
+            double dv[16];
+            bool ok = true;
+#pragma unroll
+            for (int j = 0; j < 16; j++) {
+                // lane j publishes its (updated) pivot; every lane reads it back
+                if (lane == j) tmp[j] = r[j];
                 __syncwarp();
-                if (lane > j && lane < nb) d[lane * LDB + j] /= ljj;
+                const double piv = tmp[j];
+                ok = ok && (piv > 0.0);
+                // one rsqrt on the serial pivot chain: 1/l_jj, then l_jj = piv / l_jj
+                const double pv = piv > 0.0 ? piv : 1.0;
+                const double il = rsqrt(pv);
+                const double ljj = pv * il;
+                dv[j] = il;
+                r[j] = (i == j) ? ljj : ((i > j) ? r[j] * il : r[j]);
+                if (lane < 16) tmp[16 + i] = r[j];   // column j of L (l_ij for i > j)
                 __syncwarp();
-                const int m = nb - j - 1;
-                for (int e = lane; e < m * m; e += 32) {
-                    const int ii = e / m, kk = e - ii * m;
-                    if (kk <= ii) d[(j + 1 + ii) * LDB + j + 1 + kk] -= d[(j + 1 + ii) * LDB + j] * d[(j + 1 + kk) * LDB + j];
+#pragma unroll
+                for (int k = j + 1; k < 16; k++) {
+                    const double lk = tmp[16 + k];
+                    if (i >= k) r[k] -= r[j] * lk;
                 }
                 __syncwarp();
             }
-            if (lane < nb) d[lane * LDB + lane] = diagv[j0 + lane];
+            if (!ok && lane == 0) *bad = 1;
+            // publish L_bb rows to smem (lower part) for the inverse and the panel
+            if (lane < nb) {
+#pragma unroll
+                for (int k = 0; k < 16; k++)
+                    if (k <= i && k < nb) d[i * LDB + k] = r[k];
+            }
             __syncwarp();
-            // inverse of the diagonal block, one column per lane
+            // column `lane` of X_bb = L_bb^{-1}: x_i = (delta_ic - sum_{k<i} L_ik x_k) / L_ii
+            const int c = lane & 15;
+            double xc[16];
+#pragma unroll
+            for (int ii = 0; ii < 16; ii++) {
+                double s0 = (ii == c) ? 1.0 : 0.0, s1 = 0.0;
+                if (ii < nb) {
+#pragma unroll
+                    for (int k = 0; k + 1 < ii; k += 2) {
+                        s0 -= d[ii * LDB + k] * xc[k];
+                        s1 -= d[ii * LDB + k + 1] * xc[k + 1];
+                    }
+                    if (ii & 1) s0 -= d[ii * LDB + ii - 1] * xc[ii - 1];
+                }
+                xc[ii] = (s0 + s1) * dv[ii];
+            }
             double* xd = x + j0 * LDB + j0;
             if (lane < nb) {
-                const int c = lane;
-                xd[c * LDB + c] = 1.0 / d[c * LDB + c];
-                for (int i = c + 1; i < nb; i++) {
-                    double sacc = 0.0;
-                    for (int k = c; k < i; k++) sacc += d[i * LDB + k] * xd[k * LDB + c];
-                    xd[i * LDB + c] = -sacc / d[i * LDB + i];
-                }
+#pragma unroll
+                for (int k = 0; k < 16; k++)
+                    if (k < nb) xd[k * LDB + c] = xc[k];
             }
         }
+        CHK(2);
         __syncthreads();
+        CHK(3);
         const int r0 = j0 + nb, nr = n - r0;
         if (nr > 0) {
-            // panel: L_ib = A_ib X_bb^T  (rows r0..n-1, cols j0..j0+nb-1)
-            const double* xd = x + j0 * LDB + j0;
-            double v[3];   // nr * nb <= 48 * 16 = 3 * NT
+            // panel: L_ib = A_ib X_bb^T for rows r0..n-1 (<= 48), cols j0..j0+nb-1; thread = (row group, col)
+            const int jj = tid & 15, rg = tid >> 4;
+            const double* xr = x + (j0 + jj) * LDB + j0;
+            double v[3];
 #pragma unroll
-            for (int c = 0; c < 3; c++) {
-                const int e = tid + c * NT;
-                double sacc = 0.0;
-                if (e < nr * nb) {
-                    const int i = r0 + e / nb, jj = e % nb;
-                    for (int kk = 0; kk <= jj; kk++) sacc += a[i * LDB + j0 + kk] * xd[jj * LDB + kk];
+            for (int q = 0; q < 3; q++) {
+                const int row = r0 + rg + 16 * q;
+                double s0 = 0.0, s1 = 0.0;
+                if (row < n && jj < nb) {
+                    const double* ar = a + row * LDB + j0;
+#pragma unroll
+                    for (int kk = 0; kk < 16; kk += 2) {   // X_bb upper part is 0
+                        s0 += ar[kk] * xr[kk];
+                        s1 += ar[kk + 1] * xr[kk + 1];
+                    }
                 }
-                v[c] = sacc;
+                v[q] = s0 + s1;
             }
             __syncthreads();
 #pragma unroll
-            for (int c = 0; c < 3; c++) {
-                const int e = tid + c * NT;
-                if (e < nr * nb) a[(r0 + e / nb) * LDB + j0 + e % nb] = v[c];
+            for (int q = 0; q < 3; q++) {
+                const int row = r0 + rg + 16 * q;
+                if (row < n && jj < nb) a[row * LDB + j0 + jj] = v[q];
             }
             __syncthreads();
-            // trailing update of the lower part
-            for (int e = tid; e < nr * nr; e += NT) {
-                const int ii = e / nr, kk = e - ii * nr;
-                if (kk <= ii) {
-                    const double* li = a + (r0 + ii) * LDB + j0;
-                    const double* lk = a + (r0 + kk) * LDB + j0;
-                    double sacc = 0.0;
-#pragma unroll 4
-                    for (int q = 0; q < nb; q++) sacc += li[q] * lk[q];
-                    a[(r0 + ii) * LDB + r0 + kk] -= sacc;
+            // trailing update A_rc -= sum_k L_rk L_ck (lower part), thread = (row offset, col offset) 16 x 16
+            const int tx = tid & 15, ty = tid >> 4;
+#pragma unroll
+            for (int qi = 0; qi < 3; qi++) {
+                const int row = r0 + ty + 16 * qi;
+                if (row >= n) continue;
+                const double* lr = a + row * LDB + j0;
+                double lrv[16];
+#pragma unroll
+                for (int kk = 0; kk < 16; kk++) lrv[kk] = kk < nb ? lr[kk] : 0.0;
+#pragma unroll
+                for (int qj = 0; qj < 3; qj++) {
+                    const int col = r0 + tx + 16 * qj;
+                    if (col > row) continue;
+                    const double* lc = a + col * LDB + j0;
+                    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+                    for (int kk = 0; kk < 16; kk += 2) {
+                        s0 += lrv[kk] * (kk < nb ? lc[kk] : 0.0);
+                        s1 += lrv[kk + 1] * (kk + 1 < nb ? lc[kk + 1] : 0.0);
+                    }
+                    a[row * LDB + col] -= s0 + s1;
                 }
             }
             __syncthreads();
         }
     }
-    // off-diagonal blocks of X = L^{-1}, block row by block row
+    // off-diagonal blocks of X = L^{-1}, block row by block row: X_ij = -X_ii sum_{k=j}^{i-1} L_ik X_kj
     for (int bi = 1; bi < nbk; bi++) {
         const int i0 = bi * 16, ni = min(16, n - i0);
-        // tmp[bj] (ni x 16) = sum_{k=j0}^{i0-1} L[i0+r][k] X[k][j0+c]
         for (int e = tid; e < bi * 256; e += NT) {
-            const int bj = e >> 8, r = (e >> 4) & 15, c = e & 15;
-            double sacc = 0.0;
-            if (r < ni)
-                for (int k = bj * 16 + c; k < i0; k++) sacc += a[(i0 + r) * LDB + k] * x[k * LDB + bj * 16 + c];
-            tmp[e] = sacc;
+            const int bj = e >> 8, rr = (e >> 4) & 15, c = e & 15;
+            double s0 = 0.0, s1 = 0.0;
+            if (rr < ni) {
+                const double* lr = a + (i0 + rr) * LDB;
+                const double* xcol = x + bj * 16 + c;
+                int k = bj * 16 + c;
+                for (; k + 1 < i0; k += 2) {
+                    s0 += lr[k] * xcol[k * LDB];
+                    s1 += lr[k + 1] * xcol[(k + 1) * LDB];
+                }
+                if (k < i0) s0 += lr[k] * xcol[k * LDB];
+            }
+            tmp[e] = s0 + s1;
         }
         __syncthreads();
         for (int e = tid; e < bi * 256; e += NT) {
-            const int bj = e >> 8, r = (e >> 4) & 15, c = e & 15;
-            if (r < ni) {
+            const int bj = e >> 8, rr = (e >> 4) & 15, c = e & 15;
+            if (rr < ni) {
+                const double* xr = x + (i0 + rr) * LDB + i0;
                 double sacc = 0.0;
-                for (int k = 0; k <= r; k++) sacc += x[(i0 + r) * LDB + i0 + k] * tmp[(bj << 8) + (k << 4) + c];
-                x[(i0 + r) * LDB + bj * 16 + c] = -sacc;
+                for (int k = 0; k <= rr; k++) sacc += xr[k] * tmp[(bj << 8) + (k << 4) + c];
+                x[(i0 + rr) * LDB + bj * 16 + c] = -sacc;
             }
         }
         __syncthreads();
     }
+    CHK(4);
+    // log-determinant: the n diagonal logs in parallel (warp 0), then a shuffle reduction
     if (tid < 32) {
-        double sacc = 0.0;
-        for (int j = tid; j < n; j += 32) sacc += log(diagv[j]);
+        double sl = 0.0;
+        for (int j = tid; j < n; j += 32) sl += log(a[j * LDB + j]);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
-        if (tid == 0) *red = 2.0 * sacc;
+        for (int o = 16; o > 0; o >>= 1) sl += __shfl_xor_sync(0xffffffffu, sl, o);
+        if (tid == 0) *red = 2.0 * sl;
     }
     __syncthreads();
+    CHK(5);
     const double ld = *red;
     __syncthreads();
     return ld;
 }
 
-// smem layout (doubles): [ main: GEMM tiles | factor blocks ] [ misc: 32 doubles ]
+// smem layout (doubles): [ main: GEMM tiles | factor blocks ] [ misc: MISC_DBL doubles ]
 //   factor view of main: blk[64*LDB] | inv[64*LDB] | diag[64]
-//   misc: red[0..15] (reductions) | bad flag (int) at misc+16 | work item at misc+18
+//   misc: red[0..15] (reductions) | bad flag (int) at misc+16 | work item at misc+18 | GemmDesc at misc+24
 constexpr int FAC_DBL = 2 * 64 * LDB + 64 + 768;
 constexpr int MAIN_DBL = (FAC_DBL > NSTAGE * STAGE_DBL) ? FAC_DBL : NSTAGE * STAGE_DBL;
-constexpr int SMEM_DBL = MAIN_DBL + 32;
+constexpr int SMEM_DBL = MAIN_DBL + MISC_DBL;
+__device__ __forceinline__ GemmDesc* gemm_desc(double* smem) {
+    return reinterpret_cast<GemmDesc*>(smem + MAIN_DBL + 24);
+}
+static_assert(sizeof(GemmDesc) <= (MISC_DBL - 24) * sizeof(double), "GemmDesc must fit the misc smem");
 struct FacSmem {
     double* blk;
     double* inv;
@@ -457,13 +574,30 @@ __device__ __forceinline__ void store_block_full(const double* x, double* A, lon
 
 // Blocked right-looking Cholesky of S (n x n, lower, ld) in place; Dinv receives the inverted
 // 64x64 diagonal blocks (block b at Dinv + b*4096, ld 64). Returns log|S| (all threads).
+// optional phase timing (build with -DMRA_PHASE_TIMING): CTA-cycles per phase of the bottom kernel
+__device__ unsigned long long g_phase_cycles[16];
+#ifdef MRA_PHASE_TIMING
+#define CPHASE_MARK(var) long long var = clock64()
+#define CPHASE_ADD(idx, from) do { if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[idx], (unsigned long long)(clock64() - (from))); } while (0)
+#else
+#define CPHASE_MARK(var)
+#define CPHASE_ADD(idx, from)
+#endif
 __device__ double chol_blocked(double* S, int n, long long ld, double* Dinv, const CovP& cp, double* smem) {
     FacSmem f = fac_smem(smem);
     double total = 0.0;
     for (int j0 = 0; j0 < n; j0 += 64) {
         const int nb = min(64, n - j0);
+        CPHASE_MARK(q0);
         load_block_lower(f.blk, S + (long long)j0 * ld + j0, ld, nb, 0.0);
+        CPHASE_ADD(9, q0);
+        CPHASE_MARK(q3);
         total += chol_inv_small(f.blk, f.inv, nb, f.diagv, f.bad, f.red, f.tmp);
+        CPHASE_ADD(10, q3);
+        CPHASE_ADD(6, q0);
+#ifdef MRA_PHASE_TIMING
+        if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[11], 1ULL);
+#endif
         double* Di = Dinv + (long long)(j0 / 64) * 4096;
         store_block_lower(f.blk, S + (long long)j0 * ld + j0, ld, nb);
         store_block_full(f.inv, Di, 64, nb);
@@ -471,13 +605,17 @@ __device__ double chol_blocked(double* S, int n, long long ld, double* Dinv, con
         const int r = n - j0 - nb;
         if (r > 0) {
             double* P = S + (long long)(j0 + nb) * ld + j0;
+            CPHASE_MARK(q1);
             // panel: L_ij = A_ij L_jj^{-T}  (in place, single column tile)
             cta_gemm<MEMN, MEMN, MEMN, MEMN>(r, nb, 0, op_mem(P, ld), op_mem(Di, 64), nb, op_mem(P, ld),
                                              op_mem(P, ld), 0, ci_zero(), 1.0, P, ld, cp, smem);
+            CPHASE_ADD(7, q1);
+            CPHASE_MARK(q2);
             // trailing: A_ik -= L_ij L_kj^T (lower tiles, in place)
             double* T = S + (long long)(j0 + nb) * ld + j0 + nb;
             cta_gemm<MEMN, MEMN, MEMN, MEMN>(r, r, 1, op_mem(P, ld), op_mem(P, ld), nb, op_mem(P, ld),
                                              op_mem(P, ld), 0, ci_mem(T, ld), -1.0, T, ld, cp, smem);
+            CPHASE_ADD(8, q2);
         }
     }
     return total;

@@ -59,5 +59,6 @@ cudaError_t launch_smooth(const TreeParams& tp, const double* muhat, const long 
                           cudaStream_t st);
 cudaError_t launch_fill(double* p, long long n, double v, cudaStream_t st);
 int smem_bytes();
+void phase_cycles(unsigned long long* out16, bool reset);   // -DMRA_PHASE_TIMING builds only
 
 }  // namespace mra

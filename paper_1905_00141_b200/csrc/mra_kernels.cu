@@ -27,6 +27,17 @@
 
 namespace mra {
 
+#ifdef MRA_PHASE_TIMING
+#define PHASE_MARK(var) long long var = clock64()
+#define PHASE_ADD(idx, from)                                                                  \
+    do {                                                                                      \
+        if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[idx], (unsigned long long)(clock64() - (from))); \
+    } while (0)
+#else
+#define PHASE_MARK(var)
+#define PHASE_ADD(idx, from)
+#endif
+
 __device__ __forceinline__ long long lvl_first(int J, int m) {
     long long p = 1;
     for (int i = 1; i < m; i++) p *= J;
@@ -157,6 +168,7 @@ k_bottom(TreeParams tp, long long g_first, long long g_count, double* out, long 
     FacSmem f = fac_smem(smem);
     double* red = misc_smem(smem);
     const long long leaf_id0 = lvl_first(J, M);
+    PHASE_MARK(kstart);
     for (;;) {
         const long long it = next_item(counter, smem);
         if (it >= g_count) break;
@@ -176,16 +188,24 @@ k_bottom(TreeParams tp, long long g_first, long long g_count, double* out, long 
             }
             double* Gc = G + (o0 - obase) * L.ldG;
             const double* pts = tp.pxy + 2 * o0;
+            PHASE_MARK(c0);
             point_chain(tp, m, t, n, pts, Gc, L.ldG, cp, smem);
             for (int i = threadIdx.x; i < n; i += NT) Gc[(long long)i * L.ldG + Pg] = tp.zs[o0 + i];
             __syncthreads();
+            PHASE_ADD(0, c0);
+            PHASE_MARK(c1);
             // Sigma_j = C(S,S) + tau2 I - V V^T  (nugget on the observation diagonal only, reading R2)
             cta_gemm<MEMN, MEMN, MEMN, MEMN>(n, n, 1, op_mem(Gc, L.ldG), op_mem(Gc, L.ldG), Pg, op_mem(Gc, L.ldG),
                                              op_mem(Gc, L.ldG), 0, ci_cov(pts, pts, tp.tau2), -1.0, S,
                                              L.ldS, cp, smem);
+            PHASE_ADD(1, c1);
+            PHASE_MARK(c2);
             const double ldet = chol_blocked(S, n, L.ldS, D, cp, smem);
             if (*f.bad && threadIdx.x == 0) set_err(tp.err, M, l);
+            PHASE_ADD(2, c2);
+            PHASE_MARK(c3);
             fwd_subst(S, n, L.ldS, D, Gc, ncol, L.ldG, cp, smem);
+            PHASE_ADD(3, c3);
             double u = 0.0;
             for (int i = threadIdx.x; i < n; i += NT) {
                 const double g = Gc[(long long)i * L.ldG + Pg];
@@ -201,10 +221,14 @@ k_bottom(TreeParams tp, long long g_first, long long g_count, double* out, long 
             continue;
         }
         // Atilde_p = sum_c G_c^T G_c = G_stack^T G_stack (lower)
+        PHASE_MARK(c4);
         cta_gemm<MEMT, MEMT, MEMN, MEMN>(ncol, ncol, 1, op_mem(G, L.ldG), op_mem(G, L.ldG), (int)ng, op_mem(G, 0),
                                          op_mem(G, 0), 0, ci_zero(), 1.0, A, L.ldA, cp, smem);
+        PHASE_ADD(4, c4);
+        PHASE_MARK(c5);
         double* O = out + (t - out_first) * (long long)q * q;
         const double ldm = merge_core(A, rh, L.ldA, O, q, F, Li, tp.err, m, t, cp, smem);
+        PHASE_ADD(5, c5);
         const long long id = lvl_first(J, m) + t;
         if (threadIdx.x == 0) {
             tp.dreg[id] = dsum + ldm;
@@ -212,6 +236,7 @@ k_bottom(TreeParams tp, long long g_first, long long g_count, double* out, long 
         }
         save_post(tp, m, t, q, Li, F);
     }
+    PHASE_ADD(12, kstart);
 }
 
 // --------------------------------------------------------------------------- merge
@@ -393,6 +418,14 @@ k_smooth(TreeParams tp, const double* muhat, const long long* perm, double* smoo
 
 // ------------------------------------------------------------------------ launchers
 int smem_bytes() { return SMEM_DBL * (int)sizeof(double); }
+
+void phase_cycles(unsigned long long* out16, bool reset) {
+    cudaMemcpyFromSymbol(out16, g_phase_cycles, sizeof(unsigned long long) * 16);
+    if (reset) {
+        unsigned long long z[16] = {0};
+        cudaMemcpyToSymbol(g_phase_cycles, z, sizeof z);
+    }
+}
 
 static bool g_attr_done = false;
 static int g_resident[4] = {1, 1, 1, 1};   // resident CTAs per SM x SM count, per persistent kernel

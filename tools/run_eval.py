@@ -30,3 +30,14 @@ for i in range(a.evals):
     ll = mra.mra_loglik_dev(plan, zd, w.thetas[0])["loglik"]
     torch.cuda.synchronize()
     print(f"eval {i}: loglik={ll:.10f} {1e3 * (time.time() - t):.1f} ms launches={mra.mra_last_launches(plan)}")
+import ctypes  # noqa: E402
+cyc = (ctypes.c_uint64 * 16)()
+mra._lib.mra_debug_phase_cycles(cyc, 1)
+tot = sum(cyc[:6])
+if tot:
+    names = ["chain", "sigma", "chol", "fwd", "syrk", "merge"]
+    print("bottom phases (CTA-cycles share):", ", ".join(f"{n} {100 * cyc[i] / tot:.1f}%" for i, n in enumerate(names)))
+    print("  chol split: small-factor+inverse {:.1f}%, panel {:.1f}%, trailing {:.1f}%".format(
+        *(100 * cyc[i] / tot for i in (6, 7, 8))))
+    print(f"  chol_inv_small calls={cyc[11]} cycles/call={cyc[10] / max(1, cyc[11]):.0f} load_block cycles/call={cyc[9] / max(1, cyc[11]):.0f}; "
+          f"bottom kernel CTA-cycles={cyc[12]:.3g} phase sum={tot:.3g}")
