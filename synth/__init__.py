@@ -115,9 +115,11 @@ def _dense_gp_sample(x, y, sigma2, rho, tau2, rng):
 
 
 def _strips(n: int, nstrips: int, width: float, rng: np.random.Generator):
-    """C4 swaths: `nstrips` parallel strips of `width` at one common random
-    angle, offsets uniform over the projection range of the unit square, n/nstrips points
-    uniform within strip ∩ [0,1]^2 (rejection sampling in strip coordinates)."""
+    """C4 swaths (refined in DESIGN.md reading R11): `nstrips` parallel strips of
+    `width` at one common random angle, offsets uniform over the projection range of the unit
+    square. Points are uniform over the union of the strips clipped to [0,1]^2 (constant density
+    along every swath, as in satellite swath data), so a strip gets a share of the n points
+    proportional to its clipped area. Sampled by rejection in strip coordinates."""
     theta = math.pi * rng.random()
     t = np.array([math.cos(theta), math.sin(theta)])        # along-strip direction
     nrm = np.array([-t[1], t[0]])                           # across-strip normal
@@ -126,18 +128,26 @@ def _strips(n: int, nstrips: int, width: float, rng: np.random.Generator):
     pt = corners @ t
     lo_n, hi_n = pn.min() + width / 2, pn.max() - width / 2
     offs = lo_n + (hi_n - lo_n) * rng.random(nstrips)
-    per = [n // nstrips + (1 if i < n % nstrips else 0) for i in range(nstrips)]
+    tlo, thi = pt.min(), pt.max()
+
+    def sample(o, m):
+        u = tlo + (thi - tlo) * rng.random(m)
+        v = o - width / 2 + width * rng.random(m)
+        px = u * t[0] + v * nrm[0]
+        py = u * t[1] + v * nrm[1]
+        ok = (px >= 0) & (px < 1) & (py >= 0) & (py < 1)
+        return px[ok], py[ok], ok.mean()
+
+    # clipped area of each strip (Monte Carlo acceptance rate x bounding-rectangle area)
+    area = np.array([sample(o, 20000)[2] for o in offs]) * (thi - tlo) * width
+    share = area / area.sum()
+    per = np.floor(share * n).astype(np.int64)
+    per[: n - per.sum()] += 1
     xs, ys = [], []
     for o, cnt in zip(offs, per):
         got_x, got_y, have = [], [], 0
         while have < cnt:
-            m = max(4 * (cnt - have), 1024)
-            u = pt.min() + (pt.max() - pt.min()) * rng.random(m)
-            v = o - width / 2 + width * rng.random(m)
-            px = u * t[0] + v * nrm[0]
-            py = u * t[1] + v * nrm[1]
-            ok = (px >= 0) & (px < 1) & (py >= 0) & (py < 1)
-            px, py = px[ok], py[ok]
+            px, py, _ = sample(o, max(4 * (cnt - have), 1024))
             take = min(cnt - have, px.shape[0])
             got_x.append(px[:take]); got_y.append(py[:take]); have += take
         xs.append(np.concatenate(got_x)); ys.append(np.concatenate(got_y))
@@ -163,7 +173,7 @@ def make(name: str, n: int | None = None, seed: int | None = None, device=None) 
         recipe = f"jittered {side}x{side} grid on [0,360]x[-90,90] (SURVEY.md L22)"
     elif name == "C4":
         x, y = _strips(n, spec["strips"], spec["width"], rng)
-        recipe = f"{spec['strips']} strips width {spec['width']} (SURVEY.md L21)"
+        recipe = f"{spec['strips']} strips width {spec['width']}, uniform density over the swaths (DESIGN.md R11)"
     else:
         x = x0 + (x1 - x0) * rng.random(n)
         y = y0 + (y1 - y0) * rng.random(n)
