@@ -46,7 +46,12 @@ def _load():
         lib.oracle_run.argtypes = [D, D, D, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                    ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int,
                                    ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int,
-                                   ctypes.c_int64, D, D, D, D, D, D, D, D, I64, ctypes.c_int]
+                                   ctypes.c_int64, D, D, D, D, D, D, D, D, I64, ctypes.c_int, D, D]
+        lib.oracle_finish.restype = ctypes.c_int
+        lib.oracle_finish.argtypes = [D, D, D, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                      ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int,
+                                      ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int,
+                                      D, D, D, D, D]
         lib.oracle_plan.restype = ctypes.c_int
         lib.oracle_plan.argtypes = [D, D, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                     ctypes.c_double, ctypes.POINTER(ctypes.c_int), I64, I64, D, D, D]
@@ -93,7 +98,7 @@ def plan(x, y, M, J, r, offset=E_OVER_100):
 
 
 def run(x, y, z, M, J, r, theta, offset=E_OVER_100, xscale=1.0, yscale=1.0, target=None,
-        regions=False, posterior=False, nthreads=0):
+        regions=False, posterior=False, nthreads=0, outputs=False):
     """Run the recursion. theta = (cov, sigma2, rho, tau2). target = (level, index) evaluates
     one subtree only (its d, u). Returns a dict with loglik, d, u, n_retained and optional
     per-region d/u, mu, xq (E[X(q)|y] at knots) and smooth (E[X(s_i)|y])."""
@@ -115,17 +120,44 @@ def run(x, y, z, M, J, r, theta, offset=E_OVER_100, xscale=1.0, yscale=1.0, targ
     xq = np.empty(max(1, nint * rh)) if posterior else None
     sm = np.empty(n) if posterior else None
     tl, tt = (0, 0) if target is None else target
+    P = (max(tl, 1) - 1) * rh
+    oA = np.empty(max(1, P * P)) if outputs else None
+    ow = np.empty(max(1, P)) if outputs else None
     rc = lib.oracle_run(_p(x), _p(y), _p(z), n, M, J, r, offset, xscale, yscale, int(cov), float(s2),
                         float(rho), float(t2), int(tl), int(tt), ctypes.byref(ll), ctypes.byref(d),
                         ctypes.byref(u), _p(rd), _p(ru), _p(mu), _p(xq), _p(sm), ctypes.byref(nret),
-                        int(nthreads))
+                        int(nthreads), _p(oA), _p(ow))
     if rc != 0:
         raise OracleError(f"oracle_run failed: {rc}")
     out = dict(loglik=ll.value, d=d.value, u=u.value, n_retained=nret.value, r_hat=rh)
     if regions:
         out["region_d"], out["region_u"] = rd, ru
+    if outputs:
+        out["A"] = oA[: P * P].reshape(P, P)
+        out["omega"] = ow[:P]
     if posterior:
         out["mu"] = mu[: nint * rh].reshape(nint, rh)
         out["xq"] = xq[: nint * rh].reshape(nint, rh)
         out["smooth"] = sm
     return out
+
+
+def finish(x, y, z, M, J, r, theta, s, A, omega, d, u, offset=E_OVER_100, xscale=1.0, yscale=1.0):
+    """log L merged from the given outputs of every level-s region (A [J^(s-1), P, P], omega
+    [J^(s-1), P], d, u [J^(s-1)]) -- the rank-0 half of the subtree-sharding exchange step."""
+    lib = _load()
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    z = np.ascontiguousarray(z, dtype=np.float64)
+    cov, s2, rho, t2 = theta
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    omega = np.ascontiguousarray(omega, dtype=np.float64)
+    d = np.ascontiguousarray(d, dtype=np.float64)
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    ll = ctypes.c_double()
+    rc = lib.oracle_finish(_p(x), _p(y), _p(z), x.shape[0], M, J, r, offset, xscale, yscale, int(cov),
+                           float(s2), float(rho), float(t2), int(s), _p(A), _p(omega), _p(d), _p(u),
+                           ctypes.byref(ll))
+    if rc != 0:
+        raise OracleError(f"oracle_finish failed: {rc}")
+    return ll.value

@@ -472,11 +472,13 @@ int oracle_plan(const double *x, const double *y, int64_t n, int M, int J, int r
    E[eta_R | y] in the paper's parametrization, xq [nint*rh] = E[X(q)|y]
    at every pre-finest knot, smooth [n] = E[X(s_i)|y] at the observations (NaN for
    eliminated). */
-int oracle_run(const double *x, const double *y, const double *z, int64_t n, int M, int J, int r,
-               double offset, double xscale, double yscale, int cov, double sigma2, double rho,
-               double tau2, int target_level, int64_t target_t, double *loglik, double *out_d,
-               double *out_u, double *region_d, double *region_u, double *mu, double *xq,
-               double *smooth, int64_t *n_retained, int nthreads) {
+static int run_impl(const double *x, const double *y, const double *z, int64_t n, int M, int J, int r,
+                    double offset, double xscale, double yscale, int cov, double sigma2, double rho,
+                    double tau2, int target_level, int64_t target_t, double *loglik, double *out_d,
+                    double *out_u, double *region_d, double *region_u, double *mu, double *xq,
+                    double *smooth, int64_t *n_retained, int nthreads, double *out_A, double *out_w,
+                    int given_level, const double *gA, const double *gw, const double *gd,
+                    const double *gu) {
     if (M < 1 || (J != 2 && J != 4) || r < 1 || n < 1) return -1;
     if (!(sigma2 > 0) || !(rho > 0) || !(tau2 > 0)) return -1;
 #ifdef _OPENMP
@@ -516,7 +518,26 @@ int oracle_run(const double *x, const double *y, const double *z, int64_t n, int
     int rh = o.rh;
     int fan = tl;
     while (fan < M && (ipow(J, fan - tl)) < 64) fan++;
-    if (fan > tl) {
+    if (given_level > 0) {
+        /* finish from given level-s outputs (the exchange step of subtree sharding):
+           the level-s regions' (A, omega, d, u) are supplied, the levels above are merged here */
+        fan = given_level;
+        o.fan = fan;
+        int64_t cnt = ipow(J, fan - 1);
+        int P = (fan - 1) * rh;
+        o.cA = calloc(cnt, sizeof(double *));
+        o.cw = calloc(cnt, sizeof(double *));
+        o.cd = calloc(cnt, sizeof(double));
+        o.cu = calloc(cnt, sizeof(double));
+        for (int64_t t = 0; t < cnt; t++) {
+            o.cA[t] = malloc(sizeof(double) * ((int64_t)P * P + 1));
+            o.cw[t] = malloc(sizeof(double) * (P + 1));
+            memcpy(o.cA[t], gA + t * (int64_t)P * P, sizeof(double) * P * P);
+            memcpy(o.cw[t], gw + t * (int64_t)P, sizeof(double) * P);
+            o.cd[t] = gd[t];
+            o.cu[t] = gu[t];
+        }
+    } else if (fan > tl) {
         o.fan = fan;
         int64_t cnt = ipow(J, fan - 1);
         o.cA = calloc(cnt, sizeof(double *));
@@ -543,6 +564,8 @@ int oracle_run(const double *x, const double *y, const double *z, int64_t n, int
         double *A = malloc(sizeof(double) * ((int64_t)P * P + 1)), *w = malloc(sizeof(double) * (P + 1));
         double d, u;
         rc = post_region(&o, tl, tt, A, w, &d, &u);
+        if (!rc && out_A) memcpy(out_A, A, sizeof(double) * P * P);
+        if (!rc && out_w) memcpy(out_w, w, sizeof(double) * P);
         free(A); free(w);
         if (rc) { free_all(&o); return rc; }
         if (out_d) *out_d = d;
@@ -620,6 +643,28 @@ int oracle_run(const double *x, const double *y, const double *z, int64_t n, int
     }
     free_all(&o);
     return bad ? -4 : 0;
+}
+
+int oracle_run(const double *x, const double *y, const double *z, int64_t n, int M, int J, int r,
+               double offset, double xscale, double yscale, int cov, double sigma2, double rho,
+               double tau2, int target_level, int64_t target_t, double *loglik, double *out_d,
+               double *out_u, double *region_d, double *region_u, double *mu, double *xq,
+               double *smooth, int64_t *n_retained, int nthreads, double *out_A, double *out_w) {
+    return run_impl(x, y, z, n, M, J, r, offset, xscale, yscale, cov, sigma2, rho, tau2, target_level,
+                    target_t, loglik, out_d, out_u, region_d, region_u, mu, xq, smooth, n_retained,
+                    nthreads, out_A, out_w, 0, NULL, NULL, NULL, NULL);
+}
+
+/* log L from the outputs (A, omega, d, u) of every level-s region (s >= 2), merging levels
+   s-1..1 with the recursion above (the rank-0 side of the exchange step). gA: [J^{s-1}][P][P],
+   gw: [J^{s-1}][P], gd/gu: [J^{s-1}], P = (s-1) r_hat. */
+int oracle_finish(const double *x, const double *y, const double *z, int64_t n, int M, int J, int r,
+                  double offset, double xscale, double yscale, int cov, double sigma2, double rho,
+                  double tau2, int s, const double *gA, const double *gw, const double *gd,
+                  const double *gu, double *loglik) {
+    if (s < 2 || s > M) return -1;
+    return run_impl(x, y, z, n, M, J, r, offset, xscale, yscale, cov, sigma2, rho, tau2, 0, 0, loglik,
+                    NULL, NULL, NULL, NULL, NULL, NULL, NULL, NULL, 0, NULL, NULL, s, gA, gw, gd, gu);
 }
 
 int oracle_threads(void) {

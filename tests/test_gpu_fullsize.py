@@ -1,0 +1,85 @@
+"""Full-size parity (BASELINE.json configs at their real sizes, the launch configuration bench.py
+times): the GPU evaluates the whole tree once; for a few randomly chosen subtrees the oracle
+evaluates the same subtree on exactly its observations (plus the 4 bounding-box extremes, so the
+oracle builds the identical tree) and every region's log-det term d_R and quadratic term u_R in
+the subtree must agree (1e-8 relative to max(1, |ref|); these are the basis-invariant quantities
+DESIGN.md §2 shows the whitened GPU path and the W/K oracle share)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mra():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_1905_00141_b200 import build
+    build.build()
+    import paper_1905_00141_b200 as m
+    m.load_library()
+    return m
+
+
+def _box(x, y, J, level, t):
+    x0, x1, y0, y1 = x.min(), x.max(), y.min(), y.max()
+    b = [x0, x1 + 0.01 * (x1 - x0), y0, y1 + 0.01 * (y1 - y0)]
+    path = []
+    for _ in range(level - 1):
+        path.append(t % J)
+        t //= J
+    for c in reversed(path):
+        mx, my = 0.5 * (b[0] + b[1]), 0.5 * (b[2] + b[3])
+        if J == 4:
+            b = [mx, b[1], b[2], b[3]] if c & 1 else [b[0], mx, b[2], b[3]]
+            b = [b[0], b[1], my, b[3]] if c & 2 else [b[0], b[1], b[2], my]
+        elif (b[1] - b[0]) >= (b[3] - b[2]):
+            b = [mx, b[1], b[2], b[3]] if c else [b[0], mx, b[2], b[3]]
+        else:
+            b = [b[0], b[1], my, b[3]] if c else [b[0], b[1], b[2], my]
+    return b
+
+
+def _sampled(mra, name, level, nsub, seed, theta_idx=0):
+    import torch
+    w = synth.make(name, device="cuda")
+    theta = w.thetas[theta_idx]
+    p = mra.mra_plan_create(w.x, w.y, w.M, w.J, w.r, stream=torch.cuda.current_stream())
+    zd = torch.from_numpy(w.z).cuda()
+    got = mra.mra_loglik_dev(p, zd, theta, regions=True)
+    assert np.isfinite(got["loglik"])
+    rng = np.random.default_rng(seed)
+    ext = np.unique([np.argmin(w.x), np.argmax(w.x), np.argmin(w.y), np.argmax(w.y)])
+    checked = 0
+    for t in rng.choice(w.J ** (level - 1), size=nsub, replace=False):
+        b = _box(w.x, w.y, w.J, level, int(t))
+        sel = np.nonzero((w.x >= b[0]) & (w.x < b[1]) & (w.y >= b[2]) & (w.y < b[3]))[0]
+        idx = np.union1d(sel, ext)
+        ref = oracle.run(w.x[idx], w.y[idx], w.z[idx], w.M, w.J, w.r, theta, target=(level, int(t)),
+                         regions=True)
+        ok = ~np.isnan(ref["region_d"])
+        assert ok.sum() >= (w.J ** (w.M - level + 1) - 1) // (w.J - 1)
+        gd, gu = got["region_d"][ok], got["region_u"][ok]
+        rd, ru = ref["region_d"][ok], ref["region_u"][ok]
+        assert np.all(np.abs(gd - rd) <= 1e-8 * np.maximum(1, np.abs(rd))), np.max(np.abs(gd - rd))
+        assert np.all(np.abs(gu - ru) <= 1e-8 * np.maximum(1, np.abs(ru))), np.max(np.abs(gu - ru))
+        checked += int(ok.sum())
+    return checked
+
+
+def test_C2_full_sampled(mra):
+    assert _sampled(mra, "C2", level=5, nsub=3, seed=1) > 3 * 80
+
+
+def test_C3_full_47M_sampled(mra):
+    """The 47M-observation headline workload (BASELINE configs[3]) on one GPU."""
+    assert _sampled(mra, "C3", level=7, nsub=3, seed=2) > 3 * 80
+
+
+def test_C4_full_sampled(mra):
+    """C4 at full size (skewed swath leaves up to ~9k observations), one of its 16 thetas."""
+    assert _sampled(mra, "C4", level=9, nsub=2, seed=3, theta_idx=5) > 2 * 6
