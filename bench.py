@@ -133,6 +133,18 @@ def peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
 
 
+def measured_fp64_peak():
+    """Best DMMA TFLOP/s line of the committed fp64 microbenchmark output (profiles/fp64_peak_r01.txt)."""
+    try:
+        best = 0.0
+        for line in open(os.path.join(ROOT, "profiles", "fp64_peak_r01.txt")):
+            if line.startswith("DMMA"):
+                best = max(best, float(line.split(":")[-1].split()[0]))
+        return best or None
+    except Exception:
+        return None
+
+
 def region_box(x, y, J, level, t):
     """Box of region (level, t) by the paper's split rule (only used to pre-select the oracle's
     timing sample; the oracle assigns the points itself)."""
@@ -319,7 +331,9 @@ def run_gpu(args, rank, world, local_rank):
     fm = flop_model(sizes, w.M, w.J, plan.r_hat)
     pk, src = peaks()
     bf16 = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
-    peak64 = bf16 * FP64_NOMINAL_TF / BF16_NOMINAL_TF
+    derived64 = bf16 * FP64_NOMINAL_TF / BF16_NOMINAL_TF
+    meas64 = measured_fp64_peak()
+    peak64 = meas64 or derived64
     bottom_ms, bottom_n = kt[0][1], kt[1][1]
     steps_th = args.steps * ntheta
     roof = None
@@ -337,8 +351,10 @@ def run_gpu(args, rank, world, local_rank):
                 "frac": round(achieved / peak64, 4), "traffic": traffic,
                 "kernel": "k_bottom (leaf prior chain + Sigma_j + Cholesky + TRSM + stacked SYRK + level M-1 merge)",
                 "flops_per_launch": flops_launch, "launch_ms": launch_ms,
-                "peak_source": f"{src} bf16_tflops_sustained {bf16} x {FP64_NOMINAL_TF}/{BF16_NOMINAL_TF} "
-                               "(guide's nominal fp64-tensor:bf16 ratio)",
+                "peak_source": (f"measured fp64 DMMA peak of this B200 pool (profiles/fp64_peak_r01.txt, "
+                                f"tools/fp64_peak.cu); the guide-derived figure {src} bf16_tflops_sustained "
+                                f"{bf16} x {FP64_NOMINAL_TF}/{BF16_NOMINAL_TF} = {derived64:.2f} is lower")
+                               if meas64 else f"{src} bf16_tflops_sustained {bf16} x {FP64_NOMINAL_TF}/{BF16_NOMINAL_TF}",
                 "kernel_share_of_step": round(bottom_ms / ms, 4),
                 "step_fp64_tflops": round(fm["total"] * steps_th / (ms / 1e3) / 1e12, 3)}
     cpu = None
