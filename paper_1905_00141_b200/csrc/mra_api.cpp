@@ -69,6 +69,20 @@ struct mra_plan {
     double* smooth_d = nullptr;
     uint64_t launches = 0;
     std::vector<void*> allocs;
+    // wide (big-leaf) path
+    bool wide = false;
+    struct WideSub {
+        long long g0 = 0, gcount = 0;
+        long long chain_off = 0, chain_n = 0, sigma_off = 0, sigma_n = 0;
+        std::vector<long long> upd_off, upd_n, diag_off, diag_n, pf_off, pf_n;
+    };
+    std::vector<WideSub> wsubs;
+    size_t wsub_next = 0;
+    int4* wtasks = nullptr;
+    double *wG = nullptr, *wS = nullptr, *wD = nullptr, *wlblk = nullptr;
+    long long *wS_off = nullptr, *wD_off = nullptr;
+    int* wS_ld = nullptr;
+    int wldG = 0;
     // live per-kernel timing (CUDA events on the plan stream around every launch)
     bool prof = false;
     std::vector<cudaEvent_t> evpool;
@@ -243,6 +257,8 @@ static mra_status build_host(mra_plan* P, const double* x, const double* y, uint
 
 // ------------------------------------------------------------------- device sizing
 static long long round_up(long long v, long long a) { return (v + a - 1) / a * a; }
+static mra_status size_wide(mra_plan* P, double budget, bool explicit_budget);
+static std::vector<std::pair<long long, long long>> my_runs(const mra_plan* P);
 
 static mra_status size_device(mra_plan* P, double budget_gb) {
     const int M = P->M, J = P->J, rh = P->rh;
@@ -260,15 +276,19 @@ static mra_status size_device(mra_plan* P, double budget_gb) {
     L.ldG = (int)round_up(ncol, 2);
     L.ldS = (int)round_up(std::max<long long>(P->max_leaf, 1), 2);
     L.ldA = (int)round_up(ncol, 2);
-    const long long nb = (std::max<long long>(P->max_leaf, 1) + 63) / 64;
+    // the wide path keeps G / Sigma in global per-sub-chunk buffers: its CTA slots only need A, F, L~^{-1}
+    const long long mleaf = P->wide ? 1 : std::max<long long>(P->max_leaf, 1);
+    const long long mgroup = P->wide ? 1 : std::max<long long>(P->max_group, 1);
+    if (P->wide) L.ldS = 2;
+    const long long nb = (mleaf + 63) / 64;
     long long o = 0;
-    L.oG = o; o += round_up(std::max<long long>(P->max_group, 1) * L.ldG, 32);
-    L.oS = o; o += round_up(std::max<long long>(P->max_leaf, 1) * (long long)L.ldS, 32);
+    L.oG = o; o += round_up(mgroup * L.ldG, 32);
+    L.oS = o; o += round_up(mleaf * (long long)L.ldS, 32);
     L.oD = o; o += nb * 4096;
     L.oA = o; o += round_up((long long)ncol * L.ldA, 32);
     L.oF = o; o += round_up((long long)ncol * rh, 32);
     L.oL = o; o += round_up((long long)rh * rh, 32);
-    L.oV = o; o += round_up(std::max<long long>(P->max_leaf, 1), 32);
+    L.oV = o; o += round_up(mleaf, 32);
     // merge at level m <= M-2 needs qc^2 + q rh + rh^2 with qc = m rh + 1
     long long merge_need = 0;
     for (int m = 1; m + 2 <= M; m++) {
@@ -321,6 +341,105 @@ static mra_status size_device(mra_plan* P, double budget_gb) {
         if ((s = dalloc(P, (void**)&P->out_chunk[m], sizeof(double) * Kc * ipow(J, m - c) * q_of(m, rh) * q_of(m, rh),
                         "chunk output")))
             return s;
+    if (P->wide) return size_wide(P, budget - full_bytes(c) - chunk_bytes(c, Kc), budget_gb > 0);
+    return MRA_OK;
+}
+
+// Wide path: split every posterior chunk's level-(M-1) groups into sub-chunks whose Sigma_j fit the
+// budget, and precompute each sub-chunk's task lists (int4 {leaf, i, k, 0}).
+static mra_status size_wide(mra_plan* P, double budget, bool explicit_budget) {
+    const int M = P->M, J = P->J, rh = P->rh, mg = M - 1;
+    const int ncol = mg * rh + 1, nct = (ncol + 63) / 64;
+    P->wldG = (int)round_up(ncol, 2);
+    mra_status s;
+    if ((s = dalloc(P, (void**)&P->wG, sizeof(double) * std::max<long long>(1, P->N) * P->wldG, "wide G"))) return s;
+    budget -= 8.0 * P->N * P->wldG;
+    const double cap = std::max(budget * 0.8, explicit_budget ? 1e6 : 2e9);
+    auto leaf_n = [&](long long l) { return P->leaf_off[l + 1] - P->leaf_off[l]; };
+    auto leaf_S = [&](long long l) { long long n = leaf_n(l); return n * round_up(std::max<long long>(n, 1), 2); };
+    auto leaf_D = [&](long long l) { return ((leaf_n(l) + 63) / 64) * 4096LL; };
+    std::vector<int4> tasks;
+    std::vector<long long> S_off(P->nleaf, 0), D_off(P->nleaf, 0);
+    std::vector<int> S_ld(P->nleaf, 2);
+    long long maxS = 1, maxD = 4096;
+    auto runs = my_runs(P);
+    for (auto& rg : runs) {
+        for (long long a = rg.first; a < rg.second; a += P->Kc) {
+            const long long b = std::min(rg.second, a + P->Kc);
+            const long long sc = ipow(J, mg - P->c);
+            const long long gA = a * sc, gB = b * sc;
+            long long g = gA;
+            while (g < gB) {
+                mra_plan::WideSub ws;
+                ws.g0 = g;
+                long long sS = 0, sD = 0;
+                while (g < gB) {
+                    long long addS = 0, addD = 0;
+                    for (int c = 0; c < J; c++) { addS += leaf_S(g * J + c); addD += leaf_D(g * J + c); }
+                    if (ws.gcount > 0 && 8.0 * (sS + addS + sD + addD) > cap) break;
+                    for (int c = 0; c < J; c++) {
+                        const long long l = g * J + c;
+                        S_off[l] = sS; S_ld[l] = (int)round_up(std::max<long long>(leaf_n(l), 1), 2);
+                        D_off[l] = sD;
+                        sS += leaf_S(l); sD += leaf_D(l);
+                    }
+                    ws.gcount++;
+                    g++;
+                }
+                maxS = std::max(maxS, sS);
+                maxD = std::max(maxD, sD);
+                // task lists
+                int Tmax = 0;
+                ws.chain_off = (long long)tasks.size();
+                for (long long l = ws.g0 * J; l < (ws.g0 + ws.gcount) * J; l++) {
+                    const int T = (int)((leaf_n(l) + 63) / 64);
+                    Tmax = std::max(Tmax, T);
+                    for (int i = 0; i < T; i++) tasks.push_back(make_int4((int)l, i, 0, 0));
+                }
+                ws.chain_n = (long long)tasks.size() - ws.chain_off;
+                ws.sigma_off = (long long)tasks.size();
+                for (long long l = ws.g0 * J; l < (ws.g0 + ws.gcount) * J; l++) {
+                    const int T = (int)((leaf_n(l) + 63) / 64);
+                    for (int i = 0; i < T; i++)
+                        for (int k = 0; k <= i; k++) tasks.push_back(make_int4((int)l, i, k, 0));
+                }
+                ws.sigma_n = (long long)tasks.size() - ws.sigma_off;
+                for (int st = 0; st < Tmax; st++) {
+                    ws.upd_off.push_back((long long)tasks.size());
+                    if (st > 0)
+                        for (long long l = ws.g0 * J; l < (ws.g0 + ws.gcount) * J; l++) {
+                            const int T = (int)((leaf_n(l) + 63) / 64);
+                            for (int i = st; i < T; i++) tasks.push_back(make_int4((int)l, i, 0, 0));
+                        }
+                    ws.upd_n.push_back((long long)tasks.size() - ws.upd_off.back());
+                    ws.diag_off.push_back((long long)tasks.size());
+                    for (long long l = ws.g0 * J; l < (ws.g0 + ws.gcount) * J; l++)
+                        if ((leaf_n(l) + 63) / 64 > st) tasks.push_back(make_int4((int)l, 0, 0, 0));
+                    ws.diag_n.push_back((long long)tasks.size() - ws.diag_off.back());
+                    ws.pf_off.push_back((long long)tasks.size());
+                    for (long long l = ws.g0 * J; l < (ws.g0 + ws.gcount) * J; l++) {
+                        const int T = (int)((leaf_n(l) + 63) / 64);
+                        if (T <= st) continue;
+                        for (int i = st + 1; i < T; i++) tasks.push_back(make_int4((int)l, i, 0, 0));
+                        for (int c2 = 0; c2 < nct; c2++) tasks.push_back(make_int4((int)l, c2, 1, 0));
+                    }
+                    ws.pf_n.push_back((long long)tasks.size() - ws.pf_off.back());
+                }
+                P->wsubs.push_back(std::move(ws));
+            }
+        }
+    }
+    if ((s = dalloc(P, (void**)&P->wS, 8 * maxS, "wide Sigma"))) return s;
+    if ((s = dalloc(P, (void**)&P->wD, 8 * maxD, "wide Dinv"))) return s;
+    if ((s = dalloc(P, (void**)&P->wlblk, 8 * (maxD / 4096 + 1), "wide logdets"))) return s;
+    if ((s = dalloc(P, (void**)&P->wS_off, 8 * P->nleaf, "wide S_off"))) return s;
+    if ((s = dalloc(P, (void**)&P->wD_off, 8 * P->nleaf, "wide D_off"))) return s;
+    if ((s = dalloc(P, (void**)&P->wS_ld, 4 * P->nleaf, "wide S_ld"))) return s;
+    if ((s = dalloc(P, (void**)&P->wtasks, sizeof(int4) * std::max<size_t>(1, tasks.size()), "wide tasks"))) return s;
+    CU(cudaMemcpy(P->wS_off, S_off.data(), 8 * P->nleaf, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(P->wD_off, D_off.data(), 8 * P->nleaf, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(P->wS_ld, S_ld.data(), 4 * P->nleaf, cudaMemcpyHostToDevice));
+    if (!tasks.empty()) CU(cudaMemcpy(P->wtasks, tasks.data(), sizeof(int4) * tasks.size(), cudaMemcpyHostToDevice));
     return MRA_OK;
 }
 
@@ -349,6 +468,7 @@ extern "C" mra_status mra_plan_create(const double* x, const double* y, uint64_t
     P->world = o.world > 1 ? o.world : 1;
     mra_status s = build_host(P, x, y, n);
     if (s) { delete P; return s; }
+    P->wide = M >= 2 && (o.wide > 0 || (o.wide == 0 && P->max_leaf > 1024));
     // sharding: shard level = first level with >= 8*world regions (or the caller's choice)
     if (P->world > 1) {
         int sl = o.shard_level;
@@ -553,6 +673,37 @@ static std::vector<std::pair<long long, long long>> my_runs(const mra_plan* P) {
     return runs;
 }
 
+// wide path for the level-(M-1) groups [gf, gf + gc): consumes the precomputed sub-chunks in order
+static mra_status eval_wide(mra_plan* P, const TreeParams& tp, long long gf, long long gc, double* gout,
+                            long long gout_first) {
+    WideParams wp;
+    wp.G = P->wG; wp.ldG = P->wldG; wp.S = P->wS; wp.S_off = P->wS_off; wp.S_ld = P->wS_ld;
+    wp.D = P->wD; wp.D_off = P->wD_off; wp.lblk = P->wlblk;
+    const int q = (int)q_of(P->M - 1, P->rh);
+    cudaStream_t st = P->st;
+    long long done = 0;
+    while (done < gc) {
+        if (P->wsub_next >= P->wsubs.size()) return fail(MRA_E_CUDA, "internal: wide sub-chunk schedule exhausted");
+        const auto& w = P->wsubs[P->wsub_next++];
+        if (w.g0 != gf + done) return fail(MRA_E_CUDA, "internal: wide sub-chunk schedule out of order");
+        LCHK_K(KIND_BOTTOM, launch_wide(0, tp, wp, 0, P->wtasks + w.chain_off, w.chain_n, P->grid, take_counter(P), st));
+        LCHK_K(KIND_BOTTOM, launch_wide(1, tp, wp, 0, P->wtasks + w.sigma_off, w.sigma_n, P->grid, take_counter(P), st));
+        for (size_t s2 = 0; s2 < w.diag_n.size(); s2++) {
+            if (w.upd_n[s2] > 0)
+                LCHK_K(KIND_BOTTOM, launch_wide(2, tp, wp, (int)s2, P->wtasks + w.upd_off[s2], w.upd_n[s2], P->grid,
+                                                take_counter(P), st));
+            LCHK_K(KIND_BOTTOM, launch_wide(3, tp, wp, (int)s2, P->wtasks + w.diag_off[s2], w.diag_n[s2], P->grid,
+                                            take_counter(P), st));
+            LCHK_K(KIND_BOTTOM, launch_wide(4, tp, wp, (int)s2, P->wtasks + w.pf_off[s2], w.pf_n[s2], P->grid,
+                                            take_counter(P), st));
+        }
+        LCHK_K(KIND_BOTTOM, launch_wide_group(tp, wp, w.g0, w.gcount, gout, gout_first, q, P->grid, P->ws, P->L,
+                                              take_counter(P), st));
+        done += w.gcount;
+    }
+    return MRA_OK;
+}
+
 // prior + posterior below (and at) level c for this rank's subtrees
 static mra_status eval_lower(mra_plan* P, const TreeParams& tp) {
     const int M = P->M, J = P->J, rh = P->rh, c = P->c;
@@ -584,8 +735,13 @@ static mra_status eval_lower(mra_plan* P, const TreeParams& tp) {
             range_at(P, mg, a, b, &gf, &gc);
             double* gout = (mg <= c) ? P->out_full[mg] : P->out_chunk[mg];
             const long long gout_first = (mg <= c) ? 0 : gf;
-            LCHK_K(KIND_BOTTOM, launch_bottom(tp, gf, gc, gout, gout_first, (int)q_of(mg, rh), P->grid, P->ws, P->L,
-                               take_counter(P), st));
+            if (P->wide) {
+                mra_status ws_ = eval_wide(P, tp, gf, gc, gout, gout_first);
+                if (ws_) return ws_;
+            } else {
+                LCHK_K(KIND_BOTTOM, launch_bottom(tp, gf, gc, gout, gout_first, (int)q_of(mg, rh), P->grid, P->ws,
+                                                  P->L, take_counter(P), st));
+            }
             for (int m = mg - 1; m >= c; m--) {
                 long long f, cnt, cf, ccnt;
                 range_at(P, m, a, b, &f, &cnt);
@@ -638,6 +794,7 @@ static mra_status begin_eval(mra_plan* P, const double* d_y, const mra_theta* th
     if (s) return s;
     if (cudaSetDevice(P->device) != cudaSuccess) return fail(MRA_E_CUDA, "cudaSetDevice failed");
     CU(cudaMemsetAsync(P->counters, 0, 8 * (size_t)P->n_counters, P->st));
+    P->wsub_next = 0;
     CU(cudaMemsetAsync(P->err, 0, 16, P->st));
     LCHK(launch_gather(d_y, P->perm_d, P->zs, P->N, P->st));
     return MRA_OK;
@@ -664,6 +821,8 @@ static mra_status run_eval(mra_plan* P, const double* d_y, const mra_theta* th, 
     if (P->world > 1) return fail(MRA_E_CONFIG, "sharded plan: use mra_loglik_shard / mra_loglik_finish");
     mra_status s;
     const bool want_state = post && (post->mu || post->smooth);
+    if (post && post->smooth && P->wide)
+        return fail(MRA_E_CONFIG, "posterior smoothing is not available on the wide (big-leaf) path in this build");
     if (want_state && (s = ensure_post(P))) return s;
     if ((s = begin_eval(P, d_y, th))) return s;
     TreeParams tp = tree_params(P, th);

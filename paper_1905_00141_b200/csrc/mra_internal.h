@@ -39,6 +39,19 @@ struct WsLayout {
     int ldG, ldS, ldA;
 };
 
+// wide (big-leaf) path buffers: G rows indexed by sorted observation, Sigma / inverted diagonal
+// blocks / block log-dets per leaf of the current sub-chunk (offsets valid for its leaves)
+struct WideParams {
+    double* G;
+    int ldG;
+    double* S;
+    const long long* S_off;
+    const int* S_ld;
+    double* D;
+    const long long* D_off;   // multiple of 4096; block log-det of (leaf, s) at lblk[D_off/4096 + s]
+    double* lblk;
+};
+
 // launchers (all asynchronous on `st`); return cudaGetLastError()
 cudaError_t launch_gather(const double* z, const long long* perm, double* zs, long long N, cudaStream_t st);
 // region ranges: level-m regions [t_first, t_first + t_count); output buffers are indexed by
@@ -58,6 +71,12 @@ cudaError_t launch_smooth(const TreeParams& tp, const double* muhat, const long 
                           int grid, double* ws, const WsLayout& L, unsigned long long* counter,
                           cudaStream_t st);
 cudaError_t launch_fill(double* p, long long n, double v, cudaStream_t st);
+// wide path: phase 0 chain, 1 sigma, 2 column update (step), 3 diagonal (step), 4 panel + fwd (step)
+cudaError_t launch_wide(int phase, const TreeParams& tp, const WideParams& wp, int step, const int4* tasks,
+                        long long ntask, int grid, unsigned long long* counter, cudaStream_t st);
+cudaError_t launch_wide_group(const TreeParams& tp, const WideParams& wp, long long g_first, long long g_count,
+                              double* out, long long out_first, int q, int grid, double* ws, const WsLayout& L,
+                              unsigned long long* counter, cudaStream_t st);
 int smem_bytes();
 void phase_cycles(unsigned long long* out16, bool reset);   // -DMRA_PHASE_TIMING builds only
 

@@ -152,6 +152,27 @@ __device__ __forceinline__ void save_post(const TreeParams& tp, int m, long long
     for (int e = threadIdx.x; e < q * rh; e += NT) P[rh * rh + e] = F[e];
 }
 
+// Atilde_p = G_stack^T G_stack over the group's leaves (lower), then the merge of level-(M-1) region t
+__device__ void group_tail(const TreeParams& tp, int m, long long t, const double* G, long long ldG, int ng,
+                           double dsum, double* out, long long out_first, int q, double* A, long long ldA, double* F,
+                           double* Li, const CovP& cp, double* smem) {
+    const int ncol = m * tp.rh + 1;
+    PHASE_MARK(c4);
+    cta_gemm<MEMT, MEMT, MEMN, MEMN>(ncol, ncol, 1, op_mem(G, ldG), op_mem(G, ldG), ng, op_mem(G, 0), op_mem(G, 0), 0,
+                                     ci_zero(), 1.0, A, ldA, cp, smem);
+    PHASE_ADD(4, c4);
+    PHASE_MARK(c5);
+    double* O = out + (t - out_first) * (long long)q * q;
+    const double ldm = merge_core(A, tp.rh, ldA, O, q, F, Li, tp.err, m, t, cp, smem);
+    PHASE_ADD(5, c5);
+    const long long id = lvl_first(tp.J, m) + t;
+    if (threadIdx.x == 0) {
+        tp.dreg[id] = dsum + ldm;
+        tp.ureg[id] = O[(long long)(q - 1) * q + q - 1];
+    }
+    save_post(tp, m, t, q, Li, F);
+}
+
 // -------------------------------------------------------------------------- bottom
 __global__ void __launch_bounds__(NT, MRA_MINB)
 k_bottom(TreeParams tp, long long g_first, long long g_count, double* out, long long out_first, int q, double* ws,
@@ -220,21 +241,7 @@ k_bottom(TreeParams tp, long long g_first, long long g_count, double* out, long 
             if (threadIdx.x == 0) { tp.dreg[0] = dsum; tp.ureg[0] = ulast; }
             continue;
         }
-        // Atilde_p = sum_c G_c^T G_c = G_stack^T G_stack (lower)
-        PHASE_MARK(c4);
-        cta_gemm<MEMT, MEMT, MEMN, MEMN>(ncol, ncol, 1, op_mem(G, L.ldG), op_mem(G, L.ldG), (int)ng, op_mem(G, 0),
-                                         op_mem(G, 0), 0, ci_zero(), 1.0, A, L.ldA, cp, smem);
-        PHASE_ADD(4, c4);
-        PHASE_MARK(c5);
-        double* O = out + (t - out_first) * (long long)q * q;
-        const double ldm = merge_core(A, rh, L.ldA, O, q, F, Li, tp.err, m, t, cp, smem);
-        PHASE_ADD(5, c5);
-        const long long id = lvl_first(J, m) + t;
-        if (threadIdx.x == 0) {
-            tp.dreg[id] = dsum + ldm;
-            tp.ureg[id] = O[(long long)(q - 1) * q + q - 1];
-        }
-        save_post(tp, m, t, q, Li, F);
+        group_tail(tp, m, t, G, L.ldG, (int)ng, dsum, out, out_first, q, A, L.ldA, F, Li, cp, smem);
     }
     PHASE_ADD(12, kstart);
 }
@@ -416,6 +423,185 @@ k_smooth(TreeParams tp, const double* muhat, const long long* perm, double* smoo
     }
 }
 
+
+// ====================================================================== wide (big-leaf) path
+// Leaves too large for one CTA (C4: up to ~9k observations) are processed by all CTAs together,
+// phase by phase, from precomputed task lists: row-tile V chains, Sigma tiles, a
+// left-looking batched blocked Cholesky (per step s: column update with K = 64 s, diagonal factor
+// per leaf, panel solve), batched block forward substitution, per-leaf d/u, then per group the
+// stacked SYRK + merge. Tasks are int4 {leaf, i, k, 0}.
+
+__device__ __forceinline__ int leaf_n(const TreeParams& tp, long long l) {
+    return (int)(tp.leaf_off[l + 1] - tp.leaf_off[l]);
+}
+
+// V chain + y column for 64 rows of one leaf
+__global__ void __launch_bounds__(NT, MRA_MINB)
+k_wide_chain(TreeParams tp, WideParams wp, const int4* tasks, long long ntask, unsigned long long* counter) {
+    extern __shared__ double smem[];
+    const CovP cp = to_covp(tp.cp);
+    const int m = tp.M - 1, Pg = m * tp.rh;
+    for (;;) {
+        const long long it = next_item(counter, smem);
+        if (it >= ntask) break;
+        const int4 tk = tasks[it];
+        const long long l = tk.x;
+        const long long o0 = tp.leaf_off[l] + 64LL * tk.y;
+        const int n = min(64, leaf_n(tp, l) - 64 * tk.y);
+        double* Gr = wp.G + o0 * wp.ldG;
+        point_chain(tp, m, l >> tp.lj, n, tp.pxy + 2 * o0, Gr, wp.ldG, cp, smem);
+        for (int i = threadIdx.x; i < n; i += NT) Gr[(long long)i * wp.ldG + Pg] = tp.zs[o0 + i];
+    }
+}
+
+// Sigma_l tile (i, k), k <= i: C(S_i, S_k) + tau2 delta - V_i V_k^T
+__global__ void __launch_bounds__(NT, MRA_MINB)
+k_wide_sigma(TreeParams tp, WideParams wp, const int4* tasks, long long ntask, unsigned long long* counter) {
+    extern __shared__ double smem[];
+    const CovP cp = to_covp(tp.cp);
+    const int Pg = (tp.M - 1) * tp.rh;
+    for (;;) {
+        const long long it = next_item(counter, smem);
+        if (it >= ntask) break;
+        const int4 tk = tasks[it];
+        const long long l = tk.x;
+        const int i = tk.y, k = tk.z, n = leaf_n(tp, l);
+        const long long o = tp.leaf_off[l];
+        const int ld = wp.S_ld[l];
+        double* C = wp.S + wp.S_off[l] + 64LL * i * ld + 64LL * k;
+        const double* Gi = wp.G + (o + 64LL * i) * wp.ldG;
+        const double* Gk = wp.G + (o + 64LL * k) * wp.ldG;
+        cta_gemm<MEMN, MEMN, MEMN, MEMN>(min(64, n - 64 * i), min(64, n - 64 * k), i == k, op_mem(Gi, wp.ldG),
+                                         op_mem(Gk, wp.ldG), Pg, op_mem(Gi, 0), op_mem(Gi, 0), 0,
+                                         ci_cov(tp.pxy + 2 * (o + 64LL * i), tp.pxy + 2 * (o + 64LL * k),
+                                                i == k ? tp.tau2 : 0.0),
+                                         -1.0, C, ld, cp, smem);
+    }
+}
+
+// left-looking column update at step s: A_is -= L_{i,<s} L_{s,<s}^T  (i >= s, s >= 1)
+__global__ void __launch_bounds__(NT, MRA_MINB)
+k_wide_update(TreeParams tp, WideParams wp, int s, const int4* tasks, long long ntask, unsigned long long* counter) {
+    extern __shared__ double smem[];
+    const CovP cp = to_covp(tp.cp);
+    for (;;) {
+        const long long it = next_item(counter, smem);
+        if (it >= ntask) break;
+        const int4 tk = tasks[it];
+        const long long l = tk.x;
+        const int i = tk.y, n = leaf_n(tp, l), ld = wp.S_ld[l];
+        double* Sl = wp.S + wp.S_off[l];
+        double* C = Sl + 64LL * i * ld + 64LL * s;
+        const double* Ai = Sl + 64LL * i * ld;
+        const double* As = Sl + 64LL * s * ld;
+        cta_gemm<MEMN, MEMN, MEMN, MEMN>(min(64, n - 64 * i), min(64, n - 64 * s), i == s, op_mem(Ai, ld),
+                                         op_mem(As, ld), 64 * s, op_mem(Ai, 0), op_mem(Ai, 0), 0, ci_mem(C, ld), -1.0,
+                                         C, ld, cp, smem);
+    }
+}
+
+// diagonal block of step s for every leaf with more than s blocks: L_ss, D_s = L_ss^{-1}, log-det
+__global__ void __launch_bounds__(NT, MRA_MINB)
+k_wide_diag(TreeParams tp, WideParams wp, int s, const int4* tasks, long long ntask, unsigned long long* counter) {
+    extern __shared__ double smem[];
+    FacSmem f = fac_smem(smem);
+    for (;;) {
+        const long long it = next_item(counter, smem);
+        if (it >= ntask) break;
+        if (threadIdx.x == 0) *f.bad = 0;
+        const long long l = tasks[it].x;
+        const int n = leaf_n(tp, l), ld = wp.S_ld[l], nb = min(64, n - 64 * s);
+        double* Sss = wp.S + wp.S_off[l] + 64LL * s * ld + 64LL * s;
+        double* Ds = wp.D + wp.D_off[l] + 4096LL * s;
+        load_block_lower(f.blk, Sss, ld, nb, 0.0);
+        const double ldet = chol_inv_small(f.blk, f.inv, nb, f.diagv, f.bad, f.red, f.tmp);
+        if (*f.bad && threadIdx.x == 0) set_err(tp.err, tp.M, l);
+        store_block_lower(f.blk, Sss, ld, nb);
+        store_block_full(f.inv, Ds, 64, nb);
+        if (threadIdx.x == 0) wp.lblk[wp.D_off[l] / 4096 + s] = ldet;
+    }
+}
+
+// step s, after the diagonal: panel tasks (leaf, i > s, k = 0): L_is = A_is D_s^T, and forward
+// substitution tasks (leaf, col tile c, k = 1): G_s[:, c] = D_s (G_s[:, c] - L_{s,<s} G_{<s}[:, c])
+__global__ void __launch_bounds__(NT, MRA_MINB)
+k_wide_panel_fwd(TreeParams tp, WideParams wp, int s, const int4* tasks, long long ntask, unsigned long long* counter) {
+    extern __shared__ double smem[];
+    const CovP cp = to_covp(tp.cp);
+    const int ncol = (tp.M - 1) * tp.rh + 1;
+    for (;;) {
+        const long long it = next_item(counter, smem);
+        if (it >= ntask) break;
+        const int4 tk = tasks[it];
+        const long long l = tk.x;
+        const int n = leaf_n(tp, l), ld = wp.S_ld[l], nb = min(64, n - 64 * s);
+        double* Sl = wp.S + wp.S_off[l];
+        const double* Ds = wp.D + wp.D_off[l] + 4096LL * s;
+        if (tk.z == 0) {
+            const int i = tk.y;
+            double* P = Sl + 64LL * i * ld + 64LL * s;
+            cta_gemm<MEMN, MEMN, MEMN, MEMN>(min(64, n - 64 * i), nb, 0, op_mem(P, ld), op_mem(Ds, 64), nb,
+                                             op_mem(P, 0), op_mem(P, 0), 0, ci_zero(), 1.0, P, ld, cp, smem);
+        } else {
+            const int c = tk.y;
+            const long long o = tp.leaf_off[l];
+            double* Gs = wp.G + (o + 64LL * s) * wp.ldG + 64LL * c;
+            const int nc = min(64, ncol - 64 * c);
+            if (s > 0)
+                cta_gemm<MEMN, MEMT, MEMN, MEMN>(nb, nc, 0, op_mem(Sl + 64LL * s * ld, ld),
+                                                 op_mem(wp.G + o * wp.ldG + 64LL * c, wp.ldG), 64 * s, op_mem(Sl, 0),
+                                                 op_mem(Sl, 0), 0, ci_mem(Gs, wp.ldG), -1.0, Gs, wp.ldG, cp, smem);
+            cta_gemm<MEMN, MEMT, MEMN, MEMN>(nb, nc, 0, op_mem(Ds, 64), op_mem(Gs, wp.ldG), nb, op_mem(Ds, 0),
+                                             op_mem(Ds, 0), 0, ci_zero(), 1.0, Gs, wp.ldG, cp, smem);
+        }
+    }
+}
+
+// per group: leaf d_j = sum of block log-dets, u_j = |g_j|^2, then the stacked SYRK + merge
+__global__ void __launch_bounds__(NT, MRA_MINB)
+k_wide_group(TreeParams tp, WideParams wp, long long g_first, long long g_count, double* out, long long out_first,
+             int q, double* ws, WsLayout L, unsigned long long* counter) {
+    extern __shared__ double smem[];
+    const CovP cp = to_covp(tp.cp);
+    const int M = tp.M, J = tp.J, m = M - 1, Pg = m * tp.rh;
+    double* base = ws + (long long)blockIdx.x * L.stride;
+    double *A = base + L.oA, *F = base + L.oF, *Li = base + L.oL;
+    FacSmem f = fac_smem(smem);
+    double* red = misc_smem(smem);
+    const long long leaf_id0 = lvl_first(J, M);
+    for (;;) {
+        const long long it = next_item(counter, smem);
+        if (it >= g_count) break;
+        if (threadIdx.x == 0) *f.bad = 0;
+        const long long t = g_first + it;
+        double dsum = 0.0;
+        for (int c = 0; c < J; c++) {
+            const long long l = t * J + c;
+            const long long o = tp.leaf_off[l];
+            const int n = leaf_n(tp, l);
+            double u = 0.0;
+            for (int i = threadIdx.x; i < n; i += NT) {
+                const double g = wp.G[(o + i) * wp.ldG + Pg];
+                u += g * g;
+            }
+            u = cta_sum(u, red);
+            double d = 0.0;
+            if (threadIdx.x == 0) {
+                for (int b = 0; b < (n + 63) / 64; b++) d += wp.lblk[wp.D_off[l] / 4096 + b];
+                tp.dreg[leaf_id0 + l] = d;
+                tp.ureg[leaf_id0 + l] = u;
+                red[9] = d;
+            }
+            __syncthreads();
+            dsum += red[9];
+            __syncthreads();
+        }
+        const long long o = tp.leaf_off[t * J];
+        const int ng = (int)(tp.leaf_off[t * J + J] - o);
+        group_tail(tp, m, t, wp.G + o * wp.ldG, wp.ldG, ng, dsum, out, out_first, q, A, L.ldA, F, Li, cp, smem);
+    }
+}
+
 // ------------------------------------------------------------------------ launchers
 int smem_bytes() { return SMEM_DBL * (int)sizeof(double); }
 
@@ -428,15 +614,18 @@ void phase_cycles(unsigned long long* out16, bool reset) {
 }
 
 static bool g_attr_done = false;
-static int g_resident[4] = {1, 1, 1, 1};   // resident CTAs per SM x SM count, per persistent kernel
+static int g_resident[10] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 1};   // resident CTAs per SM x SM count
 static void set_attrs() {
     if (g_attr_done) return;
     const int b = smem_bytes();
-    const void* ks[4] = {(const void*)k_prior, (const void*)k_bottom, (const void*)k_merge, (const void*)k_smooth};
+    const void* ks[10] = {(const void*)k_prior,      (const void*)k_bottom,      (const void*)k_merge,
+                          (const void*)k_smooth,     (const void*)k_wide_chain,  (const void*)k_wide_sigma,
+                          (const void*)k_wide_update, (const void*)k_wide_diag,  (const void*)k_wide_panel_fwd,
+                          (const void*)k_wide_group};
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    for (int i = 0; i < 4; i++) {
+    for (int i = 0; i < 10; i++) {
         cudaFuncSetAttribute(ks[i], cudaFuncAttributeMaxDynamicSharedMemorySize, b);
         int per = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ks[i], NT, b);
@@ -511,4 +700,32 @@ cudaError_t launch_smooth(const TreeParams& tp, const double* muhat, const long 
     return cudaGetLastError();
 }
 
+}  // namespace mra
+
+namespace mra {
+cudaError_t launch_wide(int phase, const TreeParams& tp, const WideParams& wp, int step, const int4* tasks,
+                        long long ntask, int grid, unsigned long long* counter, cudaStream_t st) {
+    set_attrs();
+    grid = clamp_grid(grid, ntask, 4 + phase);
+    if (grid < 1) return cudaSuccess;
+    const int b = smem_bytes();
+    switch (phase) {
+        case 0: k_wide_chain<<<grid, NT, b, st>>>(tp, wp, tasks, ntask, counter); break;
+        case 1: k_wide_sigma<<<grid, NT, b, st>>>(tp, wp, tasks, ntask, counter); break;
+        case 2: k_wide_update<<<grid, NT, b, st>>>(tp, wp, step, tasks, ntask, counter); break;
+        case 3: k_wide_diag<<<grid, NT, b, st>>>(tp, wp, step, tasks, ntask, counter); break;
+        case 4: k_wide_panel_fwd<<<grid, NT, b, st>>>(tp, wp, step, tasks, ntask, counter); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+cudaError_t launch_wide_group(const TreeParams& tp, const WideParams& wp, long long g_first, long long g_count,
+                              double* out, long long out_first, int q, int grid, double* ws, const WsLayout& L,
+                              unsigned long long* counter, cudaStream_t st) {
+    set_attrs();
+    grid = clamp_grid(grid, g_count, 9);
+    if (grid < 1) return cudaSuccess;
+    k_wide_group<<<grid, NT, smem_bytes(), st>>>(tp, wp, g_first, g_count, out, out_first, q, ws, L, counter);
+    return cudaGetLastError();
+}
 }  // namespace mra

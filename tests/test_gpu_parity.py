@@ -172,3 +172,20 @@ def test_bad_theta_is_arg_error(mra):
     zb = z.copy(); zb[0] = np.inf
     with pytest.raises(mra.MraError):
         mra.mra_loglik(p, zb, (0, 1.0, 0.1, 0.1))
+
+
+@pytest.mark.parametrize("n,M,J,r,cov,cl", [(6000, 3, 2, 30, EXP, 0), (9000, 4, 4, 16, MAT, 3), (3000, 2, 2, 64, EXP, 1),
+                                            (12000, 5, 2, 25, EXP, 4)])
+def test_wide_path_parity(mra, n, M, J, r, cov, cl):
+    """Big-leaf path (all CTAs cooperate per leaf; forced on for moderate leaves so the oracle stays fast):
+    multi-block left-looking Cholesky, ragged tails, empty leaves."""
+    x, y, z = synth.uniform_small(n, seed=200 + n + M, clusters=cl)
+    theta = (cov, 1.0, 0.08, 0.05)
+    p = mra.mra_plan_create(x, y, M, J, r, wide=1)
+    got = mra.mra_loglik(p, z, theta, posterior=False, regions=True)
+    ref = oracle.run(x, y, z, M, J, r, theta, regions=True)
+    _cmp(got, ref, posterior=False)
+    # a tiny Sigma budget forces several sub-chunks
+    p2 = mra.mra_plan_create(x, y, M, J, r, wide=1, mem_budget_gb=0.02)
+    got2 = mra.mra_loglik(p2, z, theta)
+    assert abs(got2["loglik"] - got["loglik"]) <= 1e-12 * abs(got["loglik"])
