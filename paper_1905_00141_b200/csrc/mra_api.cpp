@@ -67,6 +67,9 @@ struct mra_plan {
     double* muhat = nullptr;
     double* mu_d = nullptr;
     double* smooth_d = nullptr;
+    double* ws_smooth = nullptr;     // wide plans: per-CTA smoothing workspace sized for the largest leaf
+    WsLayout Ls{};
+    int smooth_grid = 0;
     uint64_t launches = 0;
     std::vector<void*> allocs;
     // wide (big-leaf) path
@@ -813,6 +816,25 @@ static mra_status ensure_post(mra_plan* P) {
     if ((s = dalloc(P, (void**)&P->muhat, 8 * std::max<long long>(P->nint * rh, 1), "muhat"))) return s;
     if ((s = dalloc(P, (void**)&P->mu_d, 8 * std::max<long long>(P->nint * rh, 1), "mu"))) return s;
     if ((s = dalloc(P, (void**)&P->smooth_d, 8 * (long long)P->n_in, "smooth"))) return s;
+    if (P->wide) {
+        // the wide path keeps no per-CTA leaf workspace; smoothing recomputes each leaf on one CTA
+        WsLayout L = P->L;
+        const long long mleaf = std::max<long long>(P->max_leaf, 1);
+        L.ldS = (int)round_up(mleaf, 2);
+        long long o = 0;
+        L.oG = o; o += round_up(mleaf * L.ldG, 32);
+        L.oS = o; o += round_up(mleaf * (long long)L.ldS, 32);
+        L.oD = o; o += ((mleaf + 63) / 64) * 4096;
+        L.oA = L.oF = L.oL = o;
+        L.oV = o; o += round_up(mleaf, 32);
+        L.stride = round_up(o, 64);
+        size_t freeb = 0, totalb = 0;
+        cudaMemGetInfo(&freeb, &totalb);
+        long long slots = std::min<long long>(P->grid, std::max<long long>(1, (long long)(0.5 * freeb / (8.0 * L.stride))));
+        P->Ls = L;
+        P->smooth_grid = (int)slots;
+        if ((s = dalloc(P, (void**)&P->ws_smooth, 8 * L.stride * slots, "smoothing workspace"))) return s;
+    }
     return MRA_OK;
 }
 
@@ -821,8 +843,6 @@ static mra_status run_eval(mra_plan* P, const double* d_y, const mra_theta* th, 
     if (P->world > 1) return fail(MRA_E_CONFIG, "sharded plan: use mra_loglik_shard / mra_loglik_finish");
     mra_status s;
     const bool want_state = post && (post->mu || post->smooth);
-    if (post && post->smooth && P->wide)
-        return fail(MRA_E_CONFIG, "posterior smoothing is not available on the wide (big-leaf) path in this build");
     if (want_state && (s = ensure_post(P))) return s;
     if ((s = begin_eval(P, d_y, th))) return s;
     TreeParams tp = tree_params(P, th);
@@ -843,7 +863,11 @@ static mra_status run_eval(mra_plan* P, const double* d_y, const mra_theta* th, 
         for (int m = 1; m < P->M; m++) LCHK(launch_mu(tp, m, P->muhat, P->mu_d, P->st));
         if (post->smooth) {
             LCHK(launch_fill(P->smooth_d, (long long)P->n_in, NAN, P->st));
-            LCHK(launch_smooth(tp, P->muhat, P->perm_d, P->smooth_d, P->grid, P->ws, P->L, take_counter(P), P->st));
+            if (P->wide)
+                LCHK(launch_smooth(tp, P->muhat, P->perm_d, P->smooth_d, P->smooth_grid, P->ws_smooth, P->Ls,
+                                   take_counter(P), P->st));
+            else
+                LCHK(launch_smooth(tp, P->muhat, P->perm_d, P->smooth_d, P->grid, P->ws, P->L, take_counter(P), P->st));
         }
         if ((s = check_err(P))) return s;
         const size_t nmu = 8 * (size_t)P->nint * P->rh;

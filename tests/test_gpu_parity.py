@@ -189,3 +189,13 @@ def test_wide_path_parity(mra, n, M, J, r, cov, cl):
     p2 = mra.mra_plan_create(x, y, M, J, r, wide=1, mem_budget_gb=0.02)
     got2 = mra.mra_loglik(p2, z, theta)
     assert abs(got2["loglik"] - got["loglik"]) <= 1e-12 * abs(got["loglik"])
+
+
+def test_wide_path_posterior(mra):
+    """Posterior state (mu, smoothing) on a plan that takes the wide path."""
+    x, y, z = synth.uniform_small(5000, seed=301, clusters=2)
+    theta = (EXP, 1.0, 0.1, 0.05)
+    p = mra.mra_plan_create(x, y, 3, 2, 30, wide=1)
+    got = mra.mra_loglik(p, z, theta, posterior=True, regions=True)
+    ref = oracle.run(x, y, z, 3, 2, 30, theta, regions=True, posterior=True)
+    _cmp(got, ref)
