@@ -388,6 +388,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle CPU work")
     ap.add_argument("--ref-budget", type=float, default=10.0, help="seconds of oracle work per reference step")
+    ap.add_argument("--dist-backend", default="nccl", help="process-group backend for N > 1 (nccl on a real "
+                    "multi-GPU node; gloo + --same-device only to exercise the sharded path on one GPU)")
+    ap.add_argument("--same-device", action="store_true", help="test only: every rank uses cuda:0")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -395,10 +398,15 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank)
         return
+    if args.same_device:
+        local_rank = 0
     if world > 1:
         import torch
         torch.cuda.set_device(local_rank)
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.dist_backend == "nccl":
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            torch.distributed.init_process_group(args.dist_backend)
     try:
         run_gpu(args, rank, world, local_rank)
     finally:

@@ -355,9 +355,8 @@ static mra_status size_wide(mra_plan* P, double budget, bool explicit_budget) {
     const int ncol = mg * rh + 1, nct = (ncol + 63) / 64;
     P->wldG = (int)round_up(ncol, 2);
     mra_status s;
-    if ((s = dalloc(P, (void**)&P->wG, sizeof(double) * std::max<long long>(1, P->N) * P->wldG, "wide G"))) return s;
-    budget -= 8.0 * P->N * P->wldG;
     const double cap = std::max(budget * 0.8, explicit_budget ? 1e6 : 2e9);
+    long long maxG = 1;
     auto leaf_n = [&](long long l) { return P->leaf_off[l + 1] - P->leaf_off[l]; };
     auto leaf_S = [&](long long l) { long long n = leaf_n(l); return n * round_up(std::max<long long>(n, 1), 2); };
     auto leaf_D = [&](long long l) { return ((leaf_n(l) + 63) / 64) * 4096LL; };
@@ -379,7 +378,8 @@ static mra_status size_wide(mra_plan* P, double budget, bool explicit_budget) {
                 while (g < gB) {
                     long long addS = 0, addD = 0;
                     for (int c = 0; c < J; c++) { addS += leaf_S(g * J + c); addD += leaf_D(g * J + c); }
-                    if (ws.gcount > 0 && 8.0 * (sS + addS + sD + addD) > cap) break;
+                    const long long gRows = P->leaf_off[(g + 1) * J] - P->leaf_off[ws.g0 * J];
+                    if (ws.gcount > 0 && 8.0 * (sS + addS + sD + addD + gRows * (long long)P->wldG) > cap) break;
                     for (int c = 0; c < J; c++) {
                         const long long l = g * J + c;
                         S_off[l] = sS; S_ld[l] = (int)round_up(std::max<long long>(leaf_n(l), 1), 2);
@@ -391,6 +391,7 @@ static mra_status size_wide(mra_plan* P, double budget, bool explicit_budget) {
                 }
                 maxS = std::max(maxS, sS);
                 maxD = std::max(maxD, sD);
+                maxG = std::max(maxG, P->leaf_off[(ws.g0 + ws.gcount) * J] - P->leaf_off[ws.g0 * J]);
                 // task lists
                 int Tmax = 0;
                 ws.chain_off = (long long)tasks.size();
@@ -432,6 +433,7 @@ static mra_status size_wide(mra_plan* P, double budget, bool explicit_budget) {
             }
         }
     }
+    if ((s = dalloc(P, (void**)&P->wG, 8 * maxG * P->wldG, "wide G"))) return s;
     if ((s = dalloc(P, (void**)&P->wS, 8 * maxS, "wide Sigma"))) return s;
     if ((s = dalloc(P, (void**)&P->wD, 8 * maxD, "wide Dinv"))) return s;
     if ((s = dalloc(P, (void**)&P->wlblk, 8 * (maxD / 4096 + 1), "wide logdets"))) return s;
@@ -689,6 +691,7 @@ static mra_status eval_wide(mra_plan* P, const TreeParams& tp, long long gf, lon
         if (P->wsub_next >= P->wsubs.size()) return fail(MRA_E_CUDA, "internal: wide sub-chunk schedule exhausted");
         const auto& w = P->wsubs[P->wsub_next++];
         if (w.g0 != gf + done) return fail(MRA_E_CUDA, "internal: wide sub-chunk schedule out of order");
+        wp.G_base = P->leaf_off[w.g0 * P->J];
         LCHK_K(KIND_BOTTOM, launch_wide(0, tp, wp, 0, P->wtasks + w.chain_off, w.chain_n, P->grid, take_counter(P), st));
         LCHK_K(KIND_BOTTOM, launch_wide(1, tp, wp, 0, P->wtasks + w.sigma_off, w.sigma_n, P->grid, take_counter(P), st));
         for (size_t s2 = 0; s2 < w.diag_n.size(); s2++) {

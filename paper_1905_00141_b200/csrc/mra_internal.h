@@ -42,7 +42,8 @@ struct WsLayout {
 // wide (big-leaf) path buffers: G rows indexed by sorted observation, Sigma / inverted diagonal
 // blocks / block log-dets per leaf of the current sub-chunk (offsets valid for its leaves)
 struct WideParams {
-    double* G;
+    double* G;                // row of sorted observation o at G + (o - G_base) * ldG
+    long long G_base;
     int ldG;
     double* S;
     const long long* S_off;

@@ -448,7 +448,7 @@ k_wide_chain(TreeParams tp, WideParams wp, const int4* tasks, long long ntask, u
         const long long l = tk.x;
         const long long o0 = tp.leaf_off[l] + 64LL * tk.y;
         const int n = min(64, leaf_n(tp, l) - 64 * tk.y);
-        double* Gr = wp.G + o0 * wp.ldG;
+        double* Gr = wp.G + (o0 - wp.G_base) * wp.ldG;
         point_chain(tp, m, l >> tp.lj, n, tp.pxy + 2 * o0, Gr, wp.ldG, cp, smem);
         for (int i = threadIdx.x; i < n; i += NT) Gr[(long long)i * wp.ldG + Pg] = tp.zs[o0 + i];
     }
@@ -469,8 +469,8 @@ k_wide_sigma(TreeParams tp, WideParams wp, const int4* tasks, long long ntask, u
         const long long o = tp.leaf_off[l];
         const int ld = wp.S_ld[l];
         double* C = wp.S + wp.S_off[l] + 64LL * i * ld + 64LL * k;
-        const double* Gi = wp.G + (o + 64LL * i) * wp.ldG;
-        const double* Gk = wp.G + (o + 64LL * k) * wp.ldG;
+        const double* Gi = wp.G + (o - wp.G_base + 64LL * i) * wp.ldG;
+        const double* Gk = wp.G + (o - wp.G_base + 64LL * k) * wp.ldG;
         cta_gemm<MEMN, MEMN, MEMN, MEMN>(min(64, n - 64 * i), min(64, n - 64 * k), i == k, op_mem(Gi, wp.ldG),
                                          op_mem(Gk, wp.ldG), Pg, op_mem(Gi, 0), op_mem(Gi, 0), 0,
                                          ci_cov(tp.pxy + 2 * (o + 64LL * i), tp.pxy + 2 * (o + 64LL * k),
@@ -545,11 +545,12 @@ k_wide_panel_fwd(TreeParams tp, WideParams wp, int s, const int4* tasks, long lo
         } else {
             const int c = tk.y;
             const long long o = tp.leaf_off[l];
-            double* Gs = wp.G + (o + 64LL * s) * wp.ldG + 64LL * c;
+            double* Gs = wp.G + (o - wp.G_base + 64LL * s) * wp.ldG + 64LL * c;
             const int nc = min(64, ncol - 64 * c);
             if (s > 0)
                 cta_gemm<MEMN, MEMT, MEMN, MEMN>(nb, nc, 0, op_mem(Sl + 64LL * s * ld, ld),
-                                                 op_mem(wp.G + o * wp.ldG + 64LL * c, wp.ldG), 64 * s, op_mem(Sl, 0),
+                                                 op_mem(wp.G + (o - wp.G_base) * wp.ldG + 64LL * c, wp.ldG), 64 * s,
+                                                 op_mem(Sl, 0),
                                                  op_mem(Sl, 0), 0, ci_mem(Gs, wp.ldG), -1.0, Gs, wp.ldG, cp, smem);
             cta_gemm<MEMN, MEMT, MEMN, MEMN>(nb, nc, 0, op_mem(Ds, 64), op_mem(Gs, wp.ldG), nb, op_mem(Ds, 0),
                                              op_mem(Ds, 0), 0, ci_zero(), 1.0, Gs, wp.ldG, cp, smem);
@@ -581,7 +582,7 @@ k_wide_group(TreeParams tp, WideParams wp, long long g_first, long long g_count,
             const int n = leaf_n(tp, l);
             double u = 0.0;
             for (int i = threadIdx.x; i < n; i += NT) {
-                const double g = wp.G[(o + i) * wp.ldG + Pg];
+                const double g = wp.G[(o - wp.G_base + i) * wp.ldG + Pg];
                 u += g * g;
             }
             u = cta_sum(u, red);
@@ -598,7 +599,8 @@ k_wide_group(TreeParams tp, WideParams wp, long long g_first, long long g_count,
         }
         const long long o = tp.leaf_off[t * J];
         const int ng = (int)(tp.leaf_off[t * J + J] - o);
-        group_tail(tp, m, t, wp.G + o * wp.ldG, wp.ldG, ng, dsum, out, out_first, q, A, L.ldA, F, Li, cp, smem);
+        group_tail(tp, m, t, wp.G + (o - wp.G_base) * wp.ldG, wp.ldG, ng, dsum, out, out_first, q, A, L.ldA, F, Li, cp,
+                   smem);
     }
 }
 

@@ -18,12 +18,15 @@ ap.add_argument("--n", type=int, default=None)
 ap.add_argument("--evals", type=int, default=1)
 ap.add_argument("--M", type=int, default=None)
 ap.add_argument("--lib", default=None)
+ap.add_argument("--wide", type=int, default=0)
+ap.add_argument("--budget", type=float, default=0.0)
 a = ap.parse_args()
 if a.lib:
     mra.load_library(a.lib)
 w = synth.make(a.config, n=a.n, device="cuda")
 M = a.M or w.M
-plan = mra.mra_plan_create(w.x, w.y, M, w.J, w.r, stream=torch.cuda.current_stream())
+plan = mra.mra_plan_create(w.x, w.y, M, w.J, w.r, stream=torch.cuda.current_stream(), wide=a.wide,
+                           mem_budget_gb=a.budget)
 zd = torch.from_numpy(w.z).cuda()
 for i in range(a.evals):
     t = time.time()
