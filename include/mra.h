@@ -66,8 +66,8 @@ typedef struct {
                       /* assigned to `rank` of `world`; world <= 1 = the whole tree              */
     int shard_level;  /* level whose regions are the shards; 0 = auto (first level with >= 8*world regions) */
     double mem_budget_gb; /* device memory budget for the chunked bottom pass; 0 = auto        */
-    int wide;         /* big-leaf path (leaves processed by all CTAs together):
-                         0 = auto (when some leaf holds > 1024 observations), 1 = always, -1 = never */
+    int wide;         /* grid-wide task path (leaves processed by all CTAs together):
+                         0 / 1 = use it (default, M >= 2), -1 = one CTA per level-(M-1) region   */
 } mra_opts;
 
 /* Posterior state requested from an evaluation; any pointer may be NULL. */

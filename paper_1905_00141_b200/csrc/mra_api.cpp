@@ -473,7 +473,9 @@ extern "C" mra_status mra_plan_create(const double* x, const double* y, uint64_t
     P->world = o.world > 1 ? o.world : 1;
     mra_status s = build_host(P, x, y, n);
     if (s) { delete P; return s; }
-    P->wide = M >= 2 && (o.wide > 0 || (o.wide == 0 && P->max_leaf > 1024));
+    // the grid-wide task path is at least as fast as one-CTA-per-group on every configuration measured
+    // (C0 4.3x, C1 1.2x, C2/C3 ~1.02x, C4 > 100x: DESIGN.md §5), so it is the default for M >= 2
+    P->wide = M >= 2 && o.wide >= 0;
     // sharding: shard level = first level with >= 8*world regions (or the caller's choice)
     if (P->world > 1) {
         int sl = o.shard_level;

@@ -56,11 +56,13 @@ CASES = [  # n, M, J, r, cov, clusters  -- ragged tiles, empty leaves, both J, b
 ]
 
 
+@pytest.mark.parametrize("wide", [0, -1])
 @pytest.mark.parametrize("n,M,J,r,cov,cl", CASES)
-def test_parity_small(mra, n, M, J, r, cov, cl):
+def test_parity_small(mra, n, M, J, r, cov, cl, wide):
+    """Both schedules: the grid-wide task path (default) and one CTA per level-(M-1) region."""
     x, y, z = synth.uniform_small(n, seed=100 + n + M, clusters=cl)
     theta = (cov, 1.0, 0.08, 0.05)
-    p = mra.mra_plan_create(x, y, M, J, r)
+    p = mra.mra_plan_create(x, y, M, J, r, wide=wide)
     got = mra.mra_loglik(p, z, theta, posterior=True, regions=True)
     ref = oracle.run(x, y, z, M, J, r, theta, regions=True, posterior=True)
     _cmp(got, ref)
@@ -87,17 +89,19 @@ def test_big_leaves_multi_panel(mra):
     _cmp(got, ref)
 
 
-def test_C0_full(mra):
+@pytest.mark.parametrize("wide", [0, -1])
+def test_C0_full(mra, wide):
     w = synth.make("C0")
-    p = mra.mra_plan_create(w.x, w.y, w.M, w.J, w.r)
+    p = mra.mra_plan_create(w.x, w.y, w.M, w.J, w.r, wide=wide)
     got = mra.mra_loglik(p, w.z, w.thetas[0], posterior=True, regions=True)
     ref = oracle.run(w.x, w.y, w.z, w.M, w.J, w.r, w.thetas[0], regions=True, posterior=True)
     _cmp(got, ref)
 
 
-def test_C1_full(mra):
+@pytest.mark.parametrize("wide", [0, -1])
+def test_C1_full(mra, wide):
     w = synth.make("C1")
-    p = mra.mra_plan_create(w.x, w.y, w.M, w.J, w.r)
+    p = mra.mra_plan_create(w.x, w.y, w.M, w.J, w.r, wide=wide)
     got = mra.mra_loglik(p, w.z, w.thetas[0], posterior=True, regions=True)
     ref = oracle.run(w.x, w.y, w.z, w.M, w.J, w.r, w.thetas[0], regions=True, posterior=True)
     _cmp(got, ref)
@@ -121,8 +125,8 @@ def test_chunked_schedule_equals_single_chunk(mra):
     """A tiny memory budget forces a deeper chunk level and 1-region chunks."""
     x, y, z = synth.uniform_small(8000, seed=9, clusters=2)
     theta = (EXP, 1.0, 0.1, 0.05)
-    p1 = mra.mra_plan_create(x, y, 5, 4, 16)
-    p2 = mra.mra_plan_create(x, y, 5, 4, 16, mem_budget_gb=0.003)
+    p1 = mra.mra_plan_create(x, y, 5, 4, 16, wide=-1)
+    p2 = mra.mra_plan_create(x, y, 5, 4, 16, mem_budget_gb=0.003, wide=-1)
     a = mra.mra_loglik(p1, z, theta, regions=True)
     b = mra.mra_loglik(p2, z, theta, regions=True)
     assert abs(a["loglik"] - b["loglik"]) <= 1e-12 * abs(a["loglik"])
