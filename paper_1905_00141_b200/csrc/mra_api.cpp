@@ -86,6 +86,7 @@ struct mra_plan {
     long long *wS_off = nullptr, *wD_off = nullptr;
     int* wS_ld = nullptr;
     int wldG = 0;
+    SyrkRing ring{};
     // live per-kernel timing (CUDA events on the plan stream around every launch)
     bool prof = false;
     std::vector<cudaEvent_t> evpool;
@@ -441,6 +442,22 @@ static mra_status size_wide(mra_plan* P, double budget, bool explicit_budget) {
     if ((s = dalloc(P, (void**)&P->wD_off, 8 * P->nleaf, "wide D_off"))) return s;
     if ((s = dalloc(P, (void**)&P->wS_ld, 4 * P->nleaf, "wide S_ld"))) return s;
     if ((s = dalloc(P, (void**)&P->wtasks, sizeof(int4) * std::max<size_t>(1, tasks.size()), "wide tasks"))) return s;
+    // Atilde slot ring of the tile-parallel SYRK: enough slots for the groups the persistent grid
+    // can have in flight (grid / tiles-per-group + the merging ones), capped by the largest sub-chunk
+    {
+        long long maxgc = 1;
+        for (auto& w : P->wsubs) maxgc = std::max(maxgc, w.gcount);
+        const long long ntile = (long long)nct * (nct + 1) / 2;
+        // a group's merge (last-arriving CTA, ~0.3 ms) holds its slot while the grid moves on through
+        // ~0.1 groups per microsecond: 64 slots keep the ring from throttling the tile tasks
+        long long ns = std::max<long long>(64, 2 * ((P->grid + ntile - 1) / ntile) + 4);
+        ns = std::min<long long>(ns, maxgc);
+        P->ring.ns = (int)ns;
+        P->ring.stride = round_up((long long)ncol * P->L.ldA, 32);
+        if ((s = dalloc(P, (void**)&P->ring.A, 8 * P->ring.stride * ns, "syrk ring"))) return s;
+        if ((s = dalloc(P, (void**)&P->ring.done, 4 * maxgc, "syrk done"))) return s;
+        if ((s = dalloc(P, (void**)&P->ring.slot_done, 8 * ns, "syrk slots"))) return s;
+    }
     CU(cudaMemcpy(P->wS_off, S_off.data(), 8 * P->nleaf, cudaMemcpyHostToDevice));
     CU(cudaMemcpy(P->wD_off, D_off.data(), 8 * P->nleaf, cudaMemcpyHostToDevice));
     CU(cudaMemcpy(P->wS_ld, S_ld.data(), 4 * P->nleaf, cudaMemcpyHostToDevice));
@@ -705,8 +722,8 @@ static mra_status eval_wide(mra_plan* P, const TreeParams& tp, long long gf, lon
             LCHK_K(KIND_BOTTOM, launch_wide(4, tp, wp, (int)s2, P->wtasks + w.pf_off[s2], w.pf_n[s2], P->grid,
                                             take_counter(P), st));
         }
-        LCHK_K(KIND_BOTTOM, launch_wide_group(tp, wp, w.g0, w.gcount, gout, gout_first, q, P->grid, P->ws, P->L,
-                                              take_counter(P), st));
+        LCHK_K(KIND_BOTTOM, launch_wide_syrk(tp, wp, w.g0, w.gcount, gout, gout_first, q, P->grid, P->ws, P->L,
+                                             take_counter(P), P->ring, st));
         done += w.gcount;
     }
     return MRA_OK;

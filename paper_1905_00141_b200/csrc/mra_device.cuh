@@ -21,18 +21,22 @@ namespace mra {
 constexpr int NT = 256;         // threads per CTA (8 warps)
 constexpr int TM = 64;          // output tile rows
 constexpr int TN = 64;          // output tile cols
-constexpr int TK = 32;          // K per smem stage
-constexpr int LDN = 36;         // smem ld of a [row][k] tile (== 4 mod 16 -> conflict-free frags)
+#ifndef MRA_TK
+#define MRA_TK 32
+#endif
+constexpr int TK = MRA_TK;      // K per smem stage
+constexpr int LDN = TK + 4;     // smem ld of a [row][k] tile (== 4 mod 16 -> conflict-free frags)
 constexpr int LDT = 68;         // smem ld of a [k][row] tile (== 4 mod 16)
-constexpr int TILE_DBL = 2304;  // max(64*36, 32*68) doubles per operand tile
+constexpr int TILE_DBL = (64 * LDN > TK * LDT) ? 64 * LDN : TK * LDT;   // doubles per operand tile
 constexpr int LDB = 65;         // smem ld of a 64x64 factor block
 
 enum Kind { MEMN = 0, MEMT = 1, COVK = 2 };
 
-// covariance parameters (exponential / Matern-3/2), planar Euclidean distance
+// covariance parameters (exponential / Matern-3/2), planar Euclidean distance; ir = 1/rho
+// (exponential) or sqrt(3)/rho (Matern-3/2), precomputed so the per-entry path has no division
 struct CovP {
     int kind;
-    double s2, rho, xs, ys;
+    double s2, rho, xs, ys, ir;
 };
 
 // one logical operand of size rows x K (points are interleaved (x, y) pairs):
@@ -72,12 +76,34 @@ __device__ __forceinline__ double2 ldpt(const double* pts, int i) {
     return reinterpret_cast<const double2*>(pts)[i];
 }
 
+// e^{-x} for x >= 0 with a short dependency chain (fp64 latency, not throughput, bounds the fused
+// covariance generation: libm exp is ~204 dependent cycles on B200, tools/bench_fp64ops.cu):
+// x = k ln2 + r, |r| <= ln2/2, e^{-r} by its degree-12 Taylor polynomial in Estrin form (truncation
+// < 2e-16 relative), 2^{-k} by exponent construction. Max error 2.1 ulp over [0, 708) (checked
+// against libm on 2e7 points); e^{-x} < 1e-307 is flushed to 0.
+__device__ __forceinline__ double exp_neg(double x) {
+    if (!(x < 708.0)) return 0.0;
+    const double L2E = 1.4426950408889634074, LN2_HI = 6.93147180369123816490e-01,
+                 LN2_LO = 1.90821492927058770002e-10, MAGIC = 6755399441055744.0;
+    const double kd = __dadd_rn(__dmul_rn(x, L2E), MAGIC) - MAGIC;   // rint(x log2 e)
+    double r = fma(-kd, LN2_HI, x);
+    r = fma(-kd, LN2_LO, r);
+    const double s = -r, s2 = s * s, s4 = s2 * s2, s8 = s4 * s4;
+    const double p01 = 1.0 + s, p23 = fma(1.0 / 6, s, 0.5), p45 = fma(1.0 / 120, s, 1.0 / 24),
+                 p67 = fma(1.0 / 5040, s, 1.0 / 720), p89 = fma(1.0 / 362880, s, 1.0 / 40320),
+                 pab = fma(1.0 / 39916800, s, 1.0 / 3628800);
+    const double q0 = fma(p23, s2, p01), q1 = fma(p67, s2, p45), q2 = fma(pab, s2, p89);
+    const double r0 = fma(q1, s4, q0), r1 = fma(1.0 / 479001600, s4, q2);
+    const double p = fma(r1, s8, r0);
+    const int k = (int)kd;
+    return p * __hiloint2double((1023 - k) << 20, 0);
+}
+
 __device__ __forceinline__ double covf(const CovP& c, double x1, double y1, double x2, double y2) {
-    double dx = (x1 - x2) * c.xs, dy = (y1 - y2) * c.ys;
-    double d = sqrt(dx * dx + dy * dy);
-    if (c.kind == 0) return c.s2 * exp(-d / c.rho);
-    double a = 1.7320508075688772935 * d / c.rho;
-    return c.s2 * (1.0 + a) * exp(-a);
+    const double dx = (x1 - x2) * c.xs, dy = (y1 - y2) * c.ys;
+    const double a = sqrt(dx * dx + dy * dy) * c.ir;
+    const double e = exp_neg(a);
+    return c.kind == 0 ? c.s2 * e : c.s2 * (1.0 + a) * e;
 }
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
@@ -87,7 +113,10 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 }
 
 // ------------------------------------------------------------- async tile staging
-constexpr int NSTAGE = 3;                  // cp.async pipeline depth
+#ifndef MRA_NSTAGE
+#define MRA_NSTAGE 3
+#endif
+constexpr int NSTAGE = MRA_NSTAGE;         // cp.async pipeline depth
 constexpr int STAGE_DBL = 2 * TILE_DBL;    // A tile + B tile
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -119,16 +148,16 @@ __device__ __forceinline__ void load_tile_async(double* s, const Op& op, int r0,
     if (KIND == MEMN) {
         if (al16) {
 #pragma unroll
-            for (int i = 0; i < 4; i++) {
-                const int e = tid + NT * i, row = e >> 4, kk = (e & 15) * 2;
+            for (int i = 0; i < TK / 16; i++) {
+                const int e = tid + NT * i, row = e / (TK / 2), kk = (e % (TK / 2)) * 2;
                 const int ok = (row < nr) ? min(2, max(0, nk - kk)) : 0;
                 const double* g = ok ? op.p + (long long)(r0 + row) * op.ld + k0 + kk : op.p;
                 cp_async16(s + row * LDN + kk, g, ok * 8);
             }
         } else {
 #pragma unroll
-            for (int i = 0; i < 8; i++) {
-                const int e = tid + NT * i, row = e >> 5, kk = e & 31;
+            for (int i = 0; i < TK / 4; i++) {
+                const int e = tid + NT * i, row = e / TK, kk = e % TK;
                 const bool ok = row < nr && kk < nk;
                 cp_async8(s + row * LDN + kk, ok ? op.p + (long long)(r0 + row) * op.ld + k0 + kk : op.p, ok ? 8 : 0);
             }
@@ -136,7 +165,7 @@ __device__ __forceinline__ void load_tile_async(double* s, const Op& op, int r0,
     } else if (KIND == MEMT) {
         if (al16) {
 #pragma unroll
-            for (int i = 0; i < 4; i++) {
+            for (int i = 0; i < TK / 8; i++) {
                 const int e = tid + NT * i, kk = e >> 5, row = (e & 31) * 2;
                 const int ok = (kk < nk) ? min(2, max(0, nr - row)) : 0;
                 const double* g = ok ? op.p + (long long)(k0 + kk) * op.ld + r0 + row : op.p;
@@ -144,19 +173,19 @@ __device__ __forceinline__ void load_tile_async(double* s, const Op& op, int r0,
             }
         } else {
 #pragma unroll
-            for (int i = 0; i < 8; i++) {
+            for (int i = 0; i < TK / 4; i++) {
                 const int e = tid + NT * i, kk = e >> 6, row = e & 63;
                 const bool ok = row < nr && kk < nk;
                 cp_async8(s + kk * LDT + row, ok ? op.p + (long long)(k0 + kk) * op.ld + r0 + row : op.p, ok ? 8 : 0);
             }
         }
     } else {
-        const int kk = tid & 31, rw = tid >> 5;
+        const int kk = tid % TK, rw = tid / TK;
         const bool kok = kk < nk;
         const double2 qk = kok ? ldpt(op.q, k0 + kk) : make_double2(0.0, 0.0);
-#pragma unroll 2
-        for (int i = 0; i < 8; i++) {
-            const int row = rw + 8 * i;
+#pragma unroll 4
+        for (int i = 0; i < TK / 4; i++) {
+            const int row = rw + (NT / TK) * i;
             double v = 0.0;
             if (kok && row < nr) {
                 const double2 pr = ldpt(op.p, r0 + row);
@@ -290,9 +319,9 @@ __device__ __noinline__ void cta_gemm_impl(double* smem) {
                         }
                     }
             if (ci.kind == 2) {
-                // covariance initial value, added by the thread that stored the element (rolled loop:
-                // one copy of the fp64 exp/sqrt sequence instead of sixteen)
-#pragma unroll 1
+                // covariance initial value, added by the thread that stored the element (4 independent
+                // fp64 sqrt/exp chains in flight per thread)
+#pragma unroll 4
                 for (int q = 0; q < 16; q++) {
                     const int mi = q >> 3, ni = (q >> 1) & 3, e = q & 1;
                     const int i = r0 + wr + mi * 8 + g, j = c0 + wc + ni * 8 + 2 * t + e;

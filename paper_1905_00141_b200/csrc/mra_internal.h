@@ -53,6 +53,15 @@ struct WideParams {
     double* lblk;
 };
 
+// ring of Atilde slots of the tile-parallel SYRK (k_wide_syrk)
+struct SyrkRing {
+    double* A;              // ns slots of stride doubles (ncol x ldA each)
+    long long stride;
+    int ns;
+    int* done;              // [groups of the launch] finished tiles
+    long long* slot_done;   // [ns] groups that have released the slot
+};
+
 // launchers (all asynchronous on `st`); return cudaGetLastError()
 cudaError_t launch_gather(const double* z, const long long* perm, double* zs, long long N, cudaStream_t st);
 // region ranges: level-m regions [t_first, t_first + t_count); output buffers are indexed by
@@ -78,6 +87,9 @@ cudaError_t launch_wide(int phase, const TreeParams& tp, const WideParams& wp, i
 cudaError_t launch_wide_group(const TreeParams& tp, const WideParams& wp, long long g_first, long long g_count,
                               double* out, long long out_first, int q, int grid, double* ws, const WsLayout& L,
                               unsigned long long* counter, cudaStream_t st);
+cudaError_t launch_wide_syrk(const TreeParams& tp, const WideParams& wp, long long g_first, long long g_count,
+                             double* out, long long out_first, int q, int grid, double* ws, const WsLayout& L,
+                             unsigned long long* counter, const SyrkRing& ring, cudaStream_t st);
 int smem_bytes();
 void phase_cycles(unsigned long long* out16, bool reset);   // -DMRA_PHASE_TIMING builds only
 

@@ -47,6 +47,7 @@ __device__ __forceinline__ long long lvl_first(int J, int m) {
 __device__ __forceinline__ CovP to_covp(const CovParams& c) {
     CovP p;
     p.kind = c.kind; p.s2 = c.s2; p.rho = c.rho; p.xs = c.xs; p.ys = c.ys;
+    p.ir = (c.kind == 0 ? 1.0 : 1.7320508075688772935) / c.rho;
     return p;
 }
 
@@ -604,6 +605,100 @@ k_wide_group(TreeParams tp, WideParams wp, long long g_first, long long g_count,
     }
 }
 
+// Tile-parallel stacked SYRK with the level-(M-1) merge done by the last-arriving CTA of each group.
+// Tasks are claimed in group-major order (task = (group, lower 64x64 tile of Atilde)), so the CTAs
+// in flight share a handful of groups and their G panels stay L2-resident (the per-CTA SYRK of
+// k_wide_group re-read every panel from HBM: 46 MB of DRAM traffic per C3 group). Atilde tiles go
+// to a ring of NS group slots; a group's slot is reused only after the merge of the group NS
+// earlier has completed (slot_done), which every waiting CTA can rely on because tasks are claimed
+// in order by co-resident CTAs (the persistent grid never exceeds residency).
+__global__ void __launch_bounds__(NT, MRA_MINB)
+k_wide_syrk(TreeParams tp, WideParams wp, long long g_first, long long g_count, double* out, long long out_first,
+            int q, double* ws, WsLayout L, unsigned long long* counter, SyrkRing ring) {
+    extern __shared__ double smem[];
+    const CovP cp = to_covp(tp.cp);
+    const int M = tp.M, J = tp.J, m = M - 1, Pg = m * tp.rh, ncol = Pg + 1;
+    const int nt = (ncol + 63) / 64, ntile = nt * (nt + 1) / 2;
+    double* base = ws + (long long)blockIdx.x * L.stride;
+    double *F = base + L.oF, *Li = base + L.oL;
+    FacSmem f = fac_smem(smem);
+    double* red = misc_smem(smem);
+    int* flag = reinterpret_cast<int*>(misc_smem(smem) + 17);
+    const long long leaf_id0 = lvl_first(J, M);
+    const long long ntask = g_count * ntile;
+    for (;;) {
+        const long long it = next_item(counter, smem);
+        if (it >= ntask) break;
+        const long long gi = it / ntile;
+        int tix = (int)(it - gi * ntile), a = 0;
+        while (tix > a) { tix -= a + 1; a++; }   // lower tile (a, b = tix), row-major over a
+        const int b = tix;
+        const long long g = g_first + gi;
+        const int slot = (int)(gi % ring.ns);
+        double* A = ring.A + (long long)slot * ring.stride;
+        if (gi >= ring.ns) {   // wait until the group NS earlier released this slot
+            if (threadIdx.x == 0) {
+                const long long need = gi / ring.ns;
+                while (*(volatile long long*)(ring.slot_done + slot) < need) __nanosleep(200);
+                __threadfence();
+            }
+            __syncthreads();
+        }
+        const long long o = tp.leaf_off[g * J];
+        const int ng = (int)(tp.leaf_off[g * J + J] - o);
+        const double* G = wp.G + (o - wp.G_base) * wp.ldG;
+        cta_gemm<MEMT, MEMT, MEMN, MEMN>(min(64, ncol - 64 * a), min(64, ncol - 64 * b), a == b,
+                                         op_mem(G + 64 * a, wp.ldG), op_mem(G + 64 * b, wp.ldG), ng, op_mem(G, 0),
+                                         op_mem(G, 0), 0, ci_zero(), 1.0, A + 64LL * a * L.ldA + 64 * b, L.ldA, cp,
+                                         smem);
+        // publish the tile; the CTA that completes the group's last tile performs the merge
+        if (threadIdx.x == 0) {
+            __threadfence();
+            const int old = atomicAdd(ring.done + gi, 1);
+            *flag = (old == ntile - 1);
+            __threadfence();
+        }
+        __syncthreads();
+        if (!*flag) continue;
+        if (threadIdx.x == 0) *f.bad = 0;
+        double dsum = 0.0;
+        for (int c = 0; c < J; c++) {
+            const long long l = g * J + c;
+            const long long ol = tp.leaf_off[l];
+            const int n = leaf_n(tp, l);
+            double u = 0.0;
+            for (int i = threadIdx.x; i < n; i += NT) {
+                const double gv = wp.G[(ol - wp.G_base + i) * wp.ldG + Pg];
+                u += gv * gv;
+            }
+            u = cta_sum(u, red);
+            if (threadIdx.x == 0) {
+                double d = 0.0;
+                for (int bb = 0; bb < (n + 63) / 64; bb++) d += wp.lblk[wp.D_off[l] / 4096 + bb];
+                tp.dreg[leaf_id0 + l] = d;
+                tp.ureg[leaf_id0 + l] = u;
+                red[9] = d;
+            }
+            __syncthreads();
+            dsum += red[9];
+            __syncthreads();
+        }
+        double* O = out + (g - out_first) * (long long)q * q;
+        const double ldm = merge_core(A, tp.rh, L.ldA, O, q, F, Li, tp.err, m, g, cp, smem);
+        const long long id = lvl_first(J, m) + g;
+        if (threadIdx.x == 0) {
+            tp.dreg[id] = dsum + ldm;
+            tp.ureg[id] = O[(long long)(q - 1) * q + q - 1];
+        }
+        save_post(tp, m, g, q, Li, F);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd((unsigned long long*)(ring.slot_done + slot), 1ULL);
+        }
+    }
+}
+
 // ------------------------------------------------------------------------ launchers
 int smem_bytes() { return SMEM_DBL * (int)sizeof(double); }
 
@@ -616,18 +711,18 @@ void phase_cycles(unsigned long long* out16, bool reset) {
 }
 
 static bool g_attr_done = false;
-static int g_resident[10] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 1};   // resident CTAs per SM x SM count
+static int g_resident[11] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1};   // resident CTAs per SM x SM count
 static void set_attrs() {
     if (g_attr_done) return;
     const int b = smem_bytes();
-    const void* ks[10] = {(const void*)k_prior,      (const void*)k_bottom,      (const void*)k_merge,
+    const void* ks[11] = {(const void*)k_prior,      (const void*)k_bottom,      (const void*)k_merge,
                           (const void*)k_smooth,     (const void*)k_wide_chain,  (const void*)k_wide_sigma,
                           (const void*)k_wide_update, (const void*)k_wide_diag,  (const void*)k_wide_panel_fwd,
-                          (const void*)k_wide_group};
+                          (const void*)k_wide_group, (const void*)k_wide_syrk};
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    for (int i = 0; i < 10; i++) {
+    for (int i = 0; i < 11; i++) {
         cudaFuncSetAttribute(ks[i], cudaFuncAttributeMaxDynamicSharedMemorySize, b);
         int per = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ks[i], NT, b);
@@ -728,6 +823,22 @@ cudaError_t launch_wide_group(const TreeParams& tp, const WideParams& wp, long l
     grid = clamp_grid(grid, g_count, 9);
     if (grid < 1) return cudaSuccess;
     k_wide_group<<<grid, NT, smem_bytes(), st>>>(tp, wp, g_first, g_count, out, out_first, q, ws, L, counter);
+    return cudaGetLastError();
+}
+}  // namespace mra
+
+namespace mra {
+cudaError_t launch_wide_syrk(const TreeParams& tp, const WideParams& wp, long long g_first, long long g_count,
+                             double* out, long long out_first, int q, int grid, double* ws, const WsLayout& L,
+                             unsigned long long* counter, const SyrkRing& ring, cudaStream_t st) {
+    set_attrs();
+    const int ncol = (tp.M - 1) * tp.rh + 1, nt = (ncol + 63) / 64;
+    grid = clamp_grid(grid, g_count * (long long)(nt * (nt + 1) / 2), 10);
+    if (grid < 1) return cudaSuccess;
+    cudaError_t e = cudaMemsetAsync(ring.done, 0, sizeof(int) * g_count, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ring.slot_done, 0, sizeof(long long) * ring.ns, st);
+    if (e != cudaSuccess) return e;
+    k_wide_syrk<<<grid, NT, smem_bytes(), st>>>(tp, wp, g_first, g_count, out, out_first, q, ws, L, counter, ring);
     return cudaGetLastError();
 }
 }  // namespace mra
