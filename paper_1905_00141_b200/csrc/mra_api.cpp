@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -78,6 +79,7 @@ struct mra_plan {
         long long g0 = 0, gcount = 0;
         long long chain_off = 0, chain_n = 0, sigma_off = 0, sigma_n = 0;
         std::vector<long long> upd_off, upd_n, diag_off, diag_n, pf_off, pf_n;
+        long long trsm_off = 0, trsm_n = 0, mt_off = 0, mt_n = 0;
     };
     std::vector<WideSub> wsubs;
     size_t wsub_next = 0;
@@ -86,7 +88,7 @@ struct mra_plan {
     long long *wS_off = nullptr, *wD_off = nullptr;
     int* wS_ld = nullptr;
     int wldG = 0;
-    SyrkRing ring{};
+    MergeRing mring{};
     // live per-kernel timing (CUDA events on the plan stream around every launch)
     bool prof = false;
     std::vector<cudaEvent_t> evpool;
@@ -353,7 +355,9 @@ static mra_status size_device(mra_plan* P, double budget_gb) {
 // budget, and precompute each sub-chunk's task lists (int4 {leaf, i, k, 0}).
 static mra_status size_wide(mra_plan* P, double budget, bool explicit_budget) {
     const int M = P->M, J = P->J, rh = P->rh, mg = M - 1;
-    const int ncol = mg * rh + 1, nct = (ncol + 63) / 64;
+    const int Pg = mg * rh, ncol = Pg + 1, nct = (ncol + 63) / 64;
+    const int qm = Pg - rh + 1, nrm = (qm + 63) / 64;   // merge tiles: q = |r| rows/cols of the merge output
+    long long mt_D2 = 0;
     P->wldG = (int)round_up(ncol, 2);
     mra_status s;
     const double cap = std::max(budget * 0.8, explicit_budget ? 1e6 : 2e9);
@@ -361,6 +365,9 @@ static mra_status size_wide(mra_plan* P, double budget, bool explicit_budget) {
     auto leaf_n = [&](long long l) { return P->leaf_off[l + 1] - P->leaf_off[l]; };
     auto leaf_S = [&](long long l) { long long n = leaf_n(l); return n * round_up(std::max<long long>(n, 1), 2); };
     auto leaf_D = [&](long long l) { return ((leaf_n(l) + 63) / 64) * 4096LL; };
+    // G = L^{-1}[V | y] through the explicit inverse X (one launch, no per-step solves) when forming X
+    // (~n^3/3) costs at most about the solve itself (n^2 ncol / 2); blocked substitution otherwise
+    auto xmode = [&](long long l) { return leaf_n(l) <= ncol; };
     std::vector<int4> tasks;
     std::vector<long long> S_off(P->nleaf, 0), D_off(P->nleaf, 0);
     std::vector<int> S_ld(P->nleaf, 2);
@@ -421,14 +428,49 @@ static mra_status size_wide(mra_plan* P, double budget, bool explicit_budget) {
                     for (long long l = ws.g0 * J; l < (ws.g0 + ws.gcount) * J; l++)
                         if ((leaf_n(l) + 63) / 64 > st) tasks.push_back(make_int4((int)l, 0, 0, 0));
                     ws.diag_n.push_back((long long)tasks.size() - ws.diag_off.back());
+                    // after the diagonal of step st: panel tasks L_is (i > st) and the tasks of row block
+                    // st of X = L^{-1} (X_{st,k}, k < st)
                     ws.pf_off.push_back((long long)tasks.size());
                     for (long long l = ws.g0 * J; l < (ws.g0 + ws.gcount) * J; l++) {
                         const int T = (int)((leaf_n(l) + 63) / 64);
                         if (T <= st) continue;
                         for (int i = st + 1; i < T; i++) tasks.push_back(make_int4((int)l, i, 0, 0));
-                        for (int c2 = 0; c2 < nct; c2++) tasks.push_back(make_int4((int)l, c2, 1, 0));
+                        if (xmode(l))
+                            for (int k = 0; k < st; k++) tasks.push_back(make_int4((int)l, k, 2, 0));
+                        else
+                            for (int c2 = 0; c2 < nct; c2++) tasks.push_back(make_int4((int)l, c2, 1, 0));
                     }
                     ws.pf_n.push_back((long long)tasks.size() - ws.pf_off.back());
+                }
+                // G = X [V | y], one task per (leaf, column tile) after the factorization
+                ws.trsm_off = (long long)tasks.size();
+                for (long long l = ws.g0 * J; l < (ws.g0 + ws.gcount) * J; l++)
+                    if (leaf_n(l) > 0 && xmode(l))
+                        for (int c2 = 0; c2 < nct; c2++) tasks.push_back(make_int4((int)l, c2, 1, 0));
+                ws.trsm_n = (long long)tasks.size() - ws.trsm_off;
+                // merge tile dataflow: step s holds T00 of group s, the F tasks of group s - D1 and the
+                // O tasks of group s - D2; D1 covers ~150 us of T00 latency (GEMM + 64x64
+                // factor) at the estimated step time
+                {
+                    const long long gc = ws.gcount;
+                    const double kavg = (double)(P->leaf_off[(ws.g0 + gc) * J] - P->leaf_off[ws.g0 * J]) / gc;
+                    const double step_us = (1.0 + nrm + nrm * (nrm + 1) / 2.0) * std::max(kavg, 64.0) * 0.066 /
+                                           std::max(1, P->grid);
+                    const long long D1 = std::min<long long>(512, std::max<long long>(2, (long long)std::ceil(150.0 / step_us)));
+                    const long long D2 = D1 + 2;
+                    mt_D2 = std::max(mt_D2, D2);
+                    ws.mt_off = (long long)tasks.size();
+                    for (long long st = 0; st < gc + D2; st++) {
+                        if (st < gc) tasks.push_back(make_int4((int)st, 0, 0, 0));
+                        const long long gf = st - D1;
+                        if (gf >= 0 && gf < gc)
+                            for (int a = 0; a < nrm; a++) tasks.push_back(make_int4((int)gf, 1, a, 0));
+                        const long long go = st - D2;
+                        if (go >= 0 && go < gc)
+                            for (int a = 0; a < nrm; a++)
+                                for (int b = 0; b <= a; b++) tasks.push_back(make_int4((int)go, 2, a, b));
+                    }
+                    ws.mt_n = (long long)tasks.size() - ws.mt_off;
                 }
                 P->wsubs.push_back(std::move(ws));
             }
@@ -442,21 +484,20 @@ static mra_status size_wide(mra_plan* P, double budget, bool explicit_budget) {
     if ((s = dalloc(P, (void**)&P->wD_off, 8 * P->nleaf, "wide D_off"))) return s;
     if ((s = dalloc(P, (void**)&P->wS_ld, 4 * P->nleaf, "wide S_ld"))) return s;
     if ((s = dalloc(P, (void**)&P->wtasks, sizeof(int4) * std::max<size_t>(1, tasks.size()), "wide tasks"))) return s;
-    // Atilde slot ring of the tile-parallel SYRK: enough slots for the groups the persistent grid
-    // can have in flight (grid / tiles-per-group + the merging ones), capped by the largest sub-chunk
+    // small-slot ring + counters of the merge tile dataflow
     {
         long long maxgc = 1;
         for (auto& w : P->wsubs) maxgc = std::max(maxgc, w.gcount);
-        const long long ntile = (long long)nct * (nct + 1) / 2;
-        // a group's merge (last-arriving CTA, ~0.3 ms) holds its slot while the grid moves on through
-        // ~0.1 groups per microsecond: 64 slots keep the ring from throttling the tile tasks
-        long long ns = std::max<long long>(64, 2 * ((P->grid + ntile - 1) / ntile) + 4);
-        ns = std::min<long long>(ns, maxgc);
-        P->ring.ns = (int)ns;
-        P->ring.stride = round_up((long long)ncol * P->L.ldA, 32);
-        if ((s = dalloc(P, (void**)&P->ring.A, 8 * P->ring.stride * ns, "syrk ring"))) return s;
-        if ((s = dalloc(P, (void**)&P->ring.done, 4 * maxgc, "syrk done"))) return s;
-        if ((s = dalloc(P, (void**)&P->ring.slot_done, 8 * ns, "syrk slots"))) return s;
+        long long ns = std::min<long long>(maxgc, mt_D2 + 8);
+        P->mring.ns = (int)ns;
+        P->mring.maxg = maxgc;
+        P->mring.stride = round_up(4096 + (long long)rh * rh + (long long)qm * rh, 32);
+        if ((s = dalloc(P, (void**)&P->mring.slot, 8 * P->mring.stride * ns, "merge slots"))) return s;
+        if ((s = dalloc(P, (void**)&P->mring.flags, 4 * 3 * maxgc, "merge flags"))) return s;
+        P->mring.chol_done = P->mring.flags;
+        P->mring.f_done = P->mring.flags + maxgc;
+        P->mring.o_done = P->mring.flags + 2 * maxgc;
+        if ((s = dalloc(P, (void**)&P->mring.slot_done, 8 * ns, "merge slot_done"))) return s;
     }
     CU(cudaMemcpy(P->wS_off, S_off.data(), 8 * P->nleaf, cudaMemcpyHostToDevice));
     CU(cudaMemcpy(P->wD_off, D_off.data(), 8 * P->nleaf, cudaMemcpyHostToDevice));
@@ -722,8 +763,10 @@ static mra_status eval_wide(mra_plan* P, const TreeParams& tp, long long gf, lon
             LCHK_K(KIND_BOTTOM, launch_wide(4, tp, wp, (int)s2, P->wtasks + w.pf_off[s2], w.pf_n[s2], P->grid,
                                             take_counter(P), st));
         }
-        LCHK_K(KIND_BOTTOM, launch_wide_syrk(tp, wp, w.g0, w.gcount, gout, gout_first, q, P->grid, P->ws, P->L,
-                                             take_counter(P), P->ring, st));
+        if (w.trsm_n > 0)
+            LCHK_K(KIND_BOTTOM, launch_wide(5, tp, wp, 0, P->wtasks + w.trsm_off, w.trsm_n, P->grid, take_counter(P), st));
+        LCHK_K(KIND_BOTTOM, launch_wide_mtile(tp, wp, w.g0, w.gcount, gout, gout_first, q, P->wtasks + w.mt_off,
+                                                  w.mt_n, P->grid, take_counter(P), P->mring, st));
         done += w.gcount;
     }
     return MRA_OK;

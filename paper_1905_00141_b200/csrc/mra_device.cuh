@@ -24,6 +24,7 @@ constexpr int TN = 64;          // output tile cols
 #ifndef MRA_TK
 #define MRA_TK 32
 #endif
+static_assert(MRA_TK % 8 == 0 && MRA_TK <= 64, "stage depth");
 constexpr int TK = MRA_TK;      // K per smem stage
 constexpr int LDN = TK + 4;     // smem ld of a [row][k] tile (== 4 mod 16 -> conflict-free frags)
 constexpr int LDT = 68;         // smem ld of a [k][row] tile (== 4 mod 16)
@@ -138,7 +139,7 @@ __device__ __forceinline__ bool op_aligned16(const Op& op) {
     return ((reinterpret_cast<uintptr_t>(op.p) & 15) == 0) && ((op.ld & 1) == 0);
 }
 
-// stage rows [r0, r0+nr) x k [k0, k0+nk) of an operand into smem (zero-padded to 64 x 32).
+// stage rows [r0, r0+nr) x k [k0, k0+nk) of an operand into smem (zero-padded to 64 x TK).
 // Memory operands go through cp.async (16-byte copies when aligned); covariance operands are
 // generated in registers (fused covariance generation) and stored.
 template <int KIND>
@@ -148,7 +149,7 @@ __device__ __forceinline__ void load_tile_async(double* s, const Op& op, int r0,
     if (KIND == MEMN) {
         if (al16) {
 #pragma unroll
-            for (int i = 0; i < TK / 16; i++) {
+            for (int i = 0; i < TK / 8; i++) {   // 64 rows x TK/2 16-byte copies over NT threads
                 const int e = tid + NT * i, row = e / (TK / 2), kk = (e % (TK / 2)) * 2;
                 const int ok = (row < nr) ? min(2, max(0, nk - kk)) : 0;
                 const double* g = ok ? op.p + (long long)(r0 + row) * op.ld + k0 + kk : op.p;

@@ -53,12 +53,14 @@ struct WideParams {
     double* lblk;
 };
 
-// ring of Atilde slots of the tile-parallel SYRK (k_wide_syrk)
-struct SyrkRing {
-    double* A;              // ns slots of stride doubles (ncol x ldA each)
+// per-group small slots (Li, F) and dependency counters of the level-(M-1) merge tile dataflow
+struct MergeRing {
+    double* slot;           // ns slots of stride doubles: [A_oo 64x64 | Li rh x rh | F q x rh]
     long long stride;
     int ns;
-    int* done;              // [groups of the launch] finished tiles
+    long long maxg;         // groups per launch (counter arrays)
+    int* flags;             // [3 * maxg]: chol_done | f_done | o_done
+    int *chol_done, *f_done, *o_done;
     long long* slot_done;   // [ns] groups that have released the slot
 };
 
@@ -81,15 +83,13 @@ cudaError_t launch_smooth(const TreeParams& tp, const double* muhat, const long 
                           int grid, double* ws, const WsLayout& L, unsigned long long* counter,
                           cudaStream_t st);
 cudaError_t launch_fill(double* p, long long n, double v, cudaStream_t st);
-// wide path: phase 0 chain, 1 sigma, 2 column update (step), 3 diagonal (step), 4 panel + fwd (step)
+// wide path: phase 0 chain, 1 sigma, 2 column update (step), 3 diagonal (step), 4 panel + X row (step),
+// 5 G = X [V | y]
 cudaError_t launch_wide(int phase, const TreeParams& tp, const WideParams& wp, int step, const int4* tasks,
                         long long ntask, int grid, unsigned long long* counter, cudaStream_t st);
-cudaError_t launch_wide_group(const TreeParams& tp, const WideParams& wp, long long g_first, long long g_count,
-                              double* out, long long out_first, int q, int grid, double* ws, const WsLayout& L,
-                              unsigned long long* counter, cudaStream_t st);
-cudaError_t launch_wide_syrk(const TreeParams& tp, const WideParams& wp, long long g_first, long long g_count,
-                             double* out, long long out_first, int q, int grid, double* ws, const WsLayout& L,
-                             unsigned long long* counter, const SyrkRing& ring, cudaStream_t st);
+cudaError_t launch_wide_mtile(const TreeParams& tp, const WideParams& wp, long long g_first, long long g_count,
+                              double* out, long long out_first, int q, const int4* tasks, long long ntask, int grid,
+                              unsigned long long* counter, const MergeRing& ring, cudaStream_t st);
 int smem_bytes();
 void phase_cycles(unsigned long long* out16, bool reset);   // -DMRA_PHASE_TIMING builds only
 

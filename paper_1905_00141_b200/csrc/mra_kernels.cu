@@ -523,13 +523,15 @@ k_wide_diag(TreeParams tp, WideParams wp, int s, const int4* tasks, long long nt
     }
 }
 
-// step s, after the diagonal: panel tasks (leaf, i > s, k = 0): L_is = A_is D_s^T, and forward
-// substitution tasks (leaf, col tile c, k = 1): G_s[:, c] = D_s (G_s[:, c] - L_{s,<s} G_{<s}[:, c])
+// step s, after the diagonal: panel tasks (leaf, i > s, 0): L_is = A_is D_s^T; for small leaves
+// (n <= ncol) the tasks of row block s of X = L^{-1} (leaf, k < s, 2): X_sk = -D_s sum_{k<=j<s} L_sj X_jk,
+// for large leaves the forward-substitution tasks of row block s (leaf, column tile, 1). X's off-diagonal blocks are
+// kept TRANSPOSED in the (otherwise unused) upper triangle of the leaf's Sigma buffer: X[a][b] (block
+// a > block b) at S[b * ld + a]; its diagonal blocks are the inverted D_s.
 __global__ void __launch_bounds__(NT, MRA_MINB)
-k_wide_panel_fwd(TreeParams tp, WideParams wp, int s, const int4* tasks, long long ntask, unsigned long long* counter) {
+k_wide_panel_x(TreeParams tp, WideParams wp, int s, const int4* tasks, long long ntask, unsigned long long* counter) {
     extern __shared__ double smem[];
     const CovP cp = to_covp(tp.cp);
-    const int ncol = (tp.M - 1) * tp.rh + 1;
     for (;;) {
         const long long it = next_item(counter, smem);
         if (it >= ntask) break;
@@ -543,158 +545,188 @@ k_wide_panel_fwd(TreeParams tp, WideParams wp, int s, const int4* tasks, long lo
             double* P = Sl + 64LL * i * ld + 64LL * s;
             cta_gemm<MEMN, MEMN, MEMN, MEMN>(min(64, n - 64 * i), nb, 0, op_mem(P, ld), op_mem(Ds, 64), nb,
                                              op_mem(P, 0), op_mem(P, 0), 0, ci_zero(), 1.0, P, ld, cp, smem);
-        } else {
-            const int c = tk.y;
+        } else if (tk.z == 1) {
+            // large leaves (n > ncol): blocked forward substitution G_s[:, c] = D_s (G_s - L_{s,<s} G_{<s})
+            // interleaved with the factorization (X = L^{-1} would cost n^3/3 > the solve itself)
+            const int c = tk.y, ncol = (tp.M - 1) * tp.rh + 1;
             const long long o = tp.leaf_off[l];
             double* Gs = wp.G + (o - wp.G_base + 64LL * s) * wp.ldG + 64LL * c;
             const int nc = min(64, ncol - 64 * c);
             if (s > 0)
                 cta_gemm<MEMN, MEMT, MEMN, MEMN>(nb, nc, 0, op_mem(Sl + 64LL * s * ld, ld),
                                                  op_mem(wp.G + (o - wp.G_base) * wp.ldG + 64LL * c, wp.ldG), 64 * s,
-                                                 op_mem(Sl, 0),
-                                                 op_mem(Sl, 0), 0, ci_mem(Gs, wp.ldG), -1.0, Gs, wp.ldG, cp, smem);
+                                                 op_mem(Sl, 0), op_mem(Sl, 0), 0, ci_mem(Gs, wp.ldG), -1.0, Gs, wp.ldG,
+                                                 cp, smem);
             cta_gemm<MEMN, MEMT, MEMN, MEMN>(nb, nc, 0, op_mem(Ds, 64), op_mem(Gs, wp.ldG), nb, op_mem(Ds, 0),
                                              op_mem(Ds, 0), 0, ci_zero(), 1.0, Gs, wp.ldG, cp, smem);
+        } else {
+            const int kb = tk.y;
+            const long long k0 = 64LL * kb, s0 = 64LL * s;
+            const double* Dk = wp.D + wp.D_off[l] + 4096LL * kb;
+            double* Yt = Sl + k0 * ld + s0;   // X_sk^T lives here (64 x nb)
+            // Y^T = D_k^T L_sk^T + sum_{k<j<s} X_jk^T L_sj^T
+            cta_gemm<MEMT, MEMN, MEMN, MEMN>(64, nb, 0, op_mem(Dk, 64), op_mem(Sl + s0 * ld + k0, ld), 64,
+                                             op_mem(Sl + k0 * ld + k0 + 64, ld), op_mem(Sl + s0 * ld + k0 + 64, ld),
+                                             (int)(s0 - k0 - 64), ci_zero(), 1.0, Yt, ld, cp, smem);
+            // X_sk^T = -Y^T D_s^T (in place: one output tile, every operand element is read first)
+            cta_gemm<MEMN, MEMN, MEMN, MEMN>(64, nb, 0, op_mem(Yt, ld), op_mem(Ds, 64), nb, op_mem(Yt, 0),
+                                             op_mem(Yt, 0), 0, ci_zero(), -1.0, Yt, ld, cp, smem);
         }
     }
 }
 
-// per group: leaf d_j = sum of block log-dets, u_j = |g_j|^2, then the stacked SYRK + merge
+// G[:, c] = X [V | y][:, c] per (leaf, 64-column tile), row blocks in DESCENDING order so the product
+// can overwrite its input: G_i = [X_{i,<i} | D_i] [B_{<i} ; B_i] only reads rows <= i of B.
 __global__ void __launch_bounds__(NT, MRA_MINB)
-k_wide_group(TreeParams tp, WideParams wp, long long g_first, long long g_count, double* out, long long out_first,
-             int q, double* ws, WsLayout L, unsigned long long* counter) {
+k_wide_trsm(TreeParams tp, WideParams wp, const int4* tasks, long long ntask, unsigned long long* counter) {
     extern __shared__ double smem[];
     const CovP cp = to_covp(tp.cp);
-    const int M = tp.M, J = tp.J, m = M - 1, Pg = m * tp.rh;
-    double* base = ws + (long long)blockIdx.x * L.stride;
-    double *A = base + L.oA, *F = base + L.oF, *Li = base + L.oL;
-    FacSmem f = fac_smem(smem);
-    double* red = misc_smem(smem);
-    const long long leaf_id0 = lvl_first(J, M);
-    for (;;) {
-        const long long it = next_item(counter, smem);
-        if (it >= g_count) break;
-        if (threadIdx.x == 0) *f.bad = 0;
-        const long long t = g_first + it;
-        double dsum = 0.0;
-        for (int c = 0; c < J; c++) {
-            const long long l = t * J + c;
-            const long long o = tp.leaf_off[l];
-            const int n = leaf_n(tp, l);
-            double u = 0.0;
-            for (int i = threadIdx.x; i < n; i += NT) {
-                const double g = wp.G[(o - wp.G_base + i) * wp.ldG + Pg];
-                u += g * g;
-            }
-            u = cta_sum(u, red);
-            double d = 0.0;
-            if (threadIdx.x == 0) {
-                for (int b = 0; b < (n + 63) / 64; b++) d += wp.lblk[wp.D_off[l] / 4096 + b];
-                tp.dreg[leaf_id0 + l] = d;
-                tp.ureg[leaf_id0 + l] = u;
-                red[9] = d;
-            }
-            __syncthreads();
-            dsum += red[9];
-            __syncthreads();
-        }
-        const long long o = tp.leaf_off[t * J];
-        const int ng = (int)(tp.leaf_off[t * J + J] - o);
-        group_tail(tp, m, t, wp.G + (o - wp.G_base) * wp.ldG, wp.ldG, ng, dsum, out, out_first, q, A, L.ldA, F, Li, cp,
-                   smem);
-    }
-}
-
-// Tile-parallel stacked SYRK with the level-(M-1) merge done by the last-arriving CTA of each group.
-// Tasks are claimed in group-major order (task = (group, lower 64x64 tile of Atilde)), so the CTAs
-// in flight share a handful of groups and their G panels stay L2-resident (the per-CTA SYRK of
-// k_wide_group re-read every panel from HBM: 46 MB of DRAM traffic per C3 group). Atilde tiles go
-// to a ring of NS group slots; a group's slot is reused only after the merge of the group NS
-// earlier has completed (slot_done), which every waiting CTA can rely on because tasks are claimed
-// in order by co-resident CTAs (the persistent grid never exceeds residency).
-__global__ void __launch_bounds__(NT, MRA_MINB)
-k_wide_syrk(TreeParams tp, WideParams wp, long long g_first, long long g_count, double* out, long long out_first,
-            int q, double* ws, WsLayout L, unsigned long long* counter, SyrkRing ring) {
-    extern __shared__ double smem[];
-    const CovP cp = to_covp(tp.cp);
-    const int M = tp.M, J = tp.J, m = M - 1, Pg = m * tp.rh, ncol = Pg + 1;
-    const int nt = (ncol + 63) / 64, ntile = nt * (nt + 1) / 2;
-    double* base = ws + (long long)blockIdx.x * L.stride;
-    double *F = base + L.oF, *Li = base + L.oL;
-    FacSmem f = fac_smem(smem);
-    double* red = misc_smem(smem);
-    int* flag = reinterpret_cast<int*>(misc_smem(smem) + 17);
-    const long long leaf_id0 = lvl_first(J, M);
-    const long long ntask = g_count * ntile;
+    const int ncol = (tp.M - 1) * tp.rh + 1;
     for (;;) {
         const long long it = next_item(counter, smem);
         if (it >= ntask) break;
-        const long long gi = it / ntile;
-        int tix = (int)(it - gi * ntile), a = 0;
-        while (tix > a) { tix -= a + 1; a++; }   // lower tile (a, b = tix), row-major over a
-        const int b = tix;
-        const long long g = g_first + gi;
-        const int slot = (int)(gi % ring.ns);
-        double* A = ring.A + (long long)slot * ring.stride;
-        if (gi >= ring.ns) {   // wait until the group NS earlier released this slot
-            if (threadIdx.x == 0) {
-                const long long need = gi / ring.ns;
-                while (*(volatile long long*)(ring.slot_done + slot) < need) __nanosleep(200);
-                __threadfence();
-            }
-            __syncthreads();
+        const int4 tk = tasks[it];
+        const long long l = tk.x;
+        const int n = leaf_n(tp, l), ld = wp.S_ld[l], c0 = 64 * tk.y, nc = min(64, ncol - c0);
+        const double* Sl = wp.S + wp.S_off[l];
+        double* Gl = wp.G + (tp.leaf_off[l] - wp.G_base) * wp.ldG + c0;
+        for (int i = (n - 1) / 64; i >= 0; i--) {
+            const int i0 = 64 * i, nb = min(64, n - i0);
+            const double* Di = wp.D + wp.D_off[l] + 4096LL * i;
+            cta_gemm<MEMT, MEMT, MEMN, MEMT>(nb, nc, 0, op_mem(Sl + i0, ld), op_mem(Gl, wp.ldG), i0, op_mem(Di, 64),
+                                             op_mem(Gl + (long long)i0 * wp.ldG, wp.ldG), nb, ci_zero(), 1.0,
+                                             Gl + (long long)i0 * wp.ldG, wp.ldG, cp, smem);
         }
+    }
+}
+
+// Level-(M-1) stacked SYRK and merge as one dataflow of tile tasks (host-ordered list, int4
+// {group, type, a, b}). With G = [G_o | G_r] (o = the group region's own rh columns, r = the rest incl.
+// the y column; q = |r|):
+//   type 0  T00(g):   A_oo = G_o^T G_o, Lt = chol(I + A_oo), Li = Lt^{-1}, log|I + A_oo|, leaf d/u
+//   type 1  F(g, a):  F_a = (G_r,a^T G_o) Li^T    (waits for T00(g), which owns the slot once it runs)
+//   type 2  O(g,a,b): O_ab = G_r,a^T G_r,b - F_a F_b^T  -> output        (waits for every F(g, .))
+// i.e. Atilde = G^T G and the merge O = A_rr - A_ro (I + A_oo)^{-1} A_or without ever storing A_rr.
+// The host staggers the three task kinds (T00 of group s, F of group s - D1, O of group s - D2) so a
+// dependency is normally complete when its consumer is claimed; waits spin on counters of tasks
+// claimed earlier by co-resident CTAs, so they always terminate. Li and F live in a ring of small
+// per-group slots (reused NS groups later, after the group's last O task).
+__global__ void __launch_bounds__(NT, MRA_MINB)
+k_wide_mtile(TreeParams tp, WideParams wp, long long g_first, double* out, long long out_first, int q,
+             const int4* tasks, long long ntask, unsigned long long* counter, MergeRing ring) {
+    extern __shared__ double smem[];
+    const CovP cp = to_covp(tp.cp);
+    const int M = tp.M, J = tp.J, m = M - 1, rh = tp.rh, Pg = m * rh;
+    const int nr = (q + 63) / 64, nO = nr * (nr + 1) / 2;
+    FacSmem f = fac_smem(smem);
+    double* red = misc_smem(smem);
+    const long long leaf_id0 = lvl_first(J, M);
+    for (;;) {
+        const long long it = next_item(counter, smem);
+        if (it >= ntask) break;
+        const int4 tk = tasks[it];
+        const long long gi = tk.x, g = g_first + gi;
+        const int slot = (int)(gi % ring.ns);
+        double* Aoo = ring.slot + (long long)slot * ring.stride;
+        double* Li = Aoo + 4096;
+        double* F = Li + rh * rh;
         const long long o = tp.leaf_off[g * J];
         const int ng = (int)(tp.leaf_off[g * J + J] - o);
         const double* G = wp.G + (o - wp.G_base) * wp.ldG;
-        cta_gemm<MEMT, MEMT, MEMN, MEMN>(min(64, ncol - 64 * a), min(64, ncol - 64 * b), a == b,
-                                         op_mem(G + 64 * a, wp.ldG), op_mem(G + 64 * b, wp.ldG), ng, op_mem(G, 0),
-                                         op_mem(G, 0), 0, ci_zero(), 1.0, A + 64LL * a * L.ldA + 64 * b, L.ldA, cp,
-                                         smem);
-        // publish the tile; the CTA that completes the group's last tile performs the merge
-        if (threadIdx.x == 0) {
-            __threadfence();
-            const int old = atomicAdd(ring.done + gi, 1);
-            *flag = (old == ntile - 1);
-            __threadfence();
-        }
-        __syncthreads();
-        if (!*flag) continue;
-        if (threadIdx.x == 0) *f.bad = 0;
-        double dsum = 0.0;
-        for (int c = 0; c < J; c++) {
-            const long long l = g * J + c;
-            const long long ol = tp.leaf_off[l];
-            const int n = leaf_n(tp, l);
-            double u = 0.0;
-            for (int i = threadIdx.x; i < n; i += NT) {
-                const double gv = wp.G[(ol - wp.G_base + i) * wp.ldG + Pg];
-                u += gv * gv;
-            }
-            u = cta_sum(u, red);
-            if (threadIdx.x == 0) {
-                double d = 0.0;
-                for (int bb = 0; bb < (n + 63) / 64; bb++) d += wp.lblk[wp.D_off[l] / 4096 + bb];
-                tp.dreg[leaf_id0 + l] = d;
-                tp.ureg[leaf_id0 + l] = u;
-                red[9] = d;
-            }
-            __syncthreads();
-            dsum += red[9];
-            __syncthreads();
-        }
-        double* O = out + (g - out_first) * (long long)q * q;
-        const double ldm = merge_core(A, tp.rh, L.ldA, O, q, F, Li, tp.err, m, g, cp, smem);
         const long long id = lvl_first(J, m) + g;
-        if (threadIdx.x == 0) {
-            tp.dreg[id] = dsum + ldm;
-            tp.ureg[id] = O[(long long)(q - 1) * q + q - 1];
-        }
-        save_post(tp, m, g, q, Li, F);
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            atomicAdd((unsigned long long*)(ring.slot_done + slot), 1ULL);
+        if (tk.y == 0) {
+            if (gi >= ring.ns) {   // the group NS earlier must have released the slot
+                if (threadIdx.x == 0) {
+                    while (*(volatile long long*)(ring.slot_done + slot) < gi / ring.ns) __nanosleep(100);
+                    __threadfence();
+                }
+                __syncthreads();
+            }
+            if (threadIdx.x == 0) *f.bad = 0;
+            double dsum = 0.0;
+            for (int c = 0; c < J; c++) {
+                const long long l = g * J + c;
+                const long long ol = tp.leaf_off[l];
+                const int n = leaf_n(tp, l);
+                double u = 0.0;
+                for (int i = threadIdx.x; i < n; i += NT) {
+                    const double gv = wp.G[(ol - wp.G_base + i) * wp.ldG + Pg];
+                    u += gv * gv;
+                }
+                u = cta_sum(u, red);
+                if (threadIdx.x == 0) {
+                    double d = 0.0;
+                    for (int bb = 0; bb < (n + 63) / 64; bb++) d += wp.lblk[wp.D_off[l] / 4096 + bb];
+                    tp.dreg[leaf_id0 + l] = d;
+                    tp.ureg[leaf_id0 + l] = u;
+                    red[9] = d;
+                }
+                __syncthreads();
+                dsum += red[9];
+                __syncthreads();
+            }
+            cta_gemm<MEMT, MEMT, MEMN, MEMN>(rh, rh, 1, op_mem(G, wp.ldG), op_mem(G, wp.ldG), ng, op_mem(G, 0),
+                                             op_mem(G, 0), 0, ci_zero(), 1.0, Aoo, 64, cp, smem);
+            load_block_lower(f.blk, Aoo, 64, rh, 1.0);
+            const double ldm = chol_inv_small(f.blk, f.inv, rh, f.diagv, f.bad, f.red, f.tmp);
+            if (*f.bad && threadIdx.x == 0) set_err(tp.err, m, g);
+            store_block_full(f.inv, Li, rh, rh);
+            if (tp.post) {
+                double* P = tp.post + tp.post_base[m] + g * ((long long)rh * rh + (long long)q * rh);
+                for (int e = threadIdx.x; e < rh * rh; e += NT) P[e] = f.inv[(e / rh) * LDB + (e % rh)];
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                tp.dreg[id] = dsum + ldm;
+                __threadfence();
+                atomicExch(ring.chol_done + gi, 1);
+            }
+        } else if (tk.y == 1) {
+            const int a = tk.z, r0 = 64 * a, nrow = min(64, q - r0);
+            double* Fa = F + (long long)r0 * rh;
+            // the slot is this group's only after T00 has waited for it (chol_done is set after that)
+            if (threadIdx.x == 0) {
+                while (*(volatile int*)(ring.chol_done + gi) == 0) __nanosleep(100);
+                __threadfence();
+            }
+            __syncthreads();
+            cta_gemm<MEMT, MEMT, MEMN, MEMN>(nrow, rh, 0, op_mem(G + rh + r0, wp.ldG), op_mem(G, wp.ldG), ng,
+                                             op_mem(G, 0), op_mem(G, 0), 0, ci_zero(), 1.0, Fa, rh, cp, smem);
+            cta_gemm<MEMN, MEMN, MEMN, MEMN>(nrow, rh, 0, op_mem(Fa, rh), op_mem(Li, rh), rh, op_mem(Fa, 0),
+                                             op_mem(Fa, 0), 0, ci_zero(), 1.0, Fa, rh, cp, smem);
+            if (tp.post) {
+                double* P = tp.post + tp.post_base[m] + g * ((long long)rh * rh + (long long)q * rh) + rh * rh +
+                            (long long)r0 * rh;
+                for (int e = threadIdx.x; e < nrow * rh; e += NT) P[e] = Fa[e];
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                __threadfence();
+                atomicAdd(ring.f_done + gi, 1);
+            }
+        } else {
+            const int a = tk.z, b = tk.w, r0 = 64 * a, c0 = 64 * b;
+            const int nrow = min(64, q - r0), ncl = min(64, q - c0);
+            double* Oab = out + (g - out_first) * (long long)q * q + (long long)r0 * q + c0;
+            cta_gemm<MEMT, MEMT, MEMN, MEMN>(nrow, ncl, a == b, op_mem(G + rh + r0, wp.ldG),
+                                             op_mem(G + rh + c0, wp.ldG), ng, op_mem(G, 0), op_mem(G, 0), 0,
+                                             ci_zero(), 1.0, Oab, q, cp, smem);
+            if (threadIdx.x == 0) {
+                while (*(volatile int*)(ring.f_done + gi) < nr) __nanosleep(100);
+                __threadfence();
+            }
+            __syncthreads();
+            cta_gemm<MEMN, MEMN, MEMN, MEMN>(nrow, ncl, a == b, op_mem(F + (long long)r0 * rh, rh),
+                                             op_mem(F + (long long)c0 * rh, rh), rh, op_mem(F, 0), op_mem(F, 0), 0,
+                                             ci_mem(Oab, q), -1.0, Oab, q, cp, smem);
+            if (threadIdx.x == 0) {
+                if (a == nr - 1 && b == nr - 1) tp.ureg[id] = Oab[(long long)(nrow - 1) * q + ncl - 1];
+                __threadfence();
+                if (atomicAdd(ring.o_done + gi, 1) == nO - 1) {
+                    __threadfence();
+                    atomicAdd((unsigned long long*)(ring.slot_done + slot), 1ULL);
+                }
+            }
         }
     }
 }
@@ -715,10 +747,10 @@ static int g_resident[11] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1};   // resident CTA
 static void set_attrs() {
     if (g_attr_done) return;
     const int b = smem_bytes();
-    const void* ks[11] = {(const void*)k_prior,      (const void*)k_bottom,      (const void*)k_merge,
-                          (const void*)k_smooth,     (const void*)k_wide_chain,  (const void*)k_wide_sigma,
-                          (const void*)k_wide_update, (const void*)k_wide_diag,  (const void*)k_wide_panel_fwd,
-                          (const void*)k_wide_group, (const void*)k_wide_syrk};
+    const void* ks[11] = {(const void*)k_prior,       (const void*)k_bottom,      (const void*)k_merge,
+                          (const void*)k_smooth,      (const void*)k_wide_chain,  (const void*)k_wide_sigma,
+                          (const void*)k_wide_update, (const void*)k_wide_diag,   (const void*)k_wide_panel_x,
+                          (const void*)k_wide_trsm,   (const void*)k_wide_mtile};
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -803,7 +835,7 @@ namespace mra {
 cudaError_t launch_wide(int phase, const TreeParams& tp, const WideParams& wp, int step, const int4* tasks,
                         long long ntask, int grid, unsigned long long* counter, cudaStream_t st) {
     set_attrs();
-    grid = clamp_grid(grid, ntask, 4 + phase);
+    grid = clamp_grid(grid, ntask, phase == 5 ? 9 : 4 + phase);
     if (grid < 1) return cudaSuccess;
     const int b = smem_bytes();
     switch (phase) {
@@ -811,34 +843,27 @@ cudaError_t launch_wide(int phase, const TreeParams& tp, const WideParams& wp, i
         case 1: k_wide_sigma<<<grid, NT, b, st>>>(tp, wp, tasks, ntask, counter); break;
         case 2: k_wide_update<<<grid, NT, b, st>>>(tp, wp, step, tasks, ntask, counter); break;
         case 3: k_wide_diag<<<grid, NT, b, st>>>(tp, wp, step, tasks, ntask, counter); break;
-        case 4: k_wide_panel_fwd<<<grid, NT, b, st>>>(tp, wp, step, tasks, ntask, counter); break;
+        case 4: k_wide_panel_x<<<grid, NT, b, st>>>(tp, wp, step, tasks, ntask, counter); break;
+        case 5: k_wide_trsm<<<grid, NT, b, st>>>(tp, wp, tasks, ntask, counter); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
 }
-cudaError_t launch_wide_group(const TreeParams& tp, const WideParams& wp, long long g_first, long long g_count,
-                              double* out, long long out_first, int q, int grid, double* ws, const WsLayout& L,
-                              unsigned long long* counter, cudaStream_t st) {
-    set_attrs();
-    grid = clamp_grid(grid, g_count, 9);
-    if (grid < 1) return cudaSuccess;
-    k_wide_group<<<grid, NT, smem_bytes(), st>>>(tp, wp, g_first, g_count, out, out_first, q, ws, L, counter);
-    return cudaGetLastError();
-}
 }  // namespace mra
 
+
 namespace mra {
-cudaError_t launch_wide_syrk(const TreeParams& tp, const WideParams& wp, long long g_first, long long g_count,
-                             double* out, long long out_first, int q, int grid, double* ws, const WsLayout& L,
-                             unsigned long long* counter, const SyrkRing& ring, cudaStream_t st) {
+cudaError_t launch_wide_mtile(const TreeParams& tp, const WideParams& wp, long long g_first, long long g_count,
+                              double* out, long long out_first, int q, const int4* tasks, long long ntask, int grid,
+                              unsigned long long* counter, const MergeRing& ring, cudaStream_t st) {
     set_attrs();
-    const int ncol = (tp.M - 1) * tp.rh + 1, nt = (ncol + 63) / 64;
-    grid = clamp_grid(grid, g_count * (long long)(nt * (nt + 1) / 2), 10);
+    grid = clamp_grid(grid, ntask, 10);
     if (grid < 1) return cudaSuccess;
-    cudaError_t e = cudaMemsetAsync(ring.done, 0, sizeof(int) * g_count, st);
+    cudaError_t e = cudaMemsetAsync(ring.flags, 0, sizeof(int) * 3 * ring.maxg, st);
     if (e == cudaSuccess) e = cudaMemsetAsync(ring.slot_done, 0, sizeof(long long) * ring.ns, st);
     if (e != cudaSuccess) return e;
-    k_wide_syrk<<<grid, NT, smem_bytes(), st>>>(tp, wp, g_first, g_count, out, out_first, q, ws, L, counter, ring);
+    (void)g_count;
+    k_wide_mtile<<<grid, NT, smem_bytes(), st>>>(tp, wp, g_first, out, out_first, q, tasks, ntask, counter, ring);
     return cudaGetLastError();
 }
 }  // namespace mra

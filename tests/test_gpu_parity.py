@@ -53,6 +53,8 @@ CASES = [  # n, M, J, r, cov, clusters  -- ragged tiles, empty leaves, both J, b
     (1200, 2, 4, 25, EXP, 0),
     (2000, 2, 2, 64, EXP, 2),
     (9000, 4, 4, 30, EXP, 5),
+    (12800, 5, 4, 64, EXP, 3),   # leaves 0..~600 around ncol = 257: both G = X[V|y] and blocked-solve leaves
+    (4000, 6, 2, 36, MAT, 2),    # n_leaf <= ncol = 181 mostly: explicit-inverse path, 1-4 row blocks
 ]
 
 

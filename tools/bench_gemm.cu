@@ -24,7 +24,11 @@ __global__ void __launch_bounds__(NT, MRA_MINB) kbench(const double* A, const do
     cp.ir = 0.5;
 #endif
     for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+#ifdef HOT
+        const int pa = (int)(blockIdx.x % 64), pb = (int)(blockIdx.x % 64);   // same panels every tile (L1/L2-hot)
+#else
         const int pa = (int)(t % 64), pb = (int)((t / 64) % 64);
+#endif
         Op a, b;
         if (KA == COVK) a = op_cov(pts + 128 * pa, pts + 128 * ((pa + 7) % 64));
         else if (KA == MEMN) a = op_mem(A + (long long)pa * 64 * K, K);

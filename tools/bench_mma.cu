@@ -1,0 +1,47 @@
+// bench_mma.cu -- ceiling of the CTA GEMM engine's inner loop (mma_ktile on smem-resident tiles) with
+// and without the per-k-tile barrier, vs the register-only DMMA peak. Diagnostic only.
+#include <cstdio>
+#include <cuda_runtime.h>
+#include "../paper_1905_00141_b200/csrc/mra_device.cuh"
+using namespace mra;
+
+template <int KA, int KB, bool SYNC>
+__global__ void __launch_bounds__(NT, 2) kloop(double* out, int iters) {
+    extern __shared__ double smem[];
+    for (int e = threadIdx.x; e < STAGE_DBL; e += NT) smem[e] = 1e-6 * (e & 63);
+    __syncthreads();
+    double acc[2][4][2] = {};
+    for (int it = 0; it < iters; it++) {
+        mma_ktile<KA, KB>(acc, smem, smem + TILE_DBL, TK);
+        if (SYNC) __syncthreads();
+    }
+    double s = 0;
+    for (int mi = 0; mi < 2; mi++) for (int ni = 0; ni < 4; ni++) s += acc[mi][ni][0] + acc[mi][ni][1];
+    if (s == 1234.5) out[0] = s;
+}
+
+template <int KA, int KB, bool SYNC>
+void run(const char* name, double* o) {
+    const int bytes = SMEM_DBL * 8, iters = 4000;
+    cudaFuncSetAttribute(kloop<KA, KB, SYNC>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    for (int per : {1, 2}) {
+        const int grid = 148 * per;
+        kloop<KA, KB, SYNC><<<grid, NT, bytes>>>(o, 10);
+        cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+        cudaEventRecord(e0);
+        kloop<KA, KB, SYNC><<<grid, NT, bytes>>>(o, iters);
+        cudaEventRecord(e1); cudaEventSynchronize(e1);
+        float ms; cudaEventElapsedTime(&ms, e0, e1);
+        const double tf = 2.0 * 64 * 64 * TK * (double)iters * grid / (ms * 1e-3) / 1e12;
+        printf("%-22s %d CTA/SM: %.2f TFLOP/s (%.1f%% of 37.15)\n", name, per, tf, 100 * tf / 37.15);
+    }
+}
+
+int main() {
+    double* o; cudaMalloc(&o, 64);
+    run<MEMN, MEMN, false>("MEMNxMEMN no-sync", o);
+    run<MEMN, MEMN, true>("MEMNxMEMN sync", o);
+    run<MEMT, MEMT, false>("MEMTxMEMT no-sync", o);
+    run<MEMT, MEMT, true>("MEMTxMEMT sync", o);
+    return 0;
+}
