@@ -182,6 +182,7 @@ __device__ __forceinline__ void load_tile_async(double* s, const Op& op, int r0,
         }
     } else {
         const int kk = tid % TK, rw = tid / TK;
+        const CovP cpl = cp;   // one copy into registers per stage (cp may live in shared memory)
         const bool kok = kk < nk;
         const double2 qk = kok ? ldpt(op.q, k0 + kk) : make_double2(0.0, 0.0);
 #pragma unroll 4
@@ -190,7 +191,7 @@ __device__ __forceinline__ void load_tile_async(double* s, const Op& op, int r0,
             double v = 0.0;
             if (kok && row < nr) {
                 const double2 pr = ldpt(op.p, r0 + row);
-                v = covf(cp, pr.x, pr.y, qk.x, qk.y);
+                v = covf(cpl, pr.x, pr.y, qk.x, qk.y);
             }
             s[row * LDN + kk] = v;
         }
@@ -228,45 +229,6 @@ __device__ __forceinline__ void mma_ktile(double (&acc)[2][4][2], const double* 
     }
 }
 
-// accumulate both K-segments of one output tile through an NSTAGE-deep cp.async pipeline
-template <int KA0, int KB0, int KA1, int KB1>
-__device__ __forceinline__ void tile_pipeline(double (&acc)[2][4][2], const Op& A0, const Op& B0, int K0,
-                                              const Op& A1, const Op& B1, int K1, int r0, int nr, int c0, int nc,
-                                              const CovP& cp, double* smem) {
-    const int T0 = (K0 + TK - 1) / TK, T1 = (K1 + TK - 1) / TK, T = T0 + T1;
-    const bool a0 = op_aligned16(A0), b0 = op_aligned16(B0), a1 = op_aligned16(A1), b1 = op_aligned16(B1);
-    __syncthreads();   // the stage buffers (and any smem view aliasing them) are free
-    // single issue site: iterations kt < 0 only prefetch (pipeline prologue)
-#pragma unroll 1
-    for (int kt = -(NSTAGE - 1); kt < T; kt++) {
-        if (kt >= 0) {
-            cp_async_wait<NSTAGE - 2>();
-            __syncthreads();
-        }
-        const int ki = kt + NSTAGE - 1;
-        if (ki < T) {
-            double* As = smem + (ki % NSTAGE) * STAGE_DBL;
-            double* Bs = As + TILE_DBL;
-            if (ki < T0) {
-                const int k0 = ki * TK, nk = min(TK, K0 - k0);
-                load_tile_async<KA0>(As, A0, r0, nr, k0, nk, cp, a0);
-                load_tile_async<KB0>(Bs, B0, c0, nc, k0, nk, cp, b0);
-            } else {
-                const int k0 = (ki - T0) * TK, nk = min(TK, K1 - k0);
-                load_tile_async<KA1>(As, A1, r0, nr, k0, nk, cp, a1);
-                load_tile_async<KB1>(Bs, B1, c0, nc, k0, nk, cp, b1);
-            }
-        }
-        cp_async_commit();
-        if (kt < 0) continue;
-        const double* As = smem + (kt % NSTAGE) * STAGE_DBL;
-        const double* Bs = As + TILE_DBL;
-        if (kt < T0) mma_ktile<KA0, KB0>(acc, As, Bs, min(TK, K0 - kt * TK));
-        else mma_ktile<KA1, KB1>(acc, As, Bs, min(TK, K1 - (kt - T0) * TK));
-    }
-    cp_async_wait<0>();
-}
-
 // GEMM call descriptor: written to shared memory by the (inlined) caller, read by the single
 // non-inlined implementation per operand-kind combination (keeps the kernels' SASS small enough
 // to stay instruction-cache resident).
@@ -282,12 +244,57 @@ struct GemmDesc {
 constexpr int MISC_DBL = 64;                 // misc smem: reductions, flags, work item, GemmDesc
 __device__ __forceinline__ GemmDesc* gemm_desc(double* smem);
 
+// accumulate both K-segments of one output tile through an NSTAGE-deep cp.async pipeline
+template <int KA0, int KB0, int KA1, int KB1>
+__device__ __forceinline__ void tile_pipeline(double (&acc)[2][4][2], const GemmDesc& d, int r0, int nr, int c0,
+                                              int nc, double* smem, bool wact) {
+    // only the current segment's two operand descriptors are held in registers (segment 1's are read
+    // from the shared-memory GemmDesc when the loads reach it): the engine sits at the 128-register
+    // budget of two 256-thread CTAs per SM
+    const int K0 = d.K0, K1 = d.K1, T0 = (K0 + TK - 1) / TK, T = T0 + (K1 + TK - 1) / TK;
+    Op a = d.A0, b = d.B0;
+    bool aal = op_aligned16(a), bal = op_aligned16(b);
+    __syncthreads();   // the stage buffers (and any smem view aliasing them) are free
+    // single issue site: iterations kt < 0 only prefetch (pipeline prologue)
+#pragma unroll 1
+    for (int kt = -(NSTAGE - 1); kt < T; kt++) {
+        if (kt >= 0) {
+            cp_async_wait<NSTAGE - 2>();
+            __syncthreads();
+        }
+        const int ki = kt + NSTAGE - 1;
+        if (ki < T) {
+            double* As = smem + (ki % NSTAGE) * STAGE_DBL;
+            double* Bs = As + TILE_DBL;
+            if (ki < T0) {
+                const int k0 = ki * TK, nk = min(TK, K0 - k0);
+                load_tile_async<KA0>(As, a, r0, nr, k0, nk, d.cp, aal);
+                load_tile_async<KB0>(Bs, b, c0, nc, k0, nk, d.cp, bal);
+            } else {
+                if (ki == T0) {
+                    a = d.A1; b = d.B1;
+                    aal = op_aligned16(a); bal = op_aligned16(b);
+                }
+                const int k0 = (ki - T0) * TK, nk = min(TK, K1 - k0);
+                load_tile_async<KA1>(As, a, r0, nr, k0, nk, d.cp, aal);
+                load_tile_async<KB1>(Bs, b, c0, nc, k0, nk, d.cp, bal);
+            }
+        }
+        cp_async_commit();
+        if (kt < 0) continue;
+        if (!wact) continue;   // this warp's 16 x 32 sub-tile holds no wanted output (it still loads)
+        const double* As = smem + (kt % NSTAGE) * STAGE_DBL;
+        const double* Bs = As + TILE_DBL;
+        if (kt < T0) mma_ktile<KA0, KB0>(acc, As, Bs, min(TK, K0 - kt * TK));
+        else mma_ktile<KA1, KB1>(acc, As, Bs, min(TK, K1 - (kt - T0) * TK));
+    }
+    cp_async_wait<0>();
+}
+
 template <int KA0, int KB0, int KA1, int KB1>
 __device__ __noinline__ void cta_gemm_impl(double* smem) {
     const GemmDesc& d = *gemm_desc(smem);
-    const Op A0 = d.A0, B0 = d.B0, A1 = d.A1, B1 = d.B1;
     const int Mr = d.Mr, Nc = d.Nc, lower = d.lower, K0 = d.K0, K1 = d.K1;
-    const CovP cp = d.cp;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
     const int wr = (warp >> 1) * 16, wc = (warp & 1) * 32;
@@ -302,7 +309,11 @@ __device__ __noinline__ void cta_gemm_impl(double* smem) {
             for (int mi = 0; mi < 2; mi++)
 #pragma unroll
                 for (int ni = 0; ni < 4; ni++) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-            if (K0 + K1 > 0) tile_pipeline<KA0, KB0, KA1, KB1>(acc, A0, B0, K0, A1, B1, K1, r0, nr, c0, nc, cp, smem);
+            // warps whose sub-tile lies outside a ragged tile (e.g. the 1-row y tile) or strictly above the
+            // diagonal of a lower-triangular tile skip their DMMAs
+            const bool wact = wr < nr && wc < nc && !(lower && tm == tn && wc > wr + 15);
+            if (K0 + K1 > 0)
+                tile_pipeline<KA0, KB0, KA1, KB1>(acc, d, r0, nr, c0, nc, smem, wact);
             const CInit ci = d.ci;
             const double alpha = d.alpha;
             double* C = d.C;
@@ -320,6 +331,7 @@ __device__ __noinline__ void cta_gemm_impl(double* smem) {
                         }
                     }
             if (ci.kind == 2) {
+                const CovP cpl = d.cp;
                 // covariance initial value, added by the thread that stored the element (4 independent
                 // fp64 sqrt/exp chains in flight per thread)
 #pragma unroll 4
@@ -328,7 +340,7 @@ __device__ __noinline__ void cta_gemm_impl(double* smem) {
                     const int i = r0 + wr + mi * 8 + g, j = c0 + wc + ni * 8 + 2 * t + e;
                     if (i < Mr && j < Nc && (!lower || j <= i)) {
                         const double2 pi = ldpt(ci.p, i), pj = ldpt(ci.q, j);
-                        C[(long long)i * ldc + j] += covf(cp, pi.x, pi.y, pj.x, pj.y) + (i == j ? ci.diag : 0.0);
+                        C[(long long)i * ldc + j] += covf(cpl, pi.x, pi.y, pj.x, pj.y) + (i == j ? ci.diag : 0.0);
                     }
                 }
             }
