@@ -62,6 +62,38 @@ def interior_flops(m, r):
     return prior, merge
 
 
+def class_flops(leaf_sizes, M, J, r):
+    """§8(d) algorithmic flops per evaluation split by the kernel classes of mra_kernel_times."""
+    n = np.asarray(leaf_sizes, dtype=np.float64)
+    n = n[n > 0]
+    P = M - 1
+    Pr = P * r
+    out = {"chain": float(np.sum(P * P * n * r * r)), "sigma": float(np.sum(n * (n + 1) * Pr)),
+           "factor": float(np.sum(n ** 3 / 3.0)), "solve": float(np.sum(n * n * (Pr + 1))),
+           "syrk_merge": float(np.sum(Pr * (Pr + 1) * n + 2 * Pr * n + 2 * n))}
+    prior = merge = 0.0
+    for m in range(1, M):
+        p_, g_ = interior_flops(m, r)
+        prior += J ** (m - 1) * p_
+        if m == M - 1:
+            out["syrk_merge"] += J ** (m - 1) * g_
+        else:
+            merge += J ** (m - 1) * g_
+    out["prior"], out["merge"] = prior, merge
+    out["bottom"] = sum(out[k] for k in ("chain", "sigma", "factor", "solve", "syrk_merge"))
+    return out
+
+
+KERNEL_NAMES = {"prior": "k_prior (levels 1..M-1 W chains, Cholesky, inverse)",
+                "bottom": "k_bottom (one CTA per level-(M-1) region: leaves + level M-1 merge)",
+                "merge": "k_merge (levels M-2..1)",
+                "chain": "k_wide_chain (leaf V chains with fused covariance generation)",
+                "sigma": "k_wide_sigma (Sigma_j = C(S,S) + tau2 I - V V^T tiles)",
+                "factor": "k_wide_update/diag/panel_x (blocked Cholesky of Sigma_j, X = L^{-1})",
+                "solve": "k_wide_trsm (G = X [V | y])",
+                "syrk_merge": "k_wide_mtile (Atilde = G^T G tiles + level M-1 merge dataflow)"}
+
+
 def flop_model(leaf_sizes, M, J, r):
     P = M - 1
     leaves = float(np.sum(leaf_flops(leaf_sizes, P, r)))
@@ -334,28 +366,34 @@ def run_gpu(args, rank, world, local_rank):
     derived64 = bf16 * FP64_NOMINAL_TF / BF16_NOMINAL_TF
     meas64 = measured_fp64_peak()
     peak64 = meas64 or derived64
-    bottom_ms, bottom_n = kt[0][1], kt[1][1]
     steps_th = args.steps * ntheta
+    cf = class_flops(sizes, w.M, w.J, plan.r_hat)
+    kms = dict(zip(mra.KERNEL_CLASSES, kt[0]))
+    kcnt = dict(zip(mra.KERNEL_CLASSES, kt[1]))
     roof = None
-    if bottom_n:
-        launch_ms = bottom_ms / bottom_n
-        flops_launch = fm["bottom"] / (bottom_n / steps_th)
+    cand = [k for k in KERNEL_NAMES if kcnt.get(k)]
+    if cand:
+        dom = max(cand, key=lambda k: kms[k])   # the dominant kernel class of the step
+        launch_ms = kms[dom] / kcnt[dom]
+        flops_launch = cf[dom] / (kcnt[dom] / steps_th)
         achieved = flops_launch / (launch_ms / 1e3) / 1e12
         traffic = None
         try:
             tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
-            traffic = tj.get(w.name, {}).get("bytes_per_launch")
+            ent = tj.get(w.name, {})
+            if ent.get("class") == dom:
+                traffic = ent.get("bytes_per_launch")
         except Exception:
             pass
         roof = {"bound": "tensor", "achieved": round(achieved, 3), "peak": round(peak64, 3), "unit": "TFLOP/s",
-                "frac": round(achieved / peak64, 4), "traffic": traffic,
-                "kernel": "k_bottom (leaf prior chain + Sigma_j + Cholesky + TRSM + stacked SYRK + level M-1 merge)",
-                "flops_per_launch": flops_launch, "launch_ms": launch_ms,
+                "frac": round(achieved / peak64, 4), "traffic": traffic, "kernel": KERNEL_NAMES[dom],
+                "class": dom, "flops_per_launch": flops_launch, "launch_ms": launch_ms,
                 "peak_source": (f"measured fp64 DMMA peak of this B200 pool (profiles/fp64_peak_r01.txt, "
                                 f"tools/fp64_peak.cu); the guide-derived figure {src} bf16_tflops_sustained "
                                 f"{bf16} x {FP64_NOMINAL_TF}/{BF16_NOMINAL_TF} = {derived64:.2f} is lower")
                                if meas64 else f"{src} bf16_tflops_sustained {bf16} x {FP64_NOMINAL_TF}/{BF16_NOMINAL_TF}",
-                "kernel_share_of_step": round(bottom_ms / ms, 4),
+                "kernel_share_of_step": round(kms[dom] / ms, 4),
+                "per_class_tflops": {k: round(cf[k] * steps_th / (kms[k] / 1e3) / 1e12, 2) for k in cand},
                 "step_fp64_tflops": round(fm["total"] * steps_th / (ms / 1e3) / 1e12, 3)}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -371,8 +409,8 @@ def run_gpu(args, rank, world, local_rank):
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8 * w.n * ntheta,
                     "d2h_bytes_per_step": 8 * ntheta},
             "gpu_launches": int(launches),
-            "kernel_ms": {"prior": kt[0][0], "bottom": kt[0][1], "merge": kt[0][2], "other": kt[0][3],
-                          "launches": kt[1]},
+            "kernel_ms": {k: round(kms[k], 3) for k in mra.KERNEL_CLASSES},
+            "kernel_launches": {k: int(kcnt[k]) for k in mra.KERNEL_CLASSES},
             "roofline": roof, "cpu_baseline": cpu, "clocks": clocks}
     print(json.dumps(line), flush=True)
 

@@ -285,13 +285,13 @@ def mra_profile(plan: PlanHandle, enable: bool = True):
     _check(_lib.mra_profile(plan.ptr, int(bool(enable))))
 
 
-KERNEL_CLASSES = ("prior", "bottom", "merge", "other")
+KERNEL_CLASSES = ("prior", "bottom", "merge", "other", "chain", "sigma", "factor", "solve", "syrk_merge")
 
 
 def mra_kernel_times(plan: PlanHandle) -> dict:
     """Accumulated device ms and launch counts per kernel class since mra_profile(plan, True)."""
-    ms = (ctypes.c_double * 4)()
-    cnt = (ctypes.c_uint64 * 4)()
+    ms = (ctypes.c_double * len(KERNEL_CLASSES))()
+    cnt = (ctypes.c_uint64 * len(KERNEL_CLASSES))()
     _check(_lib.mra_kernel_times(plan.ptr, ms, cnt))
     return {k: (ms[i], cnt[i]) for i, k in enumerate(KERNEL_CLASSES)}
 

@@ -94,11 +94,13 @@ struct mra_plan {
     std::vector<cudaEvent_t> evpool;
     size_t ev_used = 0;
     std::vector<std::pair<int, size_t>> recs;   // (kind, index of start event; end = +1)
-    double prof_ms[4] = {0, 0, 0, 0};
-    uint64_t prof_cnt[4] = {0, 0, 0, 0};
+    double prof_ms[MRA_NKCLASS] = {0};
+    uint64_t prof_cnt[MRA_NKCLASS] = {0};
 };
 
-enum { KIND_PRIOR = 0, KIND_BOTTOM = 1, KIND_MERGE = 2, KIND_OTHER = 3 };
+// kernel classes of the live timing (include/mra.h MRA_NKCLASS)
+enum { KIND_PRIOR = 0, KIND_BOTTOM = 1, KIND_MERGE = 2, KIND_OTHER = 3, KIND_CHAIN = 4, KIND_SIGMA = 5,
+       KIND_FACTOR = 6, KIND_SOLVE = 7, KIND_SYRKMERGE = 8 };
 
 static cudaEvent_t take_event(mra_plan* P) {
     if (P->ev_used == P->evpool.size()) {
@@ -648,13 +650,13 @@ extern "C" mra_status mra_profile(mra_plan* P, int enable) {
     P->prof = enable != 0;
     P->recs.clear();
     P->ev_used = 0;
-    for (int k = 0; k < 4; k++) { P->prof_ms[k] = 0; P->prof_cnt[k] = 0; }
+    for (int k = 0; k < MRA_NKCLASS; k++) { P->prof_ms[k] = 0; P->prof_cnt[k] = 0; }
     return MRA_OK;
 }
 
 extern "C" mra_status mra_kernel_times(const mra_plan* P, double* ms, uint64_t* launches) {
     if (!P) return fail(MRA_E_ARG, "plan is NULL");
-    for (int k = 0; k < 4; k++) {
+    for (int k = 0; k < MRA_NKCLASS; k++) {
         if (ms) ms[k] = P->prof_ms[k];
         if (launches) launches[k] = P->prof_cnt[k];
     }
@@ -752,20 +754,20 @@ static mra_status eval_wide(mra_plan* P, const TreeParams& tp, long long gf, lon
         const auto& w = P->wsubs[P->wsub_next++];
         if (w.g0 != gf + done) return fail(MRA_E_CUDA, "internal: wide sub-chunk schedule out of order");
         wp.G_base = P->leaf_off[w.g0 * P->J];
-        LCHK_K(KIND_BOTTOM, launch_wide(0, tp, wp, 0, P->wtasks + w.chain_off, w.chain_n, P->grid, take_counter(P), st));
-        LCHK_K(KIND_BOTTOM, launch_wide(1, tp, wp, 0, P->wtasks + w.sigma_off, w.sigma_n, P->grid, take_counter(P), st));
+        LCHK_K(KIND_CHAIN, launch_wide(0, tp, wp, 0, P->wtasks + w.chain_off, w.chain_n, P->grid, take_counter(P), st));
+        LCHK_K(KIND_SIGMA, launch_wide(1, tp, wp, 0, P->wtasks + w.sigma_off, w.sigma_n, P->grid, take_counter(P), st));
         for (size_t s2 = 0; s2 < w.diag_n.size(); s2++) {
             if (w.upd_n[s2] > 0)
-                LCHK_K(KIND_BOTTOM, launch_wide(2, tp, wp, (int)s2, P->wtasks + w.upd_off[s2], w.upd_n[s2], P->grid,
+                LCHK_K(KIND_FACTOR, launch_wide(2, tp, wp, (int)s2, P->wtasks + w.upd_off[s2], w.upd_n[s2], P->grid,
                                                 take_counter(P), st));
-            LCHK_K(KIND_BOTTOM, launch_wide(3, tp, wp, (int)s2, P->wtasks + w.diag_off[s2], w.diag_n[s2], P->grid,
+            LCHK_K(KIND_FACTOR, launch_wide(3, tp, wp, (int)s2, P->wtasks + w.diag_off[s2], w.diag_n[s2], P->grid,
                                             take_counter(P), st));
-            LCHK_K(KIND_BOTTOM, launch_wide(4, tp, wp, (int)s2, P->wtasks + w.pf_off[s2], w.pf_n[s2], P->grid,
+            LCHK_K(KIND_FACTOR, launch_wide(4, tp, wp, (int)s2, P->wtasks + w.pf_off[s2], w.pf_n[s2], P->grid,
                                             take_counter(P), st));
         }
         if (w.trsm_n > 0)
-            LCHK_K(KIND_BOTTOM, launch_wide(5, tp, wp, 0, P->wtasks + w.trsm_off, w.trsm_n, P->grid, take_counter(P), st));
-        LCHK_K(KIND_BOTTOM, launch_wide_mtile(tp, wp, w.g0, w.gcount, gout, gout_first, q, P->wtasks + w.mt_off,
+            LCHK_K(KIND_SOLVE, launch_wide(5, tp, wp, 0, P->wtasks + w.trsm_off, w.trsm_n, P->grid, take_counter(P), st));
+        LCHK_K(KIND_SYRKMERGE, launch_wide_mtile(tp, wp, w.g0, w.gcount, gout, gout_first, q, P->wtasks + w.mt_off,
                                                   w.mt_n, P->grid, take_counter(P), P->mring, st));
         done += w.gcount;
     }
