@@ -6,6 +6,7 @@ shares no code with it.
 
   oracle.run(...)       -> the recursion (oracle/mra_oracle.c, plain C + OpenMP)
   oracle.plan(...)      -> the oracle's own partition / knots / leaf assignment
+  oracle.predict(...)   -> posterior mean / variance of X at query points (the recursion)
   oracle.dense          -> the dense definition of Sigma_MRA, tiny inputs
 """
 from __future__ import annotations
@@ -55,6 +56,11 @@ def _load():
         lib.oracle_plan.restype = ctypes.c_int
         lib.oracle_plan.argtypes = [D, D, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                     ctypes.c_double, ctypes.POINTER(ctypes.c_int), I64, I64, D, D, D]
+        lib.oracle_predict.restype = ctypes.c_int
+        lib.oracle_predict.argtypes = [D, D, D, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int,
+                                       ctypes.c_double, ctypes.c_double, ctypes.c_double, D, D, ctypes.c_int64,
+                                       D, D, ctypes.c_int]
         lib.oracle_threads.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -161,3 +167,22 @@ def finish(x, y, z, M, J, r, theta, s, A, omega, d, u, offset=E_OVER_100, xscale
     if rc != 0:
         raise OracleError(f"oracle_finish failed: {rc}")
     return ll.value
+
+
+def predict(x, y, z, qx, qy, M, J, r, theta, offset=E_OVER_100, xscale=1.0, yscale=1.0, nthreads=0):
+    """Posterior mean and variance of the noise-free process X at query points (recursion in the
+    paper's W / K notation, oracle/mra_oracle.c predict_all). NaN outside the root domain."""
+    lib = _load()
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    z = np.ascontiguousarray(z, dtype=np.float64)
+    qx = np.ascontiguousarray(qx, dtype=np.float64)
+    qy = np.ascontiguousarray(qy, dtype=np.float64)
+    cov, s2, rho, t2 = theta
+    mean = np.empty(qx.shape[0])
+    var = np.empty(qx.shape[0])
+    rc = lib.oracle_predict(_p(x), _p(y), _p(z), x.shape[0], M, J, r, offset, xscale, yscale, int(cov), float(s2),
+                            float(rho), float(t2), _p(qx), _p(qy), qx.shape[0], _p(mean), _p(var), int(nthreads))
+    if rc != 0:
+        raise OracleError(f"oracle_predict failed: {rc}")
+    return mean, var

@@ -103,14 +103,22 @@ class Tree:
 
 
 def sigma_mra(x, y, M, J, r, cov_kind, sigma2, rho, offset=E_OVER_100, xs=1.0, ys=1.0,
-              return_all=False):
-    """Sigma_MRA over the retained observations (and optionally over Z = obs ∪ knots)."""
+              return_all=False, qx=None, qy=None):
+    """Sigma_MRA over the retained observations (and optionally over Z = obs ∪ knots ∪ queries).
+
+    Query points (prediction locations) join Z as finest-level points: the recursion is applied
+    to every pair of points exactly as to the observations, so Sigma_MRA(q, s) is the MRA
+    covariance the approximation assigns to a pair (q, s) (identical to C for same-leaf pairs)."""
     x = np.asarray(x, dtype=np.float64)
     y = np.asarray(y, dtype=np.float64)
     tree = Tree(x, y, M, J, r, offset)
     leaf = tree.leaf_of(x, y)
     keep = np.nonzero(leaf >= 0)[0]
     zx, zy = list(x[keep]), list(y[keep])
+    nq = 0 if qx is None else len(qx)
+    if nq:
+        zx.extend(np.asarray(qx, dtype=np.float64).tolist())
+        zy.extend(np.asarray(qy, dtype=np.float64).tolist())
     knot_sets = {}
     for m in range(1, M):
         for t in range(J ** (m - 1)):
@@ -173,3 +181,19 @@ def posterior(x, y, z, M, J, r, cov_kind, sigma2, rho, tau2, **kw):
     smooth[keep] = ez[:nobs]
     xq = {k: ez[np.array(v)] for k, v in knot_sets.items()}
     return smooth, xq
+
+
+def predict(x, y, z, qx, qy, M, J, r, cov_kind, sigma2, rho, tau2, **kw):
+    """Conditional mean / variance of the noise-free X at query points under the MRA prior (the
+    DEFINITION: kriging with Sigma_MRA): mean = Sigma(q, S) (Sigma(S,S) + tau2 I)^{-1} y,
+    var = Sigma(q,q) - Sigma(q,S) (Sigma(S,S) + tau2 I)^{-1} Sigma(S,q)."""
+    Sig, keep, nobs, knot_sets, tree = sigma_mra(x, y, M, J, r, cov_kind, sigma2, rho, return_all=True,
+                                                 qx=qx, qy=qy, **kw)
+    nq = len(qx)
+    qi = np.arange(nobs, nobs + nq)
+    C = Sig[:nobs, :nobs] + tau2 * np.eye(nobs)
+    Sqs = Sig[np.ix_(qi, np.arange(nobs))]
+    alpha = scipy.linalg.solve(C, np.asarray(z)[keep], assume_a="pos")
+    mean = Sqs @ alpha
+    var = np.diag(Sig[np.ix_(qi, qi)]) - np.einsum("ij,ji->i", Sqs, scipy.linalg.solve(C, Sqs.T, assume_a="pos"))
+    return mean, var

@@ -427,6 +427,158 @@ static int post_region(O *o, int lev, int64_t t, double *A, double *w, double *d
     return 0;
 }
 
+/* -------------------------------------------------------------- prediction */
+/* Posterior mean and variance of X(p) at query points (the paper's "prediction" calculation mode,
+ * PAPER.md:228, 494), in the W / K notation used above. For p in leaf j with
+ * ancestors a_1..a_P (P = M-1):
+ *   b^l(p)   = W^l(p, Q_{a_l})  by the same recursion as the observations (w_chain)
+ *   c        = C_M(S_j, p) = C(S_j, p) - sum_k B^k_j K_{a_k} b^k(p)^T
+ *   C_M(p,p) = C(p, p) - sum_k b^k(p) K_{a_k} b^k(p)^T
+ *   mean     = sum_l b^l(p) nu_{a_l} + c^T Sigma_j^{-1} (y_j - sum_l B^l_j nu_{a_l})
+ *   bt_l     = b^l(p) - B^{lT}_j Sigma_j^{-1} c
+ *   var      = C_M(p,p) - c^T Sigma_j^{-1} c + sum_{l,l'} bt_l^T Cov(eta_{a_l}, eta_{a_l'} | y) bt_l'
+ * where nu = E[eta | y] (the mu recursion above) and the posterior covariances of the ancestor
+ * chain (the paper's BTilde) follow top-down from
+ *   eta_R | eta_anc, y ~ N(Ktilde_R (omegatilde^m - sum_k Atilde^{m,k} eta_{a_k}), Ktilde_R):
+ *   Cov(eta_m, eta_l) = -Ktilde_m sum_{k<m} Atilde^{m,k} Cov(eta_k, eta_l)          (l < m)
+ *   Cov(eta_m, eta_m) = Ktilde_m + Ktilde_m (sum_{k,k'} Atilde^{m,k} Cov(eta_k, eta_k') Atilde^{m,k'T}) Ktilde_m
+ * Queries outside the root domain get NaN. Pinned against the dense definition (oracle/dense.py). */
+static int predict_all(O *o, const double *MU, const double *qx, const double *qy, int64_t nq,
+                       double *pmean, double *pvar) {
+    const int M = o->M, J = o->J, rh = o->rh, P = M - 1, PP = P * rh;
+    int64_t *ql = malloc(sizeof(int64_t) * (nq + 1));
+    for (int64_t i = 0; i < nq; i++) {
+        const double *b = o->box;
+        double px = qx[i], py = qy[i];
+        if (!(px >= b[0] && px < b[1] && py >= b[2] && py < b[3])) { ql[i] = -1; continue; }
+        int64_t t = 0;
+        for (int m = 1; m < M; m++) {
+            const double *bb = o->box + 4 * rid(o, m, t);
+            int c;
+            if (J == 4) c = (px >= 0.5 * (bb[0] + bb[1]) ? 1 : 0) + (py >= 0.5 * (bb[2] + bb[3]) ? 2 : 0);
+            else if (splits_x(bb)) c = px >= 0.5 * (bb[0] + bb[1]) ? 1 : 0;
+            else c = py >= 0.5 * (bb[2] + bb[3]) ? 1 : 0;
+            t = t * J + c;
+        }
+        ql[i] = t;
+    }
+    int bad = 0;
+    #pragma omp parallel for schedule(dynamic, 1) reduction(|:bad)
+    for (int64_t j = 0; j < o->nleaf; j++) {
+        int64_t nqj = 0;
+        for (int64_t i = 0; i < nq; i++) nqj += (ql[i] == j);
+        if (nqj == 0) continue;
+        int np = (int)o->lcnt[j];
+        const int64_t *idx = o->lidx + o->lstart[j];
+        double *B = malloc(sizeof(double) * ((int64_t)np * PP + 1));
+        double *S = malloc(sizeof(double) * ((int64_t)np * np + 1));
+        double **Bl = malloc(sizeof(double *) * (P + 1));
+        if (np > 0 && leaf_factor(o, j, np, B, S, Bl)) { bad |= 1; free(B); free(S); free(Bl); continue; }
+        /* rr = Sigma_j^{-1} (y_j - sum_l B^l nu_{a_l}) */
+        double *rr = malloc(sizeof(double) * (np + 1));
+        for (int i = 0; i < np; i++) {
+            double s = o->z[idx[i]];
+            for (int k = 1; k <= P; k++) {
+                int64_t ak = rid(o, k, j / ipow(J, M - k));
+                for (int q = 0; q < rh; q++) s -= Bl[k - 1][(int64_t)i * rh + q] * MU[ak * rh + q];
+            }
+            rr[i] = s;
+        }
+        if (np > 0) cholsolve(np, S, 1, rr);
+        /* posterior covariance of the ancestor chain eta_{a_1..a_P} (PP x PP), top-down */
+        double *CC = calloc((int64_t)PP * PP + 1, sizeof(double));
+        for (int m = 1; m <= P; m++) {
+            int64_t id = rid(o, m, j / ipow(J, M - m));
+            int Pp = (m - 1) * rh, Pm = m * rh;
+            const double *Ar = o->Arow[id];   /* rh x Pm: Atilde^{m,1..m} */
+            /* Gm = Atilde^{m,<m} CC[<m, <m]   (rh x Pp) */
+            double *Gm = calloc((int64_t)rh * Pp + 1, sizeof(double));
+            for (int a = 0; a < rh; a++)
+                for (int l = 0; l < Pp; l++) {
+                    double s = 0;
+                    for (int k = 0; k < Pp; k++) s += Ar[(int64_t)a * Pm + k] * CC[(int64_t)k * PP + l];
+                    Gm[(int64_t)a * Pp + l] = s;
+                }
+            /* Cov(eta_m, eta_l) = -Ktilde_m Gm */
+            double *X = malloc(sizeof(double) * ((int64_t)rh * Pp + 1));
+            for (int64_t e = 0; e < (int64_t)rh * Pp; e++) X[e] = Gm[e];
+            if (Pp) cholsolve(rh, o->LP[id], Pp, X);
+            for (int a = 0; a < rh; a++)
+                for (int l = 0; l < Pp; l++) {
+                    CC[(int64_t)(Pp + a) * PP + l] = -X[(int64_t)a * Pp + l];
+                    CC[(int64_t)l * PP + Pp + a] = -X[(int64_t)a * Pp + l];
+                }
+            /* Cov(eta_m, eta_m) = Ktilde_m + Ktilde_m (Gm Atilde^{m,<m T}) Ktilde_m */
+            /* Y = I + (Gm Atilde^T) Ktilde_m, then Ktilde_m Y = Ktilde_m + Ktilde_m Gm A^T Ktilde_m */
+            double *Y = calloc((int64_t)rh * rh, sizeof(double));
+            for (int a = 0; a < rh; a++) Y[a * rh + a] = 1.0;
+            double *Z = calloc((int64_t)rh * rh, sizeof(double));
+            for (int a = 0; a < rh; a++)
+                for (int b = 0; b < rh; b++) {
+                    double s = 0;
+                    for (int l = 0; l < Pp; l++) s += Gm[(int64_t)a * Pp + l] * Ar[(int64_t)b * Pm + l];
+                    Z[a * rh + b] = s;   /* Gm Atilde^{m,<m T}, symmetric */
+                }
+            cholsolve(rh, o->LP[id], rh, Z);          /* Ktilde Z */
+            for (int a = 0; a < rh; a++)               /* (Ktilde Z)^T = Z Ktilde */
+                for (int b = 0; b < rh; b++) Y[a * rh + b] += Z[b * rh + a];
+            cholsolve(rh, o->LP[id], rh, Y);           /* Ktilde (I + Z Ktilde) */
+            for (int a = 0; a < rh; a++)
+                for (int b = 0; b < rh; b++) CC[(int64_t)(Pp + a) * PP + Pp + b] = Y[a * rh + b];
+            free(Gm); free(X); free(Y); free(Z);
+        }
+        /* per query */
+        double *bq = malloc(sizeof(double) * (PP + 1)), *c = malloc(sizeof(double) * (np + 1));
+        double *w = malloc(sizeof(double) * (np + 1)), *bt = malloc(sizeof(double) * (PP + 1));
+        double *t = malloc(sizeof(double) * (rh + 1));
+        double **Bq = malloc(sizeof(double *) * (P + 1));
+        for (int l = 0; l < P; l++) Bq[l] = bq + (int64_t)l * rh;
+        for (int64_t iq = 0; iq < nq; iq++) {
+            if (ql[iq] != j) continue;
+            double px = qx[iq], py = qy[iq];
+            if (P > 0) w_chain(o, &px, &py, 1, M, j, P, Bq);
+            double cpp = covf(o, px, py, px, py);
+            for (int i = 0; i < np; i++) c[i] = covf(o, o->x[idx[i]], o->y[idx[i]], px, py);
+            for (int k = 1; k <= P; k++) {
+                int64_t idk = rid(o, k, j / ipow(J, M - k));
+                for (int a = 0; a < rh; a++) t[a] = Bq[k - 1][a];
+                cholsolve(rh, o->LW[idk], 1, t);                 /* K_{a_k} b^k(p)^T */
+                for (int a = 0; a < rh; a++) cpp -= Bq[k - 1][a] * t[a];
+                for (int i = 0; i < np; i++)
+                    for (int a = 0; a < rh; a++) c[i] -= Bl[k - 1][(int64_t)i * rh + a] * t[a];
+            }
+            double mean = 0.0;
+            for (int k = 1; k <= P; k++) {
+                int64_t ak = rid(o, k, j / ipow(J, M - k));
+                for (int a = 0; a < rh; a++) mean += Bq[k - 1][a] * MU[ak * rh + a];
+            }
+            for (int i = 0; i < np; i++) { mean += c[i] * rr[i]; w[i] = c[i]; }
+            if (np > 0) cholsolve(np, S, 1, w);
+            double var = cpp;
+            for (int i = 0; i < np; i++) var -= c[i] * w[i];
+            for (int l = 0; l < P; l++)
+                for (int a = 0; a < rh; a++) {
+                    double s = Bq[l][a];
+                    for (int i = 0; i < np; i++) s -= Bl[l][(int64_t)i * rh + a] * w[i];
+                    bt[l * rh + a] = s;
+                }
+            for (int e = 0; e < PP; e++) {
+                double s = 0;
+                for (int f = 0; f < PP; f++) s += CC[(int64_t)e * PP + f] * bt[f];
+                var += bt[e] * s;
+            }
+            pmean[iq] = mean;
+            pvar[iq] = var;
+        }
+        free(bq); free(c); free(w); free(bt); free(t); free(Bq);
+        free(CC); free(rr); free(B); free(S); free(Bl);
+    }
+    for (int64_t i = 0; i < nq; i++)
+        if (ql[i] < 0) { pmean[i] = NAN; pvar[i] = NAN; }
+    free(ql);
+    return bad ? -4 : 0;
+}
+
 /* ----------------------------------------------------------------- driver */
 static void free_all(O *o) {
     if (o->W) for (int64_t i = 0; i < o->nint; i++) { free(o->W[i]); free(o->LW[i]); }
@@ -478,7 +630,8 @@ static int run_impl(const double *x, const double *y, const double *z, int64_t n
                     double *out_u, double *region_d, double *region_u, double *mu, double *xq,
                     double *smooth, int64_t *n_retained, int nthreads, double *out_A, double *out_w,
                     int given_level, const double *gA, const double *gw, const double *gd,
-                    const double *gu) {
+                    const double *gu, const double *qx, const double *qy, int64_t nq, double *pmean,
+                    double *pvar) {
     if (M < 1 || (J != 2 && J != 4) || r < 1 || n < 1) return -1;
     if (!(sigma2 > 0) || !(rho > 0) || !(tau2 > 0)) return -1;
 #ifdef _OPENMP
@@ -493,7 +646,7 @@ static int run_impl(const double *x, const double *y, const double *z, int64_t n
     int tl = target_level > 0 ? target_level : 1;
     int64_t tt = target_level > 0 ? target_t : 0;
     if (tl > M || tt < 0 || tt >= ipow(J, tl - 1)) { free_all(&o); return -1; }
-    o.want_post = (mu || xq || smooth) && target_level <= 0;
+    o.want_post = (mu || xq || smooth || nq > 0) && target_level <= 0;
     o.region_d = region_d; o.region_u = region_u;
     if (region_d) for (int64_t i = 0; i < o.nreg; i++) { region_d[i] = NAN; region_u[i] = NAN; }
     int64_t nint = o.nint;
@@ -610,6 +763,7 @@ static int run_impl(const double *x, const double *y, const double *z, int64_t n
             }
         }
         if (mu) memcpy(mu, MU, sizeof(double) * nint * rh);
+        if (nq > 0 && predict_all(&o, MU, qx, qy, nq, pmean, pvar)) bad |= 1;
         if (smooth) {
             /* E[X(S_j)|y] = y_j - tau2 Sigma_j^{-1} (y_j - sum_k B^k mu_{a_k}) */
             for (int64_t i = 0; i < n; i++) smooth[i] = NAN;
@@ -652,7 +806,7 @@ int oracle_run(const double *x, const double *y, const double *z, int64_t n, int
                double *smooth, int64_t *n_retained, int nthreads, double *out_A, double *out_w) {
     return run_impl(x, y, z, n, M, J, r, offset, xscale, yscale, cov, sigma2, rho, tau2, target_level,
                     target_t, loglik, out_d, out_u, region_d, region_u, mu, xq, smooth, n_retained,
-                    nthreads, out_A, out_w, 0, NULL, NULL, NULL, NULL);
+                    nthreads, out_A, out_w, 0, NULL, NULL, NULL, NULL, NULL, NULL, 0, NULL, NULL);
 }
 
 /* log L from the outputs (A, omega, d, u) of every level-s region (s >= 2), merging levels
@@ -664,7 +818,20 @@ int oracle_finish(const double *x, const double *y, const double *z, int64_t n, 
                   const double *gu, double *loglik) {
     if (s < 2 || s > M) return -1;
     return run_impl(x, y, z, n, M, J, r, offset, xscale, yscale, cov, sigma2, rho, tau2, 0, 0, loglik,
-                    NULL, NULL, NULL, NULL, NULL, NULL, NULL, NULL, 0, NULL, NULL, s, gA, gw, gd, gu);
+                    NULL, NULL, NULL, NULL, NULL, NULL, NULL, NULL, 0, NULL, NULL, s, gA, gw, gd, gu, NULL, NULL,
+                    0, NULL, NULL);
+}
+
+/* Posterior mean / variance (noise-free X, no nugget: SPEC.md:271) at nq query locations after a
+   full evaluation; NaN for queries outside the root domain. Returns as oracle_run. */
+int oracle_predict(const double *x, const double *y, const double *z, int64_t n, int M, int J, int r,
+                   double offset, double xscale, double yscale, int cov, double sigma2, double rho,
+                   double tau2, const double *qx, const double *qy, int64_t nq, double *pmean, double *pvar,
+                   int nthreads) {
+    if (nq < 1) return -1;
+    return run_impl(x, y, z, n, M, J, r, offset, xscale, yscale, cov, sigma2, rho, tau2, 0, 0, NULL, NULL,
+                    NULL, NULL, NULL, NULL, NULL, NULL, NULL, nthreads, NULL, NULL, 0, NULL, NULL, NULL, NULL,
+                    qx, qy, nq, pmean, pvar);
 }
 
 int oracle_threads(void) {

@@ -287,3 +287,76 @@ def test_c0_inputs_shape():
     assert w.n == 4096 and (w.M, w.J, w.r) == (3, 4, 16)
     o = oracle.run(w.x, w.y, w.z, w.M, w.J, w.r, w.thetas[0])
     assert o["n_retained"] == 4096 and np.isfinite(o["loglik"])
+
+
+# ------------------------------------------------------ prediction (NEXT-1)
+def _queries(x, y, seed, k=24):
+    """Random interior points + points exactly at observations + points at level-1 knots."""
+    rng = np.random.default_rng(seed)
+    qx = np.concatenate([rng.uniform(x.min(), x.max(), k), x[:6]])
+    qy = np.concatenate([rng.uniform(y.min(), y.max(), k), y[:6]])
+    return qx, qy
+
+
+@pytest.mark.parametrize("n,M,J,r,cov,cl", [
+    (300, 3, 4, 9, EXP, 0), (250, 4, 2, 9, MAT, 2), (362, 3, 4, 16, EXP, 3),
+    (300, 2, 2, 4, MAT, 0), (280, 5, 2, 4, EXP, 4)])
+def test_P11_prediction_recursion_equals_dense_definition(n, M, J, r, cov, cl):
+    """Prediction (PAPER.md:228 'prediction' mode): the recursion's posterior
+    mean / variance of X at query points equal kriging with the explicitly assembled Sigma_MRA
+    (queries joining Z as finest-level points) -- means and variances, incl.
+    queries at observations and in empty leaves (clustered inputs)."""
+    x, y, z = synth.uniform_small(n, seed=31 + n, clusters=cl)
+    qx, qy = _queries(x, y, seed=n)
+    p = dense.Tree(x, y, M, J, r)
+    kx, ky = p.knots(1, 0)
+    qx = np.concatenate([qx, kx[:3]]); qy = np.concatenate([qy, ky[:3]])
+    th = (cov, 1.3, 0.12, 0.06)
+    m1, v1 = oracle.predict(x, y, z, qx, qy, M, J, r, th)
+    m2, v2 = dense.predict(x, y, z, qx, qy, M, J, r, cov, 1.3, 0.12, 0.06)
+    assert np.max(np.abs(m1 - m2)) <= 1e-11 * np.max(np.abs(m2))
+    assert np.max(np.abs(v1 - v2)) <= 1e-11 * 1.3
+    assert np.all(v1 > 0) and np.all(v1 <= 1.3 * (1 + 1e-12))
+
+
+def test_P11_prediction_M1_is_kriging():
+    """M = 1: textbook simple kriging with the full covariance (no approximation)."""
+    x, y, z = synth.uniform_small(240, seed=8)
+    qx, qy = _queries(x, y, seed=2)
+    s2, rho, t2 = 0.9, 0.2, 0.04
+    m1, v1 = oracle.predict(x, y, z, qx, qy, 1, 4, 9, (EXP, s2, rho, t2))
+    C = s2 * np.exp(-dense.dist(x, y, x, y) / rho) + t2 * np.eye(len(x))
+    Cq = s2 * np.exp(-dense.dist(qx, qy, x, y) / rho)
+    mean = Cq @ np.linalg.solve(C, z)
+    var = s2 - np.einsum("ij,ji->i", Cq, np.linalg.solve(C, Cq.T))
+    np.testing.assert_allclose(m1, mean, rtol=0, atol=1e-11 * np.max(np.abs(mean)))
+    np.testing.assert_allclose(v1, var, rtol=0, atol=1e-12)
+
+
+def test_P11_prediction_at_observations_equals_smoothing():
+    """A query at an observation location is X(s_i) itself: its predictive mean is the smoothing
+    mean E[X(s_i)|y] of the posterior pass (pinned by P7)."""
+    x, y, z = synth.uniform_small(400, seed=9, clusters=2)
+    th = (EXP, 1.0, 0.1, 0.05)
+    ref = oracle.run(x, y, z, 4, 4, 9, th, posterior=True)
+    m, v = oracle.predict(x, y, z, x[:50], y[:50], 4, 4, 9, th)
+    ok = ~np.isnan(ref["smooth"][:50])
+    np.testing.assert_allclose(m[ok], ref["smooth"][:50][ok], rtol=0, atol=1e-12)
+    assert np.all(v[ok] < th[3])   # posterior variance below the nugget where the point is observed
+
+
+def test_P11_prediction_far_from_data_reverts_to_prior():
+    """d >> rho from every observation (inside the domain): mean -> 0, variance -> sigma^2."""
+    rng = np.random.default_rng(4)
+    x = np.concatenate([rng.uniform(0, 0.1, 200), [1.0]])
+    y = np.concatenate([rng.uniform(0, 0.1, 200), [1.0]])
+    z = rng.standard_normal(201)
+    m, v = oracle.predict(x, y, z, np.array([0.9, 0.6]), np.array([0.1, 0.5]), 3, 4, 9, (EXP, 2.0, 0.01, 0.1))
+    assert np.all(np.abs(m) < 1e-12) and np.all(np.abs(v - 2.0) < 1e-12)
+
+
+def test_P11_prediction_outside_domain_is_nan():
+    x, y, z = synth.uniform_small(100, seed=3)
+    m, v = oracle.predict(x, y, z, np.array([x.max() * 2 + 1, x.mean()]), np.array([y.mean(), y.mean()]), 2, 4,
+                          4, (EXP, 1.0, 0.1, 0.05))
+    assert np.isnan(m[0]) and np.isnan(v[0]) and np.isfinite(m[1]) and np.isfinite(v[1])
