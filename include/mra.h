@@ -112,6 +112,22 @@ mra_status mra_loglik_dev(mra_plan* plan, const double* d_y, const mra_theta* th
 mra_status mra_loglik_batch_dev(mra_plan* plan, const double* d_y, const mra_theta* theta,
                                 int n_theta, double* loglik);
 
+/* Prediction (north_star's mra_predict; the paper's "prediction" calculation mode, PAPER.md:228,
+ * 494, 537): posterior mean and variance of the noise-free process X (no nugget)
+ * at nq query locations, under the MRA prior, given the observations and theta of the LAST
+ * evaluation on this plan -- which must have requested posterior state (post->mu or post->smooth
+ * non-NULL); otherwise MRA_E_ARG. Equals kriging with Sigma_MRA (queries treated as finest-level
+ * points of the leaf they fall in): mean = Sigma(q,S)(Sigma(S,S)+tau2 I)^{-1} y,
+ * var = Sigma(q,q) - Sigma(q,S)(Sigma(S,S)+tau2 I)^{-1} Sigma(S,q); computed per leaf from the
+ * leaf's factorization and the posterior state (mu, Ltilde^{-1}, F per region) along the ancestor
+ * chain.
+ *   qx, qy : host arrays of nq query coordinates (any order; need not be observations).
+ *   mean, var : host outputs [nq] in the caller's order; NaN for queries outside the root domain
+ *               (data bounding box with top/right pushed out 1%).
+ * Not available on sharded plans (MRA_E_CONFIG). */
+mra_status mra_predict(mra_plan* plan, const double* qx, const double* qy, uint64_t nq, double* mean,
+                       double* var);
+
 /* Multi-GPU subtree sharding, one process per GPU:
  *   mra_shard_size(plan)          -> doubles in the exchange buffer (same on every rank)
  *   mra_loglik_shard(plan, d_y, theta, d_xbuf)

@@ -53,7 +53,7 @@ class _Post(ctypes.Structure):
 
 
 _lib = None
-EXPORTS = ["mra_plan_create", "mra_loglik", "mra_loglik_dev", "mra_loglik_batch_dev", "mra_shard_size",
+EXPORTS = ["mra_plan_create", "mra_loglik", "mra_loglik_dev", "mra_loglik_batch_dev", "mra_predict", "mra_shard_size",
            "mra_loglik_shard", "mra_loglik_finish", "mra_plan_info", "mra_plan_layout", "mra_plan_shards",
            "mra_profile", "mra_kernel_times", "mra_last_launches", "mra_plan_destroy", "mra_last_error"]
 
@@ -95,6 +95,8 @@ def load_library(path: str = LIB_PATH):
                                     ctypes.POINTER(U64)]
     lib.mra_profile.restype = ctypes.c_int
     lib.mra_profile.argtypes = [P, ctypes.c_int]
+    lib.mra_predict.restype = ctypes.c_int
+    lib.mra_predict.argtypes = [P, D, D, U64, D, D]
     lib.mra_kernel_times.restype = ctypes.c_int
     lib.mra_kernel_times.argtypes = [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(U64)]
     lib.mra_last_launches.restype = U64
@@ -294,6 +296,21 @@ def mra_kernel_times(plan: PlanHandle) -> dict:
     cnt = (ctypes.c_uint64 * len(KERNEL_CLASSES))()
     _check(_lib.mra_kernel_times(plan.ptr, ms, cnt))
     return {k: (ms[i], cnt[i]) for i, k in enumerate(KERNEL_CLASSES)}
+
+
+def mra_predict(plan: PlanHandle, qx, qy):
+    """Posterior mean / variance of X at query points (host arrays) for the last evaluation, which
+    must have requested posterior state (posterior=True). NaN outside the root domain."""
+    qx = np.ascontiguousarray(qx, dtype=np.float64)
+    qy = np.ascontiguousarray(qy, dtype=np.float64)
+    if qx.shape != qy.shape or qx.ndim != 1:
+        raise ValueError("qx, qy must be 1-D arrays of equal length")
+    mean = np.empty(qx.shape[0])
+    var = np.empty(qx.shape[0])
+    D = ctypes.POINTER(ctypes.c_double)
+    _check(_lib.mra_predict(plan.ptr, qx.ctypes.data_as(D), qy.ctypes.data_as(D), qx.shape[0],
+                            mean.ctypes.data_as(D), var.ctypes.data_as(D)))
+    return mean, var
 
 
 def mra_last_launches(plan: PlanHandle) -> int:

@@ -38,6 +38,8 @@ struct mra_plan {
     long long N = 0, nreg = 0, nint = 0, nleaf = 0, n_empty = 0, max_leaf = 0, max_group = 0;
     std::vector<long long> perm, leaf_off;
     std::vector<double> kx, ky;
+    std::vector<double> box;         // interior region boxes (level-major, x0 x1 y0 y1)
+    double root[4] = {0, 0, 0, 0};   // root domain (data bounding box, top/right + 1%)
     int device = 0, nsm = 148;
     cudaStream_t st = nullptr;
     // device state
@@ -69,6 +71,12 @@ struct mra_plan {
     double* mu_d = nullptr;
     double* smooth_d = nullptr;
     double* ws_smooth = nullptr;     // wide plans: per-CTA smoothing workspace sized for the largest leaf
+    // prediction: posterior state of the last evaluation (valid only if it requested posterior state)
+    bool post_valid = false;
+    mra_theta post_theta{};
+    double* ws_pred = nullptr;
+    WsLayout Lp{};
+    int pred_grid = 0;
     WsLayout Ls{};
     int smooth_grid = 0;
     uint64_t launches = 0;
@@ -202,6 +210,8 @@ static mra_status build_host(mra_plan* P, const double* x, const double* y, uint
             }
         }
     }
+    P->root[0] = x0; P->root[1] = x1 + 0.01 * (x1 - x0);
+    P->root[2] = y0; P->root[3] = y1 + 0.01 * (y1 - y0);
     const int rh = P->rh;
     P->kx.assign(P->nint * rh, 0.0);
     P->ky.assign(P->nint * rh, 0.0);
@@ -250,6 +260,7 @@ static mra_status build_host(mra_plan* P, const double* x, const double* y, uint
         P->max_leaf = std::max(P->max_leaf, P->leaf_off[t + 1]);
         P->leaf_off[t + 1] += P->leaf_off[t];
     }
+    P->box = box;
     P->N = P->leaf_off[P->nleaf];
     if (P->N == 0) return fail(MRA_E_STRUCT, "every observation was eliminated");
     std::vector<long long> fill(P->leaf_off.begin(), P->leaf_off.end() - 1);
@@ -860,6 +871,7 @@ static mra_status begin_eval(mra_plan* P, const double* d_y, const mra_theta* th
     if (P->device < 0) return fail(MRA_E_CUDA, "host-only plan (device -2) cannot evaluate");
     P->launches = 0;
     P->next_counter = 0;
+    P->post_valid = false;   // zs (and, when requested, the posterior state) are overwritten below
     mra_status s = check_theta(th);
     if (s) return s;
     if (cudaSetDevice(P->device) != cudaSuccess) return fail(MRA_E_CUDA, "cudaSetDevice failed");
@@ -942,7 +954,129 @@ static mra_status run_eval(mra_plan* P, const double* d_y, const mra_theta* th, 
         if (post->mu && nmu) CU(cudaMemcpyAsync(post->mu, P->mu_d, nmu, k, P->st));
         if (post->smooth) CU(cudaMemcpyAsync(post->smooth, P->smooth_d, 8 * P->n_in, k, P->st));
         CU(cudaStreamSynchronize(P->st));
+        P->post_valid = true;
+        P->post_theta = *th;
     }
+    return MRA_OK;
+}
+
+// ----------------------------------------------------------------------- prediction
+extern "C" mra_status mra_predict(mra_plan* P, const double* qx, const double* qy, uint64_t nq, double* mean,
+                                  double* var) {
+    g_err.clear();
+    if (!P || !qx || !qy || !mean || !var) return fail(MRA_E_ARG, "NULL argument");
+    if (P->device < 0) return fail(MRA_E_CUDA, "host-only plan (device -2) cannot evaluate");
+    if (P->world > 1) return fail(MRA_E_CONFIG, "prediction on a sharded plan is not supported");
+    if (!P->post_valid)
+        return fail(MRA_E_ARG, "no posterior state: evaluate with posterior state (post->mu or post->smooth) first");
+    if (nq == 0) return MRA_OK;
+    if (cudaSetDevice(P->device) != cudaSuccess) return fail(MRA_E_CUDA, "cudaSetDevice failed");
+    const int M = P->M, J = P->J;
+    // leaf of each query by the plan's descent (half-open boxes); outside the root -> NaN
+    std::vector<long long> qleaf(nq);
+    for (uint64_t i = 0; i < nq; i++) {
+        const double px = qx[i], py = qy[i];
+        if (!std::isfinite(px) || !std::isfinite(py)) return fail(MRA_E_ARG, "non-finite query location");
+        if (!(px >= P->root[0] && px < P->root[1] && py >= P->root[2] && py < P->root[3])) { qleaf[i] = -1; continue; }
+        long long t = 0;
+        for (int m = 1; m < M; m++) {
+            const double* b = &P->box[4 * (lvl_first(J, m) + t)];
+            const double mx = 0.5 * (b[0] + b[1]), my = 0.5 * (b[2] + b[3]);
+            int c;
+            if (J == 4) c = (px >= mx ? 1 : 0) | (py >= my ? 2 : 0);
+            else if ((b[1] - b[0]) >= (b[3] - b[2])) c = px >= mx ? 1 : 0;
+            else c = py >= my ? 1 : 0;
+            t = t * J + c;
+        }
+        qleaf[i] = t;
+    }
+    std::vector<long long> qoff(P->nleaf + 1, 0);
+    for (uint64_t i = 0; i < nq; i++) if (qleaf[i] >= 0) qoff[qleaf[i] + 1]++;
+    std::vector<long long> leaves;
+    for (long long l = 0; l < P->nleaf; l++) {
+        if (qoff[l + 1]) leaves.push_back(l);
+        qoff[l + 1] += qoff[l];
+    }
+    const long long nin = qoff[P->nleaf];
+    std::vector<long long> fillp(qoff.begin(), qoff.end() - 1), qperm(std::max<long long>(nin, 1));
+    std::vector<double> qxy(2 * std::max<long long>(nin, 1));
+    for (uint64_t i = 0; i < nq; i++)
+        if (qleaf[i] >= 0) {
+            const long long d = fillp[qleaf[i]]++;
+            qperm[d] = (long long)i;
+            qxy[2 * d] = qx[i];
+            qxy[2 * d + 1] = qy[i];
+        }
+    mra_status s;
+    // per-CTA workspace: the leaf's G, Sigma, inverted diagonal blocks, r, and the query tiles
+    if (!P->ws_pred) {
+        const int Pg = (M - 1) * P->rh;
+        WsLayout L{};
+        const long long mleaf = std::max<long long>(P->max_leaf, 1);
+        L.ldG = (int)round_up(Pg + 1, 2);
+        L.ldS = (int)round_up(mleaf, 2);
+        long long o = 0;
+        L.oG = o; o += round_up(mleaf * L.ldG, 32);
+        L.oS = o; o += round_up(mleaf * (long long)L.ldS, 32);
+        L.oD = o; o += ((mleaf + 63) / 64) * 4096;
+        L.oV = o; o += round_up(mleaf, 32);
+        L.oQ = o; o += round_up(64LL * L.ldG, 32);
+        L.oE = o; o += round_up(mleaf * 64, 32);
+        L.oW = o; o += round_up(64LL * L.ldG, 32);
+        L.oA = L.oF = L.oL = 0;
+        L.stride = round_up(o, 64);
+        size_t freeb = 0, totalb = 0;
+        cudaMemGetInfo(&freeb, &totalb);
+        long long slots = std::min<long long>(P->grid, std::max<long long>(1, (long long)(0.4 * freeb / (8.0 * L.stride))));
+        P->Lp = L;
+        P->pred_grid = (int)slots;
+        if ((s = dalloc(P, (void**)&P->ws_pred, 8 * L.stride * slots, "prediction workspace"))) return s;
+    }
+    double *d_qxy = nullptr, *d_mean = nullptr, *d_var = nullptr;
+    long long *d_qoff = nullptr, *d_qperm = nullptr, *d_leaves = nullptr;
+    auto release = [&]() {
+        cudaFree(d_qxy); cudaFree(d_mean); cudaFree(d_var); cudaFree(d_qoff); cudaFree(d_qperm); cudaFree(d_leaves);
+    };
+#define PCU(call)                                                                              \
+    do {                                                                                       \
+        cudaError_t e_ = (call);                                                               \
+        if (e_ != cudaSuccess) {                                                               \
+            release();                                                                         \
+            return fail(e_ == cudaErrorMemoryAllocation ? MRA_E_OOM : MRA_E_CUDA,              \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));                   \
+        }                                                                                      \
+    } while (0)
+    PCU(cudaMalloc(&d_qxy, 16 * std::max<long long>(nin, 1)));
+    PCU(cudaMalloc(&d_mean, 8 * nq));
+    PCU(cudaMalloc(&d_var, 8 * nq));
+    PCU(cudaMalloc(&d_qoff, 8 * (P->nleaf + 1)));
+    PCU(cudaMalloc(&d_qperm, 8 * std::max<long long>(nin, 1)));
+    PCU(cudaMalloc(&d_leaves, 8 * std::max<size_t>(leaves.size(), 1)));
+    PCU(cudaMemcpyAsync(d_qxy, qxy.data(), 16 * std::max<long long>(nin, 1), cudaMemcpyHostToDevice, P->st));
+    PCU(cudaMemcpyAsync(d_qoff, qoff.data(), 8 * (P->nleaf + 1), cudaMemcpyHostToDevice, P->st));
+    PCU(cudaMemcpyAsync(d_qperm, qperm.data(), 8 * std::max<long long>(nin, 1), cudaMemcpyHostToDevice, P->st));
+    if (!leaves.empty())
+        PCU(cudaMemcpyAsync(d_leaves, leaves.data(), 8 * leaves.size(), cudaMemcpyHostToDevice, P->st));
+    PCU(launch_fill(d_mean, (long long)nq, NAN, P->st));
+    PCU(launch_fill(d_var, (long long)nq, NAN, P->st));
+    PCU(cudaMemsetAsync(P->err, 0, 16, P->st));
+    PCU(cudaMemsetAsync(P->counters, 0, 8, P->st));
+    TreeParams tp = tree_params(P, &P->post_theta);
+    tp.post = P->post;
+    PredParams pp{};
+    pp.qxy = d_qxy; pp.q_off = d_qoff; pp.q_perm = d_qperm; pp.leaves = d_leaves;
+    pp.n_leaves = (long long)leaves.size(); pp.muhat = P->muhat; pp.mean = d_mean; pp.var = d_var;
+    P->launches = 0;
+    PCU(launch_predict(tp, pp, P->pred_grid, P->ws_pred, P->Lp, P->counters, P->st));
+    P->launches++;
+    PCU(cudaMemcpyAsync(mean, d_mean, 8 * nq, cudaMemcpyDeviceToHost, P->st));
+    PCU(cudaMemcpyAsync(var, d_var, 8 * nq, cudaMemcpyDeviceToHost, P->st));
+    int h[4];
+    PCU(cudaMemcpyAsync(h, P->err, 16, cudaMemcpyDeviceToHost, P->st));
+    PCU(cudaStreamSynchronize(P->st));
+#undef PCU
+    release();
+    if (h[0]) return fail(MRA_E_NUMERIC, "Cholesky failed while recomputing a leaf for prediction");
     return MRA_OK;
 }
 

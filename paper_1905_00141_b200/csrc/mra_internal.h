@@ -36,7 +36,20 @@ struct TreeParams {
 struct WsLayout {
     long long stride;           // doubles per CTA slot
     long long oG, oS, oD, oA, oF, oL, oV;
+    long long oQ, oE, oW;       // prediction: query basis tile, L^{-1} C_M(S, P) tile, chain solve tile
     int ldG, ldS, ldA;
+};
+
+// prediction (mra_predict): queries sorted by leaf
+struct PredParams {
+    const double* qxy;          // [2 nq] interleaved (x, y), leaf-sorted
+    const long long* q_off;     // [n_leaves + 1] CSR offsets of each leaf's queries
+    const long long* q_perm;    // [nq] sorted position -> caller's query index
+    const long long* leaves;    // leaves that hold queries
+    long long n_leaves;
+    const double* muhat;        // whitened posterior means per interior region (k_mu)
+    double* mean;               // [nq] outputs, caller's order
+    double* var;
 };
 
 // wide (big-leaf) path buffers: G rows indexed by sorted observation, Sigma / inverted diagonal
@@ -83,6 +96,8 @@ cudaError_t launch_smooth(const TreeParams& tp, const double* muhat, const long 
                           int grid, double* ws, const WsLayout& L, unsigned long long* counter,
                           cudaStream_t st);
 cudaError_t launch_fill(double* p, long long n, double v, cudaStream_t st);
+cudaError_t launch_predict(const TreeParams& tp, const PredParams& pp, int grid, double* ws, const WsLayout& L,
+                           unsigned long long* counter, cudaStream_t st);
 // wide path: phase 0 chain, 1 sigma, 2 column update (step), 3 diagonal (step), 4 panel + X row (step),
 // 5 G = X [V | y]
 cudaError_t launch_wide(int phase, const TreeParams& tp, const WideParams& wp, int step, const int4* tasks,

@@ -425,6 +425,128 @@ k_smooth(TreeParams tp, const double* muhat, const long long* perm, double* smoo
 }
 
 
+// ---------------------------------------------------------------- prediction
+// Posterior mean and variance of the noise-free X at query points P of leaf j (the
+// "prediction" mode of PAPER.md:228; oracle: predict_all). With the whitened basis v(p) = V(p) of the
+// query (same chain as the observations), E = L_j^{-1} C_M(S_j, P), C_M(S, P) = C(S, P) - V_S V(P)^T:
+//   mean(p) = v(p) muhat + E_p^T (g - G_V muhat)
+//   var(p)  = sigma^2 - |v(p)|^2 - |E_p|^2 + |U^{-T} b(p)|^2,  b(p) = v(p) - G_V^T E_p,
+// where U^{-T} is the back substitution along the ancestor chain with the merge factors kept by the
+// posterior pass (Ltilde^{-1} and F = H^T per region): s_m = Li_m b_m, s_k = Li_k (b_k - sum_{j>k} F_j[k] s_j)
+// (the chain's posterior covariance, the paper's BTilde, is U^{-1} U^{-T} in the whitened basis).
+__global__ void __launch_bounds__(NT, MRA_MINB)
+k_predict(TreeParams tp, PredParams pp, double* ws, WsLayout L, unsigned long long* counter) {
+    extern __shared__ double smem[];
+    const CovP cp = to_covp(tp.cp);
+    const int M = tp.M, J = tp.J, rh = tp.rh, m = M - 1, Pg = m * rh, ncol = Pg + 1;
+    double* base = ws + (long long)blockIdx.x * L.stride;
+    double *G = base + L.oG, *S = base + L.oS, *D = base + L.oD, *r = base + L.oV, *Q = base + L.oQ,
+           *E = base + L.oE, *W = base + L.oW;
+    FacSmem f = fac_smem(smem);
+    auto mu_chain = [&](long long t, int col) -> double {   // muhat of the ancestor owning G column col
+        const int b = col / rh, lev = m - b;
+        const long long anc = lvl_first(J, lev) + (t >> (tp.lj * (m - lev)));
+        return pp.muhat[anc * rh + (col - b * rh)];
+    };
+    for (;;) {
+        const long long it = next_item(counter, smem);
+        if (it >= pp.n_leaves) break;
+        if (threadIdx.x == 0) *f.bad = 0;
+        const long long l = pp.leaves[it];
+        const long long t = (M == 1) ? 0 : (l >> tp.lj);
+        const long long o0 = tp.leaf_off[l];
+        const int n = (int)(tp.leaf_off[l + 1] - o0);
+        const double* pts = tp.pxy + 2 * o0;
+        if (n > 0) {   // the leaf's posterior-pass quantities: G = L^{-1}[V | y], L (blocked), r = g - G_V muhat
+            point_chain(tp, m, t, n, pts, G, L.ldG, cp, smem);
+            for (int i = threadIdx.x; i < n; i += NT) G[(long long)i * L.ldG + Pg] = tp.zs[o0 + i];
+            __syncthreads();
+            cta_gemm<MEMN, MEMN, MEMN, MEMN>(n, n, 1, op_mem(G, L.ldG), op_mem(G, L.ldG), Pg, op_mem(G, L.ldG),
+                                             op_mem(G, L.ldG), 0, ci_cov(pts, pts, tp.tau2), -1.0, S, L.ldS, cp,
+                                             smem);
+            chol_blocked(S, n, L.ldS, D, cp, smem);
+            if (*f.bad && threadIdx.x == 0) set_err(tp.err, M, l);
+            fwd_subst(S, n, L.ldS, D, G, ncol, L.ldG, cp, smem);
+            for (int i = threadIdx.x; i < n; i += NT) {
+                double s = G[(long long)i * L.ldG + Pg];
+                for (int col = 0; col < Pg; col++) s -= G[(long long)i * L.ldG + col] * mu_chain(t, col);
+                r[i] = s;
+            }
+            __syncthreads();
+        }
+        const long long q0 = pp.q_off[l], nq = pp.q_off[l + 1] - q0;
+        for (long long qt = 0; qt < nq; qt += 64) {
+            const int nt = (int)min(64LL, nq - qt);
+            const double* qp = pp.qxy + 2 * (q0 + qt);
+            point_chain(tp, m, t, nt, qp, Q, L.ldG, cp, smem);   // v(p), rows of Q
+            if (n > 0) {
+                // E = L^{-1} C_M(S, P) = L^{-1} C(S, P) - G_V V(P)^T   (G already holds L^{-1} V)
+                cta_gemm<MEMN, MEMN, MEMN, MEMN>(n, nt, 0, op_mem(G, L.ldG), op_mem(Q, L.ldG), 0, op_mem(G, 0),
+                                                 op_mem(G, 0), 0, ci_cov(pts, qp, 0.0), 1.0, E, 64, cp, smem);
+                fwd_subst(S, n, L.ldS, D, E, nt, 64, cp, smem);
+                if (Pg > 0)
+                    cta_gemm<MEMN, MEMN, MEMN, MEMN>(n, nt, 0, op_mem(G, L.ldG), op_mem(Q, L.ldG), Pg, op_mem(G, 0),
+                                                     op_mem(G, 0), 0, ci_mem(E, 64), -1.0, E, 64, cp, smem);
+            }
+            __syncthreads();
+            double mean = 0.0, var = 0.0;
+            if (threadIdx.x < nt) {
+                const int i = threadIdx.x;
+                double vv = 0.0, ee = 0.0;
+                for (int col = 0; col < Pg; col++) {
+                    const double v = Q[(long long)i * L.ldG + col];
+                    mean += v * mu_chain(t, col);
+                    vv += v * v;
+                }
+                for (int k = 0; k < n; k++) {
+                    const double e = E[(long long)k * 64 + i];
+                    mean += e * r[k];
+                    ee += e * e;
+                }
+                var = cp.s2 - vv - ee;
+            }
+            if (m >= 1) {
+                // b = v - G_V^T E  (in place over Q)
+                if (n > 0)
+                    cta_gemm<MEMT, MEMT, MEMN, MEMN>(nt, Pg, 0, op_mem(E, 64), op_mem(G, L.ldG), n, op_mem(E, 0),
+                                                     op_mem(E, 0), 0, ci_mem(Q, L.ldG), -1.0, Q, L.ldG, cp, smem);
+                // chain back substitution, levels m..1 (G column block of level k: (m - k) rh)
+                for (int k = m; k >= 1; k--) {
+                    const int cb = (m - k) * rh, qk = (k - 1) * rh + 1;
+                    const long long ak = t >> (tp.lj * (m - k));
+                    const double* Lik = tp.post + tp.post_base[k] + ak * ((long long)rh * rh + (long long)qk * rh);
+                    const double* Tk = Q + cb;
+                    for (int j = k + 1; j <= m; j++) {
+                        const int qj = (j - 1) * rh + 1;
+                        const long long aj = t >> (tp.lj * (m - j));
+                        const double* Fj = tp.post + tp.post_base[j] + aj * ((long long)rh * rh + (long long)qj * rh) +
+                                           (long long)rh * rh + (long long)(j - 1 - k) * rh * rh;
+                        cta_gemm<MEMN, MEMN, MEMN, MEMN>(nt, rh, 0, op_mem(W + (m - j) * rh, L.ldG), op_mem(Fj, rh),
+                                                         rh, op_mem(Fj, 0), op_mem(Fj, 0), 0, ci_mem(Tk, L.ldG), -1.0,
+                                                         W + cb, L.ldG, cp, smem);
+                        Tk = W + cb;
+                    }
+                    cta_gemm<MEMN, MEMN, MEMN, MEMN>(nt, rh, 0, op_mem(Tk, L.ldG), op_mem(Lik, rh), rh,
+                                                     op_mem(Lik, 0), op_mem(Lik, 0), 0, ci_zero(), 1.0, W + cb, L.ldG,
+                                                     cp, smem);
+                }
+                __syncthreads();
+                if (threadIdx.x < nt)
+                    for (int col = 0; col < Pg; col++) {
+                        const double s2 = W[(long long)threadIdx.x * L.ldG + col];
+                        var += s2 * s2;
+                    }
+            }
+            if (threadIdx.x < nt) {
+                const long long dst = pp.q_perm[q0 + qt + threadIdx.x];
+                pp.mean[dst] = mean;
+                pp.var[dst] = var;
+            }
+            __syncthreads();
+        }
+    }
+}
+
 // ====================================================================== wide (big-leaf) path
 // Leaves too large for one CTA (C4: up to ~9k observations) are processed by all CTAs together,
 // phase by phase, from precomputed task lists: row-tile V chains, Sigma tiles, a
@@ -743,18 +865,18 @@ void phase_cycles(unsigned long long* out16, bool reset) {
 }
 
 static bool g_attr_done = false;
-static int g_resident[11] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1};   // resident CTAs per SM x SM count
+static int g_resident[12] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1};   // resident CTAs per SM x SM count
 static void set_attrs() {
     if (g_attr_done) return;
     const int b = smem_bytes();
-    const void* ks[11] = {(const void*)k_prior,       (const void*)k_bottom,      (const void*)k_merge,
+    const void* ks[12] = {(const void*)k_prior,       (const void*)k_bottom,      (const void*)k_merge,
                           (const void*)k_smooth,      (const void*)k_wide_chain,  (const void*)k_wide_sigma,
                           (const void*)k_wide_update, (const void*)k_wide_diag,   (const void*)k_wide_panel_x,
-                          (const void*)k_wide_trsm,   (const void*)k_wide_mtile};
+                          (const void*)k_wide_trsm,   (const void*)k_wide_mtile,  (const void*)k_predict};
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    for (int i = 0; i < 11; i++) {
+    for (int i = 0; i < 12; i++) {
         cudaFuncSetAttribute(ks[i], cudaFuncAttributeMaxDynamicSharedMemorySize, b);
         int per = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ks[i], NT, b);
@@ -864,6 +986,17 @@ cudaError_t launch_wide_mtile(const TreeParams& tp, const WideParams& wp, long l
     if (e != cudaSuccess) return e;
     (void)g_count;
     k_wide_mtile<<<grid, NT, smem_bytes(), st>>>(tp, wp, g_first, out, out_first, q, tasks, ntask, counter, ring);
+    return cudaGetLastError();
+}
+}  // namespace mra
+
+namespace mra {
+cudaError_t launch_predict(const TreeParams& tp, const PredParams& pp, int grid, double* ws, const WsLayout& L,
+                           unsigned long long* counter, cudaStream_t st) {
+    set_attrs();
+    grid = clamp_grid(grid, pp.n_leaves, 11);
+    if (grid < 1) return cudaSuccess;
+    k_predict<<<grid, NT, smem_bytes(), st>>>(tp, pp, ws, L, counter);
     return cudaGetLastError();
 }
 }  // namespace mra
