@@ -318,18 +318,31 @@ __device__ __noinline__ void cta_gemm_impl(double* smem) {
             const double alpha = d.alpha;
             double* C = d.C;
             const long long ldc = d.ldc;
+            // the (e = 0, 1) pair of a fragment is two adjacent columns: one 16-byte access when the
+            // whole pair is in range and aligned
+            const bool vec = ((reinterpret_cast<uintptr_t>(C) & 15) == 0) && ((ldc & 1) == 0) &&
+                             (ci.kind != 1 || (((reinterpret_cast<uintptr_t>(ci.p) & 15) == 0) && ((ci.ld & 1) == 0)));
 #pragma unroll
             for (int mi = 0; mi < 2; mi++)
 #pragma unroll
-                for (int ni = 0; ni < 4; ni++)
+                for (int ni = 0; ni < 4; ni++) {
+                    const int i = r0 + wr + mi * 8 + g, j = c0 + wc + ni * 8 + 2 * t;
+                    if (vec && i < Mr && j + 1 < Nc && (!lower || j + 1 <= i)) {
+                        double2 v = make_double2(0.0, 0.0);
+                        if (ci.kind == 1) v = *reinterpret_cast<const double2*>(ci.p + (long long)i * ci.ld + j);
+                        *reinterpret_cast<double2*>(C + (long long)i * ldc + j) =
+                            make_double2(v.x + alpha * acc[mi][ni][0], v.y + alpha * acc[mi][ni][1]);
+                    } else {
 #pragma unroll
-                    for (int e = 0; e < 2; e++) {
-                        const int i = r0 + wr + mi * 8 + g, j = c0 + wc + ni * 8 + 2 * t + e;
-                        if (i < Mr && j < Nc && (!lower || j <= i)) {
-                            const double v = (ci.kind == 1) ? ci.p[(long long)i * ci.ld + j] : 0.0;
-                            C[(long long)i * ldc + j] = v + alpha * acc[mi][ni][e];
+                        for (int e = 0; e < 2; e++) {
+                            const int jj = j + e;
+                            if (i < Mr && jj < Nc && (!lower || jj <= i)) {
+                                const double v = (ci.kind == 1) ? ci.p[(long long)i * ci.ld + jj] : 0.0;
+                                C[(long long)i * ldc + jj] = v + alpha * acc[mi][ni][e];
+                            }
                         }
                     }
+                }
             if (ci.kind == 2) {
                 const CovP cpl = d.cp;
                 // covariance initial value, added by the thread that stored the element (4 independent
