@@ -401,6 +401,25 @@ def run_gpu(args, rank, world, local_rank):
         cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": "oracle",
                "sample": f"{k} whole level-{lvl} subtrees ({o} obs) of {w.name}, oracle subtree mode, "
                          f"{sec:.1f} s CPU wall"}
+    pred = None
+    if world == 1 and args.predict > 0:
+        # NEXT-1: posterior mean / variance of X at random locations of the domain
+        rng = np.random.default_rng(7)
+        qx = rng.uniform(float(np.min(w.x)), float(np.max(w.x)), args.predict)
+        qy = rng.uniform(float(np.min(w.y)), float(np.max(w.y)), args.predict)
+        mra.mra_loglik(plan, zpin_np, thetas[0], posterior=True)
+        mra.mra_predict(plan, qx[:1000], qy[:1000])          # warm-up (workspace allocation)
+        ts = []
+        for _ in range(2):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            pm, pv = mra.mra_predict(plan, qx, qy)
+            ts.append(time.perf_counter() - t0)
+        tp_ = min(ts)
+        pred = {"queries": args.predict, "value": args.predict / tp_, "unit": "queries/s", "seconds": tp_,
+                "what": "mra_predict (host query arrays in, host mean/var out; leaf assignment + sort on the "
+                        "host, one k_predict launch) after a posterior-state evaluation of the same data",
+                "finite": int(np.sum(np.isfinite(pm))), "var_min": float(np.nanmin(pv))}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -412,6 +431,8 @@ def run_gpu(args, rank, world, local_rank):
             "kernel_ms": {k: round(kms[k], 3) for k in mra.KERNEL_CLASSES},
             "kernel_launches": {k: int(kcnt[k]) for k in mra.KERNEL_CLASSES},
             "roofline": roof, "cpu_baseline": cpu, "clocks": clocks}
+    if pred:
+        line["predict"] = pred
     print(json.dumps(line), flush=True)
 
 
@@ -429,6 +450,8 @@ def main():
     ap.add_argument("--dist-backend", default="nccl", help="process-group backend for N > 1 (nccl on a real "
                     "multi-GPU node; gloo + --same-device only to exercise the sharded path on one GPU)")
     ap.add_argument("--same-device", action="store_true", help="test only: every rank uses cuda:0")
+    ap.add_argument("--predict", type=int, default=0, help="also time mra_predict at this many random query "
+                    "locations (1 GPU; after one posterior-state evaluation); adds a 'predict' key")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
