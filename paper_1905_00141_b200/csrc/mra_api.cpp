@@ -470,7 +470,7 @@ static mra_status size_wide(mra_plan* P, double budget, bool explicit_budget) {
                     const double step_us = (1.0 + nrm + nrm * (nrm + 1) / 2.0) * std::max(kavg, 64.0) * 0.066 /
                                            std::max(1, P->grid);
                     const long long D1 = std::min<long long>(512, std::max<long long>(2, (long long)std::ceil(150.0 / step_us)));
-                    const long long D2 = D1 + 2;
+                    const long long D2 = D1 + 12;   // an O task waits for all F of its group before its GEMM
                     mt_D2 = std::max(mt_D2, D2);
                     ws.mt_off = (long long)tasks.size();
                     for (long long st = 0; st < gc + D2; st++) {
@@ -504,7 +504,7 @@ static mra_status size_wide(mra_plan* P, double budget, bool explicit_budget) {
         long long ns = std::min<long long>(maxgc, mt_D2 + 8);
         P->mring.ns = (int)ns;
         P->mring.maxg = maxgc;
-        P->mring.stride = round_up(4096 + (long long)rh * rh + (long long)qm * rh, 32);
+        P->mring.stride = round_up(4096 + (long long)rh * rh + 2LL * qm * rh, 32);   // A_oo | Li | F | -F
         if ((s = dalloc(P, (void**)&P->mring.slot, 8 * P->mring.stride * ns, "merge slots"))) return s;
         if ((s = dalloc(P, (void**)&P->mring.flags, 4 * 3 * maxgc, "merge flags"))) return s;
         P->mring.chol_done = P->mring.flags;
@@ -675,10 +675,10 @@ extern "C" mra_status mra_kernel_times(const mra_plan* P, double* ms, uint64_t* 
 }
 
 // diagnostics of -DMRA_PHASE_TIMING builds (zeros otherwise): CTA-cycles per bottom-kernel phase
-extern "C" void mra_debug_phase_cycles(uint64_t* out16, int reset) {
-    unsigned long long v[16];
+extern "C" void mra_debug_phase_cycles(uint64_t* out32, int reset) {
+    unsigned long long v[32];
     phase_cycles(v, reset != 0);
-    for (int i = 0; i < 16; i++) out16[i] = v[i];
+    for (int i = 0; i < 32; i++) out32[i] = v[i];
 }
 
 extern "C" mra_status mra_plan_shards(const mra_plan* P, int* shard_level, int64_t* own, uint64_t* n_own) {

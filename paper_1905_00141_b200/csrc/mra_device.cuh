@@ -630,7 +630,7 @@ __device__ __forceinline__ void store_block_full(const double* x, double* A, lon
 // Blocked right-looking Cholesky of S (n x n, lower, ld) in place; Dinv receives the inverted
 // 64x64 diagonal blocks (block b at Dinv + b*4096, ld 64). Returns log|S| (all threads).
 // optional phase timing (build with -DMRA_PHASE_TIMING): CTA-cycles per phase of the bottom kernel
-__device__ unsigned long long g_phase_cycles[16];
+__device__ unsigned long long g_phase_cycles[32];
 #ifdef MRA_PHASE_TIMING
 #define CPHASE_MARK(var) long long var = clock64()
 #define CPHASE_ADD(idx, from) do { if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[idx], (unsigned long long)(clock64() - (from))); } while (0)

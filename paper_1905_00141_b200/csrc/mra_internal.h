@@ -68,7 +68,7 @@ struct WideParams {
 
 // per-group small slots (Li, F) and dependency counters of the level-(M-1) merge tile dataflow
 struct MergeRing {
-    double* slot;           // ns slots of stride doubles: [A_oo 64x64 | Li rh x rh | F q x rh]
+    double* slot;           // ns slots of stride doubles: [A_oo 64x64 | Li rh x rh | F q x rh | -F q x rh]
     long long stride;
     int ns;
     long long maxg;         // groups per launch (counter arrays)
@@ -106,6 +106,6 @@ cudaError_t launch_wide_mtile(const TreeParams& tp, const WideParams& wp, long l
                               double* out, long long out_first, int q, const int4* tasks, long long ntask, int grid,
                               unsigned long long* counter, const MergeRing& ring, cudaStream_t st);
 int smem_bytes();
-void phase_cycles(unsigned long long* out16, bool reset);   // -DMRA_PHASE_TIMING builds only
+void phase_cycles(unsigned long long* out32, bool reset);   // -DMRA_PHASE_TIMING builds only
 
 }  // namespace mra

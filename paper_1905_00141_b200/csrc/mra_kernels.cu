@@ -727,7 +727,8 @@ k_wide_trsm(TreeParams tp, WideParams wp, const int4* tasks, long long ntask, un
 // the y column; q = |r|):
 //   type 0  T00(g):   A_oo = G_o^T G_o, Lt = chol(I + A_oo), Li = Lt^{-1}, log|I + A_oo|, leaf d/u
 //   type 1  F(g, a):  F_a = (G_r,a^T G_o) Li^T    (waits for T00(g), which owns the slot once it runs)
-//   type 2  O(g,a,b): O_ab = G_r,a^T G_r,b - F_a F_b^T  -> output        (waits for every F(g, .))
+//   type 2  O(g,a,b): O_ab = G_r,a^T G_r,b - F_a F_b^T  -> output   (waits for every F(g, .), then ONE
+//                     two-segment GEMM with -F kept beside F)
 // i.e. Atilde = G^T G and the merge O = A_rr - A_ro (I + A_oo)^{-1} A_or without ever storing A_rr.
 // The host staggers the three task kinds (T00 of group s, F of group s - D1, O of group s - D2) so a
 // dependency is normally complete when its consumer is claimed; waits spin on counters of tasks
@@ -752,10 +753,12 @@ k_wide_mtile(TreeParams tp, WideParams wp, long long g_first, double* out, long 
         double* Aoo = ring.slot + (long long)slot * ring.stride;
         double* Li = Aoo + 4096;
         double* F = Li + rh * rh;
+        double* Fn = F + (long long)q * rh;   // -F, so an O tile is ONE two-segment GEMM
         const long long o = tp.leaf_off[g * J];
         const int ng = (int)(tp.leaf_off[g * J + J] - o);
         const double* G = wp.G + (o - wp.G_base) * wp.ldG;
         const long long id = lvl_first(J, m) + g;
+        PHASE_MARK(ph0);
         if (tk.y == 0) {
             if (gi >= ring.ns) {   // the group NS earlier must have released the slot
                 if (threadIdx.x == 0) {
@@ -803,6 +806,10 @@ k_wide_mtile(TreeParams tp, WideParams wp, long long g_first, double* out, long 
                 __threadfence();
                 atomicExch(ring.chol_done + gi, 1);
             }
+            PHASE_ADD(16, ph0);
+#ifdef MRA_PHASE_TIMING
+            if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[17], 1ULL);
+#endif
         } else if (tk.y == 1) {
             const int a = tk.z, r0 = 64 * a, nrow = min(64, q - r0);
             double* Fa = F + (long long)r0 * rh;
@@ -812,16 +819,41 @@ k_wide_mtile(TreeParams tp, WideParams wp, long long g_first, double* out, long 
                 __threadfence();
             }
             __syncthreads();
+            PHASE_ADD(19, ph0);
+            PHASE_MARK(ph1);
             cta_gemm<MEMT, MEMT, MEMN, MEMN>(nrow, rh, 0, op_mem(G + rh + r0, wp.ldG), op_mem(G, wp.ldG), ng,
                                              op_mem(G, 0), op_mem(G, 0), 0, ci_zero(), 1.0, Fa, rh, cp, smem);
+            PHASE_ADD(18, ph1);
+            PHASE_MARK(ph2);
             cta_gemm<MEMN, MEMN, MEMN, MEMN>(nrow, rh, 0, op_mem(Fa, rh), op_mem(Li, rh), rh, op_mem(Fa, 0),
                                              op_mem(Fa, 0), 0, ci_zero(), 1.0, Fa, rh, cp, smem);
-            if (tp.post) {
-                double* P = tp.post + tp.post_base[m] + g * ((long long)rh * rh + (long long)q * rh) + rh * rh +
-                            (long long)r0 * rh;
-                for (int e = threadIdx.x; e < nrow * rh; e += NT) P[e] = Fa[e];
+            {
+                double* Fna = Fn + (long long)r0 * rh;
+                double* P = tp.post ? tp.post + tp.post_base[m] + g * ((long long)rh * rh + (long long)q * rh) +
+                                          rh * rh + (long long)r0 * rh
+                                    : nullptr;
+                // all loads first (Fa / Fna / P may alias as far as the compiler knows: interleaved
+                // load-store pairs would serialise on the L2 latency)
+                double v[16];
+#pragma unroll
+                for (int u = 0; u < 16; u++) {
+                    const int e = threadIdx.x + u * NT;
+                    v[u] = (e < nrow * rh) ? __ldcg(Fa + e) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 16; u++) {
+                    const int e = threadIdx.x + u * NT;
+                    if (e < nrow * rh) {
+                        Fna[e] = -v[u];
+                        if (P) P[e] = v[u];
+                    }
+                }
             }
             __syncthreads();
+            PHASE_ADD(20, ph2);
+#ifdef MRA_PHASE_TIMING
+            if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[21], 1ULL);
+#endif
             if (threadIdx.x == 0) {
                 __threadfence();
                 atomicAdd(ring.f_done + gi, 1);
@@ -830,17 +862,23 @@ k_wide_mtile(TreeParams tp, WideParams wp, long long g_first, double* out, long 
             const int a = tk.z, b = tk.w, r0 = 64 * a, c0 = 64 * b;
             const int nrow = min(64, q - r0), ncl = min(64, q - c0);
             double* Oab = out + (g - out_first) * (long long)q * q + (long long)r0 * q + c0;
-            cta_gemm<MEMT, MEMT, MEMN, MEMN>(nrow, ncl, a == b, op_mem(G + rh + r0, wp.ldG),
-                                             op_mem(G + rh + c0, wp.ldG), ng, op_mem(G, 0), op_mem(G, 0), 0,
-                                             ci_zero(), 1.0, Oab, q, cp, smem);
+            // every F of the group is final (the host schedules O tasks ~6 steps after the F tasks)
             if (threadIdx.x == 0) {
                 while (*(volatile int*)(ring.f_done + gi) < nr) __nanosleep(100);
                 __threadfence();
             }
             __syncthreads();
-            cta_gemm<MEMN, MEMN, MEMN, MEMN>(nrow, ncl, a == b, op_mem(F + (long long)r0 * rh, rh),
-                                             op_mem(F + (long long)c0 * rh, rh), rh, op_mem(F, 0), op_mem(F, 0), 0,
-                                             ci_mem(Oab, q), -1.0, Oab, q, cp, smem);
+            PHASE_ADD(23, ph0);
+            PHASE_MARK(ph2);
+            // O_ab = G_r,a^T G_r,b + (-F_a) F_b^T   (K = n_group, then K = rh)
+            cta_gemm<MEMT, MEMT, MEMN, MEMN>(nrow, ncl, a == b, op_mem(G + rh + r0, wp.ldG),
+                                             op_mem(G + rh + c0, wp.ldG), ng, op_mem(Fn + (long long)r0 * rh, rh),
+                                             op_mem(F + (long long)c0 * rh, rh), rh, ci_zero(), 1.0, Oab, q, cp,
+                                             smem);
+            PHASE_ADD(24, ph2);
+#ifdef MRA_PHASE_TIMING
+            if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[25], 1ULL);
+#endif
             if (threadIdx.x == 0) {
                 if (a == nr - 1 && b == nr - 1) tp.ureg[id] = Oab[(long long)(nrow - 1) * q + ncl - 1];
                 __threadfence();
@@ -856,10 +894,10 @@ k_wide_mtile(TreeParams tp, WideParams wp, long long g_first, double* out, long 
 // ------------------------------------------------------------------------ launchers
 int smem_bytes() { return SMEM_DBL * (int)sizeof(double); }
 
-void phase_cycles(unsigned long long* out16, bool reset) {
-    cudaMemcpyFromSymbol(out16, g_phase_cycles, sizeof(unsigned long long) * 16);
+void phase_cycles(unsigned long long* out32, bool reset) {
+    cudaMemcpyFromSymbol(out32, g_phase_cycles, sizeof(unsigned long long) * 32);
     if (reset) {
-        unsigned long long z[16] = {0};
+        unsigned long long z[32] = {0};
         cudaMemcpyToSymbol(g_phase_cycles, z, sizeof z);
     }
 }

@@ -34,7 +34,7 @@ for i in range(a.evals):
     torch.cuda.synchronize()
     print(f"eval {i}: loglik={ll:.10f} {1e3 * (time.time() - t):.1f} ms launches={mra.mra_last_launches(plan)}")
 import ctypes  # noqa: E402
-cyc = (ctypes.c_uint64 * 16)()
+cyc = (ctypes.c_uint64 * 32)()
 mra._lib.mra_debug_phase_cycles(cyc, 1)
 tot = sum(cyc[:6])
 if tot:
@@ -44,3 +44,7 @@ if tot:
         *(100 * cyc[i] / tot for i in (6, 7, 8))))
     print(f"  chol_inv_small calls={cyc[11]} cycles/call={cyc[10] / max(1, cyc[11]):.0f} load_block cycles/call={cyc[9] / max(1, cyc[11]):.0f}; "
           f"bottom kernel CTA-cycles={cyc[12]:.3g} phase sum={tot:.3g}")
+if cyc[17] or cyc[21]:
+    per = lambda a, b: cyc[a] / max(1, cyc[b])
+    print(f"mtile per task (CTA cycles): T00 {per(16, 17):.0f} (n={cyc[17]}); F: wait {per(19, 21):.0f} gemm1 {per(18, 21):.0f} "
+          f"gemm2 {per(20, 21):.0f} (n={cyc[21]}); O: gemm1 {per(22, 25):.0f} wait {per(23, 25):.0f} gemm2 {per(24, 25):.0f} (n={cyc[25]})")
