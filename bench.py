@@ -68,8 +68,12 @@ def class_flops(leaf_sizes, M, J, r):
     n = n[n > 0]
     P = M - 1
     Pr = P * r
+    # leaves with n <= ncol are solved through the explicit inverse by k_wide_trsm ("solve"); larger leaves
+    # by the blocked substitution interleaved with their factorization ("factor"), DESIGN.md §5
+    xm = n <= Pr + 1
     out = {"chain": float(np.sum(P * P * n * r * r)), "sigma": float(np.sum(n * (n + 1) * Pr)),
-           "factor": float(np.sum(n ** 3 / 3.0)), "solve": float(np.sum(n * n * (Pr + 1))),
+           "factor": float(np.sum(n ** 3 / 3.0) + np.sum((n * n * (Pr + 1))[~xm])),
+           "solve": float(np.sum((n * n * (Pr + 1))[xm])),
            "syrk_merge": float(np.sum(Pr * (Pr + 1) * n + 2 * Pr * n + 2 * n))}
     prior = merge = 0.0
     for m in range(1, M):

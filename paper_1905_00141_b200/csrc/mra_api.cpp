@@ -86,7 +86,7 @@ struct mra_plan {
     struct WideSub {
         long long g0 = 0, gcount = 0;
         long long chain_off = 0, chain_n = 0, sigma_off = 0, sigma_n = 0;
-        std::vector<long long> upd_off, upd_n, diag_off, diag_n, pf_off, pf_n;
+        std::vector<long long> upd_off, upd_n, diag_off, diag_n, pf_off, pf_n, tr_off, tr_n;
         long long trsm_off = 0, trsm_n = 0, mt_off = 0, mt_n = 0;
     };
     std::vector<WideSub> wsubs;
@@ -381,6 +381,7 @@ static mra_status size_wide(mra_plan* P, double budget, bool explicit_budget) {
     // G = L^{-1}[V | y] through the explicit inverse X (one launch, no per-step solves) when forming X
     // (~n^3/3) costs at most about the solve itself (n^2 ncol / 2); blocked substitution otherwise
     auto xmode = [&](long long l) { return leaf_n(l) <= ncol; };
+    constexpr int NBS = 8;   // super-block of the leaf Cholesky, in 64-blocks
     std::vector<int4> tasks;
     std::vector<long long> S_off(P->nleaf, 0), D_off(P->nleaf, 0);
     std::vector<int> S_ld(P->nleaf, 2);
@@ -429,12 +430,16 @@ static mra_status size_wide(mra_plan* P, double budget, bool explicit_budget) {
                         for (int k = 0; k <= i; k++) tasks.push_back(make_int4((int)l, i, k, 0));
                 }
                 ws.sigma_n = (long long)tasks.size() - ws.sigma_off;
+                // super-blocked Cholesky of the leaves' Sigma_j (blocks of 64, super-blocks of NBS blocks):
+                // left-looking inside a super-block, one right-looking trailing update after it, so the
+                // late steps of large leaves (C4: up to 139 blocks) keep every CTA busy with K = 64 NBS
                 for (int st = 0; st < Tmax; st++) {
+                    const int kb0 = st / NBS * NBS;
                     ws.upd_off.push_back((long long)tasks.size());
-                    if (st > 0)
+                    if (st > kb0)
                         for (long long l = ws.g0 * J; l < (ws.g0 + ws.gcount) * J; l++) {
                             const int T = (int)((leaf_n(l) + 63) / 64);
-                            for (int i = st; i < T; i++) tasks.push_back(make_int4((int)l, i, 0, 0));
+                            for (int i = st; i < T; i++) tasks.push_back(make_int4((int)l, i, st, 0));
                         }
                     ws.upd_n.push_back((long long)tasks.size() - ws.upd_off.back());
                     ws.diag_off.push_back((long long)tasks.size());
@@ -454,6 +459,17 @@ static mra_status size_wide(mra_plan* P, double budget, bool explicit_budget) {
                             for (int c2 = 0; c2 < nct; c2++) tasks.push_back(make_int4((int)l, c2, 1, 0));
                     }
                     ws.pf_n.push_back((long long)tasks.size() - ws.pf_off.back());
+                    ws.tr_off.push_back((long long)tasks.size());
+                    if (st == kb0 + NBS - 1)
+                        for (long long l = ws.g0 * J; l < (ws.g0 + ws.gcount) * J; l++) {
+                            const int T = (int)((leaf_n(l) + 63) / 64);
+                            for (int i = st + 1; i < T; i++) {
+                                for (int j = st + 1; j <= i; j++) tasks.push_back(make_int4((int)l, i, j, 0));
+                                if (!xmode(l))
+                                    for (int c2 = 0; c2 < nct; c2++) tasks.push_back(make_int4((int)l, i, c2, 1));
+                            }
+                        }
+                    ws.tr_n.push_back((long long)tasks.size() - ws.tr_off.back());
                 }
                 // G = X [V | y], one task per (leaf, column tile) after the factorization
                 ws.trsm_off = (long long)tasks.size();
@@ -757,6 +773,7 @@ static mra_status eval_wide(mra_plan* P, const TreeParams& tp, long long gf, lon
     WideParams wp;
     wp.G = P->wG; wp.ldG = P->wldG; wp.S = P->wS; wp.S_off = P->wS_off; wp.S_ld = P->wS_ld;
     wp.D = P->wD; wp.D_off = P->wD_off; wp.lblk = P->wlblk;
+    wp.kb0 = wp.kb1 = 0;
     const int q = (int)q_of(P->M - 1, P->rh);
     cudaStream_t st = P->st;
     long long done = 0;
@@ -767,7 +784,11 @@ static mra_status eval_wide(mra_plan* P, const TreeParams& tp, long long gf, lon
         wp.G_base = P->leaf_off[w.g0 * P->J];
         LCHK_K(KIND_CHAIN, launch_wide(0, tp, wp, 0, P->wtasks + w.chain_off, w.chain_n, P->grid, take_counter(P), st));
         LCHK_K(KIND_SIGMA, launch_wide(1, tp, wp, 0, P->wtasks + w.sigma_off, w.sigma_n, P->grid, take_counter(P), st));
+        constexpr int NBS = 8;   // as in size_wide
         for (size_t s2 = 0; s2 < w.diag_n.size(); s2++) {
+            const int kb0 = (int)s2 / NBS * NBS;
+            wp.kb0 = kb0;
+            wp.kb1 = (int)s2;
             if (w.upd_n[s2] > 0)
                 LCHK_K(KIND_FACTOR, launch_wide(2, tp, wp, (int)s2, P->wtasks + w.upd_off[s2], w.upd_n[s2], P->grid,
                                                 take_counter(P), st));
@@ -775,6 +796,11 @@ static mra_status eval_wide(mra_plan* P, const TreeParams& tp, long long gf, lon
                                             take_counter(P), st));
             LCHK_K(KIND_FACTOR, launch_wide(4, tp, wp, (int)s2, P->wtasks + w.pf_off[s2], w.pf_n[s2], P->grid,
                                             take_counter(P), st));
+            if (w.tr_n[s2] > 0) {
+                wp.kb1 = kb0 + NBS;
+                LCHK_K(KIND_FACTOR, launch_wide(2, tp, wp, (int)s2, P->wtasks + w.tr_off[s2], w.tr_n[s2], P->grid,
+                                                take_counter(P), st));
+            }
         }
         if (w.trsm_n > 0)
             LCHK_K(KIND_SOLVE, launch_wide(5, tp, wp, 0, P->wtasks + w.trsm_off, w.trsm_n, P->grid, take_counter(P), st));

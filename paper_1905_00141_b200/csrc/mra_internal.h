@@ -64,6 +64,8 @@ struct WideParams {
     double* D;
     const long long* D_off;   // multiple of 4096; block log-det of (leaf, s) at lblk[D_off/4096 + s]
     double* lblk;
+    int kb0, kb1;             // K range [64 kb0, 64 kb1) of the update / substitution tasks of this launch
+                              // (super-blocked Cholesky: kb0 = first block of the current super-step)
 };
 
 // per-group small slots (Li, F) and dependency counters of the level-(M-1) merge tile dataflow

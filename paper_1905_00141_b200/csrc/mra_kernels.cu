@@ -83,10 +83,15 @@ __device__ void point_chain(const TreeParams& tp, int m, long long t, int n, con
         const long long akid = lvl_first(tp.J, k) + ak;
         const long long ldk = (long long)k * rh;
         const double* Rk = chain_row(tp, k, ak);
+        PHASE_MARK(pc0);
         cta_gemm<COVK, MEMN, MEMN, MEMN>(n, rh, 0, op_cov(pts, tp.kxy + 2 * akid * rh),
                                          op_mem(Rk, ldk), rh, op_mem(Gc + (long long)(m - k + 1) * rh, ldg),
                                          op_mem(Rk + rh, ldk), (k - 1) * rh, ci_zero(), 1.0,
                                          Gc + (long long)(m - k) * rh, ldg, cp, smem);
+        PHASE_ADD(26, pc0);
+#ifdef MRA_PHASE_TIMING
+        if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[27], (unsigned long long)k);   // sum of k (= K / rh)
+#endif
     }
 }
 
@@ -572,8 +577,13 @@ k_wide_chain(TreeParams tp, WideParams wp, const int4* tasks, long long ntask, u
         const long long o0 = tp.leaf_off[l] + 64LL * tk.y;
         const int n = min(64, leaf_n(tp, l) - 64 * tk.y);
         double* Gr = wp.G + (o0 - wp.G_base) * wp.ldG;
+        PHASE_MARK(pt0);
         point_chain(tp, m, l >> tp.lj, n, tp.pxy + 2 * o0, Gr, wp.ldG, cp, smem);
         for (int i = threadIdx.x; i < n; i += NT) Gr[(long long)i * wp.ldG + Pg] = tp.zs[o0 + i];
+        PHASE_ADD(28, pt0);
+#ifdef MRA_PHASE_TIMING
+        if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[29], 1ULL);
+#endif
     }
 }
 
@@ -602,11 +612,20 @@ k_wide_sigma(TreeParams tp, WideParams wp, const int4* tasks, long long ntask, u
     }
 }
 
-// left-looking column update at step s: A_is -= L_{i,<s} L_{s,<s}^T  (i >= s, s >= 1)
+// Updates of the super-blocked Cholesky (blocks of 64, super-blocks of NB blocks), K range
+// [64 kb0, 64 kb1) of the launch:
+//   type 0 (leaf, i, j): A_ij -= L_{i,K} L_{j,K}^T   (i >= j; lower when i == j) -- the left-looking update
+//          of step j inside a super-block (K = the super-block's columns left of j), or the right-looking
+//          trailing update after a super-block (K = its NB columns)
+//   type 1 (leaf, i, c): G_i[:, c] -= L_{i,K} G_K[:, c] -- trailing update of the blocked substitution
+//          (leaves solved without the explicit inverse)
 __global__ void __launch_bounds__(NT, MRA_MINB)
 k_wide_update(TreeParams tp, WideParams wp, int s, const int4* tasks, long long ntask, unsigned long long* counter) {
     extern __shared__ double smem[];
     const CovP cp = to_covp(tp.cp);
+    const int ncol = (tp.M - 1) * tp.rh + 1;
+    const int k0 = 64 * wp.kb0, K = 64 * (wp.kb1 - wp.kb0);
+    (void)s;
     for (;;) {
         const long long it = next_item(counter, smem);
         if (it >= ntask) break;
@@ -614,12 +633,23 @@ k_wide_update(TreeParams tp, WideParams wp, int s, const int4* tasks, long long 
         const long long l = tk.x;
         const int i = tk.y, n = leaf_n(tp, l), ld = wp.S_ld[l];
         double* Sl = wp.S + wp.S_off[l];
-        double* C = Sl + 64LL * i * ld + 64LL * s;
-        const double* Ai = Sl + 64LL * i * ld;
-        const double* As = Sl + 64LL * s * ld;
-        cta_gemm<MEMN, MEMN, MEMN, MEMN>(min(64, n - 64 * i), min(64, n - 64 * s), i == s, op_mem(Ai, ld),
-                                         op_mem(As, ld), 64 * s, op_mem(Ai, 0), op_mem(Ai, 0), 0, ci_mem(C, ld), -1.0,
-                                         C, ld, cp, smem);
+        const double* Ai = Sl + 64LL * i * ld + k0;
+        if (tk.w == 0) {
+            const int j = tk.z;
+            double* C = Sl + 64LL * i * ld + 64LL * j;
+            const double* Aj = Sl + 64LL * j * ld + k0;
+            cta_gemm<MEMN, MEMN, MEMN, MEMN>(min(64, n - 64 * i), min(64, n - 64 * j), i == j, op_mem(Ai, ld),
+                                             op_mem(Aj, ld), K, op_mem(Ai, 0), op_mem(Ai, 0), 0, ci_mem(C, ld), -1.0,
+                                             C, ld, cp, smem);
+        } else {
+            const int c = tk.z;
+            const long long o = tp.leaf_off[l];
+            double* Gl = wp.G + (o - wp.G_base) * wp.ldG + 64LL * c;
+            double* Gi = Gl + 64LL * i * wp.ldG;
+            cta_gemm<MEMN, MEMT, MEMN, MEMN>(min(64, n - 64 * i), min(64, ncol - 64 * c), 0, op_mem(Ai, ld),
+                                             op_mem(Gl + (long long)k0 * wp.ldG, wp.ldG), K, op_mem(Ai, 0),
+                                             op_mem(Ai, 0), 0, ci_mem(Gi, wp.ldG), -1.0, Gi, wp.ldG, cp, smem);
+        }
     }
 }
 
@@ -674,11 +704,12 @@ k_wide_panel_x(TreeParams tp, WideParams wp, int s, const int4* tasks, long long
             const long long o = tp.leaf_off[l];
             double* Gs = wp.G + (o - wp.G_base + 64LL * s) * wp.ldG + 64LL * c;
             const int nc = min(64, ncol - 64 * c);
-            if (s > 0)
-                cta_gemm<MEMN, MEMT, MEMN, MEMN>(nb, nc, 0, op_mem(Sl + 64LL * s * ld, ld),
-                                                 op_mem(wp.G + (o - wp.G_base) * wp.ldG + 64LL * c, wp.ldG), 64 * s,
-                                                 op_mem(Sl, 0), op_mem(Sl, 0), 0, ci_mem(Gs, wp.ldG), -1.0, Gs, wp.ldG,
-                                                 cp, smem);
+            const int k0 = 64 * wp.kb0;   // earlier super-blocks arrived through trailing updates
+            if (s > wp.kb0)
+                cta_gemm<MEMN, MEMT, MEMN, MEMN>(nb, nc, 0, op_mem(Sl + 64LL * s * ld + k0, ld),
+                                                 op_mem(wp.G + (o - wp.G_base + k0) * wp.ldG + 64LL * c, wp.ldG),
+                                                 64 * s - k0, op_mem(Sl, 0), op_mem(Sl, 0), 0, ci_mem(Gs, wp.ldG),
+                                                 -1.0, Gs, wp.ldG, cp, smem);
             cta_gemm<MEMN, MEMT, MEMN, MEMN>(nb, nc, 0, op_mem(Ds, 64), op_mem(Gs, wp.ldG), nb, op_mem(Ds, 0),
                                              op_mem(Ds, 0), 0, ci_zero(), 1.0, Gs, wp.ldG, cp, smem);
         } else {

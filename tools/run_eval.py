@@ -48,3 +48,6 @@ if cyc[17] or cyc[21]:
     per = lambda a, b: cyc[a] / max(1, cyc[b])
     print(f"mtile per task (CTA cycles): T00 {per(16, 17):.0f} (n={cyc[17]}); F: wait {per(19, 21):.0f} gemm1 {per(18, 21):.0f} "
           f"gemm2 {per(20, 21):.0f} (n={cyc[21]}); O: gemm1 {per(22, 25):.0f} wait {per(23, 25):.0f} gemm2 {per(24, 25):.0f} (n={cyc[25]})")
+if cyc[29]:
+    print(f"chain per task: {cyc[28] / cyc[29]:.0f} cycles; in cta_gemm calls {cyc[26] / cyc[29]:.0f}; "
+          f"sum of K/rh per task {cyc[27] / cyc[29]:.1f} (ideal DMMA cycles at 2 CTA/SM: {cyc[27] / cyc[29] * 2 * 4096:.0f})")
