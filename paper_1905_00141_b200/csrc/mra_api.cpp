@@ -488,16 +488,22 @@ static mra_status size_wide(mra_plan* P, double budget, bool explicit_budget) {
                     const long long D1 = std::min<long long>(512, std::max<long long>(2, (long long)std::ceil(150.0 / step_us)));
                     const long long D2 = D1 + 12;   // an O task waits for all F of its group before its GEMM
                     mt_D2 = std::max(mt_D2, D2);
+                    // a lone y row (q = 64 k + 1) is formed by one GEMV task per group (type 3), not by
+                    // 1-row tiles (which cost nearly a full tile each)
+                    const bool ysep = (qm % 64 == 1) && qm > 1;
+                    const int nrF = ysep ? nrm - 1 : nrm;
                     ws.mt_off = (long long)tasks.size();
                     for (long long st = 0; st < gc + D2; st++) {
                         if (st < gc) tasks.push_back(make_int4((int)st, 0, 0, 0));
                         const long long gf = st - D1;
                         if (gf >= 0 && gf < gc)
-                            for (int a = 0; a < nrm; a++) tasks.push_back(make_int4((int)gf, 1, a, 0));
+                            for (int a = 0; a < nrF; a++) tasks.push_back(make_int4((int)gf, 1, a, 0));
                         const long long go = st - D2;
-                        if (go >= 0 && go < gc)
-                            for (int a = 0; a < nrm; a++)
+                        if (go >= 0 && go < gc) {
+                            if (ysep) tasks.push_back(make_int4((int)go, 3, 0, 0));
+                            for (int a = 0; a < nrF; a++)
                                 for (int b = 0; b <= a; b++) tasks.push_back(make_int4((int)go, 2, a, b));
+                        }
                     }
                     ws.mt_n = (long long)tasks.size() - ws.mt_off;
                 }

@@ -771,7 +771,12 @@ k_wide_mtile(TreeParams tp, WideParams wp, long long g_first, double* out, long 
     extern __shared__ double smem[];
     const CovP cp = to_covp(tp.cp);
     const int M = tp.M, J = tp.J, m = M - 1, rh = tp.rh, Pg = m * rh;
-    const int nr = (q + 63) / 64, nO = nr * (nr + 1) / 2;
+    const int nr = (q + 63) / 64;
+    // when the y row is alone in the last 64-row tile (q = 64 k + 1: r_hat = 64), the tile tasks cover
+    // rows 0..q-2 only and ONE task per group forms the y row from w = g^T G (a GEMV over the group's G)
+    const bool ysep = (q % 64 == 1) && q > 1;
+    const int nrF = ysep ? nr - 1 : nr;
+    const int nO = nrF * (nrF + 1) / 2 + (ysep ? 1 : 0);
     FacSmem f = fac_smem(smem);
     double* red = misc_smem(smem);
     const long long leaf_id0 = lvl_first(J, M);
@@ -889,13 +894,91 @@ k_wide_mtile(TreeParams tp, WideParams wp, long long g_first, double* out, long 
                 __threadfence();
                 atomicAdd(ring.f_done + gi, 1);
             }
+        } else if (tk.y == 3) {
+            // y row: w = g^T [G_o | G_r] (g = G's last column), F_y = w_o Li^T, O[y, :] = w_r - F_y F^T
+            if (threadIdx.x == 0) {
+                while (*(volatile int*)(ring.f_done + gi) < nrF) __nanosleep(100);
+                __threadfence();
+            }
+            __syncthreads();
+            const int ncg = Pg + 1, np2 = (ncg + 1) / 2;            // columns of G, column pairs
+            const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+            double* part = smem;                                     // [8][2 np2] partial sums (stage area)
+            double* w = smem + 8 * 2 * np2;                          // [ncg]
+            double* fy = w + 2 * np2;                                // [rh]
+            constexpr int MAXP = 12;                                 // column pairs per lane and pass
+            for (int cb = 0; cb < np2; cb += 32 * MAXP) {
+                double2 acc2[MAXP];
+#pragma unroll
+                for (int u = 0; u < MAXP; u++) acc2[u] = make_double2(0.0, 0.0);
+                for (int r = warp; r < ng; r += NT / 32) {   // warp-strided rows, coalesced 16-byte loads
+                    const double* Gr = G + (long long)r * wp.ldG;
+                    const double gr = Gr[Pg];
+#pragma unroll
+                    for (int u = 0; u < MAXP; u++) {
+                        const int c2 = cb + lane + 32 * u;
+                        if (c2 < np2) {
+                            const double2 v = *reinterpret_cast<const double2*>(Gr + 2 * c2);
+                            acc2[u].x += gr * v.x;
+                            acc2[u].y += gr * v.y;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < MAXP; u++) {
+                    const int c2 = cb + lane + 32 * u;
+                    if (c2 < np2) {
+                        part[warp * 2 * np2 + 2 * c2] = acc2[u].x;
+                        part[warp * 2 * np2 + 2 * c2 + 1] = acc2[u].y;
+                    }
+                }
+            }
+            __syncthreads();
+            for (int c = threadIdx.x; c < ncg; c += NT) {
+                double v = 0.0;
+                for (int ww = 0; ww < NT / 32; ww++) v += part[ww * 2 * np2 + c];
+                w[c] = v;
+            }
+            __syncthreads();
+            for (int c = threadIdx.x; c < rh; c += NT) {
+                double v = 0.0;
+                for (int k = 0; k < rh; k++) v += w[k] * Li[c * rh + k];
+                fy[c] = v;
+            }
+            __syncthreads();
+            double* Fy = F + (long long)(q - 1) * rh;
+            double* Fny = Fn + (long long)(q - 1) * rh;
+            double* Py = tp.post ? tp.post + tp.post_base[m] + g * ((long long)rh * rh + (long long)q * rh) + rh * rh +
+                                       (long long)(q - 1) * rh
+                                 : nullptr;
+            for (int c = threadIdx.x; c < rh; c += NT) {
+                Fy[c] = fy[c];
+                Fny[c] = -fy[c];
+                if (Py) Py[c] = fy[c];
+            }
+            double* Oy = out + (g - out_first) * (long long)q * q + (long long)(q - 1) * q;
+            for (int b = threadIdx.x; b < q; b += NT) {
+                const double* Fb = (b == q - 1) ? fy : F + (long long)b * rh;
+                double v = w[rh + b];
+                for (int c = 0; c < rh; c++) v -= fy[c] * Fb[c];
+                Oy[b] = v;
+                if (b == q - 1) tp.ureg[id] = v;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                __threadfence();
+                if (atomicAdd(ring.o_done + gi, 1) == nO - 1) {
+                    __threadfence();
+                    atomicAdd((unsigned long long*)(ring.slot_done + slot), 1ULL);
+                }
+            }
         } else {
             const int a = tk.z, b = tk.w, r0 = 64 * a, c0 = 64 * b;
             const int nrow = min(64, q - r0), ncl = min(64, q - c0);
             double* Oab = out + (g - out_first) * (long long)q * q + (long long)r0 * q + c0;
             // every F of the group is final (the host schedules O tasks ~6 steps after the F tasks)
             if (threadIdx.x == 0) {
-                while (*(volatile int*)(ring.f_done + gi) < nr) __nanosleep(100);
+                while (*(volatile int*)(ring.f_done + gi) < nrF) __nanosleep(100);
                 __threadfence();
             }
             __syncthreads();
@@ -909,6 +992,10 @@ k_wide_mtile(TreeParams tp, WideParams wp, long long g_first, double* out, long 
             PHASE_ADD(24, ph2);
 #ifdef MRA_PHASE_TIMING
             if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[25], 1ULL);
+            if (a == nr - 1 && threadIdx.x == 0) {
+                atomicAdd(&g_phase_cycles[30], (unsigned long long)(clock64() - ph2));
+                atomicAdd(&g_phase_cycles[31], 1ULL);
+            }
 #endif
             if (threadIdx.x == 0) {
                 if (a == nr - 1 && b == nr - 1) tp.ureg[id] = Oab[(long long)(nrow - 1) * q + ncl - 1];

@@ -51,3 +51,5 @@ if cyc[17] or cyc[21]:
 if cyc[29]:
     print(f"chain per task: {cyc[28] / cyc[29]:.0f} cycles; in cta_gemm calls {cyc[26] / cyc[29]:.0f}; "
           f"sum of K/rh per task {cyc[27] / cyc[29]:.1f} (ideal DMMA cycles at 2 CTA/SM: {cyc[27] / cyc[29] * 2 * 4096:.0f})")
+if cyc[31]:
+    print(f"mtile last-row (a = nr-1) O tasks: {cyc[30] / cyc[31]:.0f} cycles each (n={cyc[31]})")
