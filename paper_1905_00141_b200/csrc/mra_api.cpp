@@ -473,9 +473,13 @@ static mra_status size_wide(mra_plan* P, double budget, bool explicit_budget) {
                 }
                 // G = X [V | y], one task per (leaf, column tile) after the factorization
                 ws.trsm_off = (long long)tasks.size();
+                // a lone y column (ncol = 64 k + 1) is one row-parallel GEMV task per leaf (type 2)
+                const bool ycol = (ncol % 64) == 1;
                 for (long long l = ws.g0 * J; l < (ws.g0 + ws.gcount) * J; l++)
-                    if (leaf_n(l) > 0 && xmode(l))
-                        for (int c2 = 0; c2 < nct; c2++) tasks.push_back(make_int4((int)l, c2, 1, 0));
+                    if (leaf_n(l) > 0 && xmode(l)) {
+                        for (int c2 = 0; c2 < (ycol ? nct - 1 : nct); c2++) tasks.push_back(make_int4((int)l, c2, 1, 0));
+                        if (ycol) tasks.push_back(make_int4((int)l, 0, 2, 0));
+                    }
                 ws.trsm_n = (long long)tasks.size() - ws.trsm_off;
                 // merge tile dataflow: step s holds T00 of group s, the F tasks of group s - D1 and the
                 // O tasks of group s - D2; D1 covers ~150 us of T00 latency (GEMM + 64x64

@@ -740,8 +740,35 @@ k_wide_trsm(TreeParams tp, WideParams wp, const int4* tasks, long long ntask, un
         if (it >= ntask) break;
         const int4 tk = tasks[it];
         const long long l = tk.x;
-        const int n = leaf_n(tp, l), ld = wp.S_ld[l], c0 = 64 * tk.y, nc = min(64, ncol - c0);
+        const int n = leaf_n(tp, l), ld = wp.S_ld[l];
         const double* Sl = wp.S + wp.S_off[l];
+        if (tk.z == 2) {
+            // the y column alone (ncol = 64 k + 1): g = X y by rows, X[i][K] = Sl[K ld + i] (K < block start)
+            // and the inverted diagonal block; row chunks descending so g can overwrite y in place
+            double* gcol = wp.G + (tp.leaf_off[l] - wp.G_base) * wp.ldG + (ncol - 1);
+            for (int base = ((n - 1) / NT) * NT; base >= 0; base -= NT) {
+                const int i = base + threadIdx.x;
+                double v = 0.0;
+                if (i < n) {
+                    const int bi = i / 64, i0 = 64 * bi;
+                    double s0 = 0.0, s1 = 0.0;
+                    int k = 0;
+                    for (; k + 1 < i0; k += 2) {
+                        s0 += Sl[(long long)k * ld + i] * gcol[(long long)k * wp.ldG];
+                        s1 += Sl[(long long)(k + 1) * ld + i] * gcol[(long long)(k + 1) * wp.ldG];
+                    }
+                    if (k < i0) s0 += Sl[(long long)k * ld + i] * gcol[(long long)k * wp.ldG];
+                    const double* Di = wp.D + wp.D_off[l] + 4096LL * bi + (long long)(i - i0) * 64;
+                    for (int kk = 0; kk <= i - i0; kk++) s1 += Di[kk] * gcol[(long long)(i0 + kk) * wp.ldG];
+                    v = s0 + s1;
+                }
+                __syncthreads();
+                if (i < n) gcol[(long long)i * wp.ldG] = v;
+                __syncthreads();
+            }
+            continue;
+        }
+        const int c0 = 64 * tk.y, nc = min(64, ncol - c0);
         double* Gl = wp.G + (tp.leaf_off[l] - wp.G_base) * wp.ldG + c0;
         for (int i = (n - 1) / 64; i >= 0; i--) {
             const int i0 = 64 * i, nb = min(64, n - i0);
