@@ -285,7 +285,9 @@ def run_gpu(args, rank, world, local_rank):
     t0 = time.time()
     plan = mra.mra_plan_create(w.x, w.y, w.M, w.J, w.r, device=local_rank, stream=stream, rank=rank,
                                world=world)
-    log(f"[rank {rank}] plan in {time.time() - t0:.1f}s: n_retained={plan.n_retained} r_hat={plan.r_hat}")
+    torch.cuda.synchronize()
+    plan_s = time.time() - t0
+    log(f"[rank {rank}] plan in {plan_s:.1f}s: n_retained={plan.n_retained} r_hat={plan.r_hat}")
     thetas = w.thetas if args.config == "C4" else w.thetas[:1]
     zd = torch.from_numpy(w.z).to(dev)
     zpin = torch.from_numpy(w.z).pin_memory()
@@ -435,6 +437,7 @@ def run_gpu(args, rank, world, local_rank):
             "kernel_ms": {k: round(kms[k], 3) for k in mra.KERNEL_CLASSES},
             "kernel_launches": {k: int(kcnt[k]) for k in mra.KERNEL_CLASSES},
             "roofline": roof, "cpu_baseline": cpu, "clocks": clocks}
+    line["plan_seconds"] = round(plan_s, 3)   # S0 (device build, not in the timed region)
     if pred:
         line["predict"] = pred
     print(json.dumps(line), flush=True)

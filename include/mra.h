@@ -68,6 +68,9 @@ typedef struct {
     double mem_budget_gb; /* device memory budget for the chunked bottom pass; 0 = auto        */
     int wide;         /* grid-wide task path (leaves processed by all CTAs together):
                          0 / 1 = use it (default, M >= 2), -1 = one CTA per level-(M-1) region   */
+    int host_plan;    /* 0 = build the partition on the device (bounding box, leaf keys, stable radix
+                         sort by leaf: SURVEY.md NEXT-2; default), 1 = on the host (OpenMP). Both give
+                         the identical plan; host-only plans (device -2) always build on the host  */
 } mra_opts;
 
 /* Posterior state requested from an evaluation; any pointer may be NULL. */

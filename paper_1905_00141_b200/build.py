@@ -7,7 +7,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["mra_kernels.cu", "mra_api.cpp"]
+SOURCES = ["mra_kernels.cu", "mra_plan.cu", "mra_api.cpp"]
 HEADERS = ["mra_device.cuh", "mra_internal.h"]
 OUT = os.path.join(HERE, "libmra_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -166,7 +166,10 @@ static double bar_pos(double lo, double hi, int nb, int i, double off) {
     return lo + off * ext + (double)i * (ext * (1.0 - 2.0 * off) / (double)(nb - 1));
 }
 
-static mra_status build_host(mra_plan* P, const double* x, const double* y, uint64_t n) {
+// partition geometry from the data bounding box: r_hat, region counts, interior boxes (level-major,
+// root = bbox with top/right pushed out 1%; J=4 quadrants / J=2 longer-axis halves,
+// PAPER.md:100-103) and the knot grids
+static mra_status build_geometry(mra_plan* P, double x0, double x1, double y0, double y1) {
     const int M = P->M, J = P->J;
     int nx = 1;
     while (nx * nx < P->r) nx++;
@@ -177,14 +180,7 @@ static mra_status build_host(mra_plan* P, const double* x, const double* y, uint
     P->nreg = (ipow(J, M) - 1) / (J - 1);
     P->nint = (ipow(J, M - 1) - 1) / (J - 1);
     P->nleaf = ipow(J, M - 1);
-    double x0 = x[0], x1 = x[0], y0 = y[0], y1 = y[0];
-    for (uint64_t i = 0; i < n; i++) {
-        if (!std::isfinite(x[i]) || !std::isfinite(y[i])) return fail(MRA_E_ARG, "non-finite location");
-        x0 = std::min(x0, x[i]); x1 = std::max(x1, x[i]);
-        y0 = std::min(y0, y[i]); y1 = std::max(y1, y[i]);
-    }
     if (!(x1 > x0) || !(y1 > y0)) return fail(MRA_E_STRUCT, "degenerate bounding box (zero extent)");
-    // interior boxes, level-major; root pushed out 1% at top/right
     std::vector<double> box(4 * std::max<long long>(P->nint, 1));
     if (P->nint > 0) {
         box[0] = x0; box[1] = x1 + 0.01 * (x1 - x0);
@@ -223,6 +219,41 @@ static mra_status build_host(mra_plan* P, const double* x, const double* y, uint
                 P->ky[id * rh + iy * P->nx + ix] = bar_pos(b[2], b[3], P->ny, iy, P->offset);
             }
     }
+    P->box = box;
+    return MRA_OK;
+}
+
+// leaf statistics from the CSR offsets
+static mra_status finish_leaves(mra_plan* P) {
+    P->n_empty = 0;
+    P->max_leaf = 0;
+    for (long long t = 0; t < P->nleaf; t++) {
+        const long long c = P->leaf_off[t + 1] - P->leaf_off[t];
+        if (c == 0) P->n_empty++;
+        P->max_leaf = std::max(P->max_leaf, c);
+    }
+    P->N = P->leaf_off[P->nleaf];
+    if (P->N == 0) return fail(MRA_E_STRUCT, "every observation was eliminated");
+    const int Jc = (P->M == 1) ? 1 : P->J;
+    P->max_group = 0;
+    for (long long g = 0; g < P->nleaf / Jc; g++)
+        P->max_group = std::max(P->max_group, P->leaf_off[(g + 1) * Jc] - P->leaf_off[g * Jc]);
+    return MRA_OK;
+}
+
+// host build (OpenMP): bounding box, leaf key by descent with the elimination test, stable counting sort
+static mra_status build_host(mra_plan* P, const double* x, const double* y, uint64_t n) {
+    const int M = P->M, J = P->J;
+    double x0 = x[0], x1 = x[0], y0 = y[0], y1 = y[0];
+    for (uint64_t i = 0; i < n; i++) {
+        if (!std::isfinite(x[i]) || !std::isfinite(y[i])) return fail(MRA_E_ARG, "non-finite location");
+        x0 = std::min(x0, x[i]); x1 = std::max(x1, x[i]);
+        y0 = std::min(y0, y[i]); y1 = std::max(y1, y[i]);
+    }
+    mra_status s = build_geometry(P, x0, x1, y0, y1);
+    if (s) return s;
+    const int rh = P->rh;
+    const std::vector<double>& box = P->box;
     // leaf key by descent; elimination test against each ancestor's bar sets
     std::vector<long long> key(n);
 #pragma omp parallel for schedule(static)
@@ -253,24 +284,113 @@ static mra_status build_host(mra_plan* P, const double* x, const double* y, uint
     P->leaf_off.assign(P->nleaf + 1, 0);
     for (uint64_t i = 0; i < n; i++)
         if (key[i] >= 0) P->leaf_off[key[i] + 1]++;
-    P->n_empty = 0;
-    P->max_leaf = 0;
-    for (long long t = 0; t < P->nleaf; t++) {
-        if (P->leaf_off[t + 1] == 0) P->n_empty++;
-        P->max_leaf = std::max(P->max_leaf, P->leaf_off[t + 1]);
-        P->leaf_off[t + 1] += P->leaf_off[t];
-    }
-    P->box = box;
-    P->N = P->leaf_off[P->nleaf];
-    if (P->N == 0) return fail(MRA_E_STRUCT, "every observation was eliminated");
+    for (long long t = 0; t < P->nleaf; t++) P->leaf_off[t + 1] += P->leaf_off[t];
+    if ((s = finish_leaves(P))) return s;
     std::vector<long long> fill(P->leaf_off.begin(), P->leaf_off.end() - 1);
     P->perm.assign(P->N, 0);
     for (uint64_t i = 0; i < n; i++)
         if (key[i] >= 0) P->perm[fill[key[i]]++] = (long long)i;
-    const int Jc = (M == 1) ? 1 : J;
-    P->max_group = 0;
-    for (long long g = 0; g < P->nleaf / Jc; g++)
-        P->max_group = std::max(P->max_group, P->leaf_off[(g + 1) * Jc] - P->leaf_off[g * Jc]);
+    return MRA_OK;
+}
+
+// device build (NEXT-2): upload, bounding box, leaf keys, stable radix sort by leaf, CSR offsets and
+// the leaf-ordered coordinates on the GPU (mra_plan.cu). Produces the host build's plan exactly; the host
+// keeps copies of leaf_off and perm (layout queries, task lists). P->pxy / P->perm_d are allocated here.
+static mra_status build_device(mra_plan* P, const double* x, const double* y, uint64_t n) {
+    cudaStream_t st = P->st;
+    const long long nn = (long long)n;
+    double *dx = nullptr, *dy = nullptr, *part = nullptr, *dbox = nullptr, *dxb = nullptr, *dyb = nullptr;
+    int *bad = nullptr, *k1 = nullptr, *i1 = nullptr, *k2 = nullptr, *i2 = nullptr;
+    unsigned int *cnt = nullptr, *bcnt = nullptr;
+    auto release = [&]() {
+        cudaFree(dx); cudaFree(dy); cudaFree(part); cudaFree(dbox); cudaFree(dxb); cudaFree(dyb); cudaFree(bad);
+        cudaFree(k1); cudaFree(i1); cudaFree(k2); cudaFree(i2); cudaFree(cnt); cudaFree(bcnt);
+    };
+#define BD(call)                                                                              \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess) {                                                              \
+            release();                                                                        \
+            return fail(e_ == cudaErrorMemoryAllocation ? MRA_E_OOM : MRA_E_CUDA,             \
+                        std::string("device plan build: " #call ": ") + cudaGetErrorString(e_)); \
+        }                                                                                     \
+    } while (0)
+    BD(cudaMalloc(&dx, 8 * nn));
+    BD(cudaMalloc(&dy, 8 * nn));
+    BD(cudaMemcpyAsync(dx, x, 8 * nn, cudaMemcpyHostToDevice, st));
+    BD(cudaMemcpyAsync(dy, y, 8 * nn, cudaMemcpyHostToDevice, st));
+    // bounding box + finiteness
+    const int nb = (int)std::min<long long>(1024, (nn + 255) / 256);
+    BD(cudaMalloc(&part, 8 * 4 * nb));
+    BD(cudaMalloc(&bad, 4));
+    BD(cudaMemsetAsync(bad, 0, 4, st));
+    BD(plan_bbox(dx, dy, nn, part, nb, bad, st));
+    std::vector<double> hp(4 * nb);
+    int hbad = 0;
+    BD(cudaMemcpyAsync(hp.data(), part, 8 * 4 * nb, cudaMemcpyDeviceToHost, st));
+    BD(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, st));
+    BD(cudaStreamSynchronize(st));
+    if (hbad) { release(); return fail(MRA_E_ARG, "non-finite location"); }
+    double x0 = hp[0], x1 = hp[1], y0 = hp[2], y1 = hp[3];
+    for (int b = 1; b < nb; b++) {
+        x0 = std::min(x0, hp[4 * b]); x1 = std::max(x1, hp[4 * b + 1]);
+        y0 = std::min(y0, hp[4 * b + 2]); y1 = std::max(y1, hp[4 * b + 3]);
+    }
+    mra_status s = build_geometry(P, x0, x1, y0, y1);
+    if (s) { release(); return s; }
+    const int M = P->M, lj = P->lj;
+    // boxes and knot bars on the device
+    const long long ni = std::max<long long>(P->nint, 1);
+    std::vector<double> hxb(ni * P->nx, 0.0), hyb(ni * P->ny, 0.0);
+    for (long long id = 0; id < P->nint; id++) {
+        for (int ix = 0; ix < P->nx; ix++) hxb[id * P->nx + ix] = P->kx[id * P->rh + ix];
+        for (int iy = 0; iy < P->ny; iy++) hyb[id * P->ny + iy] = P->ky[id * P->rh + iy * P->nx];
+    }
+    BD(cudaMalloc(&dbox, 8 * 4 * ni));
+    BD(cudaMalloc(&dxb, 8 * hxb.size()));
+    BD(cudaMalloc(&dyb, 8 * hyb.size()));
+    BD(cudaMemcpyAsync(dbox, P->box.data(), 8 * 4 * ni, cudaMemcpyHostToDevice, st));
+    BD(cudaMemcpyAsync(dxb, hxb.data(), 8 * hxb.size(), cudaMemcpyHostToDevice, st));
+    BD(cudaMemcpyAsync(dyb, hyb.data(), 8 * hyb.size(), cudaMemcpyHostToDevice, st));
+    // keys (eliminated -> n_leaves), per-leaf counts
+    BD(cudaMalloc(&k1, 4 * nn)); BD(cudaMalloc(&i1, 4 * nn));
+    BD(cudaMalloc(&k2, 4 * nn)); BD(cudaMalloc(&i2, 4 * nn));
+    BD(cudaMalloc(&cnt, 4 * (P->nleaf + 1)));
+    BD(cudaMemsetAsync(cnt, 0, 4 * (P->nleaf + 1), st));
+    PlanGeom pg{};
+    pg.M = M; pg.J = P->J; pg.nx = P->nx; pg.ny = P->ny; pg.nleaf = P->nleaf;
+    pg.box = dbox; pg.xbar = dxb; pg.ybar = dyb;
+    BD(plan_keys(dx, dy, nn, pg, k1, i1, cnt, st));
+    // stable LSD radix sort over the M base-J digits of the key (digit M-1 flags eliminated observations)
+    const int nblk = plan_radix_blocks(nn), R = 1 << lj;
+    BD(cudaMalloc(&bcnt, 4 * (size_t)R * nblk));
+    std::vector<unsigned int> hb((size_t)R * nblk);
+    for (int d = 0; d < M; d++) {
+        BD(plan_radix_count(k1, nn, lj, d, bcnt, st));
+        BD(cudaMemcpyAsync(hb.data(), bcnt, 4 * hb.size(), cudaMemcpyDeviceToHost, st));
+        BD(cudaStreamSynchronize(st));
+        unsigned int run = 0;   // exclusive scan, digit-major then block
+        for (size_t e = 0; e < hb.size(); e++) { const unsigned int c = hb[e]; hb[e] = run; run += c; }
+        BD(cudaMemcpyAsync(bcnt, hb.data(), 4 * hb.size(), cudaMemcpyHostToDevice, st));
+        BD(plan_radix_scatter(k1, i1, nn, lj, d, bcnt, k2, i2, st));
+        std::swap(k1, k2);
+        std::swap(i1, i2);
+    }
+    std::vector<unsigned int> hc(P->nleaf + 1);
+    BD(cudaMemcpyAsync(hc.data(), cnt, 4 * hc.size(), cudaMemcpyDeviceToHost, st));
+    BD(cudaStreamSynchronize(st));
+    P->leaf_off.assign(P->nleaf + 1, 0);
+    for (long long t = 0; t < P->nleaf; t++) P->leaf_off[t + 1] = P->leaf_off[t] + hc[t];
+    if ((s = finish_leaves(P))) { release(); return s; }
+    const long long N = P->N;
+    if ((s = dalloc(P, (void**)&P->pxy, 16 * N, "pxy"))) { release(); return s; }
+    if ((s = dalloc(P, (void**)&P->perm_d, 8 * N, "perm"))) { release(); return s; }
+    BD(plan_gather(dx, dy, i1, N, P->pxy, P->perm_d, st));
+    P->perm.assign(N, 0);
+    BD(cudaMemcpyAsync(P->perm.data(), P->perm_d, 8 * N, cudaMemcpyDeviceToHost, st));
+    BD(cudaStreamSynchronize(st));
+#undef BD
+    release();
     return MRA_OK;
 }
 
@@ -568,8 +688,23 @@ extern "C" mra_status mra_plan_create(const double* x, const double* y, uint64_t
     P->n_in = n;
     P->rank = o.world > 1 ? o.rank : 0;
     P->world = o.world > 1 ? o.world : 1;
-    mra_status s = build_host(P, x, y, n);
-    if (s) { delete P; return s; }
+    // S0 on the device (NEXT-2) unless this is a host-only plan, the caller asks for the host build,
+    // or the keys / indices would not fit the device build's 32-bit fields
+    const bool dev_build = o.device != -2 && !o.host_plan && n < (1ULL << 31) &&
+                           ipow(J, M - 1) < (1LL << 30);
+    mra_status s = MRA_OK;
+    if (dev_build) {
+        int dev = o.device;
+        if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) { delete P; return fail(MRA_E_CUDA, "no CUDA device"); }
+        if (cudaSetDevice(dev) != cudaSuccess) { delete P; return fail(MRA_E_CUDA, "cudaSetDevice failed (no GPU?)"); }
+        P->device = dev;
+        P->st = (cudaStream_t)o.stream;
+        s = build_device(P, x, y, n);
+        if (s) { mra_plan_destroy(P); return s; }
+    } else {
+        s = build_host(P, x, y, n);
+        if (s) { delete P; return s; }
+    }
     // the grid-wide task path is at least as fast as one-CTA-per-group on every configuration measured
     // (C0 4.3x, C1 1.2x, C2/C3 ~1.02x, C4 > 100x: DESIGN.md §5), so it is the default for M >= 2
     P->wide = M >= 2 && o.wide >= 0;
@@ -606,6 +741,7 @@ extern "C" mra_status mra_plan_create(const double* x, const double* y, uint64_t
         *out = P;
         return MRA_OK;
     }
+
     int dev = o.device;
     if (dev < 0) {
         if (cudaGetDevice(&dev) != cudaSuccess) { delete P; return fail(MRA_E_CUDA, "no CUDA device"); }
@@ -617,10 +753,12 @@ extern "C" mra_status mra_plan_create(const double* x, const double* y, uint64_t
     mra_status st;
 #define TRY(x) do { if ((st = (x))) { mra_plan_destroy(P); return st; } } while (0)
     const long long N = P->N;
-    TRY(dalloc(P, (void**)&P->pxy, 16 * N, "pxy"));
+    if (!dev_build) {
+        TRY(dalloc(P, (void**)&P->pxy, 16 * N, "pxy"));
+        TRY(dalloc(P, (void**)&P->perm_d, 8 * N, "perm"));
+    }
     TRY(dalloc(P, (void**)&P->zs, 8 * N, "zs"));
     TRY(dalloc(P, (void**)&P->zin, 8 * (long long)n, "zin"));
-    TRY(dalloc(P, (void**)&P->perm_d, 8 * N, "perm"));
     TRY(dalloc(P, (void**)&P->leaf_off_d, 8 * (P->nleaf + 1), "leaf_off"));
     TRY(dalloc(P, (void**)&P->kxy_d, 16 * std::max<long long>(1, P->nint * P->rh), "kxy"));
     TRY(dalloc(P, (void**)&P->dreg, 8 * P->nreg, "dreg"));
@@ -630,16 +768,19 @@ extern "C" mra_status mra_plan_create(const double* x, const double* y, uint64_t
     P->n_counters = 1 << 16;
     TRY(dalloc(P, (void**)&P->counters, 8 * (size_t)P->n_counters, "counters"));
     {
-        std::vector<double> sxy(2 * N), kxy(2 * std::max<long long>(1, P->nint * P->rh));
-        for (long long i = 0; i < N; i++) { sxy[2 * i] = x[P->perm[i]]; sxy[2 * i + 1] = y[P->perm[i]]; }
+        std::vector<double> kxy(2 * std::max<long long>(1, P->nint * P->rh));
         for (long long i = 0; i < P->nint * P->rh; i++) { kxy[2 * i] = P->kx[i]; kxy[2 * i + 1] = P->ky[i]; }
         auto cp = [&](void* d, const void* h, size_t b) -> mra_status {
             cudaError_t e = cudaMemcpy(d, h, b, cudaMemcpyHostToDevice);
             if (e != cudaSuccess) return fail(MRA_E_CUDA, std::string("upload: ") + cudaGetErrorString(e));
             return MRA_OK;
         };
-        TRY(cp(P->pxy, sxy.data(), 16 * N));
-        TRY(cp(P->perm_d, P->perm.data(), 8 * N));
+        if (!dev_build) {
+            std::vector<double> sxy(2 * N);
+            for (long long i = 0; i < N; i++) { sxy[2 * i] = x[P->perm[i]]; sxy[2 * i + 1] = y[P->perm[i]]; }
+            TRY(cp(P->pxy, sxy.data(), 16 * N));
+            TRY(cp(P->perm_d, P->perm.data(), 8 * N));
+        }
         TRY(cp(P->leaf_off_d, P->leaf_off.data(), 8 * (P->nleaf + 1)));
         if (P->nint) TRY(cp(P->kxy_d, kxy.data(), 16 * P->nint * P->rh));
     }

@@ -107,6 +107,24 @@ cudaError_t launch_wide(int phase, const TreeParams& tp, const WideParams& wp, i
 cudaError_t launch_wide_mtile(const TreeParams& tp, const WideParams& wp, long long g_first, long long g_count,
                               double* out, long long out_first, int q, const int4* tasks, long long ntask, int grid,
                               unsigned long long* counter, const MergeRing& ring, cudaStream_t st);
+// device plan build (mra_plan.cu): geometry of the partition (host-computed boxes and knot bars)
+struct PlanGeom {
+    int M, J, nx, ny;
+    long long nleaf;
+    const double* box;    // [4 n_interior]: x0 x1 y0 y1, level-major
+    const double* xbar;   // [n_interior * nx]
+    const double* ybar;   // [n_interior * ny]
+};
+cudaError_t plan_bbox(const double* x, const double* y, long long n, double* part, int nblk, int* bad,
+                      cudaStream_t st);
+cudaError_t plan_keys(const double* x, const double* y, long long n, const PlanGeom& pg, int* key, int* idx,
+                      unsigned int* cnt, cudaStream_t st);
+int plan_radix_blocks(long long n);
+cudaError_t plan_radix_count(const int* key, long long n, int lj, int d, unsigned int* bcnt, cudaStream_t st);
+cudaError_t plan_radix_scatter(const int* key, const int* idx, long long n, int lj, int d, const unsigned int* boff,
+                               int* key2, int* idx2, cudaStream_t st);
+cudaError_t plan_gather(const double* x, const double* y, const int* idx, long long N, double* pxy, long long* perm,
+                        cudaStream_t st);
 int smem_bytes();
 void phase_cycles(unsigned long long* out32, bool reset);   // -DMRA_PHASE_TIMING builds only
 

@@ -205,3 +205,30 @@ def test_wide_path_posterior(mra):
     got = mra.mra_loglik(p, z, theta, posterior=True, regions=True)
     ref = oracle.run(x, y, z, 3, 2, 30, theta, regions=True, posterior=True)
     _cmp(got, ref)
+
+
+@pytest.mark.parametrize("n,M,J,r,cl", [(5000, 4, 4, 16, 3), (4000, 6, 2, 9, 2), (3000, 1, 4, 16, 0),
+                                        (20000, 7, 4, 36, 4)])
+def test_device_plan_build_matches_host(mra, n, M, J, r, cl):
+    """S0 on the device (NEXT-2): leaf keys, elimination and the stable sort give the host build's plan
+    bit for bit (perm, CSR offsets, knots), hence the identical log L. Observations placed exactly on
+    pre-finest knots exercise the elimination path."""
+    x, y, z = synth.uniform_small(n, seed=900 + n, clusters=cl)
+    ph = mra.mra_plan_create(x, y, M, J, r, host_plan=1)
+    lh = mra.mra_plan_layout(ph)
+    if M > 1:   # put 7 observations on level-1 / level-2 knots
+        x = x.copy(); y = y.copy()
+        k = min(7, lh["knots_x"].size)
+        x[:k] = lh["knots_x"].ravel()[:k]
+        y[:k] = lh["knots_y"].ravel()[:k]
+        ph.close()
+        ph = mra.mra_plan_create(x, y, M, J, r, host_plan=1)
+        lh = mra.mra_plan_layout(ph)
+    pd = mra.mra_plan_create(x, y, M, J, r)
+    ld = mra.mra_plan_layout(pd)
+    assert pd.n_retained == ph.n_retained and (M == 1 or pd.n_retained < n)
+    for key in ("perm", "leaf_off", "knots_x", "knots_y"):
+        assert np.array_equal(ld[key], lh[key]), key
+    th = (EXP, 1.0, 0.1, 0.05)
+    assert mra.mra_loglik(pd, z, th)["loglik"] == mra.mra_loglik(ph, z, th)["loglik"]
+    pd.close(); ph.close()
