@@ -131,6 +131,18 @@ mra_status mra_loglik_batch_dev(mra_plan* plan, const double* d_y, const mra_the
 mra_status mra_predict(mra_plan* plan, const double* qx, const double* qy, uint64_t nq, double* mean,
                        double* var);
 
+/* The paper's "optimization" calculation mode ("a series of likelihood
+ * evaluations"): maximise log L over (sigma2, rho, tau2) for the covariance family theta->cov, by a
+ * derivative-free Nelder-Mead search on the log-parameters inside [lower, upper] (host C++ logic; every
+ * evaluation is one mra_loglik_dev on the device). A deterministic stand-in for the paper's BOBYQA.
+ *   d_y        : DEVICE array of the n observed values (original order).
+ *   theta      : in: starting point (inside the bounds); out: the best point found.
+ *   lower/upper: host arrays of 3 bounds {sigma2, rho, tau2} (> 0), or NULL for (0, inf).
+ *   max_evals  : evaluation budget (<= 0: 200); tol: simplex size in log-parameters (<= 0: 1e-6).
+ *   best_loglik, n_evals: optional outputs. Points whose factorizations fail count as -inf. */
+mra_status mra_optimize(mra_plan* plan, const double* d_y, mra_theta* theta, const double* lower,
+                        const double* upper, int max_evals, double tol, double* best_loglik, int* n_evals);
+
 /* Multi-GPU subtree sharding, one process per GPU:
  *   mra_shard_size(plan)          -> doubles in the exchange buffer (same on every rank)
  *   mra_loglik_shard(plan, d_y, theta, d_xbuf)

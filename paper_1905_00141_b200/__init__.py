@@ -53,7 +53,7 @@ class _Post(ctypes.Structure):
 
 
 _lib = None
-EXPORTS = ["mra_plan_create", "mra_loglik", "mra_loglik_dev", "mra_loglik_batch_dev", "mra_predict", "mra_shard_size",
+EXPORTS = ["mra_plan_create", "mra_loglik", "mra_loglik_dev", "mra_loglik_batch_dev", "mra_predict", "mra_optimize", "mra_shard_size",
            "mra_loglik_shard", "mra_loglik_finish", "mra_plan_info", "mra_plan_layout", "mra_plan_shards",
            "mra_profile", "mra_kernel_times", "mra_last_launches", "mra_plan_destroy", "mra_last_error"]
 
@@ -95,6 +95,9 @@ def load_library(path: str = LIB_PATH):
                                     ctypes.POINTER(U64)]
     lib.mra_profile.restype = ctypes.c_int
     lib.mra_profile.argtypes = [P, ctypes.c_int]
+    lib.mra_optimize.restype = ctypes.c_int
+    lib.mra_optimize.argtypes = [P, P, ctypes.POINTER(_Theta), D, D, ctypes.c_int, ctypes.c_double, D,
+                                 ctypes.POINTER(ctypes.c_int)]
     lib.mra_predict.restype = ctypes.c_int
     lib.mra_predict.argtypes = [P, D, D, U64, D, D]
     lib.mra_kernel_times.restype = ctypes.c_int
@@ -296,6 +299,22 @@ def mra_kernel_times(plan: PlanHandle) -> dict:
     cnt = (ctypes.c_uint64 * len(KERNEL_CLASSES))()
     _check(_lib.mra_kernel_times(plan.ptr, ms, cnt))
     return {k: (ms[i], cnt[i]) for i, k in enumerate(KERNEL_CLASSES)}
+
+
+def mra_optimize(plan: PlanHandle, y_dev, theta0, lower=None, upper=None, max_evals=200, tol=1e-6):
+    """Maximise log L over (sigma2, rho, tau2) from theta0 = (cov, sigma2, rho, tau2); y_dev a CUDA tensor.
+    Returns (theta, loglik, n_evals)."""
+    th = _Theta(int(theta0[0]), float(theta0[1]), float(theta0[2]), float(theta0[3]))
+    D = ctypes.POINTER(ctypes.c_double)
+    lo = None if lower is None else (ctypes.c_double * 3)(*[float(v) for v in lower])
+    hi = None if upper is None else (ctypes.c_double * 3)(*[float(v) for v in upper])
+    ll = ctypes.c_double()
+    ne = ctypes.c_int()
+    _check(_lib.mra_optimize(plan.ptr, ctypes.c_void_p(y_dev.data_ptr()), ctypes.byref(th),
+                             ctypes.cast(lo, D) if lo is not None else None,
+                             ctypes.cast(hi, D) if hi is not None else None, int(max_evals), float(tol),
+                             ctypes.byref(ll), ctypes.byref(ne)))
+    return (th.cov, th.sigma2, th.rho, th.tau2), ll.value, ne.value
 
 
 def mra_predict(plan: PlanHandle, qx, qy):

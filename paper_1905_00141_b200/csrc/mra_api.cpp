@@ -1283,6 +1283,98 @@ extern "C" mra_status mra_loglik_batch_dev(mra_plan* P, const double* d_y, const
     return MRA_OK;
 }
 
+// ----------------------------------------------------------------------- optimization
+// The paper's "optimization" calculation mode: maximise log L over (sigma2, rho, tau2)
+// by derivative-free search, each step one full evaluation. Nelder-Mead on the log-parameters inside
+// the box [lower, upper] (reflections clamped to the box), a deterministic stand-in for the paper's
+// BOBYQA (dlib); non-PD evaluations count as -inf.
+extern "C" mra_status mra_optimize(mra_plan* P, const double* d_y, mra_theta* theta, const double* lower,
+                                   const double* upper, int max_evals, double tol, double* best_loglik,
+                                   int* n_evals) {
+    if (!P || !d_y || !theta) return fail(MRA_E_ARG, "NULL argument");
+    if (P->world > 1) return fail(MRA_E_CONFIG, "optimization on a sharded plan is not supported");
+    mra_status s = check_theta(theta);
+    if (s) return s;
+    if (max_evals < 1) max_evals = 200;
+    if (!(tol > 0)) tol = 1e-6;
+    double lo[3], hi[3];
+    const double v0[3] = {theta->sigma2, theta->rho, theta->tau2};
+    for (int i = 0; i < 3; i++) {
+        lo[i] = lower ? std::log(lower[i]) : -INFINITY;
+        hi[i] = upper ? std::log(upper[i]) : INFINITY;
+        if (lower && upper && !(lower[i] > 0 && upper[i] >= lower[i])) return fail(MRA_E_ARG, "bad bounds");
+        if (std::log(v0[i]) < lo[i] || std::log(v0[i]) > hi[i]) return fail(MRA_E_ARG, "initial theta outside the bounds");
+    }
+    int evals = 0;
+    auto clampv = [&](double* v) { for (int i = 0; i < 3; i++) v[i] = std::min(hi[i], std::max(lo[i], v[i])); };
+    // objective: -log L (minimised); failures -> +inf
+    auto f = [&](const double* v, double* out) -> mra_status {
+        mra_theta th = *theta;
+        th.sigma2 = std::exp(v[0]); th.rho = std::exp(v[1]); th.tau2 = std::exp(v[2]);
+        double ll = NAN;
+        mra_status e = run_eval(P, d_y, &th, &ll, nullptr, false);
+        evals++;
+        if (e == MRA_E_NUMERIC || !std::isfinite(ll)) { *out = INFINITY; g_err.clear(); return MRA_OK; }
+        if (e) return e;
+        *out = -ll;
+        return MRA_OK;
+    };
+    double X[4][3], F[4];
+    for (int j = 0; j < 4; j++) {
+        for (int i = 0; i < 3; i++) X[j][i] = std::log(v0[i]) + ((j == i + 1) ? 0.5 : 0.0);
+        clampv(X[j]);
+        if ((s = f(X[j], &F[j]))) return s;
+    }
+    while (evals < max_evals) {
+        int ord[4] = {0, 1, 2, 3};
+        std::sort(ord, ord + 4, [&](int a, int b) { return F[a] < F[b]; });
+        double Xs[4][3], Fs[4];
+        for (int j = 0; j < 4; j++) { std::memcpy(Xs[j], X[ord[j]], sizeof Xs[j]); Fs[j] = F[ord[j]]; }
+        std::memcpy(X, Xs, sizeof X); std::memcpy(F, Fs, sizeof F);
+        double size = 0;
+        for (int j = 1; j < 4; j++)
+            for (int i = 0; i < 3; i++) size = std::max(size, std::fabs(X[j][i] - X[0][i]));
+        if (size < tol || (std::isfinite(F[3]) && std::fabs(F[3] - F[0]) <= tol * (1.0 + std::fabs(F[0])) && size < 1e3 * tol))
+            break;
+        double c[3] = {0, 0, 0};
+        for (int j = 0; j < 3; j++) for (int i = 0; i < 3; i++) c[i] += X[j][i] / 3.0;
+        double xr[3], fr;
+        for (int i = 0; i < 3; i++) xr[i] = c[i] + (c[i] - X[3][i]);
+        clampv(xr);
+        if ((s = f(xr, &fr))) return s;
+        if (fr < F[0]) {
+            double xe[3], fe;
+            for (int i = 0; i < 3; i++) xe[i] = c[i] + 2.0 * (c[i] - X[3][i]);
+            clampv(xe);
+            if ((s = f(xe, &fe))) return s;
+            if (fe < fr) { std::memcpy(X[3], xe, sizeof xe); F[3] = fe; }
+            else { std::memcpy(X[3], xr, sizeof xr); F[3] = fr; }
+        } else if (fr < F[2]) {
+            std::memcpy(X[3], xr, sizeof xr); F[3] = fr;
+        } else {
+            double xc[3], fc;
+            const bool outside = fr < F[3];
+            for (int i = 0; i < 3; i++) xc[i] = outside ? c[i] + 0.5 * (xr[i] - c[i]) : c[i] + 0.5 * (X[3][i] - c[i]);
+            clampv(xc);
+            if ((s = f(xc, &fc))) return s;
+            if (fc < (outside ? fr : F[3])) { std::memcpy(X[3], xc, sizeof xc); F[3] = fc; }
+            else {   // shrink towards the best vertex
+                for (int j = 1; j < 4; j++) {
+                    for (int i = 0; i < 3; i++) X[j][i] = X[0][i] + 0.5 * (X[j][i] - X[0][i]);
+                    if ((s = f(X[j], &F[j]))) return s;
+                }
+            }
+        }
+    }
+    int b = 0;
+    for (int j = 1; j < 4; j++) if (F[j] < F[b]) b = j;
+    if (!std::isfinite(F[b])) return fail(MRA_E_NUMERIC, "no feasible parameter point found");
+    theta->sigma2 = std::exp(X[b][0]); theta->rho = std::exp(X[b][1]); theta->tau2 = std::exp(X[b][2]);
+    if (best_loglik) *best_loglik = -F[b];
+    if (n_evals) *n_evals = evals;
+    return MRA_OK;
+}
+
 // ------------------------------------------------------------------------ sharding
 extern "C" uint64_t mra_shard_size(const mra_plan* P) {
     if (!P) return 0;
