@@ -933,6 +933,7 @@ static mra_status eval_wide(mra_plan* P, const TreeParams& tp, long long gf, lon
         const auto& w = P->wsubs[P->wsub_next++];
         if (w.g0 != gf + done) return fail(MRA_E_CUDA, "internal: wide sub-chunk schedule out of order");
         wp.G_base = P->leaf_off[w.g0 * P->J];
+        LCHK_K(KIND_CHAIN, launch_wide(6, tp, wp, 0, P->wtasks + w.chain_off, w.chain_n, P->grid, take_counter(P), st));
         LCHK_K(KIND_CHAIN, launch_wide(0, tp, wp, 0, P->wtasks + w.chain_off, w.chain_n, P->grid, take_counter(P), st));
         LCHK_K(KIND_SIGMA, launch_wide(1, tp, wp, 0, P->wtasks + w.sigma_off, w.sigma_n, P->grid, take_counter(P), st));
         constexpr int NBS = 8;   // as in size_wide

@@ -18,6 +18,8 @@
 //   k_mu / k_smooth   posterior state (top-down), only when requested.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "mra_device.cuh"
 #include "mra_internal.h"
 
@@ -92,6 +94,22 @@ __device__ void point_chain(const TreeParams& tp, int m, long long t, int n, con
 #ifdef MRA_PHASE_TIMING
         if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[27], (unsigned long long)k);   // sum of k (= K / rh)
 #endif
+    }
+}
+
+// V chain over covariance blocks already in place: Gc's column block m-k holds C(P, Q_{a_k}) on entry
+// (k_wide_covfill) and V^k on exit. Each step is one single-segment GEMM over the contiguous columns
+// [C_k | V^{k-1} .. V^1] that overwrites C_k (every output tile reads only its own rows).
+__device__ void point_chain_pre(const TreeParams& tp, int m, long long t, int n, double* Gc, long long ldg,
+                                const CovP& cp, double* smem) {
+    const int rh = tp.rh;
+    for (int k = 1; k <= m; k++) {
+        const long long ak = t >> (tp.lj * (m - k));
+        const long long ldk = (long long)k * rh;
+        const double* Rk = chain_row(tp, k, ak);
+        double* Ck = Gc + (long long)(m - k) * rh;
+        cta_gemm<MEMN, MEMN, MEMN, MEMN>(n, rh, 0, op_mem(Ck, ldg), op_mem(Rk, ldk), k * rh, op_mem(Ck, ldg),
+                                         op_mem(Ck, ldg), 0, ci_zero(), 1.0, Ck, ldg, cp, smem);
     }
 }
 
@@ -563,12 +581,53 @@ __device__ __forceinline__ int leaf_n(const TreeParams& tp, long long l) {
     return (int)(tp.leaf_off[l + 1] - tp.leaf_off[l]);
 }
 
-// V chain + y column for 64 rows of one leaf
+// Covariance blocks C(P, Q_{a_k}), k = 1..M-1, of 64 rows of one leaf into G's column blocks (M-1-k)
+// and the y column: a phase of its own, with no DMMA work sharing the fp64 pipe (generated inside the
+// chain GEMMs, every dependent sqrt / exp chain queued behind the other CTA's DMMAs: ~9k cycles per
+// 64 x 32 stage). Same covf arithmetic as the fused path.
+__global__ void __launch_bounds__(NT)
+k_wide_covfill(TreeParams tp, WideParams wp, const int4* tasks, long long ntask) {
+    __shared__ double2 pts_s[64];
+    __shared__ double2 knots_s[MAXM * 64];
+    const CovP cp = to_covp(tp.cp);
+    const int rh = tp.rh, m = tp.M - 1, Pg = m * rh;
+    for (long long it = blockIdx.x; it < ntask; it += gridDim.x) {
+        const int4 tk = tasks[it];
+        const long long l = tk.x, t = l >> tp.lj;
+        const long long o0 = tp.leaf_off[l] + 64LL * tk.y;
+        const int n = min(64, leaf_n(tp, l) - 64 * tk.y);
+        __syncthreads();
+        if (threadIdx.x < n) pts_s[threadIdx.x] = ldpt(tp.pxy, o0 + threadIdx.x);
+        // the knots of every ancestor, in G's column order (block b = level m - b)
+        for (int c = threadIdx.x; c < Pg; c += NT) {
+            const int b = c / rh, k = m - b;
+            const long long akid = lvl_first(tp.J, k) + (t >> (tp.lj * (m - k)));
+            knots_s[c] = ldpt(tp.kxy + 2 * akid * rh, c - b * rh);
+        }
+        __syncthreads();
+        double* Gr = wp.G + (o0 - wp.G_base) * wp.ldG;
+        // the n x Pg entries flattened over the CTA (balanced), (row, column) advanced incrementally
+        int i = 0, c = threadIdx.x;
+        while (c >= Pg) { c -= Pg; i++; }
+        const int di = NT / Pg, dc = NT - di * Pg;
+#pragma unroll 4
+        for (long long e = threadIdx.x; e < (long long)n * Pg; e += NT) {
+            const double2 pp = pts_s[i], q = knots_s[c];
+            Gr[(long long)i * wp.ldG + c] = covf(cp, pp.x, pp.y, q.x, q.y);
+            i += di;
+            c += dc;
+            if (c >= Pg) { c -= Pg; i++; }
+        }
+        for (int r = threadIdx.x; r < n; r += NT) Gr[(long long)r * wp.ldG + Pg] = tp.zs[o0 + r];
+    }
+}
+
+// V chain for 64 rows of one leaf (covariance blocks in place from k_wide_covfill)
 __global__ void __launch_bounds__(NT, MRA_MINB)
 k_wide_chain(TreeParams tp, WideParams wp, const int4* tasks, long long ntask, unsigned long long* counter) {
     extern __shared__ double smem[];
     const CovP cp = to_covp(tp.cp);
-    const int m = tp.M - 1, Pg = m * tp.rh;
+    const int m = tp.M - 1;
     for (;;) {
         const long long it = next_item(counter, smem);
         if (it >= ntask) break;
@@ -578,8 +637,7 @@ k_wide_chain(TreeParams tp, WideParams wp, const int4* tasks, long long ntask, u
         const int n = min(64, leaf_n(tp, l) - 64 * tk.y);
         double* Gr = wp.G + (o0 - wp.G_base) * wp.ldG;
         PHASE_MARK(pt0);
-        point_chain(tp, m, l >> tp.lj, n, tp.pxy + 2 * o0, Gr, wp.ldG, cp, smem);
-        for (int i = threadIdx.x; i < n; i += NT) Gr[(long long)i * wp.ldG + Pg] = tp.zs[o0 + i];
+        point_chain_pre(tp, m, l >> tp.lj, n, Gr, wp.ldG, cp, smem);
         PHASE_ADD(28, pt0);
 #ifdef MRA_PHASE_TIMING
         if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[29], 1ULL);
@@ -1140,7 +1198,7 @@ namespace mra {
 cudaError_t launch_wide(int phase, const TreeParams& tp, const WideParams& wp, int step, const int4* tasks,
                         long long ntask, int grid, unsigned long long* counter, cudaStream_t st) {
     set_attrs();
-    grid = clamp_grid(grid, ntask, phase == 5 ? 9 : 4 + phase);
+    grid = clamp_grid(grid, ntask, phase == 5 ? 9 : (phase == 6 ? 4 : 4 + phase));
     if (grid < 1) return cudaSuccess;
     const int b = smem_bytes();
     switch (phase) {
@@ -1150,6 +1208,18 @@ cudaError_t launch_wide(int phase, const TreeParams& tp, const WideParams& wp, i
         case 3: k_wide_diag<<<grid, NT, b, st>>>(tp, wp, step, tasks, ntask, counter); break;
         case 4: k_wide_panel_x<<<grid, NT, b, st>>>(tp, wp, step, tasks, ntask, counter); break;
         case 5: k_wide_trsm<<<grid, NT, b, st>>>(tp, wp, tasks, ntask, counter); break;
+        case 6: {
+            static int cf_grid = 0;
+            if (!cf_grid) {
+                int per = 1, dev = 0, nsm = 148;
+                cudaGetDevice(&dev);
+                cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_wide_covfill, NT, 0);
+                cf_grid = (per > 0 ? per : 1) * nsm;
+            }
+            k_wide_covfill<<<(int)std::min<long long>(cf_grid, ntask), NT, 0, st>>>(tp, wp, tasks, ntask);
+            break;
+        }
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
