@@ -232,3 +232,40 @@ def test_device_plan_build_matches_host(mra, n, M, J, r, cl):
     th = (EXP, 1.0, 0.1, 0.05)
     assert mra.mra_loglik(pd, z, th)["loglik"] == mra.mra_loglik(ph, z, th)["loglik"]
     pd.close(); ph.close()
+
+
+@pytest.mark.parametrize("n,M,J,r,cov,cl,dom", [
+    (800, 3, 4, 1, EXP, 0, (0.0, 1.0, 0.0, 1.0)),        # r_hat = 1: one knot per region (its midpoint, R7)
+    (900, 4, 2, 2, MAT, 0, (0.0, 3.0, 0.0, 0.5)),        # r_hat = 2 (1 x 2 bars), wide flat domain: J=2 splits x
+    (700, 3, 4, 3, EXP, 2, (-5.0, 5.0, 10.0, 11.0)),     # r_hat = 3, translated anisotropic domain, empty leaves
+    (40, 2, 4, 4, EXP, 0, (0.0, 1.0, 0.0, 1.0)),         # ~10 observations per leaf
+    (5, 2, 2, 4, MAT, 0, (0.0, 1.0, 0.0, 1.0)),          # 5 observations, most leaves empty or single
+])
+def test_edge_cases(mra, n, M, J, r, cov, cl, dom):
+    """Degenerate knot counts (r_hat 1..3), extreme aspect ratios, tiny leaves, nearly-empty trees:
+    log L, per-region terms and posterior state against the oracle."""
+    x, y, z = synth.uniform_small(n, seed=700 + n, clusters=cl, domain=dom)
+    theta = (cov, 1.1, 0.3, 0.07)
+    for wide in (0, -1):
+        p = mra.mra_plan_create(x, y, M, J, r, wide=wide)
+        got = mra.mra_loglik(p, z, theta, posterior=True, regions=True)
+        ref = oracle.run(x, y, z, M, J, r, theta, regions=True, posterior=True)
+        _cmp(got, ref)
+        p.close()
+
+
+def test_nonfinite_inputs_are_arg_errors(mra):
+    x, y, z = synth.uniform_small(300, seed=1)
+    x2 = x.copy(); x2[5] = np.nan
+    with pytest.raises(mra.MraError) as e:
+        mra.mra_plan_create(x2, y, 3, 4, 9)
+    assert e.value.status == 1
+    with pytest.raises(mra.MraError) as e:
+        mra.mra_plan_create(x2, y, 3, 4, 9, host_plan=1)
+    assert e.value.status == 1
+    p = mra.mra_plan_create(x, y, 3, 4, 9)
+    z2 = z.copy(); z2[3] = np.inf
+    with pytest.raises(mra.MraError) as e:
+        mra.mra_loglik(p, z2, (EXP, 1.0, 0.1, 0.05))
+    assert e.value.status == 1
+    p.close()
