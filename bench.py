@@ -91,7 +91,7 @@ def class_flops(leaf_sizes, M, J, r):
 KERNEL_NAMES = {"prior": "k_prior (levels 1..M-1 W chains, Cholesky, inverse)",
                 "bottom": "k_bottom (one CTA per level-(M-1) region: leaves + level M-1 merge)",
                 "merge": "k_merge (levels M-2..1)",
-                "chain": "k_wide_chain (leaf V chains with fused covariance generation)",
+                "chain": "k_wide_chain (leaf V chains: m single-segment GEMMs over the covariance blocks in place)",
                 "sigma": "k_wide_sigma (Sigma_j = C(S,S) + tau2 I - V V^T tiles)",
                 "factor": "k_wide_update/diag/panel_x (blocked Cholesky of Sigma_j, X = L^{-1})",
                 "solve": "k_wide_trsm (G = X [V | y])",
@@ -374,6 +374,8 @@ def run_gpu(args, rank, world, local_rank):
     peak64 = meas64 or derived64
     steps_th = args.steps * ntheta
     cf = class_flops(sizes, w.M, w.J, plan.r_hat)
+    # covariance generation is a write stream: 8 B per generated entry, n_j x (P r_hat + 1) per leaf
+    covgen_bytes = float(np.sum(sizes)) * ((w.M - 1) * plan.r_hat + 1) * 8.0
     kms = dict(zip(mra.KERNEL_CLASSES, kt[0]))
     kcnt = dict(zip(mra.KERNEL_CLASSES, kt[1]))
     roof = None
@@ -400,6 +402,12 @@ def run_gpu(args, rank, world, local_rank):
                                if meas64 else f"{src} bf16_tflops_sustained {bf16} x {FP64_NOMINAL_TF}/{BF16_NOMINAL_TF}",
                 "kernel_share_of_step": round(kms[dom] / ms, 4),
                 "per_class_tflops": {k: round(cf[k] * steps_th / (kms[k] / 1e3) / 1e12, 2) for k in cand},
+                "covgen": ({"kernel": "k_wide_covfill (covariance blocks of the leaf chains, HBM writes)",
+                            "ms_per_step": round(kms["covgen"] / steps_th, 3),
+                            "achieved_gbs": round(covgen_bytes * steps_th / (kms["covgen"] / 1e3) / 1e9, 1),
+                            "hbm_peak_gbs": pk.get("hbm_gbs"),
+                            "bytes_per_step": covgen_bytes}
+                           if kcnt.get("covgen") else None),
                 "step_fp64_tflops": round(fm["total"] * steps_th / (ms / 1e3) / 1e12, 3)}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:

@@ -181,8 +181,9 @@ mra_status mra_plan_shards(const mra_plan* plan, int* shard_level, int64_t* own,
  *   0 prior (k_prior)   1 bottom (k_bottom: one CTA per level-(M-1) region)   2 merge (k_merge)
  *   3 other (gather, final, posterior state)   4 chain (k_wide_chain: leaf V chains)
  *   5 sigma (k_wide_sigma)   6 factor (k_wide_update / _diag / _panel_x: blocked Cholesky, X = L^{-1})
- *   7 solve (k_wide_trsm: G = X [V | y])   8 syrk+merge (k_wide_mtile: Atilde = G^T G, merge at M-1) */
-#define MRA_NKCLASS 9
+ *   7 solve (k_wide_trsm: G = X [V | y])   8 syrk+merge (k_wide_mtile: Atilde = G^T G, merge at M-1)
+ *   9 covgen (k_wide_covfill: the covariance blocks of the leaf chains, written to HBM) */
+#define MRA_NKCLASS 10
 mra_status mra_profile(mra_plan* plan, int enable);
 mra_status mra_kernel_times(const mra_plan* plan, double* ms, uint64_t* launches);
 

@@ -290,7 +290,7 @@ def mra_profile(plan: PlanHandle, enable: bool = True):
     _check(_lib.mra_profile(plan.ptr, int(bool(enable))))
 
 
-KERNEL_CLASSES = ("prior", "bottom", "merge", "other", "chain", "sigma", "factor", "solve", "syrk_merge")
+KERNEL_CLASSES = ("prior", "bottom", "merge", "other", "chain", "sigma", "factor", "solve", "syrk_merge", "covgen")
 
 
 def mra_kernel_times(plan: PlanHandle) -> dict:

@@ -108,7 +108,7 @@ struct mra_plan {
 
 // kernel classes of the live timing (include/mra.h MRA_NKCLASS)
 enum { KIND_PRIOR = 0, KIND_BOTTOM = 1, KIND_MERGE = 2, KIND_OTHER = 3, KIND_CHAIN = 4, KIND_SIGMA = 5,
-       KIND_FACTOR = 6, KIND_SOLVE = 7, KIND_SYRKMERGE = 8 };
+       KIND_FACTOR = 6, KIND_SOLVE = 7, KIND_SYRKMERGE = 8, KIND_COVGEN = 9 };
 
 static cudaEvent_t take_event(mra_plan* P) {
     if (P->ev_used == P->evpool.size()) {
@@ -624,9 +624,10 @@ static mra_status size_wide(mra_plan* P, double budget, bool explicit_budget) {
                             for (int a = 0; a < nrF; a++) tasks.push_back(make_int4((int)gf, 1, a, 0));
                         const long long go = st - D2;
                         if (go >= 0 && go < gc) {
-                            if (ysep) tasks.push_back(make_int4((int)go, 3, 0, 0));
                             for (int a = 0; a < nrF; a++)
                                 for (int b = 0; b <= a; b++) tasks.push_back(make_int4((int)go, 2, a, b));
+                            // after the group's O tiles, which have just brought its G panels into L2
+                            if (ysep) tasks.push_back(make_int4((int)go, 3, 0, 0));
                         }
                     }
                     ws.mt_n = (long long)tasks.size() - ws.mt_off;
@@ -933,7 +934,7 @@ static mra_status eval_wide(mra_plan* P, const TreeParams& tp, long long gf, lon
         const auto& w = P->wsubs[P->wsub_next++];
         if (w.g0 != gf + done) return fail(MRA_E_CUDA, "internal: wide sub-chunk schedule out of order");
         wp.G_base = P->leaf_off[w.g0 * P->J];
-        LCHK_K(KIND_CHAIN, launch_wide(6, tp, wp, 0, P->wtasks + w.chain_off, w.chain_n, P->grid, take_counter(P), st));
+        LCHK_K(KIND_COVGEN, launch_wide(6, tp, wp, 0, P->wtasks + w.chain_off, w.chain_n, P->grid, take_counter(P), st));
         LCHK_K(KIND_CHAIN, launch_wide(0, tp, wp, 0, P->wtasks + w.chain_off, w.chain_n, P->grid, take_counter(P), st));
         LCHK_K(KIND_SIGMA, launch_wide(1, tp, wp, 0, P->wtasks + w.sigma_off, w.sigma_n, P->grid, take_counter(P), st));
         constexpr int NBS = 8;   // as in size_wide
