@@ -157,6 +157,25 @@ mra_status mra_loglik_shard(mra_plan* plan, const double* d_y, const mra_theta* 
 mra_status mra_loglik_finish(mra_plan* plan, const mra_theta* theta, const double* d_xbuf,
                              double* loglik);
 
+/* Posterior state on a sharded plan (S6 for G > 1: "broadcast of above-shard mu, then
+ * each GPU finishes S6 locally"):
+ *   mra_loglik_shard_post(plan, d_y, theta, d_xbuf)     as mra_loglik_shard, keeping this rank's
+ *        merge factors (posterior state of its subtrees);
+ *   <sum-reduce d_xbuf to rank 0>
+ *   mra_loglik_finish_post(plan, theta, d_xbuf, loglik, d_mutop)   (rank 0) as mra_loglik_finish, and
+ *        writes the posterior means of the regions above the shard level into the DEVICE buffer
+ *        d_mutop[mra_mutop_size(plan)] (whitened means, then the paper's parametrization);
+ *   <broadcast d_mutop from rank 0>
+ *   mra_posterior_shard(plan, d_mutop, d_mu, d_smooth)   (every rank) E[eta_R | y] for the regions above
+ *        the shard level and this rank's subtrees (d_mu [n_interior * r_hat], NaN for other ranks'
+ *        subtrees) and E[X(s_i) | y] for this rank's observations (d_smooth [n], original order, NaN
+ *        elsewhere); DEVICE pointers, either may be NULL. */
+uint64_t mra_mutop_size(const mra_plan* plan);
+mra_status mra_loglik_shard_post(mra_plan* plan, const double* d_y, const mra_theta* theta, double* d_xbuf);
+mra_status mra_loglik_finish_post(mra_plan* plan, const mra_theta* theta, const double* d_xbuf,
+                                  double* loglik, double* d_mutop);
+mra_status mra_posterior_shard(mra_plan* plan, const double* d_mutop, double* d_mu, double* d_smooth);
+
 /* Plan statistics (the paper's build_structure_only report): any pointer may
  * be NULL. n_regions = (J^M - 1)/(J - 1), n_leaves = J^(M-1). */
 mra_status mra_plan_info(const mra_plan* plan, uint64_t* n_retained, int* r_hat,

@@ -54,7 +54,8 @@ class _Post(ctypes.Structure):
 
 _lib = None
 EXPORTS = ["mra_plan_create", "mra_loglik", "mra_loglik_dev", "mra_loglik_batch_dev", "mra_predict", "mra_optimize", "mra_shard_size",
-           "mra_loglik_shard", "mra_loglik_finish", "mra_plan_info", "mra_plan_layout", "mra_plan_shards",
+           "mra_loglik_shard", "mra_loglik_finish", "mra_mutop_size", "mra_loglik_shard_post",
+           "mra_loglik_finish_post", "mra_posterior_shard", "mra_plan_info", "mra_plan_layout", "mra_plan_shards",
            "mra_profile", "mra_kernel_times", "mra_last_launches", "mra_plan_destroy", "mra_last_error"]
 
 
@@ -83,6 +84,14 @@ def load_library(path: str = LIB_PATH):
     lib.mra_shard_size.argtypes = [P]
     lib.mra_loglik_shard.restype = ctypes.c_int
     lib.mra_loglik_shard.argtypes = [P, P, ctypes.POINTER(_Theta), P]
+    lib.mra_mutop_size.restype = U64
+    lib.mra_mutop_size.argtypes = [P]
+    lib.mra_loglik_shard_post.restype = ctypes.c_int
+    lib.mra_loglik_shard_post.argtypes = [P, P, ctypes.POINTER(_Theta), P]
+    lib.mra_loglik_finish_post.restype = ctypes.c_int
+    lib.mra_loglik_finish_post.argtypes = [P, ctypes.POINTER(_Theta), P, D, P]
+    lib.mra_posterior_shard.restype = ctypes.c_int
+    lib.mra_posterior_shard.argtypes = [P, P, P, P]
     lib.mra_loglik_finish.restype = ctypes.c_int
     lib.mra_loglik_finish.argtypes = [P, ctypes.POINTER(_Theta), P, D]
     lib.mra_plan_info.restype = ctypes.c_int
@@ -245,6 +254,30 @@ def mra_loglik_shard(plan: PlanHandle, y_dev, theta, xbuf_dev):
     th = _theta(theta)
     _check(_lib.mra_loglik_shard(plan.ptr, ctypes.c_void_p(y_dev.data_ptr()), ctypes.byref(th),
                                  ctypes.c_void_p(xbuf_dev.data_ptr())))
+
+
+def mra_mutop_size(plan: PlanHandle) -> int:
+    return int(_lib.mra_mutop_size(plan.ptr))
+
+
+def mra_loglik_shard_post(plan: PlanHandle, y_dev, theta, xbuf_dev):
+    th = _theta(theta)
+    _check(_lib.mra_loglik_shard_post(plan.ptr, ctypes.c_void_p(y_dev.data_ptr()), ctypes.byref(th),
+                                      ctypes.c_void_p(xbuf_dev.data_ptr())))
+
+
+def mra_loglik_finish_post(plan: PlanHandle, theta, xbuf_dev, mutop_dev) -> float:
+    th = _theta(theta)
+    ll = ctypes.c_double()
+    _check(_lib.mra_loglik_finish_post(plan.ptr, ctypes.byref(th), ctypes.c_void_p(xbuf_dev.data_ptr()),
+                                       ctypes.byref(ll), ctypes.c_void_p(mutop_dev.data_ptr())))
+    return ll.value
+
+
+def mra_posterior_shard(plan: PlanHandle, mutop_dev, mu_dev=None, smooth_dev=None):
+    _check(_lib.mra_posterior_shard(plan.ptr, ctypes.c_void_p(mutop_dev.data_ptr()),
+                                    ctypes.c_void_p(mu_dev.data_ptr() if mu_dev is not None else 0),
+                                    ctypes.c_void_p(smooth_dev.data_ptr() if smooth_dev is not None else 0)))
 
 
 def mra_loglik_finish(plan: PlanHandle, theta, xbuf_dev) -> float:

@@ -1118,14 +1118,12 @@ static mra_status run_eval(mra_plan* P, const double* d_y, const mra_theta* th, 
         if (post->region_u) CU(cudaMemcpy(post->region_u, P->ureg, 8 * P->nreg, cudaMemcpyDeviceToHost));
     }
     if (want_state) {
-        for (int m = 1; m < P->M; m++) LCHK(launch_mu(tp, m, P->muhat, P->mu_d, P->st));
+        for (int m = 1; m < P->M; m++) LCHK(launch_mu(tp, m, P->muhat, P->mu_d, 0, ipow(P->J, m - 1), P->st));
         if (post->smooth) {
             LCHK(launch_fill(P->smooth_d, (long long)P->n_in, NAN, P->st));
-            if (P->wide)
-                LCHK(launch_smooth(tp, P->muhat, P->perm_d, P->smooth_d, P->smooth_grid, P->ws_smooth, P->Ls,
-                                   take_counter(P), P->st));
-            else
-                LCHK(launch_smooth(tp, P->muhat, P->perm_d, P->smooth_d, P->grid, P->ws, P->L, take_counter(P), P->st));
+            LCHK(launch_smooth(tp, P->muhat, P->perm_d, P->smooth_d, P->wide ? P->smooth_grid : P->grid,
+                               P->wide ? P->ws_smooth : P->ws, P->wide ? P->Ls : P->L, take_counter(P), 0, P->nleaf,
+                               P->st));
         }
         if ((s = check_err(P))) return s;
         const size_t nmu = 8 * (size_t)P->nint * P->rh;
@@ -1384,12 +1382,14 @@ extern "C" uint64_t mra_shard_size(const mra_plan* P) {
     return (uint64_t)(ns * q * q + 2 * ns);
 }
 
-extern "C" mra_status mra_loglik_shard(mra_plan* P, const double* d_y, const mra_theta* th, double* d_xbuf) {
+static mra_status shard_impl(mra_plan* P, const double* d_y, const mra_theta* th, double* d_xbuf, bool post) {
     if (!P || !d_y || !d_xbuf) return fail(MRA_E_ARG, "NULL argument");
     if (P->M < 2) return fail(MRA_E_CONFIG, "sharding needs M >= 2");
     mra_status s;
+    if (post && (s = ensure_post(P))) return s;
     if ((s = begin_eval(P, d_y, th))) return s;
     TreeParams tp = tree_params(P, th);
+    if (post) tp.post = P->post;
     CU(cudaMemsetAsync(P->dreg, 0, 8 * P->nreg, P->st));
     CU(cudaMemsetAsync(P->ureg, 0, 8 * P->nreg, P->st));
     const long long ns = ipow(P->J, P->c - 1), q = q_of(P->c, P->rh);
@@ -1400,16 +1400,32 @@ extern "C" mra_status mra_loglik_shard(mra_plan* P, const double* d_y, const mra
     CU(cudaMemcpyAsync(d_xbuf + ns * q * q, P->dreg + lvl_first(P->J, P->c), 8 * ns, cudaMemcpyDeviceToDevice, P->st));
     CU(cudaMemcpyAsync(d_xbuf + ns * q * q + ns, P->ureg + lvl_first(P->J, P->c), 8 * ns, cudaMemcpyDeviceToDevice,
                        P->st));
-    return check_err(P);
+    if ((s = check_err(P))) return s;
+    if (post) {
+        P->post_valid = true;   // the own subtrees' merge factors (Li, F) of this theta are kept
+        P->post_theta = *th;
+    }
+    return MRA_OK;
 }
 
-extern "C" mra_status mra_loglik_finish(mra_plan* P, const mra_theta* th, const double* d_xbuf, double* loglik) {
+extern "C" mra_status mra_loglik_shard(mra_plan* P, const double* d_y, const mra_theta* th, double* d_xbuf) {
+    return shard_impl(P, d_y, th, d_xbuf, false);
+}
+
+extern "C" mra_status mra_loglik_shard_post(mra_plan* P, const double* d_y, const mra_theta* th, double* d_xbuf) {
+    return shard_impl(P, d_y, th, d_xbuf, true);
+}
+
+static mra_status finish_impl(mra_plan* P, const mra_theta* th, const double* d_xbuf, double* loglik,
+                              double* d_mutop) {
     if (!P || !d_xbuf) return fail(MRA_E_ARG, "NULL argument");
     if (P->device < 0) return fail(MRA_E_CUDA, "host-only plan (device -2) cannot evaluate");
     mra_status s = check_theta(th);
     if (s) return s;
     if (cudaSetDevice(P->device) != cudaSuccess) return fail(MRA_E_CUDA, "cudaSetDevice failed");
+    if (d_mutop && (s = ensure_post(P))) return s;
     TreeParams tp = tree_params(P, th);
+    if (d_mutop) tp.post = P->post;
     const long long ns = ipow(P->J, P->c - 1), q = q_of(P->c, P->rh);
     CU(cudaMemcpyAsync(P->out_full[P->c], d_xbuf, 8 * ns * q * q, cudaMemcpyDeviceToDevice, P->st));
     CU(cudaMemcpyAsync(P->dreg + lvl_first(P->J, P->c), d_xbuf + ns * q * q, 8 * ns, cudaMemcpyDeviceToDevice, P->st));
@@ -1418,7 +1434,72 @@ extern "C" mra_status mra_loglik_finish(mra_plan* P, const mra_theta* th, const 
     if ((s = eval_upper(P, tp))) return s;
     double ll = NAN;
     CU(cudaMemcpyAsync(&ll, P->loglik_d, 8, cudaMemcpyDeviceToHost, P->st));
+    if (d_mutop) {
+        // posterior means of the levels above the shard level (merged here), to be broadcast
+        for (int m = 1; m < P->c; m++) LCHK(launch_mu(tp, m, P->muhat, P->mu_d, 0, ipow(P->J, m - 1), P->st));
+        const long long top = lvl_first(P->J, P->c) * P->rh;
+        if (top > 0) {
+            CU(cudaMemcpyAsync(d_mutop, P->muhat, 8 * top, cudaMemcpyDeviceToDevice, P->st));
+            CU(cudaMemcpyAsync(d_mutop + top, P->mu_d, 8 * top, cudaMemcpyDeviceToDevice, P->st));
+        }
+    }
     if ((s = check_err(P))) return s;
     if (loglik) *loglik = ll;
+    return MRA_OK;
+}
+
+extern "C" mra_status mra_loglik_finish(mra_plan* P, const mra_theta* th, const double* d_xbuf, double* loglik) {
+    return finish_impl(P, th, d_xbuf, loglik, nullptr);
+}
+
+extern "C" uint64_t mra_mutop_size(const mra_plan* P) {
+    if (!P || P->world <= 1) return 0;
+    return (uint64_t)(2 * lvl_first(P->J, P->c) * P->rh);
+}
+
+extern "C" mra_status mra_loglik_finish_post(mra_plan* P, const mra_theta* th, const double* d_xbuf, double* loglik,
+                                             double* d_mutop) {
+    if (!d_mutop && P && P->c > 1) return fail(MRA_E_ARG, "d_mutop is NULL");
+    return finish_impl(P, th, d_xbuf, loglik, d_mutop ? d_mutop : nullptr);
+}
+
+// every rank, after receiving the levels above the shard level: posterior means of its own subtrees'
+// regions and the smoothed values of its own observations (S6 for G > 1)
+extern "C" mra_status mra_posterior_shard(mra_plan* P, const double* d_mutop, double* d_mu, double* d_smooth) {
+    g_err.clear();
+    if (!P || (!d_mutop && P->c > 1)) return fail(MRA_E_ARG, "NULL argument");
+    if (P->world <= 1) return fail(MRA_E_CONFIG, "not a sharded plan");
+    if (!P->post_valid) return fail(MRA_E_ARG, "no posterior state: run mra_loglik_shard_post first");
+    if (cudaSetDevice(P->device) != cudaSuccess) return fail(MRA_E_CUDA, "cudaSetDevice failed");
+    P->launches = 0;
+    P->next_counter = 0;
+    CU(cudaMemsetAsync(P->counters, 0, 8 * (size_t)P->n_counters, P->st));
+    CU(cudaMemsetAsync(P->err, 0, 16, P->st));
+    TreeParams tp = tree_params(P, &P->post_theta);
+    tp.post = P->post;
+    const long long top = lvl_first(P->J, P->c) * P->rh, nmu = P->nint * P->rh;
+    LCHK(launch_fill(P->mu_d, std::max<long long>(nmu, 1), NAN, P->st));
+    if (top > 0) {
+        CU(cudaMemcpyAsync(P->muhat, d_mutop, 8 * top, cudaMemcpyDeviceToDevice, P->st));
+        CU(cudaMemcpyAsync(P->mu_d, d_mutop + top, 8 * top, cudaMemcpyDeviceToDevice, P->st));
+    }
+    auto runs = my_runs(P);
+    for (int m = P->c; m < P->M; m++)
+        for (auto& rg : runs) {
+            long long f, cnt;
+            range_at(P, m, rg.first, rg.second, &f, &cnt);
+            LCHK(launch_mu(tp, m, P->muhat, P->mu_d, f, cnt, P->st));
+        }
+    LCHK(launch_fill(P->smooth_d, (long long)P->n_in, NAN, P->st));
+    const long long per = ipow(P->J, P->M - P->c);
+    for (auto& rg : runs)
+        LCHK(launch_smooth(tp, P->muhat, P->perm_d, P->smooth_d, P->wide ? P->smooth_grid : P->grid,
+                           P->wide ? P->ws_smooth : P->ws, P->wide ? P->Ls : P->L, take_counter(P), rg.first * per,
+                           (rg.second - rg.first) * per, P->st));
+    mra_status s = check_err(P);
+    if (s) return s;
+    if (d_mu && nmu) CU(cudaMemcpyAsync(d_mu, P->mu_d, 8 * nmu, cudaMemcpyDeviceToDevice, P->st));
+    if (d_smooth) CU(cudaMemcpyAsync(d_smooth, P->smooth_d, 8 * P->n_in, cudaMemcpyDeviceToDevice, P->st));
+    CU(cudaStreamSynchronize(P->st));
     return MRA_OK;
 }

@@ -93,10 +93,11 @@ cudaError_t launch_merge(const TreeParams& tp, int m, long long t_first, long lo
                          int q, int grid, double* ws, long long ws_stride, unsigned long long* counter,
                          cudaStream_t st);
 cudaError_t launch_final(const TreeParams& tp, double N, double* d_loglik, cudaStream_t st);
-cudaError_t launch_mu(const TreeParams& tp, int m, double* muhat, double* mu, cudaStream_t st);
+cudaError_t launch_mu(const TreeParams& tp, int m, double* muhat, double* mu, long long t_first, long long t_count,
+                      cudaStream_t st);
 cudaError_t launch_smooth(const TreeParams& tp, const double* muhat, const long long* perm, double* smooth,
-                          int grid, double* ws, const WsLayout& L, unsigned long long* counter,
-                          cudaStream_t st);
+                          int grid, double* ws, const WsLayout& L, unsigned long long* counter, long long l_first,
+                          long long l_count, cudaStream_t st);
 cudaError_t launch_fill(double* p, long long n, double v, cudaStream_t st);
 cudaError_t launch_predict(const TreeParams& tp, const PredParams& pp, int grid, double* ws, const WsLayout& L,
                            unsigned long long* counter, cudaStream_t st);

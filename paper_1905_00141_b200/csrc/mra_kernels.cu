@@ -331,11 +331,10 @@ __global__ void k_fill(double* p, long long n, double v) {
 
 // ----------------------------------------------------------------- posterior state
 // muhat_R = Lt^{-T} (h - sum_k H^k muhat_{a_k})   (whitened), mu_R = L_R^{-T} muhat_R (paper's eta)
-__global__ void k_mu(TreeParams tp, int m, double* muhat, double* mu) {
+__global__ void k_mu(TreeParams tp, int m, double* muhat, double* mu, long long t_first, long long t_count) {
     __shared__ double tv[64], mh[64];
     const int rh = tp.rh, q = (m - 1) * rh + 1;
-    const long long cnt = lvl_first(tp.J, m + 1) - lvl_first(tp.J, m);
-    for (long long t = blockIdx.x; t < cnt; t += gridDim.x) {
+    for (long long t = t_first + blockIdx.x; t < t_first + t_count; t += gridDim.x) {
         const long long id = lvl_first(tp.J, m) + t;
         const double* Li = tp.post + tp.post_base[m] + t * ((long long)rh * rh + (long long)q * rh);
         const double* F = Li + rh * rh;
@@ -370,7 +369,7 @@ __global__ void k_mu(TreeParams tp, int m, double* muhat, double* mu) {
 // E[X(S_j)|y] = y_j - tau2 Sigma_j^{-1} (y_j - sum_k V^k muhat_{a_k})   (recomputes V, Sigma_j, L_j)
 __global__ void __launch_bounds__(NT, MRA_MINB)
 k_smooth(TreeParams tp, const double* muhat, const long long* perm, double* smooth, double* ws, WsLayout L,
-         unsigned long long* counter) {
+         unsigned long long* counter, long long l_first, long long l_count) {
     extern __shared__ double smem[];
     const CovP cp = to_covp(tp.cp);
     const int M = tp.M, rh = tp.rh, m = M - 1, Pg = m * rh;
@@ -382,8 +381,8 @@ k_smooth(TreeParams tp, const double* muhat, const long long* perm, double* smoo
     long long nleaves = 1;
     for (int i = 1; i < M; i++) nleaves *= tp.J;
     for (;;) {
-        const long long l = next_item(counter, smem);
-        if (l >= nleaves) break;
+        const long long l = l_first + next_item(counter, smem);
+        if (l >= l_first + l_count) break;
         if (threadIdx.x == 0) *f.bad = 0;
         const long long t = (M == 1) ? 0 : (l >> tp.lj);
         const long long o0 = tp.leaf_off[l];
@@ -1177,18 +1176,20 @@ cudaError_t launch_final(const TreeParams& tp, double N, double* d_loglik, cudaS
     k_final<<<1, 32, 0, st>>>(tp, N, d_loglik);
     return cudaGetLastError();
 }
-cudaError_t launch_mu(const TreeParams& tp, int m, double* muhat, double* mu, cudaStream_t st) {
-    long long cnt = 1;
-    for (int i = 1; i < m; i++) cnt *= tp.J;
-    int grid = (int)(cnt < 4096 ? cnt : 4096);
-    k_mu<<<grid, 64, 0, st>>>(tp, m, muhat, mu);
+cudaError_t launch_mu(const TreeParams& tp, int m, double* muhat, double* mu, long long t_first, long long t_count,
+                      cudaStream_t st) {
+    if (t_count < 1) return cudaSuccess;
+    int grid = (int)(t_count < 4096 ? t_count : 4096);
+    k_mu<<<grid, 64, 0, st>>>(tp, m, muhat, mu, t_first, t_count);
     return cudaGetLastError();
 }
 cudaError_t launch_smooth(const TreeParams& tp, const double* muhat, const long long* perm, double* smooth, int grid,
-                          double* ws, const WsLayout& L, unsigned long long* counter, cudaStream_t st) {
+                          double* ws, const WsLayout& L, unsigned long long* counter, long long l_first,
+                          long long l_count, cudaStream_t st) {
     set_attrs();
-    grid = clamp_grid(grid, 1LL << 40, 3);
-    k_smooth<<<grid, NT, smem_bytes(), st>>>(tp, muhat, perm, smooth, ws, L, counter);
+    grid = clamp_grid(grid, l_count, 3);
+    if (grid < 1) return cudaSuccess;
+    k_smooth<<<grid, NT, smem_bytes(), st>>>(tp, muhat, perm, smooth, ws, L, counter, l_first, l_count);
     return cudaGetLastError();
 }
 

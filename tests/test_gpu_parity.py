@@ -156,6 +156,49 @@ def test_sharded_algebra_on_one_gpu(mra):
         assert abs(ll - single) <= 1e-12 * abs(single), (world, ll, single)
 
 
+@pytest.mark.parametrize("wide", [0, -1])
+def test_sharded_posterior_on_one_gpu(mra, wide):
+    """S6 on a sharded plan, ranks emulated in sequence on one GPU: shard passes keep
+    their posterior state, rank 0 finishes and exports the above-shard means, every rank completes its
+    own subtrees' means and smoothed values. The union over ranks equals the single-GPU posterior."""
+    import torch
+    x, y, z = synth.uniform_small(9000, seed=21, clusters=3)
+    theta = (EXP, 1.0, 0.1, 0.05)
+    M, J, r = 5, 4, 16
+    p1 = mra.mra_plan_create(x, y, M, J, r, wide=wide)
+    ref = mra.mra_loglik(p1, z, theta, posterior=True)
+    p1.close()
+    zd = torch.from_numpy(z).cuda()
+    for world in (2, 3):
+        plans = [mra.mra_plan_create(x, y, M, J, r, rank=k, world=world, wide=wide) for k in range(world)]
+        size = mra.mra_shard_size(plans[0])
+        total = torch.zeros(size, dtype=torch.float64, device="cuda")
+        for pl in plans:
+            buf = torch.zeros(size, dtype=torch.float64, device="cuda")
+            mra.mra_loglik_shard_post(pl, zd, theta, buf)
+            total += buf
+        mutop = torch.empty(max(1, mra.mra_mutop_size(plans[0])), dtype=torch.float64, device="cuda")
+        ll = mra.mra_loglik_finish_post(plans[0], theta, total, mutop)
+        assert abs(ll - ref["loglik"]) <= 1e-12 * abs(ref["loglik"])
+        nmu = plans[0].n_interior * plans[0].r_hat
+        mu = np.full(nmu, np.nan)
+        sm = np.full(len(x), np.nan)
+        for pl in plans:
+            dmu = torch.empty(nmu, dtype=torch.float64, device="cuda")
+            dsm = torch.empty(len(x), dtype=torch.float64, device="cuda")
+            mra.mra_posterior_shard(pl, mutop, dmu, dsm)
+            m_, s_ = dmu.cpu().numpy(), dsm.cpu().numpy()
+            mu = np.where(np.isnan(mu), m_, mu)
+            sm = np.where(np.isnan(sm), s_, sm)
+        ref_mu = ref["mu"].ravel()
+        assert not np.any(np.isnan(mu))
+        assert np.max(np.abs(mu - ref_mu)) <= 1e-10 * np.max(np.abs(ref_mu))
+        assert np.array_equal(np.isnan(sm), np.isnan(ref["smooth"]))
+        assert np.nanmax(np.abs(sm - ref["smooth"])) <= 1e-10 * np.nanmax(np.abs(ref["smooth"]))
+        for pl in plans:
+            pl.close()
+
+
 def test_batch_thetas(mra):
     import torch
     w = synth.make("C4", n=30000)
