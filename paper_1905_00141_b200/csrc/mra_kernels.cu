@@ -114,6 +114,43 @@ __device__ void point_chain_pre(const TreeParams& tp, int m, long long t, int n,
 }
 
 // --------------------------------------------------------------------------- prior
+// Covariance blocks of the prior chains of level-m regions, in place of the chain row R (ld m rh):
+// block 0 <- C(Q_R, Q_R) (k_prior turns it into W^m, then overwrites it with L^{-1}), block m-k <-
+// C(Q_R, Q_{a_k}) for k < m (turned into V^k, then -U^k). Own phase, like k_wide_covfill: no DMMA shares
+// the fp64 pipe with the sqrt / exp chains.
+__global__ void __launch_bounds__(NT)
+k_prior_covfill(TreeParams tp, int m, long long t_first, long long nitems) {
+    __shared__ double2 pts_s[64];
+    __shared__ double2 knots_s[MAXM * 64];
+    const CovP cp = to_covp(tp.cp);
+    const int rh = tp.rh, W = m * rh;
+    const long long ldR = (long long)m * rh;
+    for (long long it = blockIdx.x; it < nitems; it += gridDim.x) {
+        const long long t = t_first + it;
+        const long long id = lvl_first(tp.J, m) + t;
+        __syncthreads();
+        if (threadIdx.x < rh) pts_s[threadIdx.x] = ldpt(tp.kxy + 2 * id * rh, threadIdx.x);
+        for (int c = threadIdx.x; c < W; c += NT) {   // column block b holds level m - b (b = 0: R itself)
+            const int b = c / rh, k = m - b;
+            const long long akid = lvl_first(tp.J, k) + (t >> (tp.lj * (m - k)));
+            knots_s[c] = ldpt(tp.kxy + 2 * akid * rh, c - b * rh);
+        }
+        __syncthreads();
+        double* R = tp.prior + tp.prior_base[m] + t * ldR * rh;
+        int i = 0, c = threadIdx.x;
+        while (c >= W) { c -= W; i++; }
+        const int di = NT / W, dc = NT - di * W;
+#pragma unroll 4
+        for (int e = threadIdx.x; e < rh * W; e += NT) {
+            const double2 pp = pts_s[i], q = knots_s[c];
+            R[(long long)i * ldR + c] = covf(cp, pp.x, pp.y, q.x, q.y);
+            i += di;
+            c += dc;
+            if (c >= W) { c -= W; i++; }
+        }
+    }
+}
+
 __global__ void __launch_bounds__(NT, MRA_MINB)
 k_prior(TreeParams tp, int m, long long t_first, long long nitems, double* ws, long long ws_stride,
         unsigned long long* counter) {
@@ -128,15 +165,14 @@ k_prior(TreeParams tp, int m, long long t_first, long long nitems, double* ws, l
         if (it >= nitems) break;
         if (threadIdx.x == 0) *f.bad = 0;
         const long long t = t_first + it;
-        const long long id = lvl_first(tp.J, m) + t;
         double* R = tp.prior + tp.prior_base[m] + t * ldR * rh;
-        const double* q = tp.kxy + 2 * id * rh;
-        // V^k_R for k < m into R's blocks m-k (they become -U after the inverse is known)
-        point_chain(tp, m - 1, t >> tp.lj, rh, q, R + rh, ldR, cp, smem);
-        // W^m_R = C(Q_R, Q_R) - sum_k V^k V^kT
+        // V^k_R for k < m over R's blocks m-k, which hold C(Q_R, Q_{a_k}) (k_prior_covfill); they become -U
+        // after the inverse is known
+        point_chain_pre(tp, m - 1, t >> tp.lj, rh, R + rh, ldR, cp, smem);
+        // W^m_R = C(Q_R, Q_R) - sum_k V^k V^kT   (C(Q_R, Q_R) in R's block 0)
         cta_gemm<MEMN, MEMN, MEMN, MEMN>(rh, rh, 1, op_mem(R + rh, ldR), op_mem(R + rh, ldR), (m - 1) * rh,
-                                         op_mem(R, ldR), op_mem(R, ldR), 0, ci_cov(q, q, 0.0), -1.0,
-                                         W, rh, cp, smem);
+                                         op_mem(R, ldR), op_mem(R, ldR), 0, ci_mem(R, ldR), -1.0, W, rh, cp,
+                                         smem);
         load_block_lower(f.blk, W, rh, rh, 0.0);
         chol_inv_small(f.blk, f.inv, rh, f.diagv, f.bad, f.red, f.tmp);
         if (*f.bad && threadIdx.x == 0) set_err(tp.err, m, t);
@@ -1148,6 +1184,19 @@ cudaError_t launch_fill(double* p, long long n, double v, cudaStream_t st) {
 cudaError_t launch_prior(const TreeParams& tp, int m, long long t_first, long long t_count, int grid, double* ws,
                          long long ws_stride, unsigned long long* counter, cudaStream_t st) {
     set_attrs();
+    if (t_count > 0) {
+        static int cf_grid = 0;
+        if (!cf_grid) {
+            int per = 1, dev = 0, nsm = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_prior_covfill, NT, 0);
+            cf_grid = (per > 0 ? per : 1) * nsm;
+        }
+        k_prior_covfill<<<(int)std::min<long long>(cf_grid, t_count), NT, 0, st>>>(tp, m, t_first, t_count);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
     grid = clamp_grid(grid, t_count, 0);
     if (grid < 1) return cudaSuccess;
     k_prior<<<grid, NT, smem_bytes(), st>>>(tp, m, t_first, t_count, ws, ws_stride, counter);
