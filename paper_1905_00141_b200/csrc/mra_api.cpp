@@ -441,8 +441,8 @@ static mra_status size_device(mra_plan* P, double budget_gb) {
     cudaMemGetInfo(&freeb, &totalb);
     double budget = budget_gb > 0 ? budget_gb * 1e9 : 0.85 * (double)freeb;
     budget -= (double)tot * 8.0;
-    // slots: 2 CTAs per SM, fewer if the per-slot workspace is huge
-    long long slots = 2LL * P->nsm;
+    // slots: the resident CTAs of the persistent grid, fewer if the per-slot workspace is huge
+    long long slots = (long long)resident_ctas_per_sm() * P->nsm;
     const double ws_cap = std::max(0.25 * budget, (double)L.stride * 8.0);
     slots = std::min<long long>(slots, std::max<long long>(1, (long long)(ws_cap / (L.stride * 8.0))));
     P->grid = (int)slots;

@@ -1,6 +1,6 @@
 // mra_device.cuh -- CTA-level fp64 building blocks for the MRA hot path on sm_100a.
 //
-// Everything here is executed by one CTA of NT = 256 threads on matrices that live in
+// Everything here is executed by one CTA of NT = 128 threads on matrices that live in
 // global memory (L2-resident per-CTA workspaces) and are staged through shared memory:
 //   cta_gemm      C = init + alpha * sum_seg opA(seg) opB(seg)^T, 64x64 output tiles,
 //                 fp64 tensor-core MMA (mma.sync.m8n8k4.f64 -> DMMA), operands either
@@ -18,9 +18,18 @@
 
 namespace mra {
 
-constexpr int NT = 256;         // threads per CTA (8 warps)
+#ifndef MRA_NT
+#define MRA_NT 128
+#endif
+constexpr int NT = MRA_NT;      // threads per CTA: 4 warps, each a 32 x 32 sub-tile of the 64 x 64 output
+                                // tile (16 DMMAs per 8 fragment loads), 3 CTAs per SM
 constexpr int TM = 64;          // output tile rows
 constexpr int TN = 64;          // output tile cols
+constexpr int NWARP = NT / 32;
+constexpr int WN = 32;                      // warp sub-tile columns
+constexpr int WM = 64 / (NWARP / (64 / WN));   // warp sub-tile rows (32 for 4 warps, 16 for 8)
+constexpr int MI = WM / 8;                  // 8-row DMMA blocks per warp
+static_assert(NWARP * WM * WN == 64 * 64, "warp tiling");
 #ifndef MRA_TK
 #define MRA_TK 32
 #endif
@@ -128,7 +137,7 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 
 // ------------------------------------------------------------- async tile staging
 #ifndef MRA_NSTAGE
-#define MRA_NSTAGE 3
+#define MRA_NSTAGE 2
 #endif
 constexpr int NSTAGE = MRA_NSTAGE;         // cp.async pipeline depth
 constexpr int STAGE_DBL = 2 * TILE_DBL;    // A tile + B tile
@@ -162,7 +171,7 @@ __device__ __forceinline__ void load_tile_async(double* s, const Op& op, int r0,
     if (KIND == MEMN) {
         if (al16) {
 #pragma unroll
-            for (int i = 0; i < TK / 8; i++) {   // 64 rows x TK/2 16-byte copies over NT threads
+            for (int i = 0; i < 32 * TK / NT; i++) {   // 64 rows x TK/2 16-byte copies over NT threads
                 const int e = tid + NT * i, row = e / (TK / 2), kk = (e % (TK / 2)) * 2;
                 const int ok = (row < nr) ? min(2, max(0, nk - kk)) : 0;
                 const double* g = ok ? op.p + (long long)(r0 + row) * op.ld + k0 + kk : op.p;
@@ -170,7 +179,7 @@ __device__ __forceinline__ void load_tile_async(double* s, const Op& op, int r0,
             }
         } else {
 #pragma unroll
-            for (int i = 0; i < TK / 4; i++) {
+            for (int i = 0; i < 64 * TK / NT; i++) {
                 const int e = tid + NT * i, row = e / TK, kk = e % TK;
                 const bool ok = row < nr && kk < nk;
                 cp_async8(s + row * LDN + kk, ok ? op.p + (long long)(r0 + row) * op.ld + k0 + kk : op.p, ok ? 8 : 0);
@@ -179,7 +188,7 @@ __device__ __forceinline__ void load_tile_async(double* s, const Op& op, int r0,
     } else if (KIND == MEMT) {
         if (al16) {
 #pragma unroll
-            for (int i = 0; i < TK / 8; i++) {
+            for (int i = 0; i < 32 * TK / NT; i++) {
                 const int e = tid + NT * i, kk = e >> 5, row = (e & 31) * 2;
                 const int ok = (kk < nk) ? min(2, max(0, nr - row)) : 0;
                 const double* g = ok ? op.p + (long long)(k0 + kk) * op.ld + r0 + row : op.p;
@@ -187,7 +196,7 @@ __device__ __forceinline__ void load_tile_async(double* s, const Op& op, int r0,
             }
         } else {
 #pragma unroll
-            for (int i = 0; i < TK / 4; i++) {
+            for (int i = 0; i < 64 * TK / NT; i++) {
                 const int e = tid + NT * i, kk = e >> 6, row = e & 63;
                 const bool ok = row < nr && kk < nk;
                 cp_async8(s + kk * LDT + row, ok ? op.p + (long long)(k0 + kk) * op.ld + r0 + row : op.p, ok ? 8 : 0);
@@ -199,7 +208,7 @@ __device__ __forceinline__ void load_tile_async(double* s, const Op& op, int r0,
         const bool kok = kk < nk;
         const double2 qk = kok ? ldpt(op.q, k0 + kk) : make_double2(0.0, 0.0);
 #pragma unroll 4
-        for (int i = 0; i < TK / 4; i++) {
+        for (int i = 0; i < 64 * TK / NT; i++) {
             const int row = rw + (NT / TK) * i;
             double v = 0.0;
             if (kok && row < nr) {
@@ -216,20 +225,20 @@ __device__ __forceinline__ double frag(const double* s, int row, int k) {
     return KIND == MEMT ? s[k * LDT + row] : s[row * LDN + k];
 }
 
-// 8 DMMAs per k-step of 4 on the warp's 16 x 32 sub-tile
+// MI x 4 DMMAs per k-step of 4 on the warp's WM x 32 sub-tile
 template <int KA, int KB>
-__device__ __forceinline__ void mma_ktile(double (&acc)[2][4][2], const double* As, const double* Bs, int nk) {
+__device__ __forceinline__ void mma_ktile(double (&acc)[MI][4][2], const double* As, const double* Bs, int nk) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
-    const int wr = (warp >> 1) * 16, wc = (warp & 1) * 32;
+    const int wr = (warp / (64 / WN)) * WM, wc = (warp % (64 / WN)) * WN;
     auto step = [&](int kk) {
-        double a[2], b[4];
+        double a[MI], b[4];
 #pragma unroll
-        for (int mi = 0; mi < 2; mi++) a[mi] = frag<KA>(As, wr + mi * 8 + g, kk + t);
+        for (int mi = 0; mi < MI; mi++) a[mi] = frag<KA>(As, wr + mi * 8 + g, kk + t);
 #pragma unroll
         for (int ni = 0; ni < 4; ni++) b[ni] = frag<KB>(Bs, wc + ni * 8 + g, kk + t);
 #pragma unroll
-        for (int mi = 0; mi < 2; mi++)
+        for (int mi = 0; mi < MI; mi++)
 #pragma unroll
             for (int ni = 0; ni < 4; ni++) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
     };
@@ -259,7 +268,7 @@ __device__ __forceinline__ GemmDesc* gemm_desc(double* smem);
 
 // accumulate both K-segments of one output tile through an NSTAGE-deep cp.async pipeline
 template <int KA0, int KB0, int KA1, int KB1>
-__device__ __forceinline__ void tile_pipeline(double (&acc)[2][4][2], const GemmDesc& d, int r0, int nr, int c0,
+__device__ __forceinline__ void tile_pipeline(double (&acc)[MI][4][2], const GemmDesc& d, int r0, int nr, int c0,
                                               int nc, double* smem, bool wact) {
     // only the current segment's two operand descriptors are held in registers (segment 1's are read
     // from the shared-memory GemmDesc when the loads reach it): the engine sits at the 128-register
@@ -310,21 +319,21 @@ __device__ __noinline__ void cta_gemm_impl(double* smem) {
     const int Mr = d.Mr, Nc = d.Nc, lower = d.lower, K0 = d.K0, K1 = d.K1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
-    const int wr = (warp >> 1) * 16, wc = (warp & 1) * 32;
+    const int wr = (warp / (64 / WN)) * WM, wc = (warp % (64 / WN)) * WN;
     const int tiles_m = (Mr + TM - 1) / TM, tiles_n = (Nc + TN - 1) / TN;
     for (int tm = 0; tm < tiles_m; tm++) {
         for (int tn = 0; tn < tiles_n; tn++) {
             if (lower && tn > tm) continue;
             const int r0 = tm * TM, c0 = tn * TN;
             const int nr = min(TM, Mr - r0), nc = min(TN, Nc - c0);
-            double acc[2][4][2];
+            double acc[MI][4][2];
 #pragma unroll
-            for (int mi = 0; mi < 2; mi++)
+            for (int mi = 0; mi < MI; mi++)
 #pragma unroll
                 for (int ni = 0; ni < 4; ni++) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
             // warps whose sub-tile lies outside a ragged tile (e.g. the 1-row y tile) or strictly above the
             // diagonal of a lower-triangular tile skip their DMMAs
-            const bool wact = wr < nr && wc < nc && !(lower && tm == tn && wc > wr + 15);
+            const bool wact = wr < nr && wc < nc && !(lower && tm == tn && wc > wr + WM - 1);
             if (K0 + K1 > 0)
                 tile_pipeline<KA0, KB0, KA1, KB1>(acc, d, r0, nr, c0, nc, smem, wact);
             const CInit ci = d.ci;
@@ -336,7 +345,7 @@ __device__ __noinline__ void cta_gemm_impl(double* smem) {
             const bool vec = ((reinterpret_cast<uintptr_t>(C) & 15) == 0) && ((ldc & 1) == 0) &&
                              (ci.kind != 1 || (((reinterpret_cast<uintptr_t>(ci.p) & 15) == 0) && ((ci.ld & 1) == 0)));
 #pragma unroll
-            for (int mi = 0; mi < 2; mi++)
+            for (int mi = 0; mi < MI; mi++)
 #pragma unroll
                 for (int ni = 0; ni < 4; ni++) {
                     const int i = r0 + wr + mi * 8 + g, j = c0 + wc + ni * 8 + 2 * t;
@@ -361,7 +370,7 @@ __device__ __noinline__ void cta_gemm_impl(double* smem) {
                 // covariance initial value, added by the thread that stored the element (4 independent
                 // fp64 sqrt/exp chains in flight per thread)
 #pragma unroll 4
-                for (int q = 0; q < 16; q++) {
+                for (int q = 0; q < MI * 8; q++) {
                     const int mi = q >> 3, ni = (q >> 1) & 3, e = q & 1;
                     const int i = r0 + wr + mi * 8 + g, j = c0 + wc + ni * 8 + 2 * t + e;
                     if (i < Mr && j < Nc && (!lower || j <= i)) {
@@ -490,12 +499,13 @@ __device__ __noinline__ double chol_inv_small(double* a, double* x, int n, doubl
         const int r0 = j0 + nb, nr = n - r0;
         if (nr > 0) {
             // panel: L_ib = A_ib X_bb^T for rows r0..n-1 (<= 48), cols j0..j0+nb-1; thread = (row group, col)
+            constexpr int RG = NT / 16, NQ = (48 + RG - 1) / RG;   // row groups per pass, passes over <= 48 rows
             const int jj = tid & 15, rg = tid >> 4;
             const double* xr = x + (j0 + jj) * LDB + j0;
-            double v[3];
+            double v[NQ];
 #pragma unroll
-            for (int q = 0; q < 3; q++) {
-                const int row = r0 + rg + 16 * q;
+            for (int q = 0; q < NQ; q++) {
+                const int row = r0 + rg + RG * q;
                 double s0 = 0.0, s1 = 0.0;
                 if (row < n && jj < nb) {
                     const double* ar = a + row * LDB + j0;
@@ -509,16 +519,16 @@ __device__ __noinline__ double chol_inv_small(double* a, double* x, int n, doubl
             }
             __syncthreads();
 #pragma unroll
-            for (int q = 0; q < 3; q++) {
-                const int row = r0 + rg + 16 * q;
+            for (int q = 0; q < NQ; q++) {
+                const int row = r0 + rg + RG * q;
                 if (row < n && jj < nb) a[row * LDB + j0 + jj] = v[q];
             }
             __syncthreads();
             // trailing update A_rc -= sum_k L_rk L_ck (lower part), thread = (row offset, col offset) 16 x 16
             const int tx = tid & 15, ty = tid >> 4;
 #pragma unroll
-            for (int qi = 0; qi < 3; qi++) {
-                const int row = r0 + ty + 16 * qi;
+            for (int qi = 0; qi < NQ; qi++) {
+                const int row = r0 + ty + RG * qi;
                 if (row >= n) continue;
                 const double* lr = a + row * LDB + j0;
                 double lrv[16];

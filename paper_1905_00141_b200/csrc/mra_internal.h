@@ -127,6 +127,7 @@ cudaError_t plan_radix_scatter(const int* key, const int* idx, long long n, int 
 cudaError_t plan_gather(const double* x, const double* y, const int* idx, long long N, double* pxy, long long* perm,
                         cudaStream_t st);
 int smem_bytes();
+int resident_ctas_per_sm();   // engine kernels (k_bottom occupancy)
 void phase_cycles(unsigned long long* out32, bool reset);   // -DMRA_PHASE_TIMING builds only
 
 }  // namespace mra

@@ -24,7 +24,7 @@
 #include "mra_internal.h"
 
 #ifndef MRA_MINB
-#define MRA_MINB 2   // resident CTAs per SM the register allocation is sized for
+#define MRA_MINB 3   // resident CTAs per SM the register allocation is sized for (128-thread CTAs)
 #endif
 
 namespace mra {
@@ -118,7 +118,9 @@ __device__ void point_chain_pre(const TreeParams& tp, int m, long long t, int n,
 // block 0 <- C(Q_R, Q_R) (k_prior turns it into W^m, then overwrites it with L^{-1}), block m-k <-
 // C(Q_R, Q_{a_k}) for k < m (turned into V^k, then -U^k). Own phase, like k_wide_covfill: no DMMA shares
 // the fp64 pipe with the sqrt / exp chains.
-__global__ void __launch_bounds__(NT)
+constexpr int CFT = 256;   // threads of the covariance-generation kernels (independent of the engine's NT)
+
+__global__ void __launch_bounds__(CFT)
 k_prior_covfill(TreeParams tp, int m, long long t_first, long long nitems) {
     __shared__ double2 pts_s[64];
     __shared__ double2 knots_s[MAXM * 64];
@@ -130,7 +132,7 @@ k_prior_covfill(TreeParams tp, int m, long long t_first, long long nitems) {
         const long long id = lvl_first(tp.J, m) + t;
         __syncthreads();
         if (threadIdx.x < rh) pts_s[threadIdx.x] = ldpt(tp.kxy + 2 * id * rh, threadIdx.x);
-        for (int c = threadIdx.x; c < W; c += NT) {   // column block b holds level m - b (b = 0: R itself)
+        for (int c = threadIdx.x; c < W; c += CFT) {   // column block b holds level m - b (b = 0: R itself)
             const int b = c / rh, k = m - b;
             const long long akid = lvl_first(tp.J, k) + (t >> (tp.lj * (m - k)));
             knots_s[c] = ldpt(tp.kxy + 2 * akid * rh, c - b * rh);
@@ -139,9 +141,9 @@ k_prior_covfill(TreeParams tp, int m, long long t_first, long long nitems) {
         double* R = tp.prior + tp.prior_base[m] + t * ldR * rh;
         int i = 0, c = threadIdx.x;
         while (c >= W) { c -= W; i++; }
-        const int di = NT / W, dc = NT - di * W;
+        const int di = CFT / W, dc = CFT - di * W;
 #pragma unroll 4
-        for (int e = threadIdx.x; e < rh * W; e += NT) {
+        for (int e = threadIdx.x; e < rh * W; e += CFT) {
             const double2 pp = pts_s[i], q = knots_s[c];
             R[(long long)i * ldR + c] = covf(cp, pp.x, pp.y, q.x, q.y);
             i += di;
@@ -326,14 +328,13 @@ k_merge(TreeParams tp, int m, long long t_first, long long t_count, const double
         if (threadIdx.x == 0) *f.bad = 0;
         const long long t = t_first + it;
         const double* C0 = child_out + (t * J - child_first) * qc2;
-        for (long long e = threadIdx.x; e < qc2; e += NT) {
-            const int i = (int)(e / qc), j = (int)(e - (long long)i * qc);
-            if (j <= i) {
+        for (int i = 0; i < qc; i++)   // lower triangle, row by row (coalesced, no index division)
+            for (int j = threadIdx.x; j <= i; j += NT) {
+                const long long e = (long long)i * qc + j;
                 double s = 0.0;
                 for (int c = 0; c < J; c++) s += C0[c * qc2 + e];
                 A[(long long)i * ldA + j] = s;
             }
-        }
         __syncthreads();
         double* O = out + (t - out_first) * (long long)q * q;
         const double ldm = merge_core(A, rh, ldA, O, q, F, Li, tp.err, m, t, cp, smem);
@@ -620,7 +621,7 @@ __device__ __forceinline__ int leaf_n(const TreeParams& tp, long long l) {
 // and the y column: a phase of its own, with no DMMA work sharing the fp64 pipe (generated inside the
 // chain GEMMs, every dependent sqrt / exp chain queued behind the other CTA's DMMAs: ~9k cycles per
 // 64 x 32 stage). Same covf arithmetic as the fused path.
-__global__ void __launch_bounds__(NT)
+__global__ void __launch_bounds__(CFT)
 k_wide_covfill(TreeParams tp, WideParams wp, const int4* tasks, long long ntask) {
     __shared__ double2 pts_s[64];
     __shared__ double2 knots_s[MAXM * 64];
@@ -634,7 +635,7 @@ k_wide_covfill(TreeParams tp, WideParams wp, const int4* tasks, long long ntask)
         __syncthreads();
         if (threadIdx.x < n) pts_s[threadIdx.x] = ldpt(tp.pxy, o0 + threadIdx.x);
         // the knots of every ancestor, in G's column order (block b = level m - b)
-        for (int c = threadIdx.x; c < Pg; c += NT) {
+        for (int c = threadIdx.x; c < Pg; c += CFT) {
             const int b = c / rh, k = m - b;
             const long long akid = lvl_first(tp.J, k) + (t >> (tp.lj * (m - k)));
             knots_s[c] = ldpt(tp.kxy + 2 * akid * rh, c - b * rh);
@@ -644,16 +645,16 @@ k_wide_covfill(TreeParams tp, WideParams wp, const int4* tasks, long long ntask)
         // the n x Pg entries flattened over the CTA (balanced), (row, column) advanced incrementally
         int i = 0, c = threadIdx.x;
         while (c >= Pg) { c -= Pg; i++; }
-        const int di = NT / Pg, dc = NT - di * Pg;
+        const int di = CFT / Pg, dc = CFT - di * Pg;
 #pragma unroll 4
-        for (long long e = threadIdx.x; e < (long long)n * Pg; e += NT) {
+        for (long long e = threadIdx.x; e < (long long)n * Pg; e += CFT) {
             const double2 pp = pts_s[i], q = knots_s[c];
             Gr[(long long)i * wp.ldG + c] = covf(cp, pp.x, pp.y, q.x, q.y);
             i += di;
             c += dc;
             if (c >= Pg) { c -= Pg; i++; }
         }
-        for (int r = threadIdx.x; r < n; r += NT) Gr[(long long)r * wp.ldG + Pg] = tp.zs[o0 + r];
+        for (int r = threadIdx.x; r < n; r += CFT) Gr[(long long)r * wp.ldG + Pg] = tp.zs[o0 + r];
     }
 }
 
@@ -990,14 +991,15 @@ k_wide_mtile(TreeParams tp, WideParams wp, long long g_first, double* out, long 
                                     : nullptr;
                 // all loads first (Fa / Fna / P may alias as far as the compiler knows: interleaved
                 // load-store pairs would serialise on the L2 latency)
-                double v[16];
+                constexpr int NU = 4096 / NT;   // nrow * rh <= 64 * 64
+                double v[NU];
 #pragma unroll
-                for (int u = 0; u < 16; u++) {
+                for (int u = 0; u < NU; u++) {
                     const int e = threadIdx.x + u * NT;
                     v[u] = (e < nrow * rh) ? __ldcg(Fa + e) : 0.0;
                 }
 #pragma unroll
-                for (int u = 0; u < 16; u++) {
+                for (int u = 0; u < NU; u++) {
                     const int e = threadIdx.x + u * NT;
                     if (e < nrow * rh) {
                         Fna[e] = -v[u];
@@ -1131,6 +1133,7 @@ k_wide_mtile(TreeParams tp, WideParams wp, long long g_first, double* out, long 
 
 // ------------------------------------------------------------------------ launchers
 int smem_bytes() { return SMEM_DBL * (int)sizeof(double); }
+int resident_ctas_per_sm();
 
 void phase_cycles(unsigned long long* out32, bool reset) {
     cudaMemcpyFromSymbol(out32, g_phase_cycles, sizeof(unsigned long long) * 32);
@@ -1190,10 +1193,10 @@ cudaError_t launch_prior(const TreeParams& tp, int m, long long t_first, long lo
             int per = 1, dev = 0, nsm = 148;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_prior_covfill, NT, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_prior_covfill, CFT, 0);
             cf_grid = (per > 0 ? per : 1) * nsm;
         }
-        k_prior_covfill<<<(int)std::min<long long>(cf_grid, t_count), NT, 0, st>>>(tp, m, t_first, t_count);
+        k_prior_covfill<<<(int)std::min<long long>(cf_grid, t_count), CFT, 0, st>>>(tp, m, t_first, t_count);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
@@ -1264,10 +1267,10 @@ cudaError_t launch_wide(int phase, const TreeParams& tp, const WideParams& wp, i
                 int per = 1, dev = 0, nsm = 148;
                 cudaGetDevice(&dev);
                 cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_wide_covfill, NT, 0);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_wide_covfill, CFT, 0);
                 cf_grid = (per > 0 ? per : 1) * nsm;
             }
-            k_wide_covfill<<<(int)std::min<long long>(cf_grid, ntask), NT, 0, st>>>(tp, wp, tasks, ntask);
+            k_wide_covfill<<<(int)std::min<long long>(cf_grid, ntask), CFT, 0, st>>>(tp, wp, tasks, ntask);
             break;
         }
         default: return cudaErrorInvalidValue;
@@ -1301,5 +1304,15 @@ cudaError_t launch_predict(const TreeParams& tp, const PredParams& pp, int grid,
     if (grid < 1) return cudaSuccess;
     k_predict<<<grid, NT, smem_bytes(), st>>>(tp, pp, ws, L, counter);
     return cudaGetLastError();
+}
+}  // namespace mra
+
+namespace mra {
+// resident CTAs per SM of the engine kernels (occupancy of k_bottom at the engine's smem size)
+int resident_ctas_per_sm() {
+    int per = 1;
+    cudaFuncSetAttribute(k_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_bottom, NT, smem_bytes());
+    return per > 0 ? per : 1;
 }
 }  // namespace mra
