@@ -1,6 +1,6 @@
 // mra_device.cuh -- CTA-level fp64 building blocks for the MRA hot path on sm_100a.
 //
-// Everything here is executed by one CTA of NT = 128 threads on matrices that live in
+// Everything here is executed by one CTA of NT = 256 threads on matrices that live in
 // global memory (L2-resident per-CTA workspaces) and are staged through shared memory:
 //   cta_gemm      C = init + alpha * sum_seg opA(seg) opB(seg)^T, 64x64 output tiles,
 //                 fp64 tensor-core MMA (mma.sync.m8n8k4.f64 -> DMMA), operands either
@@ -19,10 +19,11 @@
 namespace mra {
 
 #ifndef MRA_NT
-#define MRA_NT 128
+#define MRA_NT 256
 #endif
-constexpr int NT = MRA_NT;      // threads per CTA: 4 warps, each a 32 x 32 sub-tile of the 64 x 64 output
-                                // tile (16 DMMAs per 8 fragment loads), 3 CTAs per SM
+constexpr int NT = MRA_NT;      // threads per CTA: 8 warps of 16 x 32 sub-tiles, 2 CTAs per SM (default);
+                                // -DMRA_NT=128 -DMRA_MINB=3 -DMRA_NSTAGE=2: 4 warps of 32 x 32, 3 CTAs per SM
+                                // (faster GEMM main loop, slower latency-bound phases: DESIGN.md §5)
 constexpr int TM = 64;          // output tile rows
 constexpr int TN = 64;          // output tile cols
 constexpr int NWARP = NT / 32;
@@ -137,7 +138,7 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 
 // ------------------------------------------------------------- async tile staging
 #ifndef MRA_NSTAGE
-#define MRA_NSTAGE 2
+#define MRA_NSTAGE 3
 #endif
 constexpr int NSTAGE = MRA_NSTAGE;         // cp.async pipeline depth
 constexpr int STAGE_DBL = 2 * TILE_DBL;    // A tile + B tile

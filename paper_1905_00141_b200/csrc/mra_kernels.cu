@@ -24,7 +24,7 @@
 #include "mra_internal.h"
 
 #ifndef MRA_MINB
-#define MRA_MINB 3   // resident CTAs per SM the register allocation is sized for (128-thread CTAs)
+#define MRA_MINB 2   // resident CTAs per SM the register allocation is sized for (256-thread CTAs)
 #endif
 
 namespace mra {
@@ -328,13 +328,14 @@ k_merge(TreeParams tp, int m, long long t_first, long long t_count, const double
         if (threadIdx.x == 0) *f.bad = 0;
         const long long t = t_first + it;
         const double* C0 = child_out + (t * J - child_first) * qc2;
-        for (int i = 0; i < qc; i++)   // lower triangle, row by row (coalesced, no index division)
-            for (int j = threadIdx.x; j <= i; j += NT) {
-                const long long e = (long long)i * qc + j;
+        for (long long e = threadIdx.x; e < qc2; e += NT) {
+            const int i = (int)(e / qc), j = (int)(e - (long long)i * qc);
+            if (j <= i) {
                 double s = 0.0;
                 for (int c = 0; c < J; c++) s += C0[c * qc2 + e];
                 A[(long long)i * ldA + j] = s;
             }
+        }
         __syncthreads();
         double* O = out + (t - out_first) * (long long)q * q;
         const double ldm = merge_core(A, rh, ldA, O, q, F, Li, tp.err, m, t, cp, smem);
