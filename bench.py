@@ -281,10 +281,12 @@ def run_gpu(args, rank, world, local_rank):
     stream = torch.cuda.current_stream()
     t0 = time.time()
     w = synth.make(args.config, n=args.n, device=dev)
+    if args.M:
+        w.M = args.M
     log(f"[rank {rank}] data {w.name} n={w.n} in {time.time() - t0:.1f}s")
     t0 = time.time()
     plan = mra.mra_plan_create(w.x, w.y, w.M, w.J, w.r, device=local_rank, stream=stream, rank=rank,
-                               world=world)
+                               world=world, stream_prior=args.stream_prior)
     torch.cuda.synchronize()
     plan_s = time.time() - t0
     log(f"[rank {rank}] plan in {plan_s:.1f}s: n_retained={plan.n_retained} r_hat={plan.r_hat}")
@@ -445,6 +447,7 @@ def run_gpu(args, rank, world, local_rank):
             "kernel_ms": {k: round(kms[k], 3) for k in mra.KERNEL_CLASSES},
             "kernel_launches": {k: int(kcnt[k]) for k in mra.KERNEL_CLASSES},
             "roofline": roof, "cpu_baseline": cpu, "clocks": clocks}
+    line["plan_memory"] = mra.mra_plan_memory(plan)   # streamed prior rows (NEXT-4), chunking, device bytes
     line["plan_seconds"] = round(plan_s, 3)   # S0 (device build, not in the timed region)
     if pred:
         line["predict"] = pred
@@ -459,6 +462,9 @@ def main():
     ap.add_argument("--impl", default="mra", choices=["mra", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=list(synth.SPECS))
     ap.add_argument("--n", type=int, default=None, help="override the config's n (same recipe)")
+    ap.add_argument("--M", type=int, default=None, help="override the config's M (with --n: same leaf sizes)")
+    ap.add_argument("--stream-prior", type=int, default=0, help="plan option stream_prior (NEXT-4): 0 auto, "
+                    "1 always, -1 never")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle CPU work")
     ap.add_argument("--ref-budget", type=float, default=10.0, help="seconds of oracle work per reference step")

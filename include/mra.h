@@ -71,6 +71,14 @@ typedef struct {
     int host_plan;    /* 0 = build the partition on the device (bounding box, leaf keys, stable radix
                          sort by leaf: SURVEY.md NEXT-2; default), 1 = on the host (OpenMP). Both give
                          the identical plan; host-only plans (device -2) always build on the host  */
+    int stream_prior; /* prior chain rows of the levels >= the chunk level:
+                         0 = auto (streamed when the resident rows would take more than half the
+                         budget), 1 = always streamed: computed per chunk of subtrees right before
+                         that chunk's posterior pass, so device memory no longer grows with the
+                         number of regions (no extra arithmetic: every region's rows are still
+                         computed once); -1 = always resident. A streaming plan evaluates log L
+                         (mra_loglik*, mra_optimize, sharded log L) but keeps no posterior state:
+                         posterior requests and mra_predict return MRA_E_CONFIG.                */
 } mra_opts;
 
 /* Posterior state requested from an evaluation; any pointer may be NULL. */
@@ -181,6 +189,12 @@ mra_status mra_posterior_shard(mra_plan* plan, const double* d_mutop, double* d_
 mra_status mra_plan_info(const mra_plan* plan, uint64_t* n_retained, int* r_hat,
                          uint64_t* n_regions, uint64_t* n_leaves, uint64_t* n_empty_leaves,
                          uint64_t* max_leaf);
+
+/* Device-memory layout of a plan: whether it streams its prior rows (opts.stream_prior), the
+ * chunk level c and the number of level-c regions per chunk of the posterior pass, and the
+ * device bytes the plan holds. Any pointer may be NULL. */
+mra_status mra_plan_memory(const mra_plan* plan, int* streams_prior, int* chunk_level,
+                           uint64_t* chunk_regions, uint64_t* device_bytes);
 
 /* Copies of the plan's host-side layout: perm[n_retained] (sorted position -> original index),
  * leaf_off[n_leaves + 1] (CSR offsets of each leaf in sorted order), knots x/y

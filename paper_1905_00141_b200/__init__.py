@@ -44,7 +44,7 @@ class _Opts(ctypes.Structure):
     _fields_ = [("offset", ctypes.c_double), ("xscale", ctypes.c_double), ("yscale", ctypes.c_double),
                 ("device", ctypes.c_int), ("stream", ctypes.c_void_p), ("rank", ctypes.c_int),
                 ("world", ctypes.c_int), ("shard_level", ctypes.c_int), ("mem_budget_gb", ctypes.c_double),
-                ("wide", ctypes.c_int), ("host_plan", ctypes.c_int)]
+                ("wide", ctypes.c_int), ("host_plan", ctypes.c_int), ("stream_prior", ctypes.c_int)]
 
 
 class _Post(ctypes.Structure):
@@ -55,7 +55,7 @@ class _Post(ctypes.Structure):
 _lib = None
 EXPORTS = ["mra_plan_create", "mra_loglik", "mra_loglik_dev", "mra_loglik_batch_dev", "mra_predict", "mra_optimize", "mra_shard_size",
            "mra_loglik_shard", "mra_loglik_finish", "mra_mutop_size", "mra_loglik_shard_post",
-           "mra_loglik_finish_post", "mra_posterior_shard", "mra_plan_info", "mra_plan_layout", "mra_plan_shards",
+           "mra_loglik_finish_post", "mra_posterior_shard", "mra_plan_info", "mra_plan_layout", "mra_plan_shards", "mra_plan_memory",
            "mra_profile", "mra_kernel_times", "mra_last_launches", "mra_plan_destroy", "mra_last_error"]
 
 
@@ -101,6 +101,9 @@ def load_library(path: str = LIB_PATH):
     lib.mra_plan_layout.argtypes = [P, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64), D, D]
     lib.mra_plan_shards.restype = ctypes.c_int
     lib.mra_plan_shards.argtypes = [P, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int64),
+                                    ctypes.POINTER(U64)]
+    lib.mra_plan_memory.restype = ctypes.c_int
+    lib.mra_plan_memory.argtypes = [P, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int), ctypes.POINTER(U64),
                                     ctypes.POINTER(U64)]
     lib.mra_profile.restype = ctypes.c_int
     lib.mra_profile.argtypes = [P, ctypes.c_int]
@@ -169,14 +172,15 @@ class PlanHandle:
 
 
 def mra_plan_create(x, y, M, J, r, offset=0.0, xscale=0.0, yscale=0.0, device=-1, stream=None, rank=0,
-                    world=1, shard_level=0, mem_budget_gb=0.0, wide=0, host_plan=0) -> PlanHandle:
+                    world=1, shard_level=0, mem_budget_gb=0.0, wide=0, host_plan=0,
+                    stream_prior=0) -> PlanHandle:
     lib = load_library()
     x = np.ascontiguousarray(x, dtype=np.float64)
     y = np.ascontiguousarray(y, dtype=np.float64)
     if x.shape != y.shape or x.ndim != 1:
         raise ValueError("x and y must be 1-D arrays of equal length")
     opts = _Opts(float(offset), float(xscale), float(yscale), int(device), _stream_ptr(stream), int(rank),
-                 int(world), int(shard_level), float(mem_budget_gb), int(wide), int(host_plan))
+                 int(world), int(shard_level), float(mem_budget_gb), int(wide), int(host_plan), int(stream_prior))
     out = ctypes.c_void_p()
     _check(lib.mra_plan_create(_dptr(x), _dptr(y), x.shape[0], int(M), int(J), int(r), ctypes.byref(opts),
                                ctypes.byref(out)))
@@ -317,6 +321,14 @@ def mra_plan_shards(plan: PlanHandle) -> dict:
     _check(_lib.mra_plan_shards(plan.ptr, ctypes.byref(lvl), own.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
                                 ctypes.byref(n)))
     return dict(shard_level=lvl.value, own=own[: n.value])
+
+
+def mra_plan_memory(plan: PlanHandle) -> dict:
+    """Device-memory layout: streamed prior (NEXT-4), chunk level / size, bytes held."""
+    sp, cl = ctypes.c_int(), ctypes.c_int()
+    kc, nb = ctypes.c_uint64(), ctypes.c_uint64()
+    _check(_lib.mra_plan_memory(plan.ptr, ctypes.byref(sp), ctypes.byref(cl), ctypes.byref(kc), ctypes.byref(nb)))
+    return dict(streams_prior=bool(sp.value), chunk_level=cl.value, chunk_regions=kc.value, device_bytes=nb.value)
 
 
 def mra_profile(plan: PlanHandle, enable: bool = True):

@@ -48,6 +48,8 @@ struct mra_plan {
     double* kxy_d = nullptr;
     double* prior = nullptr;
     long long prior_base[MAXM + 1] = {0};
+    bool stream = false;             // prior rows of levels >= c live per chunk (NEXT-4)
+    size_t dev_bytes = 0;            // device memory held by the plan
     double *dreg = nullptr, *ureg = nullptr, *loglik_d = nullptr;
     int* err = nullptr;
     unsigned long long* counters = nullptr;
@@ -156,6 +158,7 @@ static mra_status dalloc(mra_plan* p, void** ptr, size_t bytes, const char* what
         return fail(e == cudaErrorMemoryAllocation ? MRA_E_OOM : MRA_E_CUDA, buf);
     }
     p->allocs.push_back(*ptr);
+    p->dev_bytes += bytes;
     return MRA_OK;
 }
 
@@ -399,16 +402,13 @@ static long long round_up(long long v, long long a) { return (v + a - 1) / a * a
 static mra_status size_wide(mra_plan* P, double budget, bool explicit_budget);
 static std::vector<std::pair<long long, long long>> my_runs(const mra_plan* P);
 
-static mra_status size_device(mra_plan* P, double budget_gb) {
+static mra_status size_device(mra_plan* P, double budget_gb, int stream_opt) {
     const int M = P->M, J = P->J, rh = P->rh;
-    // prior chain rows
+    // prior chain rows: rh x m rh per level-m region
+    auto prior_level = [&](int m) { return ipow(J, m - 1) * (long long)m * rh * rh; };
     long long tot = 0;
-    for (int m = 1; m < M; m++) {
-        P->prior_base[m] = tot;
-        tot += ipow(J, m - 1) * (long long)m * rh * rh;
-    }
+    for (int m = 1; m < M; m++) tot += prior_level(m);
     mra_status s;
-    if ((s = dalloc(P, (void**)&P->prior, sizeof(double) * tot, "prior chain rows"))) return s;
     // workspace layout (bottom kernel; also covers merge / prior / smooth)
     const int mg = M - 1, Pg = mg * rh, ncol = Pg + 1;
     WsLayout L{};
@@ -440,7 +440,15 @@ static mra_status size_device(mra_plan* P, double budget_gb) {
     size_t freeb = 0, totalb = 0;
     cudaMemGetInfo(&freeb, &totalb);
     double budget = budget_gb > 0 ? budget_gb * 1e9 : 0.85 * (double)freeb;
-    budget -= (double)tot * 8.0;
+    // resident prior rows, unless they would crowd out the posterior pass (or the caller asks to
+    // stream them): then only the levels above the chunk level stay resident (NEXT-4)
+    P->stream = M >= 2 && (stream_opt > 0 || (stream_opt == 0 && (double)tot * 8.0 > 0.5 * budget));
+    if (!P->stream) {
+        long long o2 = 0;
+        for (int m = 1; m < M; m++) { P->prior_base[m] = o2; o2 += prior_level(m); }
+        if ((s = dalloc(P, (void**)&P->prior, sizeof(double) * tot, "prior chain rows"))) return s;
+        budget -= (double)tot * 8.0;
+    }
     // slots: the resident CTAs of the persistent grid, fewer if the per-slot workspace is huge
     long long slots = (long long)resident_ctas_per_sm() * P->nsm;
     const double ws_cap = std::max(0.25 * budget, (double)L.stride * 8.0);
@@ -449,7 +457,8 @@ static mra_status size_device(mra_plan* P, double budget_gb) {
     if ((s = dalloc(P, (void**)&P->ws, sizeof(double) * L.stride * slots, "workspace"))) return s;
     budget -= (double)L.stride * slots * 8.0;
     // choose chunk level c and chunk size Kc so the posterior outputs fit
-    const double out_budget = std::max(0.5 * budget, 1e8);
+    // (an explicit budget is honoured down to tiny chunks: the tests use it to force many chunks)
+    const double out_budget = std::max(0.5 * budget, budget_gb > 0 ? 1e5 : 1e8);
     auto full_bytes = [&](int c) {
         double b = 0;
         for (int m = 1; m <= c && m < M; m++) b += (double)ipow(J, m - 1) * q_of(m, rh) * q_of(m, rh) * 8.0;
@@ -458,6 +467,10 @@ static mra_status size_device(mra_plan* P, double budget_gb) {
     auto chunk_bytes = [&](int c, long long Kc) {
         double b = 0;
         for (int m = c + 1; m < M; m++) b += (double)Kc * ipow(J, m - c) * q_of(m, rh) * q_of(m, rh) * 8.0;
+        if (P->stream) {   // prior rows: levels < c for every region, levels >= c for one chunk
+            for (int m = 1; m < c; m++) b += (double)prior_level(m) * 8.0;
+            for (int m = c; m < M; m++) b += (double)Kc * ipow(J, m - c) * m * rh * rh * 8.0;
+        }
         return b;
     };
     int c = 1;
@@ -472,6 +485,15 @@ static mra_status size_device(mra_plan* P, double budget_gb) {
     while (Kc > 1 && full_bytes(c) + chunk_bytes(c, Kc) > out_budget) Kc = (Kc + 1) / 2;
     P->c = c;
     P->Kc = Kc;
+    if (P->stream) {
+        long long o2 = 0;
+        for (int m = 1; m < M; m++) {
+            P->prior_base[m] = o2;
+            o2 += m < c ? prior_level(m) : Kc * ipow(J, m - c) * (long long)m * rh * rh;
+        }
+        if ((s = dalloc(P, (void**)&P->prior, sizeof(double) * o2, "prior chain rows (resident levels + one chunk)")))
+            return s;
+    }
     for (int m = 1; m <= c && m < M; m++)
         if ((s = dalloc(P, (void**)&P->out_full[m], sizeof(double) * ipow(J, m - 1) * q_of(m, rh) * q_of(m, rh),
                         "level output")))
@@ -785,7 +807,7 @@ extern "C" mra_status mra_plan_create(const double* x, const double* y, uint64_t
         TRY(cp(P->leaf_off_d, P->leaf_off.data(), 8 * (P->nleaf + 1)));
         if (P->nint) TRY(cp(P->kxy_d, kxy.data(), 16 * P->nint * P->rh));
     }
-    TRY(size_device(P, o.mem_budget_gb));
+    TRY(size_device(P, o.mem_budget_gb, o.stream_prior));
 #undef TRY
     *out = P;
     return MRA_OK;
@@ -847,6 +869,16 @@ extern "C" void mra_debug_phase_cycles(uint64_t* out32, int reset) {
     unsigned long long v[32];
     phase_cycles(v, reset != 0);
     for (int i = 0; i < 32; i++) out32[i] = v[i];
+}
+
+extern "C" mra_status mra_plan_memory(const mra_plan* P, int* streams_prior, int* chunk_level,
+                                      uint64_t* chunk_regions, uint64_t* device_bytes) {
+    if (!P) return fail(MRA_E_ARG, "plan is NULL");
+    if (streams_prior) *streams_prior = P->stream ? 1 : 0;
+    if (chunk_level) *chunk_level = P->c;
+    if (chunk_regions) *chunk_regions = (uint64_t)P->Kc;
+    if (device_bytes) *device_bytes = (uint64_t)P->dev_bytes;
+    return MRA_OK;
 }
 
 extern "C" mra_status mra_plan_shards(const mra_plan* P, int* shard_level, int64_t* own, uint64_t* n_own) {
@@ -965,12 +997,14 @@ static mra_status eval_wide(mra_plan* P, const TreeParams& tp, long long gf, lon
 }
 
 // prior + posterior below (and at) level c for this rank's subtrees
-static mra_status eval_lower(mra_plan* P, const TreeParams& tp) {
+static mra_status eval_lower(mra_plan* P, const TreeParams& tp0) {
     const int M = P->M, J = P->J, rh = P->rh, c = P->c;
+    const TreeParams& tp = tp0;
     cudaStream_t st = P->st;
     auto runs = my_runs(P);
-    // prior: levels < c for every region, levels >= c for own subtrees
+    // prior: levels < c for every region, levels >= c for own subtrees (streaming plans: per chunk, below)
     for (int m = 1; m < M; m++) {
+        if (m >= c && P->stream) break;
         if (m < c) {
             TreeParams t2 = tp;
             LCHK_K(KIND_PRIOR, launch_prior(t2, m, 0, ipow(J, m - 1), P->grid, P->ws, P->ws_stride, take_counter(P), st));
@@ -990,6 +1024,16 @@ static mra_status eval_lower(mra_plan* P, const TreeParams& tp) {
             if (M == 1) {
                 LCHK_K(KIND_BOTTOM, launch_bottom(tp, 0, 1, nullptr, 0, 0, P->grid, P->ws, P->L, take_counter(P), st));
                 continue;
+            }
+            TreeParams tp = tp0;
+            if (P->stream) {
+                // this chunk's prior rows, levels c..M-1, top-down (their ancestors above c are resident)
+                for (int m = c; m < M; m++) {
+                    long long f, cnt;
+                    range_at(P, m, a, b, &f, &cnt);
+                    tp.prior_first[m] = f;
+                    LCHK_K(KIND_PRIOR, launch_prior(tp, m, f, cnt, P->grid, P->ws, P->ws_stride, take_counter(P), st));
+                }
             }
             long long gf, gc;
             range_at(P, mg, a, b, &gf, &gc);
@@ -1063,6 +1107,10 @@ static mra_status begin_eval(mra_plan* P, const double* d_y, const mra_theta* th
 
 static mra_status ensure_post(mra_plan* P) {
     if (P->post) return MRA_OK;
+    if (P->stream)
+        return fail(MRA_E_CONFIG, "this plan streams its prior rows per chunk (stream_prior, NEXT-4) and keeps no "
+                                  "posterior state; build it with stream_prior = -1 for posterior means, smoothing "
+                                  "or prediction");
     const int M = P->M, J = P->J, rh = P->rh;
     long long tot = 0;
     for (int m = 1; m < M; m++) {

@@ -441,28 +441,35 @@ __device__ __noinline__ double chol_inv_small(double* a, double* x, int n, doubl
                 r[k] = (i < nb && k < nb && k <= i) ? d[i * LDB + k] : (i == k ? 1.0 : 0.0);
             double dv[16];
             bool ok = true;
+            // the lane's own running diagonal a_ii - sum_{j<i} l_ij^2, kept apart from r[] so that
+            // the serial pivot chain is shuffle -> rsqrt -> scale -> fma per column (no smem trip);
+            // the off-diagonal columns travel through a double-buffered smem column one step ahead.
+            double dg = 1.0;
+#pragma unroll
+            for (int k = 0; k < 16; k++)
+                if (i == k) dg = r[k];
 #pragma unroll
             for (int j = 0; j < 16; j++) {
-                // lane j publishes its (updated) pivot; every lane reads it back
-                if (lane == j) tmp[j] = r[j];
-                __syncwarp();
-                const double piv = tmp[j];
+                const double piv = __shfl_sync(0xffffffffu, dg, j);
                 ok = ok && (piv > 0.0);
                 // one rsqrt on the serial pivot chain: 1/l_jj, then l_jj = piv / l_jj
                 const double pv = piv > 0.0 ? piv : 1.0;
                 const double il = rsqrt(pv);
                 const double ljj = pv * il;
                 dv[j] = il;
-                r[j] = (i == j) ? ljj : ((i > j) ? r[j] * il : r[j]);
-                if (lane < 16) tmp[16 + i] = r[j];   // column j of L (l_ij for i > j)
+                const double lij = r[j] * il;
+                r[j] = (i == j) ? ljj : ((i > j) ? lij : r[j]);
+                if (i > j) dg -= lij * lij;
+                double* col = tmp + 16 + 16 * (j & 1);
+                if (lane < 16) col[i] = r[j];   // column j of L (l_ij for i > j)
                 __syncwarp();
 #pragma unroll
                 for (int k = j + 1; k < 16; k++) {
-                    const double lk = tmp[16 + k];
+                    const double lk = col[k];
                     if (i >= k) r[k] -= r[j] * lk;
                 }
-                __syncwarp();
             }
+            __syncwarp();
             if (!ok && lane == 0) *bad = 1;
             // publish L_bb rows to smem (lower part) for the inverse and the panel
             if (lane < nb) {

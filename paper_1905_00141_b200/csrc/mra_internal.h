@@ -23,7 +23,9 @@ struct TreeParams {
     const long long* leaf_off;  // [n_leaves + 1]
     const double* kxy;          // [2 * n_interior * rh] knots, level-major regions, interleaved (x, y)
     double* prior;              // chain rows R_R = [Linv_R | -U^{m-1}_R .. -U^1_R], rh x m*rh each
-    long long prior_base[MAXM + 1];  // offset (doubles) of level m's first region
+    long long prior_base[MAXM + 1];  // offset (doubles) of level m's first stored region
+    long long prior_first[MAXM + 1]; // index (within level m) of that region: 0 when the level is resident,
+                                     // the chunk's first region when the plan streams the prior (NEXT-4)
     double* dreg;               // [n_regions] per-region log-det term
     double* ureg;               // [n_regions] per-region quadratic term
     int* err;                   // [4]: flag, level, index lo, index hi

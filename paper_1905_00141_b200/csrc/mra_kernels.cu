@@ -71,7 +71,7 @@ __device__ __forceinline__ long long next_item(unsigned long long* counter, doub
 }
 
 __device__ __forceinline__ const double* chain_row(const TreeParams& tp, int k, long long ak) {
-    return tp.prior + tp.prior_base[k] + ak * (long long)k * tp.rh * tp.rh;
+    return tp.prior + tp.prior_base[k] + (ak - tp.prior_first[k]) * (long long)k * tp.rh * tp.rh;
 }
 
 // V chain of a point set P (n points inside level-m region t): for k = 1..m
@@ -138,7 +138,7 @@ k_prior_covfill(TreeParams tp, int m, long long t_first, long long nitems) {
             knots_s[c] = ldpt(tp.kxy + 2 * akid * rh, c - b * rh);
         }
         __syncthreads();
-        double* R = tp.prior + tp.prior_base[m] + t * ldR * rh;
+        double* R = tp.prior + tp.prior_base[m] + (t - tp.prior_first[m]) * ldR * rh;
         int i = 0, c = threadIdx.x;
         while (c >= W) { c -= W; i++; }
         const int di = CFT / W, dc = CFT - di * W;
@@ -167,7 +167,7 @@ k_prior(TreeParams tp, int m, long long t_first, long long nitems, double* ws, l
         if (it >= nitems) break;
         if (threadIdx.x == 0) *f.bad = 0;
         const long long t = t_first + it;
-        double* R = tp.prior + tp.prior_base[m] + t * ldR * rh;
+        double* R = tp.prior + tp.prior_base[m] + (t - tp.prior_first[m]) * ldR * rh;
         // V^k_R for k < m over R's blocks m-k, which hold C(Q_R, Q_{a_k}) (k_prior_covfill); they become -U
         // after the inverse is known
         point_chain_pre(tp, m - 1, t >> tp.lj, rh, R + rh, ldR, cp, smem);

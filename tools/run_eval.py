@@ -20,19 +20,28 @@ ap.add_argument("--M", type=int, default=None)
 ap.add_argument("--lib", default=None)
 ap.add_argument("--wide", type=int, default=0)
 ap.add_argument("--budget", type=float, default=0.0)
+ap.add_argument("--prof", action="store_true", help="per-class device times of the last evaluation")
+ap.add_argument("--stream", type=int, default=0, help="stream_prior: 0 auto, 1 always, -1 never (NEXT-4)")
 a = ap.parse_args()
 if a.lib:
     mra.load_library(a.lib)
 w = synth.make(a.config, n=a.n, device="cuda")
 M = a.M or w.M
 plan = mra.mra_plan_create(w.x, w.y, M, w.J, w.r, stream=torch.cuda.current_stream(), wide=a.wide,
-                           mem_budget_gb=a.budget)
+                           mem_budget_gb=a.budget, stream_prior=a.stream)
+torch.cuda.synchronize()
+print(f"plan: n={w.n} M={M} retained={plan.n_retained} memory={mra.mra_plan_memory(plan)} "
+      f"torch max allocated {torch.cuda.max_memory_allocated() / 1e9:.1f} GB")
 zd = torch.from_numpy(w.z).cuda()
 for i in range(a.evals):
+    if a.prof and i == a.evals - 1:
+        mra.mra_profile(plan, True)
     t = time.time()
     ll = mra.mra_loglik_dev(plan, zd, w.thetas[0])["loglik"]
     torch.cuda.synchronize()
     print(f"eval {i}: loglik={ll:.10f} {1e3 * (time.time() - t):.1f} ms launches={mra.mra_last_launches(plan)}")
+if a.prof:
+    print("kernel classes (ms, launches):", {k: (round(v[0], 1), v[1]) for k, v in mra.mra_kernel_times(plan).items() if v[1]})
 import ctypes  # noqa: E402
 cyc = (ctypes.c_uint64 * 32)()
 mra._lib.mra_debug_phase_cycles(cyc, 1)
