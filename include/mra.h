@@ -123,6 +123,12 @@ mra_status mra_loglik_dev(mra_plan* plan, const double* d_y, const mra_theta* th
 mra_status mra_loglik_batch_dev(mra_plan* plan, const double* d_y, const mra_theta* theta,
                                 int n_theta, double* loglik);
 
+/* Same sweep with y a HOST array of n values in the original input order (copied to the device once,
+ * SURVEY.md §8(b) mra_loglik_batch). NaN/Inf in y -> MRA_E_ARG; the first failing theta's status is
+ * returned and loglik[] holds the values evaluated before it. */
+mra_status mra_loglik_batch(mra_plan* plan, const double* y, const mra_theta* theta, int n_theta,
+                            double* loglik);
+
 /* Prediction (north_star's mra_predict; the paper's "prediction" calculation mode, PAPER.md:228,
  * 494, 537): posterior mean and variance of the noise-free process X (no nugget)
  * at nq query locations, under the MRA prior, given the observations and theta of the LAST

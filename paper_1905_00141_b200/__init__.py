@@ -53,7 +53,7 @@ class _Post(ctypes.Structure):
 
 
 _lib = None
-EXPORTS = ["mra_plan_create", "mra_loglik", "mra_loglik_dev", "mra_loglik_batch_dev", "mra_predict", "mra_optimize", "mra_shard_size",
+EXPORTS = ["mra_plan_create", "mra_loglik", "mra_loglik_dev", "mra_loglik_batch_dev", "mra_loglik_batch", "mra_predict", "mra_optimize", "mra_shard_size",
            "mra_loglik_shard", "mra_loglik_finish", "mra_mutop_size", "mra_loglik_shard_post",
            "mra_loglik_finish_post", "mra_posterior_shard", "mra_plan_info", "mra_plan_layout", "mra_plan_shards", "mra_plan_memory",
            "mra_profile", "mra_kernel_times", "mra_last_launches", "mra_plan_destroy", "mra_last_error"]
@@ -80,6 +80,8 @@ def load_library(path: str = LIB_PATH):
     lib.mra_loglik_dev.argtypes = [P, P, ctypes.POINTER(_Theta), D, ctypes.POINTER(_Post)]
     lib.mra_loglik_batch_dev.restype = ctypes.c_int
     lib.mra_loglik_batch_dev.argtypes = [P, P, ctypes.POINTER(_Theta), ctypes.c_int, D]
+    lib.mra_loglik_batch.restype = ctypes.c_int
+    lib.mra_loglik_batch.argtypes = [P, D, ctypes.POINTER(_Theta), ctypes.c_int, D]
     lib.mra_shard_size.restype = U64
     lib.mra_shard_size.argtypes = [P]
     lib.mra_loglik_shard.restype = ctypes.c_int
@@ -247,6 +249,17 @@ def mra_loglik_batch_dev(plan: PlanHandle, y_dev, thetas):
     arr = (_Theta * len(thetas))(*[_theta(t) for t in thetas])
     out = np.empty(len(thetas))
     _check(_lib.mra_loglik_batch_dev(plan.ptr, ctypes.c_void_p(y_dev.data_ptr()), arr, len(thetas), _dptr(out)))
+    return out
+
+
+def mra_loglik_batch(plan: PlanHandle, y, thetas):
+    """Likelihood sweep with y a host array (copied to the device once)."""
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    if y.shape != (plan.n,):
+        raise ValueError("y must have one value per input location")
+    arr = (_Theta * len(thetas))(*[_theta(t) for t in thetas])
+    out = np.empty(len(thetas))
+    _check(_lib.mra_loglik_batch(plan.ptr, _dptr(y), arr, len(thetas), _dptr(out)))
     return out
 
 

@@ -1331,6 +1331,17 @@ extern "C" mra_status mra_loglik_batch_dev(mra_plan* P, const double* d_y, const
     return MRA_OK;
 }
 
+extern "C" mra_status mra_loglik_batch(mra_plan* P, const double* y, const mra_theta* th, int n_theta,
+                                       double* loglik) {
+    if (!P || !y || !th || !loglik || n_theta < 0) return fail(MRA_E_ARG, "bad arguments");
+    if (P->device < 0) return fail(MRA_E_CUDA, "host-only plan (device -2) cannot evaluate");
+    for (uint64_t i = 0; i < P->n_in; i++)
+        if (!std::isfinite(y[i])) return fail(MRA_E_ARG, "non-finite observation value");
+    if (cudaSetDevice(P->device) != cudaSuccess) return fail(MRA_E_CUDA, "cudaSetDevice failed");
+    CU(cudaMemcpyAsync(P->zin, y, 8 * P->n_in, cudaMemcpyHostToDevice, P->st));   // once for the sweep
+    return mra_loglik_batch_dev(P, P->zin, th, n_theta, loglik);
+}
+
 // ----------------------------------------------------------------------- optimization
 // The paper's "optimization" calculation mode: maximise log L over (sigma2, rho, tau2)
 // by derivative-free search, each step one full evaluation. Nelder-Mead on the log-parameters inside

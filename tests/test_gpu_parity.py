@@ -209,6 +209,7 @@ def test_batch_thetas(mra):
     for t, g in zip(th, got):
         ref = oracle.run(w.x, w.y, w.z, 7, w.J, w.r, t)["loglik"]
         assert abs(g - ref) <= 1e-9 * abs(ref)
+    np.testing.assert_array_equal(mra.mra_loglik_batch(p, w.z, th), got)   # host-y entry: same kernels
 
 
 def test_bad_theta_is_arg_error(mra):
