@@ -7,8 +7,8 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["mra_kernels.cu", "mra_plan.cu", "mra_api.cpp"]
-HEADERS = ["mra_device.cuh", "mra_internal.h"]
+SOURCES = ["mra_kernels.cu", "mra_kernels_gemm.cu", "mra_plan.cu", "mra_api.cpp"]
+HEADERS = ["mra_device.cuh", "mra_internal.h", "mra_kcommon.cuh"]
 OUT = os.path.join(HERE, "libmra_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

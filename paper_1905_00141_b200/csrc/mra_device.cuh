@@ -16,11 +16,23 @@
 #pragma once
 #include <cstdint>
 
-namespace mra {
-
 #ifndef MRA_NT
 #define MRA_NT 256
 #endif
+#ifndef MRA_TK
+#define MRA_TK 32
+#endif
+#ifndef MRA_NSTAGE
+#define MRA_NSTAGE 3
+#endif
+// every engine shape gets its own inline namespace, so translation units built with different shapes
+// (mra_kernels.cu, mra_kernels_gemm.cu) can be linked into one library
+#define MRA_ENG_NS_(a, b, c) eng_##a##_##b##_##c
+#define MRA_ENG_NS_X(a, b, c) MRA_ENG_NS_(a, b, c)
+#define MRA_ENG_NS MRA_ENG_NS_X(MRA_NT, MRA_TK, MRA_NSTAGE)
+
+namespace mra {
+inline namespace MRA_ENG_NS {
 constexpr int NT = MRA_NT;      // threads per CTA: 8 warps of 16 x 32 sub-tiles, 2 CTAs per SM (default);
                                 // -DMRA_NT=128 -DMRA_MINB=3 -DMRA_NSTAGE=2: 4 warps of 32 x 32, 3 CTAs per SM
                                 // (faster GEMM main loop, slower latency-bound phases: DESIGN.md §5)
@@ -605,14 +617,21 @@ __device__ __noinline__ double chol_inv_small(double* a, double* x, int n, doubl
     return ld;
 }
 
-// smem layout (doubles): [ main: GEMM tiles | factor blocks ] [ misc: MISC_DBL doubles ]
+// smem layout (doubles): [ misc: MISC_DBL doubles ] [ main: GEMM tiles | factor blocks ]
+//   kernels address the main area (`smem` = dyn_smem()); misc sits just below it, so a kernel that only
+//   runs GEMMs needs GEMM_SMEM_DBL, one that also factors needs SMEM_DBL
 //   factor view of main: blk[64*LDB] | inv[64*LDB] | diag[64]
 //   misc: red[0..15] (reductions) | bad flag (int) at misc+16 | work item at misc+18 | GemmDesc at misc+24
 constexpr int FAC_DBL = 2 * 64 * LDB + 64 + 768;
 constexpr int MAIN_DBL = (FAC_DBL > NSTAGE * STAGE_DBL) ? FAC_DBL : NSTAGE * STAGE_DBL;
 constexpr int SMEM_DBL = MAIN_DBL + MISC_DBL;
+constexpr int GEMM_SMEM_DBL = NSTAGE * STAGE_DBL + MISC_DBL;
+__device__ __forceinline__ double* dyn_smem() {
+    extern __shared__ double smem_raw[];
+    return smem_raw + MISC_DBL;
+}
 __device__ __forceinline__ GemmDesc* gemm_desc(double* smem) {
-    return reinterpret_cast<GemmDesc*>(smem + MAIN_DBL + 24);
+    return reinterpret_cast<GemmDesc*>(smem - MISC_DBL + 24);
 }
 static_assert(sizeof(GemmDesc) <= (MISC_DBL - 24) * sizeof(double), "GemmDesc must fit the misc smem");
 struct FacSmem {
@@ -623,7 +642,7 @@ struct FacSmem {
     double* red;
     int* bad;
 };
-__device__ __forceinline__ double* misc_smem(double* smem) { return smem + MAIN_DBL; }
+__device__ __forceinline__ double* misc_smem(double* smem) { return smem - MISC_DBL; }
 __device__ __forceinline__ FacSmem fac_smem(double* smem) {
     FacSmem f;
     f.blk = smem;
@@ -661,7 +680,7 @@ __device__ __forceinline__ void store_block_full(const double* x, double* A, lon
 // Blocked right-looking Cholesky of S (n x n, lower, ld) in place; Dinv receives the inverted
 // 64x64 diagonal blocks (block b at Dinv + b*4096, ld 64). Returns log|S| (all threads).
 // optional phase timing (build with -DMRA_PHASE_TIMING): CTA-cycles per phase of the bottom kernel
-__device__ unsigned long long g_phase_cycles[32];
+static __device__ unsigned long long g_phase_cycles[32];   // per translation unit (debug counters)
 #ifdef MRA_PHASE_TIMING
 #define CPHASE_MARK(var) long long var = clock64()
 #define CPHASE_ADD(idx, from) do { if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[idx], (unsigned long long)(clock64() - (from))); } while (0)
@@ -742,4 +761,5 @@ __device__ __forceinline__ double cta_sum(double v, double* red) {
     return s;
 }
 
+}  // inline namespace MRA_ENG_NS
 }  // namespace mra

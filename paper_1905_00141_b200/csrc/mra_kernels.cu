@@ -23,102 +23,9 @@
 #include "mra_device.cuh"
 #include "mra_internal.h"
 
-#ifndef MRA_MINB
-#define MRA_MINB 2   // resident CTAs per SM the register allocation is sized for (256-thread CTAs)
-#endif
+#include "mra_kcommon.cuh"
 
 namespace mra {
-
-#ifdef MRA_PHASE_TIMING
-#define PHASE_MARK(var) long long var = clock64()
-#define PHASE_ADD(idx, from)                                                                  \
-    do {                                                                                      \
-        if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[idx], (unsigned long long)(clock64() - (from))); \
-    } while (0)
-#else
-#define PHASE_MARK(var)
-#define PHASE_ADD(idx, from)
-#endif
-
-__device__ __forceinline__ long long lvl_first(int J, int m) {
-    long long p = 1;
-    for (int i = 1; i < m; i++) p *= J;
-    return (p - 1) / (J - 1);
-}
-
-__device__ __forceinline__ CovP to_covp(const CovParams& c) {
-    CovP p;
-    p.kind = c.kind; p.s2 = c.s2; p.rho = c.rho; p.xs = c.xs; p.ys = c.ys;
-    p.ir = (c.kind == 0 ? 1.0 : 1.7320508075688772935) / c.rho;
-    return p;
-}
-
-__device__ __forceinline__ void set_err(int* err, int level, long long idx) {
-    if (atomicCAS(err, 0, 1) == 0) {
-        err[1] = level;
-        *reinterpret_cast<long long*>(err + 2) = idx;
-    }
-}
-
-// persistent work queue: returns the next item index (uniform across the CTA)
-__device__ __forceinline__ long long next_item(unsigned long long* counter, double* smem) {
-    long long* slot = reinterpret_cast<long long*>(misc_smem(smem) + 18);
-    __syncthreads();
-    if (threadIdx.x == 0) *slot = (long long)atomicAdd(counter, 1ULL);
-    __syncthreads();
-    long long v = *slot;
-    return v;
-}
-
-__device__ __forceinline__ const double* chain_row(const TreeParams& tp, int k, long long ak) {
-    return tp.prior + tp.prior_base[k] + (ak - tp.prior_first[k]) * (long long)k * tp.rh * tp.rh;
-}
-
-// V chain of a point set P (n points inside level-m region t): for k = 1..m
-//   V^k(P) = [ C(P, Q_{a_k}) | V^{k-1}(P) .. V^1(P) ] R_{a_k}^T        (K = k * rh)
-// written into Gc at column block m-k (levels in descending order), ld ldg.
-__device__ void point_chain(const TreeParams& tp, int m, long long t, int n, const double* pts, double* Gc,
-                            long long ldg, const CovP& cp, double* smem) {
-    const int rh = tp.rh;
-    for (int k = 1; k <= m; k++) {
-        const long long ak = t >> (tp.lj * (m - k));
-        const long long akid = lvl_first(tp.J, k) + ak;
-        const long long ldk = (long long)k * rh;
-        const double* Rk = chain_row(tp, k, ak);
-        PHASE_MARK(pc0);
-        cta_gemm<COVK, MEMN, MEMN, MEMN>(n, rh, 0, op_cov(pts, tp.kxy + 2 * akid * rh),
-                                         op_mem(Rk, ldk), rh, op_mem(Gc + (long long)(m - k + 1) * rh, ldg),
-                                         op_mem(Rk + rh, ldk), (k - 1) * rh, ci_zero(), 1.0,
-                                         Gc + (long long)(m - k) * rh, ldg, cp, smem);
-        PHASE_ADD(26, pc0);
-#ifdef MRA_PHASE_TIMING
-        if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[27], (unsigned long long)k);   // sum of k (= K / rh)
-#endif
-    }
-}
-
-// V chain over covariance blocks already in place: Gc's column block m-k holds C(P, Q_{a_k}) on entry
-// (k_wide_covfill) and V^k on exit. Each step is one single-segment GEMM over the contiguous columns
-// [C_k | V^{k-1} .. V^1] that overwrites C_k (every output tile reads only its own rows).
-__device__ void point_chain_pre(const TreeParams& tp, int m, long long t, int n, double* Gc, long long ldg,
-                                const CovP& cp, double* smem) {
-    const int rh = tp.rh;
-    for (int k = 1; k <= m; k++) {
-        const long long ak = t >> (tp.lj * (m - k));
-        const long long ldk = (long long)k * rh;
-        const double* Rk = chain_row(tp, k, ak);
-        double* Ck = Gc + (long long)(m - k) * rh;
-        cta_gemm<MEMN, MEMN, MEMN, MEMN>(n, rh, 0, op_mem(Ck, ldg), op_mem(Rk, ldk), k * rh, op_mem(Ck, ldg),
-                                         op_mem(Ck, ldg), 0, ci_zero(), 1.0, Ck, ldg, cp, smem);
-    }
-}
-
-// --------------------------------------------------------------------------- prior
-// Covariance blocks of the prior chains of level-m regions, in place of the chain row R (ld m rh):
-// block 0 <- C(Q_R, Q_R) (k_prior turns it into W^m, then overwrites it with L^{-1}), block m-k <-
-// C(Q_R, Q_{a_k}) for k < m (turned into V^k, then -U^k). Own phase, like k_wide_covfill: no DMMA shares
-// the fp64 pipe with the sqrt / exp chains.
-constexpr int CFT = 256;   // threads of the covariance-generation kernels (independent of the engine's NT)
 
 __global__ void __launch_bounds__(CFT)
 k_prior_covfill(TreeParams tp, int m, long long t_first, long long nitems) {
@@ -156,7 +63,7 @@ k_prior_covfill(TreeParams tp, int m, long long t_first, long long nitems) {
 __global__ void __launch_bounds__(NT, MRA_MINB)
 k_prior(TreeParams tp, int m, long long t_first, long long nitems, double* ws, long long ws_stride,
         unsigned long long* counter) {
-    extern __shared__ double smem[];
+    double* smem = dyn_smem();
     const CovP cp = to_covp(tp.cp);
     const int rh = tp.rh;
     double* W = ws + (long long)blockIdx.x * ws_stride;
@@ -239,7 +146,7 @@ __device__ void group_tail(const TreeParams& tp, int m, long long t, const doubl
 __global__ void __launch_bounds__(NT, MRA_MINB)
 k_bottom(TreeParams tp, long long g_first, long long g_count, double* out, long long out_first, int q, double* ws,
          WsLayout L, unsigned long long* counter) {
-    extern __shared__ double smem[];
+    double* smem = dyn_smem();
     const CovP cp = to_covp(tp.cp);
     const int M = tp.M, J = tp.J, rh = tp.rh;
     const int m = M - 1;                 // group level; 0 when M == 1 (the root is the only leaf)
@@ -312,7 +219,7 @@ k_bottom(TreeParams tp, long long g_first, long long g_count, double* out, long 
 __global__ void __launch_bounds__(NT, MRA_MINB)
 k_merge(TreeParams tp, int m, long long t_first, long long t_count, const double* child_out, long long child_first,
         double* out, long long out_first, int q, double* ws, long long ws_stride, unsigned long long* counter) {
-    extern __shared__ double smem[];
+    double* smem = dyn_smem();
     const CovP cp = to_covp(tp.cp);
     const int J = tp.J, rh = tp.rh;
     const int qc = m * rh + 1;
@@ -408,7 +315,7 @@ __global__ void k_mu(TreeParams tp, int m, double* muhat, double* mu, long long 
 __global__ void __launch_bounds__(NT, MRA_MINB)
 k_smooth(TreeParams tp, const double* muhat, const long long* perm, double* smooth, double* ws, WsLayout L,
          unsigned long long* counter, long long l_first, long long l_count) {
-    extern __shared__ double smem[];
+    double* smem = dyn_smem();
     const CovP cp = to_covp(tp.cp);
     const int M = tp.M, rh = tp.rh, m = M - 1, Pg = m * rh;
     double* base = ws + (long long)blockIdx.x * L.stride;
@@ -496,7 +403,7 @@ k_smooth(TreeParams tp, const double* muhat, const long long* perm, double* smoo
 // (the chain's posterior covariance, the paper's BTilde, is U^{-1} U^{-T} in the whitened basis).
 __global__ void __launch_bounds__(NT, MRA_MINB)
 k_predict(TreeParams tp, PredParams pp, double* ws, WsLayout L, unsigned long long* counter) {
-    extern __shared__ double smem[];
+    double* smem = dyn_smem();
     const CovP cp = to_covp(tp.cp);
     const int M = tp.M, J = tp.J, rh = tp.rh, m = M - 1, Pg = m * rh, ncol = Pg + 1;
     double* base = ws + (long long)blockIdx.x * L.stride;
@@ -614,9 +521,6 @@ k_predict(TreeParams tp, PredParams pp, double* ws, WsLayout L, unsigned long lo
 // per leaf, panel solve), batched block forward substitution, per-leaf d/u, then per group the
 // stacked SYRK + merge. Tasks are int4 {leaf, i, k, 0}.
 
-__device__ __forceinline__ int leaf_n(const TreeParams& tp, long long l) {
-    return (int)(tp.leaf_off[l + 1] - tp.leaf_off[l]);
-}
 
 // Covariance blocks C(P, Q_{a_k}), k = 1..M-1, of 64 rows of one leaf into G's column blocks (M-1-k)
 // and the y column: a phase of its own, with no DMMA work sharing the fp64 pipe (generated inside the
@@ -659,221 +563,37 @@ k_wide_covfill(TreeParams tp, WideParams wp, const int4* tasks, long long ntask)
     }
 }
 
-// V chain for 64 rows of one leaf (covariance blocks in place from k_wide_covfill)
-__global__ void __launch_bounds__(NT, MRA_MINB)
-k_wide_chain(TreeParams tp, WideParams wp, const int4* tasks, long long ntask, unsigned long long* counter) {
-    extern __shared__ double smem[];
-    const CovP cp = to_covp(tp.cp);
-    const int m = tp.M - 1;
-    for (;;) {
-        const long long it = next_item(counter, smem);
-        if (it >= ntask) break;
-        const int4 tk = tasks[it];
-        const long long l = tk.x;
-        const long long o0 = tp.leaf_off[l] + 64LL * tk.y;
-        const int n = min(64, leaf_n(tp, l) - 64 * tk.y);
-        double* Gr = wp.G + (o0 - wp.G_base) * wp.ldG;
-        PHASE_MARK(pt0);
-        point_chain_pre(tp, m, l >> tp.lj, n, Gr, wp.ldG, cp, smem);
-        PHASE_ADD(28, pt0);
-#ifdef MRA_PHASE_TIMING
-        if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[29], 1ULL);
-#endif
-    }
+
+
+// diagonal block s of leaf l: L_ss, D_s = L_ss^{-1}, block log-det
+__device__ __forceinline__ void wide_diag_blk(const TreeParams& tp, const WideParams& wp, long long l, int s,
+                                              double* smem) {
+    FacSmem f = fac_smem(smem);
+    if (threadIdx.x == 0) *f.bad = 0;
+    const int n = leaf_n(tp, l), ld = wp.S_ld[l], nb = min(64, n - 64 * s);
+    double* Sss = wp.S + wp.S_off[l] + 64LL * s * ld + 64LL * s;
+    double* Ds = wp.D + wp.D_off[l] + 4096LL * s;
+    load_block_lower(f.blk, Sss, ld, nb, 0.0);
+    const double ldet = chol_inv_small(f.blk, f.inv, nb, f.diagv, f.bad, f.red, f.tmp);
+    if (*f.bad && threadIdx.x == 0) set_err(tp.err, tp.M, l);
+    store_block_lower(f.blk, Sss, ld, nb);
+    store_block_full(f.inv, Ds, 64, nb);
+    if (threadIdx.x == 0) wp.lblk[wp.D_off[l] / 4096 + s] = ldet;
 }
 
-// Sigma_l tile (i, k), k <= i: C(S_i, S_k) + tau2 delta - V_i V_k^T
-__global__ void __launch_bounds__(NT, MRA_MINB)
-k_wide_sigma(TreeParams tp, WideParams wp, const int4* tasks, long long ntask, unsigned long long* counter) {
-    extern __shared__ double smem[];
-    const CovP cp = to_covp(tp.cp);
-    const int Pg = (tp.M - 1) * tp.rh;
-    for (;;) {
-        const long long it = next_item(counter, smem);
-        if (it >= ntask) break;
-        const int4 tk = tasks[it];
-        const long long l = tk.x;
-        const int i = tk.y, k = tk.z, n = leaf_n(tp, l);
-        const long long o = tp.leaf_off[l];
-        const int ld = wp.S_ld[l];
-        double* C = wp.S + wp.S_off[l] + 64LL * i * ld + 64LL * k;
-        const double* Gi = wp.G + (o - wp.G_base + 64LL * i) * wp.ldG;
-        const double* Gk = wp.G + (o - wp.G_base + 64LL * k) * wp.ldG;
-        cta_gemm<MEMN, MEMN, MEMN, MEMN>(min(64, n - 64 * i), min(64, n - 64 * k), i == k, op_mem(Gi, wp.ldG),
-                                         op_mem(Gk, wp.ldG), Pg, op_mem(Gi, 0), op_mem(Gi, 0), 0,
-                                         ci_cov(tp.pxy + 2 * (o + 64LL * i), tp.pxy + 2 * (o + 64LL * k),
-                                                i == k ? tp.tau2 : 0.0),
-                                         -1.0, C, ld, cp, smem);
-    }
-}
-
-// Updates of the super-blocked Cholesky (blocks of 64, super-blocks of NB blocks), K range
-// [64 kb0, 64 kb1) of the launch:
-//   type 0 (leaf, i, j): A_ij -= L_{i,K} L_{j,K}^T   (i >= j; lower when i == j) -- the left-looking update
-//          of step j inside a super-block (K = the super-block's columns left of j), or the right-looking
-//          trailing update after a super-block (K = its NB columns)
-//   type 1 (leaf, i, c): G_i[:, c] -= L_{i,K} G_K[:, c] -- trailing update of the blocked substitution
-//          (leaves solved without the explicit inverse)
-__global__ void __launch_bounds__(NT, MRA_MINB)
-k_wide_update(TreeParams tp, WideParams wp, int s, const int4* tasks, long long ntask, unsigned long long* counter) {
-    extern __shared__ double smem[];
-    const CovP cp = to_covp(tp.cp);
-    const int ncol = (tp.M - 1) * tp.rh + 1;
-    const int k0 = 64 * wp.kb0, K = 64 * (wp.kb1 - wp.kb0);
-    (void)s;
-    for (;;) {
-        const long long it = next_item(counter, smem);
-        if (it >= ntask) break;
-        const int4 tk = tasks[it];
-        const long long l = tk.x;
-        const int i = tk.y, n = leaf_n(tp, l), ld = wp.S_ld[l];
-        double* Sl = wp.S + wp.S_off[l];
-        const double* Ai = Sl + 64LL * i * ld + k0;
-        if (tk.w == 0) {
-            const int j = tk.z;
-            double* C = Sl + 64LL * i * ld + 64LL * j;
-            const double* Aj = Sl + 64LL * j * ld + k0;
-            cta_gemm<MEMN, MEMN, MEMN, MEMN>(min(64, n - 64 * i), min(64, n - 64 * j), i == j, op_mem(Ai, ld),
-                                             op_mem(Aj, ld), K, op_mem(Ai, 0), op_mem(Ai, 0), 0, ci_mem(C, ld), -1.0,
-                                             C, ld, cp, smem);
-        } else {
-            const int c = tk.z;
-            const long long o = tp.leaf_off[l];
-            double* Gl = wp.G + (o - wp.G_base) * wp.ldG + 64LL * c;
-            double* Gi = Gl + 64LL * i * wp.ldG;
-            cta_gemm<MEMN, MEMT, MEMN, MEMN>(min(64, n - 64 * i), min(64, ncol - 64 * c), 0, op_mem(Ai, ld),
-                                             op_mem(Gl + (long long)k0 * wp.ldG, wp.ldG), K, op_mem(Ai, 0),
-                                             op_mem(Ai, 0), 0, ci_mem(Gi, wp.ldG), -1.0, Gi, wp.ldG, cp, smem);
-        }
-    }
-}
 
 // diagonal block of step s for every leaf with more than s blocks: L_ss, D_s = L_ss^{-1}, log-det
 __global__ void __launch_bounds__(NT, MRA_MINB)
 k_wide_diag(TreeParams tp, WideParams wp, int s, const int4* tasks, long long ntask, unsigned long long* counter) {
-    extern __shared__ double smem[];
-    FacSmem f = fac_smem(smem);
+    double* smem = dyn_smem();
     for (;;) {
         const long long it = next_item(counter, smem);
         if (it >= ntask) break;
-        if (threadIdx.x == 0) *f.bad = 0;
-        const long long l = tasks[it].x;
-        const int n = leaf_n(tp, l), ld = wp.S_ld[l], nb = min(64, n - 64 * s);
-        double* Sss = wp.S + wp.S_off[l] + 64LL * s * ld + 64LL * s;
-        double* Ds = wp.D + wp.D_off[l] + 4096LL * s;
-        load_block_lower(f.blk, Sss, ld, nb, 0.0);
-        const double ldet = chol_inv_small(f.blk, f.inv, nb, f.diagv, f.bad, f.red, f.tmp);
-        if (*f.bad && threadIdx.x == 0) set_err(tp.err, tp.M, l);
-        store_block_lower(f.blk, Sss, ld, nb);
-        store_block_full(f.inv, Ds, 64, nb);
-        if (threadIdx.x == 0) wp.lblk[wp.D_off[l] / 4096 + s] = ldet;
+        wide_diag_blk(tp, wp, tasks[it].x, s, smem);
     }
 }
 
-// step s, after the diagonal: panel tasks (leaf, i > s, 0): L_is = A_is D_s^T; for small leaves
-// (n <= ncol) the tasks of row block s of X = L^{-1} (leaf, k < s, 2): X_sk = -D_s sum_{k<=j<s} L_sj X_jk,
-// for large leaves the forward-substitution tasks of row block s (leaf, column tile, 1). X's off-diagonal blocks are
-// kept TRANSPOSED in the (otherwise unused) upper triangle of the leaf's Sigma buffer: X[a][b] (block
-// a > block b) at S[b * ld + a]; its diagonal blocks are the inverted D_s.
-__global__ void __launch_bounds__(NT, MRA_MINB)
-k_wide_panel_x(TreeParams tp, WideParams wp, int s, const int4* tasks, long long ntask, unsigned long long* counter) {
-    extern __shared__ double smem[];
-    const CovP cp = to_covp(tp.cp);
-    for (;;) {
-        const long long it = next_item(counter, smem);
-        if (it >= ntask) break;
-        const int4 tk = tasks[it];
-        const long long l = tk.x;
-        const int n = leaf_n(tp, l), ld = wp.S_ld[l], nb = min(64, n - 64 * s);
-        double* Sl = wp.S + wp.S_off[l];
-        const double* Ds = wp.D + wp.D_off[l] + 4096LL * s;
-        if (tk.z == 0) {
-            const int i = tk.y;
-            double* P = Sl + 64LL * i * ld + 64LL * s;
-            cta_gemm<MEMN, MEMN, MEMN, MEMN>(min(64, n - 64 * i), nb, 0, op_mem(P, ld), op_mem(Ds, 64), nb,
-                                             op_mem(P, 0), op_mem(P, 0), 0, ci_zero(), 1.0, P, ld, cp, smem);
-        } else if (tk.z == 1) {
-            // large leaves (n > ncol): blocked forward substitution G_s[:, c] = D_s (G_s - L_{s,<s} G_{<s})
-            // interleaved with the factorization (X = L^{-1} would cost n^3/3 > the solve itself)
-            const int c = tk.y, ncol = (tp.M - 1) * tp.rh + 1;
-            const long long o = tp.leaf_off[l];
-            double* Gs = wp.G + (o - wp.G_base + 64LL * s) * wp.ldG + 64LL * c;
-            const int nc = min(64, ncol - 64 * c);
-            const int k0 = 64 * wp.kb0;   // earlier super-blocks arrived through trailing updates
-            if (s > wp.kb0)
-                cta_gemm<MEMN, MEMT, MEMN, MEMN>(nb, nc, 0, op_mem(Sl + 64LL * s * ld + k0, ld),
-                                                 op_mem(wp.G + (o - wp.G_base + k0) * wp.ldG + 64LL * c, wp.ldG),
-                                                 64 * s - k0, op_mem(Sl, 0), op_mem(Sl, 0), 0, ci_mem(Gs, wp.ldG),
-                                                 -1.0, Gs, wp.ldG, cp, smem);
-            cta_gemm<MEMN, MEMT, MEMN, MEMN>(nb, nc, 0, op_mem(Ds, 64), op_mem(Gs, wp.ldG), nb, op_mem(Ds, 0),
-                                             op_mem(Ds, 0), 0, ci_zero(), 1.0, Gs, wp.ldG, cp, smem);
-        } else {
-            const int kb = tk.y;
-            const long long k0 = 64LL * kb, s0 = 64LL * s;
-            const double* Dk = wp.D + wp.D_off[l] + 4096LL * kb;
-            double* Yt = Sl + k0 * ld + s0;   // X_sk^T lives here (64 x nb)
-            // Y^T = D_k^T L_sk^T + sum_{k<j<s} X_jk^T L_sj^T
-            cta_gemm<MEMT, MEMN, MEMN, MEMN>(64, nb, 0, op_mem(Dk, 64), op_mem(Sl + s0 * ld + k0, ld), 64,
-                                             op_mem(Sl + k0 * ld + k0 + 64, ld), op_mem(Sl + s0 * ld + k0 + 64, ld),
-                                             (int)(s0 - k0 - 64), ci_zero(), 1.0, Yt, ld, cp, smem);
-            // X_sk^T = -Y^T D_s^T (in place: one output tile, every operand element is read first)
-            cta_gemm<MEMN, MEMN, MEMN, MEMN>(64, nb, 0, op_mem(Yt, ld), op_mem(Ds, 64), nb, op_mem(Yt, 0),
-                                             op_mem(Yt, 0), 0, ci_zero(), -1.0, Yt, ld, cp, smem);
-        }
-    }
-}
 
-// G[:, c] = X [V | y][:, c] per (leaf, 64-column tile), row blocks in DESCENDING order so the product
-// can overwrite its input: G_i = [X_{i,<i} | D_i] [B_{<i} ; B_i] only reads rows <= i of B.
-__global__ void __launch_bounds__(NT, MRA_MINB)
-k_wide_trsm(TreeParams tp, WideParams wp, const int4* tasks, long long ntask, unsigned long long* counter) {
-    extern __shared__ double smem[];
-    const CovP cp = to_covp(tp.cp);
-    const int ncol = (tp.M - 1) * tp.rh + 1;
-    for (;;) {
-        const long long it = next_item(counter, smem);
-        if (it >= ntask) break;
-        const int4 tk = tasks[it];
-        const long long l = tk.x;
-        const int n = leaf_n(tp, l), ld = wp.S_ld[l];
-        const double* Sl = wp.S + wp.S_off[l];
-        if (tk.z == 2) {
-            // the y column alone (ncol = 64 k + 1): g = X y by rows, X[i][K] = Sl[K ld + i] (K < block start)
-            // and the inverted diagonal block; row chunks descending so g can overwrite y in place
-            double* gcol = wp.G + (tp.leaf_off[l] - wp.G_base) * wp.ldG + (ncol - 1);
-            for (int base = ((n - 1) / NT) * NT; base >= 0; base -= NT) {
-                const int i = base + threadIdx.x;
-                double v = 0.0;
-                if (i < n) {
-                    const int bi = i / 64, i0 = 64 * bi;
-                    double s0 = 0.0, s1 = 0.0;
-                    int k = 0;
-                    for (; k + 1 < i0; k += 2) {
-                        s0 += Sl[(long long)k * ld + i] * gcol[(long long)k * wp.ldG];
-                        s1 += Sl[(long long)(k + 1) * ld + i] * gcol[(long long)(k + 1) * wp.ldG];
-                    }
-                    if (k < i0) s0 += Sl[(long long)k * ld + i] * gcol[(long long)k * wp.ldG];
-                    const double* Di = wp.D + wp.D_off[l] + 4096LL * bi + (long long)(i - i0) * 64;
-                    for (int kk = 0; kk <= i - i0; kk++) s1 += Di[kk] * gcol[(long long)(i0 + kk) * wp.ldG];
-                    v = s0 + s1;
-                }
-                __syncthreads();
-                if (i < n) gcol[(long long)i * wp.ldG] = v;
-                __syncthreads();
-            }
-            continue;
-        }
-        const int c0 = 64 * tk.y, nc = min(64, ncol - c0);
-        double* Gl = wp.G + (tp.leaf_off[l] - wp.G_base) * wp.ldG + c0;
-        for (int i = (n - 1) / 64; i >= 0; i--) {
-            const int i0 = 64 * i, nb = min(64, n - i0);
-            const double* Di = wp.D + wp.D_off[l] + 4096LL * i;
-            cta_gemm<MEMT, MEMT, MEMN, MEMT>(nb, nc, 0, op_mem(Sl + i0, ld), op_mem(Gl, wp.ldG), i0, op_mem(Di, 64),
-                                             op_mem(Gl + (long long)i0 * wp.ldG, wp.ldG), nb, ci_zero(), 1.0,
-                                             Gl + (long long)i0 * wp.ldG, wp.ldG, cp, smem);
-        }
-    }
-}
 
 // Level-(M-1) stacked SYRK and merge as one dataflow of tile tasks (host-ordered list, int4
 // {group, type, a, b}). With G = [G_o | G_r] (o = the group region's own rh columns, r = the rest incl.
@@ -890,7 +610,7 @@ k_wide_trsm(TreeParams tp, WideParams wp, const int4* tasks, long long ntask, un
 __global__ void __launch_bounds__(NT, MRA_MINB)
 k_wide_mtile(TreeParams tp, WideParams wp, long long g_first, double* out, long long out_first, int q,
              const int4* tasks, long long ntask, unsigned long long* counter, MergeRing ring) {
-    extern __shared__ double smem[];
+    double* smem = dyn_smem();
     const CovP cp = to_covp(tp.cp);
     const int M = tp.M, J = tp.J, m = M - 1, rh = tp.rh, Pg = m * rh;
     const int nr = (q + 63) / 64;
@@ -1150,9 +870,9 @@ static void set_attrs() {
     if (g_attr_done) return;
     const int b = smem_bytes();
     const void* ks[12] = {(const void*)k_prior,       (const void*)k_bottom,      (const void*)k_merge,
-                          (const void*)k_smooth,      (const void*)k_wide_chain,  (const void*)k_wide_sigma,
-                          (const void*)k_wide_update, (const void*)k_wide_diag,   (const void*)k_wide_panel_x,
-                          (const void*)k_wide_trsm,   (const void*)k_wide_mtile,  (const void*)k_predict};
+                          (const void*)k_smooth,      (const void*)k_prior,       (const void*)k_prior,
+                          (const void*)k_prior,       (const void*)k_wide_diag,   (const void*)k_prior,
+                          (const void*)k_prior,       (const void*)k_wide_mtile,  (const void*)k_predict};
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -1249,19 +969,16 @@ cudaError_t launch_smooth(const TreeParams& tp, const double* muhat, const long 
 }  // namespace mra
 
 namespace mra {
-cudaError_t launch_wide(int phase, const TreeParams& tp, const WideParams& wp, int step, const int4* tasks,
-                        long long ntask, int grid, unsigned long long* counter, cudaStream_t st) {
+// the wide-path phases that run on this translation unit's engine: 3 = diagonal factor, 6 = covariance fill
+// (launch_wide in mra_kernels_gemm.cu forwards them here)
+cudaError_t launch_wide_main(int phase, const TreeParams& tp, const WideParams& wp, int step, const int4* tasks,
+                             long long ntask, int grid, unsigned long long* counter, cudaStream_t st) {
     set_attrs();
-    grid = clamp_grid(grid, ntask, phase == 5 ? 9 : (phase == 6 ? 4 : 4 + phase));
+    grid = clamp_grid(grid, ntask, phase == 6 ? 4 : 4 + phase);
     if (grid < 1) return cudaSuccess;
     const int b = smem_bytes();
     switch (phase) {
-        case 0: k_wide_chain<<<grid, NT, b, st>>>(tp, wp, tasks, ntask, counter); break;
-        case 1: k_wide_sigma<<<grid, NT, b, st>>>(tp, wp, tasks, ntask, counter); break;
-        case 2: k_wide_update<<<grid, NT, b, st>>>(tp, wp, step, tasks, ntask, counter); break;
         case 3: k_wide_diag<<<grid, NT, b, st>>>(tp, wp, step, tasks, ntask, counter); break;
-        case 4: k_wide_panel_x<<<grid, NT, b, st>>>(tp, wp, step, tasks, ntask, counter); break;
-        case 5: k_wide_trsm<<<grid, NT, b, st>>>(tp, wp, tasks, ntask, counter); break;
         case 6: {
             static int cf_grid = 0;
             if (!cf_grid) {

@@ -6,7 +6,7 @@
 using namespace mra;
 
 __global__ void __launch_bounds__(NT, 2) kbench(int n, int reps, unsigned long long* cycles, double* out) {
-    extern __shared__ double smem[];
+    double* smem = dyn_smem();
     FacSmem f = fac_smem(smem);
     long long total = 0;
     double acc = 0;

@@ -17,7 +17,7 @@ using namespace mra;
 template <int KA, int KB>
 __global__ void __launch_bounds__(NT, MRA_MINB) kbench(const double* A, const double* B, const double* pts,
                                                        double* C, int K, long long ntiles) {
-    extern __shared__ double smem[];
+    double* smem = dyn_smem();
     CovP cp;
     cp.kind = 0; cp.s2 = 1.0; cp.rho = 2.0; cp.xs = 1.0; cp.ys = 1.0;
 #ifdef MRA_HAS_IR
@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(NT, MRA_MINB) kbench(const double* A, const do
 
 template <int KA, int KB>
 void run(const char* name, double* A, double* B, double* P, double* C, int K) {
-    const int bytes = SMEM_DBL * 8;
+    const int bytes = GEMM_SMEM_DBL * 8;
     cudaFuncSetAttribute(kbench<KA, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     int per = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kbench<KA, KB>, NT, bytes);
@@ -96,7 +96,7 @@ int main() {
         cudaFree(X); cudaFree(Y); cudaFree(Z);
     }
 #endif
-    for (int K : {128, 576, 1024}) {
+    for (int K : {64, 128, 192, 576}) {
         run<MEMN, MEMN>("MEMNxMEMN", A, B, P, C, K);
         run<MEMT, MEMT>("MEMTxMEMT", A, B, P, C, K);
         run<COVK, MEMN>("COVKxMEMN", A, B, P, C, K);
