@@ -630,7 +630,7 @@ static mra_status size_wide(mra_plan* P, double budget, bool explicit_budget) {
                     const long long gc = ws.gcount;
                     const double kavg = (double)(P->leaf_off[(ws.g0 + gc) * J] - P->leaf_off[ws.g0 * J]) / gc;
                     const double step_us = (1.0 + nrm + nrm * (nrm + 1) / 2.0) * std::max(kavg, 64.0) * 0.066 /
-                                           std::max(1, P->grid);
+                                           std::max(1, wide_mtile_resident());
                     const long long D1 = std::min<long long>(512, std::max<long long>(2, (long long)std::ceil(150.0 / step_us)));
                     const long long D2 = D1 + 12;   // an O task waits for all F of its group before its GEMM
                     mt_D2 = std::max(mt_D2, D2);

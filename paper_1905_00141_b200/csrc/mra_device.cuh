@@ -422,6 +422,9 @@ __device__ __forceinline__ void cta_gemm(int Mr, int Nc, int lower, const Op& A0
 //   form the panel L_ib = A_ib D_bb^{-T} and the trailing update A -= L_ib L_kb^T;
 //   then X = L^{-1} is assembled block-row by block-row: X_ij = -X_ii sum_k L_ik X_kj.
 // a: n x n (ld LDB), lower, overwritten by L. x: n x n (ld LDB) receives L^{-1} (upper part 0).
+// x == a: in place -- a receives L^{-1} (upper part 0) and L itself is not kept: each diagonal block
+// is replaced by its inverse as soon as it is factored (the panels need only the inverse), and the
+// block-row assembly of the off-diagonal blocks reads row i of L before overwriting it (through tmp).
 // tmp: >= 3*256 doubles of smem scratch. Returns log|A| (all threads); *bad set if not PD.
 #ifdef MRA_CHOL_DEBUG
 __device__ long long g_chol_dbg[16];
@@ -434,9 +437,10 @@ __device__ __noinline__ double chol_inv_small(double* a, double* x, int n, doubl
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     CHK(0);
     const int nbk = (n + 15) >> 4;
+    const bool inplace = (x == a);
     for (int e = tid; e < 64 * 64; e += NT) {
         const int i = e >> 6, j = e & 63;
-        if (i < n && j < n) x[i * LDB + j] = 0.0;
+        if (i < n && j < n && (!inplace || j > i)) x[i * LDB + j] = 0.0;
     }
     CHK(1);
     for (int b = 0; b < nbk; b++) {
@@ -507,6 +511,7 @@ __device__ __noinline__ double chol_inv_small(double* a, double* x, int n, doubl
                 xc[ii] = (s0 + s1) * dv[ii];
             }
             double* xd = x + j0 * LDB + j0;
+            if (inplace) __syncwarp();   // every lane has read L_bb before X_bb replaces it
             if (lane < nb) {
 #pragma unroll
                 for (int k = 0; k < 16; k++)
@@ -605,7 +610,7 @@ __device__ __noinline__ double chol_inv_small(double* a, double* x, int n, doubl
     // log-determinant: the n diagonal logs in parallel (warp 0), then a shuffle reduction
     if (tid < 32) {
         double sl = 0.0;
-        for (int j = tid; j < n; j += 32) sl += log(a[j * LDB + j]);
+        for (int j = tid; j < n; j += 32) sl += inplace ? -log(a[j * LDB + j]) : log(a[j * LDB + j]);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) sl += __shfl_xor_sync(0xffffffffu, sl, o);
         if (tid == 0) *red = 2.0 * sl;
@@ -651,6 +656,16 @@ __device__ __forceinline__ FacSmem fac_smem(double* smem) {
     f.tmp = f.diagv + 64;
     f.red = misc_smem(smem);
     f.bad = reinterpret_cast<int*>(misc_smem(smem) + 16);
+    return f;
+}
+
+// in-place factor view (chol_inv_small with x == blk): blk[64*LDB] | diag[64] | tmp[768]
+constexpr int FAC_IN_DBL = 64 * LDB + 64 + 768;
+__device__ __forceinline__ FacSmem fac_smem_inplace(double* smem) {
+    FacSmem f = fac_smem(smem);
+    f.inv = f.blk;
+    f.diagv = smem + 64 * LDB;
+    f.tmp = f.diagv + 64;
     return f;
 }
 

@@ -257,19 +257,302 @@ k_wide_trsm(TreeParams tp, WideParams wp, const int4* tasks, long long ntask, un
     }
 }
 
-static int g_gemm_resident[6] = {1, 1, 1, 1, 1, 1};   // resident CTAs per SM x SM count, by phase
+// diagonal block s of leaf l: D_s = L_ss^{-1} (in place; L_ss itself is never read again: panels, X rows,
+// substitutions and trsm use D_s), block log-det
+__device__ __forceinline__ void wide_diag_blk(const TreeParams& tp, const WideParams& wp, long long l, int s,
+                                              double* smem) {
+    FacSmem f = fac_smem_inplace(smem);
+    if (threadIdx.x == 0) *f.bad = 0;
+    const int n = leaf_n(tp, l), ld = wp.S_ld[l], nb = min(64, n - 64 * s);
+    double* Sss = wp.S + wp.S_off[l] + 64LL * s * ld + 64LL * s;
+    double* Ds = wp.D + wp.D_off[l] + 4096LL * s;
+    load_block_lower(f.blk, Sss, ld, nb, 0.0);
+    const double ldet = chol_inv_small(f.blk, f.inv, nb, f.diagv, f.bad, f.red, f.tmp);
+    if (*f.bad && threadIdx.x == 0) set_err(tp.err, tp.M, l);
+    store_block_full(f.inv, Ds, 64, nb);
+    if (threadIdx.x == 0) wp.lblk[wp.D_off[l] / 4096 + s] = ldet;
+}
+
+// diagonal block of step s for every leaf with more than s blocks: L_ss, D_s = L_ss^{-1}, log-det
+__global__ void __launch_bounds__(NT, MRA_MINB)
+k_wide_diag(TreeParams tp, WideParams wp, int s, const int4* tasks, long long ntask, unsigned long long* counter) {
+    double* smem = dyn_smem();
+    for (;;) {
+        const long long it = next_item(counter, smem);
+        if (it >= ntask) break;
+        wide_diag_blk(tp, wp, tasks[it].x, s, smem);
+    }
+}
+
+// Level-(M-1) stacked SYRK and merge as one dataflow of tile tasks (host-ordered list, int4
+// {group, type, a, b}). With G = [G_o | G_r] (o = the group region's own rh columns, r = the rest incl.
+// the y column; q = |r|):
+//   type 0  T00(g):   A_oo = G_o^T G_o, Lt = chol(I + A_oo), Li = Lt^{-1}, log|I + A_oo|, leaf d/u
+//   type 1  F(g, a):  F_a = (G_r,a^T G_o) Li^T    (waits for T00(g), which owns the slot once it runs)
+//   type 2  O(g,a,b): O_ab = G_r,a^T G_r,b - F_a F_b^T  -> output   (waits for every F(g, .), then ONE
+//                     two-segment GEMM with -F kept beside F)
+// i.e. Atilde = G^T G and the merge O = A_rr - A_ro (I + A_oo)^{-1} A_or without ever storing A_rr.
+// The host staggers the three task kinds (T00 of group s, F of group s - D1, O of group s - D2) so a
+// dependency is normally complete when its consumer is claimed; waits spin on counters of tasks
+// claimed earlier by co-resident CTAs, so they always terminate. Li and F live in a ring of small
+// per-group slots (reused NS groups later, after the group's last O task).
+__global__ void __launch_bounds__(NT, MRA_MINB)
+k_wide_mtile(TreeParams tp, WideParams wp, long long g_first, double* out, long long out_first, int q,
+             const int4* tasks, long long ntask, unsigned long long* counter, MergeRing ring) {
+    double* smem = dyn_smem();
+    const CovP cp = to_covp(tp.cp);
+    const int M = tp.M, J = tp.J, m = M - 1, rh = tp.rh, Pg = m * rh;
+    const int nr = (q + 63) / 64;
+    // when the y row is alone in the last 64-row tile (q = 64 k + 1: r_hat = 64), the tile tasks cover
+    // rows 0..q-2 only and ONE task per group forms the y row from w = g^T G (a GEMV over the group's G)
+    const bool ysep = (q % 64 == 1) && q > 1;
+    const int nrF = ysep ? nr - 1 : nr;
+    const int nO = nrF * (nrF + 1) / 2 + (ysep ? 1 : 0);
+    FacSmem f = fac_smem_inplace(smem);
+    double* red = misc_smem(smem);
+    const long long leaf_id0 = lvl_first(J, M);
+    for (;;) {
+        const long long it = next_item(counter, smem);
+        if (it >= ntask) break;
+        const int4 tk = tasks[it];
+        const long long gi = tk.x, g = g_first + gi;
+        const int slot = (int)(gi % ring.ns);
+        double* Aoo = ring.slot + (long long)slot * ring.stride;
+        double* Li = Aoo + 4096;
+        double* F = Li + rh * rh;
+        double* Fn = F + (long long)q * rh;   // -F, so an O tile is ONE two-segment GEMM
+        const long long o = tp.leaf_off[g * J];
+        const int ng = (int)(tp.leaf_off[g * J + J] - o);
+        const double* G = wp.G + (o - wp.G_base) * wp.ldG;
+        const long long id = lvl_first(J, m) + g;
+        PHASE_MARK(ph0);
+        if (tk.y == 0) {
+            if (gi >= ring.ns) {   // the group NS earlier must have released the slot
+                if (threadIdx.x == 0) {
+                    while (*(volatile long long*)(ring.slot_done + slot) < gi / ring.ns) __nanosleep(100);
+                    __threadfence();
+                }
+                __syncthreads();
+            }
+            if (threadIdx.x == 0) *f.bad = 0;
+            double dsum = 0.0;
+            for (int c = 0; c < J; c++) {
+                const long long l = g * J + c;
+                const long long ol = tp.leaf_off[l];
+                const int n = leaf_n(tp, l);
+                double u = 0.0;
+                for (int i = threadIdx.x; i < n; i += NT) {
+                    const double gv = wp.G[(ol - wp.G_base + i) * wp.ldG + Pg];
+                    u += gv * gv;
+                }
+                u = cta_sum(u, red);
+                if (threadIdx.x == 0) {
+                    double d = 0.0;
+                    for (int bb = 0; bb < (n + 63) / 64; bb++) d += wp.lblk[wp.D_off[l] / 4096 + bb];
+                    tp.dreg[leaf_id0 + l] = d;
+                    tp.ureg[leaf_id0 + l] = u;
+                    red[9] = d;
+                }
+                __syncthreads();
+                dsum += red[9];
+                __syncthreads();
+            }
+            cta_gemm<MEMT, MEMT, MEMN, MEMN>(rh, rh, 1, op_mem(G, wp.ldG), op_mem(G, wp.ldG), ng, op_mem(G, 0),
+                                             op_mem(G, 0), 0, ci_zero(), 1.0, Aoo, 64, cp, smem);
+            load_block_lower(f.blk, Aoo, 64, rh, 1.0);
+            const double ldm = chol_inv_small(f.blk, f.inv, rh, f.diagv, f.bad, f.red, f.tmp);
+            if (*f.bad && threadIdx.x == 0) set_err(tp.err, m, g);
+            store_block_full(f.inv, Li, rh, rh);
+            if (tp.post) {
+                double* P = tp.post + tp.post_base[m] + g * ((long long)rh * rh + (long long)q * rh);
+                for (int e = threadIdx.x; e < rh * rh; e += NT) P[e] = f.inv[(e / rh) * LDB + (e % rh)];
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                tp.dreg[id] = dsum + ldm;
+                __threadfence();
+                atomicExch(ring.chol_done + gi, 1);
+            }
+            PHASE_ADD(16, ph0);
+#ifdef MRA_PHASE_TIMING
+            if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[17], 1ULL);
+#endif
+        } else if (tk.y == 1) {
+            const int a = tk.z, r0 = 64 * a, nrow = min(64, q - r0);
+            double* Fa = F + (long long)r0 * rh;
+            // the slot is this group's only after T00 has waited for it (chol_done is set after that)
+            if (threadIdx.x == 0) {
+                while (*(volatile int*)(ring.chol_done + gi) == 0) __nanosleep(100);
+                __threadfence();
+            }
+            __syncthreads();
+            PHASE_ADD(19, ph0);
+            PHASE_MARK(ph1);
+            cta_gemm<MEMT, MEMT, MEMN, MEMN>(nrow, rh, 0, op_mem(G + rh + r0, wp.ldG), op_mem(G, wp.ldG), ng,
+                                             op_mem(G, 0), op_mem(G, 0), 0, ci_zero(), 1.0, Fa, rh, cp, smem);
+            PHASE_ADD(18, ph1);
+            PHASE_MARK(ph2);
+            cta_gemm<MEMN, MEMN, MEMN, MEMN>(nrow, rh, 0, op_mem(Fa, rh), op_mem(Li, rh), rh, op_mem(Fa, 0),
+                                             op_mem(Fa, 0), 0, ci_zero(), 1.0, Fa, rh, cp, smem);
+            {
+                double* Fna = Fn + (long long)r0 * rh;
+                double* P = tp.post ? tp.post + tp.post_base[m] + g * ((long long)rh * rh + (long long)q * rh) +
+                                          rh * rh + (long long)r0 * rh
+                                    : nullptr;
+                // all loads first (Fa / Fna / P may alias as far as the compiler knows: interleaved
+                // load-store pairs would serialise on the L2 latency)
+                constexpr int NU = 4096 / NT;   // nrow * rh <= 64 * 64
+                double v[NU];
+#pragma unroll
+                for (int u = 0; u < NU; u++) {
+                    const int e = threadIdx.x + u * NT;
+                    v[u] = (e < nrow * rh) ? __ldcg(Fa + e) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < NU; u++) {
+                    const int e = threadIdx.x + u * NT;
+                    if (e < nrow * rh) {
+                        Fna[e] = -v[u];
+                        if (P) P[e] = v[u];
+                    }
+                }
+            }
+            __syncthreads();
+            PHASE_ADD(20, ph2);
+#ifdef MRA_PHASE_TIMING
+            if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[21], 1ULL);
+#endif
+            if (threadIdx.x == 0) {
+                __threadfence();
+                atomicAdd(ring.f_done + gi, 1);
+            }
+        } else if (tk.y == 3) {
+            // y row: w = g^T [G_o | G_r] (g = G's last column), F_y = w_o Li^T, O[y, :] = w_r - F_y F^T
+            if (threadIdx.x == 0) {
+                while (*(volatile int*)(ring.f_done + gi) < nrF) __nanosleep(100);
+                __threadfence();
+            }
+            __syncthreads();
+            const int ncg = Pg + 1, np2 = (ncg + 1) / 2;            // columns of G, column pairs
+            const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+            constexpr int MAXP = 12, CH = 2 * 32 * MAXP;            // column pairs per lane, columns per chunk
+            double* w = smem;                                        // [2 np2]
+            double* fy = w + 2 * np2;                                // [rh]
+            double* part = fy + 64;                                  // [NT / 32][CH] per-warp partial sums
+            for (int cb = 0; cb < np2; cb += 32 * MAXP) {
+                double2 acc2[MAXP];
+#pragma unroll
+                for (int u = 0; u < MAXP; u++) acc2[u] = make_double2(0.0, 0.0);
+                for (int r = warp; r < ng; r += NT / 32) {   // warp-strided rows, coalesced 16-byte loads
+                    const double* Gr = G + (long long)r * wp.ldG;
+                    const double gr = Gr[Pg];
+#pragma unroll
+                    for (int u = 0; u < MAXP; u++) {
+                        const int c2 = cb + lane + 32 * u;
+                        if (c2 < np2) {
+                            const double2 v = *reinterpret_cast<const double2*>(Gr + 2 * c2);
+                            acc2[u].x += gr * v.x;
+                            acc2[u].y += gr * v.y;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < MAXP; u++) {
+                    part[warp * CH + 2 * (lane + 32 * u)] = acc2[u].x;
+                    part[warp * CH + 2 * (lane + 32 * u) + 1] = acc2[u].y;
+                }
+                __syncthreads();
+                for (int c = threadIdx.x; c < CH && 2 * cb + c < 2 * np2; c += NT) {
+                    double v = 0.0;
+                    for (int ww = 0; ww < NT / 32; ww++) v += part[ww * CH + c];
+                    w[2 * cb + c] = v;
+                }
+                __syncthreads();
+            }
+            for (int c = threadIdx.x; c < rh; c += NT) {
+                double v = 0.0;
+                for (int k = 0; k < rh; k++) v += w[k] * Li[c * rh + k];
+                fy[c] = v;
+            }
+            __syncthreads();
+            double* Fy = F + (long long)(q - 1) * rh;
+            double* Fny = Fn + (long long)(q - 1) * rh;
+            double* Py = tp.post ? tp.post + tp.post_base[m] + g * ((long long)rh * rh + (long long)q * rh) + rh * rh +
+                                       (long long)(q - 1) * rh
+                                 : nullptr;
+            for (int c = threadIdx.x; c < rh; c += NT) {
+                Fy[c] = fy[c];
+                Fny[c] = -fy[c];
+                if (Py) Py[c] = fy[c];
+            }
+            double* Oy = out + (g - out_first) * (long long)q * q + (long long)(q - 1) * q;
+            for (int b = threadIdx.x; b < q; b += NT) {
+                const double* Fb = (b == q - 1) ? fy : F + (long long)b * rh;
+                double v = w[rh + b];
+                for (int c = 0; c < rh; c++) v -= fy[c] * Fb[c];
+                Oy[b] = v;
+                if (b == q - 1) tp.ureg[id] = v;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                __threadfence();
+                if (atomicAdd(ring.o_done + gi, 1) == nO - 1) {
+                    __threadfence();
+                    atomicAdd((unsigned long long*)(ring.slot_done + slot), 1ULL);
+                }
+            }
+        } else {
+            const int a = tk.z, b = tk.w, r0 = 64 * a, c0 = 64 * b;
+            const int nrow = min(64, q - r0), ncl = min(64, q - c0);
+            double* Oab = out + (g - out_first) * (long long)q * q + (long long)r0 * q + c0;
+            // every F of the group is final (the host schedules O tasks ~6 steps after the F tasks)
+            if (threadIdx.x == 0) {
+                while (*(volatile int*)(ring.f_done + gi) < nrF) __nanosleep(100);
+                __threadfence();
+            }
+            __syncthreads();
+            PHASE_ADD(23, ph0);
+            PHASE_MARK(ph2);
+            // O_ab = G_r,a^T G_r,b + (-F_a) F_b^T   (K = n_group, then K = rh)
+            cta_gemm<MEMT, MEMT, MEMN, MEMN>(nrow, ncl, a == b, op_mem(G + rh + r0, wp.ldG),
+                                             op_mem(G + rh + c0, wp.ldG), ng, op_mem(Fn + (long long)r0 * rh, rh),
+                                             op_mem(F + (long long)c0 * rh, rh), rh, ci_zero(), 1.0, Oab, q, cp,
+                                             smem);
+            PHASE_ADD(24, ph2);
+#ifdef MRA_PHASE_TIMING
+            if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[25], 1ULL);
+            if (a == nr - 1 && threadIdx.x == 0) {
+                atomicAdd(&g_phase_cycles[30], (unsigned long long)(clock64() - ph2));
+                atomicAdd(&g_phase_cycles[31], 1ULL);
+            }
+#endif
+            if (threadIdx.x == 0) {
+                if (a == nr - 1 && b == nr - 1) tp.ureg[id] = Oab[(long long)(nrow - 1) * q + ncl - 1];
+                __threadfence();
+                if (atomicAdd(ring.o_done + gi, 1) == nO - 1) {
+                    __threadfence();
+                    atomicAdd((unsigned long long*)(ring.slot_done + slot), 1ULL);
+                }
+            }
+        }
+    }
+}
+
+static int g_gemm_resident[7] = {1, 1, 1, 1, 1, 1, 1};   // resident CTAs per SM x SM count, by phase (6: mtile)
 static bool g_gemm_attr_done = false;
-static int gemm_smem_bytes() { return GEMM_SMEM_DBL * (int)sizeof(double); }
+// the stages, or the in-place 64 x 64 factor view (diag, T00 of mtile) if larger, plus the misc area
+constexpr int UNIT_SMEM_DBL = (FAC_IN_DBL > NSTAGE * STAGE_DBL ? FAC_IN_DBL : NSTAGE * STAGE_DBL) + MISC_DBL;
+static int gemm_smem_bytes() { return UNIT_SMEM_DBL * (int)sizeof(double); }
 static void gemm_set_attrs() {
     if (g_gemm_attr_done) return;
     const int b = gemm_smem_bytes();
-    const void* ks[6] = {(const void*)k_wide_chain, (const void*)k_wide_sigma, (const void*)k_wide_update,
-                         nullptr, (const void*)k_wide_panel_x, (const void*)k_wide_trsm};
+    const void* ks[7] = {(const void*)k_wide_chain,   (const void*)k_wide_sigma, (const void*)k_wide_update,
+                         (const void*)k_wide_diag,    (const void*)k_wide_panel_x, (const void*)k_wide_trsm,
+                         (const void*)k_wide_mtile};
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    for (int i = 0; i < 6; i++) {
-        if (!ks[i]) continue;
+    for (int i = 0; i < 7; i++) {
         cudaFuncSetAttribute(ks[i], cudaFuncAttributeMaxDynamicSharedMemorySize, b);
         int per = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ks[i], NT, b);
@@ -278,11 +561,11 @@ static void gemm_set_attrs() {
     g_gemm_attr_done = true;
 }
 
-// phases: 0 chain, 1 sigma, 2 update, 3 diag, 4 panel_x, 5 trsm, 6 covfill (3 and 6: mra_kernels.cu).
+// phases: 0 chain, 1 sigma, 2 update, 3 diag, 4 panel_x, 5 trsm, 6 covfill (6: mra_kernels.cu).
 // `grid` is ignored for this unit's phases: a persistent grid of every resident CTA pulls the tasks.
 cudaError_t launch_wide(int phase, const TreeParams& tp, const WideParams& wp, int step, const int4* tasks,
                         long long ntask, int grid, unsigned long long* counter, cudaStream_t st) {
-    if (phase == 3 || phase == 6) return launch_wide_main(phase, tp, wp, step, tasks, ntask, grid, counter, st);
+    if (phase == 6) return launch_wide_main(phase, tp, wp, step, tasks, ntask, grid, counter, st);
     if (phase < 0 || phase > 6) return cudaErrorInvalidValue;
     gemm_set_attrs();
     long long g = g_gemm_resident[phase];
@@ -293,11 +576,37 @@ cudaError_t launch_wide(int phase, const TreeParams& tp, const WideParams& wp, i
         case 0: k_wide_chain<<<(int)g, NT, b, st>>>(tp, wp, tasks, ntask, counter); break;
         case 1: k_wide_sigma<<<(int)g, NT, b, st>>>(tp, wp, tasks, ntask, counter); break;
         case 2: k_wide_update<<<(int)g, NT, b, st>>>(tp, wp, step, tasks, ntask, counter); break;
+        case 3: k_wide_diag<<<(int)g, NT, b, st>>>(tp, wp, step, tasks, ntask, counter); break;
         case 4: k_wide_panel_x<<<(int)g, NT, b, st>>>(tp, wp, step, tasks, ntask, counter); break;
         case 5: k_wide_trsm<<<(int)g, NT, b, st>>>(tp, wp, tasks, ntask, counter); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
+}
+
+// the level-(M-1) merge tile dataflow: every CTA of the grid must be resident (consumers spin on tasks
+// claimed earlier by co-resident CTAs), so the grid is exactly the resident CTA count
+cudaError_t launch_wide_mtile(const TreeParams& tp, const WideParams& wp, long long g_first, long long g_count,
+                              double* out, long long out_first, int q, const int4* tasks, long long ntask, int grid,
+                              unsigned long long* counter, const MergeRing& ring, cudaStream_t st) {
+    gemm_set_attrs();
+    (void)grid;
+    (void)g_count;
+    long long gr = g_gemm_resident[6];
+    if (ntask < gr) gr = ntask;
+    if (gr < 1) return cudaSuccess;
+    cudaError_t e = cudaMemsetAsync(ring.flags, 0, sizeof(int) * 3 * ring.maxg, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ring.slot_done, 0, sizeof(long long) * ring.ns, st);
+    if (e != cudaSuccess) return e;
+    k_wide_mtile<<<(int)gr, NT, gemm_smem_bytes(), st>>>(tp, wp, g_first, out, out_first, q, tasks, ntask, counter,
+                                                        ring);
+    return cudaGetLastError();
+}
+
+// resident CTAs of the merge tile dataflow (the host sizes its look-ahead D1 with it)
+int wide_mtile_resident() {
+    gemm_set_attrs();
+    return g_gemm_resident[6];
 }
 
 }  // namespace mra
