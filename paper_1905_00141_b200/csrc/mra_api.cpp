@@ -450,7 +450,10 @@ static mra_status size_device(mra_plan* P, double budget_gb, int stream_opt) {
         budget -= (double)tot * 8.0;
     }
     // slots: the resident CTAs of the persistent grid, fewer if the per-slot workspace is huge
-    long long slots = (long long)resident_ctas_per_sm() * P->nsm;
+    // (wide plans: as many as the GEMM unit's prior / merge kernels keep resident; the bottom path's
+    // one-CTA-per-group kernel needs far larger slots and runs on the default engine)
+    long long slots = (long long)(P->wide ? std::max(resident_ctas_per_sm(), unit_ctas_per_sm())
+                                          : resident_ctas_per_sm()) * P->nsm;
     const double ws_cap = std::max(0.25 * budget, (double)L.stride * 8.0);
     slots = std::min<long long>(slots, std::max<long long>(1, (long long)(ws_cap / (L.stride * 8.0))));
     P->grid = (int)slots;

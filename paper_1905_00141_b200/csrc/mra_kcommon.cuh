@@ -105,5 +105,41 @@ __device__ __forceinline__ int leaf_n(const TreeParams& tp, long long l) {
     return (int)(tp.leaf_off[l + 1] - tp.leaf_off[l]);
 }
 
+
+// factor view of the smem main area: out of place (mra_kernels.cu: L and L^{-1} both kept, 76 KB) or in
+// place (mra_kernels_gemm.cu: L^{-1} overwrites L, 42 KB), chosen per translation unit
+#ifndef MRA_FAC_INPLACE
+#define MRA_FAC_INPLACE 0
+#endif
+__device__ __forceinline__ FacSmem fac_view(double* smem) {
+    return MRA_FAC_INPLACE ? fac_smem_inplace(smem) : fac_smem(smem);
+}
+
+// merge of region with Atilde (ncol x ncol lower, ld ldA): Lt = chol(I + A_oo), Li = Lt^{-1},
+// F = A_ro Li^T, O = A_rr - F F^T (q = ncol - rh). Returns log|I + A_oo|.
+__device__ double merge_core(const double* A, int rh, long long ldA, double* O, int q, double* F, double* Li,
+                             int* err, int level, long long t, const CovP& cp, double* smem) {
+    FacSmem f = fac_view(smem);
+    load_block_lower(f.blk, A, ldA, rh, 1.0);
+    const double ld = chol_inv_small(f.blk, f.inv, rh, f.diagv, f.bad, f.red, f.tmp);
+    if (*f.bad && threadIdx.x == 0) set_err(err, level, t);
+    store_block_full(f.inv, Li, rh, rh);
+    __syncthreads();
+    cta_gemm<MEMN, MEMN, MEMN, MEMN>(q, rh, 0, op_mem(A + (long long)rh * ldA, ldA), op_mem(Li, rh), rh,
+                                     op_mem(Li, rh), op_mem(Li, rh), 0, ci_zero(), 1.0, F, rh, cp, smem);
+    cta_gemm<MEMN, MEMN, MEMN, MEMN>(q, q, 1, op_mem(F, rh), op_mem(F, rh), rh, op_mem(F, rh), op_mem(F, rh), 0,
+                                     ci_mem(A + (long long)rh * ldA + rh, ldA), -1.0, O, q, cp, smem);
+    return ld;
+}
+
+__device__ __forceinline__ void save_post(const TreeParams& tp, int m, long long t, int q, const double* Li,
+                                          const double* F) {
+    if (!tp.post) return;
+    const int rh = tp.rh;
+    double* P = tp.post + tp.post_base[m] + t * ((long long)rh * rh + (long long)q * rh);
+    for (int e = threadIdx.x; e < rh * rh; e += NT) P[e] = Li[e];
+    for (int e = threadIdx.x; e < q * rh; e += NT) P[rh * rh + e] = F[e];
+}
+
 }  // inline namespace MRA_ENG_NS
 }  // namespace mra

@@ -60,66 +60,8 @@ k_prior_covfill(TreeParams tp, int m, long long t_first, long long nitems) {
     }
 }
 
-__global__ void __launch_bounds__(NT, MRA_MINB)
-k_prior(TreeParams tp, int m, long long t_first, long long nitems, double* ws, long long ws_stride,
-        unsigned long long* counter) {
-    double* smem = dyn_smem();
-    const CovP cp = to_covp(tp.cp);
-    const int rh = tp.rh;
-    double* W = ws + (long long)blockIdx.x * ws_stride;
-    FacSmem f = fac_smem(smem);
-    const long long ldR = (long long)m * rh;
-    for (;;) {
-        const long long it = next_item(counter, smem);
-        if (it >= nitems) break;
-        if (threadIdx.x == 0) *f.bad = 0;
-        const long long t = t_first + it;
-        double* R = tp.prior + tp.prior_base[m] + (t - tp.prior_first[m]) * ldR * rh;
-        // V^k_R for k < m over R's blocks m-k, which hold C(Q_R, Q_{a_k}) (k_prior_covfill); they become -U
-        // after the inverse is known
-        point_chain_pre(tp, m - 1, t >> tp.lj, rh, R + rh, ldR, cp, smem);
-        // W^m_R = C(Q_R, Q_R) - sum_k V^k V^kT   (C(Q_R, Q_R) in R's block 0)
-        cta_gemm<MEMN, MEMN, MEMN, MEMN>(rh, rh, 1, op_mem(R + rh, ldR), op_mem(R + rh, ldR), (m - 1) * rh,
-                                         op_mem(R, ldR), op_mem(R, ldR), 0, ci_mem(R, ldR), -1.0, W, rh, cp,
-                                         smem);
-        load_block_lower(f.blk, W, rh, rh, 0.0);
-        chol_inv_small(f.blk, f.inv, rh, f.diagv, f.bad, f.red, f.tmp);
-        if (*f.bad && threadIdx.x == 0) set_err(tp.err, m, t);
-        store_block_full(f.inv, R, ldR, rh);
-        __syncthreads();
-        // -U = -L^{-1} V  (in place over the V blocks; single row tile)
-        if (m > 1)
-            cta_gemm<MEMN, MEMT, MEMN, MEMN>(rh, (m - 1) * rh, 0, op_mem(R, ldR), op_mem(R + rh, ldR), rh,
-                                             op_mem(R, ldR), op_mem(R, ldR), 0, ci_zero(), -1.0, R + rh, ldR, cp,
-                                             smem);
-    }
-}
 
-// merge of region with Atilde (ncol x ncol lower, ld ldA): Lt = chol(I + A_oo), Li = Lt^{-1},
-// F = A_ro Li^T, O = A_rr - F F^T (q = ncol - rh). Returns log|I + A_oo|.
-__device__ double merge_core(const double* A, int rh, long long ldA, double* O, int q, double* F, double* Li,
-                             int* err, int level, long long t, const CovP& cp, double* smem) {
-    FacSmem f = fac_smem(smem);
-    load_block_lower(f.blk, A, ldA, rh, 1.0);
-    const double ld = chol_inv_small(f.blk, f.inv, rh, f.diagv, f.bad, f.red, f.tmp);
-    if (*f.bad && threadIdx.x == 0) set_err(err, level, t);
-    store_block_full(f.inv, Li, rh, rh);
-    __syncthreads();
-    cta_gemm<MEMN, MEMN, MEMN, MEMN>(q, rh, 0, op_mem(A + (long long)rh * ldA, ldA), op_mem(Li, rh), rh,
-                                     op_mem(Li, rh), op_mem(Li, rh), 0, ci_zero(), 1.0, F, rh, cp, smem);
-    cta_gemm<MEMN, MEMN, MEMN, MEMN>(q, q, 1, op_mem(F, rh), op_mem(F, rh), rh, op_mem(F, rh), op_mem(F, rh), 0,
-                                     ci_mem(A + (long long)rh * ldA + rh, ldA), -1.0, O, q, cp, smem);
-    return ld;
-}
 
-__device__ __forceinline__ void save_post(const TreeParams& tp, int m, long long t, int q, const double* Li,
-                                          const double* F) {
-    if (!tp.post) return;
-    const int rh = tp.rh;
-    double* P = tp.post + tp.post_base[m] + t * ((long long)rh * rh + (long long)q * rh);
-    for (int e = threadIdx.x; e < rh * rh; e += NT) P[e] = Li[e];
-    for (int e = threadIdx.x; e < q * rh; e += NT) P[rh * rh + e] = F[e];
-}
 
 // Atilde_p = G_stack^T G_stack over the group's leaves (lower), then the merge of level-(M-1) region t
 __device__ void group_tail(const TreeParams& tp, int m, long long t, const double* G, long long ldG, int ng,
@@ -215,48 +157,6 @@ k_bottom(TreeParams tp, long long g_first, long long g_count, double* out, long 
     PHASE_ADD(12, kstart);
 }
 
-// --------------------------------------------------------------------------- merge
-__global__ void __launch_bounds__(NT, MRA_MINB)
-k_merge(TreeParams tp, int m, long long t_first, long long t_count, const double* child_out, long long child_first,
-        double* out, long long out_first, int q, double* ws, long long ws_stride, unsigned long long* counter) {
-    double* smem = dyn_smem();
-    const CovP cp = to_covp(tp.cp);
-    const int J = tp.J, rh = tp.rh;
-    const int qc = m * rh + 1;
-    const int ldA = qc + (qc & 1);   // even leading dimension -> 16-byte cp.async rows
-    double* A = ws + (long long)blockIdx.x * ws_stride;
-    double* F = A + (long long)qc * ldA;
-    double* Li = F + (long long)q * rh;
-    FacSmem f = fac_smem(smem);
-    const long long qc2 = (long long)qc * qc;
-    for (;;) {
-        const long long it = next_item(counter, smem);
-        if (it >= t_count) break;
-        if (threadIdx.x == 0) *f.bad = 0;
-        const long long t = t_first + it;
-        const double* C0 = child_out + (t * J - child_first) * qc2;
-        for (long long e = threadIdx.x; e < qc2; e += NT) {
-            const int i = (int)(e / qc), j = (int)(e - (long long)i * qc);
-            if (j <= i) {
-                double s = 0.0;
-                for (int c = 0; c < J; c++) s += C0[c * qc2 + e];
-                A[(long long)i * ldA + j] = s;
-            }
-        }
-        __syncthreads();
-        double* O = out + (t - out_first) * (long long)q * q;
-        const double ldm = merge_core(A, rh, ldA, O, q, F, Li, tp.err, m, t, cp, smem);
-        const long long id = lvl_first(J, m) + t;
-        if (threadIdx.x == 0) {
-            const long long c0 = lvl_first(J, m + 1) + t * J;
-            double ds = 0.0;
-            for (int c = 0; c < J; c++) ds += tp.dreg[c0 + c];
-            tp.dreg[id] = ds + ldm;
-            tp.ureg[id] = O[(long long)(q - 1) * q + q - 1];
-        }
-        save_post(tp, m, t, q, Li, F);
-    }
-}
 
 // log L = -1/2 (N log 2 pi + d_root + u_root)
 __global__ void k_final(TreeParams tp, double N, double* loglik) {
@@ -588,10 +488,10 @@ static int g_resident[12] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1};   // resident 
 static void set_attrs() {
     if (g_attr_done) return;
     const int b = smem_bytes();
-    const void* ks[12] = {(const void*)k_prior,       (const void*)k_bottom,      (const void*)k_merge,
-                          (const void*)k_smooth,      (const void*)k_prior,       (const void*)k_prior,
-                          (const void*)k_prior,       (const void*)k_prior,       (const void*)k_prior,
-                          (const void*)k_prior,       (const void*)k_prior,       (const void*)k_predict};
+    const void* ks[12] = {(const void*)k_bottom,      (const void*)k_bottom,      (const void*)k_bottom,
+                          (const void*)k_smooth,      (const void*)k_bottom,       (const void*)k_bottom,
+                          (const void*)k_bottom,       (const void*)k_bottom,       (const void*)k_bottom,
+                          (const void*)k_bottom,       (const void*)k_bottom,       (const void*)k_predict};
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -640,10 +540,7 @@ cudaError_t launch_prior(const TreeParams& tp, int m, long long t_first, long lo
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
-    grid = clamp_grid(grid, t_count, 0);
-    if (grid < 1) return cudaSuccess;
-    k_prior<<<grid, NT, smem_bytes(), st>>>(tp, m, t_first, t_count, ws, ws_stride, counter);
-    return cudaGetLastError();
+    return launch_prior_unit(tp, m, t_first, t_count, grid, ws, ws_stride, counter, st);
 }
 cudaError_t launch_bottom(const TreeParams& tp, long long g_first, long long g_count, double* out, long long out_first,
                           int q, int grid, double* ws, const WsLayout& L, unsigned long long* counter,
@@ -652,16 +549,6 @@ cudaError_t launch_bottom(const TreeParams& tp, long long g_first, long long g_c
     grid = clamp_grid(grid, g_count, 1);
     if (grid < 1) return cudaSuccess;
     k_bottom<<<grid, NT, smem_bytes(), st>>>(tp, g_first, g_count, out, out_first, q, ws, L, counter);
-    return cudaGetLastError();
-}
-cudaError_t launch_merge(const TreeParams& tp, int m, long long t_first, long long t_count, const double* child_out,
-                         long long child_first, double* out, long long out_first, int q, int grid, double* ws,
-                         long long ws_stride, unsigned long long* counter, cudaStream_t st) {
-    set_attrs();
-    grid = clamp_grid(grid, t_count, 2);
-    if (grid < 1) return cudaSuccess;
-    k_merge<<<grid, NT, smem_bytes(), st>>>(tp, m, t_first, t_count, child_out, child_first, out, out_first, q, ws,
-                                           ws_stride, counter);
     return cudaGetLastError();
 }
 cudaError_t launch_final(const TreeParams& tp, double N, double* d_loglik, cudaStream_t st) {

@@ -29,6 +29,7 @@
 #define MRA_TK MRA_GEMM_TK
 #define MRA_NSTAGE MRA_GEMM_NSTAGE
 #define MRA_MINB MRA_GEMM_MINB
+#define MRA_FAC_INPLACE 1
 
 #include <cuda_runtime.h>
 
@@ -538,7 +539,113 @@ k_wide_mtile(TreeParams tp, WideParams wp, long long g_first, double* out, long 
     }
 }
 
-static int g_gemm_resident[7] = {1, 1, 1, 1, 1, 1, 1};   // resident CTAs per SM x SM count, by phase (6: mtile)
+__global__ void __launch_bounds__(NT, MRA_MINB)
+k_prior(TreeParams tp, int m, long long t_first, long long nitems, double* ws, long long ws_stride,
+        unsigned long long* counter) {
+    double* smem = dyn_smem();
+    const CovP cp = to_covp(tp.cp);
+    const int rh = tp.rh;
+    double* W = ws + (long long)blockIdx.x * ws_stride;
+    FacSmem f = fac_view(smem);
+    const long long ldR = (long long)m * rh;
+    for (;;) {
+        const long long it = next_item(counter, smem);
+        if (it >= nitems) break;
+        if (threadIdx.x == 0) *f.bad = 0;
+        const long long t = t_first + it;
+        double* R = tp.prior + tp.prior_base[m] + (t - tp.prior_first[m]) * ldR * rh;
+        // V^k_R for k < m over R's blocks m-k, which hold C(Q_R, Q_{a_k}) (k_prior_covfill); they become -U
+        // after the inverse is known
+        point_chain_pre(tp, m - 1, t >> tp.lj, rh, R + rh, ldR, cp, smem);
+        // W^m_R = C(Q_R, Q_R) - sum_k V^k V^kT   (C(Q_R, Q_R) in R's block 0)
+        cta_gemm<MEMN, MEMN, MEMN, MEMN>(rh, rh, 1, op_mem(R + rh, ldR), op_mem(R + rh, ldR), (m - 1) * rh,
+                                         op_mem(R, ldR), op_mem(R, ldR), 0, ci_mem(R, ldR), -1.0, W, rh, cp,
+                                         smem);
+        load_block_lower(f.blk, W, rh, rh, 0.0);
+        chol_inv_small(f.blk, f.inv, rh, f.diagv, f.bad, f.red, f.tmp);
+        if (*f.bad && threadIdx.x == 0) set_err(tp.err, m, t);
+        store_block_full(f.inv, R, ldR, rh);
+        __syncthreads();
+        // -U = -L^{-1} V  (in place over the V blocks; single row tile)
+        if (m > 1)
+            cta_gemm<MEMN, MEMT, MEMN, MEMN>(rh, (m - 1) * rh, 0, op_mem(R, ldR), op_mem(R + rh, ldR), rh,
+                                             op_mem(R, ldR), op_mem(R, ldR), 0, ci_zero(), -1.0, R + rh, ldR, cp,
+                                             smem);
+    }
+}
+
+// --------------------------------------------------------------------------- merge
+__global__ void __launch_bounds__(NT, MRA_MINB)
+k_merge(TreeParams tp, int m, long long t_first, long long t_count, const double* child_out, long long child_first,
+        double* out, long long out_first, int q, double* ws, long long ws_stride, unsigned long long* counter) {
+    double* smem = dyn_smem();
+    const CovP cp = to_covp(tp.cp);
+    const int J = tp.J, rh = tp.rh;
+    const int qc = m * rh + 1;
+    const int ldA = qc + (qc & 1);   // even leading dimension -> 16-byte cp.async rows
+    double* A = ws + (long long)blockIdx.x * ws_stride;
+    double* F = A + (long long)qc * ldA;
+    double* Li = F + (long long)q * rh;
+    FacSmem f = fac_view(smem);
+    const long long qc2 = (long long)qc * qc;
+    for (;;) {
+        const long long it = next_item(counter, smem);
+        if (it >= t_count) break;
+        if (threadIdx.x == 0) *f.bad = 0;
+        const long long t = t_first + it;
+        const double* C0 = child_out + (t * J - child_first) * qc2;
+        // Atilde = sum of the J children (lower triangle): one warp per row, lanes along the row, U column
+        // groups per pass so every lane has U*J independent streaming loads in flight (the children's
+        // outputs are read exactly once: evict-first)
+        {
+            constexpr int U = 4;
+            const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+            for (int i = warp; i < qc; i += NT / 32) {
+                const double* ci = C0 + (long long)i * qc;
+                double* Ai = A + (long long)i * ldA;
+                for (int j0 = 0; j0 <= i; j0 += 32 * U) {
+                    double v[U];
+#pragma unroll
+                    for (int u = 0; u < U; u++) {
+                        const int j = j0 + lane + 32 * u;
+                        double sacc = 0.0;
+                        if (j <= i) {
+                            const double* p = ci + j;
+                            if (J == 4) {
+                                const double a0 = __ldcs(p), a1 = __ldcs(p + qc2), a2 = __ldcs(p + 2 * qc2),
+                                             a3 = __ldcs(p + 3 * qc2);
+                                sacc = (((sacc + a0) + a1) + a2) + a3;
+                            } else {
+                                for (int c = 0; c < J; c++) sacc += __ldcs(p + c * qc2);
+                            }
+                        }
+                        v[u] = sacc;
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; u++) {
+                        const int j = j0 + lane + 32 * u;
+                        if (j <= i) Ai[j] = v[u];
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        double* O = out + (t - out_first) * (long long)q * q;
+        const double ldm = merge_core(A, rh, ldA, O, q, F, Li, tp.err, m, t, cp, smem);
+        const long long id = lvl_first(J, m) + t;
+        if (threadIdx.x == 0) {
+            const long long c0 = lvl_first(J, m + 1) + t * J;
+            double ds = 0.0;
+            for (int c = 0; c < J; c++) ds += tp.dreg[c0 + c];
+            tp.dreg[id] = ds + ldm;
+            tp.ureg[id] = O[(long long)(q - 1) * q + q - 1];
+        }
+        save_post(tp, m, t, q, Li, F);
+    }
+}
+
+static int g_gemm_resident[9] = {1, 1, 1, 1, 1, 1, 1, 1, 1};   // resident CTAs per SM x SM count, by phase
+                                                               // (6: mtile, 7: prior, 8: merge)
 static bool g_gemm_attr_done = false;
 // the stages, or the in-place 64 x 64 factor view (diag, T00 of mtile) if larger, plus the misc area
 constexpr int UNIT_SMEM_DBL = (FAC_IN_DBL > NSTAGE * STAGE_DBL ? FAC_IN_DBL : NSTAGE * STAGE_DBL) + MISC_DBL;
@@ -546,13 +653,13 @@ static int gemm_smem_bytes() { return UNIT_SMEM_DBL * (int)sizeof(double); }
 static void gemm_set_attrs() {
     if (g_gemm_attr_done) return;
     const int b = gemm_smem_bytes();
-    const void* ks[7] = {(const void*)k_wide_chain,   (const void*)k_wide_sigma, (const void*)k_wide_update,
+    const void* ks[9] = {(const void*)k_wide_chain,   (const void*)k_wide_sigma, (const void*)k_wide_update,
                          (const void*)k_wide_diag,    (const void*)k_wide_panel_x, (const void*)k_wide_trsm,
-                         (const void*)k_wide_mtile};
+                         (const void*)k_wide_mtile,   (const void*)k_prior,      (const void*)k_merge};
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    for (int i = 0; i < 7; i++) {
+    for (int i = 0; i < 9; i++) {
         cudaFuncSetAttribute(ks[i], cudaFuncAttributeMaxDynamicSharedMemorySize, b);
         int per = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ks[i], NT, b);
@@ -601,6 +708,36 @@ cudaError_t launch_wide_mtile(const TreeParams& tp, const WideParams& wp, long l
     k_wide_mtile<<<(int)gr, NT, gemm_smem_bytes(), st>>>(tp, wp, g_first, out, out_first, q, tasks, ntask, counter,
                                                         ring);
     return cudaGetLastError();
+}
+
+cudaError_t launch_merge(const TreeParams& tp, int m, long long t_first, long long t_count, const double* child_out,
+                         long long child_first, double* out, long long out_first, int q, int grid, double* ws,
+                         long long ws_stride, unsigned long long* counter, cudaStream_t st) {
+    gemm_set_attrs();
+    grid = (int)std::min<long long>({(long long)grid, (long long)g_gemm_resident[8], t_count});
+    if (grid < 1) return cudaSuccess;
+    k_merge<<<grid, NT, gemm_smem_bytes(), st>>>(tp, m, t_first, t_count, child_out, child_first, out, out_first, q, ws,
+                                           ws_stride, counter);
+    return cudaGetLastError();
+}
+
+// k_prior of one level (the covariance blocks are filled first by launch_prior in mra_kernels.cu)
+cudaError_t launch_prior_unit(const TreeParams& tp, int m, long long t_first, long long t_count, int grid, double* ws,
+                              long long ws_stride, unsigned long long* counter, cudaStream_t st) {
+    gemm_set_attrs();
+    grid = (int)std::min<long long>({(long long)grid, (long long)g_gemm_resident[7], t_count});
+    if (grid < 1) return cudaSuccess;
+    k_prior<<<grid, NT, gemm_smem_bytes(), st>>>(tp, m, t_first, t_count, ws, ws_stride, counter);
+    return cudaGetLastError();
+}
+
+// resident CTAs per SM of this unit's kernels (the plan sizes its per-CTA workspace slots with it)
+int unit_ctas_per_sm() {
+    gemm_set_attrs();
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    return std::max(1, g_gemm_resident[8] / nsm);
 }
 
 // resident CTAs of the merge tile dataflow (the host sizes its look-ahead D1 with it)
