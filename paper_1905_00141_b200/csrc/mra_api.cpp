@@ -627,15 +627,19 @@ static mra_status size_wide(mra_plan* P, double budget, bool explicit_budget) {
                     }
                 ws.trsm_n = (long long)tasks.size() - ws.trsm_off;
                 // merge tile dataflow: step s holds T00 of group s, the F tasks of group s - D1 and the
-                // O tasks of group s - D2; D1 covers ~150 us of T00 latency (GEMM + 64x64
-                // factor) at the estimated step time
+                // O tasks of group s - D2; D1 covers ~1.2 ms of steps at the estimated step
+                // time, D2 = D1 + 96 (measured on C3 / C4 / C2 with MRA_MT_D1US / MRA_MT_D2ADD: the merge tile
+                // kernel takes 710 / 25.4 / 13.8 ms at 150 us + 12, 668 / 11.6 / 12.3 ms at 1.2 ms + 96, flat
+                // beyond; with 4 CTAs per SM a consumer claimed too soon stalls its whole CTA)
                 {
                     const long long gc = ws.gcount;
                     const double kavg = (double)(P->leaf_off[(ws.g0 + gc) * J] - P->leaf_off[ws.g0 * J]) / gc;
                     const double step_us = (1.0 + nrm + nrm * (nrm + 1) / 2.0) * std::max(kavg, 64.0) * 0.066 /
                                            std::max(1, wide_mtile_resident());
-                    const long long D1 = std::min<long long>(512, std::max<long long>(2, (long long)std::ceil(150.0 / step_us)));
-                    const long long D2 = D1 + 12;   // an O task waits for all F of its group before its GEMM
+                    static const double D1_US = [] { const char* e = getenv("MRA_MT_D1US"); return e ? atof(e) : 1200.0; }();
+                    static const long long D2_ADD = [] { const char* e = getenv("MRA_MT_D2ADD"); return e ? atoll(e) : 96LL; }();
+                    const long long D1 = std::min<long long>(512, std::max<long long>(2, (long long)std::ceil(D1_US / step_us)));
+                    const long long D2 = D1 + D2_ADD;   // an O task waits for all F of its group before its GEMM
                     mt_D2 = std::max(mt_D2, D2);
                     // a lone y row (q = 64 k + 1) is formed by one GEMV task per group (type 3), not by
                     // 1-row tiles (which cost nearly a full tile each)
