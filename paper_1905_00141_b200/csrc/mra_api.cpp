@@ -49,6 +49,11 @@ struct mra_plan {
     double* prior = nullptr;
     long long prior_base[MAXM + 1] = {0};
     bool stream = false;             // prior rows of levels >= c live per chunk (NEXT-4)
+    // host-y entry points: the H2D copy of y runs on its own stream while the prior levels (which do
+    // not read y) run on st; st waits for it just before the gather into leaf order
+    const double* host_y_pending = nullptr;
+    cudaStream_t cst = nullptr;
+    cudaEvent_t cev = nullptr;
     size_t dev_bytes = 0;            // device memory held by the plan
     double *dreg = nullptr, *ureg = nullptr, *loglik_d = nullptr;
     int* err = nullptr;
@@ -825,6 +830,8 @@ extern "C" void mra_plan_destroy(mra_plan* P) {
     if (P->device >= 0 && cudaSetDevice(P->device) == cudaSuccess) {
         cudaDeviceSynchronize();
         for (cudaEvent_t e : P->evpool) cudaEventDestroy(e);
+        if (P->cev) cudaEventDestroy(P->cev);
+        if (P->cst) cudaStreamDestroy(P->cst);
         for (void* a : P->allocs) cudaFree(a);
     }
     delete P;
@@ -1004,6 +1011,8 @@ static mra_status eval_wide(mra_plan* P, const TreeParams& tp, long long gf, lon
 }
 
 // prior + posterior below (and at) level c for this rank's subtrees
+static mra_status flush_host_y(mra_plan* P);
+
 static mra_status eval_lower(mra_plan* P, const TreeParams& tp0) {
     const int M = P->M, J = P->J, rh = P->rh, c = P->c;
     const TreeParams& tp = tp0;
@@ -1023,6 +1032,8 @@ static mra_status eval_lower(mra_plan* P, const TreeParams& tp0) {
             }
         }
     }
+    mra_status hs = flush_host_y(P);
+    if (hs) return hs;
     // posterior: chunks of Kc level-c regions
     for (auto& rg : runs) {
         for (long long a = rg.first; a < rg.second; a += P->Kc) {
@@ -1108,7 +1119,23 @@ static mra_status begin_eval(mra_plan* P, const double* d_y, const mra_theta* th
     CU(cudaMemsetAsync(P->counters, 0, 8 * (size_t)P->n_counters, P->st));
     P->wsub_next = 0;
     CU(cudaMemsetAsync(P->err, 0, 16, P->st));
-    LCHK(launch_gather(d_y, P->perm_d, P->zs, P->N, P->st));
+    if (!P->host_y_pending) LCHK(launch_gather(d_y, P->perm_d, P->zs, P->N, P->st));
+    return MRA_OK;
+}
+
+// the deferred host-y copy (mra_loglik / mra_loglik_batch): issued after the prior launches, on the copy
+// stream, so it overlaps them; the gather into leaf order then waits for it on the plan stream
+static mra_status flush_host_y(mra_plan* P) {
+    if (!P->host_y_pending) return MRA_OK;
+    if (!P->cst) {
+        CU(cudaStreamCreateWithFlags(&P->cst, cudaStreamNonBlocking));
+        CU(cudaEventCreateWithFlags(&P->cev, cudaEventDisableTiming));
+    }
+    CU(cudaMemcpyAsync(P->zin, P->host_y_pending, 8 * P->n_in, cudaMemcpyHostToDevice, P->cst));
+    CU(cudaEventRecord(P->cev, P->cst));
+    CU(cudaStreamWaitEvent(P->st, P->cev, 0));
+    P->host_y_pending = nullptr;
+    LCHK(launch_gather(P->zin, P->perm_d, P->zs, P->N, P->st));
     return MRA_OK;
 }
 
@@ -1149,6 +1176,14 @@ static mra_status ensure_post(mra_plan* P) {
         if ((s = dalloc(P, (void**)&P->ws_smooth, 8 * L.stride * slots, "smoothing workspace"))) return s;
     }
     return MRA_OK;
+}
+
+// NaN / Inf scan of a host array (OpenMP: 47M values in a few ms)
+static bool all_finite(const double* y, uint64_t n) {
+    long long bad = 0;
+#pragma omp parallel for schedule(static) reduction(+ : bad)
+    for (long long i = 0; i < (long long)n; i++) bad += !std::isfinite(y[i]);
+    return bad == 0;
 }
 
 static mra_status run_eval(mra_plan* P, const double* d_y, const mra_theta* th, double* loglik, mra_post* post,
@@ -1321,11 +1356,12 @@ extern "C" mra_status mra_loglik_dev(mra_plan* P, const double* d_y, const mra_t
 extern "C" mra_status mra_loglik(mra_plan* P, const double* y, const mra_theta* th, double* loglik, mra_post* post) {
     if (!P || !y) return fail(MRA_E_ARG, "plan or y is NULL");
     if (P->device < 0) return fail(MRA_E_CUDA, "host-only plan (device -2) cannot evaluate");
-    for (uint64_t i = 0; i < P->n_in; i++)
-        if (!std::isfinite(y[i])) return fail(MRA_E_ARG, "non-finite observation value");
+    if (!all_finite(y, P->n_in)) return fail(MRA_E_ARG, "non-finite observation value");
     if (cudaSetDevice(P->device) != cudaSuccess) return fail(MRA_E_CUDA, "cudaSetDevice failed");
-    CU(cudaMemcpyAsync(P->zin, y, 8 * P->n_in, cudaMemcpyHostToDevice, P->st));
-    return run_eval(P, P->zin, th, loglik, post, true);
+    P->host_y_pending = y;   // copied by flush_host_y, overlapping the prior levels
+    const mra_status s = run_eval(P, P->zin, th, loglik, post, true);
+    P->host_y_pending = nullptr;
+    return s;
 }
 
 extern "C" mra_status mra_loglik_batch_dev(mra_plan* P, const double* d_y, const mra_theta* th, int n_theta,
@@ -1342,11 +1378,14 @@ extern "C" mra_status mra_loglik_batch(mra_plan* P, const double* y, const mra_t
                                        double* loglik) {
     if (!P || !y || !th || !loglik || n_theta < 0) return fail(MRA_E_ARG, "bad arguments");
     if (P->device < 0) return fail(MRA_E_CUDA, "host-only plan (device -2) cannot evaluate");
-    for (uint64_t i = 0; i < P->n_in; i++)
-        if (!std::isfinite(y[i])) return fail(MRA_E_ARG, "non-finite observation value");
+    if (!all_finite(y, P->n_in)) return fail(MRA_E_ARG, "non-finite observation value");
     if (cudaSetDevice(P->device) != cudaSuccess) return fail(MRA_E_CUDA, "cudaSetDevice failed");
-    CU(cudaMemcpyAsync(P->zin, y, 8 * P->n_in, cudaMemcpyHostToDevice, P->st));   // once for the sweep
-    return mra_loglik_batch_dev(P, P->zin, th, n_theta, loglik);
+    if (n_theta == 0) return MRA_OK;
+    P->host_y_pending = y;   // copied once, during the first evaluation's prior levels
+    mra_status s = run_eval(P, P->zin, th, loglik, nullptr, false);
+    P->host_y_pending = nullptr;
+    if (s) return s;
+    return mra_loglik_batch_dev(P, P->zin, th + 1, n_theta - 1, loglik + 1);
 }
 
 // ----------------------------------------------------------------------- optimization
