@@ -285,8 +285,9 @@ def run_gpu(args, rank, world, local_rank):
         w.M = args.M
     log(f"[rank {rank}] data {w.name} n={w.n} in {time.time() - t0:.1f}s")
     t0 = time.time()
+    lanes = args.theta_lanes if args.theta_lanes is not None else 1
     plan = mra.mra_plan_create(w.x, w.y, w.M, w.J, w.r, device=local_rank, stream=stream, rank=rank,
-                               world=world, stream_prior=args.stream_prior)
+                               world=world, stream_prior=args.stream_prior, theta_lanes=lanes)
     torch.cuda.synchronize()
     plan_s = time.time() - t0
     log(f"[rank {rank}] plan in {plan_s:.1f}s: n_retained={plan.n_retained} r_hat={plan.r_hat}")
@@ -300,6 +301,10 @@ def run_gpu(args, rank, world, local_rank):
         xbuf = torch.zeros(mra.mra_shard_size(plan), dtype=torch.float64, device=dev)
 
     def step(host=False):
+        if world == 1 and len(thetas) > 1:   # a sweep: the batch entry points (theta lanes run concurrently)
+            if host:
+                return list(mra.mra_loglik_batch(plan, zpin_np, thetas))
+            return list(mra.mra_loglik_batch_dev(plan, zd, thetas))
         lls = []
         for th in thetas:
             if world == 1:
@@ -439,9 +444,11 @@ def run_gpu(args, rank, world, local_rank):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_block(w, plan, world),
+            "config": dict(config_block(w, plan, world), theta_lanes=lanes),
             "loglik": lls[0], "n_theta_per_step": ntheta, "flops_per_step": fm["total"] * ntheta,
-            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8 * w.n * ntheta,
+            "e2e": {"value": e2e_val, "unit": UNIT,
+                    # a sweep (mra_loglik_batch) copies y once per step, single evaluations once per theta
+                    "h2d_bytes_per_step": 8 * w.n * (1 if (ntheta > 1 and world == 1) else ntheta),
                     "d2h_bytes_per_step": 8 * ntheta},
             "gpu_launches": int(launches),
             "kernel_ms": {k: round(kms[k], 3) for k in mra.KERNEL_CLASSES},
@@ -463,6 +470,8 @@ def main():
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=list(synth.SPECS))
     ap.add_argument("--n", type=int, default=None, help="override the config's n (same recipe)")
     ap.add_argument("--M", type=int, default=None, help="override the config's M (with --n: same leaf sizes)")
+    ap.add_argument("--theta-lanes", type=int, default=None, help="plan option theta_lanes (NEXT-3): concurrent "
+                    "evaluation contexts for a theta sweep (C4: no gain, its phases already fill the GPU; see DESIGN.md)")
     ap.add_argument("--stream-prior", type=int, default=0, help="plan option stream_prior (NEXT-4): 0 auto, "
                     "1 always, -1 never")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -79,6 +79,11 @@ typedef struct {
                          computed once); -1 = always resident. A streaming plan evaluates log L
                          (mra_loglik*, mra_optimize, sharded log L) but keeps no posterior state:
                          posterior requests and mra_predict return MRA_E_CONFIG.                */
+    int theta_lanes;  /* theta-batched sweeps: 0 / 1 = one evaluation at a time;
+                         k > 1 = the plan keeps k evaluation contexts (each with its own stream and
+                         1/k of the memory budget, sharing the partition and task lists), and
+                         mra_loglik_batch* evaluates k parameter sets concurrently, so the phases'
+                         tails and small launches of one theta are filled by another's work        */
 } mra_opts;
 
 /* Posterior state requested from an evaluation; any pointer may be NULL. */

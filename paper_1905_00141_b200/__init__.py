@@ -44,7 +44,8 @@ class _Opts(ctypes.Structure):
     _fields_ = [("offset", ctypes.c_double), ("xscale", ctypes.c_double), ("yscale", ctypes.c_double),
                 ("device", ctypes.c_int), ("stream", ctypes.c_void_p), ("rank", ctypes.c_int),
                 ("world", ctypes.c_int), ("shard_level", ctypes.c_int), ("mem_budget_gb", ctypes.c_double),
-                ("wide", ctypes.c_int), ("host_plan", ctypes.c_int), ("stream_prior", ctypes.c_int)]
+                ("wide", ctypes.c_int), ("host_plan", ctypes.c_int), ("stream_prior", ctypes.c_int),
+                ("theta_lanes", ctypes.c_int)]
 
 
 class _Post(ctypes.Structure):
@@ -175,14 +176,15 @@ class PlanHandle:
 
 def mra_plan_create(x, y, M, J, r, offset=0.0, xscale=0.0, yscale=0.0, device=-1, stream=None, rank=0,
                     world=1, shard_level=0, mem_budget_gb=0.0, wide=0, host_plan=0,
-                    stream_prior=0) -> PlanHandle:
+                    stream_prior=0, theta_lanes=0) -> PlanHandle:
     lib = load_library()
     x = np.ascontiguousarray(x, dtype=np.float64)
     y = np.ascontiguousarray(y, dtype=np.float64)
     if x.shape != y.shape or x.ndim != 1:
         raise ValueError("x and y must be 1-D arrays of equal length")
     opts = _Opts(float(offset), float(xscale), float(yscale), int(device), _stream_ptr(stream), int(rank),
-                 int(world), int(shard_level), float(mem_budget_gb), int(wide), int(host_plan), int(stream_prior))
+                 int(world), int(shard_level), float(mem_budget_gb), int(wide), int(host_plan), int(stream_prior),
+                 int(theta_lanes))
     out = ctypes.c_void_p()
     _check(lib.mra_plan_create(_dptr(x), _dptr(y), x.shape[0], int(M), int(J), int(r), ctypes.byref(opts),
                                ctypes.byref(out)))

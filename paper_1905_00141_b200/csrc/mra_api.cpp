@@ -19,6 +19,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "mra_internal.h"
@@ -88,6 +89,13 @@ struct mra_plan {
     int smooth_grid = 0;
     uint64_t launches = 0;
     std::vector<void*> allocs;
+    std::vector<size_t> alloc_bytes;   // parallel to allocs
+    // theta lanes (NEXT-3): evaluation contexts sharing this plan's read-only device data, each with its
+    // own stream and mutable buffers; mra_loglik_batch* runs one theta per lane concurrently
+    std::vector<mra_plan*> lanes;
+    bool is_lane = false;
+    int n_lanes = 1;                   // requested evaluation contexts (opts.theta_lanes)
+    cudaEvent_t lane_ev = nullptr;
     // wide (big-leaf) path
     bool wide = false;
     struct WideSub {
@@ -163,6 +171,7 @@ static mra_status dalloc(mra_plan* p, void** ptr, size_t bytes, const char* what
         return fail(e == cudaErrorMemoryAllocation ? MRA_E_OOM : MRA_E_CUDA, buf);
     }
     p->allocs.push_back(*ptr);
+    p->alloc_bytes.push_back(bytes);
     p->dev_bytes += bytes;
     return MRA_OK;
 }
@@ -445,6 +454,7 @@ static mra_status size_device(mra_plan* P, double budget_gb, int stream_opt) {
     size_t freeb = 0, totalb = 0;
     cudaMemGetInfo(&freeb, &totalb);
     double budget = budget_gb > 0 ? budget_gb * 1e9 : 0.85 * (double)freeb;
+    budget /= std::max(1, P->n_lanes);   // every theta lane (NEXT-3) holds the same buffers
     // resident prior rows, unless they would crowd out the posterior pass (or the caller asks to
     // stream them): then only the levels above the chunk level stay resident (NEXT-4)
     P->stream = M >= 2 && (stream_opt > 0 || (stream_opt == 0 && (double)tot * 8.0 > 0.5 * budget));
@@ -703,6 +713,77 @@ static mra_status size_wide(mra_plan* P, double budget, bool explicit_budget) {
 // --------------------------------------------------------------------- C ABI entry
 extern "C" const char* mra_last_error(void) { return g_err.c_str(); }
 
+// an evaluation context for theta-batched sweeps: a copy of the plan's host metadata that shares its
+// read-only device data (observations, knots, CSR, task lists) and owns the buffers an evaluation
+// writes (sorted y, prior rows, per-region terms, merge outputs, workspaces, counters, wide buffers)
+static mra_status make_lane(mra_plan* P, mra_plan** out) {
+    mra_plan* Q = new mra_plan(*P);
+    Q->allocs.clear();
+    Q->alloc_bytes.clear();
+    Q->dev_bytes = 0;
+    Q->evpool.clear();
+    Q->ev_used = 0;
+    Q->recs.clear();
+    Q->lanes.clear();
+    Q->is_lane = true;
+    Q->lane_ev = nullptr;
+    Q->cst = nullptr;
+    Q->cev = nullptr;
+    Q->host_y_pending = nullptr;
+    Q->post = Q->muhat = Q->mu_d = Q->smooth_d = Q->ws_smooth = Q->ws_pred = nullptr;
+    Q->post_valid = false;
+    Q->st = nullptr;
+    *out = nullptr;
+    if (cudaStreamCreateWithFlags(&Q->st, cudaStreamNonBlocking) != cudaSuccess) {
+        delete Q;
+        return fail(MRA_E_CUDA, "theta lane: cudaStreamCreate failed");
+    }
+    auto bytes_of = [&](const void* ptr) -> size_t {
+        for (size_t i = 0; i < P->allocs.size(); i++)
+            if (P->allocs[i] == ptr) return P->alloc_bytes[i];
+        return 0;
+    };
+    mra_status s = MRA_OK;
+    auto dup = [&](auto*& f, const char* what) {
+        if (s || !f) return;
+        const size_t b = bytes_of(f);
+        if (!b) { s = fail(MRA_E_CUDA, std::string("theta lane: unknown buffer ") + what); return; }
+        void* p = nullptr;
+        s = dalloc(Q, &p, b, what);
+        f = reinterpret_cast<std::remove_reference_t<decltype(f)>>(p);
+    };
+    dup(Q->zs, "lane zs");
+    dup(Q->prior, "lane prior");
+    dup(Q->dreg, "lane dreg");
+    dup(Q->ureg, "lane ureg");
+    dup(Q->loglik_d, "lane loglik");
+    dup(Q->err, "lane err");
+    dup(Q->counters, "lane counters");
+    dup(Q->ws, "lane workspace");
+    for (int m = 0; m <= MAXM; m++) {
+        dup(Q->out_full[m], "lane level output");
+        dup(Q->out_chunk[m], "lane chunk output");
+    }
+    dup(Q->wG, "lane wide G");
+    dup(Q->wS, "lane wide Sigma");
+    dup(Q->wD, "lane wide Dinv");
+    dup(Q->wlblk, "lane wide logdets");
+    dup(Q->mring.slot, "lane merge slots");
+    dup(Q->mring.flags, "lane merge flags");
+    dup(Q->mring.slot_done, "lane merge slot_done");
+    if (Q->mring.flags) {
+        Q->mring.chol_done = Q->mring.flags;
+        Q->mring.f_done = Q->mring.flags + Q->mring.maxg;
+        Q->mring.o_done = Q->mring.flags + 2 * Q->mring.maxg;
+    }
+    if (s) {
+        mra_plan_destroy(Q);
+        return s;
+    }
+    *out = Q;
+    return MRA_OK;
+}
+
 extern "C" mra_status mra_plan_create(const double* x, const double* y, uint64_t n, int M, int J, int r,
                                       const mra_opts* opts, mra_plan** out) {
     g_err.clear();
@@ -819,7 +900,14 @@ extern "C" mra_status mra_plan_create(const double* x, const double* y, uint64_t
         TRY(cp(P->leaf_off_d, P->leaf_off.data(), 8 * (P->nleaf + 1)));
         if (P->nint) TRY(cp(P->kxy_d, kxy.data(), 16 * P->nint * P->rh));
     }
+    P->n_lanes = std::max(1, std::min(o.theta_lanes, 16));
+    if (P->world > 1) P->n_lanes = 1;
     TRY(size_device(P, o.mem_budget_gb, o.stream_prior));
+    for (int k = 1; k < P->n_lanes; k++) {
+        mra_plan* Q = nullptr;
+        TRY(make_lane(P, &Q));
+        P->lanes.push_back(Q);
+    }
 #undef TRY
     *out = P;
     return MRA_OK;
@@ -827,8 +915,12 @@ extern "C" mra_status mra_plan_create(const double* x, const double* y, uint64_t
 
 extern "C" void mra_plan_destroy(mra_plan* P) {
     if (!P) return;
+    for (mra_plan* Q : P->lanes) mra_plan_destroy(Q);
+    P->lanes.clear();
     if (P->device >= 0 && cudaSetDevice(P->device) == cudaSuccess) {
         cudaDeviceSynchronize();
+        if (P->is_lane && P->st) cudaStreamDestroy(P->st);
+        if (P->lane_ev) cudaEventDestroy(P->lane_ev);
         for (cudaEvent_t e : P->evpool) cudaEventDestroy(e);
         if (P->cev) cudaEventDestroy(P->cev);
         if (P->cst) cudaStreamDestroy(P->cst);
@@ -862,6 +954,7 @@ extern "C" uint64_t mra_last_launches(const mra_plan* P) { return P ? P->launche
 
 extern "C" mra_status mra_profile(mra_plan* P, int enable) {
     if (!P) return fail(MRA_E_ARG, "plan is NULL");
+    for (mra_plan* Q : P->lanes) mra_profile(Q, enable);
     P->prof = enable != 0;
     P->recs.clear();
     P->ev_used = 0;
@@ -871,9 +964,12 @@ extern "C" mra_status mra_profile(mra_plan* P, int enable) {
 
 extern "C" mra_status mra_kernel_times(const mra_plan* P, double* ms, uint64_t* launches) {
     if (!P) return fail(MRA_E_ARG, "plan is NULL");
-    for (int k = 0; k < MRA_NKCLASS; k++) {
-        if (ms) ms[k] = P->prof_ms[k];
-        if (launches) launches[k] = P->prof_cnt[k];
+    for (int k = 0; k < MRA_NKCLASS; k++) {   // summed over the theta lanes
+        double t = P->prof_ms[k];
+        uint64_t c = P->prof_cnt[k];
+        for (const mra_plan* Q : P->lanes) { t += Q->prof_ms[k]; c += Q->prof_cnt[k]; }
+        if (ms) ms[k] = t;
+        if (launches) launches[k] = c;
     }
     return MRA_OK;
 }
@@ -891,7 +987,11 @@ extern "C" mra_status mra_plan_memory(const mra_plan* P, int* streams_prior, int
     if (streams_prior) *streams_prior = P->stream ? 1 : 0;
     if (chunk_level) *chunk_level = P->c;
     if (chunk_regions) *chunk_regions = (uint64_t)P->Kc;
-    if (device_bytes) *device_bytes = (uint64_t)P->dev_bytes;
+    if (device_bytes) {
+        uint64_t b = P->dev_bytes;
+        for (const mra_plan* Q : P->lanes) b += Q->dev_bytes;   // theta lanes (NEXT-3)
+        *device_bytes = b;
+    }
     return MRA_OK;
 }
 
@@ -1364,13 +1464,56 @@ extern "C" mra_status mra_loglik(mra_plan* P, const double* y, const mra_theta* 
     return s;
 }
 
+// one log-likelihood evaluation issued on the context's stream without waiting (theta lanes)
+static mra_status issue_eval(mra_plan* P, const double* d_y, const mra_theta* th) {
+    mra_status s;
+    if ((s = begin_eval(P, d_y, th))) return s;
+    TreeParams tp = tree_params(P, th);
+    if ((s = eval_lower(P, tp))) return s;
+    return eval_upper(P, tp);
+}
+static mra_status finish_eval(mra_plan* P, double* loglik) {
+    mra_status s = check_err(P);   // synchronises the context's stream
+    if (s) return s;
+    CU(cudaMemcpy(loglik, P->loglik_d, 8, cudaMemcpyDeviceToHost));
+    return MRA_OK;
+}
+
 extern "C" mra_status mra_loglik_batch_dev(mra_plan* P, const double* d_y, const mra_theta* th, int n_theta,
                                            double* loglik) {
     if (!P || !d_y || !th || !loglik || n_theta < 0) return fail(MRA_E_ARG, "bad arguments");
-    for (int i = 0; i < n_theta; i++) {
-        mra_status s = run_eval(P, d_y, th + i, loglik + i, nullptr, false);
-        if (s) return s;
+    uint64_t total = 0;
+    const int L = std::min<int>(n_theta, 1 + (int)P->lanes.size());
+    if (L <= 1 || P->world > 1) {
+        for (int i = 0; i < n_theta; i++) {
+            mra_status s = run_eval(P, d_y, th + i, loglik + i, nullptr, false);
+            if (s) return s;
+            total += P->launches;
+        }
+        P->launches = total;
+        return MRA_OK;
     }
+    for (int i = 0; i < n_theta; i++)
+        if (mra_status s = check_theta(th + i)) return s;
+    if (cudaSetDevice(P->device) != cudaSuccess) return fail(MRA_E_CUDA, "cudaSetDevice failed");
+    // the lanes start after everything the caller queued on the plan stream (e.g. the write of y)
+    if (!P->lane_ev) CU(cudaEventCreateWithFlags(&P->lane_ev, cudaEventDisableTiming));
+    CU(cudaEventRecord(P->lane_ev, P->st));
+    for (mra_plan* Q : P->lanes) CU(cudaStreamWaitEvent(Q->st, P->lane_ev, 0));
+    auto lane = [&](int j) { return j == 0 ? P : P->lanes[j - 1]; };
+    for (int i0 = 0; i0 < n_theta; i0 += L) {
+        const int nb = std::min(L, n_theta - i0);
+        mra_status first = MRA_OK;
+        int issued = 0;
+        for (int j = 0; j < nb && !first; j++, issued++) first = issue_eval(lane(j), d_y, th + i0 + j);
+        for (int j = 0; j < issued; j++) {
+            mra_status s = finish_eval(lane(j), loglik + i0 + j);
+            if (!first) first = s;
+            total += lane(j)->launches;
+        }
+        if (first) return first;
+    }
+    P->launches = total;   // every launch of the sweep (mra_last_launches)
     return MRA_OK;
 }
 
@@ -1381,11 +1524,18 @@ extern "C" mra_status mra_loglik_batch(mra_plan* P, const double* y, const mra_t
     if (!all_finite(y, P->n_in)) return fail(MRA_E_ARG, "non-finite observation value");
     if (cudaSetDevice(P->device) != cudaSuccess) return fail(MRA_E_CUDA, "cudaSetDevice failed");
     if (n_theta == 0) return MRA_OK;
+    if (!P->lanes.empty()) {   // copied once; the lanes wait for it through the plan stream
+        CU(cudaMemcpyAsync(P->zin, y, 8 * P->n_in, cudaMemcpyHostToDevice, P->st));
+        return mra_loglik_batch_dev(P, P->zin, th, n_theta, loglik);
+    }
     P->host_y_pending = y;   // copied once, during the first evaluation's prior levels
     mra_status s = run_eval(P, P->zin, th, loglik, nullptr, false);
     P->host_y_pending = nullptr;
     if (s) return s;
-    return mra_loglik_batch_dev(P, P->zin, th + 1, n_theta - 1, loglik + 1);
+    const uint64_t first = P->launches;
+    s = mra_loglik_batch_dev(P, P->zin, th + 1, n_theta - 1, loglik + 1);
+    P->launches += first;
+    return s;
 }
 
 // ----------------------------------------------------------------------- optimization
