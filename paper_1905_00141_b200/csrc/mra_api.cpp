@@ -1574,12 +1574,35 @@ extern "C" mra_status mra_optimize(mra_plan* P, const double* d_y, mra_theta* th
         *out = -ll;
         return MRA_OK;
     };
+    // several independent points (initial simplex, shrink): one theta sweep, concurrent on a laned plan
+    auto f_many = [&](double (*Xs)[3], double* out, int n) -> mra_status {
+        if (!P->lanes.empty()) {
+            std::vector<mra_theta> ths(n, *theta);
+            for (int j = 0; j < n; j++) {
+                ths[j].sigma2 = std::exp(Xs[j][0]); ths[j].rho = std::exp(Xs[j][1]); ths[j].tau2 = std::exp(Xs[j][2]);
+            }
+            std::vector<double> ll(n, NAN);
+            if (mra_loglik_batch_dev(P, d_y, ths.data(), n, ll.data()) == MRA_OK) {
+                bool ok = true;
+                for (int j = 0; j < n; j++) ok = ok && std::isfinite(ll[j]);
+                if (ok) {
+                    for (int j = 0; j < n; j++) out[j] = -ll[j];
+                    evals += n;
+                    return MRA_OK;
+                }
+            }
+            g_err.clear();   // a failing point: evaluate one by one below (non-PD counts as +inf)
+        }
+        for (int j = 0; j < n; j++)
+            if (mra_status e = f(Xs[j], out + j)) return e;
+        return MRA_OK;
+    };
     double X[4][3], F[4];
     for (int j = 0; j < 4; j++) {
         for (int i = 0; i < 3; i++) X[j][i] = std::log(v0[i]) + ((j == i + 1) ? 0.5 : 0.0);
         clampv(X[j]);
-        if ((s = f(X[j], &F[j]))) return s;
     }
+    if ((s = f_many(X, F, 4))) return s;
     while (evals < max_evals) {
         int ord[4] = {0, 1, 2, 3};
         std::sort(ord, ord + 4, [&](int a, int b) { return F[a] < F[b]; });
@@ -1614,10 +1637,9 @@ extern "C" mra_status mra_optimize(mra_plan* P, const double* d_y, mra_theta* th
             if ((s = f(xc, &fc))) return s;
             if (fc < (outside ? fr : F[3])) { std::memcpy(X[3], xc, sizeof xc); F[3] = fc; }
             else {   // shrink towards the best vertex
-                for (int j = 1; j < 4; j++) {
+                for (int j = 1; j < 4; j++)
                     for (int i = 0; i < 3; i++) X[j][i] = X[0][i] + 0.5 * (X[j][i] - X[0][i]);
-                    if ((s = f(X[j], &F[j]))) return s;
-                }
+                if ((s = f_many(X + 1, F + 1, 3))) return s;
             }
         }
     }

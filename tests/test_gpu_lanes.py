@@ -85,3 +85,15 @@ def test_lanes_memory_profile_and_errors(mra):
         mra.mra_loglik_batch_dev(p3, zd, bad)
     assert e.value.status == 1
     np.testing.assert_array_equal(mra.mra_loglik_batch_dev(p3, zd, th[:3]), mra.mra_loglik_batch_dev(p1, zd, th[:3]))
+
+
+def test_optimizer_on_laned_plan(mra):
+    """mra_optimize evaluates its initial simplex and shrink points as one sweep on a laned plan:
+    same evaluations, same decisions, bitwise the same optimum."""
+    import torch
+    x, y, z = synth.uniform_small(6000, seed=43)
+    zd = torch.from_numpy(z).cuda()
+    th0 = (EXP, 1.0, 0.1, 0.05)
+    a = mra.mra_optimize(mra.mra_plan_create(x, y, 4, 4, 16), zd, th0, max_evals=40)
+    b = mra.mra_optimize(mra.mra_plan_create(x, y, 4, 4, 16, theta_lanes=4), zd, th0, max_evals=40)
+    assert tuple(a[0]) == tuple(b[0]) and a[1] == b[1] and a[2] == b[2]
