@@ -120,3 +120,39 @@ def test_shard_assignment_partitions_subtrees():
 def test_atilde_eq1():
     assert abs(mra.atilde_bound_gib(2, 10, 256) - 11.25) < 1e-12
     assert abs(mra.atilde_bound_gib(2, 14, 49) - 13.34) < 0.005
+
+
+def test_ctypes_structs_match_the_header(tmp_path):
+    """The binding's ctypes mirrors of mra_opts / mra_theta / mra_post have the C layout of include/mra.h
+    (field order, offsets, size), checked against gcc's own offsetof."""
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("gcc not available")
+    structs = {"mra_opts": mra._Opts, "mra_theta": mra._Theta, "mra_post": mra._Post}
+    src = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{os.path.join(ROOT, "include", "mra.h")}"',
+           "int main(void) {"]
+    for cname, py in structs.items():
+        src.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
+        for fname, _ in py._fields_:
+            src.append(f'printf("{cname} {fname} %zu\\n", offsetof({cname}, {fname}));')
+    src += ["return 0;", "}"]
+    c = tmp_path / "layout.c"
+    c.write_text("\n".join(src))
+    exe = tmp_path / "layout"
+    subprocess.check_call([gcc, str(c), "-o", str(exe)])
+    got = {}
+    for line in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.splitlines():
+        cname, what, v = line.split()
+        got[(cname, what)] = int(v)
+    for cname, py in structs.items():
+        assert got[(cname, "size")] == ctypes.sizeof(py), cname
+        for fname, _ in py._fields_:
+            assert got[(cname, fname)] == getattr(py, fname).offset, (cname, fname)
+    # and every C field is mirrored (no field missing at the end)
+    hdr = open(os.path.join(ROOT, "include", "mra.h")).read()
+    body = hdr[hdr.index("typedef struct {", hdr.index("Plan options")):hdr.index("} mra_opts;")]
+    cfields = re.findall(r"^\s+(?:int|double|void\*)\s+([a-z_0-9, ]+);", body, re.M)
+    names = [n.strip() for grp in cfields for n in grp.split(",")]
+    assert names == [f for f, _ in mra._Opts._fields_]
