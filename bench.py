@@ -355,12 +355,14 @@ def run_gpu(args, rank, world, local_rank):
             t = mra.mra_kernel_times(plan)
             mra.mra_profile(plan, False)
             kt = ([t[k][0] for k in mra.KERNEL_CLASSES], [t[k][1] for k in mra.KERNEL_CLASSES])
+        timed.last_steps = list(ev)   # per-step device ms of this rank (mean(sd), median)
         return ms, lls, launches, clocks, kt
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     ms, lls, launches, clocks, kt = timed(args.steps, prof=True)
+    step_list = list(timed.last_steps)
     ms_e2e, _, _, _, _ = timed(max(1, min(args.steps, 3)), host=True)
     e2e_steps = max(1, min(args.steps, 3))
     if rank != 0:
@@ -450,6 +452,9 @@ def run_gpu(args, rank, world, local_rank):
                     # a sweep (mra_loglik_batch) copies y once per step, single evaluations once per theta
                     "h2d_bytes_per_step": 8 * w.n * (1 if (ntheta > 1 and world == 1) else ntheta),
                     "d2h_bytes_per_step": 8 * ntheta},
+            "step_ms": {"mean": float(np.mean(step_list)), "sd": float(np.std(step_list, ddof=1)) if len(step_list) > 1
+                        else 0.0, "median": float(np.median(step_list)), "runs": len(step_list),
+                        "note": "rank 0's per-step device times; ms_per_step is the max over ranks of their sums / steps"},
             "gpu_launches": int(launches),
             "kernel_ms": {k: round(kms[k], 3) for k in mra.KERNEL_CLASSES},
             "kernel_launches": {k: int(kcnt[k]) for k in mra.KERNEL_CLASSES},
