@@ -97,3 +97,17 @@ def test_optimizer_on_laned_plan(mra):
     a = mra.mra_optimize(mra.mra_plan_create(x, y, 4, 4, 16), zd, th0, max_evals=40)
     b = mra.mra_optimize(mra.mra_plan_create(x, y, 4, 4, 16, theta_lanes=4), zd, th0, max_evals=40)
     assert tuple(a[0]) == tuple(b[0]) and a[1] == b[1] and a[2] == b[2]
+
+
+def test_lanes_on_streaming_multichunk_plan(mra):
+    """Lanes of a plan that streams its prior per chunk (NEXT-4) and runs many chunks: each lane owns its
+    chunk-sized prior buffer; the sweep equals the resident one-lane plan bitwise."""
+    import torch
+    x, y, z = synth.uniform_small(10000, seed=44, clusters=2)
+    th = _thetas(EXP, 5)
+    ref = mra.mra_plan_create(x, y, 5, 4, 16, stream_prior=-1)
+    par = mra.mra_plan_create(x, y, 5, 4, 16, stream_prior=1, mem_budget_gb=0.008, theta_lanes=2)
+    info = mra.mra_plan_memory(par)
+    assert info["streams_prior"] and info["chunk_regions"] < 4 ** (info["chunk_level"] - 1)
+    zd = torch.from_numpy(z).cuda()
+    np.testing.assert_array_equal(mra.mra_loglik_batch_dev(ref, zd, th), mra.mra_loglik_batch_dev(par, zd, th))
