@@ -1278,10 +1278,11 @@ static mra_status ensure_post(mra_plan* P) {
     return MRA_OK;
 }
 
-// NaN / Inf scan of a host array (OpenMP: 47M values in a few ms)
+// NaN / Inf scan of a host array (OpenMP above 4M values: 47M in a few ms; below, waking the thread
+// team costs more than the scan)
 static bool all_finite(const double* y, uint64_t n) {
     long long bad = 0;
-#pragma omp parallel for schedule(static) reduction(+ : bad)
+#pragma omp parallel for schedule(static) reduction(+ : bad) if (n > (4u << 20))
     for (long long i = 0; i < (long long)n; i++) bad += !std::isfinite(y[i]);
     return bad == 0;
 }
