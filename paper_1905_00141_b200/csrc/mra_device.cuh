@@ -99,27 +99,40 @@ __device__ __forceinline__ double2 ldpt(const double* pts, int i) {
     return reinterpret_cast<const double2*>(pts)[i];
 }
 
-// e^{-x} for x >= 0 with a short dependency chain (fp64 latency, not throughput, bounds the fused
-// covariance generation: libm exp is ~204 dependent cycles on B200, tools/bench_fp64ops.cu):
-// x = k ln2 + r, |r| <= ln2/2, e^{-r} by its degree-12 Taylor polynomial in Estrin form (truncation
-// < 2e-16 relative), 2^{-k} by exponent construction. Max error 2.1 ulp over [0, 708) (checked
-// against libm on 2e7 points); e^{-x} < 1e-307 is flushed to 0.
+// e^{-x} for x >= 0 with a short dependency chain (libm exp is ~204 dependent cycles on B200,
+// tools/bench_fp64ops.cu); e^{-x} < 1e-307 is flushed to 0.
+//   e^{-x} = 2^{-e} 2^{-j/32} e^{-r},  k = rint(32 x / ln 2) = 32 e + j,  r = x - k ln2/32 in [-ln2/64, ln2/64]
+// (Cody-Waite split of ln2/32: the high part has 32 significant bits, exact for k < 2^21); e^{-r} by its
+// degree-6 Taylor polynomial (truncation < 3.5e-18) as e^{-r} - 1; 2^{-j/32} from a 32-entry table
+// (L1-resident, read with __ldg). About 16 fp64 operations (the degree-12 form without the table took
+// 23); max error measured by tools/check_exp.cu.
+static __device__ const double g_exp2m32[32] = {
+    1.0, 0.9785720620877001, 0.9576032806985737, 0.93708381705515,
+    0.9170040432046712, 0.8973545375015536, 0.8781260801866497, 0.859309649061239,
+    0.8408964152537145, 0.8228777390769825, 0.8052451659746271, 0.7879904225539432,
+    0.7711054127039704, 0.7545822137967114, 0.7384130729697497, 0.7225904034885233,
+    0.7071067811865476, 0.691954940981916, 0.6771277734684463, 0.6626183215798707,
+    0.6484197773255048, 0.6345254785958666, 0.620928906036742, 0.6076236799902345,
+    0.5946035575013605, 0.5818624293887887, 0.5693943173783458, 0.5571933712979462,
+    0.5452538663326288, 0.5335702003384118, 0.5221368912137069, 0.5109485743270583};
 __device__ __forceinline__ double exp_neg(double x) {
     if (!(x < 708.0)) return 0.0;
-    const double L2E = 1.4426950408889634074, LN2_HI = 6.93147180369123816490e-01,
-                 LN2_LO = 1.90821492927058770002e-10, MAGIC = 6755399441055744.0;
-    const double kd = __dadd_rn(__dmul_rn(x, L2E), MAGIC) - MAGIC;   // rint(x log2 e)
-    double r = fma(-kd, LN2_HI, x);
-    r = fma(-kd, LN2_LO, r);
-    const double s = -r, s2 = s * s, s4 = s2 * s2, s8 = s4 * s4;
-    const double p01 = 1.0 + s, p23 = fma(1.0 / 6, s, 0.5), p45 = fma(1.0 / 120, s, 1.0 / 24),
-                 p67 = fma(1.0 / 5040, s, 1.0 / 720), p89 = fma(1.0 / 362880, s, 1.0 / 40320),
-                 pab = fma(1.0 / 39916800, s, 1.0 / 3628800);
-    const double q0 = fma(p23, s2, p01), q1 = fma(p67, s2, p45), q2 = fma(pab, s2, p89);
-    const double r0 = fma(q1, s4, q0), r1 = fma(1.0 / 479001600, s4, q2);
-    const double p = fma(r1, s8, r0);
+    const double K32 = 46.166241308446828384,                          // 32 / ln 2
+        LN2_32_HI = 6.93147180369123816490e-01 / 32, LN2_32_LO = 1.90821492927058770002e-10 / 32,
+        MAGIC = 6755399441055744.0;
+    const double kd = __dadd_rn(__dmul_rn(x, K32), MAGIC) - MAGIC;   // rint(32 x / ln 2)
+    double s = fma(kd, LN2_32_HI, -x);                               // s = -r
+    s = fma(kd, LN2_32_LO, s);
+    // w = e^s - 1 = s + s^2 (1/2 + s/6 + s^2 (1/24 + s/120 + s^2/720)); the result t (1 + w) is rounded
+    // once, so only t's own rounding and that final fma reach the last bits
+    const double s2 = s * s;
+    const double a = fma(1.0 / 6, s, 0.5), b = fma(1.0 / 120, s, 1.0 / 24);
+    const double c = fma(1.0 / 720, s2, b);
+    const double u = fma(c, s2, a);
+    const double w = fma(u, s2, s);
     const int k = (int)kd;
-    return p * __hiloint2double((1023 - k) << 20, 0);
+    const double t = __ldg(g_exp2m32 + (k & 31));
+    return fma(t, w, t) * __hiloint2double((1023 - (k >> 5)) << 20, 0);
 }
 
 // sqrt(q) from the single-precision MUFU reciprocal square root, one fp64 Newton step on 1/sqrt and one
