@@ -213,7 +213,7 @@ __device__ __forceinline__ void load_tile_async(double* s, const Op& op, int r0,
         }
     } else if (KIND == MEMT) {
         if (al16) {
-#pragma unroll
+#pragma unroll 2
             for (int i = 0; i < 32 * TK / NT; i++) {
                 const int e = tid + NT * i, kk = e >> 5, row = (e & 31) * 2;
                 const int ok = (kk < nk) ? min(2, max(0, nr - row)) : 0;
