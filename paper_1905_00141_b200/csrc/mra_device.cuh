@@ -339,7 +339,9 @@ __device__ __forceinline__ void tile_pipeline(double (&acc)[MI][4][2], const Gem
     cp_async_wait<0>();
 }
 
-template <int KA0, int KB0, int KA1, int KB1>
+// EPI = 1: the epilogue can add a covariance initial value (ci_cov); only the instantiations that need it
+// carry that code (it costs the other GEMMs registers: at 128 the MEMT x MEMT one would spill)
+template <int KA0, int KB0, int KA1, int KB1, int EPI>
 __device__ __noinline__ void cta_gemm_impl(double* smem) {
     const GemmDesc& d = *gemm_desc(smem);
     const int Mr = d.Mr, Nc = d.Nc, lower = d.lower, K0 = d.K0, K1 = d.K1;
@@ -391,7 +393,8 @@ __device__ __noinline__ void cta_gemm_impl(double* smem) {
                         }
                     }
                 }
-            if (ci.kind == 2) {
+            if (EPI == 0 && ci.kind == 2) __trap();   // a covariance init needs the EPI = 1 instantiation
+            if (EPI == 1 && ci.kind == 2) {
                 const CovP cpl = d.cp;
                 // covariance initial value, added by the thread that stored the element (4 independent
                 // fp64 sqrt/exp chains in flight per thread)
@@ -413,7 +416,7 @@ __device__ __noinline__ void cta_gemm_impl(double* smem) {
 // C[Mr x Nc] = init + alpha * (A0 B0^T [K0] + A1 B1^T [K1]); lower != 0 -> only i >= j written.
 // In-place use (C aliasing the operands / init) is safe when every output tile reads only its own
 // rows (A side) / columns (B side) of the aliased region -- see DESIGN.md §5.
-template <int KA0, int KB0, int KA1, int KB1>
+template <int KA0, int KB0, int KA1, int KB1, int EPI = 0>
 __device__ __forceinline__ void cta_gemm(int Mr, int Nc, int lower, const Op& A0, const Op& B0, int K0,
                                          const Op& A1, const Op& B1, int K1, const CInit& ci, double alpha,
                                          double* C, long long ldc, const CovP& cp, double* smem) {
@@ -425,7 +428,7 @@ __device__ __forceinline__ void cta_gemm(int Mr, int Nc, int lower, const Op& A0
         d->Mr = Mr; d->Nc = Nc; d->lower = lower; d->K0 = K0; d->K1 = K1;
     }
     __syncthreads();
-    cta_gemm_impl<KA0, KB0, KA1, KB1>(smem);
+    cta_gemm_impl<KA0, KB0, KA1, KB1, EPI>(smem);
 }
 
 // ---------------------------------------------------------------- small factor blocks

@@ -127,7 +127,7 @@ k_bottom(TreeParams tp, long long g_first, long long g_count, double* out, long 
             PHASE_ADD(0, c0);
             PHASE_MARK(c1);
             // Sigma_j = C(S,S) + tau2 I - V V^T  (nugget on the observation diagonal only, reading R2)
-            cta_gemm<MEMN, MEMN, MEMN, MEMN>(n, n, 1, op_mem(Gc, L.ldG), op_mem(Gc, L.ldG), Pg, op_mem(Gc, L.ldG),
+            cta_gemm<MEMN, MEMN, MEMN, MEMN, 1>(n, n, 1, op_mem(Gc, L.ldG), op_mem(Gc, L.ldG), Pg, op_mem(Gc, L.ldG),
                                              op_mem(Gc, L.ldG), 0, ci_cov(pts, pts, tp.tau2), -1.0, S,
                                              L.ldS, cp, smem);
             PHASE_ADD(1, c1);
@@ -235,7 +235,7 @@ k_smooth(TreeParams tp, const double* muhat, const long long* perm, double* smoo
         if (n == 0) continue;
         const double* pts = tp.pxy + 2 * o0;
         point_chain(tp, m, t, n, pts, G, L.ldG, cp, smem);
-        cta_gemm<MEMN, MEMN, MEMN, MEMN>(n, n, 1, op_mem(G, L.ldG), op_mem(G, L.ldG), Pg, op_mem(G, L.ldG),
+        cta_gemm<MEMN, MEMN, MEMN, MEMN, 1>(n, n, 1, op_mem(G, L.ldG), op_mem(G, L.ldG), Pg, op_mem(G, L.ldG),
                                          op_mem(G, L.ldG), 0, ci_cov(pts, pts, tp.tau2), -1.0, S, L.ldS, cp,
                                          smem);
         chol_blocked(S, n, L.ldS, D, cp, smem);
@@ -328,7 +328,7 @@ k_predict(TreeParams tp, PredParams pp, double* ws, WsLayout L, unsigned long lo
             point_chain(tp, m, t, n, pts, G, L.ldG, cp, smem);
             for (int i = threadIdx.x; i < n; i += NT) G[(long long)i * L.ldG + Pg] = tp.zs[o0 + i];
             __syncthreads();
-            cta_gemm<MEMN, MEMN, MEMN, MEMN>(n, n, 1, op_mem(G, L.ldG), op_mem(G, L.ldG), Pg, op_mem(G, L.ldG),
+            cta_gemm<MEMN, MEMN, MEMN, MEMN, 1>(n, n, 1, op_mem(G, L.ldG), op_mem(G, L.ldG), Pg, op_mem(G, L.ldG),
                                              op_mem(G, L.ldG), 0, ci_cov(pts, pts, tp.tau2), -1.0, S, L.ldS, cp,
                                              smem);
             chol_blocked(S, n, L.ldS, D, cp, smem);
@@ -348,7 +348,7 @@ k_predict(TreeParams tp, PredParams pp, double* ws, WsLayout L, unsigned long lo
             point_chain(tp, m, t, nt, qp, Q, L.ldG, cp, smem);   // v(p), rows of Q
             if (n > 0) {
                 // E = L^{-1} C_M(S, P) = L^{-1} C(S, P) - G_V V(P)^T   (G already holds L^{-1} V)
-                cta_gemm<MEMN, MEMN, MEMN, MEMN>(n, nt, 0, op_mem(G, L.ldG), op_mem(Q, L.ldG), 0, op_mem(G, 0),
+                cta_gemm<MEMN, MEMN, MEMN, MEMN, 1>(n, nt, 0, op_mem(G, L.ldG), op_mem(Q, L.ldG), 0, op_mem(G, 0),
                                                  op_mem(G, 0), 0, ci_cov(pts, qp, 0.0), 1.0, E, 64, cp, smem);
                 fwd_subst(S, n, L.ldS, D, E, nt, 64, cp, smem);
                 if (Pg > 0)

@@ -81,7 +81,7 @@ k_wide_sigma(TreeParams tp, WideParams wp, const int4* tasks, long long ntask, u
         double* C = wp.S + wp.S_off[l] + 64LL * i * ld + 64LL * k;
         const double* Gi = wp.G + (o - wp.G_base + 64LL * i) * wp.ldG;
         const double* Gk = wp.G + (o - wp.G_base + 64LL * k) * wp.ldG;
-        cta_gemm<MEMN, MEMN, MEMN, MEMN>(min(64, n - 64 * i), min(64, n - 64 * k), i == k, op_mem(Gi, wp.ldG),
+        cta_gemm<MEMN, MEMN, MEMN, MEMN, 1>(min(64, n - 64 * i), min(64, n - 64 * k), i == k, op_mem(Gi, wp.ldG),
                                          op_mem(Gk, wp.ldG), Pg, op_mem(Gi, 0), op_mem(Gi, 0), 0,
                                          ci_cov(tp.pxy + 2 * (o + 64LL * i), tp.pxy + 2 * (o + 64LL * k),
                                                 i == k ? tp.tau2 : 0.0),
