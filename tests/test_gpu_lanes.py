@@ -111,3 +111,27 @@ def test_lanes_on_streaming_multichunk_plan(mra):
     assert info["streams_prior"] and info["chunk_regions"] < 4 ** (info["chunk_level"] - 1)
     zd = torch.from_numpy(z).cuda()
     np.testing.assert_array_equal(mra.mra_loglik_batch_dev(ref, zd, th), mra.mra_loglik_batch_dev(par, zd, th))
+
+
+def test_numeric_failure_is_reported_and_plan_recovers(mra):
+    """A parameter set whose leaf covariance is numerically singular (50 copies of one location and a
+    nugget of 1e-30) makes a Cholesky pivot non-positive: MRA_E_NUMERIC naming the region, in single
+    evaluations and inside a laned sweep; the plan evaluates the next parameter set correctly."""
+    import torch
+    x, y, z = synth.uniform_small(3000, seed=45)
+    x[:50] = 0.3141
+    y[:50] = 0.2718
+    good = (EXP, 1.0, 0.1, 0.05)
+    bad = (EXP, 1.0, 0.1, 1e-30)
+    ref = mra.mra_loglik(mra.mra_plan_create(x, y, 4, 4, 16), z, good)["loglik"]
+    zd = torch.from_numpy(z).cuda()
+    for lanes in (1, 3):
+        p = mra.mra_plan_create(x, y, 4, 4, 16, theta_lanes=lanes)
+        with pytest.raises(mra.MraError) as e:
+            mra.mra_loglik_dev(p, zd, bad)
+        assert e.value.status == 4 and "Cholesky" in str(e.value)
+        with pytest.raises(mra.MraError) as e:
+            mra.mra_loglik_batch_dev(p, zd, [good, bad, good, good])
+        assert e.value.status == 4
+        assert mra.mra_loglik_dev(p, zd, good)["loglik"] == ref
+        np.testing.assert_array_equal(mra.mra_loglik_batch_dev(p, zd, [good, good, good]), [ref, ref, ref])
