@@ -976,9 +976,10 @@ extern "C" mra_status mra_kernel_times(const mra_plan* P, double* ms, uint64_t* 
 
 // diagnostics of -DMRA_PHASE_TIMING builds (zeros otherwise): CTA-cycles per bottom-kernel phase
 extern "C" void mra_debug_phase_cycles(uint64_t* out32, int reset) {
-    unsigned long long v[32];
+    unsigned long long v[32], w[32];
     phase_cycles(v, reset != 0);
-    for (int i = 0; i < 32; i++) out32[i] = v[i];
+    phase_cycles_unit(w, reset != 0);   // the GEMM unit's kernels count into their own copy
+    for (int i = 0; i < 32; i++) out32[i] = v[i] + w[i];
 }
 
 extern "C" mra_status mra_plan_memory(const mra_plan* P, int* streams_prior, int* chunk_level,

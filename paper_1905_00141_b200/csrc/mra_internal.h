@@ -112,6 +112,7 @@ cudaError_t launch_wide_main(int phase, const TreeParams& tp, const WideParams& 
 cudaError_t launch_prior_unit(const TreeParams& tp, int m, long long t_first, long long t_count, int grid, double* ws,
                               long long ws_stride, unsigned long long* counter, cudaStream_t st);
 int unit_ctas_per_sm();
+void phase_cycles_unit(unsigned long long* out32, bool reset);
 int wide_mtile_resident();
 cudaError_t launch_wide_mtile(const TreeParams& tp, const WideParams& wp, long long g_first, long long g_count,
                               double* out, long long out_first, int q, const int4* tasks, long long ntask, int grid,

@@ -740,6 +740,15 @@ int unit_ctas_per_sm() {
     return std::max(1, g_gemm_resident[8] / nsm);
 }
 
+// -DMRA_PHASE_TIMING diagnostics of this unit's kernels (g_phase_cycles is per translation unit)
+void phase_cycles_unit(unsigned long long* out32, bool reset) {
+    cudaMemcpyFromSymbol(out32, g_phase_cycles, sizeof(unsigned long long) * 32);
+    if (reset) {
+        unsigned long long z[32] = {0};
+        cudaMemcpyToSymbol(g_phase_cycles, z, sizeof z);
+    }
+}
+
 // resident CTAs of the merge tile dataflow (the host sizes its look-ahead D1 with it)
 int wide_mtile_resident() {
     gemm_set_attrs();
