@@ -284,6 +284,8 @@ def test_device_plan_build_matches_host(mra, n, M, J, r, cl):
     (700, 3, 4, 3, EXP, 2, (-5.0, 5.0, 10.0, 11.0)),     # r_hat = 3, translated anisotropic domain, empty leaves
     (40, 2, 4, 4, EXP, 0, (0.0, 1.0, 0.0, 1.0)),         # ~10 observations per leaf
     (5, 2, 2, 4, MAT, 0, (0.0, 1.0, 0.0, 1.0)),          # 5 observations, most leaves empty or single
+    (4000, 12, 2, 9, EXP, 3, (0.0, 1.0, 0.0, 1.0)),      # deep tree: 11 ancestor levels, 2,048 mostly empty leaves
+    (2000, 7, 4, 16, EXP, 0, (0.0, 1.0, 0.0, 1.0)),      # 4,096 leaves for 2,000 observations
 ])
 def test_edge_cases(mra, n, M, J, r, cov, cl, dom):
     """Degenerate knot counts (r_hat 1..3), extreme aspect ratios, tiny leaves, nearly-empty trees:
