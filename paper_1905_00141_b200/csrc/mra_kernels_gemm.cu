@@ -577,14 +577,15 @@ k_prior(TreeParams tp, int m, long long t_first, long long nitems, double* ws, l
 // --------------------------------------------------------------------------- merge
 __global__ void __launch_bounds__(NT, MRA_MINB)
 k_merge(TreeParams tp, int m, long long t_first, long long t_count, const double* child_out, long long child_first,
-        double* out, long long out_first, int q, double* ws, long long ws_stride, unsigned long long* counter) {
+        double* out, long long out_first, int q, double* ws, long long ws_stride, unsigned long long* counter,
+        int presummed) {
     double* smem = dyn_smem();
     const CovP cp = to_covp(tp.cp);
     const int J = tp.J, rh = tp.rh;
     const int qc = m * rh + 1;
     const int ldA = qc + (qc & 1);   // even leading dimension -> 16-byte cp.async rows
-    double* A = ws + (long long)blockIdx.x * ws_stride;
-    double* F = A + (long long)qc * ldA;
+    double* Aws = ws + (long long)blockIdx.x * ws_stride;
+    double* F = Aws + (long long)qc * ldA;
     double* Li = F + (long long)q * rh;
     FacSmem f = fac_view(smem);
     const long long qc2 = (long long)qc * qc;
@@ -594,6 +595,10 @@ k_merge(TreeParams tp, int m, long long t_first, long long t_count, const double
         if (threadIdx.x == 0) *f.bad = 0;
         const long long t = t_first + it;
         const double* C0 = child_out + (t * J - child_first) * qc2;
+        // presummed: k_merge_sum has already accumulated Atilde into the first child's block (ld qc)
+        const double* A = presummed ? C0 : Aws;
+        const long long lda = presummed ? qc : ldA;
+        if (!presummed)
         // Atilde = sum of the J children (lower triangle): one warp per row, lanes along the row, U column
         // groups per pass so every lane has U*J independent streaming loads in flight (the children's
         // outputs are read exactly once: evict-first)
@@ -602,7 +607,7 @@ k_merge(TreeParams tp, int m, long long t_first, long long t_count, const double
             const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
             for (int i = warp; i < qc; i += NT / 32) {
                 const double* ci = C0 + (long long)i * qc;
-                double* Ai = A + (long long)i * ldA;
+                double* Ai = Aws + (long long)i * ldA;
                 for (int j0 = 0; j0 <= i; j0 += 32 * U) {
                     double v[U];
 #pragma unroll
@@ -631,7 +636,7 @@ k_merge(TreeParams tp, int m, long long t_first, long long t_count, const double
         }
         __syncthreads();
         double* O = out + (t - out_first) * (long long)q * q;
-        const double ldm = merge_core(A, rh, ldA, O, q, F, Li, tp.err, m, t, cp, smem);
+        const double ldm = merge_core(A, rh, lda, O, q, F, Li, tp.err, m, t, cp, smem);
         const long long id = lvl_first(J, m) + t;
         if (threadIdx.x == 0) {
             const long long c0 = lvl_first(J, m + 1) + t * J;
@@ -641,6 +646,46 @@ k_merge(TreeParams tp, int m, long long t_first, long long t_count, const double
             tp.ureg[id] = O[(long long)(q - 1) * q + q - 1];
         }
         save_post(tp, m, t, q, Li, F);
+    }
+}
+
+// Atilde of every level-m region of [t_first, t_first + t_count), accumulated IN PLACE into its first child's
+// output block (lower triangle, ld qc): a grid-wide streaming pass (one warp per row, U column groups per
+// lane, J evict-first loads each) for the large levels, where the per-region sum inside k_merge left HBM idle
+// while the CTA factored and multiplied. The children's outputs have no other consumer.
+__global__ void __launch_bounds__(256)
+k_merge_sum(int J, int qc, long long t_first, long long t_count, double* child_out, long long child_first) {
+    constexpr int U = 4;
+    const long long qc2 = (long long)qc * qc, rows = t_count * qc;
+    const int lane = threadIdx.x & 31;
+    const long long w0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long r = w0; r < rows; r += nw) {
+        const long long t = t_first + r / qc;
+        const int i = (int)(r % qc);
+        double* c0 = child_out + (t * J - child_first) * qc2 + (long long)i * qc;
+        for (int j0 = 0; j0 <= i; j0 += 32 * U) {
+            double v[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int j = j0 + lane + 32 * u;
+                double sacc = 0.0;
+                if (j <= i) {
+                    const double* p = c0 + j;
+                    if (J == 4) {
+                        const double a0 = __ldcs(p), a1 = __ldcs(p + qc2), a2 = __ldcs(p + 2 * qc2), a3 = __ldcs(p + 3 * qc2);
+                        sacc = (((sacc + a0) + a1) + a2) + a3;
+                    } else {
+                        for (int c = 0; c < J; c++) sacc += __ldcs(p + c * qc2);
+                    }
+                }
+                v[u] = sacc;
+            }
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int j = j0 + lane + 32 * u;
+                if (j <= i) c0[j] = v[u];
+            }
+        }
     }
 }
 
@@ -716,8 +761,21 @@ cudaError_t launch_merge(const TreeParams& tp, int m, long long t_first, long lo
     gemm_set_attrs();
     grid = (int)std::min<long long>({(long long)grid, (long long)g_gemm_resident[8], t_count});
     if (grid < 1) return cudaSuccess;
+    // large levels (several regions per CTA): the child sums as one streaming pass first
+    const int presummed = t_count >= 4LL * grid ? 1 : 0;
+    if (presummed) {
+        int dev = 0, nsm = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        const int qc = m * tp.rh + 1;
+        const long long rows = t_count * qc;
+        const int sg = (int)std::min<long long>((rows + 7) / 8, 8LL * nsm);
+        k_merge_sum<<<sg, 256, 0, st>>>(tp.J, qc, t_first, t_count, const_cast<double*>(child_out), child_first);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
     k_merge<<<grid, NT, gemm_smem_bytes(), st>>>(tp, m, t_first, t_count, child_out, child_first, out, out_first, q, ws,
-                                           ws_stride, counter);
+                                           ws_stride, counter, presummed);
     return cudaGetLastError();
 }
 
