@@ -1029,6 +1029,7 @@ static mra_status check_theta(const mra_theta* th) {
 #define LCHK_K(kind, expr)                                                                   \
     do {                                                                                     \
         size_t ev0_ = 0;                                                                     \
+        const unsigned long long k0_ = g_kernel_launches;                                    \
         if (P->prof) {                                                                       \
             ev0_ = P->ev_used;                                                               \
             cudaEventRecord(take_event(P), P->st);                                           \
@@ -1038,7 +1039,7 @@ static mra_status check_theta(const mra_theta* th) {
             cudaEventRecord(take_event(P), P->st);                                           \
             P->recs.push_back({(kind), ev0_});                                               \
         }                                                                                    \
-        P->launches++;                                                                       \
+        P->launches += g_kernel_launches - k0_;   /* kernels this wrapper actually launched */ \
         if (e_ != cudaSuccess) return fail(MRA_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 #define LCHK(expr) LCHK_K(KIND_OTHER, expr)
@@ -1435,9 +1436,9 @@ extern "C" mra_status mra_predict(mra_plan* P, const double* qx, const double* q
     PredParams pp{};
     pp.qxy = d_qxy; pp.q_off = d_qoff; pp.q_perm = d_qperm; pp.leaves = d_leaves;
     pp.n_leaves = (long long)leaves.size(); pp.muhat = P->muhat; pp.mean = d_mean; pp.var = d_var;
-    P->launches = 0;
+    const unsigned long long k0 = g_kernel_launches;
     PCU(launch_predict(tp, pp, P->pred_grid, P->ws_pred, P->Lp, P->counters, P->st));
-    P->launches++;
+    P->launches = g_kernel_launches - k0;
     PCU(cudaMemcpyAsync(mean, d_mean, 8 * nq, cudaMemcpyDeviceToHost, P->st));
     PCU(cudaMemcpyAsync(var, d_var, 8 * nq, cudaMemcpyDeviceToHost, P->st));
     int h[4];

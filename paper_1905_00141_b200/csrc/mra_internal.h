@@ -137,6 +137,7 @@ cudaError_t plan_gather(const double* x, const double* y, const int* idx, long l
                         cudaStream_t st);
 int smem_bytes();
 int resident_ctas_per_sm();   // engine kernels (k_bottom occupancy)
+extern unsigned long long g_kernel_launches;   // host-side count of every kernel this library launched
 void phase_cycles(unsigned long long* out32, bool reset);   // -DMRA_PHASE_TIMING builds only
 
 }  // namespace mra

@@ -475,6 +475,8 @@ k_wide_covfill(TreeParams tp, WideParams wp, const int4* tasks, long long ntask)
 int smem_bytes() { return SMEM_DBL * (int)sizeof(double); }
 int resident_ctas_per_sm();
 
+unsigned long long g_kernel_launches = 0;
+
 void phase_cycles(unsigned long long* out32, bool reset) {
     cudaMemcpyFromSymbol(out32, g_phase_cycles, sizeof(unsigned long long) * 32);
     if (reset) {
@@ -514,6 +516,7 @@ cudaError_t launch_gather(const double* z, const long long* perm, double* zs, lo
     long long blocks = (N + 255) / 256;
     if (blocks > 4096) blocks = 4096;
     if (blocks < 1) blocks = 1;
+    ++g_kernel_launches;
     k_gather<<<(int)blocks, 256, 0, st>>>(z, perm, zs, N);
     return cudaGetLastError();
 }
@@ -521,6 +524,7 @@ cudaError_t launch_fill(double* p, long long n, double v, cudaStream_t st) {
     long long blocks = (n + 255) / 256;
     if (blocks > 4096) blocks = 4096;
     if (blocks < 1) blocks = 1;
+    ++g_kernel_launches;
     k_fill<<<(int)blocks, 256, 0, st>>>(p, n, v);
     return cudaGetLastError();
 }
@@ -536,6 +540,7 @@ cudaError_t launch_prior(const TreeParams& tp, int m, long long t_first, long lo
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_prior_covfill, CFT, 0);
             cf_grid = (per > 0 ? per : 1) * nsm;
         }
+        ++g_kernel_launches;
         k_prior_covfill<<<(int)std::min<long long>(cf_grid, t_count), CFT, 0, st>>>(tp, m, t_first, t_count);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
@@ -548,10 +553,12 @@ cudaError_t launch_bottom(const TreeParams& tp, long long g_first, long long g_c
     set_attrs();
     grid = clamp_grid(grid, g_count, 1);
     if (grid < 1) return cudaSuccess;
+    ++g_kernel_launches;
     k_bottom<<<grid, NT, smem_bytes(), st>>>(tp, g_first, g_count, out, out_first, q, ws, L, counter);
     return cudaGetLastError();
 }
 cudaError_t launch_final(const TreeParams& tp, double N, double* d_loglik, cudaStream_t st) {
+    ++g_kernel_launches;
     k_final<<<1, 32, 0, st>>>(tp, N, d_loglik);
     return cudaGetLastError();
 }
@@ -559,6 +566,7 @@ cudaError_t launch_mu(const TreeParams& tp, int m, double* muhat, double* mu, lo
                       cudaStream_t st) {
     if (t_count < 1) return cudaSuccess;
     int grid = (int)(t_count < 4096 ? t_count : 4096);
+    ++g_kernel_launches;
     k_mu<<<grid, 64, 0, st>>>(tp, m, muhat, mu, t_first, t_count);
     return cudaGetLastError();
 }
@@ -568,6 +576,7 @@ cudaError_t launch_smooth(const TreeParams& tp, const double* muhat, const long 
     set_attrs();
     grid = clamp_grid(grid, l_count, 3);
     if (grid < 1) return cudaSuccess;
+    ++g_kernel_launches;
     k_smooth<<<grid, NT, smem_bytes(), st>>>(tp, muhat, perm, smooth, ws, L, counter, l_first, l_count);
     return cudaGetLastError();
 }
@@ -593,6 +602,7 @@ cudaError_t launch_wide_main(int phase, const TreeParams& tp, const WideParams& 
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_wide_covfill, CFT, 0);
                 cf_grid = (per > 0 ? per : 1) * nsm;
             }
+            ++g_kernel_launches;
             k_wide_covfill<<<(int)std::min<long long>(cf_grid, ntask), CFT, 0, st>>>(tp, wp, tasks, ntask);
             break;
         }
@@ -610,6 +620,7 @@ cudaError_t launch_predict(const TreeParams& tp, const PredParams& pp, int grid,
     set_attrs();
     grid = clamp_grid(grid, pp.n_leaves, 11);
     if (grid < 1) return cudaSuccess;
+    ++g_kernel_launches;
     k_predict<<<grid, NT, smem_bytes(), st>>>(tp, pp, ws, L, counter);
     return cudaGetLastError();
 }

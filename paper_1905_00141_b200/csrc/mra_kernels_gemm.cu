@@ -725,12 +725,12 @@ cudaError_t launch_wide(int phase, const TreeParams& tp, const WideParams& wp, i
     if (g < 1) return cudaSuccess;
     const int b = gemm_smem_bytes();
     switch (phase) {
-        case 0: k_wide_chain<<<(int)g, NT, b, st>>>(tp, wp, tasks, ntask, counter); break;
-        case 1: k_wide_sigma<<<(int)g, NT, b, st>>>(tp, wp, tasks, ntask, counter); break;
-        case 2: k_wide_update<<<(int)g, NT, b, st>>>(tp, wp, step, tasks, ntask, counter); break;
-        case 3: k_wide_diag<<<(int)g, NT, b, st>>>(tp, wp, step, tasks, ntask, counter); break;
-        case 4: k_wide_panel_x<<<(int)g, NT, b, st>>>(tp, wp, step, tasks, ntask, counter); break;
-        case 5: k_wide_trsm<<<(int)g, NT, b, st>>>(tp, wp, tasks, ntask, counter); break;
+        case 0: ++g_kernel_launches; k_wide_chain<<<(int)g, NT, b, st>>>(tp, wp, tasks, ntask, counter); break;
+        case 1: ++g_kernel_launches; k_wide_sigma<<<(int)g, NT, b, st>>>(tp, wp, tasks, ntask, counter); break;
+        case 2: ++g_kernel_launches; k_wide_update<<<(int)g, NT, b, st>>>(tp, wp, step, tasks, ntask, counter); break;
+        case 3: ++g_kernel_launches; k_wide_diag<<<(int)g, NT, b, st>>>(tp, wp, step, tasks, ntask, counter); break;
+        case 4: ++g_kernel_launches; k_wide_panel_x<<<(int)g, NT, b, st>>>(tp, wp, step, tasks, ntask, counter); break;
+        case 5: ++g_kernel_launches; k_wide_trsm<<<(int)g, NT, b, st>>>(tp, wp, tasks, ntask, counter); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
@@ -750,6 +750,7 @@ cudaError_t launch_wide_mtile(const TreeParams& tp, const WideParams& wp, long l
     cudaError_t e = cudaMemsetAsync(ring.flags, 0, sizeof(int) * 3 * ring.maxg, st);
     if (e == cudaSuccess) e = cudaMemsetAsync(ring.slot_done, 0, sizeof(long long) * ring.ns, st);
     if (e != cudaSuccess) return e;
+    ++g_kernel_launches;
     k_wide_mtile<<<(int)gr, NT, gemm_smem_bytes(), st>>>(tp, wp, g_first, out, out_first, q, tasks, ntask, counter,
                                                         ring);
     return cudaGetLastError();
@@ -770,10 +771,12 @@ cudaError_t launch_merge(const TreeParams& tp, int m, long long t_first, long lo
         const int qc = m * tp.rh + 1;
         const long long rows = t_count * qc;
         const int sg = (int)std::min<long long>((rows + 7) / 8, 8LL * nsm);
+        ++g_kernel_launches;
         k_merge_sum<<<sg, 256, 0, st>>>(tp.J, qc, t_first, t_count, const_cast<double*>(child_out), child_first);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
+    ++g_kernel_launches;
     k_merge<<<grid, NT, gemm_smem_bytes(), st>>>(tp, m, t_first, t_count, child_out, child_first, out, out_first, q, ws,
                                            ws_stride, counter, presummed);
     return cudaGetLastError();
@@ -785,6 +788,7 @@ cudaError_t launch_prior_unit(const TreeParams& tp, int m, long long t_first, lo
     gemm_set_attrs();
     grid = (int)std::min<long long>({(long long)grid, (long long)g_gemm_resident[7], t_count});
     if (grid < 1) return cudaSuccess;
+    ++g_kernel_launches;
     k_prior<<<grid, NT, gemm_smem_bytes(), st>>>(tp, m, t_first, t_count, ws, ws_stride, counter);
     return cudaGetLastError();
 }

@@ -144,12 +144,14 @@ static int grid_for(long long n) {
 
 cudaError_t plan_bbox(const double* x, const double* y, long long n, double* part, int nblk, int* bad,
                       cudaStream_t st) {
+    ++g_kernel_launches;
     k_plan_bbox<<<nblk, PB_NT, 0, st>>>(x, y, n, part, bad);
     return cudaGetLastError();
 }
 
 cudaError_t plan_keys(const double* x, const double* y, long long n, const PlanGeom& pg, int* key, int* idx,
                       unsigned int* cnt, cudaStream_t st) {
+    ++g_kernel_launches;
     k_plan_keys<<<grid_for(n), 256, 0, st>>>(x, y, n, pg, key, idx, cnt);
     return cudaGetLastError();
 }
@@ -158,6 +160,7 @@ int plan_radix_blocks(long long n) { return (int)((n + PB_CHUNK - 1) / PB_CHUNK)
 
 cudaError_t plan_radix_count(const int* key, long long n, int lj, int d, unsigned int* bcnt, cudaStream_t st) {
     const int nblk = plan_radix_blocks(n);
+    ++g_kernel_launches;
     k_plan_radix_count<<<nblk, PB_NT, 0, st>>>(key, n, lj, d, bcnt, nblk);
     return cudaGetLastError();
 }
@@ -165,12 +168,14 @@ cudaError_t plan_radix_count(const int* key, long long n, int lj, int d, unsigne
 cudaError_t plan_radix_scatter(const int* key, const int* idx, long long n, int lj, int d, const unsigned int* boff,
                                int* key2, int* idx2, cudaStream_t st) {
     const int nblk = plan_radix_blocks(n);
+    ++g_kernel_launches;
     k_plan_radix_scatter<<<nblk, PB_NT, 0, st>>>(key, idx, n, lj, d, boff, nblk, key2, idx2);
     return cudaGetLastError();
 }
 
 cudaError_t plan_gather(const double* x, const double* y, const int* idx, long long N, double* pxy, long long* perm,
                         cudaStream_t st) {
+    ++g_kernel_launches;
     k_plan_gather<<<grid_for(N), 256, 0, st>>>(x, y, idx, N, pxy, perm);
     return cudaGetLastError();
 }
