@@ -114,7 +114,8 @@ def flop_model(leaf_sizes, M, J, r):
 
 # --------------------------------------------------------------------------- helpers
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region, plus one NVML
+    sample at its start and one at its end (regions shorter than the sampling period still get samples)."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
@@ -122,8 +123,27 @@ class ClockSampler:
     def __init__(self, index):
         self.index = index
         self.p = None
+        self.extra = []   # NVML samples at start / stop: a timed region shorter than nvidia-smi's period
+
+    def _nvml_sample(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            sm = float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+            mx = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+            names = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+                     "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                     "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                     "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+            self.extra.append((sm, mx, {k for k, bit in names.items() if r & bit}))
+        except Exception:
+            pass
 
     def start(self):
+        self.extra = []
+        self._nvml_sample()
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                        "--format=csv,noheader,nounits", "-lms", "200"],
@@ -132,15 +152,20 @@ class ClockSampler:
             self.p = None
 
     def stop(self):
-        if self.p is None:
-            return None
-        self.p.terminate()
-        try:
-            out, _ = self.p.communicate(timeout=5)
-        except Exception:
-            self.p.kill()
-            return None
+        self._nvml_sample()
+        out = ""
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                self.p.kill()
+                out = ""
         sm, mx, reasons = [], 0.0, set()
+        for s_, m_, r_ in self.extra:
+            sm.append(s_)
+            mx = max(mx, m_)
+            reasons |= r_
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in out.strip().splitlines():
             f = [x.strip() for x in line.split(",")]

@@ -900,6 +900,12 @@ extern "C" mra_status mra_plan_create(const double* x, const double* y, uint64_t
         TRY(cp(P->leaf_off_d, P->leaf_off.data(), 8 * (P->nleaf + 1)));
         if (P->nint) TRY(cp(P->kxy_d, kxy.data(), 16 * P->nint * P->rh));
     }
+    // the copy stream / event of the host-y entry points (created here, not inside the first timed call)
+    if (cudaStreamCreateWithFlags(&P->cst, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&P->cev, cudaEventDisableTiming) != cudaSuccess) {
+        mra_plan_destroy(P);
+        return fail(MRA_E_CUDA, "copy stream / event creation failed");
+    }
     P->n_lanes = std::max(1, std::min(o.theta_lanes, 16));
     if (P->world > 1) P->n_lanes = 1;
     TRY(size_device(P, o.mem_budget_gb, o.stream_prior));
