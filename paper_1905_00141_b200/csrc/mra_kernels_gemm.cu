@@ -274,8 +274,10 @@ __device__ __forceinline__ void wide_diag_blk(const TreeParams& tp, const WidePa
     if (threadIdx.x == 0) wp.lblk[wp.D_off[l] / 4096 + s] = ldet;
 }
 
-// diagonal block of step s for every leaf with more than s blocks: L_ss, D_s = L_ss^{-1}, log-det
-__global__ void __launch_bounds__(NT, MRA_MINB)
+// diagonal block of step s for every leaf with more than s blocks: L_ss, D_s = L_ss^{-1}, log-det.
+// No GEMM here: the 42 KB factor view and 96 registers let FIVE CTAs share an SM (factor class 180 -> 174 ms
+// on C3), one more latency-bound factorization in flight than the GEMM kernels' four
+__global__ void __launch_bounds__(NT, 5)
 k_wide_diag(TreeParams tp, WideParams wp, int s, const int4* tasks, long long ntask, unsigned long long* counter) {
     double* smem = dyn_smem();
     for (;;) {
