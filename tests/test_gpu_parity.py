@@ -315,3 +315,16 @@ def test_nonfinite_inputs_are_arg_errors(mra):
         mra.mra_loglik(p, z2, (EXP, 1.0, 0.1, 0.05))
     assert e.value.status == 1
     p.close()
+
+
+def test_input_order_does_not_change_the_result(mra):
+    """The plan sorts observations by leaf (stable on the input index): permuting the input permutes
+    the smoothed values and leaves log L unchanged up to the within-leaf summation order."""
+    x, y, z = synth.uniform_small(6000, seed=46, clusters=2)
+    theta = (EXP, 1.0, 0.1, 0.05)
+    a = mra.mra_loglik(mra.mra_plan_create(x, y, 5, 4, 16), z, theta, posterior=True)
+    perm = np.random.default_rng(0).permutation(len(x))
+    b = mra.mra_loglik(mra.mra_plan_create(x[perm], y[perm], 5, 4, 16), z[perm], theta, posterior=True)
+    assert abs(a["loglik"] - b["loglik"]) <= 1e-12 * abs(a["loglik"])
+    np.testing.assert_allclose(b["smooth"], a["smooth"][perm], rtol=1e-10, atol=1e-12)
+    np.testing.assert_allclose(b["mu"], a["mu"], rtol=1e-9, atol=1e-12)
