@@ -328,3 +328,24 @@ def test_input_order_does_not_change_the_result(mra):
     assert abs(a["loglik"] - b["loglik"]) <= 1e-12 * abs(a["loglik"])
     np.testing.assert_allclose(b["smooth"], a["smooth"][perm], rtol=1e-10, atol=1e-12)
     np.testing.assert_allclose(b["mu"], a["mu"], rtol=1e-9, atol=1e-12)
+
+
+def test_closed_form_invariances(mra):
+    """Closed forms the MRA likelihood obeys exactly: scaling sigma2 and tau2 by c scales
+    Sigma_MRA + tau2 I by c, so d' = d + N log c and u' = u / c; scaling the coordinates and rho by s
+    leaves every covariance, the partition and the knots (relative to the bounding box) unchanged."""
+    x, y, z = synth.uniform_small(5000, seed=47, clusters=2)
+    p = mra.mra_plan_create(x, y, 5, 4, 16)
+    a = mra.mra_loglik(p, z, (EXP, 1.3, 0.12, 0.04), posterior=True)
+    c = 3.7
+    b = mra.mra_loglik(p, z, (EXP, 1.3 * c, 0.12, 0.04 * c), posterior=True)
+    N = p.n_retained
+    assert abs(b["d"] - (a["d"] + N * np.log(c))) <= 1e-10 * abs(b["d"])
+    assert abs(b["u"] - a["u"] / c) <= 1e-10 * abs(b["u"])
+    np.testing.assert_allclose(b["smooth"], a["smooth"], rtol=1e-9, atol=1e-12)   # E[X|y] is scale-free
+    s = 8.0   # a power of two: the scaled coordinates and knots are exact
+    q = mra.mra_plan_create(x * s, y * s, 5, 4, 16)
+    for cov in (EXP, MAT):
+        la = mra.mra_loglik(p, z, (cov, 1.3, 0.12, 0.04))["loglik"]
+        lb = mra.mra_loglik(q, z, (cov, 1.3, 0.12 * s, 0.04))["loglik"]
+        assert abs(la - lb) <= 1e-12 * abs(la)
