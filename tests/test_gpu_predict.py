@@ -80,3 +80,18 @@ def test_predict_C1_full_size(mra):
     """C1 at full size (131,072 observations, M = 6, r_hat = 36): 3,000 random queries + observations."""
     w = synth.make("C1")
     _check(mra, w.x, w.y, w.z, w.M, w.J, w.r, w.thetas[0], k=3000, seed=1)
+
+
+def test_prediction_at_observations_equals_smoothing(mra):
+    """Two independent GPU paths to the same quantity: mra_predict at the observed locations (k_predict:
+    query basis + back substitution) and the smoothed values of the evaluation (k_smooth): E[X(s_i) | y]."""
+    x, y, z = synth.uniform_small(4000, seed=48, clusters=2)
+    theta = (0, 1.0, 0.1, 0.05)
+    for wide in (0, -1):
+        p = mra.mra_plan_create(x, y, 5, 4, 16, wide=wide)
+        post = mra.mra_loglik(p, z, theta, posterior=True)
+        mean, var = mra.mra_predict(p, x, y)
+        ok = ~np.isnan(post["smooth"])
+        assert ok.sum() == p.n_retained
+        np.testing.assert_allclose(mean[ok], post["smooth"][ok], rtol=1e-9, atol=1e-11)
+        assert np.all(var[ok] >= -1e-12) and np.all(var[ok] <= 1.0 + 1e-12)
