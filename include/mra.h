@@ -36,7 +36,8 @@ typedef enum {
     MRA_E_STRUCT = 3,   /* degenerate bounding box, or every observation eliminated      */
     MRA_E_NUMERIC = 4,  /* a Cholesky factorization failed (not positive definite)       */
     MRA_E_CUDA = 5,     /* CUDA runtime error / no device                                  */
-    MRA_E_OOM = 6       /* device allocation failed                                        */
+    MRA_E_OOM = 6,      /* device (or host) allocation failed                              */
+    MRA_E_NCCL = 7      /* NCCL library missing, communicator setup or a collective failed */
 } mra_status;
 
 typedef enum {
@@ -84,6 +85,23 @@ typedef struct {
                          1/k of the memory budget, sharing the partition and task lists), and
                          mra_loglik_batch* evaluates k parameter sets concurrently, so the phases'
                          tails and small launches of one theta are filled by another's work        */
+    /* --- appended in round 2 (the fields above keep their offsets) --- */
+    const void* nccl_id;  /* NULL = no in-library collective (world > 1 then needs the _shard / _finish
+                         pair and a caller-side reduce). Otherwise the 128-byte ncclUniqueId every rank
+                         of `world` received from rank 0 (mra_nccl_unique_id): the plan creates its own
+                         NCCL communicator (rank, world) on `device`, and mra_loglik / mra_loglik_dev /
+                         mra_loglik_batch* / mra_optimize / mra_predict run the sharded evaluation with
+                         the exchange step inside the library (PAPER.md:460-462,
+                         477-479): ncclBroadcast of the above-shard prior rows from rank 0, ncclReduce
+                         (sum) of the packed shard-root outputs to rank 0, rank 0 merges the levels above
+                         the shard level, ncclBroadcast of log L (every rank returns it) and of the
+                         above-shard posterior means; posterior outputs are completed on every rank by
+                         an all-reduce. Every rank must make the same calls in the same order. With
+                         world == 1 the same sharded schedule runs on one rank (a test of the path).  */
+    void* (*dalloc)(size_t bytes, int device, void* stream);   /* device allocator hook (e.g. torch's
+                         caching allocator); NULL = cudaMalloc. Every device buffer the plan owns or
+                         uses temporarily is taken from it; returns NULL on failure (-> MRA_E_OOM)  */
+    void (*dfree)(void* ptr, int device, void* stream);        /* its release; required with dalloc    */
 } mra_opts;
 
 /* Posterior state requested from an evaluation; any pointer may be NULL. */
@@ -162,14 +180,17 @@ mra_status mra_predict(mra_plan* plan, const double* qx, const double* qy, uint6
 mra_status mra_optimize(mra_plan* plan, const double* d_y, mra_theta* theta, const double* lower,
                         const double* upper, int max_evals, double tol, double* best_loglik, int* n_evals);
 
-/* Multi-GPU subtree sharding, one process per GPU:
- *   mra_shard_size(plan)          -> doubles in the exchange buffer (same on every rank)
+/* Multi-GPU subtree sharding, one process per GPU, with the exchange done by the caller
+ * (plans without opts.nccl_id; with it, mra_loglik* do all of this inside the library):
+ *   mra_shard_size(plan)          -> doubles in the exchange buffer (same on every rank): per level-s
+ *        region the lower triangle of its q x q augmented output, packed row by row (i(i+1)/2 + j),
+ *        then the regions' d, then u, then one error count (> 0: a Cholesky failed on some rank)
  *   mra_loglik_shard(plan, d_y, theta, d_xbuf)
  *        evaluates this rank's subtrees and writes their shard-root outputs into the
  *        zero-initialised DEVICE buffer d_xbuf (slots of other ranks stay zero);
  *   <the caller sum-reduces d_xbuf to rank 0, e.g. ncclReduce / torch.distributed.reduce>
  *   mra_loglik_finish(plan, theta, d_xbuf, loglik)   (rank 0) merges the levels above the
- *        shard level and returns log L. */
+ *        shard level and returns log L (MRA_E_NUMERIC if the reduced error count is > 0). */
 uint64_t mra_shard_size(const mra_plan* plan);
 mra_status mra_loglik_shard(mra_plan* plan, const double* d_y, const mra_theta* theta,
                             double* d_xbuf);
@@ -235,6 +256,11 @@ mra_status mra_kernel_times(const mra_plan* plan, double* ms, uint64_t* launches
 uint64_t mra_last_launches(const mra_plan* plan);
 
 void mra_plan_destroy(mra_plan* plan);
+
+/* A fresh ncclUniqueId (128 bytes written to id_out), to be created on rank 0 and sent to every rank
+ * (e.g. with torch.distributed.broadcast_object_list) before mra_plan_create with opts.nccl_id.
+ * MRA_E_NCCL if no NCCL library can be loaded (libnccl.so.2, or the path in $MRA_NCCL_LIB). */
+mra_status mra_nccl_unique_id(void* id_out);
 
 /* Thread-local text of the last error ("" if none). */
 const char* mra_last_error(void);

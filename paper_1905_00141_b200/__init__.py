@@ -40,12 +40,17 @@ class _Theta(ctypes.Structure):
                 ("tau2", ctypes.c_double)]
 
 
+_DALLOC = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p)
+_DFREE = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p)
+
+
 class _Opts(ctypes.Structure):
     _fields_ = [("offset", ctypes.c_double), ("xscale", ctypes.c_double), ("yscale", ctypes.c_double),
                 ("device", ctypes.c_int), ("stream", ctypes.c_void_p), ("rank", ctypes.c_int),
                 ("world", ctypes.c_int), ("shard_level", ctypes.c_int), ("mem_budget_gb", ctypes.c_double),
                 ("wide", ctypes.c_int), ("host_plan", ctypes.c_int), ("stream_prior", ctypes.c_int),
-                ("theta_lanes", ctypes.c_int)]
+                ("theta_lanes", ctypes.c_int), ("nccl_id", ctypes.c_void_p), ("dalloc", _DALLOC),
+                ("dfree", _DFREE)]
 
 
 class _Post(ctypes.Structure):
@@ -57,7 +62,8 @@ _lib = None
 EXPORTS = ["mra_plan_create", "mra_loglik", "mra_loglik_dev", "mra_loglik_batch_dev", "mra_loglik_batch", "mra_predict", "mra_optimize", "mra_shard_size",
            "mra_loglik_shard", "mra_loglik_finish", "mra_mutop_size", "mra_loglik_shard_post",
            "mra_loglik_finish_post", "mra_posterior_shard", "mra_plan_info", "mra_plan_layout", "mra_plan_shards", "mra_plan_memory",
-           "mra_profile", "mra_kernel_times", "mra_last_launches", "mra_plan_destroy", "mra_last_error"]
+           "mra_profile", "mra_kernel_times", "mra_last_launches", "mra_plan_destroy", "mra_last_error",
+           "mra_nccl_unique_id"]
 
 
 def load_library(path: str = LIB_PATH):
@@ -123,6 +129,8 @@ def load_library(path: str = LIB_PATH):
     lib.mra_plan_destroy.argtypes = [P]
     lib.mra_last_error.restype = ctypes.c_char_p
     lib.mra_last_error.argtypes = []
+    lib.mra_nccl_unique_id.restype = ctypes.c_int
+    lib.mra_nccl_unique_id.argtypes = [P]
     _lib = lib
     return lib
 
@@ -152,8 +160,9 @@ def _stream_ptr(stream):
 class PlanHandle:
     """Owning handle of an mra_plan (destroyed on close / garbage collection)."""
 
-    def __init__(self, ptr, n, M, J, r):
+    def __init__(self, ptr, n, M, J, r, keep=()):
         self.ptr = ptr
+        self._keep = keep            # allocator-hook callbacks must outlive the plan
         self.n, self.M, self.J, self.r = n, M, J, r
         info = mra_plan_info(self)
         self.n_retained = info["n_retained"]
@@ -174,21 +183,56 @@ class PlanHandle:
             pass
 
 
+def mra_nccl_unique_id() -> bytes:
+    """A fresh 128-byte ncclUniqueId (create on rank 0, send to every rank, pass as nccl_id=)."""
+    lib = load_library()
+    buf = ctypes.create_string_buffer(128)
+    _check(lib.mra_nccl_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
+    return buf.raw
+
+
+def _torch_hooks():
+    """Allocator hooks that take the plan's device memory from torch's caching allocator."""
+    import torch
+
+    def _alloc(nbytes, device, stream):
+        try:
+            with torch.cuda.device(device):
+                return torch.cuda.caching_allocator_alloc(int(nbytes), device, stream or 0)
+        except Exception:
+            return None
+
+    def _free(ptr, device, stream):
+        torch.cuda.caching_allocator_delete(ptr)
+
+    return _DALLOC(_alloc), _DFREE(_free)
+
+
 def mra_plan_create(x, y, M, J, r, offset=0.0, xscale=0.0, yscale=0.0, device=-1, stream=None, rank=0,
                     world=1, shard_level=0, mem_budget_gb=0.0, wide=0, host_plan=0,
-                    stream_prior=0, theta_lanes=0) -> PlanHandle:
+                    stream_prior=0, theta_lanes=0, nccl_id=None, torch_alloc=False) -> PlanHandle:
+    """Build a plan. nccl_id (bytes from mra_nccl_unique_id on rank 0) gives the plan its own NCCL communicator
+    for the in-library exchange step of subtree sharding; torch_alloc=True routes its device memory through
+    torch's caching allocator (opts.dalloc / dfree)."""
     lib = load_library()
     x = np.ascontiguousarray(x, dtype=np.float64)
     y = np.ascontiguousarray(y, dtype=np.float64)
     if x.shape != y.shape or x.ndim != 1:
         raise ValueError("x and y must be 1-D arrays of equal length")
+    idbuf = None
+    if nccl_id is not None:
+        if len(nccl_id) != 128:
+            raise ValueError("nccl_id must be the 128 bytes of an ncclUniqueId")
+        idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+    hooks = _torch_hooks() if torch_alloc else (_DALLOC(), _DFREE())
     opts = _Opts(float(offset), float(xscale), float(yscale), int(device), _stream_ptr(stream), int(rank),
                  int(world), int(shard_level), float(mem_budget_gb), int(wide), int(host_plan), int(stream_prior),
-                 int(theta_lanes))
+                 int(theta_lanes), ctypes.cast(idbuf, ctypes.c_void_p) if idbuf is not None else None,
+                 hooks[0], hooks[1])
     out = ctypes.c_void_p()
     _check(lib.mra_plan_create(_dptr(x), _dptr(y), x.shape[0], int(M), int(J), int(r), ctypes.byref(opts),
                                ctypes.byref(out)))
-    return PlanHandle(out.value, x.shape[0], M, J, r)
+    return PlanHandle(out.value, x.shape[0], M, J, r, keep=hooks if torch_alloc else ())
 
 
 def _post_struct(plan, posterior, regions, host, device=None):
@@ -237,8 +281,18 @@ def mra_loglik(plan: PlanHandle, y, theta, posterior=False, regions=False):
     return _result(plan, ll, post, bufs, posterior)
 
 
+def _check_dev(t, n, what="y_dev"):
+    """A device buffer handed to the library: contiguous float64 CUDA memory of at least n values."""
+    import torch
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.float64 or not t.is_cuda or not t.is_contiguous():
+        raise ValueError(f"{what} must be a contiguous torch.float64 CUDA tensor")
+    if t.numel() < n:
+        raise ValueError(f"{what} holds {t.numel()} values, the call needs {n}")
+
+
 def mra_loglik_dev(plan: PlanHandle, y_dev, theta, posterior=False, regions=False):
     """y_dev: torch float64 CUDA tensor (original order). Posterior outputs stay on the device."""
+    _check_dev(y_dev, plan.n)
     th = _theta(theta)
     ll = ctypes.c_double()
     post, bufs = _post_struct(plan, posterior, regions, host=False, device=y_dev.device)
@@ -248,6 +302,7 @@ def mra_loglik_dev(plan: PlanHandle, y_dev, theta, posterior=False, regions=Fals
 
 
 def mra_loglik_batch_dev(plan: PlanHandle, y_dev, thetas):
+    _check_dev(y_dev, plan.n)
     arr = (_Theta * len(thetas))(*[_theta(t) for t in thetas])
     out = np.empty(len(thetas))
     _check(_lib.mra_loglik_batch_dev(plan.ptr, ctypes.c_void_p(y_dev.data_ptr()), arr, len(thetas), _dptr(out)))
@@ -270,6 +325,8 @@ def mra_shard_size(plan: PlanHandle) -> int:
 
 
 def mra_loglik_shard(plan: PlanHandle, y_dev, theta, xbuf_dev):
+    _check_dev(y_dev, plan.n)
+    _check_dev(xbuf_dev, mra_shard_size(plan), "xbuf_dev")
     th = _theta(theta)
     _check(_lib.mra_loglik_shard(plan.ptr, ctypes.c_void_p(y_dev.data_ptr()), ctypes.byref(th),
                                  ctypes.c_void_p(xbuf_dev.data_ptr())))
@@ -280,12 +337,16 @@ def mra_mutop_size(plan: PlanHandle) -> int:
 
 
 def mra_loglik_shard_post(plan: PlanHandle, y_dev, theta, xbuf_dev):
+    _check_dev(y_dev, plan.n)
+    _check_dev(xbuf_dev, mra_shard_size(plan), "xbuf_dev")
     th = _theta(theta)
     _check(_lib.mra_loglik_shard_post(plan.ptr, ctypes.c_void_p(y_dev.data_ptr()), ctypes.byref(th),
                                       ctypes.c_void_p(xbuf_dev.data_ptr())))
 
 
 def mra_loglik_finish_post(plan: PlanHandle, theta, xbuf_dev, mutop_dev) -> float:
+    _check_dev(xbuf_dev, mra_shard_size(plan), "xbuf_dev")
+    _check_dev(mutop_dev, mra_mutop_size(plan), "mutop_dev")
     th = _theta(theta)
     ll = ctypes.c_double()
     _check(_lib.mra_loglik_finish_post(plan.ptr, ctypes.byref(th), ctypes.c_void_p(xbuf_dev.data_ptr()),
@@ -294,12 +355,18 @@ def mra_loglik_finish_post(plan: PlanHandle, theta, xbuf_dev, mutop_dev) -> floa
 
 
 def mra_posterior_shard(plan: PlanHandle, mutop_dev, mu_dev=None, smooth_dev=None):
+    _check_dev(mutop_dev, mra_mutop_size(plan), "mutop_dev")
+    if mu_dev is not None:
+        _check_dev(mu_dev, plan.n_interior * plan.r_hat, "mu_dev")
+    if smooth_dev is not None:
+        _check_dev(smooth_dev, plan.n, "smooth_dev")
     _check(_lib.mra_posterior_shard(plan.ptr, ctypes.c_void_p(mutop_dev.data_ptr()),
                                     ctypes.c_void_p(mu_dev.data_ptr() if mu_dev is not None else 0),
                                     ctypes.c_void_p(smooth_dev.data_ptr() if smooth_dev is not None else 0)))
 
 
 def mra_loglik_finish(plan: PlanHandle, theta, xbuf_dev) -> float:
+    _check_dev(xbuf_dev, mra_shard_size(plan), "xbuf_dev")
     th = _theta(theta)
     ll = ctypes.c_double()
     _check(_lib.mra_loglik_finish(plan.ptr, ctypes.byref(th), ctypes.c_void_p(xbuf_dev.data_ptr()),
@@ -364,6 +431,7 @@ def mra_kernel_times(plan: PlanHandle) -> dict:
 def mra_optimize(plan: PlanHandle, y_dev, theta0, lower=None, upper=None, max_evals=200, tol=1e-6):
     """Maximise log L over (sigma2, rho, tau2) from theta0 = (cov, sigma2, rho, tau2); y_dev a CUDA tensor.
     Returns (theta, loglik, n_evals)."""
+    _check_dev(y_dev, plan.n)
     th = _Theta(int(theta0[0]), float(theta0[1]), float(theta0[2]), float(theta0[3]))
     D = ctypes.POINTER(ctypes.c_double)
     lo = None if lower is None else (ctypes.c_double * 3)(*[float(v) for v in lower])

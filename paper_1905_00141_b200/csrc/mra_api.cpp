@@ -12,12 +12,17 @@
 #include "../../include/mra.h"
 
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>   // types and prototypes only: the library is dlopen'ed (nccl_api below)
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
+#include <mutex>
+#include <new>
 #include <string>
 #include <type_traits>
 #include <vector>
@@ -30,6 +35,59 @@ static thread_local std::string g_err;
 static mra_status fail(mra_status s, const std::string& msg) {
     g_err = msg;
     return s;
+}
+
+// every extern "C" entry runs its body through this: no C++ exception (host std::bad_alloc from a huge
+// plan, std::length_error, ...) ever crosses the C ABI (include/mra.h: "No call aborts")
+template <class F>
+static mra_status guarded(F&& f) {
+    try {
+        return f();
+    } catch (const std::bad_alloc&) {
+        return fail(MRA_E_OOM, "host allocation failed (std::bad_alloc)");
+    } catch (const std::exception& e) {
+        return fail(MRA_E_OOM, std::string("host exception: ") + e.what());
+    } catch (...) {
+        return fail(MRA_E_OOM, "unknown host exception");
+    }
+}
+
+// ---------------------------------------------------------------- NCCL (dlopen'ed)
+// The in-library exchange step of subtree sharding. NCCL is
+// loaded at run time: the copy torch already mapped (libnccl.so.2 by soname), else the system one, or
+// $MRA_NCCL_LIB; a missing library is MRA_E_NCCL at plan creation, not a link-time dependency.
+struct NcclApi {
+    decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+    decltype(&ncclCommInitRank) commInitRank = nullptr;
+    decltype(&ncclCommDestroy) commDestroy = nullptr;
+    decltype(&ncclReduce) reduce = nullptr;
+    decltype(&ncclBroadcast) broadcast = nullptr;
+    decltype(&ncclAllReduce) allReduce = nullptr;
+    decltype(&ncclGetErrorString) errStr = nullptr;
+    bool ok = false;
+};
+static const NcclApi* nccl_api() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        const char* cands[3] = {getenv("MRA_NCCL_LIB"), "libnccl.so.2", "libnccl.so"};
+        void* h = nullptr;
+        for (const char* c : cands)
+            if (c && *c && (h = dlopen(c, RTLD_NOW | RTLD_GLOBAL))) break;
+        if (!h) return;
+#define NSYM(f, n) api.f = reinterpret_cast<decltype(api.f)>(dlsym(h, n))
+        NSYM(getUniqueId, "ncclGetUniqueId");
+        NSYM(commInitRank, "ncclCommInitRank");
+        NSYM(commDestroy, "ncclCommDestroy");
+        NSYM(reduce, "ncclReduce");
+        NSYM(broadcast, "ncclBroadcast");
+        NSYM(allReduce, "ncclAllReduce");
+        NSYM(errStr, "ncclGetErrorString");
+#undef NSYM
+        api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.reduce && api.broadcast &&
+                 api.allReduce && api.errStr;
+    });
+    return api.ok ? &api : nullptr;
 }
 
 struct mra_plan {
@@ -72,6 +130,16 @@ struct mra_plan {
     // sharding
     int rank = 0, world = 1;
     std::vector<long long> my_c;     // level-c regions owned by this rank (sorted)
+    // in-library exchange (opts.nccl_id): own communicator and exchange buffers
+    bool nccl = false;
+    ncclComm_t comm = nullptr;
+    double* xbuf = nullptr;          // packed exchange buffer (mra_shard_size doubles)
+    double* bcast = nullptr;         // [4] log L, error flag, d, u broadcast from rank 0
+    double* mutop = nullptr;         // above-shard posterior means (mra_mutop_size doubles)
+    double* sm_sorted = nullptr;     // smoothed values in leaf order (all-reduced across ranks)
+    // device allocator hooks (opts.dalloc / dfree; NULL = cudaMalloc / cudaFree)
+    void* (*ualloc)(size_t, int, void*) = nullptr;
+    void (*ufree)(void*, int, void*) = nullptr;
     // posterior state
     double* post = nullptr;
     long long post_base[MAXM + 1] = {0};
@@ -161,9 +229,24 @@ static long long q_of(int m, int rh) { return (long long)(m - 1) * rh + 1; }
                         std::string(#call) + ": " + cudaGetErrorString(e_));                   \
     } while (0)
 
+// raw device allocation through the plan's hooks (torch's caching allocator when given)
+static cudaError_t talloc(const mra_plan* p, void** ptr, size_t bytes) {
+    if (bytes == 0) bytes = 8;
+    if (p->ualloc) {
+        *ptr = p->ualloc(bytes, p->device, (void*)p->st);
+        return *ptr ? cudaSuccess : cudaErrorMemoryAllocation;
+    }
+    return cudaMalloc(ptr, bytes);
+}
+static void tfree(const mra_plan* p, void* ptr) {
+    if (!ptr) return;
+    if (p->ufree) p->ufree(ptr, p->device, (void*)p->st);
+    else cudaFree(ptr);
+}
+
 static mra_status dalloc(mra_plan* p, void** ptr, size_t bytes, const char* what) {
     if (bytes == 0) bytes = 8;
-    cudaError_t e = cudaMalloc(ptr, bytes);
+    cudaError_t e = talloc(p, ptr, bytes);
     if (e != cudaSuccess) {
         cudaGetLastError();
         char buf[256];
@@ -320,8 +403,10 @@ static mra_status build_device(mra_plan* P, const double* x, const double* y, ui
     int *bad = nullptr, *k1 = nullptr, *i1 = nullptr, *k2 = nullptr, *i2 = nullptr;
     unsigned int *cnt = nullptr, *bcnt = nullptr;
     auto release = [&]() {
-        cudaFree(dx); cudaFree(dy); cudaFree(part); cudaFree(dbox); cudaFree(dxb); cudaFree(dyb); cudaFree(bad);
-        cudaFree(k1); cudaFree(i1); cudaFree(k2); cudaFree(i2); cudaFree(cnt); cudaFree(bcnt);
+        cudaStreamSynchronize(st);
+        for (void* v : {(void*)dx, (void*)dy, (void*)part, (void*)dbox, (void*)dxb, (void*)dyb, (void*)bad, (void*)k1,
+                        (void*)i1, (void*)k2, (void*)i2, (void*)cnt, (void*)bcnt})
+            tfree(P, v);
     };
 #define BD(call)                                                                              \
     do {                                                                                      \
@@ -332,14 +417,14 @@ static mra_status build_device(mra_plan* P, const double* x, const double* y, ui
                         std::string("device plan build: " #call ": ") + cudaGetErrorString(e_)); \
         }                                                                                     \
     } while (0)
-    BD(cudaMalloc(&dx, 8 * nn));
-    BD(cudaMalloc(&dy, 8 * nn));
+    BD(talloc(P, (void**)&dx, 8 * nn));
+    BD(talloc(P, (void**)&dy, 8 * nn));
     BD(cudaMemcpyAsync(dx, x, 8 * nn, cudaMemcpyHostToDevice, st));
     BD(cudaMemcpyAsync(dy, y, 8 * nn, cudaMemcpyHostToDevice, st));
     // bounding box + finiteness
     const int nb = (int)std::min<long long>(1024, (nn + 255) / 256);
-    BD(cudaMalloc(&part, 8 * 4 * nb));
-    BD(cudaMalloc(&bad, 4));
+    BD(talloc(P, (void**)&part, 8 * 4 * nb));
+    BD(talloc(P, (void**)&bad, 4));
     BD(cudaMemsetAsync(bad, 0, 4, st));
     BD(plan_bbox(dx, dy, nn, part, nb, bad, st));
     std::vector<double> hp(4 * nb);
@@ -363,16 +448,16 @@ static mra_status build_device(mra_plan* P, const double* x, const double* y, ui
         for (int ix = 0; ix < P->nx; ix++) hxb[id * P->nx + ix] = P->kx[id * P->rh + ix];
         for (int iy = 0; iy < P->ny; iy++) hyb[id * P->ny + iy] = P->ky[id * P->rh + iy * P->nx];
     }
-    BD(cudaMalloc(&dbox, 8 * 4 * ni));
-    BD(cudaMalloc(&dxb, 8 * hxb.size()));
-    BD(cudaMalloc(&dyb, 8 * hyb.size()));
+    BD(talloc(P, (void**)&dbox, 8 * 4 * ni));
+    BD(talloc(P, (void**)&dxb, 8 * hxb.size()));
+    BD(talloc(P, (void**)&dyb, 8 * hyb.size()));
     BD(cudaMemcpyAsync(dbox, P->box.data(), 8 * 4 * ni, cudaMemcpyHostToDevice, st));
     BD(cudaMemcpyAsync(dxb, hxb.data(), 8 * hxb.size(), cudaMemcpyHostToDevice, st));
     BD(cudaMemcpyAsync(dyb, hyb.data(), 8 * hyb.size(), cudaMemcpyHostToDevice, st));
     // keys (eliminated -> n_leaves), per-leaf counts
-    BD(cudaMalloc(&k1, 4 * nn)); BD(cudaMalloc(&i1, 4 * nn));
-    BD(cudaMalloc(&k2, 4 * nn)); BD(cudaMalloc(&i2, 4 * nn));
-    BD(cudaMalloc(&cnt, 4 * (P->nleaf + 1)));
+    BD(talloc(P, (void**)&k1, 4 * nn)); BD(talloc(P, (void**)&i1, 4 * nn));
+    BD(talloc(P, (void**)&k2, 4 * nn)); BD(talloc(P, (void**)&i2, 4 * nn));
+    BD(talloc(P, (void**)&cnt, 4 * (P->nleaf + 1)));
     BD(cudaMemsetAsync(cnt, 0, 4 * (P->nleaf + 1), st));
     PlanGeom pg{};
     pg.M = M; pg.J = P->J; pg.nx = P->nx; pg.ny = P->ny; pg.nleaf = P->nleaf;
@@ -380,7 +465,7 @@ static mra_status build_device(mra_plan* P, const double* x, const double* y, ui
     BD(plan_keys(dx, dy, nn, pg, k1, i1, cnt, st));
     // stable LSD radix sort over the M base-J digits of the key (digit M-1 flags eliminated observations)
     const int nblk = plan_radix_blocks(nn), R = 1 << lj;
-    BD(cudaMalloc(&bcnt, 4 * (size_t)R * nblk));
+    BD(talloc(P, (void**)&bcnt, 4 * (size_t)R * nblk));
     std::vector<unsigned int> hb((size_t)R * nblk);
     for (int d = 0; d < M; d++) {
         BD(plan_radix_count(k1, nn, lj, d, bcnt, st));
@@ -493,7 +578,7 @@ static mra_status size_device(mra_plan* P, double budget_gb, int stream_opt) {
     };
     int c = 1;
     const int cmax = std::max(1, M - 1);
-    if (P->world > 1) {
+    if (P->world > 1 || P->nccl) {
         c = P->c;   // shard level fixed by the caller / auto rule
     } else {
         while (c < cmax && full_bytes(c) + chunk_bytes(c, 1) > out_budget) c++;
@@ -786,137 +871,165 @@ static mra_status make_lane(mra_plan* P, mra_plan** out) {
 
 extern "C" mra_status mra_plan_create(const double* x, const double* y, uint64_t n, int M, int J, int r,
                                       const mra_opts* opts, mra_plan** out) {
-    g_err.clear();
-    if (!out) return fail(MRA_E_ARG, "out is NULL");
-    *out = nullptr;
-    if (!x || !y || n == 0) return fail(MRA_E_ARG, "x/y NULL or n == 0");
-    if (M < 1 || M > MAXM - 1) return fail(MRA_E_CONFIG, "M out of range [1, 22]");
-    if (J != 2 && J != 4) return fail(MRA_E_CONFIG, "J must be 2 or 4 (PAPER.md:100)");
-    if (r < 1) return fail(MRA_E_CONFIG, "r must be >= 1");
-    mra_opts o{};
-    if (opts) o = *opts;
-    mra_plan* P = new mra_plan();
-    P->M = M; P->J = J; P->lj = (J == 4) ? 2 : 1; P->r = r;
-    P->offset = o.offset > 0 ? o.offset : std::exp(1.0) / 100.0;
-    if (!(P->offset > 0 && P->offset < 0.5)) { delete P; return fail(MRA_E_ARG, "offset must be in (0, 0.5)"); }
-    P->xs = o.xscale > 0 ? o.xscale : 1.0;
-    P->ys = o.yscale > 0 ? o.yscale : 1.0;
-    P->n_in = n;
-    P->rank = o.world > 1 ? o.rank : 0;
-    P->world = o.world > 1 ? o.world : 1;
-    // S0 on the device (NEXT-2) unless this is a host-only plan, the caller asks for the host build,
-    // or the keys / indices would not fit the device build's 32-bit fields
-    const bool dev_build = o.device != -2 && !o.host_plan && n < (1ULL << 31) &&
-                           ipow(J, M - 1) < (1LL << 30);
-    mra_status s = MRA_OK;
-    if (dev_build) {
-        int dev = o.device;
-        if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) { delete P; return fail(MRA_E_CUDA, "no CUDA device"); }
-        if (cudaSetDevice(dev) != cudaSuccess) { delete P; return fail(MRA_E_CUDA, "cudaSetDevice failed (no GPU?)"); }
-        P->device = dev;
-        P->st = (cudaStream_t)o.stream;
-        s = build_device(P, x, y, n);
-        if (s) { mra_plan_destroy(P); return s; }
-    } else {
-        s = build_host(P, x, y, n);
-        if (s) { delete P; return s; }
-    }
-    // the grid-wide task path is at least as fast as one-CTA-per-group on every configuration measured
-    // (C0 4.3x, C1 1.2x, C2/C3 ~1.02x, C4 > 100x: DESIGN.md §5), so it is the default for M >= 2
-    P->wide = M >= 2 && o.wide >= 0;
-    // sharding: shard level = first level with >= 8*world regions (or the caller's choice)
-    if (P->world > 1) {
-        int sl = o.shard_level;
-        if (sl <= 0) { sl = 1; while (sl < M - 1 && ipow(J, sl - 1) < 8LL * P->world) sl++; }
-        if (sl >= M) sl = M - 1;
-        if (sl < 1) { delete P; return fail(MRA_E_CONFIG, "tree too shallow to shard (need M >= 2)"); }
-        P->c = sl;
-        // LPT over the per-shard leaf work (sum n_j^3 + n_j^2 ((M-1) r_hat))
-        const long long ns = ipow(J, sl - 1), per = ipow(J, M - sl);
-        std::vector<std::pair<double, long long>> cost(ns);
-        for (long long s2 = 0; s2 < ns; s2++) {
-            double cst = 0;
-            for (long long l = s2 * per; l < (s2 + 1) * per; l++) {
-                const double nj = (double)(P->leaf_off[l + 1] - P->leaf_off[l]);
-                cst += nj * nj * nj / 3.0 + nj * nj * (M - 1) * P->rh * 2.0 + nj * std::pow((M - 1) * P->rh, 2);
+    return guarded([&]() -> mra_status {
+        g_err.clear();
+        if (!out) return fail(MRA_E_ARG, "out is NULL");
+        *out = nullptr;
+        if (!x || !y || n == 0) return fail(MRA_E_ARG, "x/y NULL or n == 0");
+        if (M < 1 || M > MAXM - 1) return fail(MRA_E_CONFIG, "M out of range [1, 23]");
+        if (J != 2 && J != 4) return fail(MRA_E_CONFIG, "J must be 2 or 4 (PAPER.md:100)");
+        if (r < 1) return fail(MRA_E_CONFIG, "r must be >= 1");
+        // the task lists index leaves with 32-bit fields and the host keeps O(regions) metadata: bound the tree
+        if (ipow(J, M - 1) > (1LL << 30)) return fail(MRA_E_CONFIG, "tree too large: J^(M-1) leaves must be <= 2^30");
+        mra_opts o{};
+        if (opts) o = *opts;
+        if ((o.dalloc == nullptr) != (o.dfree == nullptr)) return fail(MRA_E_ARG, "dalloc and dfree must be given together");
+        mra_plan* P = new mra_plan();
+        P->ualloc = o.dalloc;
+        P->ufree = o.dfree;
+        P->M = M; P->J = J; P->lj = (J == 4) ? 2 : 1; P->r = r;
+        P->offset = o.offset > 0 ? o.offset : std::exp(1.0) / 100.0;
+        if (!(P->offset > 0 && P->offset < 0.5)) { delete P; return fail(MRA_E_ARG, "offset must be in (0, 0.5)"); }
+        P->xs = o.xscale > 0 ? o.xscale : 1.0;
+        P->ys = o.yscale > 0 ? o.yscale : 1.0;
+        P->n_in = n;
+        P->rank = o.world > 1 ? o.rank : 0;
+        P->world = o.world > 1 ? o.world : 1;
+        P->nccl = o.nccl_id != nullptr;
+        if (P->nccl && o.device == -2) { delete P; return fail(MRA_E_ARG, "a host-only plan has no communicator"); }
+        if (o.world > 1 && (o.rank < 0 || o.rank >= o.world)) { delete P; return fail(MRA_E_ARG, "rank out of [0, world)"); }
+        // S0 on the device (NEXT-2) unless this is a host-only plan, the caller asks for the host build,
+        // or the keys / indices would not fit the device build's 32-bit fields
+        const bool dev_build = o.device != -2 && !o.host_plan && n < (1ULL << 31) &&
+                               ipow(J, M - 1) < (1LL << 30);
+        mra_status s = MRA_OK;
+        if (dev_build) {
+            int dev = o.device;
+            if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) { delete P; return fail(MRA_E_CUDA, "no CUDA device"); }
+            if (cudaSetDevice(dev) != cudaSuccess) { delete P; return fail(MRA_E_CUDA, "cudaSetDevice failed (no GPU?)"); }
+            P->device = dev;
+            P->st = (cudaStream_t)o.stream;
+            s = build_device(P, x, y, n);
+            if (s) { mra_plan_destroy(P); return s; }
+        } else {
+            s = build_host(P, x, y, n);
+            if (s) { delete P; return s; }
+        }
+        // the grid-wide task path is at least as fast as one-CTA-per-group on every configuration measured
+        // (C0 4.3x, C1 1.2x, C2/C3 ~1.02x, C4 > 100x: DESIGN.md §5), so it is the default for M >= 2
+        P->wide = M >= 2 && o.wide >= 0;
+        // sharding: shard level = first level with >= 8*world regions (or the caller's choice); an in-library
+        // communicator runs the sharded schedule at any world size (world 1: the path on one rank)
+        if (P->world > 1 || P->nccl) {
+            int sl = o.shard_level;
+            if (sl <= 0) { sl = 1; while (sl < M - 1 && ipow(J, sl - 1) < 8LL * P->world) sl++; }
+            if (sl >= M) sl = M - 1;
+            if (sl < 1) { delete P; return fail(MRA_E_CONFIG, "tree too shallow to shard (need M >= 2)"); }
+            P->c = sl;
+            // LPT over the per-shard leaf work (sum n_j^3 + n_j^2 ((M-1) r_hat))
+            const long long ns = ipow(J, sl - 1), per = ipow(J, M - sl);
+            std::vector<std::pair<double, long long>> cost(ns);
+            for (long long s2 = 0; s2 < ns; s2++) {
+                double cst = 0;
+                for (long long l = s2 * per; l < (s2 + 1) * per; l++) {
+                    const double nj = (double)(P->leaf_off[l + 1] - P->leaf_off[l]);
+                    cst += nj * nj * nj / 3.0 + nj * nj * (M - 1) * P->rh * 2.0 + nj * std::pow((M - 1) * P->rh, 2);
+                }
+                cost[s2] = {cst + 1.0, s2};
             }
-            cost[s2] = {cst + 1.0, s2};
+            std::sort(cost.begin(), cost.end(), [](auto& a, auto& b) { return a.first > b.first || (a.first == b.first && a.second < b.second); });
+            std::vector<double> load(P->world, 0.0);
+            for (auto& cs : cost) {
+                int best = 0;
+                for (int w = 1; w < P->world; w++) if (load[w] < load[best]) best = w;
+                load[best] += cs.first;
+                if (best == P->rank) P->my_c.push_back(cs.second);
+            }
+            std::sort(P->my_c.begin(), P->my_c.end());
         }
-        std::sort(cost.begin(), cost.end(), [](auto& a, auto& b) { return a.first > b.first || (a.first == b.first && a.second < b.second); });
-        std::vector<double> load(P->world, 0.0);
-        for (auto& cs : cost) {
-            int best = 0;
-            for (int w = 1; w < P->world; w++) if (load[w] < load[best]) best = w;
-            load[best] += cs.first;
-            if (best == P->rank) P->my_c.push_back(cs.second);
+        if (o.device == -2) {   // host-only plan: structure only (PAPER.md:228 build_structure_only)
+            P->device = -2;
+            *out = P;
+            return MRA_OK;
         }
-        std::sort(P->my_c.begin(), P->my_c.end());
-    }
-    if (o.device == -2) {   // host-only plan: structure only (PAPER.md:228 build_structure_only)
-        P->device = -2;
+    
+        int dev = o.device;
+        if (dev < 0) {
+            if (cudaGetDevice(&dev) != cudaSuccess) { delete P; return fail(MRA_E_CUDA, "no CUDA device"); }
+        }
+        P->device = dev;
+        if (cudaSetDevice(dev) != cudaSuccess) { delete P; return fail(MRA_E_CUDA, "cudaSetDevice failed (no GPU?)"); }
+        cudaDeviceGetAttribute(&P->nsm, cudaDevAttrMultiProcessorCount, dev);
+        P->st = (cudaStream_t)o.stream;
+        mra_status st;
+    #define TRY(x) do { if ((st = (x))) { mra_plan_destroy(P); return st; } } while (0)
+        const long long N = P->N;
+        if (!dev_build) {
+            TRY(dalloc(P, (void**)&P->pxy, 16 * N, "pxy"));
+            TRY(dalloc(P, (void**)&P->perm_d, 8 * N, "perm"));
+        }
+        TRY(dalloc(P, (void**)&P->zs, 8 * N, "zs"));
+        TRY(dalloc(P, (void**)&P->zin, 8 * (long long)n, "zin"));
+        TRY(dalloc(P, (void**)&P->leaf_off_d, 8 * (P->nleaf + 1), "leaf_off"));
+        TRY(dalloc(P, (void**)&P->kxy_d, 16 * std::max<long long>(1, P->nint * P->rh), "kxy"));
+        TRY(dalloc(P, (void**)&P->dreg, 8 * P->nreg, "dreg"));
+        TRY(dalloc(P, (void**)&P->ureg, 8 * P->nreg, "ureg"));
+        TRY(dalloc(P, (void**)&P->loglik_d, 8, "loglik"));
+        TRY(dalloc(P, (void**)&P->err, 16, "err"));
+        P->n_counters = 1 << 16;
+        TRY(dalloc(P, (void**)&P->counters, 8 * (size_t)P->n_counters, "counters"));
+        {
+            std::vector<double> kxy(2 * std::max<long long>(1, P->nint * P->rh));
+            for (long long i = 0; i < P->nint * P->rh; i++) { kxy[2 * i] = P->kx[i]; kxy[2 * i + 1] = P->ky[i]; }
+            auto cp = [&](void* d, const void* h, size_t b) -> mra_status {
+                cudaError_t e = cudaMemcpy(d, h, b, cudaMemcpyHostToDevice);
+                if (e != cudaSuccess) return fail(MRA_E_CUDA, std::string("upload: ") + cudaGetErrorString(e));
+                return MRA_OK;
+            };
+            if (!dev_build) {
+                std::vector<double> sxy(2 * N);
+                for (long long i = 0; i < N; i++) { sxy[2 * i] = x[P->perm[i]]; sxy[2 * i + 1] = y[P->perm[i]]; }
+                TRY(cp(P->pxy, sxy.data(), 16 * N));
+                TRY(cp(P->perm_d, P->perm.data(), 8 * N));
+            }
+            TRY(cp(P->leaf_off_d, P->leaf_off.data(), 8 * (P->nleaf + 1)));
+            if (P->nint) TRY(cp(P->kxy_d, kxy.data(), 16 * P->nint * P->rh));
+        }
+        // the copy stream / event of the host-y entry points (created here, not inside the first timed call)
+        if (cudaStreamCreateWithFlags(&P->cst, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&P->cev, cudaEventDisableTiming) != cudaSuccess) {
+            mra_plan_destroy(P);
+            return fail(MRA_E_CUDA, "copy stream / event creation failed");
+        }
+        P->n_lanes = std::max(1, std::min(o.theta_lanes, 16));
+        if (P->world > 1 || P->nccl) P->n_lanes = 1;
+        TRY(size_device(P, o.mem_budget_gb, o.stream_prior));
+        if (P->nccl) {
+            const NcclApi* nc = nccl_api();
+            if (!nc) {
+                mra_plan_destroy(P);
+                return fail(MRA_E_NCCL, "opts.nccl_id given but no NCCL library could be loaded (libnccl.so.2 / $MRA_NCCL_LIB)");
+            }
+            ncclUniqueId id;
+            std::memcpy(&id, o.nccl_id, sizeof id);
+            const ncclResult_t r0 = nc->commInitRank(&P->comm, P->world, id, P->rank);
+            if (r0 != ncclSuccess) {
+                P->comm = nullptr;
+                mra_plan_destroy(P);
+                return fail(MRA_E_NCCL, std::string("ncclCommInitRank: ") + nc->errStr(r0));
+            }
+            TRY(dalloc(P, (void**)&P->xbuf, 8 * mra_shard_size(P), "exchange buffer"));
+            TRY(dalloc(P, (void**)&P->bcast, 8 * 4, "broadcast scalars"));
+        }
+        for (int k = 1; k < P->n_lanes; k++) {
+            mra_plan* Q = nullptr;
+            TRY(make_lane(P, &Q));
+            P->lanes.push_back(Q);
+        }
+    #undef TRY
         *out = P;
         return MRA_OK;
-    }
-
-    int dev = o.device;
-    if (dev < 0) {
-        if (cudaGetDevice(&dev) != cudaSuccess) { delete P; return fail(MRA_E_CUDA, "no CUDA device"); }
-    }
-    P->device = dev;
-    if (cudaSetDevice(dev) != cudaSuccess) { delete P; return fail(MRA_E_CUDA, "cudaSetDevice failed (no GPU?)"); }
-    cudaDeviceGetAttribute(&P->nsm, cudaDevAttrMultiProcessorCount, dev);
-    P->st = (cudaStream_t)o.stream;
-    mra_status st;
-#define TRY(x) do { if ((st = (x))) { mra_plan_destroy(P); return st; } } while (0)
-    const long long N = P->N;
-    if (!dev_build) {
-        TRY(dalloc(P, (void**)&P->pxy, 16 * N, "pxy"));
-        TRY(dalloc(P, (void**)&P->perm_d, 8 * N, "perm"));
-    }
-    TRY(dalloc(P, (void**)&P->zs, 8 * N, "zs"));
-    TRY(dalloc(P, (void**)&P->zin, 8 * (long long)n, "zin"));
-    TRY(dalloc(P, (void**)&P->leaf_off_d, 8 * (P->nleaf + 1), "leaf_off"));
-    TRY(dalloc(P, (void**)&P->kxy_d, 16 * std::max<long long>(1, P->nint * P->rh), "kxy"));
-    TRY(dalloc(P, (void**)&P->dreg, 8 * P->nreg, "dreg"));
-    TRY(dalloc(P, (void**)&P->ureg, 8 * P->nreg, "ureg"));
-    TRY(dalloc(P, (void**)&P->loglik_d, 8, "loglik"));
-    TRY(dalloc(P, (void**)&P->err, 16, "err"));
-    P->n_counters = 1 << 16;
-    TRY(dalloc(P, (void**)&P->counters, 8 * (size_t)P->n_counters, "counters"));
-    {
-        std::vector<double> kxy(2 * std::max<long long>(1, P->nint * P->rh));
-        for (long long i = 0; i < P->nint * P->rh; i++) { kxy[2 * i] = P->kx[i]; kxy[2 * i + 1] = P->ky[i]; }
-        auto cp = [&](void* d, const void* h, size_t b) -> mra_status {
-            cudaError_t e = cudaMemcpy(d, h, b, cudaMemcpyHostToDevice);
-            if (e != cudaSuccess) return fail(MRA_E_CUDA, std::string("upload: ") + cudaGetErrorString(e));
-            return MRA_OK;
-        };
-        if (!dev_build) {
-            std::vector<double> sxy(2 * N);
-            for (long long i = 0; i < N; i++) { sxy[2 * i] = x[P->perm[i]]; sxy[2 * i + 1] = y[P->perm[i]]; }
-            TRY(cp(P->pxy, sxy.data(), 16 * N));
-            TRY(cp(P->perm_d, P->perm.data(), 8 * N));
-        }
-        TRY(cp(P->leaf_off_d, P->leaf_off.data(), 8 * (P->nleaf + 1)));
-        if (P->nint) TRY(cp(P->kxy_d, kxy.data(), 16 * P->nint * P->rh));
-    }
-    // the copy stream / event of the host-y entry points (created here, not inside the first timed call)
-    if (cudaStreamCreateWithFlags(&P->cst, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&P->cev, cudaEventDisableTiming) != cudaSuccess) {
-        mra_plan_destroy(P);
-        return fail(MRA_E_CUDA, "copy stream / event creation failed");
-    }
-    P->n_lanes = std::max(1, std::min(o.theta_lanes, 16));
-    if (P->world > 1) P->n_lanes = 1;
-    TRY(size_device(P, o.mem_budget_gb, o.stream_prior));
-    for (int k = 1; k < P->n_lanes; k++) {
-        mra_plan* Q = nullptr;
-        TRY(make_lane(P, &Q));
-        P->lanes.push_back(Q);
-    }
-#undef TRY
-    *out = P;
-    return MRA_OK;
+    });
 }
 
 extern "C" void mra_plan_destroy(mra_plan* P) {
@@ -930,54 +1043,65 @@ extern "C" void mra_plan_destroy(mra_plan* P) {
         for (cudaEvent_t e : P->evpool) cudaEventDestroy(e);
         if (P->cev) cudaEventDestroy(P->cev);
         if (P->cst) cudaStreamDestroy(P->cst);
-        for (void* a : P->allocs) cudaFree(a);
+        for (void* a : P->allocs) tfree(P, a);
+        if (P->comm && !P->is_lane) {
+            if (const NcclApi* nc = nccl_api()) nc->commDestroy(P->comm);
+        }
     }
     delete P;
 }
 
 extern "C" mra_status mra_plan_info(const mra_plan* P, uint64_t* n_retained, int* r_hat, uint64_t* n_regions,
                                     uint64_t* n_leaves, uint64_t* n_empty, uint64_t* max_leaf) {
-    if (!P) return fail(MRA_E_ARG, "plan is NULL");
-    if (n_retained) *n_retained = (uint64_t)P->N;
-    if (r_hat) *r_hat = P->rh;
-    if (n_regions) *n_regions = (uint64_t)P->nreg;
-    if (n_leaves) *n_leaves = (uint64_t)P->nleaf;
-    if (n_empty) *n_empty = (uint64_t)P->n_empty;
-    if (max_leaf) *max_leaf = (uint64_t)P->max_leaf;
-    return MRA_OK;
+    return guarded([&]() -> mra_status {
+        if (!P) return fail(MRA_E_ARG, "plan is NULL");
+        if (n_retained) *n_retained = (uint64_t)P->N;
+        if (r_hat) *r_hat = P->rh;
+        if (n_regions) *n_regions = (uint64_t)P->nreg;
+        if (n_leaves) *n_leaves = (uint64_t)P->nleaf;
+        if (n_empty) *n_empty = (uint64_t)P->n_empty;
+        if (max_leaf) *max_leaf = (uint64_t)P->max_leaf;
+        return MRA_OK;
+    });
 }
 
 extern "C" mra_status mra_plan_layout(const mra_plan* P, int64_t* perm, int64_t* leaf_off, double* kx, double* ky) {
-    if (!P) return fail(MRA_E_ARG, "plan is NULL");
-    if (perm) std::memcpy(perm, P->perm.data(), 8 * P->N);
-    if (leaf_off) std::memcpy(leaf_off, P->leaf_off.data(), 8 * (P->nleaf + 1));
-    if (kx && P->nint) std::memcpy(kx, P->kx.data(), 8 * P->nint * P->rh);
-    if (ky && P->nint) std::memcpy(ky, P->ky.data(), 8 * P->nint * P->rh);
-    return MRA_OK;
+    return guarded([&]() -> mra_status {
+        if (!P) return fail(MRA_E_ARG, "plan is NULL");
+        if (perm) std::memcpy(perm, P->perm.data(), 8 * P->N);
+        if (leaf_off) std::memcpy(leaf_off, P->leaf_off.data(), 8 * (P->nleaf + 1));
+        if (kx && P->nint) std::memcpy(kx, P->kx.data(), 8 * P->nint * P->rh);
+        if (ky && P->nint) std::memcpy(ky, P->ky.data(), 8 * P->nint * P->rh);
+        return MRA_OK;
+    });
 }
 
 extern "C" uint64_t mra_last_launches(const mra_plan* P) { return P ? P->launches : 0; }
 
 extern "C" mra_status mra_profile(mra_plan* P, int enable) {
-    if (!P) return fail(MRA_E_ARG, "plan is NULL");
-    for (mra_plan* Q : P->lanes) mra_profile(Q, enable);
-    P->prof = enable != 0;
-    P->recs.clear();
-    P->ev_used = 0;
-    for (int k = 0; k < MRA_NKCLASS; k++) { P->prof_ms[k] = 0; P->prof_cnt[k] = 0; }
-    return MRA_OK;
+    return guarded([&]() -> mra_status {
+        if (!P) return fail(MRA_E_ARG, "plan is NULL");
+        for (mra_plan* Q : P->lanes) mra_profile(Q, enable);
+        P->prof = enable != 0;
+        P->recs.clear();
+        P->ev_used = 0;
+        for (int k = 0; k < MRA_NKCLASS; k++) { P->prof_ms[k] = 0; P->prof_cnt[k] = 0; }
+        return MRA_OK;
+    });
 }
 
 extern "C" mra_status mra_kernel_times(const mra_plan* P, double* ms, uint64_t* launches) {
-    if (!P) return fail(MRA_E_ARG, "plan is NULL");
-    for (int k = 0; k < MRA_NKCLASS; k++) {   // summed over the theta lanes
-        double t = P->prof_ms[k];
-        uint64_t c = P->prof_cnt[k];
-        for (const mra_plan* Q : P->lanes) { t += Q->prof_ms[k]; c += Q->prof_cnt[k]; }
-        if (ms) ms[k] = t;
-        if (launches) launches[k] = c;
-    }
-    return MRA_OK;
+    return guarded([&]() -> mra_status {
+        if (!P) return fail(MRA_E_ARG, "plan is NULL");
+        for (int k = 0; k < MRA_NKCLASS; k++) {   // summed over the theta lanes
+            double t = P->prof_ms[k];
+            uint64_t c = P->prof_cnt[k];
+            for (const mra_plan* Q : P->lanes) { t += Q->prof_ms[k]; c += Q->prof_cnt[k]; }
+            if (ms) ms[k] = t;
+            if (launches) launches[k] = c;
+        }
+        return MRA_OK;
+    });
 }
 
 // diagnostics of -DMRA_PHASE_TIMING builds (zeros otherwise): CTA-cycles per bottom-kernel phase
@@ -990,24 +1114,28 @@ extern "C" void mra_debug_phase_cycles(uint64_t* out32, int reset) {
 
 extern "C" mra_status mra_plan_memory(const mra_plan* P, int* streams_prior, int* chunk_level,
                                       uint64_t* chunk_regions, uint64_t* device_bytes) {
-    if (!P) return fail(MRA_E_ARG, "plan is NULL");
-    if (streams_prior) *streams_prior = P->stream ? 1 : 0;
-    if (chunk_level) *chunk_level = P->c;
-    if (chunk_regions) *chunk_regions = (uint64_t)P->Kc;
-    if (device_bytes) {
-        uint64_t b = P->dev_bytes;
-        for (const mra_plan* Q : P->lanes) b += Q->dev_bytes;   // theta lanes (NEXT-3)
-        *device_bytes = b;
-    }
-    return MRA_OK;
+    return guarded([&]() -> mra_status {
+        if (!P) return fail(MRA_E_ARG, "plan is NULL");
+        if (streams_prior) *streams_prior = P->stream ? 1 : 0;
+        if (chunk_level) *chunk_level = P->c;
+        if (chunk_regions) *chunk_regions = (uint64_t)P->Kc;
+        if (device_bytes) {
+            uint64_t b = P->dev_bytes;
+            for (const mra_plan* Q : P->lanes) b += Q->dev_bytes;   // theta lanes (NEXT-3)
+            *device_bytes = b;
+        }
+        return MRA_OK;
+    });
 }
 
 extern "C" mra_status mra_plan_shards(const mra_plan* P, int* shard_level, int64_t* own, uint64_t* n_own) {
-    if (!P) return fail(MRA_E_ARG, "plan is NULL");
-    if (shard_level) *shard_level = P->world > 1 ? P->c : 0;
-    if (n_own) *n_own = (uint64_t)P->my_c.size();
-    if (own) for (size_t i = 0; i < P->my_c.size(); i++) own[i] = P->my_c[i];
-    return MRA_OK;
+    return guarded([&]() -> mra_status {
+        if (!P) return fail(MRA_E_ARG, "plan is NULL");
+        if (shard_level) *shard_level = P->world > 1 ? P->c : 0;
+        if (n_own) *n_own = (uint64_t)P->my_c.size();
+        if (own) for (size_t i = 0; i < P->my_c.size(); i++) own[i] = P->my_c[i];
+        return MRA_OK;
+    });
 }
 
 // ------------------------------------------------------------------------ evaluation
@@ -1050,7 +1178,16 @@ static mra_status check_theta(const mra_theta* th) {
     } while (0)
 #define LCHK(expr) LCHK_K(KIND_OTHER, expr)
 
-static unsigned long long* take_counter(mra_plan* P) { return P->counters + (P->next_counter++ % P->n_counters); }
+// one zeroed work-queue counter per persistent launch. The array is zeroed per evaluation; an evaluation that
+// uses them all (very many chunks / sub-chunks) re-zeroes the array on the plan stream before reusing it --
+// stream order puts that memset after every earlier launch that counted with them
+static unsigned long long* take_counter(mra_plan* P) {
+    if (P->next_counter >= P->n_counters) {
+        cudaMemsetAsync(P->counters, 0, 8 * (size_t)P->n_counters, P->st);
+        P->next_counter = 0;
+    }
+    return P->counters + P->next_counter++;
+}
 
 // ranges of level-m regions under the level-c regions [a, b)
 static void range_at(const mra_plan* P, int m, long long a, long long b, long long* f, long long* cnt) {
@@ -1126,10 +1263,23 @@ static mra_status eval_lower(mra_plan* P, const TreeParams& tp0) {
     const TreeParams& tp = tp0;
     cudaStream_t st = P->st;
     auto runs = my_runs(P);
-    // prior: levels < c for every region, levels >= c for own subtrees (streaming plans: per chunk, below)
+    // prior: levels < c for every region, levels >= c for own subtrees (streaming plans: per chunk, below).
+    // With the in-library exchange, rank 0 computes the above-shard levels and broadcasts their chain rows
+    // (north_star: "ancestor W and K blocks are broadcast down with NCCL"); without it every rank
+    // replicates that small computation (21 regions for C3 at 8 GPUs)
     for (int m = 1; m < M; m++) {
+        if (m == c && P->nccl && c > 1) {
+            const NcclApi* nc = nccl_api();
+            const size_t cnt_top = (size_t)(P->prior_base[c] - P->prior_base[1]);   // levels 1..c-1, contiguous
+            if (cnt_top) {
+                const ncclResult_t r0 = nc->broadcast(P->prior + P->prior_base[1], P->prior + P->prior_base[1], cnt_top,
+                                                      ncclFloat64, 0, P->comm, st);
+                if (r0 != ncclSuccess) return fail(MRA_E_NCCL, std::string("ncclBroadcast(prior rows): ") + nc->errStr(r0));
+            }
+        }
         if (m >= c && P->stream) break;
         if (m < c) {
+            if (P->nccl && P->rank != 0) continue;   // received from rank 0 (above)
             TreeParams t2 = tp;
             LCHK_K(KIND_PRIOR, launch_prior(t2, m, 0, ipow(J, m - 1), P->grid, P->ws, P->ws_stride, take_counter(P), st));
         } else {
@@ -1295,9 +1445,15 @@ static bool all_finite(const double* y, uint64_t n) {
     return bad == 0;
 }
 
+static mra_status run_eval_nccl(mra_plan* P, const double* d_y, const mra_theta* th, double* loglik, mra_post* post,
+                                bool host_post);
+
 static mra_status run_eval(mra_plan* P, const double* d_y, const mra_theta* th, double* loglik, mra_post* post,
                            bool host_post) {
-    if (P->world > 1) return fail(MRA_E_CONFIG, "sharded plan: use mra_loglik_shard / mra_loglik_finish");
+    if (P->nccl) return run_eval_nccl(P, d_y, th, loglik, post, host_post);
+    if (P->world > 1)
+        return fail(MRA_E_CONFIG, "sharded plan without a communicator (opts.nccl_id): use mra_loglik_shard / "
+                                  "mra_loglik_finish");
     mra_status s;
     const bool want_state = post && (post->mu || post->smooth);
     if (want_state && (s = ensure_post(P))) return s;
@@ -1339,138 +1495,167 @@ static mra_status run_eval(mra_plan* P, const double* d_y, const mra_theta* th, 
 // ----------------------------------------------------------------------- prediction
 extern "C" mra_status mra_predict(mra_plan* P, const double* qx, const double* qy, uint64_t nq, double* mean,
                                   double* var) {
-    g_err.clear();
-    if (!P || !qx || !qy || !mean || !var) return fail(MRA_E_ARG, "NULL argument");
-    if (P->device < 0) return fail(MRA_E_CUDA, "host-only plan (device -2) cannot evaluate");
-    if (P->world > 1) return fail(MRA_E_CONFIG, "prediction on a sharded plan is not supported");
-    if (!P->post_valid)
-        return fail(MRA_E_ARG, "no posterior state: evaluate with posterior state (post->mu or post->smooth) first");
-    if (nq == 0) return MRA_OK;
-    if (cudaSetDevice(P->device) != cudaSuccess) return fail(MRA_E_CUDA, "cudaSetDevice failed");
-    const int M = P->M, J = P->J;
-    // leaf of each query by the plan's descent (half-open boxes); outside the root -> NaN
-    std::vector<long long> qleaf(nq);
-    for (uint64_t i = 0; i < nq; i++) {
-        const double px = qx[i], py = qy[i];
-        if (!std::isfinite(px) || !std::isfinite(py)) return fail(MRA_E_ARG, "non-finite query location");
-        if (!(px >= P->root[0] && px < P->root[1] && py >= P->root[2] && py < P->root[3])) { qleaf[i] = -1; continue; }
-        long long t = 0;
-        for (int m = 1; m < M; m++) {
-            const double* b = &P->box[4 * (lvl_first(J, m) + t)];
-            const double mx = 0.5 * (b[0] + b[1]), my = 0.5 * (b[2] + b[3]);
-            int c;
-            if (J == 4) c = (px >= mx ? 1 : 0) | (py >= my ? 2 : 0);
-            else if ((b[1] - b[0]) >= (b[3] - b[2])) c = px >= mx ? 1 : 0;
-            else c = py >= my ? 1 : 0;
-            t = t * J + c;
+    return guarded([&]() -> mra_status {
+        g_err.clear();
+        if (!P || !qx || !qy || !mean || !var) return fail(MRA_E_ARG, "NULL argument");
+        if (P->device < 0) return fail(MRA_E_CUDA, "host-only plan (device -2) cannot evaluate");
+        if (P->world > 1 && !P->nccl)
+            return fail(MRA_E_CONFIG, "prediction on a sharded plan needs the in-library exchange (opts.nccl_id)");
+        if (!P->post_valid)
+            return fail(MRA_E_ARG, "no posterior state: evaluate with posterior state (post->mu or post->smooth) first");
+        if (nq == 0) return MRA_OK;
+        if (cudaSetDevice(P->device) != cudaSuccess) return fail(MRA_E_CUDA, "cudaSetDevice failed");
+        const int M = P->M, J = P->J;
+        // leaf of each query by the plan's descent (half-open boxes); outside the root -> NaN
+        std::vector<long long> qleaf(nq);
+        for (uint64_t i = 0; i < nq; i++) {
+            const double px = qx[i], py = qy[i];
+            if (!std::isfinite(px) || !std::isfinite(py)) return fail(MRA_E_ARG, "non-finite query location");
+            if (!(px >= P->root[0] && px < P->root[1] && py >= P->root[2] && py < P->root[3])) { qleaf[i] = -1; continue; }
+            long long t = 0;
+            for (int m = 1; m < M; m++) {
+                const double* b = &P->box[4 * (lvl_first(J, m) + t)];
+                const double mx = 0.5 * (b[0] + b[1]), my = 0.5 * (b[2] + b[3]);
+                int c;
+                if (J == 4) c = (px >= mx ? 1 : 0) | (py >= my ? 2 : 0);
+                else if ((b[1] - b[0]) >= (b[3] - b[2])) c = px >= mx ? 1 : 0;
+                else c = py >= my ? 1 : 0;
+                t = t * J + c;
+            }
+            qleaf[i] = t;
         }
-        qleaf[i] = t;
-    }
-    std::vector<long long> qoff(P->nleaf + 1, 0);
-    for (uint64_t i = 0; i < nq; i++) if (qleaf[i] >= 0) qoff[qleaf[i] + 1]++;
-    std::vector<long long> leaves;
-    for (long long l = 0; l < P->nleaf; l++) {
-        if (qoff[l + 1]) leaves.push_back(l);
-        qoff[l + 1] += qoff[l];
-    }
-    const long long nin = qoff[P->nleaf];
-    std::vector<long long> fillp(qoff.begin(), qoff.end() - 1), qperm(std::max<long long>(nin, 1));
-    std::vector<double> qxy(2 * std::max<long long>(nin, 1));
-    for (uint64_t i = 0; i < nq; i++)
-        if (qleaf[i] >= 0) {
-            const long long d = fillp[qleaf[i]]++;
-            qperm[d] = (long long)i;
-            qxy[2 * d] = qx[i];
-            qxy[2 * d + 1] = qy[i];
+        std::vector<long long> qoff(P->nleaf + 1, 0);
+        for (uint64_t i = 0; i < nq; i++) if (qleaf[i] >= 0) qoff[qleaf[i] + 1]++;
+        // sharded plans: this rank predicts the queries of its own leaves; the others come from the all-reduce
+        std::vector<char> own_leaf;
+        if (P->nccl) {
+            own_leaf.assign(P->nleaf, 0);
+            const long long per = ipow(J, M - P->c);
+            for (long long t : P->my_c)
+                for (long long l = t * per; l < (t + 1) * per; l++) own_leaf[l] = 1;
         }
-    mra_status s;
-    // per-CTA workspace: the leaf's G, Sigma, inverted diagonal blocks, r, and the query tiles
-    if (!P->ws_pred) {
-        const int Pg = (M - 1) * P->rh;
-        WsLayout L{};
-        const long long mleaf = std::max<long long>(P->max_leaf, 1);
-        L.ldG = (int)round_up(Pg + 1, 2);
-        L.ldS = (int)round_up(mleaf, 2);
-        long long o = 0;
-        L.oG = o; o += round_up(mleaf * L.ldG, 32);
-        L.oS = o; o += round_up(mleaf * (long long)L.ldS, 32);
-        L.oD = o; o += ((mleaf + 63) / 64) * 4096;
-        L.oV = o; o += round_up(mleaf, 32);
-        L.oQ = o; o += round_up(64LL * L.ldG, 32);
-        L.oE = o; o += round_up(mleaf * 64, 32);
-        L.oW = o; o += round_up(64LL * L.ldG, 32);
-        L.oA = L.oF = L.oL = 0;
-        L.stride = round_up(o, 64);
-        size_t freeb = 0, totalb = 0;
-        cudaMemGetInfo(&freeb, &totalb);
-        long long slots = std::min<long long>(P->grid, std::max<long long>(1, (long long)(0.4 * freeb / (8.0 * L.stride))));
-        P->Lp = L;
-        P->pred_grid = (int)slots;
-        if ((s = dalloc(P, (void**)&P->ws_pred, 8 * L.stride * slots, "prediction workspace"))) return s;
-    }
-    double *d_qxy = nullptr, *d_mean = nullptr, *d_var = nullptr;
-    long long *d_qoff = nullptr, *d_qperm = nullptr, *d_leaves = nullptr;
-    auto release = [&]() {
-        cudaFree(d_qxy); cudaFree(d_mean); cudaFree(d_var); cudaFree(d_qoff); cudaFree(d_qperm); cudaFree(d_leaves);
-    };
-#define PCU(call)                                                                              \
-    do {                                                                                       \
-        cudaError_t e_ = (call);                                                               \
-        if (e_ != cudaSuccess) {                                                               \
-            release();                                                                         \
-            return fail(e_ == cudaErrorMemoryAllocation ? MRA_E_OOM : MRA_E_CUDA,              \
-                        std::string(#call) + ": " + cudaGetErrorString(e_));                   \
-        }                                                                                      \
-    } while (0)
-    PCU(cudaMalloc(&d_qxy, 16 * std::max<long long>(nin, 1)));
-    PCU(cudaMalloc(&d_mean, 8 * nq));
-    PCU(cudaMalloc(&d_var, 8 * nq));
-    PCU(cudaMalloc(&d_qoff, 8 * (P->nleaf + 1)));
-    PCU(cudaMalloc(&d_qperm, 8 * std::max<long long>(nin, 1)));
-    PCU(cudaMalloc(&d_leaves, 8 * std::max<size_t>(leaves.size(), 1)));
-    PCU(cudaMemcpyAsync(d_qxy, qxy.data(), 16 * std::max<long long>(nin, 1), cudaMemcpyHostToDevice, P->st));
-    PCU(cudaMemcpyAsync(d_qoff, qoff.data(), 8 * (P->nleaf + 1), cudaMemcpyHostToDevice, P->st));
-    PCU(cudaMemcpyAsync(d_qperm, qperm.data(), 8 * std::max<long long>(nin, 1), cudaMemcpyHostToDevice, P->st));
-    if (!leaves.empty())
-        PCU(cudaMemcpyAsync(d_leaves, leaves.data(), 8 * leaves.size(), cudaMemcpyHostToDevice, P->st));
-    PCU(launch_fill(d_mean, (long long)nq, NAN, P->st));
-    PCU(launch_fill(d_var, (long long)nq, NAN, P->st));
-    PCU(cudaMemsetAsync(P->err, 0, 16, P->st));
-    PCU(cudaMemsetAsync(P->counters, 0, 8, P->st));
-    TreeParams tp = tree_params(P, &P->post_theta);
-    tp.post = P->post;
-    PredParams pp{};
-    pp.qxy = d_qxy; pp.q_off = d_qoff; pp.q_perm = d_qperm; pp.leaves = d_leaves;
-    pp.n_leaves = (long long)leaves.size(); pp.muhat = P->muhat; pp.mean = d_mean; pp.var = d_var;
-    const unsigned long long k0 = g_kernel_launches;
-    PCU(launch_predict(tp, pp, P->pred_grid, P->ws_pred, P->Lp, P->counters, P->st));
-    P->launches = g_kernel_launches - k0;
-    PCU(cudaMemcpyAsync(mean, d_mean, 8 * nq, cudaMemcpyDeviceToHost, P->st));
-    PCU(cudaMemcpyAsync(var, d_var, 8 * nq, cudaMemcpyDeviceToHost, P->st));
-    int h[4];
-    PCU(cudaMemcpyAsync(h, P->err, 16, cudaMemcpyDeviceToHost, P->st));
-    PCU(cudaStreamSynchronize(P->st));
-#undef PCU
-    release();
-    if (h[0]) return fail(MRA_E_NUMERIC, "Cholesky failed while recomputing a leaf for prediction");
-    return MRA_OK;
+        std::vector<long long> leaves;
+        for (long long l = 0; l < P->nleaf; l++) {
+            if (qoff[l + 1] && (own_leaf.empty() || own_leaf[l])) leaves.push_back(l);
+            qoff[l + 1] += qoff[l];
+        }
+        const long long nin = qoff[P->nleaf];
+        std::vector<long long> fillp(qoff.begin(), qoff.end() - 1), qperm(std::max<long long>(nin, 1));
+        std::vector<double> qxy(2 * std::max<long long>(nin, 1));
+        for (uint64_t i = 0; i < nq; i++)
+            if (qleaf[i] >= 0) {
+                const long long d = fillp[qleaf[i]]++;
+                qperm[d] = (long long)i;
+                qxy[2 * d] = qx[i];
+                qxy[2 * d + 1] = qy[i];
+            }
+        mra_status s;
+        // per-CTA workspace: the leaf's G, Sigma, inverted diagonal blocks, r, and the query tiles
+        if (!P->ws_pred) {
+            const int Pg = (M - 1) * P->rh;
+            WsLayout L{};
+            const long long mleaf = std::max<long long>(P->max_leaf, 1);
+            L.ldG = (int)round_up(Pg + 1, 2);
+            L.ldS = (int)round_up(mleaf, 2);
+            long long o = 0;
+            L.oG = o; o += round_up(mleaf * L.ldG, 32);
+            L.oS = o; o += round_up(mleaf * (long long)L.ldS, 32);
+            L.oD = o; o += ((mleaf + 63) / 64) * 4096;
+            L.oV = o; o += round_up(mleaf, 32);
+            L.oQ = o; o += round_up(64LL * L.ldG, 32);
+            L.oE = o; o += round_up(mleaf * 64, 32);
+            L.oW = o; o += round_up(64LL * L.ldG, 32);
+            L.oA = L.oF = L.oL = 0;
+            L.stride = round_up(o, 64);
+            size_t freeb = 0, totalb = 0;
+            cudaMemGetInfo(&freeb, &totalb);
+            long long slots = std::min<long long>(P->grid, std::max<long long>(1, (long long)(0.4 * freeb / (8.0 * L.stride))));
+            P->Lp = L;
+            P->pred_grid = (int)slots;
+            if ((s = dalloc(P, (void**)&P->ws_pred, 8 * L.stride * slots, "prediction workspace"))) return s;
+        }
+        double *d_qxy = nullptr, *d_mean = nullptr, *d_var = nullptr;
+        long long *d_qoff = nullptr, *d_qperm = nullptr, *d_leaves = nullptr;
+        auto release = [&]() {
+            cudaStreamSynchronize(P->st);
+            for (void* v : {(void*)d_qxy, (void*)d_mean, (void*)d_var, (void*)d_qoff, (void*)d_qperm, (void*)d_leaves})
+                tfree(P, v);
+        };
+    #define PCU(call)                                                                              \
+        do {                                                                                       \
+            cudaError_t e_ = (call);                                                               \
+            if (e_ != cudaSuccess) {                                                               \
+                release();                                                                         \
+                return fail(e_ == cudaErrorMemoryAllocation ? MRA_E_OOM : MRA_E_CUDA,              \
+                            std::string(#call) + ": " + cudaGetErrorString(e_));                   \
+            }                                                                                      \
+        } while (0)
+        PCU(talloc(P, (void**)&d_qxy, 16 * std::max<long long>(nin, 1)));
+        PCU(talloc(P, (void**)&d_mean, 8 * nq));
+        PCU(talloc(P, (void**)&d_var, 8 * nq));
+        PCU(talloc(P, (void**)&d_qoff, 8 * (P->nleaf + 1)));
+        PCU(talloc(P, (void**)&d_qperm, 8 * std::max<long long>(nin, 1)));
+        PCU(talloc(P, (void**)&d_leaves, 8 * std::max<size_t>(leaves.size(), 1)));
+        PCU(cudaMemcpyAsync(d_qxy, qxy.data(), 16 * std::max<long long>(nin, 1), cudaMemcpyHostToDevice, P->st));
+        PCU(cudaMemcpyAsync(d_qoff, qoff.data(), 8 * (P->nleaf + 1), cudaMemcpyHostToDevice, P->st));
+        PCU(cudaMemcpyAsync(d_qperm, qperm.data(), 8 * std::max<long long>(nin, 1), cudaMemcpyHostToDevice, P->st));
+        if (!leaves.empty())
+            PCU(cudaMemcpyAsync(d_leaves, leaves.data(), 8 * leaves.size(), cudaMemcpyHostToDevice, P->st));
+        PCU(launch_fill(d_mean, (long long)nq, P->nccl ? 0.0 : NAN, P->st));
+        PCU(launch_fill(d_var, (long long)nq, P->nccl ? 0.0 : NAN, P->st));
+        PCU(cudaMemsetAsync(P->err, 0, 16, P->st));
+        PCU(cudaMemsetAsync(P->counters, 0, 8, P->st));
+        TreeParams tp = tree_params(P, &P->post_theta);
+        tp.post = P->post;
+        PredParams pp{};
+        pp.qxy = d_qxy; pp.q_off = d_qoff; pp.q_perm = d_qperm; pp.leaves = d_leaves;
+        pp.n_leaves = (long long)leaves.size(); pp.muhat = P->muhat; pp.mean = d_mean; pp.var = d_var;
+        const unsigned long long k0 = g_kernel_launches;
+        PCU(launch_predict(tp, pp, P->pred_grid, P->ws_pred, P->Lp, P->counters, P->st));
+        P->launches = g_kernel_launches - k0;
+        if (P->nccl) {
+            const NcclApi* nc = nccl_api();
+            ncclResult_t r0 = nc->allReduce(d_mean, d_mean, nq, ncclFloat64, ncclSum, P->comm, P->st);
+            if (r0 == ncclSuccess) r0 = nc->allReduce(d_var, d_var, nq, ncclFloat64, ncclSum, P->comm, P->st);
+            if (r0 != ncclSuccess) {
+                release();
+                return fail(MRA_E_NCCL, std::string("ncclAllReduce(prediction): ") + nc->errStr(r0));
+            }
+        }
+        PCU(cudaMemcpyAsync(mean, d_mean, 8 * nq, cudaMemcpyDeviceToHost, P->st));
+        PCU(cudaMemcpyAsync(var, d_var, 8 * nq, cudaMemcpyDeviceToHost, P->st));
+        int h[4];
+        PCU(cudaMemcpyAsync(h, P->err, 16, cudaMemcpyDeviceToHost, P->st));
+        PCU(cudaStreamSynchronize(P->st));
+    #undef PCU
+        release();
+        if (h[0]) return fail(MRA_E_NUMERIC, "Cholesky failed while recomputing a leaf for prediction");
+        if (P->nccl)
+            for (uint64_t i = 0; i < nq; i++)
+                if (qleaf[i] < 0) mean[i] = var[i] = NAN;
+        return MRA_OK;
+    });
 }
 
 extern "C" mra_status mra_loglik_dev(mra_plan* P, const double* d_y, const mra_theta* th, double* loglik,
                                      mra_post* post) {
-    if (!P || !d_y) return fail(MRA_E_ARG, "plan or y is NULL");
-    return run_eval(P, d_y, th, loglik, post, false);
+    return guarded([&]() -> mra_status {
+        if (!P || !d_y) return fail(MRA_E_ARG, "plan or y is NULL");
+        return run_eval(P, d_y, th, loglik, post, false);
+    });
 }
 
 extern "C" mra_status mra_loglik(mra_plan* P, const double* y, const mra_theta* th, double* loglik, mra_post* post) {
-    if (!P || !y) return fail(MRA_E_ARG, "plan or y is NULL");
-    if (P->device < 0) return fail(MRA_E_CUDA, "host-only plan (device -2) cannot evaluate");
-    if (!all_finite(y, P->n_in)) return fail(MRA_E_ARG, "non-finite observation value");
-    if (cudaSetDevice(P->device) != cudaSuccess) return fail(MRA_E_CUDA, "cudaSetDevice failed");
-    P->host_y_pending = y;   // copied by flush_host_y, overlapping the prior levels
-    const mra_status s = run_eval(P, P->zin, th, loglik, post, true);
-    P->host_y_pending = nullptr;
-    return s;
+    return guarded([&]() -> mra_status {
+        if (!P || !y) return fail(MRA_E_ARG, "plan or y is NULL");
+        if (P->device < 0) return fail(MRA_E_CUDA, "host-only plan (device -2) cannot evaluate");
+        if (!all_finite(y, P->n_in)) return fail(MRA_E_ARG, "non-finite observation value");
+        if (cudaSetDevice(P->device) != cudaSuccess) return fail(MRA_E_CUDA, "cudaSetDevice failed");
+        P->host_y_pending = y;   // copied by flush_host_y, overlapping the prior levels
+        const mra_status s = run_eval(P, P->zin, th, loglik, post, true);
+        P->host_y_pending = nullptr;
+        return s;
+    });
 }
 
 // one log-likelihood evaluation issued on the context's stream without waiting (theta lanes)
@@ -1490,61 +1675,65 @@ static mra_status finish_eval(mra_plan* P, double* loglik) {
 
 extern "C" mra_status mra_loglik_batch_dev(mra_plan* P, const double* d_y, const mra_theta* th, int n_theta,
                                            double* loglik) {
-    if (!P || !d_y || !th || !loglik || n_theta < 0) return fail(MRA_E_ARG, "bad arguments");
-    uint64_t total = 0;
-    const int L = std::min<int>(n_theta, 1 + (int)P->lanes.size());
-    if (L <= 1 || P->world > 1) {
-        for (int i = 0; i < n_theta; i++) {
-            mra_status s = run_eval(P, d_y, th + i, loglik + i, nullptr, false);
-            if (s) return s;
-            total += P->launches;
+    return guarded([&]() -> mra_status {
+        if (!P || !d_y || !th || !loglik || n_theta < 0) return fail(MRA_E_ARG, "bad arguments");
+        uint64_t total = 0;
+        const int L = std::min<int>(n_theta, 1 + (int)P->lanes.size());
+        if (L <= 1 || P->world > 1) {
+            for (int i = 0; i < n_theta; i++) {
+                mra_status s = run_eval(P, d_y, th + i, loglik + i, nullptr, false);
+                if (s) return s;
+                total += P->launches;
+            }
+            P->launches = total;
+            return MRA_OK;
         }
-        P->launches = total;
+        for (int i = 0; i < n_theta; i++)
+            if (mra_status s = check_theta(th + i)) return s;
+        if (cudaSetDevice(P->device) != cudaSuccess) return fail(MRA_E_CUDA, "cudaSetDevice failed");
+        // the lanes start after everything the caller queued on the plan stream (e.g. the write of y)
+        if (!P->lane_ev) CU(cudaEventCreateWithFlags(&P->lane_ev, cudaEventDisableTiming));
+        CU(cudaEventRecord(P->lane_ev, P->st));
+        for (mra_plan* Q : P->lanes) CU(cudaStreamWaitEvent(Q->st, P->lane_ev, 0));
+        auto lane = [&](int j) { return j == 0 ? P : P->lanes[j - 1]; };
+        for (int i0 = 0; i0 < n_theta; i0 += L) {
+            const int nb = std::min(L, n_theta - i0);
+            mra_status first = MRA_OK;
+            int issued = 0;
+            for (int j = 0; j < nb && !first; j++, issued++) first = issue_eval(lane(j), d_y, th + i0 + j);
+            for (int j = 0; j < issued; j++) {
+                mra_status s = finish_eval(lane(j), loglik + i0 + j);
+                if (!first) first = s;
+                total += lane(j)->launches;
+            }
+            if (first) return first;
+        }
+        P->launches = total;   // every launch of the sweep (mra_last_launches)
         return MRA_OK;
-    }
-    for (int i = 0; i < n_theta; i++)
-        if (mra_status s = check_theta(th + i)) return s;
-    if (cudaSetDevice(P->device) != cudaSuccess) return fail(MRA_E_CUDA, "cudaSetDevice failed");
-    // the lanes start after everything the caller queued on the plan stream (e.g. the write of y)
-    if (!P->lane_ev) CU(cudaEventCreateWithFlags(&P->lane_ev, cudaEventDisableTiming));
-    CU(cudaEventRecord(P->lane_ev, P->st));
-    for (mra_plan* Q : P->lanes) CU(cudaStreamWaitEvent(Q->st, P->lane_ev, 0));
-    auto lane = [&](int j) { return j == 0 ? P : P->lanes[j - 1]; };
-    for (int i0 = 0; i0 < n_theta; i0 += L) {
-        const int nb = std::min(L, n_theta - i0);
-        mra_status first = MRA_OK;
-        int issued = 0;
-        for (int j = 0; j < nb && !first; j++, issued++) first = issue_eval(lane(j), d_y, th + i0 + j);
-        for (int j = 0; j < issued; j++) {
-            mra_status s = finish_eval(lane(j), loglik + i0 + j);
-            if (!first) first = s;
-            total += lane(j)->launches;
-        }
-        if (first) return first;
-    }
-    P->launches = total;   // every launch of the sweep (mra_last_launches)
-    return MRA_OK;
+    });
 }
 
 extern "C" mra_status mra_loglik_batch(mra_plan* P, const double* y, const mra_theta* th, int n_theta,
                                        double* loglik) {
-    if (!P || !y || !th || !loglik || n_theta < 0) return fail(MRA_E_ARG, "bad arguments");
-    if (P->device < 0) return fail(MRA_E_CUDA, "host-only plan (device -2) cannot evaluate");
-    if (!all_finite(y, P->n_in)) return fail(MRA_E_ARG, "non-finite observation value");
-    if (cudaSetDevice(P->device) != cudaSuccess) return fail(MRA_E_CUDA, "cudaSetDevice failed");
-    if (n_theta == 0) return MRA_OK;
-    if (!P->lanes.empty()) {   // copied once; the lanes wait for it through the plan stream
-        CU(cudaMemcpyAsync(P->zin, y, 8 * P->n_in, cudaMemcpyHostToDevice, P->st));
-        return mra_loglik_batch_dev(P, P->zin, th, n_theta, loglik);
-    }
-    P->host_y_pending = y;   // copied once, during the first evaluation's prior levels
-    mra_status s = run_eval(P, P->zin, th, loglik, nullptr, false);
-    P->host_y_pending = nullptr;
-    if (s) return s;
-    const uint64_t first = P->launches;
-    s = mra_loglik_batch_dev(P, P->zin, th + 1, n_theta - 1, loglik + 1);
-    P->launches += first;
-    return s;
+    return guarded([&]() -> mra_status {
+        if (!P || !y || !th || !loglik || n_theta < 0) return fail(MRA_E_ARG, "bad arguments");
+        if (P->device < 0) return fail(MRA_E_CUDA, "host-only plan (device -2) cannot evaluate");
+        if (!all_finite(y, P->n_in)) return fail(MRA_E_ARG, "non-finite observation value");
+        if (cudaSetDevice(P->device) != cudaSuccess) return fail(MRA_E_CUDA, "cudaSetDevice failed");
+        if (n_theta == 0) return MRA_OK;
+        if (!P->lanes.empty()) {   // copied once; the lanes wait for it through the plan stream
+            CU(cudaMemcpyAsync(P->zin, y, 8 * P->n_in, cudaMemcpyHostToDevice, P->st));
+            return mra_loglik_batch_dev(P, P->zin, th, n_theta, loglik);
+        }
+        P->host_y_pending = y;   // copied once, during the first evaluation's prior levels
+        mra_status s = run_eval(P, P->zin, th, loglik, nullptr, false);
+        P->host_y_pending = nullptr;
+        if (s) return s;
+        const uint64_t first = P->launches;
+        s = mra_loglik_batch_dev(P, P->zin, th + 1, n_theta - 1, loglik + 1);
+        P->launches += first;
+        return s;
+    });
 }
 
 // ----------------------------------------------------------------------- optimization
@@ -1555,122 +1744,136 @@ extern "C" mra_status mra_loglik_batch(mra_plan* P, const double* y, const mra_t
 extern "C" mra_status mra_optimize(mra_plan* P, const double* d_y, mra_theta* theta, const double* lower,
                                    const double* upper, int max_evals, double tol, double* best_loglik,
                                    int* n_evals) {
-    if (!P || !d_y || !theta) return fail(MRA_E_ARG, "NULL argument");
-    if (P->world > 1) return fail(MRA_E_CONFIG, "optimization on a sharded plan is not supported");
-    mra_status s = check_theta(theta);
-    if (s) return s;
-    if (max_evals < 1) max_evals = 200;
-    if (!(tol > 0)) tol = 1e-6;
-    double lo[3], hi[3];
-    const double v0[3] = {theta->sigma2, theta->rho, theta->tau2};
-    for (int i = 0; i < 3; i++) {
-        lo[i] = lower ? std::log(lower[i]) : -INFINITY;
-        hi[i] = upper ? std::log(upper[i]) : INFINITY;
-        if (lower && upper && !(lower[i] > 0 && upper[i] >= lower[i])) return fail(MRA_E_ARG, "bad bounds");
-        if (std::log(v0[i]) < lo[i] || std::log(v0[i]) > hi[i]) return fail(MRA_E_ARG, "initial theta outside the bounds");
-    }
-    int evals = 0;
-    auto clampv = [&](double* v) { for (int i = 0; i < 3; i++) v[i] = std::min(hi[i], std::max(lo[i], v[i])); };
-    // objective: -log L (minimised); failures -> +inf
-    auto f = [&](const double* v, double* out) -> mra_status {
-        mra_theta th = *theta;
-        th.sigma2 = std::exp(v[0]); th.rho = std::exp(v[1]); th.tau2 = std::exp(v[2]);
-        double ll = NAN;
-        mra_status e = run_eval(P, d_y, &th, &ll, nullptr, false);
-        evals++;
-        if (e == MRA_E_NUMERIC || !std::isfinite(ll)) { *out = INFINITY; g_err.clear(); return MRA_OK; }
-        if (e) return e;
-        *out = -ll;
-        return MRA_OK;
-    };
-    // several independent points (initial simplex, shrink): one theta sweep, concurrent on a laned plan
-    auto f_many = [&](double (*Xs)[3], double* out, int n) -> mra_status {
-        if (!P->lanes.empty()) {
-            std::vector<mra_theta> ths(n, *theta);
-            for (int j = 0; j < n; j++) {
-                ths[j].sigma2 = std::exp(Xs[j][0]); ths[j].rho = std::exp(Xs[j][1]); ths[j].tau2 = std::exp(Xs[j][2]);
+    return guarded([&]() -> mra_status {
+        if (!P || !d_y || !theta) return fail(MRA_E_ARG, "NULL argument");
+        if (P->world > 1 && !P->nccl)
+            return fail(MRA_E_CONFIG, "optimization on a sharded plan needs the in-library exchange (opts.nccl_id)");
+        mra_status s = check_theta(theta);
+        if (s) return s;
+        if (max_evals < 1) max_evals = 200;
+        if (!(tol > 0)) tol = 1e-6;
+        double lo[3], hi[3];
+        const double v0[3] = {theta->sigma2, theta->rho, theta->tau2};
+        for (int i = 0; i < 3; i++) {
+            lo[i] = lower ? std::log(lower[i]) : -INFINITY;
+            hi[i] = upper ? std::log(upper[i]) : INFINITY;
+            if (lower && upper && !(lower[i] > 0 && upper[i] >= lower[i])) return fail(MRA_E_ARG, "bad bounds");
+            if (std::log(v0[i]) < lo[i] || std::log(v0[i]) > hi[i]) return fail(MRA_E_ARG, "initial theta outside the bounds");
+        }
+        int evals = 0;
+        auto clampv = [&](double* v) { for (int i = 0; i < 3; i++) v[i] = std::min(hi[i], std::max(lo[i], v[i])); };
+        // objective: -log L (minimised); failures -> +inf
+        auto f = [&](const double* v, double* out) -> mra_status {
+            mra_theta th = *theta;
+            th.sigma2 = std::exp(v[0]); th.rho = std::exp(v[1]); th.tau2 = std::exp(v[2]);
+            double ll = NAN;
+            mra_status e = run_eval(P, d_y, &th, &ll, nullptr, false);
+            evals++;
+            if (e == MRA_E_NUMERIC || !std::isfinite(ll)) { *out = INFINITY; g_err.clear(); return MRA_OK; }
+            if (e) return e;
+            *out = -ll;
+            return MRA_OK;
+        };
+        // several independent points (initial simplex, shrink): one theta sweep, concurrent on a laned plan
+        auto f_many = [&](double (*Xs)[3], double* out, int n) -> mra_status {
+            if (!P->lanes.empty()) {
+                std::vector<mra_theta> ths(n, *theta);
+                for (int j = 0; j < n; j++) {
+                    ths[j].sigma2 = std::exp(Xs[j][0]); ths[j].rho = std::exp(Xs[j][1]); ths[j].tau2 = std::exp(Xs[j][2]);
+                }
+                std::vector<double> ll(n, NAN);
+                if (mra_loglik_batch_dev(P, d_y, ths.data(), n, ll.data()) == MRA_OK) {
+                    bool ok = true;
+                    for (int j = 0; j < n; j++) ok = ok && std::isfinite(ll[j]);
+                    if (ok) {
+                        for (int j = 0; j < n; j++) out[j] = -ll[j];
+                        evals += n;
+                        return MRA_OK;
+                    }
+                }
+                g_err.clear();   // a failing point: evaluate one by one below (non-PD counts as +inf)
             }
-            std::vector<double> ll(n, NAN);
-            if (mra_loglik_batch_dev(P, d_y, ths.data(), n, ll.data()) == MRA_OK) {
-                bool ok = true;
-                for (int j = 0; j < n; j++) ok = ok && std::isfinite(ll[j]);
-                if (ok) {
-                    for (int j = 0; j < n; j++) out[j] = -ll[j];
-                    evals += n;
-                    return MRA_OK;
+            for (int j = 0; j < n; j++)
+                if (mra_status e = f(Xs[j], out + j)) return e;
+            return MRA_OK;
+        };
+        double X[4][3], F[4];
+        for (int j = 0; j < 4; j++) {
+            for (int i = 0; i < 3; i++) X[j][i] = std::log(v0[i]) + ((j == i + 1) ? 0.5 : 0.0);
+            clampv(X[j]);
+        }
+        if ((s = f_many(X, F, 4))) return s;
+        while (evals < max_evals) {
+            int ord[4] = {0, 1, 2, 3};
+            std::sort(ord, ord + 4, [&](int a, int b) { return F[a] < F[b]; });
+            double Xs[4][3], Fs[4];
+            for (int j = 0; j < 4; j++) { std::memcpy(Xs[j], X[ord[j]], sizeof Xs[j]); Fs[j] = F[ord[j]]; }
+            std::memcpy(X, Xs, sizeof X); std::memcpy(F, Fs, sizeof F);
+            double size = 0;
+            for (int j = 1; j < 4; j++)
+                for (int i = 0; i < 3; i++) size = std::max(size, std::fabs(X[j][i] - X[0][i]));
+            if (size < tol || (std::isfinite(F[3]) && std::fabs(F[3] - F[0]) <= tol * (1.0 + std::fabs(F[0])) && size < 1e3 * tol))
+                break;
+            double c[3] = {0, 0, 0};
+            for (int j = 0; j < 3; j++) for (int i = 0; i < 3; i++) c[i] += X[j][i] / 3.0;
+            double xr[3], fr;
+            for (int i = 0; i < 3; i++) xr[i] = c[i] + (c[i] - X[3][i]);
+            clampv(xr);
+            if ((s = f(xr, &fr))) return s;
+            if (fr < F[0]) {
+                double xe[3], fe;
+                for (int i = 0; i < 3; i++) xe[i] = c[i] + 2.0 * (c[i] - X[3][i]);
+                clampv(xe);
+                if ((s = f(xe, &fe))) return s;
+                if (fe < fr) { std::memcpy(X[3], xe, sizeof xe); F[3] = fe; }
+                else { std::memcpy(X[3], xr, sizeof xr); F[3] = fr; }
+            } else if (fr < F[2]) {
+                std::memcpy(X[3], xr, sizeof xr); F[3] = fr;
+            } else {
+                double xc[3], fc;
+                const bool outside = fr < F[3];
+                for (int i = 0; i < 3; i++) xc[i] = outside ? c[i] + 0.5 * (xr[i] - c[i]) : c[i] + 0.5 * (X[3][i] - c[i]);
+                clampv(xc);
+                if ((s = f(xc, &fc))) return s;
+                if (fc < (outside ? fr : F[3])) { std::memcpy(X[3], xc, sizeof xc); F[3] = fc; }
+                else {   // shrink towards the best vertex
+                    for (int j = 1; j < 4; j++)
+                        for (int i = 0; i < 3; i++) X[j][i] = X[0][i] + 0.5 * (X[j][i] - X[0][i]);
+                    if ((s = f_many(X + 1, F + 1, 3))) return s;
                 }
             }
-            g_err.clear();   // a failing point: evaluate one by one below (non-PD counts as +inf)
         }
-        for (int j = 0; j < n; j++)
-            if (mra_status e = f(Xs[j], out + j)) return e;
+        int b = 0;
+        for (int j = 1; j < 4; j++) if (F[j] < F[b]) b = j;
+        if (!std::isfinite(F[b])) return fail(MRA_E_NUMERIC, "no feasible parameter point found");
+        theta->sigma2 = std::exp(X[b][0]); theta->rho = std::exp(X[b][1]); theta->tau2 = std::exp(X[b][2]);
+        if (best_loglik) *best_loglik = -F[b];
+        if (n_evals) *n_evals = evals;
         return MRA_OK;
-    };
-    double X[4][3], F[4];
-    for (int j = 0; j < 4; j++) {
-        for (int i = 0; i < 3; i++) X[j][i] = std::log(v0[i]) + ((j == i + 1) ? 0.5 : 0.0);
-        clampv(X[j]);
-    }
-    if ((s = f_many(X, F, 4))) return s;
-    while (evals < max_evals) {
-        int ord[4] = {0, 1, 2, 3};
-        std::sort(ord, ord + 4, [&](int a, int b) { return F[a] < F[b]; });
-        double Xs[4][3], Fs[4];
-        for (int j = 0; j < 4; j++) { std::memcpy(Xs[j], X[ord[j]], sizeof Xs[j]); Fs[j] = F[ord[j]]; }
-        std::memcpy(X, Xs, sizeof X); std::memcpy(F, Fs, sizeof F);
-        double size = 0;
-        for (int j = 1; j < 4; j++)
-            for (int i = 0; i < 3; i++) size = std::max(size, std::fabs(X[j][i] - X[0][i]));
-        if (size < tol || (std::isfinite(F[3]) && std::fabs(F[3] - F[0]) <= tol * (1.0 + std::fabs(F[0])) && size < 1e3 * tol))
-            break;
-        double c[3] = {0, 0, 0};
-        for (int j = 0; j < 3; j++) for (int i = 0; i < 3; i++) c[i] += X[j][i] / 3.0;
-        double xr[3], fr;
-        for (int i = 0; i < 3; i++) xr[i] = c[i] + (c[i] - X[3][i]);
-        clampv(xr);
-        if ((s = f(xr, &fr))) return s;
-        if (fr < F[0]) {
-            double xe[3], fe;
-            for (int i = 0; i < 3; i++) xe[i] = c[i] + 2.0 * (c[i] - X[3][i]);
-            clampv(xe);
-            if ((s = f(xe, &fe))) return s;
-            if (fe < fr) { std::memcpy(X[3], xe, sizeof xe); F[3] = fe; }
-            else { std::memcpy(X[3], xr, sizeof xr); F[3] = fr; }
-        } else if (fr < F[2]) {
-            std::memcpy(X[3], xr, sizeof xr); F[3] = fr;
-        } else {
-            double xc[3], fc;
-            const bool outside = fr < F[3];
-            for (int i = 0; i < 3; i++) xc[i] = outside ? c[i] + 0.5 * (xr[i] - c[i]) : c[i] + 0.5 * (X[3][i] - c[i]);
-            clampv(xc);
-            if ((s = f(xc, &fc))) return s;
-            if (fc < (outside ? fr : F[3])) { std::memcpy(X[3], xc, sizeof xc); F[3] = fc; }
-            else {   // shrink towards the best vertex
-                for (int j = 1; j < 4; j++)
-                    for (int i = 0; i < 3; i++) X[j][i] = X[0][i] + 0.5 * (X[j][i] - X[0][i]);
-                if ((s = f_many(X + 1, F + 1, 3))) return s;
-            }
-        }
-    }
-    int b = 0;
-    for (int j = 1; j < 4; j++) if (F[j] < F[b]) b = j;
-    if (!std::isfinite(F[b])) return fail(MRA_E_NUMERIC, "no feasible parameter point found");
-    theta->sigma2 = std::exp(X[b][0]); theta->rho = std::exp(X[b][1]); theta->tau2 = std::exp(X[b][2]);
-    if (best_loglik) *best_loglik = -F[b];
-    if (n_evals) *n_evals = evals;
-    return MRA_OK;
+    });
 }
 
 // ------------------------------------------------------------------------ sharding
-extern "C" uint64_t mra_shard_size(const mra_plan* P) {
-    if (!P) return 0;
+// Exchange buffer (include/mra.h mra_shard_size): per level-c region the lower triangle of its q x q augmented
+// output packed row by row, then the regions' d, u, then one error flag -- zero outside this rank's slots, so
+// a sum-reduce over ranks assembles every region once (the paper's supervisor gather).
+static long long xbuf_len(const mra_plan* P) {
     const long long ns = ipow(P->J, P->c - 1), q = q_of(P->c, P->rh);
-    return (uint64_t)(ns * q * q + 2 * ns);
+    return ns * q * (q + 1) / 2 + 2 * ns + 1;
 }
 
-static mra_status shard_impl(mra_plan* P, const double* d_y, const mra_theta* th, double* d_xbuf, bool post) {
+extern "C" uint64_t mra_shard_size(const mra_plan* P) {
+    if (!P) return 0;
+    return (uint64_t)xbuf_len(P);
+}
+
+// this rank's subtrees, packed into d_xbuf. check = false (in-library exchange): a Cholesky failure is not
+// returned here but travels to rank 0 as the buffer's error flag, so no rank leaves the collectives early
+static mra_status shard_impl(mra_plan* P, const double* d_y, const mra_theta* th, double* d_xbuf, bool post,
+                             bool check) {
     if (!P || !d_y || !d_xbuf) return fail(MRA_E_ARG, "NULL argument");
     if (P->M < 2) return fail(MRA_E_CONFIG, "sharding needs M >= 2");
+    if (P->world <= 1 && !P->nccl) return fail(MRA_E_CONFIG, "not a sharded plan");
     mra_status s;
     if (post && (s = ensure_post(P))) return s;
     if ((s = begin_eval(P, d_y, th))) return s;
@@ -1681,12 +1884,9 @@ static mra_status shard_impl(mra_plan* P, const double* d_y, const mra_theta* th
     const long long ns = ipow(P->J, P->c - 1), q = q_of(P->c, P->rh);
     CU(cudaMemsetAsync(P->out_full[P->c], 0, 8 * ns * q * q, P->st));
     if ((s = eval_lower(P, tp))) return s;
-    // exchange buffer: [ns * q * q outputs][ns d][ns u]; only own slots are non-zero
-    CU(cudaMemcpyAsync(d_xbuf, P->out_full[P->c], 8 * ns * q * q, cudaMemcpyDeviceToDevice, P->st));
-    CU(cudaMemcpyAsync(d_xbuf + ns * q * q, P->dreg + lvl_first(P->J, P->c), 8 * ns, cudaMemcpyDeviceToDevice, P->st));
-    CU(cudaMemcpyAsync(d_xbuf + ns * q * q + ns, P->ureg + lvl_first(P->J, P->c), 8 * ns, cudaMemcpyDeviceToDevice,
-                       P->st));
-    if ((s = check_err(P))) return s;
+    const long long f = lvl_first(P->J, P->c);
+    LCHK(launch_pack_exchange(P->out_full[P->c], ns, (int)q, P->dreg + f, P->ureg + f, P->err, d_xbuf, P->st));
+    if (check && (s = check_err(P))) return s;
     if (post) {
         P->post_valid = true;   // the own subtrees' merge factors (Li, F) of this theta are kept
         P->post_theta = *th;
@@ -1695,13 +1895,15 @@ static mra_status shard_impl(mra_plan* P, const double* d_y, const mra_theta* th
 }
 
 extern "C" mra_status mra_loglik_shard(mra_plan* P, const double* d_y, const mra_theta* th, double* d_xbuf) {
-    return shard_impl(P, d_y, th, d_xbuf, false);
+    return guarded([&]() -> mra_status { return shard_impl(P, d_y, th, d_xbuf, false, true); });
 }
 
 extern "C" mra_status mra_loglik_shard_post(mra_plan* P, const double* d_y, const mra_theta* th, double* d_xbuf) {
-    return shard_impl(P, d_y, th, d_xbuf, true);
+    return guarded([&]() -> mra_status { return shard_impl(P, d_y, th, d_xbuf, true, true); });
 }
 
+// rank 0: the reduced buffer -> merges of the levels above the shard level -> log L (and the above-shard
+// posterior means into d_mutop). The caller's stream order makes the buffer complete before this runs.
 static mra_status finish_impl(mra_plan* P, const mra_theta* th, const double* d_xbuf, double* loglik,
                               double* d_mutop) {
     if (!P || !d_xbuf) return fail(MRA_E_ARG, "NULL argument");
@@ -1709,21 +1911,25 @@ static mra_status finish_impl(mra_plan* P, const mra_theta* th, const double* d_
     mra_status s = check_theta(th);
     if (s) return s;
     if (cudaSetDevice(P->device) != cudaSuccess) return fail(MRA_E_CUDA, "cudaSetDevice failed");
+    const long long ns = ipow(P->J, P->c - 1), q = q_of(P->c, P->rh);
+    double flag = 0.0;
+    CU(cudaMemcpyAsync(&flag, d_xbuf + xbuf_len(P) - 1, 8, cudaMemcpyDeviceToHost, P->st));
+    CU(cudaStreamSynchronize(P->st));
+    if (flag != 0.0)
+        return fail(MRA_E_NUMERIC, "Cholesky failed (matrix not positive definite) in the subtrees of "
+                                   + std::to_string((long long)flag) + " shard(s)");
     if (d_mutop && (s = ensure_post(P))) return s;
     TreeParams tp = tree_params(P, th);
     if (d_mutop) tp.post = P->post;
-    const long long ns = ipow(P->J, P->c - 1), q = q_of(P->c, P->rh);
-    CU(cudaMemcpyAsync(P->out_full[P->c], d_xbuf, 8 * ns * q * q, cudaMemcpyDeviceToDevice, P->st));
-    CU(cudaMemcpyAsync(P->dreg + lvl_first(P->J, P->c), d_xbuf + ns * q * q, 8 * ns, cudaMemcpyDeviceToDevice, P->st));
-    CU(cudaMemcpyAsync(P->ureg + lvl_first(P->J, P->c), d_xbuf + ns * q * q + ns, 8 * ns, cudaMemcpyDeviceToDevice,
-                       P->st));
+    const long long f = lvl_first(P->J, P->c);
+    LCHK(launch_unpack_exchange(d_xbuf, ns, (int)q, P->out_full[P->c], P->dreg + f, P->ureg + f, P->st));
     if ((s = eval_upper(P, tp))) return s;
     double ll = NAN;
     CU(cudaMemcpyAsync(&ll, P->loglik_d, 8, cudaMemcpyDeviceToHost, P->st));
     if (d_mutop) {
         // posterior means of the levels above the shard level (merged here), to be broadcast
         for (int m = 1; m < P->c; m++) LCHK(launch_mu(tp, m, P->muhat, P->mu_d, 0, ipow(P->J, m - 1), P->st));
-        const long long top = lvl_first(P->J, P->c) * P->rh;
+        const long long top = f * P->rh;
         if (top > 0) {
             CU(cudaMemcpyAsync(d_mutop, P->muhat, 8 * top, cudaMemcpyDeviceToDevice, P->st));
             CU(cudaMemcpyAsync(d_mutop + top, P->mu_d, 8 * top, cudaMemcpyDeviceToDevice, P->st));
@@ -1735,36 +1941,34 @@ static mra_status finish_impl(mra_plan* P, const mra_theta* th, const double* d_
 }
 
 extern "C" mra_status mra_loglik_finish(mra_plan* P, const mra_theta* th, const double* d_xbuf, double* loglik) {
-    return finish_impl(P, th, d_xbuf, loglik, nullptr);
+    return guarded([&]() -> mra_status { return finish_impl(P, th, d_xbuf, loglik, nullptr); });
 }
 
 extern "C" uint64_t mra_mutop_size(const mra_plan* P) {
-    if (!P || P->world <= 1) return 0;
+    if (!P || (P->world <= 1 && !P->nccl)) return 0;
     return (uint64_t)(2 * lvl_first(P->J, P->c) * P->rh);
 }
 
 extern "C" mra_status mra_loglik_finish_post(mra_plan* P, const mra_theta* th, const double* d_xbuf, double* loglik,
                                              double* d_mutop) {
-    if (!d_mutop && P && P->c > 1) return fail(MRA_E_ARG, "d_mutop is NULL");
-    return finish_impl(P, th, d_xbuf, loglik, d_mutop ? d_mutop : nullptr);
+    return guarded([&]() -> mra_status {
+        if (!d_mutop && P && P->c > 1) return fail(MRA_E_ARG, "d_mutop is NULL");
+        return finish_impl(P, th, d_xbuf, loglik, d_mutop);
+    });
 }
 
-// every rank, after receiving the levels above the shard level: posterior means of its own subtrees'
-// regions and the smoothed values of its own observations (S6 for G > 1)
-extern "C" mra_status mra_posterior_shard(mra_plan* P, const double* d_mutop, double* d_mu, double* d_smooth) {
-    g_err.clear();
-    if (!P || (!d_mutop && P->c > 1)) return fail(MRA_E_ARG, "NULL argument");
-    if (P->world <= 1) return fail(MRA_E_CONFIG, "not a sharded plan");
+// every rank, after receiving the levels above the shard level: posterior means of its own subtrees' regions
+// and the smoothed values of its own observations (S6 for G > 1). fill = value of the entries
+// this rank does not own (NaN for the caller-driven API; 0 when the in-library exchange all-reduces them)
+static mra_status posterior_local(mra_plan* P, const double* d_mutop, double fill) {
     if (!P->post_valid) return fail(MRA_E_ARG, "no posterior state: run mra_loglik_shard_post first");
-    if (cudaSetDevice(P->device) != cudaSuccess) return fail(MRA_E_CUDA, "cudaSetDevice failed");
-    P->launches = 0;
     P->next_counter = 0;
     CU(cudaMemsetAsync(P->counters, 0, 8 * (size_t)P->n_counters, P->st));
     CU(cudaMemsetAsync(P->err, 0, 16, P->st));
     TreeParams tp = tree_params(P, &P->post_theta);
     tp.post = P->post;
     const long long top = lvl_first(P->J, P->c) * P->rh, nmu = P->nint * P->rh;
-    LCHK(launch_fill(P->mu_d, std::max<long long>(nmu, 1), NAN, P->st));
+    LCHK(launch_fill(P->mu_d, std::max<long long>(nmu, 1), fill, P->st));
     if (top > 0) {
         CU(cudaMemcpyAsync(P->muhat, d_mutop, 8 * top, cudaMemcpyDeviceToDevice, P->st));
         CU(cudaMemcpyAsync(P->mu_d, d_mutop + top, 8 * top, cudaMemcpyDeviceToDevice, P->st));
@@ -1776,16 +1980,142 @@ extern "C" mra_status mra_posterior_shard(mra_plan* P, const double* d_mutop, do
             range_at(P, m, rg.first, rg.second, &f, &cnt);
             LCHK(launch_mu(tp, m, P->muhat, P->mu_d, f, cnt, P->st));
         }
-    LCHK(launch_fill(P->smooth_d, (long long)P->n_in, NAN, P->st));
+    LCHK(launch_fill(P->smooth_d, (long long)P->n_in, fill, P->st));
     const long long per = ipow(P->J, P->M - P->c);
     for (auto& rg : runs)
         LCHK(launch_smooth(tp, P->muhat, P->perm_d, P->smooth_d, P->wide ? P->smooth_grid : P->grid,
                            P->wide ? P->ws_smooth : P->ws, P->wide ? P->Ls : P->L, take_counter(P), rg.first * per,
                            (rg.second - rg.first) * per, P->st));
-    mra_status s = check_err(P);
-    if (s) return s;
-    if (d_mu && nmu) CU(cudaMemcpyAsync(d_mu, P->mu_d, 8 * nmu, cudaMemcpyDeviceToDevice, P->st));
-    if (d_smooth) CU(cudaMemcpyAsync(d_smooth, P->smooth_d, 8 * P->n_in, cudaMemcpyDeviceToDevice, P->st));
-    CU(cudaStreamSynchronize(P->st));
+    return check_err(P);
+}
+
+extern "C" mra_status mra_posterior_shard(mra_plan* P, const double* d_mutop, double* d_mu, double* d_smooth) {
+    return guarded([&]() -> mra_status {
+        g_err.clear();
+        if (!P || (!d_mutop && P->c > 1)) return fail(MRA_E_ARG, "NULL argument");
+        if (P->world <= 1 && !P->nccl) return fail(MRA_E_CONFIG, "not a sharded plan");
+        if (cudaSetDevice(P->device) != cudaSuccess) return fail(MRA_E_CUDA, "cudaSetDevice failed");
+        P->launches = 0;
+        mra_status s = posterior_local(P, d_mutop, NAN);
+        if (s) return s;
+        const long long nmu = P->nint * P->rh;
+        if (d_mu && nmu) CU(cudaMemcpyAsync(d_mu, P->mu_d, 8 * nmu, cudaMemcpyDeviceToDevice, P->st));
+        if (d_smooth) CU(cudaMemcpyAsync(d_smooth, P->smooth_d, 8 * P->n_in, cudaMemcpyDeviceToDevice, P->st));
+        CU(cudaStreamSynchronize(P->st));
+        return MRA_OK;
+    });
+}
+
+// ------------------------------------------------------- in-library exchange (opts.nccl_id)
+#define NC(call, what)                                                                          \
+    do {                                                                                        \
+        const ncclResult_t r_ = (call);                                                         \
+        if (r_ != ncclSuccess) return fail(MRA_E_NCCL, std::string(what) + ": " + nc->errStr(r_)); \
+    } while (0)
+
+// One sharded evaluation with the exchange step inside the library: every rank runs its
+// subtrees (the above-shard prior rows arrive by broadcast inside eval_lower), the packed shard outputs are
+// sum-reduced to rank 0, rank 0 merges the levels above the shard level, log L / d / u / the error flag are
+// broadcast, and -- when posterior state is requested -- the above-shard means (and merge factors, for
+// prediction) are broadcast and each rank's own means / smoothed values are all-reduced into full arrays.
+static mra_status run_eval_nccl(mra_plan* P, const double* d_y, const mra_theta* th, double* loglik, mra_post* post,
+                                bool host_post) {
+    const NcclApi* nc = nccl_api();
+    if (!nc || !P->comm) return fail(MRA_E_NCCL, "plan has no communicator");
+    const bool want_state = post && (post->mu || post->smooth);
+    mra_status s;
+    if (want_state && (s = ensure_post(P))) return s;
+    if (want_state && !P->mutop) {
+        if ((s = dalloc(P, (void**)&P->mutop, 8 * std::max<uint64_t>(1, mra_mutop_size(P)), "mutop"))) return s;
+        if ((s = dalloc(P, (void**)&P->sm_sorted, 8 * std::max<long long>(1, P->N), "sorted smoothing"))) return s;
+    }
+    if ((s = shard_impl(P, d_y, th, P->xbuf, want_state, false))) return s;
+    cudaStream_t st = P->st;
+    const size_t xl = (size_t)xbuf_len(P);
+    NC(nc->reduce(P->xbuf, P->xbuf, xl, ncclFloat64, ncclSum, 0, P->comm, st), "ncclReduce(shard outputs)");
+    double hv[4] = {NAN, 0.0, NAN, NAN};
+    if (P->rank == 0) {
+        const mra_status fs = finish_impl(P, th, P->xbuf, &hv[0], want_state ? P->mutop : nullptr);
+        if (fs == MRA_E_NUMERIC) {
+            hv[1] = 1.0;
+        } else if (fs) {
+            hv[1] = 2.0;   // other ranks report a generic failure; rank 0 returns its own status below
+        } else {
+            CU(cudaMemcpy(&hv[2], P->dreg, 8, cudaMemcpyDeviceToHost));
+            CU(cudaMemcpy(&hv[3], P->ureg, 8, cudaMemcpyDeviceToHost));
+        }
+        CU(cudaMemcpyAsync(P->bcast, hv, 32, cudaMemcpyHostToDevice, st));
+        NC(nc->broadcast(P->bcast, P->bcast, 4, ncclFloat64, 0, P->comm, st), "ncclBroadcast(log L)");
+        CU(cudaStreamSynchronize(st));
+        if (fs) return fs;
+    } else {
+        NC(nc->broadcast(P->bcast, P->bcast, 4, ncclFloat64, 0, P->comm, st), "ncclBroadcast(log L)");
+        CU(cudaMemcpyAsync(hv, P->bcast, 32, cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        if (P->prof) prof_collect(P);
+        if (hv[1] == 1.0) return fail(MRA_E_NUMERIC, "Cholesky failed (matrix not positive definite) on some rank");
+        if (hv[1] != 0.0) return fail(MRA_E_CUDA, "rank 0 failed to merge the levels above the shard level");
+    }
+    if (loglik) *loglik = hv[0];
+    if (post) {
+        post->d = hv[2];
+        post->u = hv[3];
+        if (post->region_d || post->region_u) {
+            // every region once: own subtrees on their rank, the shard level and above on rank 0
+            const long long f = lvl_first(P->J, P->c), ns = ipow(P->J, P->c - 1);
+            if (P->rank != 0) {
+                CU(cudaMemsetAsync(P->dreg, 0, 8 * (f + ns), st));
+                CU(cudaMemsetAsync(P->ureg, 0, 8 * (f + ns), st));
+            }
+            NC(nc->allReduce(P->dreg, P->dreg, (size_t)P->nreg, ncclFloat64, ncclSum, P->comm, st), "ncclAllReduce(d_R)");
+            NC(nc->allReduce(P->ureg, P->ureg, (size_t)P->nreg, ncclFloat64, ncclSum, P->comm, st), "ncclAllReduce(u_R)");
+            if (post->region_d) CU(cudaMemcpyAsync(post->region_d, P->dreg, 8 * P->nreg, cudaMemcpyDeviceToHost, st));
+            if (post->region_u) CU(cudaMemcpyAsync(post->region_u, P->ureg, 8 * P->nreg, cudaMemcpyDeviceToHost, st));
+            CU(cudaStreamSynchronize(st));
+        }
+    }
+    if (!want_state) return MRA_OK;
+    // above-shard means, and the above-shard merge factors (Ltilde^{-1}, F) that prediction walks through
+    const uint64_t nmt = mra_mutop_size(P);
+    if (nmt) NC(nc->broadcast(P->mutop, P->mutop, nmt, ncclFloat64, 0, P->comm, st), "ncclBroadcast(mu top)");
+    const long long ptop = P->post_base[P->c] - P->post_base[1];
+    if (ptop > 0)
+        NC(nc->broadcast(P->post + P->post_base[1], P->post + P->post_base[1], (size_t)ptop, ncclFloat64, 0, P->comm, st),
+           "ncclBroadcast(top merge factors)");
+    if ((s = posterior_local(P, P->mutop, 0.0))) return s;
+    // full arrays on every rank: mu by a sum over ranks (rank 0 alone contributes the above-shard levels), the
+    // smoothed values through the leaf order (so observations eliminated at knots come back as NaN)
+    const long long top = lvl_first(P->J, P->c) * P->rh, nmu = P->nint * P->rh;
+    if (P->rank != 0 && top > 0) CU(cudaMemsetAsync(P->mu_d, 0, 8 * top, st));
+    if (nmu) NC(nc->allReduce(P->mu_d, P->mu_d, (size_t)nmu, ncclFloat64, ncclSum, P->comm, st), "ncclAllReduce(mu)");
+    CU(cudaMemsetAsync(P->sm_sorted, 0, 8 * P->N, st));
+    const long long per = ipow(P->J, P->M - P->c);
+    for (auto& rg : my_runs(P)) {
+        const long long o0 = P->leaf_off[rg.first * per], o1 = P->leaf_off[rg.second * per];
+        if (o1 > o0) LCHK(launch_gather(P->smooth_d, P->perm_d + o0, P->sm_sorted + o0, o1 - o0, st));
+    }
+    NC(nc->allReduce(P->sm_sorted, P->sm_sorted, (size_t)P->N, ncclFloat64, ncclSum, P->comm, st),
+       "ncclAllReduce(smoothing)");
+    LCHK(launch_fill(P->smooth_d, (long long)P->n_in, NAN, st));
+    LCHK(launch_scatter(P->sm_sorted, P->perm_d, P->smooth_d, P->N, st));
+    const cudaMemcpyKind k = host_post ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    if (post->mu && nmu) CU(cudaMemcpyAsync(post->mu, P->mu_d, 8 * nmu, k, st));
+    if (post->smooth) CU(cudaMemcpyAsync(post->smooth, P->smooth_d, 8 * P->n_in, k, st));
+    CU(cudaStreamSynchronize(st));
+    P->post_valid = true;
+    P->post_theta = *th;
     return MRA_OK;
+}
+
+extern "C" mra_status mra_nccl_unique_id(void* id_out) {
+    return guarded([&]() -> mra_status {
+        g_err.clear();
+        if (!id_out) return fail(MRA_E_ARG, "id_out is NULL");
+        const NcclApi* nc = nccl_api();
+        if (!nc) return fail(MRA_E_NCCL, "no NCCL library could be loaded (libnccl.so.2 / $MRA_NCCL_LIB)");
+        ncclUniqueId id;
+        NC(nc->getUniqueId(&id), "ncclGetUniqueId");
+        std::memcpy(id_out, &id, sizeof id);
+        return MRA_OK;
+    });
 }

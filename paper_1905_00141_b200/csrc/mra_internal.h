@@ -101,6 +101,12 @@ cudaError_t launch_smooth(const TreeParams& tp, const double* muhat, const long 
                           int grid, double* ws, const WsLayout& L, unsigned long long* counter, long long l_first,
                           long long l_count, cudaStream_t st);
 cudaError_t launch_fill(double* p, long long n, double v, cudaStream_t st);
+cudaError_t launch_scatter(const double* zs, const long long* perm, double* z, long long N, cudaStream_t st);
+// exchange buffer of subtree sharding (packed lower triangles, d, u, error flag; include/mra.h)
+cudaError_t launch_pack_exchange(const double* out, long long ns, int q, const double* d, const double* u,
+                                 const int* err, double* xbuf, cudaStream_t st);
+cudaError_t launch_unpack_exchange(const double* xbuf, long long ns, int q, double* out, double* d, double* u,
+                                   cudaStream_t st);
 cudaError_t launch_predict(const TreeParams& tp, const PredParams& pp, int grid, double* ws, const WsLayout& L,
                            unsigned long long* counter, cudaStream_t st);
 // wide path: phase 0 chain, 1 sigma, 2 column update (step), 3 diagonal (step), 4 panel + X row (step),
@@ -137,7 +143,7 @@ cudaError_t plan_gather(const double* x, const double* y, const int* idx, long l
                         cudaStream_t st);
 int smem_bytes();
 int resident_ctas_per_sm();   // engine kernels (k_bottom occupancy)
-extern unsigned long long g_kernel_launches;   // host-side count of every kernel this library launched
+extern thread_local unsigned long long g_kernel_launches;   // host-side count of every kernel this library launched
 void phase_cycles(unsigned long long* out32, bool reset);   // -DMRA_PHASE_TIMING builds only
 
 }  // namespace mra

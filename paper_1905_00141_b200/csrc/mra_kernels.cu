@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
 
 #include "mra_device.cuh"
 #include "mra_internal.h"
@@ -172,6 +173,58 @@ __global__ void k_gather(const double* z, const long long* perm, double* zs, lon
 __global__ void k_fill(double* p, long long n, double v) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
         p[i] = v;
+}
+
+__global__ void k_scatter(const double* zs, const long long* perm, double* z, long long N) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x)
+        z[perm[i]] = zs[i];
+}
+
+// ------------------------------------------------------------- exchange buffer (subtree sharding)
+// packed layout (include/mra.h mra_shard_size): ns lower triangles of q x q, row by row (i(i+1)/2 + j),
+// then d[ns], u[ns], then one error flag. Row of packed index r: i = floor((sqrt(8r+1)-1)/2), fixed up
+// in integers (the fp64 estimate is exact or off by one for r < 2^50).
+__device__ __forceinline__ void tri_rc(long long r, int* i, int* j) {
+    long long ii = (long long)((sqrt(8.0 * (double)r + 1.0) - 1.0) * 0.5);
+    while (ii * (ii + 1) / 2 > r) ii--;
+    while ((ii + 1) * (ii + 2) / 2 <= r) ii++;
+    *i = (int)ii;
+    *j = (int)(r - ii * (ii + 1) / 2);
+}
+__global__ void k_pack_exchange(const double* out, long long ns, int q, const double* d, const double* u,
+                                const int* err, double* xbuf) {
+    const long long qq = (long long)q * (q + 1) / 2, tot = ns * qq;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot + 2 * ns + 1;
+         e += (long long)gridDim.x * blockDim.x) {
+        if (e < tot) {
+            const long long t = e / qq;
+            int i, j;
+            tri_rc(e - t * qq, &i, &j);
+            xbuf[e] = out[t * q * q + (long long)i * q + j];
+        } else if (e < tot + ns) {
+            xbuf[e] = d[e - tot];
+        } else if (e < tot + 2 * ns) {
+            xbuf[e] = u[e - tot - ns];
+        } else {
+            xbuf[e] = err[0] ? 1.0 : 0.0;
+        }
+    }
+}
+__global__ void k_unpack_exchange(const double* xbuf, long long ns, int q, double* out, double* d, double* u) {
+    const long long qq = (long long)q * (q + 1) / 2, tot = ns * qq;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot + 2 * ns;
+         e += (long long)gridDim.x * blockDim.x) {
+        if (e < tot) {
+            const long long t = e / qq;
+            int i, j;
+            tri_rc(e - t * qq, &i, &j);
+            out[t * q * q + (long long)i * q + j] = xbuf[e];
+        } else if (e < tot + ns) {
+            d[e - tot] = xbuf[e];
+        } else {
+            u[e - tot - ns] = xbuf[e];
+        }
+    }
 }
 
 // ----------------------------------------------------------------- posterior state
@@ -475,7 +528,9 @@ k_wide_covfill(TreeParams tp, WideParams wp, const int4* tasks, long long ntask)
 int smem_bytes() { return SMEM_DBL * (int)sizeof(double); }
 int resident_ctas_per_sm();
 
-unsigned long long g_kernel_launches = 0;
+// per host thread: a plan is single-entrant and a call runs on the calling thread, so the difference of this
+// counter around a call is exactly that call's launches even when other threads drive other plans
+thread_local unsigned long long g_kernel_launches = 0;
 
 void phase_cycles(unsigned long long* out32, bool reset) {
     cudaMemcpyFromSymbol(out32, g_phase_cycles, sizeof(unsigned long long) * 32);
@@ -485,29 +540,49 @@ void phase_cycles(unsigned long long* out32, bool reset) {
     }
 }
 
-static bool g_attr_done = false;
-static int g_resident[12] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1};   // resident CTAs per SM x SM count
-static void set_attrs() {
-    if (g_attr_done) return;
+// occupancy and the >48 KB dynamic-smem attribute are per device: cached per device ordinal (a plan may
+// live on any device of the process, opts.device), computed once under a lock
+constexpr int MAXDEV = 64;
+struct DevAttrs {
+    bool done = false;
+    int resident[12] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1};   // resident CTAs per SM x SM count
+    int cf_prior = 1, cf_wide = 1;                             // covariance-fill grids
+};
+static DevAttrs g_dev_attrs[MAXDEV];
+static std::mutex g_attr_mu;
+static const DevAttrs& set_attrs() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= MAXDEV) dev = 0;
+    DevAttrs& A = g_dev_attrs[dev];
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    if (A.done) return A;
     const int b = smem_bytes();
     const void* ks[12] = {(const void*)k_bottom,      (const void*)k_bottom,      (const void*)k_bottom,
                           (const void*)k_smooth,      (const void*)k_bottom,       (const void*)k_bottom,
                           (const void*)k_bottom,       (const void*)k_bottom,       (const void*)k_bottom,
                           (const void*)k_bottom,       (const void*)k_bottom,       (const void*)k_predict};
-    int dev = 0, nsm = 148;
-    cudaGetDevice(&dev);
+    int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     for (int i = 0; i < 12; i++) {
         cudaFuncSetAttribute(ks[i], cudaFuncAttributeMaxDynamicSharedMemorySize, b);
         int per = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ks[i], NT, b);
-        g_resident[i] = (per > 0 ? per : 1) * nsm;
+        A.resident[i] = (per > 0 ? per : 1) * nsm;
     }
-    g_attr_done = true;
+    int per = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_prior_covfill, CFT, 0);
+    A.cf_prior = (per > 0 ? per : 1) * nsm;
+    per = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_wide_covfill, CFT, 0);
+    A.cf_wide = (per > 0 ? per : 1) * nsm;
+    A.done = true;
+    return A;
 }
 // persistent grid: never more CTAs than can be resident at once (they pull work from a queue)
 static int clamp_grid(int grid, long long items, int kidx) {
-    if (grid > g_resident[kidx]) grid = g_resident[kidx];
+    const int res = set_attrs().resident[kidx];
+    if (grid > res) grid = res;
     if (items < grid) grid = (int)items;
     return grid;
 }
@@ -520,6 +595,30 @@ cudaError_t launch_gather(const double* z, const long long* perm, double* zs, lo
     k_gather<<<(int)blocks, 256, 0, st>>>(z, perm, zs, N);
     return cudaGetLastError();
 }
+cudaError_t launch_scatter(const double* zs, const long long* perm, double* z, long long N, cudaStream_t st) {
+    long long blocks = (N + 255) / 256;
+    if (blocks > 4096) blocks = 4096;
+    if (blocks < 1) blocks = 1;
+    ++g_kernel_launches;
+    k_scatter<<<(int)blocks, 256, 0, st>>>(zs, perm, z, N);
+    return cudaGetLastError();
+}
+cudaError_t launch_pack_exchange(const double* out, long long ns, int q, const double* d, const double* u,
+                                 const int* err, double* xbuf, cudaStream_t st) {
+    const long long n = ns * (long long)q * (q + 1) / 2 + 2 * ns + 1;
+    const long long blocks = std::min<long long>(4096, (n + 255) / 256);
+    ++g_kernel_launches;
+    k_pack_exchange<<<(int)blocks, 256, 0, st>>>(out, ns, q, d, u, err, xbuf);
+    return cudaGetLastError();
+}
+cudaError_t launch_unpack_exchange(const double* xbuf, long long ns, int q, double* out, double* d, double* u,
+                                   cudaStream_t st) {
+    const long long n = ns * (long long)q * (q + 1) / 2 + 2 * ns;
+    const long long blocks = std::min<long long>(4096, (n + 255) / 256);
+    ++g_kernel_launches;
+    k_unpack_exchange<<<(int)blocks, 256, 0, st>>>(xbuf, ns, q, out, d, u);
+    return cudaGetLastError();
+}
 cudaError_t launch_fill(double* p, long long n, double v, cudaStream_t st) {
     long long blocks = (n + 255) / 256;
     if (blocks > 4096) blocks = 4096;
@@ -530,16 +629,8 @@ cudaError_t launch_fill(double* p, long long n, double v, cudaStream_t st) {
 }
 cudaError_t launch_prior(const TreeParams& tp, int m, long long t_first, long long t_count, int grid, double* ws,
                          long long ws_stride, unsigned long long* counter, cudaStream_t st) {
-    set_attrs();
     if (t_count > 0) {
-        static int cf_grid = 0;
-        if (!cf_grid) {
-            int per = 1, dev = 0, nsm = 148;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_prior_covfill, CFT, 0);
-            cf_grid = (per > 0 ? per : 1) * nsm;
-        }
+        const int cf_grid = set_attrs().cf_prior;
         ++g_kernel_launches;
         k_prior_covfill<<<(int)std::min<long long>(cf_grid, t_count), CFT, 0, st>>>(tp, m, t_first, t_count);
         cudaError_t e = cudaGetLastError();
@@ -594,14 +685,7 @@ cudaError_t launch_wide_main(int phase, const TreeParams& tp, const WideParams& 
     const int b = smem_bytes();
     switch (phase) {
         case 6: {
-            static int cf_grid = 0;
-            if (!cf_grid) {
-                int per = 1, dev = 0, nsm = 148;
-                cudaGetDevice(&dev);
-                cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_wide_covfill, CFT, 0);
-                cf_grid = (per > 0 ? per : 1) * nsm;
-            }
+            const int cf_grid = set_attrs().cf_wide;
             ++g_kernel_launches;
             k_wide_covfill<<<(int)std::min<long long>(cf_grid, ntask), CFT, 0, st>>>(tp, wp, tasks, ntask);
             break;

@@ -34,6 +34,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
 
 #include "mra_device.cuh"
 #include "mra_internal.h"
@@ -691,28 +692,39 @@ k_merge_sum(int J, int qc, long long t_first, long long t_count, double* child_o
     }
 }
 
-static int g_gemm_resident[9] = {1, 1, 1, 1, 1, 1, 1, 1, 1};   // resident CTAs per SM x SM count, by phase
-                                                               // (6: mtile, 7: prior, 8: merge)
-static bool g_gemm_attr_done = false;
+// resident CTAs per SM x SM count, by phase (6: mtile, 7: prior, 8: merge), per device ordinal (the smem
+// attribute and occupancy are per device; computed once per device under a lock)
+constexpr int MAXDEV = 64;
+struct GemmAttrs {
+    bool done = false;
+    int resident[9] = {1, 1, 1, 1, 1, 1, 1, 1, 1};
+    int nsm = 148;
+};
+static GemmAttrs g_gemm_attrs[MAXDEV];
+static std::mutex g_gemm_mu;
 // the stages, or the in-place 64 x 64 factor view (diag, T00 of mtile) if larger, plus the misc area
 constexpr int UNIT_SMEM_DBL = (FAC_IN_DBL > NSTAGE * STAGE_DBL ? FAC_IN_DBL : NSTAGE * STAGE_DBL) + MISC_DBL;
 static int gemm_smem_bytes() { return UNIT_SMEM_DBL * (int)sizeof(double); }
-static void gemm_set_attrs() {
-    if (g_gemm_attr_done) return;
+static const GemmAttrs& gemm_set_attrs() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= MAXDEV) dev = 0;
+    GemmAttrs& A = g_gemm_attrs[dev];
+    std::lock_guard<std::mutex> lk(g_gemm_mu);
+    if (A.done) return A;
     const int b = gemm_smem_bytes();
     const void* ks[9] = {(const void*)k_wide_chain,   (const void*)k_wide_sigma, (const void*)k_wide_update,
                          (const void*)k_wide_diag,    (const void*)k_wide_panel_x, (const void*)k_wide_trsm,
                          (const void*)k_wide_mtile,   (const void*)k_prior,      (const void*)k_merge};
-    int dev = 0, nsm = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&A.nsm, cudaDevAttrMultiProcessorCount, dev);
     for (int i = 0; i < 9; i++) {
         cudaFuncSetAttribute(ks[i], cudaFuncAttributeMaxDynamicSharedMemorySize, b);
         int per = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ks[i], NT, b);
-        g_gemm_resident[i] = (per > 0 ? per : 1) * nsm;
+        A.resident[i] = (per > 0 ? per : 1) * A.nsm;
     }
-    g_gemm_attr_done = true;
+    A.done = true;
+    return A;
 }
 
 // phases: 0 chain, 1 sigma, 2 update, 3 diag, 4 panel_x, 5 trsm, 6 covfill (6: mra_kernels.cu).
@@ -721,8 +733,7 @@ cudaError_t launch_wide(int phase, const TreeParams& tp, const WideParams& wp, i
                         long long ntask, int grid, unsigned long long* counter, cudaStream_t st) {
     if (phase == 6) return launch_wide_main(phase, tp, wp, step, tasks, ntask, grid, counter, st);
     if (phase < 0 || phase > 6) return cudaErrorInvalidValue;
-    gemm_set_attrs();
-    long long g = g_gemm_resident[phase];
+    long long g = gemm_set_attrs().resident[phase];
     if (ntask < g) g = ntask;
     if (g < 1) return cudaSuccess;
     const int b = gemm_smem_bytes();
@@ -743,10 +754,9 @@ cudaError_t launch_wide(int phase, const TreeParams& tp, const WideParams& wp, i
 cudaError_t launch_wide_mtile(const TreeParams& tp, const WideParams& wp, long long g_first, long long g_count,
                               double* out, long long out_first, int q, const int4* tasks, long long ntask, int grid,
                               unsigned long long* counter, const MergeRing& ring, cudaStream_t st) {
-    gemm_set_attrs();
     (void)grid;
     (void)g_count;
-    long long gr = g_gemm_resident[6];
+    long long gr = gemm_set_attrs().resident[6];
     if (ntask < gr) gr = ntask;
     if (gr < 1) return cudaSuccess;
     cudaError_t e = cudaMemsetAsync(ring.flags, 0, sizeof(int) * 3 * ring.maxg, st);
@@ -761,15 +771,13 @@ cudaError_t launch_wide_mtile(const TreeParams& tp, const WideParams& wp, long l
 cudaError_t launch_merge(const TreeParams& tp, int m, long long t_first, long long t_count, const double* child_out,
                          long long child_first, double* out, long long out_first, int q, int grid, double* ws,
                          long long ws_stride, unsigned long long* counter, cudaStream_t st) {
-    gemm_set_attrs();
-    grid = (int)std::min<long long>({(long long)grid, (long long)g_gemm_resident[8], t_count});
+    const GemmAttrs& A = gemm_set_attrs();
+    grid = (int)std::min<long long>({(long long)grid, (long long)A.resident[8], t_count});
     if (grid < 1) return cudaSuccess;
     // large levels (several regions per CTA): the child sums as one streaming pass first
     const int presummed = t_count >= 4LL * grid ? 1 : 0;
     if (presummed) {
-        int dev = 0, nsm = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        const int nsm = A.nsm;
         const int qc = m * tp.rh + 1;
         const long long rows = t_count * qc;
         const int sg = (int)std::min<long long>((rows + 7) / 8, 8LL * nsm);
@@ -787,8 +795,7 @@ cudaError_t launch_merge(const TreeParams& tp, int m, long long t_first, long lo
 // k_prior of one level (the covariance blocks are filled first by launch_prior in mra_kernels.cu)
 cudaError_t launch_prior_unit(const TreeParams& tp, int m, long long t_first, long long t_count, int grid, double* ws,
                               long long ws_stride, unsigned long long* counter, cudaStream_t st) {
-    gemm_set_attrs();
-    grid = (int)std::min<long long>({(long long)grid, (long long)g_gemm_resident[7], t_count});
+    grid = (int)std::min<long long>({(long long)grid, (long long)gemm_set_attrs().resident[7], t_count});
     if (grid < 1) return cudaSuccess;
     ++g_kernel_launches;
     k_prior<<<grid, NT, gemm_smem_bytes(), st>>>(tp, m, t_first, t_count, ws, ws_stride, counter);
@@ -797,11 +804,8 @@ cudaError_t launch_prior_unit(const TreeParams& tp, int m, long long t_first, lo
 
 // resident CTAs per SM of this unit's kernels (the plan sizes its per-CTA workspace slots with it)
 int unit_ctas_per_sm() {
-    gemm_set_attrs();
-    int dev = 0, nsm = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    return std::max(1, g_gemm_resident[8] / nsm);
+    const GemmAttrs& A = gemm_set_attrs();
+    return std::max(1, A.resident[8] / A.nsm);
 }
 
 // -DMRA_PHASE_TIMING diagnostics of this unit's kernels (g_phase_cycles is per translation unit)
@@ -815,8 +819,7 @@ void phase_cycles_unit(unsigned long long* out32, bool reset) {
 
 // resident CTAs of the merge tile dataflow (the host sizes its look-ahead D1 with it)
 int wide_mtile_resident() {
-    gemm_set_attrs();
-    return g_gemm_resident[6];
+    return gemm_set_attrs().resident[6];
 }
 
 }  // namespace mra

@@ -153,6 +153,40 @@ def test_ctypes_structs_match_the_header(tmp_path):
     # and every C field is mirrored (no field missing at the end)
     hdr = open(os.path.join(ROOT, "include", "mra.h")).read()
     body = hdr[hdr.index("typedef struct {", hdr.index("Plan options")):hdr.index("} mra_opts;")]
-    cfields = re.findall(r"^\s+(?:int|double|void\*)\s+([a-z_0-9, ]+);", body, re.M)
-    names = [n.strip() for grp in cfields for n in grp.split(",")]
+    cfields = re.findall(r"^\s+(?:const\s+)?(?:int|double|void\*)\s+([a-z_0-9, ]+);|^\s+void\*?\s*\(\*([a-z_0-9]+)\)",
+                         body, re.M)
+    names = [n.strip() for plain, fp in cfields for n in (plain.split(",") if plain else [fp])]
     assert names == [f for f, _ in mra._Opts._fields_]
+
+
+def test_tree_size_bounds_are_config_errors():
+    """an oversized tree is MRA_E_CONFIG before any O(regions) host allocation (no abort)."""
+    x, y, _ = synth.uniform_small(100, seed=2)
+    for M, J in ((23, 4), (24, 2), (40, 4)):
+        with pytest.raises(mra.MraError) as e:
+            mra.mra_plan_create(x, y, M, J, 4, device=-2)
+        assert e.value.status == 2
+    with pytest.raises(mra.MraError) as e:
+        mra.mra_plan_create(x, y, 3, 4, 4, device=-2, rank=3, world=2)
+    assert e.value.status == 1                     # rank outside [0, world)
+
+
+def test_nccl_unique_id_without_gpu():
+    """The in-library exchange loads NCCL at run time (dlopen); an id can be made on a host without a GPU."""
+    a, b = mra.mra_nccl_unique_id(), mra.mra_nccl_unique_id()
+    assert len(a) == 128 and len(b) == 128 and a != b
+    with pytest.raises(ValueError):
+        mra.mra_plan_create(np.random.rand(10), np.random.rand(10), 2, 4, 4, device=-2, nccl_id=b"short")
+    x, y, _ = synth.uniform_small(200, seed=3)
+    with pytest.raises(mra.MraError) as e:     # a host-only plan cannot hold a communicator
+        mra.mra_plan_create(x, y, 3, 4, 4, device=-2, nccl_id=a)
+    assert e.value.status == 1
+
+
+def test_shard_size_is_packed_lower_triangles():
+    """Exchange buffer = per level-s region the packed lower triangle of its q x q output + d, u, + 1 flag."""
+    w = synth.make("C1", n=20000)
+    p = mra.mra_plan_create(w.x, w.y, w.M, w.J, w.r, device=-2, rank=0, world=2)
+    s = mra.mra_plan_shards(p)["shard_level"]
+    ns, q = w.J ** (s - 1), (s - 1) * p.r_hat + 1
+    assert mra.mra_shard_size(p) == ns * q * (q + 1) // 2 + 2 * ns + 1

@@ -44,7 +44,7 @@ def _box(x, y, J, level, t):
     return b
 
 
-def _sampled(mra, name, level, nsub, seed, theta_idx=0):
+def _sampled(mra, name, level, nsub, seed, theta_idx=0, largest=False):
     import torch
     w = synth.make(name, device="cuda")
     theta = w.thetas[theta_idx]
@@ -55,7 +55,14 @@ def _sampled(mra, name, level, nsub, seed, theta_idx=0):
     rng = np.random.default_rng(seed)
     ext = np.unique([np.argmin(w.x), np.argmax(w.x), np.argmin(w.y), np.argmax(w.y)])
     checked = 0
-    for t in rng.choice(w.J ** (level - 1), size=nsub, replace=False):
+    subs = list(rng.choice(w.J ** (level - 1), size=nsub, replace=False))
+    if largest:
+        # the level-`level` subtree holding the largest leaf (C4: the ~9k-observation swath leaves)
+        lay = mra.mra_plan_layout(p)["leaf_off"]
+        big = int(np.argmax(np.diff(lay)))
+        t_big = big // (w.J ** (w.M - level))
+        subs = [t_big] + [t for t in subs if t != t_big][: nsub - 1]
+    for t in subs:
         b = _box(w.x, w.y, w.J, level, int(t))
         sel = np.nonzero((w.x >= b[0]) & (w.x < b[1]) & (w.y >= b[2]) & (w.y < b[3]))[0]
         idx = np.union1d(sel, ext)
@@ -82,4 +89,11 @@ def test_C3_full_47M_sampled(mra):
 
 def test_C4_full_sampled(mra):
     """C4 at full size (skewed swath leaves up to ~9k observations), one of its 16 thetas."""
-    assert _sampled(mra, "C4", level=9, nsub=2, seed=3, theta_idx=5) > 2 * 6
+    assert _sampled(mra, "C4", level=9, nsub=2, seed=3, theta_idx=5, largest=True) > 2 * 6
+
+
+def test_C4_largest_leaf_corner_thetas(mra):
+    """C4's largest leaf under the two extreme thetas of the sweep (shortest range / smallest nugget: the worst
+    conditioned leaf Cholesky; longest range / largest nugget)."""
+    for ti in (0, 15):
+        assert _sampled(mra, "C4", level=10, nsub=1, seed=4, theta_idx=ti, largest=True) >= 3
