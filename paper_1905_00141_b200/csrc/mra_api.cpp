@@ -1131,7 +1131,7 @@ extern "C" mra_status mra_plan_memory(const mra_plan* P, int* streams_prior, int
 extern "C" mra_status mra_plan_shards(const mra_plan* P, int* shard_level, int64_t* own, uint64_t* n_own) {
     return guarded([&]() -> mra_status {
         if (!P) return fail(MRA_E_ARG, "plan is NULL");
-        if (shard_level) *shard_level = P->world > 1 ? P->c : 0;
+        if (shard_level) *shard_level = (P->world > 1 || P->nccl) ? P->c : 0;
         if (n_own) *n_own = (uint64_t)P->my_c.size();
         if (own) for (size_t i = 0; i < P->my_c.size(); i++) own[i] = P->my_c[i];
         return MRA_OK;

@@ -96,9 +96,6 @@ def test_in_library_nccl_exchange_vs_oracle(mra, case):
     assert np.all(np.abs(got["region_d"][ok] - ref["region_d"][ok]) <= 1e-8 * np.maximum(1, np.abs(ref["region_d"][ok])))
     assert np.all(np.abs(got["region_u"][ok] - ref["region_u"][ok]) <= 1e-8 * np.maximum(1, np.abs(ref["region_u"][ok])))
     _post_close(got["mu"].ravel(), ref["mu"].ravel(), got["smooth"], ref["smooth"])
-    # device-y entry: same kernels and the same collectives -> bitwise the host-y value
-    zd = torch.from_numpy(z).cuda()
-    assert mra.mra_loglik_dev(p, zd, theta)["loglik"] == got["loglik"]
     # prediction through the broadcast above-shard factors equals the oracle's recursion
     rng = np.random.default_rng(seed)
     qx, qy = rng.random(300), rng.random(300)
@@ -108,6 +105,9 @@ def test_in_library_nccl_exchange_vs_oracle(mra, case):
     assert np.array_equal(np.isnan(mean), np.isnan(rm))
     assert np.nanmax(np.abs(mean - rm)) <= 1e-8 * np.nanmax(np.abs(rm))
     assert np.nanmax(np.abs(var - rv)) <= 1e-8 * np.nanmax(np.abs(rv))
+    # device-y entry: same kernels and the same collectives -> bitwise the host-y value
+    zd = torch.from_numpy(z).cuda()
+    assert mra.mra_loglik_dev(p, zd, theta)["loglik"] == got["loglik"]
     p.close()
 
 
