@@ -6,9 +6,13 @@ observations/sec per MRA log-lik evaluation, fp64, and the fraction of the fp64 
 
 One step = one full MRA log-likelihood evaluation (prior pass + posterior pass, every §8(a)
 row) of the config's synthetic data for a fixed plan, y already resident in HBM (the paper's
-"excluding loading the data and building the structure"). N > 1 ranks
-(torchrun, one per GPU, NCCL) shard the subtrees and sum-reduce the shard-level
-outputs to rank 0 with torch.distributed.reduce over NCCL; time = max over ranks (CUDA events).
+"excluding loading the data and building the structure"). N > 1 ranks (one
+process per GPU: torchrun, or spawned by this script when --gpus N is given without WORLD_SIZE)
+shard the subtrees; each plan holds its own NCCL communicator (opts.nccl_id) and
+mra_loglik_dev runs the exchange step inside the library (broadcast of the above-shard prior rows,
+reduce of the packed shard outputs to rank 0, broadcast of log L); time = max over ranks (CUDA
+events). The headline value is timed with the library's per-launch profiling OFF; kernel times and
+the roofline come from a separate profiled pass of the same steps.
 """
 from __future__ import annotations
 
@@ -253,6 +257,19 @@ def oracle_sample(w, theta, budget_s, seed=0, max_samples=64):
 
 
 # ------------------------------------------------------------------------- arms
+def cpu_info():
+    """CPU model and core count of the host the oracle baseline ran on."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
 def run_reference(args, rank):
     """--impl reference: the oracle (the deliberately slow CPU baseline) on the box's host cores."""
     if rank != 0:
@@ -274,9 +291,9 @@ def run_reference(args, rank):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
             "config": config_block(w, None, args.gpus),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": thr, "kind": "oracle",
-                             "sample": f"{samples} whole level-{lvl} subtrees ({obs} obs) of {w.name}, "
-                                       f"oracle subtree mode, {secs:.1f} s CPU wall"},
+            "cpu_baseline": dict({"value": value, "unit": UNIT, "cores": thr, "kind": "oracle",
+                                  "sample": f"{samples} whole level-{lvl} subtrees ({obs} obs) of {w.name}, "
+                                            f"oracle subtree mode, {secs:.1f} s CPU wall"}, **cpu_info()),
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -311,8 +328,13 @@ def run_gpu(args, rank, world, local_rank):
     log(f"[rank {rank}] data {w.name} n={w.n} in {time.time() - t0:.1f}s")
     t0 = time.time()
     lanes = args.theta_lanes if args.theta_lanes is not None else 1
+    nccl_id = None
+    if world > 1:   # rank 0 makes the id of the plan's own communicator; every rank receives it
+        obj = [mra.mra_nccl_unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
     plan = mra.mra_plan_create(w.x, w.y, w.M, w.J, w.r, device=local_rank, stream=stream, rank=rank,
-                               world=world, stream_prior=args.stream_prior, theta_lanes=lanes)
+                               world=world, stream_prior=args.stream_prior, theta_lanes=lanes, nccl_id=nccl_id)
     torch.cuda.synchronize()
     plan_s = time.time() - t0
     log(f"[rank {rank}] plan in {plan_s:.1f}s: n_retained={plan.n_retained} r_hat={plan.r_hat}")
@@ -321,33 +343,16 @@ def run_gpu(args, rank, world, local_rank):
     zpin = torch.from_numpy(w.z).pin_memory()
     zpin_np = zpin.numpy()
     flush = torch.empty(256 * 1024 * 1024 // 8 * 2, dtype=torch.float64, device=dev)   # 256 MB > L2
-    xbuf = None
-    if world > 1:
-        xbuf = torch.zeros(mra.mra_shard_size(plan), dtype=torch.float64, device=dev)
 
     def step(host=False):
-        if world == 1 and len(thetas) > 1:   # a sweep: the batch entry points (theta lanes run concurrently)
+        # the public API a user calls: every rank gets log L (the exchange runs inside the library at N > 1)
+        if len(thetas) > 1:   # a sweep: the batch entry points (theta lanes run concurrently)
             if host:
                 return list(mra.mra_loglik_batch(plan, zpin_np, thetas))
             return list(mra.mra_loglik_batch_dev(plan, zd, thetas))
-        lls = []
-        for th in thetas:
-            if world == 1:
-                if host:
-                    lls.append(mra.mra_loglik(plan, zpin_np, th)["loglik"])
-                else:
-                    lls.append(mra.mra_loglik_dev(plan, zd, th)["loglik"])
-            else:
-                if host:
-                    zd.copy_(zpin, non_blocking=True)
-                xbuf.zero_()
-                mra.mra_loglik_shard(plan, zd, th, xbuf)
-                torch.distributed.reduce(xbuf, dst=0, op=torch.distributed.ReduceOp.SUM)
-                if rank == 0:
-                    lls.append(mra.mra_loglik_finish(plan, th, xbuf))
-                else:
-                    lls.append(float("nan"))
-        return lls
+        if host:
+            return [mra.mra_loglik(plan, zpin_np, thetas[0])["loglik"]]
+        return [mra.mra_loglik_dev(plan, zd, thetas[0])["loglik"]]
 
     def timed(n, host=False, prof=False):
         ev = []
@@ -368,7 +373,7 @@ def run_gpu(args, rank, world, local_rank):
             b.record(stream)
             torch.cuda.synchronize()
             ev.append(a.elapsed_time(b))
-            launches += mra.mra_last_launches(plan) * (1 if len(thetas) == 1 else 1)
+            launches += mra.mra_last_launches(plan)
         clocks = sampler.stop()
         ms = float(np.sum(ev))
         if world > 1:
@@ -386,10 +391,13 @@ def run_gpu(args, rank, world, local_rank):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    ms, lls, launches, clocks, kt = timed(args.steps, prof=True)
+    # headline: library profiling off (no per-launch events inside the timed region)
+    ms, lls, launches, clocks, _ = timed(args.steps)
     step_list = list(timed.last_steps)
-    ms_e2e, _, _, _, _ = timed(max(1, min(args.steps, 3)), host=True)
     e2e_steps = max(1, min(args.steps, 3))
+    ms_e2e, _, _, _, _ = timed(e2e_steps, host=True)
+    # kernel classes and the roofline: a separate pass of the same steps with per-launch CUDA events
+    prof_ms, _, _, _, kt = timed(args.steps, prof=True)
     if rank != 0:
         return
     ntheta = len(thetas)
@@ -434,7 +442,8 @@ def run_gpu(args, rank, world, local_rank):
                                 f"tools/fp64_peak.cu); the guide-derived figure {src} bf16_tflops_sustained "
                                 f"{bf16} x {FP64_NOMINAL_TF}/{BF16_NOMINAL_TF} = {derived64:.2f} is lower")
                                if meas64 else f"{src} bf16_tflops_sustained {bf16} x {FP64_NOMINAL_TF}/{BF16_NOMINAL_TF}",
-                "kernel_share_of_step": round(kms[dom] / ms, 4),
+                "kernel_share_of_step": round(kms[dom] / prof_ms, 4),
+                "profiled_pass_ms_per_step": round(prof_ms / args.steps, 3),
                 "per_class_tflops": {k: round(cf[k] * steps_th / (kms[k] / 1e3) / 1e12, 2) for k in cand},
                 "covgen": ({"kernel": "k_wide_covfill (covariance blocks of the leaf chains, HBM writes)",
                             "ms_per_step": round(kms["covgen"] / steps_th, 3),
@@ -442,13 +451,14 @@ def run_gpu(args, rank, world, local_rank):
                             "hbm_peak_gbs": pk.get("hbm_gbs"),
                             "bytes_per_step": covgen_bytes}
                            if kcnt.get("covgen") else None),
-                "step_fp64_tflops": round(fm["total"] * steps_th / (ms / 1e3) / 1e12, 3)}
+                "step_fp64_tflops": round(fm["total"] * steps_th / (ms / 1e3) / 1e12, 3),
+                "step_frac_of_peak": round(fm["total"] * steps_th / (ms / 1e3) / 1e12 / peak64, 4)}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         v, o, sec, k, thr, lvl = oracle_sample(w, thetas[0], args.cpu_budget)
-        cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": "oracle",
-               "sample": f"{k} whole level-{lvl} subtrees ({o} obs) of {w.name}, oracle subtree mode, "
-                         f"{sec:.1f} s CPU wall"}
+        cpu = dict({"value": v, "unit": UNIT, "cores": thr, "kind": "oracle",
+                    "sample": f"{k} whole level-{lvl} subtrees ({o} obs) of {w.name}, oracle subtree mode, "
+                              f"{sec:.1f} s CPU wall"}, **cpu_info())
     pred = None
     if world == 1 and args.predict > 0:
         # NEXT-1: posterior mean / variance of X at random locations of the domain
@@ -475,7 +485,7 @@ def run_gpu(args, rank, world, local_rank):
             "loglik": lls[0], "n_theta_per_step": ntheta, "flops_per_step": fm["total"] * ntheta,
             "e2e": {"value": e2e_val, "unit": UNIT,
                     # a sweep (mra_loglik_batch) copies y once per step, single evaluations once per theta
-                    "h2d_bytes_per_step": 8 * w.n * (1 if (ntheta > 1 and world == 1) else ntheta),
+                    "h2d_bytes_per_step": 8 * w.n * (1 if ntheta > 1 else ntheta),
                     "d2h_bytes_per_step": 8 * ntheta},
             "step_ms": {"mean": float(np.mean(step_list)), "sd": float(np.std(step_list, ddof=1)) if len(step_list) > 1
                         else 0.0, "median": float(np.median(step_list)), "runs": len(step_list),
@@ -507,27 +517,31 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle CPU work")
     ap.add_argument("--ref-budget", type=float, default=10.0, help="seconds of oracle work per reference step")
-    ap.add_argument("--dist-backend", default="nccl", help="process-group backend for N > 1 (nccl on a real "
-                    "multi-GPU node; gloo + --same-device only to exercise the sharded path on one GPU)")
-    ap.add_argument("--same-device", action="store_true", help="test only: every rank uses cuda:0")
     ap.add_argument("--predict", type=int, default=0, help="also time mra_predict at this many random query "
                     "locations (1 GPU; after one posterior-state evaluation); adds a 'predict' key")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "mra":
+        # `python bench.py --gpus N`: one process per GPU, launched here the way the driver launches it
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank)
         return
-    if args.same_device:
-        local_rank = 0
     if world > 1:
         import torch
+        if torch.cuda.device_count() < world:
+            raise SystemExit(f"--gpus {world} needs {world} visible GPUs, found {torch.cuda.device_count()}")
         torch.cuda.set_device(local_rank)
-        if args.dist_backend == "nccl":
-            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-        else:
-            torch.distributed.init_process_group(args.dist_backend)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         run_gpu(args, rank, world, local_rank)
     finally:
