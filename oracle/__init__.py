@@ -21,26 +21,40 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "mra_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
+_LIB_LD = os.path.join(_HERE, "liboracle_ld.so")
 E_OVER_100 = math.e / 100.0
 _lib = None
+_lib_ld = None
 
 
-def build(force: bool = False) -> str:
+def build(force: bool = False, extended: bool = False) -> str:
     """Compile the oracle (gcc, -O2, OpenMP, no FMA contraction so the plan formulas are
-    evaluated exactly as written)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        cmd = ["gcc", "-O2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-shared", "-fPIC",
-               "-o", _LIB + ".tmp", _SRC, "-lm"]
+    evaluated exactly as written). extended=True: the same source with the recursion's arithmetic
+    in x87 extended precision (-DORACLE_LONG_DOUBLE; plan unchanged), a referee for rounding
+    questions (R12)."""
+    out = _LIB_LD if extended else _LIB
+    if force or not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-shared", "-fPIC"] + \
+              (["-DORACLE_LONG_DOUBLE"] if extended else []) + ["-o", out + ".tmp", _SRC, "-lm"]
         subprocess.check_call(cmd)
-        os.replace(_LIB + ".tmp", _LIB)
-    return _LIB
+        os.replace(out + ".tmp", out)
+    return out
 
 
-def _load():
-    global _lib
+def _load(extended: bool = False):
+    global _lib, _lib_ld
+    if extended:
+        if _lib_ld is None:
+            _lib_ld = _declare(ctypes.CDLL(build(extended=True)))
+        return _lib_ld
     if _lib is None:
         build()
-        lib = ctypes.CDLL(_LIB)
+        _lib = _declare(ctypes.CDLL(_LIB))
+    return _lib
+
+
+def _declare(lib):
+    if True:
         D = ctypes.POINTER(ctypes.c_double)
         I64 = ctypes.POINTER(ctypes.c_int64)
         lib.oracle_run.restype = ctypes.c_int
@@ -62,8 +76,7 @@ def _load():
                                        ctypes.c_double, ctypes.c_double, ctypes.c_double, D, D, ctypes.c_int64,
                                        D, D, ctypes.c_int]
         lib.oracle_threads.restype = ctypes.c_int
-        _lib = lib
-    return _lib
+    return lib
 
 
 def _p(a):
@@ -104,11 +117,12 @@ def plan(x, y, M, J, r, offset=E_OVER_100):
 
 
 def run(x, y, z, M, J, r, theta, offset=E_OVER_100, xscale=1.0, yscale=1.0, target=None,
-        regions=False, posterior=False, nthreads=0, outputs=False):
+        regions=False, posterior=False, nthreads=0, outputs=False, extended=False):
     """Run the recursion. theta = (cov, sigma2, rho, tau2). target = (level, index) evaluates
     one subtree only (its d, u). Returns a dict with loglik, d, u, n_retained and optional
-    per-region d/u, mu, xq (E[X(q)|y] at knots) and smooth (E[X(s_i)|y])."""
-    lib = _load()
+    per-region d/u, mu, xq (E[X(q)|y] at knots) and smooth (E[X(s_i)|y]). extended=True runs the
+    extended-precision build of the same loops (results rounded to fp64 on output)."""
+    lib = _load(extended)
     x = np.ascontiguousarray(x, dtype=np.float64)
     y = np.ascontiguousarray(y, dtype=np.float64)
     z = np.ascontiguousarray(z, dtype=np.float64)

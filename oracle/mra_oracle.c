@@ -37,6 +37,18 @@
 #include <omp.h>
 #endif
 
+/* Arithmetic type of the recursion. The oracle proper is fp64 (the paper's precision);
+ * -DORACLE_LONG_DOUBLE builds the SAME loops in x87 extended precision (64-bit significand) as a referee
+ * for cases where fp64 rounding itself is in question (R12). The plan (boxes, knots, leaf
+ * assignment) stays fp64 in both builds, so both evaluate the identical partition. tgmath.h makes
+ * sqrt / exp / log follow the argument type. */
+#ifdef ORACLE_LONG_DOUBLE
+typedef long double real;
+#else
+typedef double real;
+#endif
+#include <tgmath.h>
+
 /* ------------------------------------------------------------------ types */
 typedef struct {
     const double *x, *y, *z;
@@ -55,18 +67,18 @@ typedef struct {
     int64_t nret;
     /* prior */
     char *need;
-    double **W;           /* interior region R at level m: m blocks rh x rh, W^1_R..W^m_R */
-    double **LW;          /* chol(W^m_R), rh x rh lower */
-    double *ldW;          /* log|W^m_R| */
+    real **W;           /* interior region R at level m: m blocks rh x rh, W^1_R..W^m_R */
+    real **LW;          /* chol(W^m_R), rh x rh lower */
+    real *ldW;          /* log|W^m_R| */
     /* posterior state */
     int want_post;
-    double **Arow;        /* rh x (m rh): Atilde^{m,1..m} */
-    double **wm;          /* rh: omegatilde^m */
-    double **LP;          /* chol(W^m + Atilde^{mm}) */
+    real **Arow;        /* rh x (m rh): Atilde^{m,1..m} */
+    real **wm;          /* rh: omegatilde^m */
+    real **LP;          /* chol(W^m + Atilde^{mm}) */
     double *region_d, *region_u;
     /* fan-out cache */
     int fan;
-    double **cA, **cw, *cd, *cu;
+    real **cA, **cw, *cd, *cu;
 } O;
 
 static int64_t ipow(int64_t b, int e) { int64_t v = 1; while (e-- > 0) v *= b; return v; }
@@ -76,25 +88,25 @@ static int64_t rid(const O *o, int m, int64_t t) { return lvl_first(o, m) + t; }
 
 /* covariance: exponential ("exponential covariance function") or
    Matern nu=3/2 (BASELINE C2; reading R3), planar Euclidean distance (reading R4) */
-static double covf(const O *o, double x1, double y1, double x2, double y2) {
-    double dx = (x1 - x2) * o->xs, dy = (y1 - y2) * o->ys;
-    double d = sqrt(dx * dx + dy * dy);
+static real covf(const O *o, real x1, real y1, real x2, real y2) {
+    real dx = (x1 - x2) * o->xs, dy = (y1 - y2) * o->ys;
+    real d = sqrt(dx * dx + dy * dy);
     if (o->cov == 0) return o->s2 * exp(-d / o->rho);
-    double a = sqrt(3.0) * d / o->rho;
+    real a = sqrt((real)3) * d / o->rho;
     return o->s2 * (1.0 + a) * exp(-a);
 }
 
 /* ------------------------------------------------------ dense helpers (plain) */
 /* in-place lower Cholesky of n x n row-major A; returns 0 on success */
-static int chol(int n, double *A) {
+static int chol(int n, real *A) {
     for (int j = 0; j < n; j++) {
-        double s = A[(int64_t)j * n + j];
+        real s = A[(int64_t)j * n + j];
         for (int k = 0; k < j; k++) s -= A[(int64_t)j * n + k] * A[(int64_t)j * n + k];
         if (!(s > 0.0)) return -1;
-        double L = sqrt(s);
+        real L = sqrt(s);
         A[(int64_t)j * n + j] = L;
         for (int i = j + 1; i < n; i++) {
-            double t = A[(int64_t)i * n + j];
+            real t = A[(int64_t)i * n + j];
             for (int k = 0; k < j; k++) t -= A[(int64_t)i * n + k] * A[(int64_t)j * n + k];
             A[(int64_t)i * n + j] = t / L;
         }
@@ -102,32 +114,32 @@ static int chol(int n, double *A) {
     }
     return 0;
 }
-static double logdet_chol(int n, const double *L) {
-    double s = 0;
+static real logdet_chol(int n, const real *L) {
+    real s = 0;
     for (int i = 0; i < n; i++) s += log(L[(int64_t)i * n + i]);
     return 2.0 * s;
 }
 /* B (n x k, ld k) <- A^{-1} B with A = L L^T */
-static void cholsolve(int n, const double *L, int k, double *B) {
+static void cholsolve(int n, const real *L, int k, real *B) {
     for (int c = 0; c < k; c++) {
         for (int i = 0; i < n; i++) {
-            double t = B[(int64_t)i * k + c];
+            real t = B[(int64_t)i * k + c];
             for (int j = 0; j < i; j++) t -= L[(int64_t)i * n + j] * B[(int64_t)j * k + c];
             B[(int64_t)i * k + c] = t / L[(int64_t)i * n + i];
         }
         for (int i = n - 1; i >= 0; i--) {
-            double t = B[(int64_t)i * k + c];
+            real t = B[(int64_t)i * k + c];
             for (int j = i + 1; j < n; j++) t -= L[(int64_t)j * n + i] * B[(int64_t)j * k + c];
             B[(int64_t)i * k + c] = t / L[(int64_t)i * n + i];
         }
     }
 }
 /* C (m x n) -= A (m x k) B (k x n), all row-major with the given leading dims */
-static void gemm_sub(int m, int n, int k, const double *A, int lda, const double *B, int ldb,
-                     double *C, int ldc) {
+static void gemm_sub(int m, int n, int k, const real *A, int lda, const real *B, int ldb,
+                     real *C, int ldc) {
     for (int i = 0; i < m; i++)
         for (int p = 0; p < k; p++) {
-            double a = A[(int64_t)i * lda + p];
+            real a = A[(int64_t)i * lda + p];
             for (int j = 0; j < n; j++) C[(int64_t)i * ldc + j] -= a * B[(int64_t)p * ldb + j];
         }
 }
@@ -246,21 +258,21 @@ static int build_plan(O *o) {
  *   W^l = C(Q, Q_{a_l}) - sum_{k<l} W^k(Q) K_{a_k} (W^k_{a_l})^T,   K_{a_k} = (W^k_{a_k})^{-1}
  * (north_star; PAPER.md:84-92 evaluated at the knots). When L == lev the ancestor at
  * level L is the region itself and W^k_{a_L} = Wout[k-1] (np == rh). */
-static void w_chain(O *o, const double *px, const double *py, int np, int lev, int64_t t,
-                    int L, double **Wout) {
+static void w_chain(O *o, const real *px, const real *py, int np, int lev, int64_t t,
+                    int L, real **Wout) {
     int rh = o->rh;
-    double *T = malloc(sizeof(double) * rh * (np > rh ? np : rh));
+    real *T = malloc(sizeof(real) * rh * (np > rh ? np : rh));
     for (int l = 1; l <= L; l++) {
         int64_t al = t / ipow(o->J, lev - l);
         int64_t idl = rid(o, l, al);
-        double *Wl = Wout[l - 1];
+        real *Wl = Wout[l - 1];
         for (int i = 0; i < np; i++)
             for (int j = 0; j < rh; j++)
                 Wl[(int64_t)i * rh + j] = covf(o, px[i], py[i], o->kx[idl * rh + j], o->ky[idl * rh + j]);
         for (int k = 1; k < l; k++) {
             int64_t ak = t / ipow(o->J, lev - k);
             int64_t idk = rid(o, k, ak);
-            const double *Wk_al = (l == lev) ? Wout[k - 1] : o->W[idl] + (int64_t)(k - 1) * rh * rh;
+            const real *Wk_al = (l == lev) ? Wout[k - 1] : o->W[idl] + (int64_t)(k - 1) * rh * rh;
             int nal = (l == lev) ? np : rh;
             /* T = K_{a_k} (W^k_{a_l})^T : rh x nal */
             for (int p = 0; p < rh; p++)
@@ -275,15 +287,14 @@ static void w_chain(O *o, const double *px, const double *py, int np, int lev, i
 static int prior_region(O *o, int m, int64_t t) {
     int rh = o->rh;
     int64_t id = rid(o, m, t);
-    double *px = malloc(sizeof(double) * rh), *py = malloc(sizeof(double) * rh);
-    memcpy(px, o->kx + id * rh, sizeof(double) * rh);
-    memcpy(py, o->ky + id * rh, sizeof(double) * rh);
-    o->W[id] = malloc(sizeof(double) * m * rh * rh);
-    double **Wout = malloc(sizeof(double *) * m);
+    real *px = malloc(sizeof(real) * rh), *py = malloc(sizeof(real) * rh);
+    for (int i = 0; i < rh; i++) { px[i] = o->kx[id * rh + i]; py[i] = o->ky[id * rh + i]; }
+    o->W[id] = malloc(sizeof(real) * m * rh * rh);
+    real **Wout = malloc(sizeof(real *) * m);
     for (int l = 0; l < m; l++) Wout[l] = o->W[id] + (int64_t)l * rh * rh;
     w_chain(o, px, py, rh, m, t, m, Wout);
-    o->LW[id] = malloc(sizeof(double) * rh * rh);
-    memcpy(o->LW[id], Wout[m - 1], sizeof(double) * rh * rh);
+    o->LW[id] = malloc(sizeof(real) * rh * rh);
+    memcpy(o->LW[id], Wout[m - 1], sizeof(real) * rh * rh);
     int rc = chol(rh, o->LW[id]);
     o->ldW[id] = rc ? NAN : logdet_chol(rh, o->LW[id]);
     free(Wout); free(px); free(py);
@@ -293,17 +304,17 @@ static int prior_region(O *o, int m, int64_t t) {
 /* ------------------------------------------------------------- posterior */
 /* leaf j: B^l = W^l(S_j, Q_{a_l}), Sigma_j = W^M(S_j,S_j) + tau2 I,
    A^{k,l} = B^{kT} Sigma^{-1} B^l, omega^k = B^{kT} Sigma^{-1} y, d = log|Sigma|, u = y^T Sigma^{-1} y */
-static int leaf_factor(O *o, int64_t j, int np, double *B, double *S, double **Bl) {
+static int leaf_factor(O *o, int64_t j, int np, real *B, real *S, real **Bl) {
     int rh = o->rh, P = o->M - 1;
     const int64_t *idx = o->lidx + o->lstart[j];
-    double *px = malloc(sizeof(double) * (np + 1)), *py = malloc(sizeof(double) * (np + 1));
+    real *px = malloc(sizeof(real) * (np + 1)), *py = malloc(sizeof(real) * (np + 1));
     for (int i = 0; i < np; i++) { px[i] = o->x[idx[i]]; py[i] = o->y[idx[i]]; }
     for (int l = 0; l < P; l++) Bl[l] = B + (int64_t)l * np * rh;
     if (P > 0) w_chain(o, px, py, np, o->M, j, P, Bl);
     /* W^M = C(S,S) - sum_k B^k K_{a_k} B^{kT} */
     for (int i = 0; i < np; i++)
         for (int q = 0; q < np; q++) S[(int64_t)i * np + q] = covf(o, px[i], py[i], px[q], py[q]);
-    double *T = malloc(sizeof(double) * rh * (np + 1));
+    real *T = malloc(sizeof(real) * rh * (np + 1));
     for (int k = 1; k <= P; k++) {
         int64_t idk = rid(o, k, j / ipow(o->J, o->M - k));
         for (int p = 0; p < rh; p++)
@@ -316,21 +327,21 @@ static int leaf_factor(O *o, int64_t j, int np, double *B, double *S, double **B
     return chol(np, S);
 }
 
-static int leaf_terms(O *o, int64_t j, double *A, double *w, double *d, double *u) {
+static int leaf_terms(O *o, int64_t j, real *A, real *w, real *d, real *u) {
     int rh = o->rh, P = o->M - 1, PP = P * rh;
     int np = (int)o->lcnt[j];
-    memset(A, 0, sizeof(double) * PP * PP);
-    memset(w, 0, sizeof(double) * (PP + 1));
+    memset(A, 0, sizeof(real) * PP * PP);
+    memset(w, 0, sizeof(real) * (PP + 1));
     *d = 0; *u = 0;
     if (np == 0) return 0;   /* empty leaf: zero contribution (reading R10) */
-    double *B = malloc(sizeof(double) * ((int64_t)np * PP + 1));
-    double *S = malloc(sizeof(double) * (int64_t)np * np);
-    double **Bl = malloc(sizeof(double *) * (P + 1));
+    real *B = malloc(sizeof(real) * ((int64_t)np * PP + 1));
+    real *S = malloc(sizeof(real) * (int64_t)np * np);
+    real **Bl = malloc(sizeof(real *) * (P + 1));
     int rc = leaf_factor(o, j, np, B, S, Bl);
     if (rc) { free(B); free(S); free(Bl); return -4; }
     /* X = Sigma^{-1} [B^1 .. B^P | y] */
     int nc = PP + 1;
-    double *X = malloc(sizeof(double) * (int64_t)np * nc);
+    real *X = malloc(sizeof(real) * (int64_t)np * nc);
     const int64_t *idx = o->lidx + o->lstart[j];
     for (int i = 0; i < np; i++) {
         for (int l = 0; l < P; l++)
@@ -341,11 +352,11 @@ static int leaf_terms(O *o, int64_t j, double *A, double *w, double *d, double *
     for (int k = 0; k < P; k++)
         for (int a = 0; a < rh; a++)
             for (int c = 0; c < nc; c++) {
-                double s = 0;
+                real s = 0;
                 for (int i = 0; i < np; i++) s += Bl[k][(int64_t)i * rh + a] * X[(int64_t)i * nc + c];
                 if (c < PP) A[(int64_t)(k * rh + a) * PP + c] = s; else w[k * rh + a] = s;
             }
-    double uu = 0;
+    real uu = 0;
     for (int i = 0; i < np; i++) uu += o->z[idx[i]] * X[(int64_t)i * nc + PP];
     *u = uu;
     *d = logdet_chol(np, S);
@@ -354,13 +365,13 @@ static int leaf_terms(O *o, int64_t j, double *A, double *w, double *d, double *
 }
 
 /* region (lev, t): output A (P x P, P = (lev-1) rh), omega (P), d, u for its parent */
-static int post_region(O *o, int lev, int64_t t, double *A, double *w, double *d, double *u) {
+static int post_region(O *o, int lev, int64_t t, real *A, real *w, real *d, real *u) {
     int64_t id = rid(o, lev, t);
     int rc = 0;
     if (o->cA && lev == o->fan && o->cA[t]) {
         int P = (lev - 1) * o->rh;
-        memcpy(A, o->cA[t], sizeof(double) * P * P);
-        memcpy(w, o->cw[t], sizeof(double) * (P + 1));
+        memcpy(A, o->cA[t], sizeof(real) * P * P);
+        memcpy(w, o->cw[t], sizeof(real) * (P + 1));
         *d = o->cd[t]; *u = o->cu[t];
         return 0;
     }
@@ -370,9 +381,9 @@ static int post_region(O *o, int lev, int64_t t, double *A, double *w, double *d
         return rc;
     }
     int rh = o->rh, m = lev, Pm = m * rh, Pp = (m - 1) * rh;
-    double *At = calloc((int64_t)Pm * Pm, sizeof(double)), *wt = calloc(Pm + 1, sizeof(double));
-    double *Ac = malloc(sizeof(double) * ((int64_t)Pm * Pm + 1)), *wc = malloc(sizeof(double) * (Pm + 1));
-    double dt = 0, ut = 0, dc, uc;
+    real *At = calloc((int64_t)Pm * Pm, sizeof(real)), *wt = calloc(Pm + 1, sizeof(real));
+    real *Ac = malloc(sizeof(real) * ((int64_t)Pm * Pm + 1)), *wc = malloc(sizeof(real) * (Pm + 1));
+    real dt = 0, ut = 0, dc, uc;
     /* Atilde = sum over children (fixed child order), PAPER.md:462 supervisor gather */
     for (int c = 0; c < o->J && !rc; c++) {
         rc = post_region(o, m + 1, t * o->J + c, Ac, wc, &dc, &uc);
@@ -382,7 +393,7 @@ static int post_region(O *o, int lev, int64_t t, double *A, double *w, double *d
     }
     if (rc) { free(At); free(wt); free(Ac); free(wc); return rc; }
     /* Ktilde^{-1} = K^{-1} + Atilde^{m,m} = W^m + Atilde^{m,m} (north_star; reading R1) */
-    double *LPm = malloc(sizeof(double) * rh * rh);
+    real *LPm = malloc(sizeof(real) * rh * rh);
     for (int a = 0; a < rh; a++)
         for (int b = 0; b < rh; b++)
             LPm[a * rh + b] = o->W[id][(int64_t)(m - 1) * rh * rh + a * rh + b] +
@@ -390,7 +401,7 @@ static int post_region(O *o, int lev, int64_t t, double *A, double *w, double *d
     if (chol(rh, LPm)) { free(At); free(wt); free(Ac); free(wc); free(LPm); return -4; }
     /* X = Ktilde [Atilde^{m,1..m-1} | omegatilde^m] : rh x (Pp+1) */
     int nc = Pp + 1;
-    double *X = malloc(sizeof(double) * rh * nc);
+    real *X = malloc(sizeof(real) * rh * nc);
     for (int a = 0; a < rh; a++) {
         for (int c = 0; c < Pp; c++) X[a * nc + c] = At[(int64_t)(Pp + a) * Pm + c];
         X[a * nc + Pp] = wt[Pp + a];
@@ -399,26 +410,26 @@ static int post_region(O *o, int lev, int64_t t, double *A, double *w, double *d
     /* A^{k,l} = Atilde^{k,l} - Atilde^{k,m} Ktilde Atilde^{m,l}; omega^k likewise */
     for (int a = 0; a < Pp; a++) {
         for (int b = 0; b < Pp; b++) {
-            double s = At[(int64_t)a * Pm + b];
+            real s = At[(int64_t)a * Pm + b];
             for (int q = 0; q < rh; q++) s -= At[(int64_t)a * Pm + Pp + q] * X[q * nc + b];
             A[(int64_t)a * Pp + b] = s;
         }
-        double s = wt[a];
+        real s = wt[a];
         for (int q = 0; q < rh; q++) s -= At[(int64_t)a * Pm + Pp + q] * X[q * nc + Pp];
         w[a] = s;
     }
-    double qf = 0;
+    real qf = 0;
     for (int q = 0; q < rh; q++) qf += wt[Pp + q] * X[q * nc + Pp];
     /* d = sum d_c + log|Ktilde^{-1}| - log|W^m| ;  u = sum u_c - omegatilde^mT Ktilde omegatilde^m */
     *d = dt + logdet_chol(rh, LPm) - o->ldW[id];
     *u = ut - qf;
     if (o->region_d) { o->region_d[id] = *d; o->region_u[id] = *u; }
     if (o->want_post) {
-        o->Arow[id] = malloc(sizeof(double) * rh * Pm);
+        o->Arow[id] = malloc(sizeof(real) * rh * Pm);
         for (int a = 0; a < rh; a++)
             for (int c = 0; c < Pm; c++) o->Arow[id][(int64_t)a * Pm + c] = At[(int64_t)(Pp + a) * Pm + c];
-        o->wm[id] = malloc(sizeof(double) * rh);
-        memcpy(o->wm[id], wt + Pp, sizeof(double) * rh);
+        o->wm[id] = malloc(sizeof(real) * rh);
+        memcpy(o->wm[id], wt + Pp, sizeof(real) * rh);
         o->LP[id] = LPm;
     } else {
         free(LPm);
@@ -443,7 +454,7 @@ static int post_region(O *o, int lev, int64_t t, double *A, double *w, double *d
  *   Cov(eta_m, eta_l) = -Ktilde_m sum_{k<m} Atilde^{m,k} Cov(eta_k, eta_l)          (l < m)
  *   Cov(eta_m, eta_m) = Ktilde_m + Ktilde_m (sum_{k,k'} Atilde^{m,k} Cov(eta_k, eta_k') Atilde^{m,k'T}) Ktilde_m
  * Queries outside the root domain get NaN. Pinned against the dense definition (oracle/dense.py). */
-static int predict_all(O *o, const double *MU, const double *qx, const double *qy, int64_t nq,
+static int predict_all(O *o, const real *MU, const double *qx, const double *qy, int64_t nq,
                        double *pmean, double *pvar) {
     const int M = o->M, J = o->J, rh = o->rh, P = M - 1, PP = P * rh;
     int64_t *ql = malloc(sizeof(int64_t) * (nq + 1));
@@ -470,14 +481,14 @@ static int predict_all(O *o, const double *MU, const double *qx, const double *q
         if (nqj == 0) continue;
         int np = (int)o->lcnt[j];
         const int64_t *idx = o->lidx + o->lstart[j];
-        double *B = malloc(sizeof(double) * ((int64_t)np * PP + 1));
-        double *S = malloc(sizeof(double) * ((int64_t)np * np + 1));
-        double **Bl = malloc(sizeof(double *) * (P + 1));
+        real *B = malloc(sizeof(real) * ((int64_t)np * PP + 1));
+        real *S = malloc(sizeof(real) * ((int64_t)np * np + 1));
+        real **Bl = malloc(sizeof(real *) * (P + 1));
         if (np > 0 && leaf_factor(o, j, np, B, S, Bl)) { bad |= 1; free(B); free(S); free(Bl); continue; }
         /* rr = Sigma_j^{-1} (y_j - sum_l B^l nu_{a_l}) */
-        double *rr = malloc(sizeof(double) * (np + 1));
+        real *rr = malloc(sizeof(real) * (np + 1));
         for (int i = 0; i < np; i++) {
-            double s = o->z[idx[i]];
+            real s = o->z[idx[i]];
             for (int k = 1; k <= P; k++) {
                 int64_t ak = rid(o, k, j / ipow(J, M - k));
                 for (int q = 0; q < rh; q++) s -= Bl[k - 1][(int64_t)i * rh + q] * MU[ak * rh + q];
@@ -486,21 +497,21 @@ static int predict_all(O *o, const double *MU, const double *qx, const double *q
         }
         if (np > 0) cholsolve(np, S, 1, rr);
         /* posterior covariance of the ancestor chain eta_{a_1..a_P} (PP x PP), top-down */
-        double *CC = calloc((int64_t)PP * PP + 1, sizeof(double));
+        real *CC = calloc((int64_t)PP * PP + 1, sizeof(real));
         for (int m = 1; m <= P; m++) {
             int64_t id = rid(o, m, j / ipow(J, M - m));
             int Pp = (m - 1) * rh, Pm = m * rh;
-            const double *Ar = o->Arow[id];   /* rh x Pm: Atilde^{m,1..m} */
+            const real *Ar = o->Arow[id];   /* rh x Pm: Atilde^{m,1..m} */
             /* Gm = Atilde^{m,<m} CC[<m, <m]   (rh x Pp) */
-            double *Gm = calloc((int64_t)rh * Pp + 1, sizeof(double));
+            real *Gm = calloc((int64_t)rh * Pp + 1, sizeof(real));
             for (int a = 0; a < rh; a++)
                 for (int l = 0; l < Pp; l++) {
-                    double s = 0;
+                    real s = 0;
                     for (int k = 0; k < Pp; k++) s += Ar[(int64_t)a * Pm + k] * CC[(int64_t)k * PP + l];
                     Gm[(int64_t)a * Pp + l] = s;
                 }
             /* Cov(eta_m, eta_l) = -Ktilde_m Gm */
-            double *X = malloc(sizeof(double) * ((int64_t)rh * Pp + 1));
+            real *X = malloc(sizeof(real) * ((int64_t)rh * Pp + 1));
             for (int64_t e = 0; e < (int64_t)rh * Pp; e++) X[e] = Gm[e];
             if (Pp) cholsolve(rh, o->LP[id], Pp, X);
             for (int a = 0; a < rh; a++)
@@ -510,12 +521,12 @@ static int predict_all(O *o, const double *MU, const double *qx, const double *q
                 }
             /* Cov(eta_m, eta_m) = Ktilde_m + Ktilde_m (Gm Atilde^{m,<m T}) Ktilde_m */
             /* Y = I + (Gm Atilde^T) Ktilde_m, then Ktilde_m Y = Ktilde_m + Ktilde_m Gm A^T Ktilde_m */
-            double *Y = calloc((int64_t)rh * rh, sizeof(double));
+            real *Y = calloc((int64_t)rh * rh, sizeof(real));
             for (int a = 0; a < rh; a++) Y[a * rh + a] = 1.0;
-            double *Z = calloc((int64_t)rh * rh, sizeof(double));
+            real *Z = calloc((int64_t)rh * rh, sizeof(real));
             for (int a = 0; a < rh; a++)
                 for (int b = 0; b < rh; b++) {
-                    double s = 0;
+                    real s = 0;
                     for (int l = 0; l < Pp; l++) s += Gm[(int64_t)a * Pp + l] * Ar[(int64_t)b * Pm + l];
                     Z[a * rh + b] = s;   /* Gm Atilde^{m,<m T}, symmetric */
                 }
@@ -528,16 +539,16 @@ static int predict_all(O *o, const double *MU, const double *qx, const double *q
             free(Gm); free(X); free(Y); free(Z);
         }
         /* per query */
-        double *bq = malloc(sizeof(double) * (PP + 1)), *c = malloc(sizeof(double) * (np + 1));
-        double *w = malloc(sizeof(double) * (np + 1)), *bt = malloc(sizeof(double) * (PP + 1));
-        double *t = malloc(sizeof(double) * (rh + 1));
-        double **Bq = malloc(sizeof(double *) * (P + 1));
+        real *bq = malloc(sizeof(real) * (PP + 1)), *c = malloc(sizeof(real) * (np + 1));
+        real *w = malloc(sizeof(real) * (np + 1)), *bt = malloc(sizeof(real) * (PP + 1));
+        real *t = malloc(sizeof(real) * (rh + 1));
+        real **Bq = malloc(sizeof(real *) * (P + 1));
         for (int l = 0; l < P; l++) Bq[l] = bq + (int64_t)l * rh;
         for (int64_t iq = 0; iq < nq; iq++) {
             if (ql[iq] != j) continue;
-            double px = qx[iq], py = qy[iq];
+            real px = qx[iq], py = qy[iq];
             if (P > 0) w_chain(o, &px, &py, 1, M, j, P, Bq);
-            double cpp = covf(o, px, py, px, py);
+            real cpp = covf(o, px, py, px, py);
             for (int i = 0; i < np; i++) c[i] = covf(o, o->x[idx[i]], o->y[idx[i]], px, py);
             for (int k = 1; k <= P; k++) {
                 int64_t idk = rid(o, k, j / ipow(J, M - k));
@@ -547,23 +558,23 @@ static int predict_all(O *o, const double *MU, const double *qx, const double *q
                 for (int i = 0; i < np; i++)
                     for (int a = 0; a < rh; a++) c[i] -= Bl[k - 1][(int64_t)i * rh + a] * t[a];
             }
-            double mean = 0.0;
+            real mean = 0.0;
             for (int k = 1; k <= P; k++) {
                 int64_t ak = rid(o, k, j / ipow(J, M - k));
                 for (int a = 0; a < rh; a++) mean += Bq[k - 1][a] * MU[ak * rh + a];
             }
             for (int i = 0; i < np; i++) { mean += c[i] * rr[i]; w[i] = c[i]; }
             if (np > 0) cholsolve(np, S, 1, w);
-            double var = cpp;
+            real var = cpp;
             for (int i = 0; i < np; i++) var -= c[i] * w[i];
             for (int l = 0; l < P; l++)
                 for (int a = 0; a < rh; a++) {
-                    double s = Bq[l][a];
+                    real s = Bq[l][a];
                     for (int i = 0; i < np; i++) s -= Bl[l][(int64_t)i * rh + a] * w[i];
                     bt[l * rh + a] = s;
                 }
             for (int e = 0; e < PP; e++) {
-                double s = 0;
+                real s = 0;
                 for (int f = 0; f < PP; f++) s += CC[(int64_t)e * PP + f] * bt[f];
                 var += bt[e] * s;
             }
@@ -650,12 +661,12 @@ static int run_impl(const double *x, const double *y, const double *z, int64_t n
     o.region_d = region_d; o.region_u = region_u;
     if (region_d) for (int64_t i = 0; i < o.nreg; i++) { region_d[i] = NAN; region_u[i] = NAN; }
     int64_t nint = o.nint;
-    o.W = calloc(nint + 1, sizeof(double *));
-    o.LW = calloc(nint + 1, sizeof(double *));
-    o.ldW = calloc(nint + 1, sizeof(double));
-    o.Arow = calloc(nint + 1, sizeof(double *));
-    o.wm = calloc(nint + 1, sizeof(double *));
-    o.LP = calloc(nint + 1, sizeof(double *));
+    o.W = calloc(nint + 1, sizeof(real *));
+    o.LW = calloc(nint + 1, sizeof(real *));
+    o.ldW = calloc(nint + 1, sizeof(real));
+    o.Arow = calloc(nint + 1, sizeof(real *));
+    o.wm = calloc(nint + 1, sizeof(real *));
+    o.LP = calloc(nint + 1, sizeof(real *));
     /* prior, top-down, levels 1..M-1 (regions of a level are independent) */
     int bad = 0;
     for (int m = 1; m < M && !bad; m++) {
@@ -678,32 +689,32 @@ static int run_impl(const double *x, const double *y, const double *z, int64_t n
         o.fan = fan;
         int64_t cnt = ipow(J, fan - 1);
         int P = (fan - 1) * rh;
-        o.cA = calloc(cnt, sizeof(double *));
-        o.cw = calloc(cnt, sizeof(double *));
-        o.cd = calloc(cnt, sizeof(double));
-        o.cu = calloc(cnt, sizeof(double));
+        o.cA = calloc(cnt, sizeof(real *));
+        o.cw = calloc(cnt, sizeof(real *));
+        o.cd = calloc(cnt, sizeof(real));
+        o.cu = calloc(cnt, sizeof(real));
         for (int64_t t = 0; t < cnt; t++) {
-            o.cA[t] = malloc(sizeof(double) * ((int64_t)P * P + 1));
-            o.cw[t] = malloc(sizeof(double) * (P + 1));
-            memcpy(o.cA[t], gA + t * (int64_t)P * P, sizeof(double) * P * P);
-            memcpy(o.cw[t], gw + t * (int64_t)P, sizeof(double) * P);
+            o.cA[t] = malloc(sizeof(real) * ((int64_t)P * P + 1));
+            o.cw[t] = malloc(sizeof(real) * (P + 1));
+            for (int64_t e = 0; e < (int64_t)P * P; e++) o.cA[t][e] = gA[t * (int64_t)P * P + e];
+            for (int e = 0; e < P; e++) o.cw[t][e] = gw[t * (int64_t)P + e];
             o.cd[t] = gd[t];
             o.cu[t] = gu[t];
         }
     } else if (fan > tl) {
         o.fan = fan;
         int64_t cnt = ipow(J, fan - 1);
-        o.cA = calloc(cnt, sizeof(double *));
-        o.cw = calloc(cnt, sizeof(double *));
-        o.cd = calloc(cnt, sizeof(double));
-        o.cu = calloc(cnt, sizeof(double));
+        o.cA = calloc(cnt, sizeof(real *));
+        o.cw = calloc(cnt, sizeof(real *));
+        o.cd = calloc(cnt, sizeof(real));
+        o.cu = calloc(cnt, sizeof(real));
         int P = (fan - 1) * rh;
         int64_t lo = tt * ipow(J, fan - tl), hi = (tt + 1) * ipow(J, fan - tl);
         #pragma omp parallel for schedule(dynamic, 1) reduction(|:bad)
         for (int64_t t = lo; t < hi; t++) {
-            double *A = malloc(sizeof(double) * ((int64_t)P * P + 1));
-            double *w = malloc(sizeof(double) * (P + 1));
-            double d, u;
+            real *A = malloc(sizeof(real) * ((int64_t)P * P + 1));
+            real *w = malloc(sizeof(real) * (P + 1));
+            real d, u;
             int e = post_region(&o, fan, t, A, w, &d, &u);
             if (e) bad |= 1;
             o.cd[t] = d; o.cu[t] = u;
@@ -714,30 +725,30 @@ static int run_impl(const double *x, const double *y, const double *z, int64_t n
     }
     {
         int P = (tl - 1) * rh;
-        double *A = malloc(sizeof(double) * ((int64_t)P * P + 1)), *w = malloc(sizeof(double) * (P + 1));
-        double d, u;
+        real *A = malloc(sizeof(real) * ((int64_t)P * P + 1)), *w = malloc(sizeof(real) * (P + 1));
+        real d, u;
         rc = post_region(&o, tl, tt, A, w, &d, &u);
-        if (!rc && out_A) memcpy(out_A, A, sizeof(double) * P * P);
-        if (!rc && out_w) memcpy(out_w, w, sizeof(double) * P);
+        if (!rc && out_A) for (int64_t e = 0; e < (int64_t)P * P; e++) out_A[e] = A[e];
+        if (!rc && out_w) for (int e = 0; e < P; e++) out_w[e] = w[e];
         free(A); free(w);
         if (rc) { free_all(&o); return rc; }
         if (out_d) *out_d = d;
         if (out_u) *out_u = u;
         if (loglik) *loglik = target_level > 0 ? NAN
-                                  : -0.5 * ((double)o.nret * log(2.0 * M_PI) + d + u);
+                                  : -0.5 * ((real)o.nret * log(2 * acos((real)-1)) + d + u);
     }
     if (o.want_post) {
         /* mu_R = Ktilde_R (omegatilde^m - sum_{k<m} Atilde^{m,k} mu_{a_k}), top-down */
-        double *MU = calloc(nint * rh + 1, sizeof(double));
+        real *MU = calloc(nint * rh + 1, sizeof(real));
         for (int m = 1; m < M; m++) {
             int64_t cnt = ipow(J, m - 1);
             #pragma omp parallel for schedule(static)
             for (int64_t t = 0; t < cnt; t++) {
                 int64_t id = rid(&o, m, t);
                 int Pm = m * rh;
-                double *v = malloc(sizeof(double) * rh);
+                real *v = malloc(sizeof(real) * rh);
                 for (int a = 0; a < rh; a++) {
-                    double s = o.wm[id][a];
+                    real s = o.wm[id][a];
                     for (int k = 1; k < m; k++) {
                         int64_t ak = rid(&o, k, t / ipow(J, m - k));
                         for (int q = 0; q < rh; q++)
@@ -746,12 +757,12 @@ static int run_impl(const double *x, const double *y, const double *z, int64_t n
                     v[a] = s;
                 }
                 cholsolve(rh, o.LP[id], 1, v);
-                memcpy(MU + id * rh, v, sizeof(double) * rh);
+                memcpy(MU + id * rh, v, sizeof(real) * rh);
                 /* E[X(q)|y] at the knots of R: sum_{k<=m} W^k_R mu_{a_k} (the
                    finer levels vanish at a level-m knot since C_{m+1}(q, .) = 0) */
                 if (xq)
                     for (int a = 0; a < rh; a++) {
-                        double s = 0;
+                        real s = 0;
                         for (int k = 1; k <= m; k++) {
                             int64_t ak = rid(&o, k, t / ipow(J, m - k));
                             for (int q = 0; q < rh; q++)
@@ -762,7 +773,7 @@ static int run_impl(const double *x, const double *y, const double *z, int64_t n
                 free(v);
             }
         }
-        if (mu) memcpy(mu, MU, sizeof(double) * nint * rh);
+        if (mu) for (int64_t e = 0; e < nint * rh; e++) mu[e] = MU[e];
         if (nq > 0 && predict_all(&o, MU, qx, qy, nq, pmean, pvar)) bad |= 1;
         if (smooth) {
             /* E[X(S_j)|y] = y_j - tau2 Sigma_j^{-1} (y_j - sum_k B^k mu_{a_k}) */
@@ -772,15 +783,15 @@ static int run_impl(const double *x, const double *y, const double *z, int64_t n
             for (int64_t j = 0; j < o.nleaf; j++) {
                 int np = (int)o.lcnt[j];
                 if (np == 0) continue;
-                double *B = malloc(sizeof(double) * ((int64_t)np * P * rh + 1));
-                double *S = malloc(sizeof(double) * (int64_t)np * np);
-                double **Bl = malloc(sizeof(double *) * (P + 1));
-                double *v = malloc(sizeof(double) * np);
+                real *B = malloc(sizeof(real) * ((int64_t)np * P * rh + 1));
+                real *S = malloc(sizeof(real) * (int64_t)np * np);
+                real **Bl = malloc(sizeof(real *) * (P + 1));
+                real *v = malloc(sizeof(real) * np);
                 if (leaf_factor(&o, j, np, B, S, Bl)) { bad |= 1; }
                 else {
                     const int64_t *idx = o.lidx + o.lstart[j];
                     for (int i = 0; i < np; i++) {
-                        double s = o.z[idx[i]];
+                        real s = o.z[idx[i]];
                         for (int k = 1; k <= P; k++) {
                             int64_t ak = rid(&o, k, j / ipow(J, M - k));
                             for (int q = 0; q < rh; q++) s -= Bl[k - 1][(int64_t)i * rh + q] * MU[ak * rh + q];
