@@ -360,3 +360,38 @@ def test_P11_prediction_outside_domain_is_nan():
     m, v = oracle.predict(x, y, z, np.array([x.max() * 2 + 1, x.mean()]), np.array([y.mean(), y.mean()]), 2, 4,
                           4, (EXP, 1.0, 0.1, 0.05))
     assert np.isnan(m[0]) and np.isnan(v[0]) and np.isfinite(m[1]) and np.isfinite(v[1])
+
+
+@pytest.mark.parametrize("n,M,J,r,cov,cl", [(300, 3, 4, 9, 0, 0), (300, 4, 2, 4, 1, 2), (430, 3, 4, 16, 1, 0)])
+def test_extended_precision_build_pins(n, M, J, r, cov, cl):
+    """The extended-precision build of the oracle (referee of DESIGN.md R12) is the same recursion: it equals
+    the dense definition of Sigma_MRA (P2) and the fp64 oracle on well-conditioned inputs, log L / d / u to
+    1e-12 and the smoothed values to 1e-10."""
+    x, y, z = synth.uniform_small(n, seed=60 + n, clusters=cl)
+    theta = (cov, 1.0, 0.2, 0.1)
+    e = oracle.run(x, y, z, M, J, r, theta, posterior=True, extended=True)
+    d = oracle.run(x, y, z, M, J, r, theta, posterior=True)
+    for k in ("loglik", "d", "u"):
+        assert abs(e[k] - d[k]) <= 1e-12 * abs(d[k]), k
+    assert np.nanmax(np.abs(e["smooth"] - d["smooth"])) <= 1e-10 * np.nanmax(np.abs(d["smooth"]))
+    dn = dense.loglik(x, y, z, M, J, r, *theta)
+    assert abs(e["loglik"] - dn) <= 1e-11 * abs(dn)
+
+
+@pytest.mark.parametrize("xs,ys,J,cov", [(2.0, 0.5, 4, 0), (0.3, 1.7, 2, 1)])
+def test_axis_scaled_distance_pins(xs, ys, J, cov):
+    """Reading R4's per-axis distance scaling (C2's "Euclidean distance on scaled coordinates"):
+    the oracle with xscale / yscale != 1 equals the dense definition with the same scaled distance, and
+    scaling an axis is the same as scaling that coordinate with the knots (the partition is affine-invariant
+    for power-of-two factors)."""
+    x, y, z = synth.uniform_small(350, seed=81, clusters=2)
+    theta = (cov, 1.2, 0.25, 0.06)
+    got = oracle.run(x, y, z, 3, J, 9, theta, xscale=xs, yscale=ys)["loglik"]
+    ref = dense.loglik(x, y, z, 3, J, 9, *theta, xs=xs, ys=ys)
+    assert abs(got - ref) <= 1e-12 * abs(ref)
+    unscaled = oracle.run(x, y, z, 3, J, 9, theta)["loglik"]
+    assert abs(got - unscaled) > 1e-6 * abs(unscaled)          # the scaling is not a no-op
+    # x scale 2 with a J=4 tree == the coordinates x * 2 (exact in binary), knots scaling along
+    if J == 4 and xs == 2.0 and ys == 0.5:
+        alt = oracle.run(x * 2.0, y * 0.5, z, 3, J, 9, theta)["loglik"]
+        assert abs(got - alt) <= 1e-12 * abs(alt)
