@@ -246,6 +246,9 @@ static void tfree(const mra_plan* p, void* ptr) {
 
 static mra_status dalloc(mra_plan* p, void** ptr, size_t bytes, const char* what) {
     if (bytes == 0) bytes = 8;
+    // slack: a bulk-copied k-row of a transposed operand is rounded up to an even number of doubles, so the copy
+    // may read one double past the operand's last row (never used, but it must be mapped memory)
+    bytes += 256;
     cudaError_t e = talloc(p, ptr, bytes);
     if (e != cudaSuccess) {
         cudaGetLastError();

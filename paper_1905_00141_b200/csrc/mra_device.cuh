@@ -252,7 +252,9 @@ __device__ __forceinline__ double frag(const double* s, int row, int k) {
 }
 
 // MI x 4 DMMAs per k-step of 4 on the warp's WM x 32 sub-tile
-template <int KA, int KB>
+// MASK: the ragged k-tile's fragments with k >= nk are zeroed (the bulk-copy path leaves stale values there; the
+// cp.async path zero-fills, MASK = false)
+template <int KA, int KB, bool MASK = false>
 __device__ __forceinline__ void mma_ktile(double (&acc)[MI][4][2], const double* As, const double* Bs, int nk) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
@@ -271,9 +273,23 @@ __device__ __forceinline__ void mma_ktile(double (&acc)[MI][4][2], const double*
     if (nk == TK) {
 #pragma unroll
         for (int kk = 0; kk < TK; kk += 4) step(kk);
-    } else {
+    } else if (!MASK) {
         const int nk4 = (nk + 3) & ~3;
         for (int kk = 0; kk < nk4; kk += 4) step(kk);
+    } else {
+        const int nk4 = (nk + 3) & ~3;
+        for (int kk = 0; kk < nk4; kk += 4) {
+            const bool kin = kk + t < nk;
+            double a[MI], b[4];
+#pragma unroll
+            for (int mi = 0; mi < MI; mi++) a[mi] = kin ? frag<KA>(As, wr + mi * 8 + g, kk + t) : 0.0;
+#pragma unroll
+            for (int ni = 0; ni < 4; ni++) b[ni] = kin ? frag<KB>(Bs, wc + ni * 8 + g, kk + t) : 0.0;
+#pragma unroll
+            for (int mi = 0; mi < MI; mi++)
+#pragma unroll
+                for (int ni = 0; ni < 4; ni++) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+        }
     }
 }
 
@@ -288,9 +304,61 @@ struct GemmDesc {
     double* C;
     long long ldc;
     int Mr, Nc, lower, K0, K1;
+    int amask;   // bulk-copy engine: bit o set = operand o (A0 B0 A1 B1) staged by 1-D bulk copies
 };
+#ifdef MRA_BULK
+constexpr int MISC_DBL = 72;                 // misc smem: reductions, flags, work item, GemmDesc, BulkState
+#else
 constexpr int MISC_DBL = 64;                 // misc smem: reductions, flags, work item, GemmDesc
+#endif
 __device__ __forceinline__ GemmDesc* gemm_desc(double* smem);
+
+#ifdef MRA_BULK
+// ------------------------------------------------------------ bulk-copy staging (GEMM unit)
+// A transposed operand (MEMT: X[i][k] = p[k ld + i]) has each k-row of a tile contiguous in memory, so its
+// 64 x TK k-tile is TK 1-D bulk copies (cp.async.bulk, the TMA unit, <= 512 B each) into the padded [k][LDT]
+// layout, completing on an mbarrier transaction count -- no per-thread cp.async issue and, when every operand
+// of a call is staged this way, no CTA barrier per k-tile (full / empty barriers per stage instead). No tensor
+// map is involved. Row-major operands (MEMN, 128-byte k-rows: too small for the bulk engine, 46 % of the fp64
+// peak in tools/bench_bulk2.cu) stay on cp.async. The per-CTA state persists across the GEMM calls of a kernel
+// (engine_init).
+struct BulkState {
+    unsigned long long full[NSTAGE], empty[NSTAGE];   // all-bulk pipeline
+    unsigned gs;                                      // all-bulk k-tiles staged so far
+    unsigned pad;
+};
+__device__ __forceinline__ BulkState* bulk_state(double* smem);
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile("{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n"
+                 ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(double* dst, const double* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool bulk_ok(const Op& op) {
+    return ((reinterpret_cast<uintptr_t>(op.p) & 15) == 0) && ((op.ld & 1) == 0) && op.ld > 0;
+}
+// bytes of one MEMT k-tile: nk k-rows of the rows [r0, r0 + nr) rounded up to an even count (16-byte multiple;
+// the extra double is past the operand's last row: plan buffers carry slack, its value is never used)
+__device__ __forceinline__ unsigned bulk_bytes(int nr, int nk) { return (unsigned)(nk * ((nr + 1) & ~1) * 8); }
+// warp 0: copy the k-rows [k0, k0 + nk) of rows [r0, r0 + nr) of a MEMT operand into s ([k][LDT])
+__device__ __forceinline__ void bulk_tile_t(double* s, const Op& op, int r0, int nr, int k0, int nk,
+                                            unsigned long long* bar) {
+    const int lane = threadIdx.x & 31;
+    const unsigned rb = (unsigned)(((nr + 1) & ~1) * 8);
+    for (int k = lane; k < nk; k += 32) bulk_g2s(s + k * LDT, op.p + (long long)(k0 + k) * op.ld + r0, rb, bar);
+}
+#endif
 
 // accumulate both K-segments of one output tile through an NSTAGE-deep cp.async pipeline
 template <int KA0, int KB0, int KA1, int KB1>
@@ -339,9 +407,55 @@ __device__ __forceinline__ void tile_pipeline(double (&acc)[MI][4][2], const Gem
     cp_async_wait<0>();
 }
 
+#ifdef MRA_BULK
+// every operand of the call is a bulk-staged MEMT: warp 0 keeps NSTAGE - 1 k-tiles in flight (lane 0 waits for a
+// stage's empty barrier and posts the byte count, the lanes issue the k-row copies), every warp waits on the
+// stage's full barrier, runs its DMMAs and arrives on the empty barrier
+template <int KA0, int KB0, int KA1, int KB1>
+__device__ __forceinline__ void tile_pipeline_bulk(double (&acc)[MI][4][2], const GemmDesc& d, int r0, int nr, int c0,
+                                                   int nc, double* smem, bool wact, unsigned gs) {
+    BulkState* bs = bulk_state(smem);
+    const int K0 = d.K0, K1 = d.K1, T0 = (K0 + TK - 1) / TK, T = T0 + (K1 + TK - 1) / TK;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    auto issue = [&](int ki) {
+        const unsigned sidx = gs + ki, b = sidx % NSTAGE, n = sidx / NSTAGE;
+        const bool s0 = ki < T0;
+        const int k0 = (s0 ? ki : ki - T0) * TK, nk = min(TK, (s0 ? K0 : K1) - k0);
+        if (lane == 0) {
+            if (n > 0) mbar_wait(&bs->empty[b], (n - 1) & 1);
+            mbar_expect_tx(&bs->full[b], bulk_bytes(nr, nk) + bulk_bytes(nc, nk));
+        }
+        __syncwarp();
+        double* As = smem + b * STAGE_DBL;
+        bulk_tile_t(As, s0 ? d.A0 : d.A1, r0, nr, k0, nk, &bs->full[b]);
+        bulk_tile_t(As + TILE_DBL, s0 ? d.B0 : d.B1, c0, nc, k0, nk, &bs->full[b]);
+    };
+    if (warp == 0)
+        for (int ki = 0; ki < NSTAGE - 1 && ki < T; ki++) issue(ki);
+#pragma unroll 1
+    for (int kt = 0; kt < T; kt++) {
+        if (warp == 0 && kt + NSTAGE - 1 < T) issue(kt + NSTAGE - 1);
+        const unsigned sidx = gs + kt, b = sidx % NSTAGE;
+        mbar_wait(&bs->full[b], (sidx / NSTAGE) & 1);
+        if (wact) {
+            const double* As = smem + b * STAGE_DBL;
+            const double* Bs = As + TILE_DBL;
+            if (kt < T0) mma_ktile<KA0, KB0, true>(acc, As, Bs, min(TK, K0 - kt * TK));
+            else mma_ktile<KA1, KB1, true>(acc, As, Bs, min(TK, K1 - (kt - T0) * TK));
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bs->empty[b]);
+    }
+}
+
+#endif
+
 // EPI = 1: the epilogue can add a covariance initial value (ci_cov); only the instantiations that need it
 // carry that code (it costs the other GEMMs registers: at 128 the MEMT x MEMT one would spill)
-template <int KA0, int KB0, int KA1, int KB1, int EPI>
+// MODE (bulk-copy engine): 0 cp.async only, 1 every operand bulk-staged (a call mixing the two kinds stages all of
+// them by cp.async: split it into an all-MEMT call and a cp.async call where it matters); separate
+// non-inlined instantiations, so the paths do not share a register allocation
+template <int KA0, int KB0, int KA1, int KB1, int EPI, int MODE>
 __device__ __noinline__ void cta_gemm_impl(double* smem) {
     const GemmDesc& d = *gemm_desc(smem);
     const int Mr = d.Mr, Nc = d.Nc, lower = d.lower, K0 = d.K0, K1 = d.K1;
@@ -349,6 +463,19 @@ __device__ __noinline__ void cta_gemm_impl(double* smem) {
     const int g = lane >> 2, t = lane & 3;
     const int wr = (warp / (64 / WN)) * WM, wc = (warp % (64 / WN)) * WN;
     const int tiles_m = (Mr + TM - 1) / TM, tiles_n = (Nc + TN - 1) / TN;
+#ifdef MRA_BULK
+    BulkState* bs = bulk_state(smem);
+    unsigned gs = bs->gs;
+    if (MODE != 0) {
+        __syncthreads();   // the stage area's previous users are done before the bulk engine writes it
+        if (threadIdx.x < 32) {
+            // order earlier generic writes of the operands (this CTA's, and through the caller's acquire other
+            // CTAs') and of the stage area before the async-proxy copies
+            asm volatile("fence.proxy.async.global;\n" ::: "memory");
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        }
+    }
+#endif
     for (int tm = 0; tm < tiles_m; tm++) {
         for (int tn = 0; tn < tiles_n; tn++) {
             if (lower && tn > tm) continue;
@@ -362,6 +489,12 @@ __device__ __noinline__ void cta_gemm_impl(double* smem) {
             // warps whose sub-tile lies outside a ragged tile (e.g. the 1-row y tile) or strictly above the
             // diagonal of a lower-triangular tile skip their DMMAs
             const bool wact = wr < nr && wc < nc && !(lower && tm == tn && wc > wr + WM - 1);
+#ifdef MRA_BULK
+            if (MODE == 1) {
+                tile_pipeline_bulk<KA0, KB0, KA1, KB1>(acc, d, r0, nr, c0, nc, smem, wact, gs);
+                gs += (K0 + TK - 1) / TK + (K1 + TK - 1) / TK;
+            } else
+#endif
             if (K0 + K1 > 0)
                 tile_pipeline<KA0, KB0, KA1, KB1>(acc, d, r0, nr, c0, nc, smem, wact);
             const CInit ci = d.ci;
@@ -410,6 +543,9 @@ __device__ __noinline__ void cta_gemm_impl(double* smem) {
             }
         }
     }
+#ifdef MRA_BULK
+    if (MODE != 0 && threadIdx.x == 0) bs->gs = gs;
+#endif
     __syncthreads();
 }
 
@@ -427,8 +563,32 @@ __device__ __forceinline__ void cta_gemm(int Mr, int Nc, int lower, const Op& A0
         d->ci = ci; d->cp = cp; d->alpha = alpha; d->C = C; d->ldc = ldc;
         d->Mr = Mr; d->Nc = Nc; d->lower = lower; d->K0 = K0; d->K1 = K1;
     }
+#ifdef MRA_BULK
+    // per-operand staging: a 16-byte-aligned MEMT operand (even ld) by bulk copies, everything else by cp.async
+    constexpr bool any_t = KA0 == MEMT || KB0 == MEMT || KA1 == MEMT || KB1 == MEMT;
+    int am = 0, need = 0;
+    if (any_t && K0 + K1 > 0) {
+        if (K0 > 0) {
+            need |= 3;
+            if (KA0 == MEMT && bulk_ok(A0)) am |= 1;
+            if (KB0 == MEMT && bulk_ok(B0)) am |= 2;
+        }
+        if (K1 > 0) {
+            need |= 12;
+            if (KA1 == MEMT && bulk_ok(A1)) am |= 4;
+            if (KB1 == MEMT && bulk_ok(B1)) am |= 8;
+        }
+    }
+    if (threadIdx.x == 0) d->amask = am;
     __syncthreads();
-    cta_gemm_impl<KA0, KB0, KA1, KB1, EPI>(smem);
+    if (any_t && am != 0 && am == need)
+        cta_gemm_impl<KA0, KB0, KA1, KB1, EPI, any_t ? 1 : 0>(smem);
+    else
+        cta_gemm_impl<KA0, KB0, KA1, KB1, EPI, 0>(smem);
+#else
+    __syncthreads();
+    cta_gemm_impl<KA0, KB0, KA1, KB1, EPI, 0>(smem);
+#endif
 }
 
 // ---------------------------------------------------------------- small factor blocks
@@ -654,7 +814,26 @@ __device__ __forceinline__ double* dyn_smem() {
 __device__ __forceinline__ GemmDesc* gemm_desc(double* smem) {
     return reinterpret_cast<GemmDesc*>(smem - MISC_DBL + 24);
 }
-static_assert(sizeof(GemmDesc) <= (MISC_DBL - 24) * sizeof(double), "GemmDesc must fit the misc smem");
+#ifdef MRA_BULK
+__device__ __forceinline__ BulkState* bulk_state(double* smem) {
+    return reinterpret_cast<BulkState*>(smem - MISC_DBL + 64);
+}
+static_assert(sizeof(BulkState) <= 8 * sizeof(double), "BulkState must fit the misc smem");
+// once per kernel, before its first GEMM: the bulk engine's barriers and counters
+__device__ __forceinline__ void engine_init(double* smem) {
+    BulkState* bs = bulk_state(smem);
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < NSTAGE; b++) {
+            mbar_init(&bs->full[b], 1);
+            mbar_init(&bs->empty[b], NT / 32);
+        }
+        bs->gs = 0;
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+}
+#endif
+static_assert(sizeof(GemmDesc) <= 40 * sizeof(double), "GemmDesc must fit the misc smem");
 struct FacSmem {
     double* blk;
     double* inv;

@@ -30,6 +30,9 @@
 #define MRA_NSTAGE MRA_GEMM_NSTAGE
 #define MRA_MINB MRA_GEMM_MINB
 #define MRA_FAC_INPLACE 1
+#ifndef MRA_NO_BULK
+#define MRA_BULK 1   // transposed operands staged by 1-D bulk copies + mbarriers (mra_device.cuh); -DMRA_NO_BULK: cp.async
+#endif
 
 #include <cuda_runtime.h>
 
@@ -42,10 +45,17 @@
 
 namespace mra {
 
+#ifdef MRA_BULK
+#define ENGINE_INIT(smem) engine_init(smem)
+#else
+#define ENGINE_INIT(smem) ((void)0)
+#endif
+
 // V chain for 64 rows of one leaf (covariance blocks in place from k_wide_covfill)
 __global__ void __launch_bounds__(NT, MRA_MINB)
 k_wide_chain(TreeParams tp, WideParams wp, const int4* tasks, long long ntask, unsigned long long* counter) {
     double* smem = dyn_smem();
+    ENGINE_INIT(smem);
     const CovP cp = to_covp(tp.cp);
     const int m = tp.M - 1;
     for (;;) {
@@ -69,6 +79,7 @@ k_wide_chain(TreeParams tp, WideParams wp, const int4* tasks, long long ntask, u
 __global__ void __launch_bounds__(NT, MRA_MINB)
 k_wide_sigma(TreeParams tp, WideParams wp, const int4* tasks, long long ntask, unsigned long long* counter) {
     double* smem = dyn_smem();
+    ENGINE_INIT(smem);
     const CovP cp = to_covp(tp.cp);
     const int Pg = (tp.M - 1) * tp.rh;
     for (;;) {
@@ -141,6 +152,7 @@ __device__ __forceinline__ void wide_xrow(const TreeParams& tp, const WideParams
 __global__ void __launch_bounds__(NT, MRA_MINB)
 k_wide_update(TreeParams tp, WideParams wp, int s, const int4* tasks, long long ntask, unsigned long long* counter) {
     double* smem = dyn_smem();
+    ENGINE_INIT(smem);
     const CovP cp = to_covp(tp.cp);
     const int ncol = (tp.M - 1) * tp.rh + 1;
     const int k0 = 64 * wp.kb0, K = 64 * (wp.kb1 - wp.kb0);
@@ -175,6 +187,7 @@ k_wide_update(TreeParams tp, WideParams wp, int s, const int4* tasks, long long 
 __global__ void __launch_bounds__(NT, MRA_MINB)
 k_wide_panel_x(TreeParams tp, WideParams wp, int s, const int4* tasks, long long ntask, unsigned long long* counter) {
     double* smem = dyn_smem();
+    ENGINE_INIT(smem);
     const CovP cp = to_covp(tp.cp);
     for (;;) {
         const long long it = next_item(counter, smem);
@@ -212,6 +225,7 @@ k_wide_panel_x(TreeParams tp, WideParams wp, int s, const int4* tasks, long long
 __global__ void __launch_bounds__(NT, MRA_MINB)
 k_wide_trsm(TreeParams tp, WideParams wp, const int4* tasks, long long ntask, unsigned long long* counter) {
     double* smem = dyn_smem();
+    ENGINE_INIT(smem);
     const CovP cp = to_covp(tp.cp);
     const int ncol = (tp.M - 1) * tp.rh + 1;
     for (;;) {
@@ -252,9 +266,20 @@ k_wide_trsm(TreeParams tp, WideParams wp, const int4* tasks, long long ntask, un
         for (int i = (n - 1) / 64; i >= 0; i--) {
             const int i0 = 64 * i, nb = min(64, n - i0);
             const double* Di = wp.D + wp.D_off[l] + 4096LL * i;
+            double* Gi = Gl + (long long)i0 * wp.ldG;
+            // G_i = D_i B_i (single tile, in place: every operand element is read before the epilogue), then
+            // G_i += X_{i,<i} B_{<i} (both operands transposed: the bulk-copy engine; B_{<i} is still the input,
+            // the row blocks run in descending order)
+#ifdef MRA_SPLIT_O
+            cta_gemm<MEMN, MEMT, MEMN, MEMN>(nb, nc, 0, op_mem(Di, 64), op_mem(Gi, wp.ldG), nb, op_mem(Di, 0),
+                                             op_mem(Di, 0), 0, ci_zero(), 1.0, Gi, wp.ldG, cp, smem);
+            if (i0 > 0)
+                cta_gemm<MEMT, MEMT, MEMN, MEMN>(nb, nc, 0, op_mem(Sl + i0, ld), op_mem(Gl, wp.ldG), i0, op_mem(Gl, 0),
+                                                 op_mem(Gl, 0), 0, ci_mem(Gi, wp.ldG), 1.0, Gi, wp.ldG, cp, smem);
+#else
             cta_gemm<MEMT, MEMT, MEMN, MEMT>(nb, nc, 0, op_mem(Sl + i0, ld), op_mem(Gl, wp.ldG), i0, op_mem(Di, 64),
-                                             op_mem(Gl + (long long)i0 * wp.ldG, wp.ldG), nb, ci_zero(), 1.0,
-                                             Gl + (long long)i0 * wp.ldG, wp.ldG, cp, smem);
+                                             op_mem(Gi, wp.ldG), nb, ci_zero(), 1.0, Gi, wp.ldG, cp, smem);
+#endif
         }
     }
 }
@@ -281,6 +306,7 @@ __device__ __forceinline__ void wide_diag_blk(const TreeParams& tp, const WidePa
 __global__ void __launch_bounds__(NT, 5)
 k_wide_diag(TreeParams tp, WideParams wp, int s, const int4* tasks, long long ntask, unsigned long long* counter) {
     double* smem = dyn_smem();
+    ENGINE_INIT(smem);
     for (;;) {
         const long long it = next_item(counter, smem);
         if (it >= ntask) break;
@@ -304,6 +330,7 @@ __global__ void __launch_bounds__(NT, MRA_MINB)
 k_wide_mtile(TreeParams tp, WideParams wp, long long g_first, double* out, long long out_first, int q,
              const int4* tasks, long long ntask, unsigned long long* counter, MergeRing ring) {
     double* smem = dyn_smem();
+    ENGINE_INIT(smem);
     const CovP cp = to_covp(tp.cp);
     const int M = tp.M, J = tp.J, m = M - 1, rh = tp.rh, Pg = m * rh;
     const int nr = (q + 63) / 64;
@@ -517,11 +544,22 @@ k_wide_mtile(TreeParams tp, WideParams wp, long long g_first, double* out, long 
             __syncthreads();
             PHASE_ADD(23, ph0);
             PHASE_MARK(ph2);
-            // O_ab = G_r,a^T G_r,b + (-F_a) F_b^T   (K = n_group, then K = rh)
+            // O_ab = G_r,a^T G_r,b + (-F_a) F_b^T: the transposed-operand product (K = n_group) on the bulk-copy
+            // engine, then the K = rh correction on cp.async, in place (each element re-read by the thread that
+            // wrote it)
+#ifdef MRA_SPLIT_O
+            cta_gemm<MEMT, MEMT, MEMN, MEMN>(nrow, ncl, a == b, op_mem(G + rh + r0, wp.ldG),
+                                             op_mem(G + rh + c0, wp.ldG), ng, op_mem(G, 0), op_mem(G, 0), 0,
+                                             ci_zero(), 1.0, Oab, q, cp, smem);
+            cta_gemm<MEMN, MEMN, MEMN, MEMN>(nrow, ncl, a == b, op_mem(Fn + (long long)r0 * rh, rh),
+                                             op_mem(F + (long long)c0 * rh, rh), rh, op_mem(F, 0), op_mem(F, 0), 0,
+                                             ci_mem(Oab, q), 1.0, Oab, q, cp, smem);
+#else
             cta_gemm<MEMT, MEMT, MEMN, MEMN>(nrow, ncl, a == b, op_mem(G + rh + r0, wp.ldG),
                                              op_mem(G + rh + c0, wp.ldG), ng, op_mem(Fn + (long long)r0 * rh, rh),
                                              op_mem(F + (long long)c0 * rh, rh), rh, ci_zero(), 1.0, Oab, q, cp,
                                              smem);
+#endif
             PHASE_ADD(24, ph2);
 #ifdef MRA_PHASE_TIMING
             if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[25], 1ULL);
@@ -546,6 +584,7 @@ __global__ void __launch_bounds__(NT, MRA_MINB)
 k_prior(TreeParams tp, int m, long long t_first, long long nitems, double* ws, long long ws_stride,
         unsigned long long* counter) {
     double* smem = dyn_smem();
+    ENGINE_INIT(smem);
     const CovP cp = to_covp(tp.cp);
     const int rh = tp.rh;
     double* W = ws + (long long)blockIdx.x * ws_stride;
@@ -583,6 +622,7 @@ k_merge(TreeParams tp, int m, long long t_first, long long t_count, const double
         double* out, long long out_first, int q, double* ws, long long ws_stride, unsigned long long* counter,
         int presummed) {
     double* smem = dyn_smem();
+    ENGINE_INIT(smem);
     const CovP cp = to_covp(tp.cp);
     const int J = tp.J, rh = tp.rh;
     const int qc = m * rh + 1;
