@@ -176,6 +176,10 @@ struct mra_plan {
     size_t wsub_next = 0;
     int4* wtasks = nullptr;
     double *wG = nullptr, *wS = nullptr, *wD = nullptr, *wlblk = nullptr;
+    long long wG_rows = 0;
+    // TMA tensor maps of this context's long-lived buffers (G, prior rows per level, merge ring): handed to the GEMM
+    // unit's kernels by value (build_registry)
+    TmaReg treg{};
     long long *wS_off = nullptr, *wD_off = nullptr;
     int* wS_ld = nullptr;
     int wldG = 0;
@@ -769,6 +773,7 @@ static mra_status size_wide(mra_plan* P, double budget, bool explicit_budget) {
         }
     }
     if ((s = dalloc(P, (void**)&P->wG, 8 * maxG * P->wldG, "wide G"))) return s;
+    P->wG_rows = maxG;
     if ((s = dalloc(P, (void**)&P->wS, 8 * maxS, "wide Sigma"))) return s;
     if ((s = dalloc(P, (void**)&P->wD, 8 * maxD, "wide Dinv"))) return s;
     if ((s = dalloc(P, (void**)&P->wlblk, 8 * (maxD / 4096 + 1), "wide logdets"))) return s;
@@ -800,6 +805,29 @@ static mra_status size_wide(mra_plan* P, double budget, bool explicit_budget) {
 
 // --------------------------------------------------------------------- C ABI entry
 extern "C" const char* mra_last_error(void) { return g_err.c_str(); }
+
+// the context's TMA registry: G (leaf rows, row-major and transposed views), the prior chain rows of every level
+// (both views), the merge ring (row-major, when its slots are laid out in whole rows of r_hat). MRA_NO_TMA=1
+// leaves it empty (every GEMM then stages by cp.async / bulk copies).
+static void build_registry(mra_plan* P) {
+    P->treg = TmaReg{};
+    if (getenv("MRA_NO_TMA")) return;
+    const int rh = P->rh, M = P->M, J = P->J;
+    if (P->wG && P->wG_rows > 0) {
+        tma_register(P->treg, 0, P->wG, P->wldG, P->wG_rows);
+        tma_register(P->treg, 1, P->wG, P->wldG, P->wG_rows);
+    }
+    if (P->prior)
+        for (int m = 1; m < M; m++) {
+            long long regions = ipow(J, m - 1);
+            if (P->stream && m >= P->c) regions = P->Kc * ipow(J, m - P->c);
+            const long long ld = (long long)m * rh, rows = regions * rh;
+            tma_register(P->treg, 0, P->prior + P->prior_base[m], ld, rows);
+            tma_register(P->treg, 1, P->prior + P->prior_base[m], ld, rows);
+        }
+    if (P->mring.slot && P->mring.stride % rh == 0 && 4096 % rh == 0)
+        tma_register(P->treg, 0, P->mring.slot, rh, P->mring.stride * P->mring.ns / rh);
+}
 
 // an evaluation context for theta-batched sweeps: a copy of the plan's host metadata that shares its
 // read-only device data (observations, knots, CSR, task lists) and owns the buffers an evaluation
@@ -868,6 +896,7 @@ static mra_status make_lane(mra_plan* P, mra_plan** out) {
         mra_plan_destroy(Q);
         return s;
     }
+    build_registry(Q);   // the lane's own buffers
     *out = Q;
     return MRA_OK;
 }
@@ -1007,6 +1036,7 @@ extern "C" mra_status mra_plan_create(const double* x, const double* y, uint64_t
         P->n_lanes = std::max(1, std::min(o.theta_lanes, 16));
         if (P->world > 1 || P->nccl) P->n_lanes = 1;
         TRY(size_device(P, o.mem_budget_gb, o.stream_prior));
+    build_registry(P);
         if (P->nccl) {
             const NcclApi* nc = nccl_api();
             if (!nc) {
@@ -1228,30 +1258,30 @@ static mra_status eval_wide(mra_plan* P, const TreeParams& tp, long long gf, lon
         const auto& w = P->wsubs[P->wsub_next++];
         if (w.g0 != gf + done) return fail(MRA_E_CUDA, "internal: wide sub-chunk schedule out of order");
         wp.G_base = P->leaf_off[w.g0 * P->J];
-        LCHK_K(KIND_COVGEN, launch_wide(6, tp, wp, 0, P->wtasks + w.chain_off, w.chain_n, P->grid, take_counter(P), st));
-        LCHK_K(KIND_CHAIN, launch_wide(0, tp, wp, 0, P->wtasks + w.chain_off, w.chain_n, P->grid, take_counter(P), st));
-        LCHK_K(KIND_SIGMA, launch_wide(1, tp, wp, 0, P->wtasks + w.sigma_off, w.sigma_n, P->grid, take_counter(P), st));
+        LCHK_K(KIND_COVGEN, launch_wide(6, tp, P->treg, wp, 0, P->wtasks + w.chain_off, w.chain_n, P->grid, take_counter(P), st));
+        LCHK_K(KIND_CHAIN, launch_wide(0, tp, P->treg, wp, 0, P->wtasks + w.chain_off, w.chain_n, P->grid, take_counter(P), st));
+        LCHK_K(KIND_SIGMA, launch_wide(1, tp, P->treg, wp, 0, P->wtasks + w.sigma_off, w.sigma_n, P->grid, take_counter(P), st));
         constexpr int NBS = 8;   // as in size_wide
         for (size_t s2 = 0; s2 < w.diag_n.size(); s2++) {
             const int kb0 = (int)s2 / NBS * NBS;
             wp.kb0 = kb0;
             wp.kb1 = (int)s2;
             if (w.upd_n[s2] > 0)
-                LCHK_K(KIND_FACTOR, launch_wide(2, tp, wp, (int)s2, P->wtasks + w.upd_off[s2], w.upd_n[s2], P->grid,
+                LCHK_K(KIND_FACTOR, launch_wide(2, tp, P->treg, wp, (int)s2, P->wtasks + w.upd_off[s2], w.upd_n[s2], P->grid,
                                                 take_counter(P), st));
-            LCHK_K(KIND_FACTOR, launch_wide(3, tp, wp, (int)s2, P->wtasks + w.diag_off[s2], w.diag_n[s2], P->grid,
+            LCHK_K(KIND_FACTOR, launch_wide(3, tp, P->treg, wp, (int)s2, P->wtasks + w.diag_off[s2], w.diag_n[s2], P->grid,
                                             take_counter(P), st));
-            LCHK_K(KIND_FACTOR, launch_wide(4, tp, wp, (int)s2, P->wtasks + w.pf_off[s2], w.pf_n[s2], P->grid,
+            LCHK_K(KIND_FACTOR, launch_wide(4, tp, P->treg, wp, (int)s2, P->wtasks + w.pf_off[s2], w.pf_n[s2], P->grid,
                                             take_counter(P), st));
             if (w.tr_n[s2] > 0) {
                 wp.kb1 = kb0 + NBS;
-                LCHK_K(KIND_FACTOR, launch_wide(2, tp, wp, (int)s2, P->wtasks + w.tr_off[s2], w.tr_n[s2], P->grid,
+                LCHK_K(KIND_FACTOR, launch_wide(2, tp, P->treg, wp, (int)s2, P->wtasks + w.tr_off[s2], w.tr_n[s2], P->grid,
                                                 take_counter(P), st));
             }
         }
         if (w.trsm_n > 0)
-            LCHK_K(KIND_SOLVE, launch_wide(5, tp, wp, 0, P->wtasks + w.trsm_off, w.trsm_n, P->grid, take_counter(P), st));
-        LCHK_K(KIND_SYRKMERGE, launch_wide_mtile(tp, wp, w.g0, w.gcount, gout, gout_first, q, P->wtasks + w.mt_off,
+            LCHK_K(KIND_SOLVE, launch_wide(5, tp, P->treg, wp, 0, P->wtasks + w.trsm_off, w.trsm_n, P->grid, take_counter(P), st));
+        LCHK_K(KIND_SYRKMERGE, launch_wide_mtile(tp, P->treg, wp, w.g0, w.gcount, gout, gout_first, q, P->wtasks + w.mt_off,
                                                   w.mt_n, P->grid, take_counter(P), P->mring, st));
         done += w.gcount;
     }
@@ -1284,12 +1314,12 @@ static mra_status eval_lower(mra_plan* P, const TreeParams& tp0) {
         if (m < c) {
             if (P->nccl && P->rank != 0) continue;   // received from rank 0 (above)
             TreeParams t2 = tp;
-            LCHK_K(KIND_PRIOR, launch_prior(t2, m, 0, ipow(J, m - 1), P->grid, P->ws, P->ws_stride, take_counter(P), st));
+            LCHK_K(KIND_PRIOR, launch_prior(t2, P->treg, m, 0, ipow(J, m - 1), P->grid, P->ws, P->ws_stride, take_counter(P), st));
         } else {
             for (auto& rg : runs) {
                 long long f, cnt;
                 range_at(P, m, rg.first, rg.second, &f, &cnt);
-                LCHK_K(KIND_PRIOR, launch_prior(tp, m, f, cnt, P->grid, P->ws, P->ws_stride, take_counter(P), st));
+                LCHK_K(KIND_PRIOR, launch_prior(tp, P->treg, m, f, cnt, P->grid, P->ws, P->ws_stride, take_counter(P), st));
             }
         }
     }
@@ -1311,7 +1341,7 @@ static mra_status eval_lower(mra_plan* P, const TreeParams& tp0) {
                     long long f, cnt;
                     range_at(P, m, a, b, &f, &cnt);
                     tp.prior_first[m] = f;
-                    LCHK_K(KIND_PRIOR, launch_prior(tp, m, f, cnt, P->grid, P->ws, P->ws_stride, take_counter(P), st));
+                    LCHK_K(KIND_PRIOR, launch_prior(tp, P->treg, m, f, cnt, P->grid, P->ws, P->ws_stride, take_counter(P), st));
                 }
             }
             long long gf, gc;
@@ -1333,7 +1363,7 @@ static mra_status eval_lower(mra_plan* P, const TreeParams& tp0) {
                 const long long cfirst = (m + 1 <= c) ? 0 : cf;
                 double* o = (m <= c) ? P->out_full[m] : P->out_chunk[m];
                 const long long ofirst = (m <= c) ? 0 : f;
-                LCHK_K(KIND_MERGE, launch_merge(tp, m, f, cnt, cout_, cfirst, o, ofirst, (int)q_of(m, rh), P->grid, P->ws,
+                LCHK_K(KIND_MERGE, launch_merge(tp, P->treg, m, f, cnt, cout_, cfirst, o, ofirst, (int)q_of(m, rh), P->grid, P->ws,
                                   P->ws_stride, take_counter(P), st));
             }
         }
@@ -1345,7 +1375,7 @@ static mra_status eval_lower(mra_plan* P, const TreeParams& tp0) {
 static mra_status eval_upper(mra_plan* P, const TreeParams& tp) {
     const int M = P->M, J = P->J, rh = P->rh, c = P->c;
     for (int m = std::min(c - 1, M - 2); m >= 1; m--)
-        LCHK_K(KIND_MERGE, launch_merge(tp, m, 0, ipow(J, m - 1), P->out_full[m + 1], 0, P->out_full[m], 0, (int)q_of(m, rh),
+        LCHK_K(KIND_MERGE, launch_merge(tp, P->treg, m, 0, ipow(J, m - 1), P->out_full[m + 1], 0, P->out_full[m], 0, (int)q_of(m, rh),
                           P->grid, P->ws, P->ws_stride, take_counter(P), P->st));
     LCHK(launch_final(tp, (double)P->N, P->loglik_d, P->st));
     return MRA_OK;

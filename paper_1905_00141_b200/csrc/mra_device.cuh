@@ -15,6 +15,9 @@
 // tensor path on sm_100a is the warp-level DMMA.
 #pragma once
 #include <cstdint>
+#ifdef MRA_BULK
+#include "mra_internal.h"   // TmaReg
+#endif
 
 #ifndef MRA_NT
 #define MRA_NT 256
@@ -246,15 +249,20 @@ __device__ __forceinline__ void load_tile_async(double* s, const Op& op, int r0,
     }
 }
 
-template <int KIND>
+// LAY 1: the layouts TMA tensor loads produce (GEMM unit, MODE 3): MEMN [64 rows][16 k] with the 128-byte swizzle
+// (16-byte chunk index ^= row & 7), MEMT [8 row octets][16 k][8 rows]; both conflict-free for the fragment loads
+template <int KIND, int LAY = 0>
 __device__ __forceinline__ double frag(const double* s, int row, int k) {
+    if (LAY == 1)
+        return KIND == MEMT ? s[(row >> 3) * 128 + k * 8 + (row & 7)]
+                            : s[row * 16 + ((((k >> 1) ^ (row & 7)) << 1) | (k & 1))];
     return KIND == MEMT ? s[k * LDT + row] : s[row * LDN + k];
 }
 
 // MI x 4 DMMAs per k-step of 4 on the warp's WM x 32 sub-tile
 // MASK: the ragged k-tile's fragments with k >= nk are zeroed (the bulk-copy path leaves stale values there; the
 // cp.async path zero-fills, MASK = false)
-template <int KA, int KB, bool MASK = false>
+template <int KA, int KB, bool MASK = false, int LAY = 0>
 __device__ __forceinline__ void mma_ktile(double (&acc)[MI][4][2], const double* As, const double* Bs, int nk) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
@@ -262,9 +270,9 @@ __device__ __forceinline__ void mma_ktile(double (&acc)[MI][4][2], const double*
     auto step = [&](int kk) {
         double a[MI], b[4];
 #pragma unroll
-        for (int mi = 0; mi < MI; mi++) a[mi] = frag<KA>(As, wr + mi * 8 + g, kk + t);
+        for (int mi = 0; mi < MI; mi++) a[mi] = frag<KA, LAY>(As, wr + mi * 8 + g, kk + t);
 #pragma unroll
-        for (int ni = 0; ni < 4; ni++) b[ni] = frag<KB>(Bs, wc + ni * 8 + g, kk + t);
+        for (int ni = 0; ni < 4; ni++) b[ni] = frag<KB, LAY>(Bs, wc + ni * 8 + g, kk + t);
 #pragma unroll
         for (int mi = 0; mi < MI; mi++)
 #pragma unroll
@@ -282,9 +290,9 @@ __device__ __forceinline__ void mma_ktile(double (&acc)[MI][4][2], const double*
             const bool kin = kk + t < nk;
             double a[MI], b[4];
 #pragma unroll
-            for (int mi = 0; mi < MI; mi++) a[mi] = kin ? frag<KA>(As, wr + mi * 8 + g, kk + t) : 0.0;
+            for (int mi = 0; mi < MI; mi++) a[mi] = kin ? frag<KA, LAY>(As, wr + mi * 8 + g, kk + t) : 0.0;
 #pragma unroll
-            for (int ni = 0; ni < 4; ni++) b[ni] = kin ? frag<KB>(Bs, wc + ni * 8 + g, kk + t) : 0.0;
+            for (int ni = 0; ni < 4; ni++) b[ni] = kin ? frag<KB, LAY>(Bs, wc + ni * 8 + g, kk + t) : 0.0;
 #pragma unroll
             for (int mi = 0; mi < MI; mi++)
 #pragma unroll
@@ -304,10 +312,13 @@ struct GemmDesc {
     double* C;
     long long ldc;
     int Mr, Nc, lower, K0, K1;
-    int amask;   // bulk-copy engine: bit o set = operand o (A0 B0 A1 B1) staged by 1-D bulk copies
+    int amask;   // staging mode of the call (GEMM unit: 0 cp.async, 1 bulk copies, 3 TMA tensor loads)
+    int ti[4], trow[4], tcol[4];   // TMA (MODE 3): registry entry and buffer coordinates of operand o
 };
 #ifdef MRA_BULK
-constexpr int MISC_DBL = 72;                 // misc smem: reductions, flags, work item, GemmDesc, BulkState
+constexpr int MISC_DBL = 256;                // misc smem (2 KB, so the main area is 1024-byte aligned for the swizzled
+                                             // TMA stages): reductions, flags, work item, GemmDesc, BulkState, and
+                                             // (from 128) the registry's buffer table (RegMeta[TMA_NREG])
 #else
 constexpr int MISC_DBL = 64;                 // misc smem: reductions, flags, work item, GemmDesc
 #endif
@@ -323,8 +334,9 @@ __device__ __forceinline__ GemmDesc* gemm_desc(double* smem);
 // peak in tools/bench_bulk2.cu) stay on cp.async. The per-CTA state persists across the GEMM calls of a kernel
 // (engine_init).
 struct BulkState {
-    unsigned long long full[NSTAGE], empty[NSTAGE];   // all-bulk pipeline
-    unsigned gs;                                      // all-bulk k-tiles staged so far
+    unsigned long long full[NSTAGE], empty[NSTAGE];   // all-bulk / all-TMA pipelines
+    const TmaReg* reg;                                // the kernel's tensor-map registry (param space), or nullptr
+    unsigned gs;                                      // k-tiles staged so far by the barrier pipelines
     unsigned pad;
 };
 __device__ __forceinline__ BulkState* bulk_state(double* smem);
@@ -357,6 +369,51 @@ __device__ __forceinline__ void bulk_tile_t(double* s, const Op& op, int r0, int
     const int lane = threadIdx.x & 31;
     const unsigned rb = (unsigned)(((nr + 1) & ~1) * 8);
     for (int k = lane; k < nk; k += 32) bulk_g2s(s + k * LDT, op.p + (long long)(k0 + k) * op.ld + r0, rb, bar);
+}
+__device__ __forceinline__ void tma_load2(double* dst, const CUtensorMap* map, int c0, int c1, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
+                 ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_load3(double* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                          unsigned long long* bar) {
+    asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
+                 ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)) : "memory");
+}
+// the registry's buffer table, copied to shared memory by engine_init (a lookup per GEMM call reads it there,
+// not the kernel parameter: parameters beyond 4 KB are fetched through global memory)
+struct RegMeta {
+    unsigned long long base, end;
+    long long ld;
+    int kind, n;   // n: entries (valid in element 0)
+};
+__device__ __forceinline__ RegMeta* reg_meta(double* smem);
+// registry entry of an operand (kind matching, inside the buffer, the buffer's row stride), its buffer row and
+// column; a MEMT operand must start on a column octet. -1: not registered
+template <int KIND>
+__device__ __forceinline__ int tma_find(const RegMeta* rm, const Op& op, int* row, int* col) {
+    if (KIND != MEMN && KIND != MEMT) return -1;
+    const unsigned long long p = reinterpret_cast<unsigned long long>(op.p);
+    const int kd = KIND == MEMT ? 1 : 0;
+    const int n = rm[0].n;
+    for (int i = 0; i < n; i++) {
+        if (rm[i].kind != kd || rm[i].ld != op.ld || p < rm[i].base || p >= rm[i].end) continue;
+        const unsigned long long off = p - rm[i].base;
+        if (off & 7) return -1;
+        const long long e = (long long)(off >> 3), r = e / op.ld, c = e % op.ld;
+        if ((KIND == MEMT && (c & 7)) || r > 0x7fffffffLL) return -1;
+        *row = (int)r;
+        *col = (int)c;
+        return i;
+    }
+    return -1;
+}
+// one operand k-tile by TMA (thread 0): MEMN box (16 k, 64 rows) at (col + k0, row + r0); MEMT box (8, 16, 8) at
+// (0, row + k0, (col + r0) / 8)
+template <int KIND>
+__device__ __forceinline__ void tma_tile(double* dst, const TmaReg* reg, int ti, int trow, int tcol, int r0, int k0,
+                                         unsigned long long* bar) {
+    if (KIND == MEMN) tma_load2(dst, &reg->map[ti], tcol + k0, trow + r0, bar);
+    else tma_load3(dst, &reg->map[ti], 0, trow + k0, (tcol + r0) >> 3, bar);
 }
 #endif
 
@@ -448,12 +505,53 @@ __device__ __forceinline__ void tile_pipeline_bulk(double (&acc)[MI][4][2], cons
     }
 }
 
+// every operand of the call lies in a registered buffer: thread 0 keeps NSTAGE - 1 k-tiles in flight, one TMA tensor
+// load per operand k-tile (16 KB per stage); full / empty barriers as the bulk pipeline; ragged k-tiles masked (the
+// boxes read the buffer's next columns / rows there)
+template <int KA0, int KB0, int KA1, int KB1>
+__device__ __forceinline__ void tile_pipeline_tma(double (&acc)[MI][4][2], const GemmDesc& d, int r0, int c0,
+                                                  double* smem, bool wact, unsigned gs) {
+    BulkState* bs = bulk_state(smem);
+    const TmaReg* reg = bs->reg;
+    const int K0 = d.K0, K1 = d.K1, T0 = (K0 + TK - 1) / TK, T = T0 + (K1 + TK - 1) / TK;
+    const int lane = threadIdx.x & 31;
+    auto issue = [&](int ki) {
+        const unsigned sidx = gs + ki, b = sidx % NSTAGE, n = sidx / NSTAGE;
+        if (n > 0) mbar_wait(&bs->empty[b], (n - 1) & 1);
+        mbar_expect_tx(&bs->full[b], 2u * 64 * 16 * 8);
+        double* As = smem + b * STAGE_DBL;
+        if (ki < T0) {
+            tma_tile<KA0>(As, reg, d.ti[0], d.trow[0], d.tcol[0], r0, ki * TK, &bs->full[b]);
+            tma_tile<KB0>(As + TILE_DBL, reg, d.ti[1], d.trow[1], d.tcol[1], c0, ki * TK, &bs->full[b]);
+        } else {
+            tma_tile<KA1>(As, reg, d.ti[2], d.trow[2], d.tcol[2], r0, (ki - T0) * TK, &bs->full[b]);
+            tma_tile<KB1>(As + TILE_DBL, reg, d.ti[3], d.trow[3], d.tcol[3], c0, (ki - T0) * TK, &bs->full[b]);
+        }
+    };
+    if (threadIdx.x == 0)
+        for (int ki = 0; ki < NSTAGE - 1 && ki < T; ki++) issue(ki);
+#pragma unroll 1
+    for (int kt = 0; kt < T; kt++) {
+        if (threadIdx.x == 0 && kt + NSTAGE - 1 < T) issue(kt + NSTAGE - 1);
+        __syncwarp();
+        const unsigned sidx = gs + kt, b = sidx % NSTAGE;
+        mbar_wait(&bs->full[b], (sidx / NSTAGE) & 1);
+        if (wact) {
+            const double* As = smem + b * STAGE_DBL;
+            const double* Bs = As + TILE_DBL;
+            if (kt < T0) mma_ktile<KA0, KB0, true, 1>(acc, As, Bs, min(TK, K0 - kt * TK));
+            else mma_ktile<KA1, KB1, true, 1>(acc, As, Bs, min(TK, K1 - (kt - T0) * TK));
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bs->empty[b]);
+    }
+}
 #endif
 
 // EPI = 1: the epilogue can add a covariance initial value (ci_cov); only the instantiations that need it
 // carry that code (it costs the other GEMMs registers: at 128 the MEMT x MEMT one would spill)
-// MODE (bulk-copy engine): 0 cp.async only, 1 every operand bulk-staged (a call mixing the two kinds stages all of
-// them by cp.async: split it into an all-MEMT call and a cp.async call where it matters); separate
+// MODE (GEMM unit): 0 cp.async only, 1 every operand a bulk-copied MEMT, 3 every operand in the TMA registry (a call
+// mixing kinds stages everything by cp.async); separate
 // non-inlined instantiations, so the paths do not share a register allocation
 template <int KA0, int KB0, int KA1, int KB1, int EPI, int MODE>
 __device__ __noinline__ void cta_gemm_impl(double* smem) {
@@ -492,6 +590,9 @@ __device__ __noinline__ void cta_gemm_impl(double* smem) {
 #ifdef MRA_BULK
             if (MODE == 1) {
                 tile_pipeline_bulk<KA0, KB0, KA1, KB1>(acc, d, r0, nr, c0, nc, smem, wact, gs);
+                gs += (K0 + TK - 1) / TK + (K1 + TK - 1) / TK;
+            } else if (MODE == 3) {
+                tile_pipeline_tma<KA0, KB0, KA1, KB1>(acc, d, r0, c0, smem, wact, gs);
                 gs += (K0 + TK - 1) / TK + (K1 + TK - 1) / TK;
             } else
 #endif
@@ -564,24 +665,42 @@ __device__ __forceinline__ void cta_gemm(int Mr, int Nc, int lower, const Op& A0
         d->Mr = Mr; d->Nc = Nc; d->lower = lower; d->K0 = K0; d->K1 = K1;
     }
 #ifdef MRA_BULK
-    // per-operand staging: a 16-byte-aligned MEMT operand (even ld) by bulk copies, everything else by cp.async
+    // staging mode, decided by thread 0 (uniform through the descriptor): 3 when every operand lies in a buffer of
+    // the kernel's TMA registry (tensor loads), 1 when every operand is a 16-byte-aligned MEMT with an even ld (1-D
+    // bulk copies), else 0 (cp.async)
     constexpr bool any_t = KA0 == MEMT || KB0 == MEMT || KA1 == MEMT || KB1 == MEMT;
-    int am = 0, need = 0;
-    if (any_t && K0 + K1 > 0) {
-        if (K0 > 0) {
-            need |= 3;
-            if (KA0 == MEMT && bulk_ok(A0)) am |= 1;
-            if (KB0 == MEMT && bulk_ok(B0)) am |= 2;
+    constexpr bool tk_ok = (KA0 == MEMN || KA0 == MEMT) && (KB0 == MEMN || KB0 == MEMT) &&
+                           (KA1 == MEMN || KA1 == MEMT) && (KB1 == MEMN || KB1 == MEMT);
+    if (threadIdx.x == 0) {
+        int mode = 0;
+        if (tk_ok && K0 + K1 > 0) {
+            const RegMeta* reg = reg_meta(smem);
+            bool tma = bulk_state(smem)->reg != nullptr;
+            if (tma && K0 > 0) {
+                d->ti[0] = tma_find<KA0>(reg, A0, &d->trow[0], &d->tcol[0]);
+                d->ti[1] = tma_find<KB0>(reg, B0, &d->trow[1], &d->tcol[1]);
+                tma = d->ti[0] >= 0 && d->ti[1] >= 0;
+            }
+            if (tma && K1 > 0) {
+                d->ti[2] = tma_find<KA1>(reg, A1, &d->trow[2], &d->tcol[2]);
+                d->ti[3] = tma_find<KB1>(reg, B1, &d->trow[3], &d->tcol[3]);
+                tma = d->ti[2] >= 0 && d->ti[3] >= 0;
+            }
+            if (tma) mode = 3;
         }
-        if (K1 > 0) {
-            need |= 12;
-            if (KA1 == MEMT && bulk_ok(A1)) am |= 4;
-            if (KB1 == MEMT && bulk_ok(B1)) am |= 8;
+        if (mode == 0 && any_t && K0 + K1 > 0) {
+            bool ok = true;
+            if (K0 > 0) ok = KA0 == MEMT && KB0 == MEMT && bulk_ok(A0) && bulk_ok(B0);
+            if (ok && K1 > 0) ok = KA1 == MEMT && KB1 == MEMT && bulk_ok(A1) && bulk_ok(B1);
+            if (ok) mode = 1;
         }
+        d->amask = mode;
     }
-    if (threadIdx.x == 0) d->amask = am;
     __syncthreads();
-    if (any_t && am != 0 && am == need)
+    const int mode = d->amask;
+    if (tk_ok && mode == 3)
+        cta_gemm_impl<KA0, KB0, KA1, KB1, EPI, tk_ok ? 3 : 0>(smem);
+    else if (any_t && mode == 1)
         cta_gemm_impl<KA0, KB0, KA1, KB1, EPI, any_t ? 1 : 0>(smem);
     else
         cta_gemm_impl<KA0, KB0, KA1, KB1, EPI, 0>(smem);
@@ -808,7 +927,11 @@ constexpr int MAIN_DBL = (FAC_DBL > NSTAGE * STAGE_DBL) ? FAC_DBL : NSTAGE * STA
 constexpr int SMEM_DBL = MAIN_DBL + MISC_DBL;
 constexpr int GEMM_SMEM_DBL = NSTAGE * STAGE_DBL + MISC_DBL;
 __device__ __forceinline__ double* dyn_smem() {
+#ifdef MRA_BULK
+    extern __shared__ __align__(1024) double smem_raw[];
+#else
     extern __shared__ double smem_raw[];
+#endif
     return smem_raw + MISC_DBL;
 }
 __device__ __forceinline__ GemmDesc* gemm_desc(double* smem) {
@@ -820,9 +943,26 @@ __device__ __forceinline__ BulkState* bulk_state(double* smem) {
 }
 static_assert(sizeof(BulkState) <= 8 * sizeof(double), "BulkState must fit the misc smem");
 // once per kernel, before its first GEMM: the bulk engine's barriers and counters
-__device__ __forceinline__ void engine_init(double* smem) {
+__device__ __forceinline__ RegMeta* reg_meta(double* smem) {
+    return reinterpret_cast<RegMeta*>(smem - MISC_DBL + 128);
+}
+static_assert(sizeof(RegMeta) * TMA_NREG <= 128 * sizeof(double), "RegMeta table must fit the misc smem");
+__device__ __forceinline__ void engine_init(double* smem, const TmaReg* reg) {
     BulkState* bs = bulk_state(smem);
+    RegMeta* rm = reg_meta(smem);
+    const int nreg = reg ? reg->n : 0;
+    if (threadIdx.x < TMA_NREG) {
+        RegMeta e{0, 0, 0, -1, nreg};
+        if ((int)threadIdx.x < nreg) {
+            e.base = reg->base[threadIdx.x];
+            e.end = e.base + reg->bytes[threadIdx.x];
+            e.ld = reg->ld[threadIdx.x];
+            e.kind = reg->kind[threadIdx.x];
+        }
+        rm[threadIdx.x] = e;
+    }
     if (threadIdx.x == 0) {
+        bs->reg = nreg > 0 ? reg : nullptr;
         for (int b = 0; b < NSTAGE; b++) {
             mbar_init(&bs->full[b], 1);
             mbar_init(&bs->empty[b], NT / 32);
@@ -865,12 +1005,20 @@ __device__ __forceinline__ FacSmem fac_smem_inplace(double* smem) {
 }
 
 // load lower n x n block of global A (ld) into blk; add `shift` to the diagonal
+// every element copied by cp.async (all of a thread's copies in flight at once: the block usually comes from L2 or
+// HBM, and a load-then-store loop exposes one memory latency per element), then the diagonal shift
 __device__ __forceinline__ void load_block_lower(double* blk, const double* A, long long ld, int n, double shift) {
     for (int e = threadIdx.x; e < 64 * 64; e += NT) {
-        int i = e >> 6, j = e & 63;
-        if (i < n && j <= i) blk[i * LDB + j] = A[(long long)i * ld + j] + (i == j ? shift : 0.0);
+        const int i = e >> 6, j = e & 63;
+        if (i < n && j <= i) cp_async8(blk + i * LDB + j, A + (long long)i * ld + j, 8);
     }
+    cp_async_commit();
+    cp_async_wait<0>();
     __syncthreads();
+    if (shift != 0.0) {
+        for (int i = threadIdx.x; i < n; i += NT) blk[i * LDB + i] += shift;
+        __syncthreads();
+    }
 }
 // store lower part of blk (n x n) to global (upper part untouched)
 __device__ __forceinline__ void store_block_lower(const double* blk, double* A, long long ld, int n) {

@@ -2,6 +2,7 @@
 // sm_100a kernels (mra_kernels.cu). Not part of the public ABI.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace mra {
@@ -70,6 +71,22 @@ struct WideParams {
                               // (super-blocked Cholesky: kb0 = first block of the current super-step)
 };
 
+// TMA tensor maps of one evaluation context's long-lived buffers (the leaf rows G, the prior chain rows of each
+// level, the merge ring), encoded once on the host and handed to the GEMM unit's kernels BY VALUE as a
+// __grid_constant__ parameter: never modified on the device. A GEMM operand that lies inside a registered buffer
+// with the buffer's row stride is staged by cp.async.bulk.tensor at (row, column) coordinates of that buffer.
+//   kind 0 (row-major operand, MEMN): 2-D (columns = ld, rows), box 16 x 64, 128-byte swizzle
+//   kind 1 (transposed operand, MEMT): 3-D (8, rows, ceil(ld / 8)) with strides (ld, 8) doubles, box 8 x 16 x 8
+constexpr int TMA_NREG = 32;
+struct alignas(64) TmaReg {
+    CUtensorMap map[TMA_NREG];
+    unsigned long long base[TMA_NREG];
+    unsigned long long bytes[TMA_NREG];
+    long long ld[TMA_NREG];
+    int kind[TMA_NREG];
+    int n;
+};
+
 // per-group small slots (Li, F) and dependency counters of the level-(M-1) merge tile dataflow
 struct MergeRing {
     double* slot;           // ns slots of stride doubles: [A_oo 64x64 | Li rh x rh | F q x rh | -F q x rh]
@@ -81,16 +98,19 @@ struct MergeRing {
     long long* slot_done;   // [ns] groups that have released the slot
 };
 
+// register buffer [base, base + rows * ld) with row stride ld (doubles) under `kind`; false if full or not encodable
+bool tma_register(TmaReg& reg, int kind, const double* base, long long ld, long long rows);
+
 // launchers (all asynchronous on `st`); return cudaGetLastError()
 cudaError_t launch_gather(const double* z, const long long* perm, double* zs, long long N, cudaStream_t st);
 // region ranges: level-m regions [t_first, t_first + t_count); output buffers are indexed by
 // (t - out_first), child buffers by (child t - child_first)
-cudaError_t launch_prior(const TreeParams& tp, int m, long long t_first, long long t_count, int grid,
-                         double* ws, long long ws_stride, unsigned long long* counter, cudaStream_t st);
+cudaError_t launch_prior(const TreeParams& tp, const TmaReg& reg, int m, long long t_first, long long t_count,
+                         int grid, double* ws, long long ws_stride, unsigned long long* counter, cudaStream_t st);
 cudaError_t launch_bottom(const TreeParams& tp, long long g_first, long long g_count, double* out,
                           long long out_first, int q, int grid, double* ws, const WsLayout& L,
                           unsigned long long* counter, cudaStream_t st);
-cudaError_t launch_merge(const TreeParams& tp, int m, long long t_first, long long t_count,
+cudaError_t launch_merge(const TreeParams& tp, const TmaReg& reg, int m, long long t_first, long long t_count,
                          const double* child_out, long long child_first, double* out, long long out_first,
                          int q, int grid, double* ws, long long ws_stride, unsigned long long* counter,
                          cudaStream_t st);
@@ -111,16 +131,17 @@ cudaError_t launch_predict(const TreeParams& tp, const PredParams& pp, int grid,
                            unsigned long long* counter, cudaStream_t st);
 // wide path: phase 0 chain, 1 sigma, 2 column update (step), 3 diagonal (step), 4 panel + X row (step),
 // 5 G = X [V | y]
-cudaError_t launch_wide(int phase, const TreeParams& tp, const WideParams& wp, int step, const int4* tasks,
-                        long long ntask, int grid, unsigned long long* counter, cudaStream_t st);
+cudaError_t launch_wide(int phase, const TreeParams& tp, const TmaReg& reg, const WideParams& wp, int step,
+                        const int4* tasks, long long ntask, int grid, unsigned long long* counter, cudaStream_t st);
 cudaError_t launch_wide_main(int phase, const TreeParams& tp, const WideParams& wp, int step, const int4* tasks,
                         long long ntask, int grid, unsigned long long* counter, cudaStream_t st);
-cudaError_t launch_prior_unit(const TreeParams& tp, int m, long long t_first, long long t_count, int grid, double* ws,
-                              long long ws_stride, unsigned long long* counter, cudaStream_t st);
+cudaError_t launch_prior_unit(const TreeParams& tp, const TmaReg& reg, int m, long long t_first, long long t_count,
+                              int grid, double* ws, long long ws_stride, unsigned long long* counter, cudaStream_t st);
 int unit_ctas_per_sm();
 void phase_cycles_unit(unsigned long long* out32, bool reset);
 int wide_mtile_resident();
-cudaError_t launch_wide_mtile(const TreeParams& tp, const WideParams& wp, long long g_first, long long g_count,
+cudaError_t launch_wide_mtile(const TreeParams& tp, const TmaReg& reg, const WideParams& wp, long long g_first,
+                              long long g_count,
                               double* out, long long out_first, int q, const int4* tasks, long long ntask, int grid,
                               unsigned long long* counter, const MergeRing& ring, cudaStream_t st);
 // device plan build (mra_plan.cu): geometry of the partition (host-computed boxes and knot bars)

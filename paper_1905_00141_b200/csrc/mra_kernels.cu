@@ -627,8 +627,8 @@ cudaError_t launch_fill(double* p, long long n, double v, cudaStream_t st) {
     k_fill<<<(int)blocks, 256, 0, st>>>(p, n, v);
     return cudaGetLastError();
 }
-cudaError_t launch_prior(const TreeParams& tp, int m, long long t_first, long long t_count, int grid, double* ws,
-                         long long ws_stride, unsigned long long* counter, cudaStream_t st) {
+cudaError_t launch_prior(const TreeParams& tp, const TmaReg& reg, int m, long long t_first, long long t_count, int grid,
+                         double* ws, long long ws_stride, unsigned long long* counter, cudaStream_t st) {
     if (t_count > 0) {
         const int cf_grid = set_attrs().cf_prior;
         ++g_kernel_launches;
@@ -636,7 +636,7 @@ cudaError_t launch_prior(const TreeParams& tp, int m, long long t_first, long lo
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
-    return launch_prior_unit(tp, m, t_first, t_count, grid, ws, ws_stride, counter, st);
+    return launch_prior_unit(tp, reg, m, t_first, t_count, grid, ws, ws_stride, counter, st);
 }
 cudaError_t launch_bottom(const TreeParams& tp, long long g_first, long long g_count, double* out, long long out_first,
                           int q, int grid, double* ws, const WsLayout& L, unsigned long long* counter,

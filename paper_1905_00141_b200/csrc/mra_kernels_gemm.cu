@@ -34,7 +34,9 @@
 #define MRA_BULK 1   // transposed operands staged by 1-D bulk copies + mbarriers (mra_device.cuh); -DMRA_NO_BULK: cp.async
 #endif
 
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <mutex>
@@ -46,14 +48,20 @@
 namespace mra {
 
 #ifdef MRA_BULK
-#define ENGINE_INIT(smem) engine_init(smem)
+#define ENGINE_INIT(smem) engine_init(smem, &reg)
+// kernels whose GEMM operands never lie in a registered buffer (the per-leaf Sigma / X, the merge workspaces) skip
+// the per-call registry lookup
+#define ENGINE_INIT_NOREG(smem) ((void)reg, engine_init(smem, nullptr))
 #else
-#define ENGINE_INIT(smem) ((void)0)
+#define ENGINE_INIT(smem) ((void)reg)
+#define ENGINE_INIT_NOREG(smem) ((void)reg)
 #endif
+// every kernel of the unit that runs GEMMs takes the context's tensor-map registry by value (param space)
+#define TREG const __grid_constant__ TmaReg reg
 
 // V chain for 64 rows of one leaf (covariance blocks in place from k_wide_covfill)
 __global__ void __launch_bounds__(NT, MRA_MINB)
-k_wide_chain(TreeParams tp, WideParams wp, const int4* tasks, long long ntask, unsigned long long* counter) {
+k_wide_chain(TreeParams tp, TREG, WideParams wp, const int4* tasks, long long ntask, unsigned long long* counter) {
     double* smem = dyn_smem();
     ENGINE_INIT(smem);
     const CovP cp = to_covp(tp.cp);
@@ -77,7 +85,7 @@ k_wide_chain(TreeParams tp, WideParams wp, const int4* tasks, long long ntask, u
 
 // Sigma_l tile (i, k), k <= i: C(S_i, S_k) + tau2 delta - V_i V_k^T
 __global__ void __launch_bounds__(NT, MRA_MINB)
-k_wide_sigma(TreeParams tp, WideParams wp, const int4* tasks, long long ntask, unsigned long long* counter) {
+k_wide_sigma(TreeParams tp, TREG, WideParams wp, const int4* tasks, long long ntask, unsigned long long* counter) {
     double* smem = dyn_smem();
     ENGINE_INIT(smem);
     const CovP cp = to_covp(tp.cp);
@@ -150,9 +158,9 @@ __device__ __forceinline__ void wide_xrow(const TreeParams& tp, const WideParams
 //   type 1 (leaf, i, c): G_i[:, c] -= L_{i,K} G_K[:, c] -- trailing update of the blocked substitution
 //          (leaves solved without the explicit inverse)
 __global__ void __launch_bounds__(NT, MRA_MINB)
-k_wide_update(TreeParams tp, WideParams wp, int s, const int4* tasks, long long ntask, unsigned long long* counter) {
+k_wide_update(TreeParams tp, TREG, WideParams wp, int s, const int4* tasks, long long ntask, unsigned long long* counter) {
     double* smem = dyn_smem();
-    ENGINE_INIT(smem);
+    ENGINE_INIT_NOREG(smem);
     const CovP cp = to_covp(tp.cp);
     const int ncol = (tp.M - 1) * tp.rh + 1;
     const int k0 = 64 * wp.kb0, K = 64 * (wp.kb1 - wp.kb0);
@@ -185,9 +193,9 @@ k_wide_update(TreeParams tp, WideParams wp, int s, const int4* tasks, long long 
 // kept TRANSPOSED in the (otherwise unused) upper triangle of the leaf's Sigma buffer: X[a][b] (block
 // a > block b) at S[b * ld + a]; its diagonal blocks are the inverted D_s.
 __global__ void __launch_bounds__(NT, MRA_MINB)
-k_wide_panel_x(TreeParams tp, WideParams wp, int s, const int4* tasks, long long ntask, unsigned long long* counter) {
+k_wide_panel_x(TreeParams tp, TREG, WideParams wp, int s, const int4* tasks, long long ntask, unsigned long long* counter) {
     double* smem = dyn_smem();
-    ENGINE_INIT(smem);
+    ENGINE_INIT_NOREG(smem);
     const CovP cp = to_covp(tp.cp);
     for (;;) {
         const long long it = next_item(counter, smem);
@@ -223,9 +231,9 @@ k_wide_panel_x(TreeParams tp, WideParams wp, int s, const int4* tasks, long long
 // G[:, c] = X [V | y][:, c] per (leaf, 64-column tile), row blocks in DESCENDING order so the product
 // can overwrite its input: G_i = [X_{i,<i} | D_i] [B_{<i} ; B_i] only reads rows <= i of B.
 __global__ void __launch_bounds__(NT, MRA_MINB)
-k_wide_trsm(TreeParams tp, WideParams wp, const int4* tasks, long long ntask, unsigned long long* counter) {
+k_wide_trsm(TreeParams tp, TREG, WideParams wp, const int4* tasks, long long ntask, unsigned long long* counter) {
     double* smem = dyn_smem();
-    ENGINE_INIT(smem);
+    ENGINE_INIT_NOREG(smem);
     const CovP cp = to_covp(tp.cp);
     const int ncol = (tp.M - 1) * tp.rh + 1;
     for (;;) {
@@ -304,9 +312,9 @@ __device__ __forceinline__ void wide_diag_blk(const TreeParams& tp, const WidePa
 // No GEMM here: the 42 KB factor view and 96 registers let FIVE CTAs share an SM (factor class 180 -> 174 ms
 // on C3), one more latency-bound factorization in flight than the GEMM kernels' four
 __global__ void __launch_bounds__(NT, 5)
-k_wide_diag(TreeParams tp, WideParams wp, int s, const int4* tasks, long long ntask, unsigned long long* counter) {
+k_wide_diag(TreeParams tp, TREG, WideParams wp, int s, const int4* tasks, long long ntask, unsigned long long* counter) {
     double* smem = dyn_smem();
-    ENGINE_INIT(smem);
+    ENGINE_INIT_NOREG(smem);
     for (;;) {
         const long long it = next_item(counter, smem);
         if (it >= ntask) break;
@@ -327,7 +335,7 @@ k_wide_diag(TreeParams tp, WideParams wp, int s, const int4* tasks, long long nt
 // claimed earlier by co-resident CTAs, so they always terminate. Li and F live in a ring of small
 // per-group slots (reused NS groups later, after the group's last O task).
 __global__ void __launch_bounds__(NT, MRA_MINB)
-k_wide_mtile(TreeParams tp, WideParams wp, long long g_first, double* out, long long out_first, int q,
+k_wide_mtile(TreeParams tp, TREG, WideParams wp, long long g_first, double* out, long long out_first, int q,
              const int4* tasks, long long ntask, unsigned long long* counter, MergeRing ring) {
     double* smem = dyn_smem();
     ENGINE_INIT(smem);
@@ -581,7 +589,7 @@ k_wide_mtile(TreeParams tp, WideParams wp, long long g_first, double* out, long 
 }
 
 __global__ void __launch_bounds__(NT, MRA_MINB)
-k_prior(TreeParams tp, int m, long long t_first, long long nitems, double* ws, long long ws_stride,
+k_prior(TreeParams tp, TREG, int m, long long t_first, long long nitems, double* ws, long long ws_stride,
         unsigned long long* counter) {
     double* smem = dyn_smem();
     ENGINE_INIT(smem);
@@ -618,11 +626,11 @@ k_prior(TreeParams tp, int m, long long t_first, long long nitems, double* ws, l
 
 // --------------------------------------------------------------------------- merge
 __global__ void __launch_bounds__(NT, MRA_MINB)
-k_merge(TreeParams tp, int m, long long t_first, long long t_count, const double* child_out, long long child_first,
+k_merge(TreeParams tp, TREG, int m, long long t_first, long long t_count, const double* child_out, long long child_first,
         double* out, long long out_first, int q, double* ws, long long ws_stride, unsigned long long* counter,
         int presummed) {
     double* smem = dyn_smem();
-    ENGINE_INIT(smem);
+    ENGINE_INIT_NOREG(smem);
     const CovP cp = to_covp(tp.cp);
     const int J = tp.J, rh = tp.rh;
     const int qc = m * rh + 1;
@@ -769,8 +777,8 @@ static const GemmAttrs& gemm_set_attrs() {
 
 // phases: 0 chain, 1 sigma, 2 update, 3 diag, 4 panel_x, 5 trsm, 6 covfill (6: mra_kernels.cu).
 // `grid` is ignored for this unit's phases: a persistent grid of every resident CTA pulls the tasks.
-cudaError_t launch_wide(int phase, const TreeParams& tp, const WideParams& wp, int step, const int4* tasks,
-                        long long ntask, int grid, unsigned long long* counter, cudaStream_t st) {
+cudaError_t launch_wide(int phase, const TreeParams& tp, const TmaReg& reg, const WideParams& wp, int step,
+                        const int4* tasks, long long ntask, int grid, unsigned long long* counter, cudaStream_t st) {
     if (phase == 6) return launch_wide_main(phase, tp, wp, step, tasks, ntask, grid, counter, st);
     if (phase < 0 || phase > 6) return cudaErrorInvalidValue;
     long long g = gemm_set_attrs().resident[phase];
@@ -778,12 +786,12 @@ cudaError_t launch_wide(int phase, const TreeParams& tp, const WideParams& wp, i
     if (g < 1) return cudaSuccess;
     const int b = gemm_smem_bytes();
     switch (phase) {
-        case 0: ++g_kernel_launches; k_wide_chain<<<(int)g, NT, b, st>>>(tp, wp, tasks, ntask, counter); break;
-        case 1: ++g_kernel_launches; k_wide_sigma<<<(int)g, NT, b, st>>>(tp, wp, tasks, ntask, counter); break;
-        case 2: ++g_kernel_launches; k_wide_update<<<(int)g, NT, b, st>>>(tp, wp, step, tasks, ntask, counter); break;
-        case 3: ++g_kernel_launches; k_wide_diag<<<(int)g, NT, b, st>>>(tp, wp, step, tasks, ntask, counter); break;
-        case 4: ++g_kernel_launches; k_wide_panel_x<<<(int)g, NT, b, st>>>(tp, wp, step, tasks, ntask, counter); break;
-        case 5: ++g_kernel_launches; k_wide_trsm<<<(int)g, NT, b, st>>>(tp, wp, tasks, ntask, counter); break;
+        case 0: ++g_kernel_launches; k_wide_chain<<<(int)g, NT, b, st>>>(tp, reg, wp, tasks, ntask, counter); break;
+        case 1: ++g_kernel_launches; k_wide_sigma<<<(int)g, NT, b, st>>>(tp, reg, wp, tasks, ntask, counter); break;
+        case 2: ++g_kernel_launches; k_wide_update<<<(int)g, NT, b, st>>>(tp, reg, wp, step, tasks, ntask, counter); break;
+        case 3: ++g_kernel_launches; k_wide_diag<<<(int)g, NT, b, st>>>(tp, reg, wp, step, tasks, ntask, counter); break;
+        case 4: ++g_kernel_launches; k_wide_panel_x<<<(int)g, NT, b, st>>>(tp, reg, wp, step, tasks, ntask, counter); break;
+        case 5: ++g_kernel_launches; k_wide_trsm<<<(int)g, NT, b, st>>>(tp, reg, wp, tasks, ntask, counter); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
@@ -791,7 +799,8 @@ cudaError_t launch_wide(int phase, const TreeParams& tp, const WideParams& wp, i
 
 // the level-(M-1) merge tile dataflow: every CTA of the grid must be resident (consumers spin on tasks
 // claimed earlier by co-resident CTAs), so the grid is exactly the resident CTA count
-cudaError_t launch_wide_mtile(const TreeParams& tp, const WideParams& wp, long long g_first, long long g_count,
+cudaError_t launch_wide_mtile(const TreeParams& tp, const TmaReg& reg, const WideParams& wp, long long g_first,
+                              long long g_count,
                               double* out, long long out_first, int q, const int4* tasks, long long ntask, int grid,
                               unsigned long long* counter, const MergeRing& ring, cudaStream_t st) {
     (void)grid;
@@ -803,12 +812,12 @@ cudaError_t launch_wide_mtile(const TreeParams& tp, const WideParams& wp, long l
     if (e == cudaSuccess) e = cudaMemsetAsync(ring.slot_done, 0, sizeof(long long) * ring.ns, st);
     if (e != cudaSuccess) return e;
     ++g_kernel_launches;
-    k_wide_mtile<<<(int)gr, NT, gemm_smem_bytes(), st>>>(tp, wp, g_first, out, out_first, q, tasks, ntask, counter,
+    k_wide_mtile<<<(int)gr, NT, gemm_smem_bytes(), st>>>(tp, reg, wp, g_first, out, out_first, q, tasks, ntask, counter,
                                                         ring);
     return cudaGetLastError();
 }
 
-cudaError_t launch_merge(const TreeParams& tp, int m, long long t_first, long long t_count, const double* child_out,
+cudaError_t launch_merge(const TreeParams& tp, const TmaReg& reg, int m, long long t_first, long long t_count, const double* child_out,
                          long long child_first, double* out, long long out_first, int q, int grid, double* ws,
                          long long ws_stride, unsigned long long* counter, cudaStream_t st) {
     const GemmAttrs& A = gemm_set_attrs();
@@ -827,18 +836,18 @@ cudaError_t launch_merge(const TreeParams& tp, int m, long long t_first, long lo
         if (e != cudaSuccess) return e;
     }
     ++g_kernel_launches;
-    k_merge<<<grid, NT, gemm_smem_bytes(), st>>>(tp, m, t_first, t_count, child_out, child_first, out, out_first, q, ws,
+    k_merge<<<grid, NT, gemm_smem_bytes(), st>>>(tp, reg, m, t_first, t_count, child_out, child_first, out, out_first, q, ws,
                                            ws_stride, counter, presummed);
     return cudaGetLastError();
 }
 
 // k_prior of one level (the covariance blocks are filled first by launch_prior in mra_kernels.cu)
-cudaError_t launch_prior_unit(const TreeParams& tp, int m, long long t_first, long long t_count, int grid, double* ws,
-                              long long ws_stride, unsigned long long* counter, cudaStream_t st) {
+cudaError_t launch_prior_unit(const TreeParams& tp, const TmaReg& reg, int m, long long t_first, long long t_count,
+                              int grid, double* ws, long long ws_stride, unsigned long long* counter, cudaStream_t st) {
     grid = (int)std::min<long long>({(long long)grid, (long long)gemm_set_attrs().resident[7], t_count});
     if (grid < 1) return cudaSuccess;
     ++g_kernel_launches;
-    k_prior<<<grid, NT, gemm_smem_bytes(), st>>>(tp, m, t_first, t_count, ws, ws_stride, counter);
+    k_prior<<<grid, NT, gemm_smem_bytes(), st>>>(tp, reg, m, t_first, t_count, ws, ws_stride, counter);
     return cudaGetLastError();
 }
 
@@ -855,6 +864,50 @@ void phase_cycles_unit(unsigned long long* out32, bool reset) {
         unsigned long long z[32] = {0};
         cudaMemcpyToSymbol(g_phase_cycles, z, sizeof z);
     }
+}
+
+// Host encoding of a registry entry (cuTensorMapEncodeTiled through the runtime's driver entry point, so the
+// library has no link-time dependency on libcuda). MEMN: 2-D (ld columns, rows), row stride ld, box (16, 64),
+// 128-byte swizzle; MEMT: 3-D (8, rows, ceil(ld / 8)), strides (ld, 8) doubles, box (8, 16, 8), no swizzle.
+bool tma_register(TmaReg& reg, int kind, const double* base, long long ld, long long rows) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    });
+    if (!encode || reg.n >= TMA_NREG || !base || ld <= 0 || (ld & 1) || rows <= 0 ||
+        (reinterpret_cast<uintptr_t>(base) & 15))
+        return false;
+    CUtensorMap* m = &reg.map[reg.n];
+    CUresult r;
+    if (kind == 0) {
+        cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
+        cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+        cuuint32_t box[2] = {16, 64};
+        cuuint32_t es[2] = {1, 1};
+        r = encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    } else {
+        cuuint64_t dims[3] = {8, (cuuint64_t)rows, (cuuint64_t)((ld + 7) / 8)};
+        cuuint64_t strides[2] = {(cuuint64_t)ld * 8, 64};
+        cuuint32_t box[3] = {8, 16, 8};
+        cuuint32_t es[3] = {1, 1, 1};
+        r = encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
+    if (r != CUDA_SUCCESS) return false;
+    reg.base[reg.n] = reinterpret_cast<unsigned long long>(base);
+    reg.bytes[reg.n] = (unsigned long long)(ld * rows * 8);
+    reg.ld[reg.n] = ld;
+    reg.kind[reg.n] = kind;
+    reg.n++;
+    return true;
 }
 
 // resident CTAs of the merge tile dataflow (the host sizes its look-ahead D1 with it)
