@@ -262,8 +262,13 @@ __device__ __forceinline__ double frag(const double* s, int row, int k) {
 // MI x 4 DMMAs per k-step of 4 on the warp's WM x 32 sub-tile
 // MASK: the ragged k-tile's fragments with k >= nk are zeroed (the bulk-copy path leaves stale values there; the
 // cp.async path zero-fills, MASK = false)
-template <int KA, int KB, bool MASK = false, int LAY = 0>
-__device__ __forceinline__ void mma_ktile(double (&acc)[MI][4][2], const double* As, const double* Bs, int nk) {
+// tri (TRI instantiations only: the Sigma tiles, EPI = 1): the warp's sub-tile sits on the diagonal of a lower-triangular
+// output tile (WM == WN): the 8 x 8 blocks strictly above the diagonal are not needed (the epilogue never stores
+// them), so their DMMAs are not issued -- the SM's fp64 pipe is shared by the co-resident CTAs, which get that
+// time. (Compiled into every instantiation, the branch slowed the others by a few % through code size.)
+template <int KA, int KB, bool MASK = false, int LAY = 0, bool TRI = false>
+__device__ __forceinline__ void mma_ktile(double (&acc)[MI][4][2], const double* As, const double* Bs, int nk,
+                                          bool tri = false) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
     const int wr = (warp / (64 / WN)) * WM, wc = (warp % (64 / WN)) * WN;
@@ -273,10 +278,18 @@ __device__ __forceinline__ void mma_ktile(double (&acc)[MI][4][2], const double*
         for (int mi = 0; mi < MI; mi++) a[mi] = frag<KA, LAY>(As, wr + mi * 8 + g, kk + t);
 #pragma unroll
         for (int ni = 0; ni < 4; ni++) b[ni] = frag<KB, LAY>(Bs, wc + ni * 8 + g, kk + t);
+        if (TRI && WM == WN && tri) {
 #pragma unroll
-        for (int mi = 0; mi < MI; mi++)
+            for (int mi = 0; mi < MI; mi++)
 #pragma unroll
-            for (int ni = 0; ni < 4; ni++) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+                for (int ni = 0; ni < 4; ni++)
+                    if (ni <= mi) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+        } else {
+#pragma unroll
+            for (int mi = 0; mi < MI; mi++)
+#pragma unroll
+                for (int ni = 0; ni < 4; ni++) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+        }
     };
     if (nk == TK) {
 #pragma unroll
@@ -296,7 +309,8 @@ __device__ __forceinline__ void mma_ktile(double (&acc)[MI][4][2], const double*
 #pragma unroll
             for (int mi = 0; mi < MI; mi++)
 #pragma unroll
-                for (int ni = 0; ni < 4; ni++) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+                for (int ni = 0; ni < 4; ni++)
+                    if (!(TRI && WM == WN && tri) || ni <= mi) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
         }
     }
 }
@@ -418,9 +432,9 @@ __device__ __forceinline__ void tma_tile(double* dst, const TmaReg* reg, int ti,
 #endif
 
 // accumulate both K-segments of one output tile through an NSTAGE-deep cp.async pipeline
-template <int KA0, int KB0, int KA1, int KB1>
+template <int KA0, int KB0, int KA1, int KB1, bool TRI = false>
 __device__ __forceinline__ void tile_pipeline(double (&acc)[MI][4][2], const GemmDesc& d, int r0, int nr, int c0,
-                                              int nc, double* smem, bool wact) {
+                                              int nc, double* smem, int wact) {
     // only the current segment's two operand descriptors are held in registers (segment 1's are read
     // from the shared-memory GemmDesc when the loads reach it): the engine sits at the 128-register
     // budget of two 256-thread CTAs per SM
@@ -458,8 +472,8 @@ __device__ __forceinline__ void tile_pipeline(double (&acc)[MI][4][2], const Gem
         if (!wact) continue;   // this warp's 16 x 32 sub-tile holds no wanted output (it still loads)
         const double* As = smem + (kt % NSTAGE) * STAGE_DBL;
         const double* Bs = As + TILE_DBL;
-        if (kt < T0) mma_ktile<KA0, KB0>(acc, As, Bs, min(TK, K0 - kt * TK));
-        else mma_ktile<KA1, KB1>(acc, As, Bs, min(TK, K1 - (kt - T0) * TK));
+        if (kt < T0) mma_ktile<KA0, KB0, false, 0, TRI>(acc, As, Bs, min(TK, K0 - kt * TK), wact == 2);
+        else mma_ktile<KA1, KB1, false, 0, TRI>(acc, As, Bs, min(TK, K1 - (kt - T0) * TK), wact == 2);
     }
     cp_async_wait<0>();
 }
@@ -468,9 +482,9 @@ __device__ __forceinline__ void tile_pipeline(double (&acc)[MI][4][2], const Gem
 // every operand of the call is a bulk-staged MEMT: warp 0 keeps NSTAGE - 1 k-tiles in flight (lane 0 waits for a
 // stage's empty barrier and posts the byte count, the lanes issue the k-row copies), every warp waits on the
 // stage's full barrier, runs its DMMAs and arrives on the empty barrier
-template <int KA0, int KB0, int KA1, int KB1>
+template <int KA0, int KB0, int KA1, int KB1, bool TRI = false>
 __device__ __forceinline__ void tile_pipeline_bulk(double (&acc)[MI][4][2], const GemmDesc& d, int r0, int nr, int c0,
-                                                   int nc, double* smem, bool wact, unsigned gs) {
+                                                   int nc, double* smem, int wact, unsigned gs) {
     BulkState* bs = bulk_state(smem);
     const int K0 = d.K0, K1 = d.K1, T0 = (K0 + TK - 1) / TK, T = T0 + (K1 + TK - 1) / TK;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -497,8 +511,8 @@ __device__ __forceinline__ void tile_pipeline_bulk(double (&acc)[MI][4][2], cons
         if (wact) {
             const double* As = smem + b * STAGE_DBL;
             const double* Bs = As + TILE_DBL;
-            if (kt < T0) mma_ktile<KA0, KB0, true>(acc, As, Bs, min(TK, K0 - kt * TK));
-            else mma_ktile<KA1, KB1, true>(acc, As, Bs, min(TK, K1 - (kt - T0) * TK));
+            if (kt < T0) mma_ktile<KA0, KB0, true, 0, TRI>(acc, As, Bs, min(TK, K0 - kt * TK), wact == 2);
+            else mma_ktile<KA1, KB1, true, 0, TRI>(acc, As, Bs, min(TK, K1 - (kt - T0) * TK), wact == 2);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&bs->empty[b]);
@@ -508,9 +522,9 @@ __device__ __forceinline__ void tile_pipeline_bulk(double (&acc)[MI][4][2], cons
 // every operand of the call lies in a registered buffer: thread 0 keeps NSTAGE - 1 k-tiles in flight, one TMA tensor
 // load per operand k-tile (16 KB per stage); full / empty barriers as the bulk pipeline; ragged k-tiles masked (the
 // boxes read the buffer's next columns / rows there)
-template <int KA0, int KB0, int KA1, int KB1>
+template <int KA0, int KB0, int KA1, int KB1, bool TRI = false>
 __device__ __forceinline__ void tile_pipeline_tma(double (&acc)[MI][4][2], const GemmDesc& d, int r0, int c0,
-                                                  double* smem, bool wact, unsigned gs) {
+                                                  double* smem, int wact, unsigned gs) {
     BulkState* bs = bulk_state(smem);
     const TmaReg* reg = bs->reg;
     const int K0 = d.K0, K1 = d.K1, T0 = (K0 + TK - 1) / TK, T = T0 + (K1 + TK - 1) / TK;
@@ -539,8 +553,8 @@ __device__ __forceinline__ void tile_pipeline_tma(double (&acc)[MI][4][2], const
         if (wact) {
             const double* As = smem + b * STAGE_DBL;
             const double* Bs = As + TILE_DBL;
-            if (kt < T0) mma_ktile<KA0, KB0, true, 1>(acc, As, Bs, min(TK, K0 - kt * TK));
-            else mma_ktile<KA1, KB1, true, 1>(acc, As, Bs, min(TK, K1 - (kt - T0) * TK));
+            if (kt < T0) mma_ktile<KA0, KB0, true, 1, TRI>(acc, As, Bs, min(TK, K0 - kt * TK), wact == 2);
+            else mma_ktile<KA1, KB1, true, 1, TRI>(acc, As, Bs, min(TK, K1 - (kt - T0) * TK), wact == 2);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&bs->empty[b]);
@@ -586,18 +600,21 @@ __device__ __noinline__ void cta_gemm_impl(double* smem) {
                 for (int ni = 0; ni < 4; ni++) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
             // warps whose sub-tile lies outside a ragged tile (e.g. the 1-row y tile) or strictly above the
             // diagonal of a lower-triangular tile skip their DMMAs
-            const bool wact = wr < nr && wc < nc && !(lower && tm == tn && wc > wr + WM - 1);
+            // 0: the warp's sub-tile holds no wanted output; 1: active; 2: active on the diagonal of a lower tile
+            const int wact = (wr < nr && wc < nc && !(lower && tm == tn && wc > wr + WM - 1))
+                                 ? ((WM == WN && lower && tm == tn && wr == wc) ? 2 : 1)
+                                 : 0;
 #ifdef MRA_BULK
             if (MODE == 1) {
-                tile_pipeline_bulk<KA0, KB0, KA1, KB1>(acc, d, r0, nr, c0, nc, smem, wact, gs);
+                tile_pipeline_bulk<KA0, KB0, KA1, KB1, EPI == 1>(acc, d, r0, nr, c0, nc, smem, wact, gs);
                 gs += (K0 + TK - 1) / TK + (K1 + TK - 1) / TK;
             } else if (MODE == 3) {
-                tile_pipeline_tma<KA0, KB0, KA1, KB1>(acc, d, r0, c0, smem, wact, gs);
+                tile_pipeline_tma<KA0, KB0, KA1, KB1, EPI == 1>(acc, d, r0, c0, smem, wact, gs);
                 gs += (K0 + TK - 1) / TK + (K1 + TK - 1) / TK;
             } else
 #endif
             if (K0 + K1 > 0)
-                tile_pipeline<KA0, KB0, KA1, KB1>(acc, d, r0, nr, c0, nc, smem, wact);
+                tile_pipeline<KA0, KB0, KA1, KB1, EPI == 1>(acc, d, r0, nr, c0, nc, smem, wact);
             const CInit ci = d.ci;
             const double alpha = d.alpha;
             double* C = d.C;
