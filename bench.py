@@ -334,7 +334,8 @@ def run_gpu(args, rank, world, local_rank):
         torch.distributed.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     plan = mra.mra_plan_create(w.x, w.y, w.M, w.J, w.r, device=local_rank, stream=stream, rank=rank,
-                               world=world, stream_prior=args.stream_prior, theta_lanes=lanes, nccl_id=nccl_id)
+                               world=world, stream_prior=args.stream_prior, theta_lanes=lanes, nccl_id=nccl_id,
+                               graph=bool(args.graph))
     torch.cuda.synchronize()
     plan_s = time.time() - t0
     log(f"[rank {rank}] plan in {plan_s:.1f}s: n_retained={plan.n_retained} r_hat={plan.r_hat}")
@@ -481,7 +482,7 @@ def run_gpu(args, rank, world, local_rank):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": dict(config_block(w, plan, world), theta_lanes=lanes),
+            "config": dict(config_block(w, plan, world), theta_lanes=lanes, cuda_graph=bool(args.graph)),
             "loglik": lls[0], "n_theta_per_step": ntheta, "flops_per_step": fm["total"] * ntheta,
             "e2e": {"value": e2e_val, "unit": UNIT,
                     # a sweep (mra_loglik_batch) copies y once per step, single evaluations once per theta
@@ -514,6 +515,8 @@ def main():
                     "evaluation contexts for a theta sweep (C4: no gain, its phases already fill the GPU; see DESIGN.md)")
     ap.add_argument("--stream-prior", type=int, default=0, help="plan option stream_prior (NEXT-4): 0 auto, "
                     "1 always, -1 never")
+    ap.add_argument("--graph", type=int, default=0, help="plan option graph: log-L evaluations on device y replayed as "
+                    "a CUDA graph (theta from device memory); measured no faster: C0 0.98 -> 1.24 ms, C1 3.15 -> 3.10, C2 equal")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle CPU work")
     ap.add_argument("--ref-budget", type=float, default=10.0, help="seconds of oracle work per reference step")

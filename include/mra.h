@@ -102,6 +102,10 @@ typedef struct {
                          caching allocator); NULL = cudaMalloc. Every device buffer the plan owns or
                          uses temporarily is taken from it; returns NULL on failure (-> MRA_E_OOM)  */
     void (*dfree)(void* ptr, int device, void* stream);        /* its release; required with dalloc    */
+    int graph;        /* 1 = mra_loglik_dev evaluations (log L only, one context, no communicator, profiling off) are
+                         captured once as a CUDA graph and replayed: theta is read from a small device buffer the
+                         call refreshes, so one graph serves every (sigma2, rho, tau2) of a covariance family; it
+                         is re-captured when the family or the y pointer changes. 0 = direct launches (default). */
 } mra_opts;
 
 /* Posterior state requested from an evaluation; any pointer may be NULL. */

@@ -50,7 +50,7 @@ class _Opts(ctypes.Structure):
                 ("world", ctypes.c_int), ("shard_level", ctypes.c_int), ("mem_budget_gb", ctypes.c_double),
                 ("wide", ctypes.c_int), ("host_plan", ctypes.c_int), ("stream_prior", ctypes.c_int),
                 ("theta_lanes", ctypes.c_int), ("nccl_id", ctypes.c_void_p), ("dalloc", _DALLOC),
-                ("dfree", _DFREE)]
+                ("dfree", _DFREE), ("graph", ctypes.c_int)]
 
 
 class _Post(ctypes.Structure):
@@ -210,7 +210,7 @@ def _torch_hooks():
 
 def mra_plan_create(x, y, M, J, r, offset=0.0, xscale=0.0, yscale=0.0, device=-1, stream=None, rank=0,
                     world=1, shard_level=0, mem_budget_gb=0.0, wide=0, host_plan=0,
-                    stream_prior=0, theta_lanes=0, nccl_id=None, torch_alloc=False) -> PlanHandle:
+                    stream_prior=0, theta_lanes=0, nccl_id=None, torch_alloc=False, graph=False) -> PlanHandle:
     """Build a plan. nccl_id (bytes from mra_nccl_unique_id on rank 0) gives the plan its own NCCL communicator
     for the in-library exchange step of subtree sharding; torch_alloc=True routes its device memory through
     torch's caching allocator (opts.dalloc / dfree)."""
@@ -228,7 +228,7 @@ def mra_plan_create(x, y, M, J, r, offset=0.0, xscale=0.0, yscale=0.0, device=-1
     opts = _Opts(float(offset), float(xscale), float(yscale), int(device), _stream_ptr(stream), int(rank),
                  int(world), int(shard_level), float(mem_budget_gb), int(wide), int(host_plan), int(stream_prior),
                  int(theta_lanes), ctypes.cast(idbuf, ctypes.c_void_p) if idbuf is not None else None,
-                 hooks[0], hooks[1])
+                 hooks[0], hooks[1], int(bool(graph)))
     out = ctypes.c_void_p()
     _check(lib.mra_plan_create(_dptr(x), _dptr(y), x.shape[0], int(M), int(J), int(r), ctypes.byref(opts),
                                ctypes.byref(out)))

@@ -177,6 +177,16 @@ struct mra_plan {
     int4* wtasks = nullptr;
     double *wG = nullptr, *wS = nullptr, *wD = nullptr, *wlblk = nullptr;
     long long wG_rows = 0;
+    // CUDA-graph replay of log-L evaluations (opts.graph)
+    bool use_graph = false;
+    double* theta_d = nullptr;        // {sigma2, rho, tau2} read by the kernels of a replayed evaluation
+    double* theta_h = nullptr;        // pinned staging of theta_d
+    cudaGraphExec_t gexec = nullptr;
+    cudaStream_t gst = nullptr;       // the plan's own stream for capture / replay (the caller's stream may be the
+    cudaEvent_t gev = nullptr;        // legacy default stream, which cannot be captured); ordered after the caller's
+    const double* g_y = nullptr;      // key of the captured graph: y pointer and covariance family
+    int g_cov = -1;
+    uint64_t g_launches = 0;
     // TMA tensor maps of this context's long-lived buffers (G, prior rows per level, merge ring): handed to the GEMM
     // unit's kernels by value (build_registry)
     TmaReg treg{};
@@ -847,6 +857,12 @@ static mra_status make_lane(mra_plan* P, mra_plan** out) {
     Q->cev = nullptr;
     Q->host_y_pending = nullptr;
     Q->post = Q->muhat = Q->mu_d = Q->smooth_d = Q->ws_smooth = Q->ws_pred = nullptr;
+    Q->use_graph = false;
+    Q->gexec = nullptr;
+    Q->gst = nullptr;
+    Q->gev = nullptr;
+    Q->theta_h = nullptr;
+    Q->theta_d = nullptr;
     Q->post_valid = false;
     Q->st = nullptr;
     *out = nullptr;
@@ -1036,6 +1052,17 @@ extern "C" mra_status mra_plan_create(const double* x, const double* y, uint64_t
         P->n_lanes = std::max(1, std::min(o.theta_lanes, 16));
         if (P->world > 1 || P->nccl) P->n_lanes = 1;
         TRY(size_device(P, o.mem_budget_gb, o.stream_prior));
+    init_kernel_attrs();   // smem attributes / occupancy now: nothing of the kind may run inside a graph capture
+    if (o.graph) {
+        P->use_graph = true;
+        TRY(dalloc(P, (void**)&P->theta_d, 8 * 4, "theta"));
+        if (cudaMallocHost((void**)&P->theta_h, 32) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&P->gst, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&P->gev, cudaEventDisableTiming) != cudaSuccess) {
+            mra_plan_destroy(P);
+            return fail(MRA_E_CUDA, "graph staging (pinned theta, stream, event)");
+        }
+    }
     build_registry(P);
         if (P->nccl) {
             const NcclApi* nc = nccl_api();
@@ -1072,6 +1099,10 @@ extern "C" void mra_plan_destroy(mra_plan* P) {
     if (P->device >= 0 && cudaSetDevice(P->device) == cudaSuccess) {
         cudaDeviceSynchronize();
         if (P->is_lane && P->st) cudaStreamDestroy(P->st);
+        if (P->gexec) cudaGraphExecDestroy(P->gexec);
+        if (P->gev) cudaEventDestroy(P->gev);
+        if (P->gst) cudaStreamDestroy(P->gst);
+        if (P->theta_h && !P->is_lane) cudaFreeHost(P->theta_h);
         if (P->lane_ev) cudaEventDestroy(P->lane_ev);
         for (cudaEvent_t e : P->evpool) cudaEventDestroy(e);
         if (P->cev) cudaEventDestroy(P->cev);
@@ -1181,6 +1212,7 @@ static TreeParams tree_params(mra_plan* P, const mra_theta* th) {
     tp.kxy = P->kxy_d; tp.prior = P->prior;
     for (int m = 0; m <= MAXM; m++) { tp.prior_base[m] = P->prior_base[m]; tp.post_base[m] = P->post_base[m]; }
     tp.dreg = P->dreg; tp.ureg = P->ureg; tp.err = P->err; tp.post = nullptr;
+    tp.theta_dev = nullptr;
     return tp;
 }
 
@@ -1481,6 +1513,65 @@ static bool all_finite(const double* y, uint64_t n) {
 static mra_status run_eval_nccl(mra_plan* P, const double* d_y, const mra_theta* th, double* loglik, mra_post* post,
                                 bool host_post);
 
+// opts.graph: the whole log-L evaluation (memsets, gather, prior, the wide phases, merges, final) captured once on the
+// plan stream as a CUDA graph and replayed; the kernels read theta from P->theta_d (refreshed before each replay),
+// so the graph depends only on the plan, the y pointer and the covariance family (re-captured when those change)
+static mra_status run_eval_graph_on(mra_plan* P, const double* d_y, const mra_theta* th, double* loglik,
+                                   mra_post* post);
+static mra_status run_eval_graph(mra_plan* P, const double* d_y, const mra_theta* th, double* loglik, mra_post* post) {
+    mra_status s = check_theta(th);
+    if (s) return s;
+    if (cudaSetDevice(P->device) != cudaSuccess) return fail(MRA_E_CUDA, "cudaSetDevice failed");
+    g_err.clear();
+    // capture / replay on the plan's own stream, after everything the caller queued (e.g. the write of y)
+    CU(cudaEventRecord(P->gev, P->st));
+    CU(cudaStreamWaitEvent(P->gst, P->gev, 0));
+    cudaStream_t user = P->st;
+    P->st = P->gst;
+    s = run_eval_graph_on(P, d_y, th, loglik, post);
+    P->st = user;
+    return s;
+}
+static mra_status run_eval_graph_on(mra_plan* P, const double* d_y, const mra_theta* th, double* loglik,
+                                   mra_post* post) {
+    mra_status s;
+    if (!P->gexec || P->g_y != d_y || P->g_cov != th->cov) {
+        if (P->gexec) { cudaGraphExecDestroy(P->gexec); P->gexec = nullptr; }
+        CU(cudaStreamBeginCapture(P->st, cudaStreamCaptureModeThreadLocal));
+        mra_status cs = begin_eval(P, d_y, th);
+        TreeParams tp = tree_params(P, th);
+        tp.theta_dev = P->theta_d;
+        if (!cs) cs = eval_lower(P, tp);
+        if (!cs) cs = eval_upper(P, tp);
+        cudaGraph_t g = nullptr;
+        const cudaError_t ec = cudaStreamEndCapture(P->st, &g);
+        if (cs) { if (g) cudaGraphDestroy(g); return cs; }
+        if (ec != cudaSuccess) return fail(MRA_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(ec));
+        const cudaError_t ei = cudaGraphInstantiate(&P->gexec, g, 0);
+        cudaGraphDestroy(g);
+        if (ei != cudaSuccess) { P->gexec = nullptr; return fail(MRA_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ei)); }
+        P->g_y = d_y;
+        P->g_cov = th->cov;
+        P->g_launches = P->launches;
+    }
+    P->post_valid = false;
+    P->theta_h[0] = th->sigma2; P->theta_h[1] = th->rho; P->theta_h[2] = th->tau2; P->theta_h[3] = 0.0;
+    CU(cudaMemcpyAsync(P->theta_d, P->theta_h, 32, cudaMemcpyHostToDevice, P->st));
+    CU(cudaGraphLaunch(P->gexec, P->st));
+    P->launches = P->g_launches;
+    double ll = NAN;
+    CU(cudaMemcpyAsync(&ll, P->loglik_d, 8, cudaMemcpyDeviceToHost, P->st));
+    if ((s = check_err(P))) return s;
+    if (loglik) *loglik = ll;
+    if (post) {
+        CU(cudaMemcpy(&post->d, P->dreg, 8, cudaMemcpyDeviceToHost));
+        CU(cudaMemcpy(&post->u, P->ureg, 8, cudaMemcpyDeviceToHost));
+        if (post->region_d) CU(cudaMemcpy(post->region_d, P->dreg, 8 * P->nreg, cudaMemcpyDeviceToHost));
+        if (post->region_u) CU(cudaMemcpy(post->region_u, P->ureg, 8 * P->nreg, cudaMemcpyDeviceToHost));
+    }
+    return MRA_OK;
+}
+
 static mra_status run_eval(mra_plan* P, const double* d_y, const mra_theta* th, double* loglik, mra_post* post,
                            bool host_post) {
     if (P->nccl) return run_eval_nccl(P, d_y, th, loglik, post, host_post);
@@ -1490,6 +1581,7 @@ static mra_status run_eval(mra_plan* P, const double* d_y, const mra_theta* th, 
     mra_status s;
     const bool want_state = post && (post->mu || post->smooth);
     if (want_state && (s = ensure_post(P))) return s;
+    if (P->use_graph && !want_state && !P->prof && !P->host_y_pending) return run_eval_graph(P, d_y, th, loglik, post);
     if ((s = begin_eval(P, d_y, th))) return s;
     TreeParams tp = tree_params(P, th);
     if (want_state) tp.post = P->post;

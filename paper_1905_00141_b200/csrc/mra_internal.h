@@ -33,6 +33,7 @@ struct TreeParams {
     // posterior-state storage (nullptr unless requested)
     double* post;               // per interior region: Ltilde^{-1} (rh x rh) then F = H^T (q x rh)
     long long post_base[MAXM + 1];
+    const double* theta_dev;    // nullptr, or {sigma2, rho, tau2} in device memory (evaluations replayed as graphs)
 };
 
 // per-CTA workspace layout of the bottom / smoothing kernels (offsets in doubles)
@@ -138,6 +139,7 @@ cudaError_t launch_wide_main(int phase, const TreeParams& tp, const WideParams& 
 cudaError_t launch_prior_unit(const TreeParams& tp, const TmaReg& reg, int m, long long t_first, long long t_count,
                               int grid, double* ws, long long ws_stride, unsigned long long* counter, cudaStream_t st);
 int unit_ctas_per_sm();
+void init_kernel_attrs();   // every kernel's smem attribute / occupancy for the current device (before any capture)
 void phase_cycles_unit(unsigned long long* out32, bool reset);
 int wide_mtile_resident();
 cudaError_t launch_wide_mtile(const TreeParams& tp, const TmaReg& reg, const WideParams& wp, long long g_first,

@@ -33,6 +33,18 @@ __device__ __forceinline__ CovP to_covp(const CovParams& c) {
     p.ir = (c.kind == 0 ? 1.0 : 1.7320508075688772935) / c.rho;
     return p;
 }
+// theta of the evaluation: by value in TreeParams, or -- for an evaluation replayed as a CUDA graph -- read from the
+// plan's device buffer {sigma2, rho, tau2} that the host refreshes before each replay (the covariance family is
+// part of the graph's key)
+__device__ __forceinline__ CovP covp_of(const TreeParams& tp) {
+    CovParams c = tp.cp;
+    if (tp.theta_dev) {
+        c.s2 = tp.theta_dev[0];
+        c.rho = tp.theta_dev[1];
+    }
+    return to_covp(c);
+}
+__device__ __forceinline__ double tau2_of(const TreeParams& tp) { return tp.theta_dev ? tp.theta_dev[2] : tp.tau2; }
 
 __device__ __forceinline__ void set_err(int* err, int level, long long idx) {
     if (atomicCAS(err, 0, 1) == 0) {

@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(CFT)
 k_prior_covfill(TreeParams tp, int m, long long t_first, long long nitems) {
     __shared__ double2 pts_s[64];
     __shared__ double2 knots_s[MAXM * 64];
-    const CovP cp = to_covp(tp.cp);
+    const CovP cp = covp_of(tp);
     const int rh = tp.rh, W = m * rh;
     const long long ldR = (long long)m * rh;
     for (long long it = blockIdx.x; it < nitems; it += gridDim.x) {
@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(NT, MRA_MINB)
 k_bottom(TreeParams tp, long long g_first, long long g_count, double* out, long long out_first, int q, double* ws,
          WsLayout L, unsigned long long* counter) {
     double* smem = dyn_smem();
-    const CovP cp = to_covp(tp.cp);
+    const CovP cp = covp_of(tp);
     const int M = tp.M, J = tp.J, rh = tp.rh;
     const int m = M - 1;                 // group level; 0 when M == 1 (the root is the only leaf)
     const int Jc = (M == 1) ? 1 : J;     // leaves per group
@@ -129,7 +129,7 @@ k_bottom(TreeParams tp, long long g_first, long long g_count, double* out, long 
             PHASE_MARK(c1);
             // Sigma_j = C(S,S) + tau2 I - V V^T  (nugget on the observation diagonal only, reading R2)
             cta_gemm<MEMN, MEMN, MEMN, MEMN, 1>(n, n, 1, op_mem(Gc, L.ldG), op_mem(Gc, L.ldG), Pg, op_mem(Gc, L.ldG),
-                                             op_mem(Gc, L.ldG), 0, ci_cov(pts, pts, tp.tau2), -1.0, S,
+                                             op_mem(Gc, L.ldG), 0, ci_cov(pts, pts, tau2_of(tp)), -1.0, S,
                                              L.ldS, cp, smem);
             PHASE_ADD(1, c1);
             PHASE_MARK(c2);
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(NT, MRA_MINB)
 k_smooth(TreeParams tp, const double* muhat, const long long* perm, double* smooth, double* ws, WsLayout L,
          unsigned long long* counter, long long l_first, long long l_count) {
     double* smem = dyn_smem();
-    const CovP cp = to_covp(tp.cp);
+    const CovP cp = covp_of(tp);
     const int M = tp.M, rh = tp.rh, m = M - 1, Pg = m * rh;
     double* base = ws + (long long)blockIdx.x * L.stride;
     double *G = base + L.oG, *S = base + L.oS, *D = base + L.oD, *r = base + L.oV;
@@ -289,7 +289,7 @@ k_smooth(TreeParams tp, const double* muhat, const long long* perm, double* smoo
         const double* pts = tp.pxy + 2 * o0;
         point_chain(tp, m, t, n, pts, G, L.ldG, cp, smem);
         cta_gemm<MEMN, MEMN, MEMN, MEMN, 1>(n, n, 1, op_mem(G, L.ldG), op_mem(G, L.ldG), Pg, op_mem(G, L.ldG),
-                                         op_mem(G, L.ldG), 0, ci_cov(pts, pts, tp.tau2), -1.0, S, L.ldS, cp,
+                                         op_mem(G, L.ldG), 0, ci_cov(pts, pts, tau2_of(tp)), -1.0, S, L.ldS, cp,
                                          smem);
         chol_blocked(S, n, L.ldS, D, cp, smem);
         if (*f.bad && threadIdx.x == 0) set_err(tp.err, M, l);
@@ -340,7 +340,7 @@ k_smooth(TreeParams tp, const double* muhat, const long long* perm, double* smoo
             }
             __syncthreads();
         }
-        for (int i = threadIdx.x; i < n; i += NT) smooth[perm[o0 + i]] = tp.zs[o0 + i] - tp.tau2 * r[i];
+        for (int i = threadIdx.x; i < n; i += NT) smooth[perm[o0 + i]] = tp.zs[o0 + i] - tau2_of(tp) * r[i];
     }
 }
 
@@ -357,7 +357,7 @@ k_smooth(TreeParams tp, const double* muhat, const long long* perm, double* smoo
 __global__ void __launch_bounds__(NT, MRA_MINB)
 k_predict(TreeParams tp, PredParams pp, double* ws, WsLayout L, unsigned long long* counter) {
     double* smem = dyn_smem();
-    const CovP cp = to_covp(tp.cp);
+    const CovP cp = covp_of(tp);
     const int M = tp.M, J = tp.J, rh = tp.rh, m = M - 1, Pg = m * rh, ncol = Pg + 1;
     double* base = ws + (long long)blockIdx.x * L.stride;
     double *G = base + L.oG, *S = base + L.oS, *D = base + L.oD, *r = base + L.oV, *Q = base + L.oQ,
@@ -382,7 +382,7 @@ k_predict(TreeParams tp, PredParams pp, double* ws, WsLayout L, unsigned long lo
             for (int i = threadIdx.x; i < n; i += NT) G[(long long)i * L.ldG + Pg] = tp.zs[o0 + i];
             __syncthreads();
             cta_gemm<MEMN, MEMN, MEMN, MEMN, 1>(n, n, 1, op_mem(G, L.ldG), op_mem(G, L.ldG), Pg, op_mem(G, L.ldG),
-                                             op_mem(G, L.ldG), 0, ci_cov(pts, pts, tp.tau2), -1.0, S, L.ldS, cp,
+                                             op_mem(G, L.ldG), 0, ci_cov(pts, pts, tau2_of(tp)), -1.0, S, L.ldS, cp,
                                              smem);
             chol_blocked(S, n, L.ldS, D, cp, smem);
             if (*f.bad && threadIdx.x == 0) set_err(tp.err, M, l);
@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(CFT)
 k_wide_covfill(TreeParams tp, WideParams wp, const int4* tasks, long long ntask) {
     __shared__ double2 pts_s[64];
     __shared__ double2 knots_s[MAXM * 64];
-    const CovP cp = to_covp(tp.cp);
+    const CovP cp = covp_of(tp);
     const int rh = tp.rh, m = tp.M - 1, Pg = m * rh;
     for (long long it = blockIdx.x; it < ntask; it += gridDim.x) {
         const int4 tk = tasks[it];
@@ -579,6 +579,8 @@ static const DevAttrs& set_attrs() {
     A.done = true;
     return A;
 }
+void init_kernel_attrs_main() { set_attrs(); }
+
 // persistent grid: never more CTAs than can be resident at once (they pull work from a queue)
 static int clamp_grid(int grid, long long items, int kidx) {
     const int res = set_attrs().resident[kidx];

@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(NT, MRA_MINB)
 k_wide_chain(TreeParams tp, TREG, WideParams wp, const int4* tasks, long long ntask, unsigned long long* counter) {
     double* smem = dyn_smem();
     ENGINE_INIT(smem);
-    const CovP cp = to_covp(tp.cp);
+    const CovP cp = covp_of(tp);
     const int m = tp.M - 1;
     for (;;) {
         const long long it = next_item(counter, smem);
@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(NT, MRA_MINB)
 k_wide_sigma(TreeParams tp, TREG, WideParams wp, const int4* tasks, long long ntask, unsigned long long* counter) {
     double* smem = dyn_smem();
     ENGINE_INIT(smem);
-    const CovP cp = to_covp(tp.cp);
+    const CovP cp = covp_of(tp);
     const int Pg = (tp.M - 1) * tp.rh;
     for (;;) {
         const long long it = next_item(counter, smem);
@@ -104,7 +104,7 @@ k_wide_sigma(TreeParams tp, TREG, WideParams wp, const int4* tasks, long long nt
         cta_gemm<MEMN, MEMN, MEMN, MEMN, 1>(min(64, n - 64 * i), min(64, n - 64 * k), i == k, op_mem(Gi, wp.ldG),
                                          op_mem(Gk, wp.ldG), Pg, op_mem(Gi, 0), op_mem(Gi, 0), 0,
                                          ci_cov(tp.pxy + 2 * (o + 64LL * i), tp.pxy + 2 * (o + 64LL * k),
-                                                i == k ? tp.tau2 : 0.0),
+                                                i == k ? tau2_of(tp) : 0.0),
                                          -1.0, C, ld, cp, smem);
     }
 }
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(NT, MRA_MINB)
 k_wide_update(TreeParams tp, TREG, WideParams wp, int s, const int4* tasks, long long ntask, unsigned long long* counter) {
     double* smem = dyn_smem();
     ENGINE_INIT_NOREG(smem);
-    const CovP cp = to_covp(tp.cp);
+    const CovP cp = covp_of(tp);
     const int ncol = (tp.M - 1) * tp.rh + 1;
     const int k0 = 64 * wp.kb0, K = 64 * (wp.kb1 - wp.kb0);
     (void)s;
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(NT, MRA_MINB)
 k_wide_panel_x(TreeParams tp, TREG, WideParams wp, int s, const int4* tasks, long long ntask, unsigned long long* counter) {
     double* smem = dyn_smem();
     ENGINE_INIT_NOREG(smem);
-    const CovP cp = to_covp(tp.cp);
+    const CovP cp = covp_of(tp);
     for (;;) {
         const long long it = next_item(counter, smem);
         if (it >= ntask) break;
@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(NT, MRA_MINB)
 k_wide_trsm(TreeParams tp, TREG, WideParams wp, const int4* tasks, long long ntask, unsigned long long* counter) {
     double* smem = dyn_smem();
     ENGINE_INIT_NOREG(smem);
-    const CovP cp = to_covp(tp.cp);
+    const CovP cp = covp_of(tp);
     const int ncol = (tp.M - 1) * tp.rh + 1;
     for (;;) {
         const long long it = next_item(counter, smem);
@@ -339,7 +339,7 @@ k_wide_mtile(TreeParams tp, TREG, WideParams wp, long long g_first, double* out,
              const int4* tasks, long long ntask, unsigned long long* counter, MergeRing ring) {
     double* smem = dyn_smem();
     ENGINE_INIT(smem);
-    const CovP cp = to_covp(tp.cp);
+    const CovP cp = covp_of(tp);
     const int M = tp.M, J = tp.J, m = M - 1, rh = tp.rh, Pg = m * rh;
     const int nr = (q + 63) / 64;
     // when the y row is alone in the last 64-row tile (q = 64 k + 1: r_hat = 64), the tile tasks cover
@@ -593,7 +593,7 @@ k_prior(TreeParams tp, TREG, int m, long long t_first, long long nitems, double*
         unsigned long long* counter) {
     double* smem = dyn_smem();
     ENGINE_INIT(smem);
-    const CovP cp = to_covp(tp.cp);
+    const CovP cp = covp_of(tp);
     const int rh = tp.rh;
     double* W = ws + (long long)blockIdx.x * ws_stride;
     FacSmem f = fac_view(smem);
@@ -631,7 +631,7 @@ k_merge(TreeParams tp, TREG, int m, long long t_first, long long t_count, const 
         int presummed) {
     double* smem = dyn_smem();
     ENGINE_INIT_NOREG(smem);
-    const CovP cp = to_covp(tp.cp);
+    const CovP cp = covp_of(tp);
     const int J = tp.J, rh = tp.rh;
     const int qc = m * rh + 1;
     const int ldA = qc + (qc & 1);   // even leading dimension -> 16-byte cp.async rows
@@ -908,6 +908,12 @@ bool tma_register(TmaReg& reg, int kind, const double* base, long long ld, long 
     reg.kind[reg.n] = kind;
     reg.n++;
     return true;
+}
+
+void init_kernel_attrs_main();   // mra_kernels.cu
+void init_kernel_attrs() {
+    gemm_set_attrs();
+    init_kernel_attrs_main();
 }
 
 // resident CTAs of the merge tile dataflow (the host sizes its look-ahead D1 with it)

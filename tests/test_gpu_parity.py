@@ -390,3 +390,30 @@ def test_axis_scaled_distance(mra, xs, ys, J, cov):
         ref = oracle.run(x, y, z, 4, J, 16, theta, xscale=xs, yscale=ys, regions=True, posterior=True)
         _cmp(got, ref)
         p.close()
+
+
+def test_graph_replay_equals_direct_launches(mra):
+    """opts.graph: the evaluation captured once as a CUDA graph and replayed with theta read from device memory gives
+    bitwise the direct launches' log L for several thetas of a family, re-captures for another family / y buffer,
+    and posterior requests fall back to direct launches."""
+    import torch
+    x, y, z = synth.uniform_small(6000, seed=91, clusters=2)
+    zd = torch.from_numpy(z).cuda()
+    zd2 = zd.clone()
+    pg = mra.mra_plan_create(x, y, 5, 4, 16, graph=True, stream=torch.cuda.current_stream())
+    pd = mra.mra_plan_create(x, y, 5, 4, 16, stream=torch.cuda.current_stream())
+    for th in [(EXP, 1.0, 0.1, 0.05), (EXP, 1.7, 0.05, 0.2), (MAT, 1.2, 0.2, 0.03), (EXP, 0.8, 0.3, 0.01)]:
+        for y_dev in (zd, zd2):
+            a = mra.mra_loglik_dev(pg, y_dev, th, regions=True)
+            b = mra.mra_loglik_dev(pd, y_dev, th, regions=True)
+            assert a["loglik"] == b["loglik"], th
+            assert np.array_equal(a["region_d"], b["region_d"]) and np.array_equal(a["region_u"], b["region_u"])
+            assert mra.mra_last_launches(pg) == mra.mra_last_launches(pd)
+    ref = oracle.run(x, y, z, 5, 4, 16, (EXP, 0.8, 0.3, 0.01))["loglik"]
+    assert abs(a["loglik"] - ref) <= 1e-9 * abs(ref)
+    post = mra.mra_loglik_dev(pg, zd, (EXP, 1.0, 0.1, 0.05), posterior=True)
+    postd = mra.mra_loglik_dev(pd, zd, (EXP, 1.0, 0.1, 0.05), posterior=True)
+    assert torch.equal(post["smooth"], postd["smooth"])
+    with pytest.raises(mra.MraError) as e:      # a failing Cholesky inside a replay is still reported
+        mra.mra_loglik_dev(pg, zd, (EXP, 1.0, 0.1, -1.0))
+    assert e.value.status == 1
