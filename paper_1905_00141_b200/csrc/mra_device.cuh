@@ -266,27 +266,27 @@ __device__ __forceinline__ double frag(const double* s, int row, int k) {
 // output tile (WM == WN): the 8 x 8 blocks strictly above the diagonal are not needed (the epilogue never stores
 // them), so their DMMAs are not issued -- the SM's fp64 pipe is shared by the co-resident CTAs, which get that
 // time. (Compiled into every instantiation, the branch slowed the others by a few % through code size.)
-template <int KA, int KB, bool MASK = false, int LAY = 0, bool TRI = false>
-__device__ __forceinline__ void mma_ktile(double (&acc)[MI][4][2], const double* As, const double* Bs, int nk,
-                                          bool tri = false) {
+template <int KA, int KB, bool MASK, int LAY, bool TRI, int MV>
+__device__ __forceinline__ void mma_ktile_v(double (&acc)[MI][4][2], const double* As, const double* Bs, int nk,
+                                            bool tri) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
     const int wr = (warp / (64 / WN)) * WM, wc = (warp % (64 / WN)) * WN;
     auto step = [&](int kk) {
-        double a[MI], b[4];
+        double a[MV], b[4];
 #pragma unroll
-        for (int mi = 0; mi < MI; mi++) a[mi] = frag<KA, LAY>(As, wr + mi * 8 + g, kk + t);
+        for (int mi = 0; mi < MV; mi++) a[mi] = frag<KA, LAY>(As, wr + mi * 8 + g, kk + t);
 #pragma unroll
         for (int ni = 0; ni < 4; ni++) b[ni] = frag<KB, LAY>(Bs, wc + ni * 8 + g, kk + t);
         if (TRI && WM == WN && tri) {
 #pragma unroll
-            for (int mi = 0; mi < MI; mi++)
+            for (int mi = 0; mi < MV; mi++)
 #pragma unroll
                 for (int ni = 0; ni < 4; ni++)
                     if (ni <= mi) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
         } else {
 #pragma unroll
-            for (int mi = 0; mi < MI; mi++)
+            for (int mi = 0; mi < MV; mi++)
 #pragma unroll
                 for (int ni = 0; ni < 4; ni++) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
         }
@@ -301,19 +301,41 @@ __device__ __forceinline__ void mma_ktile(double (&acc)[MI][4][2], const double*
         const int nk4 = (nk + 3) & ~3;
         for (int kk = 0; kk < nk4; kk += 4) {
             const bool kin = kk + t < nk;
-            double a[MI], b[4];
+            double a[MV], b[4];
 #pragma unroll
-            for (int mi = 0; mi < MI; mi++) a[mi] = kin ? frag<KA, LAY>(As, wr + mi * 8 + g, kk + t) : 0.0;
+            for (int mi = 0; mi < MV; mi++) a[mi] = kin ? frag<KA, LAY>(As, wr + mi * 8 + g, kk + t) : 0.0;
 #pragma unroll
             for (int ni = 0; ni < 4; ni++) b[ni] = kin ? frag<KB, LAY>(Bs, wc + ni * 8 + g, kk + t) : 0.0;
 #pragma unroll
-            for (int mi = 0; mi < MI; mi++)
+            for (int mi = 0; mi < MV; mi++)
 #pragma unroll
                 for (int ni = 0; ni < 4; ni++)
                     if (!(TRI && WM == WN && tri) || ni <= mi) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
         }
     }
 }
+
+// act (cta_gemm_impl): bits 0-1 active / on the diagonal of a lower tile, bits 2-4 how many of the warp's 8-row
+// blocks hold wanted rows. RAG: a warp whose wanted rows (a ragged last row tile) lie in the first half of its row
+// blocks runs a second unrolled body without the other half's DMMAs (a branch: predicated-off DMMAs still occupy
+// the pipe; one extra body, not one per count, to keep the code instruction-cache resident)
+template <int KA, int KB, bool MASK = false, int LAY = 0, bool TRI = false, bool RAG = false>
+__device__ __forceinline__ void mma_ktile(double (&acc)[MI][4][2], const double* As, const double* Bs, int nk,
+                                          int act) {
+    const bool tri = (act & 3) == 2;
+    if constexpr (RAG) {
+        if (2 * ((act >> 2) & 7) <= MI && !(TRI && tri)) {
+            mma_ktile_v<KA, KB, MASK, LAY, false, MI / 2>(acc, As, Bs, nk, false);
+            return;
+        }
+    }
+    mma_ktile_v<KA, KB, MASK, LAY, TRI, MI>(acc, As, Bs, nk, tri);
+}
+
+// the ragged-row body where it pays: not in the merge-tile GEMMs (G^T G and -F F^T: their rows are whole tiles
+// but for the one y row, and the extra body cost mtile 2 %)
+template <int KA0, int KB0, int KA1, int KB1>
+__host__ __device__ constexpr bool rag_of() { return !(KA0 == MEMT && KB0 == MEMT && KA1 == MEMN && KB1 == MEMN); }
 
 // GEMM call descriptor: written to shared memory by the (inlined) caller, read by the single
 // non-inlined implementation per operand-kind combination (keeps the kernels' SASS small enough
@@ -469,11 +491,11 @@ __device__ __forceinline__ void tile_pipeline(double (&acc)[MI][4][2], const Gem
         }
         cp_async_commit();
         if (kt < 0) continue;
-        if (!wact) continue;   // this warp's 16 x 32 sub-tile holds no wanted output (it still loads)
+        if (!(wact & 3)) continue;   // this warp's sub-tile holds no wanted output (it still loads)
         const double* As = smem + (kt % NSTAGE) * STAGE_DBL;
         const double* Bs = As + TILE_DBL;
-        if (kt < T0) mma_ktile<KA0, KB0, false, 0, TRI>(acc, As, Bs, min(TK, K0 - kt * TK), wact == 2);
-        else mma_ktile<KA1, KB1, false, 0, TRI>(acc, As, Bs, min(TK, K1 - (kt - T0) * TK), wact == 2);
+        if (kt < T0) mma_ktile<KA0, KB0, false, 0, TRI, rag_of<KA0, KB0, KA1, KB1>()>(acc, As, Bs, min(TK, K0 - kt * TK), wact);
+        else mma_ktile<KA1, KB1, false, 0, TRI, rag_of<KA0, KB0, KA1, KB1>()>(acc, As, Bs, min(TK, K1 - (kt - T0) * TK), wact);
     }
     cp_async_wait<0>();
 }
@@ -508,11 +530,11 @@ __device__ __forceinline__ void tile_pipeline_bulk(double (&acc)[MI][4][2], cons
         if (warp == 0 && kt + NSTAGE - 1 < T) issue(kt + NSTAGE - 1);
         const unsigned sidx = gs + kt, b = sidx % NSTAGE;
         mbar_wait(&bs->full[b], (sidx / NSTAGE) & 1);
-        if (wact) {
+        if (wact & 3) {
             const double* As = smem + b * STAGE_DBL;
             const double* Bs = As + TILE_DBL;
-            if (kt < T0) mma_ktile<KA0, KB0, true, 0, TRI>(acc, As, Bs, min(TK, K0 - kt * TK), wact == 2);
-            else mma_ktile<KA1, KB1, true, 0, TRI>(acc, As, Bs, min(TK, K1 - (kt - T0) * TK), wact == 2);
+            if (kt < T0) mma_ktile<KA0, KB0, true, 0, TRI, rag_of<KA0, KB0, KA1, KB1>()>(acc, As, Bs, min(TK, K0 - kt * TK), wact);
+            else mma_ktile<KA1, KB1, true, 0, TRI, rag_of<KA0, KB0, KA1, KB1>()>(acc, As, Bs, min(TK, K1 - (kt - T0) * TK), wact);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&bs->empty[b]);
@@ -550,11 +572,11 @@ __device__ __forceinline__ void tile_pipeline_tma(double (&acc)[MI][4][2], const
         __syncwarp();
         const unsigned sidx = gs + kt, b = sidx % NSTAGE;
         mbar_wait(&bs->full[b], (sidx / NSTAGE) & 1);
-        if (wact) {
+        if (wact & 3) {
             const double* As = smem + b * STAGE_DBL;
             const double* Bs = As + TILE_DBL;
-            if (kt < T0) mma_ktile<KA0, KB0, true, 1, TRI>(acc, As, Bs, min(TK, K0 - kt * TK), wact == 2);
-            else mma_ktile<KA1, KB1, true, 1, TRI>(acc, As, Bs, min(TK, K1 - (kt - T0) * TK), wact == 2);
+            if (kt < T0) mma_ktile<KA0, KB0, true, 1, TRI, rag_of<KA0, KB0, KA1, KB1>()>(acc, As, Bs, min(TK, K0 - kt * TK), wact);
+            else mma_ktile<KA1, KB1, true, 1, TRI, rag_of<KA0, KB0, KA1, KB1>()>(acc, As, Bs, min(TK, K1 - (kt - T0) * TK), wact);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&bs->empty[b]);
@@ -601,8 +623,9 @@ __device__ __noinline__ void cta_gemm_impl(double* smem) {
             // warps whose sub-tile lies outside a ragged tile (e.g. the 1-row y tile) or strictly above the
             // diagonal of a lower-triangular tile skip their DMMAs
             // 0: the warp's sub-tile holds no wanted output; 1: active; 2: active on the diagonal of a lower tile
+            // (bits 2-4: how many of its 8-row blocks hold wanted rows, mma_ktile)
             const int wact = (wr < nr && wc < nc && !(lower && tm == tn && wc > wr + WM - 1))
-                                 ? ((WM == WN && lower && tm == tn && wr == wc) ? 2 : 1)
+                                 ? ((WM == WN && lower && tm == tn && wr == wc) ? 2 : 1) | (min(MI, (nr - wr + 7) >> 3) << 2)
                                  : 0;
 #ifdef MRA_BULK
             if (MODE == 1) {
