@@ -763,14 +763,17 @@ __device__ __forceinline__ void cta_gemm(int Mr, int Nc, int lower, const Op& A0
 // tmp: >= 3*256 doubles of smem scratch. Returns log|A| (all threads); *bad set if not PD.
 #ifdef MRA_CHOL_DEBUG
 __device__ long long g_chol_dbg[16];
-#define CHK(k) do { if (threadIdx.x == 0 && blockIdx.x == 0) g_chol_dbg[k] += clock64(); } while (0)
+// phase k accumulates the cycles since the previous CHK (thread 0 of CTA 0)
+#define CHK(k) do { const long long _t = clock64(); if (threadIdx.x == 0 && blockIdx.x == 0) g_chol_dbg[k] += _t - chk_last; chk_last = _t; } while (0)
+#define CHK_START long long chk_last = clock64()
 #else
 #define CHK(k)
+#define CHK_START
 #endif
 __device__ __noinline__ double chol_inv_small(double* a, double* x, int n, double* diagv, int* bad, double* red,
                                               double* tmp) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    CHK(0);
+    CHK_START;
     const int nbk = (n + 15) >> 4;
     const bool inplace = (x == a);
     for (int e = tid; e < 64 * 64; e += NT) {
@@ -821,6 +824,7 @@ __device__ __noinline__ double chol_inv_small(double* a, double* x, int n, doubl
                 }
             }
             __syncwarp();
+            CHK(6);
             if (!ok && lane == 0) *bad = 1;
             // publish L_bb rows to smem (lower part) for the inverse and the panel
             if (lane < nb) {
@@ -858,6 +862,54 @@ __device__ __noinline__ double chol_inv_small(double* a, double* x, int n, doubl
         CHK(3);
         const int r0 = j0 + nb, nr = n - r0;
         if (nr > 0) {
+#ifndef MRA_CHOL_SCALAR
+            // panel L_ib = A_ib X_bb^T (rows r0..n-1, <= 48; the nb columns of block b) and trailing update
+            // A_rc -= L_rb L_cb^T (lower part) as 8 x 8 DMMA tiles (m8n8k4, K = 16 masked to nb), warp-strided
+            {
+                const int g = lane >> 2, t = lane & 3, nw = NT / 32;
+                const int rb = (nr + 7) >> 3, cbn = (nb + 7) >> 3;
+                // the panel tiles go to the scratch first (every operand is read before A_ib is overwritten)
+                for (int tsk = warp; tsk < rb * cbn; tsk += nw) {
+                    const int m = tsk / cbn, cc = tsk % cbn;
+                    double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+                    for (int k0 = 0; k0 < 16; k0 += 4) {
+                        const int k = k0 + t;
+                        const double av = k < nb ? a[(r0 + 8 * m + g) * LDB + j0 + k] : 0.0;
+                        const double bv = (k < nb && 8 * cc + g < nb) ? x[(j0 + 8 * cc + g) * LDB + j0 + k] : 0.0;
+                        dmma(d0, d1, av, bv);
+                    }
+                    double* pt = tmp + (8 * m + g) * 16 + 8 * cc + 2 * t;
+                    pt[0] = d0;
+                    pt[1] = d1;
+                }
+                __syncthreads();
+                for (int e = tid; e < nr * 16; e += NT) {
+                    const int rr = e >> 4, c = e & 15;
+                    if (c < nb) a[(r0 + rr) * LDB + j0 + c] = tmp[e];
+                }
+                __syncthreads();
+                CHK(7);
+                for (int tsk = warp; tsk < rb * (rb + 1) / 2; tsk += nw) {
+                    int m = 0;
+                    while ((m + 1) * (m + 2) / 2 <= tsk) m++;
+                    const int cc = tsk - m * (m + 1) / 2;
+                    double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+                    for (int k0 = 0; k0 < 16; k0 += 4) {
+                        const int k = k0 + t;
+                        const double av = k < nb ? a[(r0 + 8 * m + g) * LDB + j0 + k] : 0.0;
+                        const double bv = k < nb ? a[(r0 + 8 * cc + g) * LDB + j0 + k] : 0.0;
+                        dmma(d0, d1, av, bv);
+                    }
+                    const int row = r0 + 8 * m + g, col = r0 + 8 * cc + 2 * t;
+                    if (row < n) {
+                        if (col <= row) a[row * LDB + col] -= d0;
+                        if (col + 1 <= row) a[row * LDB + col + 1] -= d1;
+                    }
+                }
+            }
+#else
             // panel: L_ib = A_ib X_bb^T for rows r0..n-1 (<= 48), cols j0..j0+nb-1; thread = (row group, col)
             constexpr int RG = NT / 16, NQ = (48 + RG - 1) / RG;   // row groups per pass, passes over <= 48 rows
             const int jj = tid & 15, rg = tid >> 4;
@@ -884,6 +936,7 @@ __device__ __noinline__ double chol_inv_small(double* a, double* x, int n, doubl
                 if (row < n && jj < nb) a[row * LDB + j0 + jj] = v[q];
             }
             __syncthreads();
+            CHK(7);
             // trailing update A_rc -= sum_k L_rk L_ck (lower part), thread = (row offset, col offset) 16 x 16
             const int tx = tid & 15, ty = tid >> 4;
 #pragma unroll
@@ -908,9 +961,49 @@ __device__ __noinline__ double chol_inv_small(double* a, double* x, int n, doubl
                     a[row * LDB + col] -= s0 + s1;
                 }
             }
+#endif
+            __syncthreads();
+            CHK(8);
+        }
+    }
+    // off-diagonal blocks of X = L^{-1}, block row by block row: X_ij = -X_ii sum_{k=j}^{i-1} L_ik X_kj, as 8 x 8
+    // DMMA tiles: Y_j = L_{i,j..i-1} X_{j..i-1,j} (K = 16 (i - j)) into the scratch, then X_ij = -X_ii Y_j (K = 16)
+#ifndef MRA_CHOL_SCALAR
+    {
+        const int g = lane >> 2, t = lane & 3, nw = NT / 32;
+        for (int bi = 1; bi < nbk; bi++) {
+            const int i0 = bi * 16, ni = min(16, n - i0);
+            for (int tsk = warp; tsk < 4 * bi; tsk += nw) {
+                const int bj = tsk >> 2, mr = (tsk >> 1) & 1, mc = tsk & 1;
+                double d0 = 0.0, d1 = 0.0;
+                const double* lr = a + (i0 + 8 * mr + g) * LDB;
+                const double* xc = x + 16 * bj + 8 * mc + g;
+                for (int k0 = 16 * bj; k0 < i0; k0 += 4) dmma(d0, d1, lr[k0 + t], xc[(k0 + t) * LDB]);
+                double* y = tmp + (bj << 8) + (8 * mr + g) * 16 + 8 * mc + 2 * t;
+                y[0] = d0;
+                y[1] = d1;
+            }
+            __syncthreads();
+            for (int tsk = warp; tsk < 4 * bi; tsk += nw) {
+                const int bj = tsk >> 2, mr = (tsk >> 1) & 1, mc = tsk & 1;
+                double d0 = 0.0, d1 = 0.0;
+                const double* xr = x + (i0 + 8 * mr + g) * LDB + i0;
+                const double* yc = tmp + (bj << 8) + 8 * mc + g;
+#pragma unroll
+                for (int k0 = 0; k0 < 16; k0 += 4) {
+                    const int k = k0 + t;
+                    dmma(d0, d1, k < ni ? xr[k] : 0.0, k < ni ? yc[k * 16] : 0.0);
+                }
+                const int rr = 8 * mr + g, c = 16 * bj + 8 * mc + 2 * t;
+                if (rr < ni) {
+                    x[(i0 + rr) * LDB + c] = -d0;
+                    x[(i0 + rr) * LDB + c + 1] = -d1;
+                }
+            }
             __syncthreads();
         }
     }
+#else
     // off-diagonal blocks of X = L^{-1}, block row by block row: X_ij = -X_ii sum_{k=j}^{i-1} L_ik X_kj
     for (int bi = 1; bi < nbk; bi++) {
         const int i0 = bi * 16, ni = min(16, n - i0);
@@ -941,6 +1034,7 @@ __device__ __noinline__ double chol_inv_small(double* a, double* x, int n, doubl
         }
         __syncthreads();
     }
+#endif
     CHK(4);
     // log-determinant: the n diagonal logs in parallel (warp 0), then a shuffle reduction
     if (tid < 32) {
