@@ -190,3 +190,19 @@ def test_shard_size_is_packed_lower_triangles():
     s = mra.mra_plan_shards(p)["shard_level"]
     ns, q = w.J ** (s - 1), (s - 1) * p.r_hat + 1
     assert mra.mra_shard_size(p) == ns * q * (q + 1) // 2 + 2 * ns + 1
+
+
+def test_shard_assignment_contiguous_on_uniform_data():
+    """Uniform leaves (C3 recipe): every rank's subtrees form ONE contiguous run (the smallest-max-load
+    contiguous split is within 3 % of LPT there), the runs cover the shard level in rank order."""
+    w = synth.make("C3", n=200_000)
+    world = 8
+    prev_end = 0
+    for rank in range(world):
+        p = mra.mra_plan_create(w.x, w.y, w.M, w.J, w.r, device=-2, rank=rank, world=world)
+        own = mra.mra_plan_shards(p)["own"]
+        assert len(own) > 0
+        np.testing.assert_array_equal(own, np.arange(own[0], own[0] + len(own)))
+        assert own[0] == prev_end
+        prev_end = own[-1] + 1
+    assert prev_end == w.J ** (mra.mra_plan_shards(p)["shard_level"] - 1)
