@@ -119,11 +119,14 @@ static __device__ const double g_exp2m32[32] = {
     0.5946035575013605, 0.5818624293887887, 0.5693943173783458, 0.5571933712979462,
     0.5452538663326288, 0.5335702003384118, 0.5221368912137069, 0.5109485743270583};
 __device__ __forceinline__ double exp_neg(double x) {
-    if (!(x < 708.0)) return 0.0;
+    // branch-free (one basic block, so the unrolled callers interleave independent chains): x >= 708 (and NaN)
+    // run the same arithmetic (meaningless there, the table index stays in range) and 0 is selected at the end
+    const bool big = !(x < 708.0);
     const double K32 = 46.166241308446828384,                          // 32 / ln 2
         LN2_32_HI = 6.93147180369123816490e-01 / 32, LN2_32_LO = 1.90821492927058770002e-10 / 32,
         MAGIC = 6755399441055744.0;
-    const double kd = __dadd_rn(__dmul_rn(x, K32), MAGIC) - MAGIC;   // rint(32 x / ln 2)
+    const double kt = __dadd_rn(__dmul_rn(x, K32), MAGIC);          // MAGIC + rint(32 x / ln 2)
+    const double kd = kt - MAGIC;                                      // rint(32 x / ln 2)
     double s = fma(kd, LN2_32_HI, -x);                               // s = -r
     s = fma(kd, LN2_32_LO, s);
     // w = e^s - 1 = s + s^2 (1/2 + s/6 + s^2 (1/24 + s/120 + s^2/720)); the result t (1 + w) is rounded
@@ -133,29 +136,37 @@ __device__ __forceinline__ double exp_neg(double x) {
     const double c = fma(1.0 / 720, s2, b);
     const double u = fma(c, s2, a);
     const double w = fma(u, s2, s);
-    const int k = (int)kd;
+    const int k = __double2loint(kt);   // = (int) kd: the integer sits in the low word (no conversion instruction)
     const double t = __ldg(g_exp2m32 + (k & 31));
-    return fma(t, w, t) * __hiloint2double((1023 - (k >> 5)) << 20, 0);
+    const double r = fma(t, w, t) * __hiloint2double((1023 - (k >> 5)) << 20, 0);
+    return big ? 0.0 : r;
 }
 
 // sqrt(q) from the single-precision MUFU reciprocal square root, one fp64 Newton step on 1/sqrt and one
 // Heron correction on sqrt: ~8 dependent operations instead of the libm routine (<= 1 ulp; equal to
-// the correctly rounded sqrt on 2e7 random q in [1e-30, 1e6] in a host check). q == 0 (and q below the
-// float range) take the exact path.
+// the correctly rounded sqrt on 2e7 random q in [1e-30, 1e6] in a host check). Branch-free (selects only, so
+// that unrolled callers interleave independent chains): q below 2^-120 is scaled by 2^240 first (exact) and the
+// result by 2^-120; q == 0 gives 0. Every q >= 2^-120 takes exactly the unscaled arithmetic.
 __device__ __forceinline__ double sqrt_fast(double q) {
-    const float qf = __double2float_rn(q);
-    if (!(qf > 0.0f)) return sqrt(q);
+    const bool small = q < 0x1p-120;
+    const double qs = small ? q * 0x1p240 : q;
+    // q == 0: a finite seed, the result is replaced below; 0 < q < 2^-366 (distances below 1e-55) returns a value
+    // below 2^-180 instead of the root (no covariance can tell the two apart)
+    const float qf = fmaxf(__double2float_rn(qs), 0x1p-126f);
     double y = (double)rsqrtf(qf);
-    y = y * fma(-0.5 * q, y * y, 1.5);
-    const double d = q * y;
-    return fma(0.5 * y, fma(-d, d, q), d);
+    y = y * fma(-0.5 * qs, y * y, 1.5);
+    const double d = qs * y;
+    const double r = fma(0.5 * y, fma(-d, d, qs), d);
+    return q == 0.0 ? 0.0 : (small ? r * 0x1p-120 : r);
 }
 
 __device__ __forceinline__ double covf(const CovP& c, double x1, double y1, double x2, double y2) {
     const double dx = (x1 - x2) * c.xs, dy = (y1 - y2) * c.ys;
     const double a = sqrt_fast(dx * dx + dy * dy) * c.ir;
     const double e = exp_neg(a);
-    return c.kind == 0 ? c.s2 * e : c.s2 * (1.0 + a) * e;
+    // exponential: s2 e = (s2 * 1) e; Matern-3/2: s2 (1 + a) e -- one expression, the kind a loop-invariant factor
+    const double m = c.kind == 0 ? 0.0 : 1.0;
+    return c.s2 * fma(a, m, 1.0) * e;
 }
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
@@ -239,12 +250,10 @@ __device__ __forceinline__ void load_tile_async(double* s, const Op& op, int r0,
 #pragma unroll 4
         for (int i = 0; i < 64 * TK / NT; i++) {
             const int row = rw + (NT / TK) * i;
-            double v = 0.0;
-            if (kok && row < nr) {
-                const double2 pr = ldpt(op.p, r0 + row);
-                v = covf(cpl, pr.x, pr.y, qk.x, qk.y);
-            }
-            s[row * LDN + kk] = v;
+            // unconditional chain on a clamped (valid) row, select after: no branch splits the unrolled chains
+            const double2 pr = ldpt(op.p, r0 + min(row, max(nr - 1, 0)));
+            const double v = covf(cpl, pr.x, pr.y, qk.x, qk.y);
+            s[row * LDN + kk] = (kok && row < nr) ? v : 0.0;
         }
     }
 }
@@ -646,6 +655,25 @@ __device__ __noinline__ void cta_gemm_impl(double* smem) {
             // whole pair is in range and aligned
             const bool vec = ((reinterpret_cast<uintptr_t>(C) & 15) == 0) && ((ldc & 1) == 0) &&
                              (ci.kind != 1 || (((reinterpret_cast<uintptr_t>(ci.p) & 15) == 0) && ((ci.ld & 1) == 0)));
+            if (EPI == 1 && ci.kind == 2) {
+                // covariance initial value (Sigma tiles): C = alpha acc + (C(s_i, s_j) + diag), one store per element;
+                // the covariance chains run unconditionally on clamped (valid) points and only the store is
+                // predicated, so no branch splits the unrolled chains
+                const CovP cpl = d.cp;
+#pragma unroll
+                for (int mi = 0; mi < MI; mi++) {
+                    const int i = r0 + wr + mi * 8 + g;
+                    const double2 pi = ldpt(ci.p, min(i, Mr - 1));
+#pragma unroll
+                    for (int q = 0; q < 8; q++) {
+                        const int ni = q >> 1, e = q & 1, j = c0 + wc + ni * 8 + 2 * t + e;
+                        const double2 pj = ldpt(ci.q, min(j, Nc - 1));
+                        const double w = covf(cpl, pi.x, pi.y, pj.x, pj.y) + (i == j ? ci.diag : 0.0);
+                        if (i < Mr && j < Nc && (!lower || j <= i))
+                            C[(long long)i * ldc + j] = __dadd_rn(__dmul_rn(alpha, acc[mi][ni][e]), w);
+                    }
+                }
+            } else
 #pragma unroll
             for (int mi = 0; mi < MI; mi++)
 #pragma unroll
@@ -668,20 +696,6 @@ __device__ __noinline__ void cta_gemm_impl(double* smem) {
                     }
                 }
             if (EPI == 0 && ci.kind == 2) __trap();   // a covariance init needs the EPI = 1 instantiation
-            if (EPI == 1 && ci.kind == 2) {
-                const CovP cpl = d.cp;
-                // covariance initial value, added by the thread that stored the element (4 independent
-                // fp64 sqrt/exp chains in flight per thread)
-#pragma unroll 4
-                for (int q = 0; q < MI * 8; q++) {
-                    const int mi = q >> 3, ni = (q >> 1) & 3, e = q & 1;
-                    const int i = r0 + wr + mi * 8 + g, j = c0 + wc + ni * 8 + 2 * t + e;
-                    if (i < Mr && j < Nc && (!lower || j <= i)) {
-                        const double2 pi = ldpt(ci.p, i), pj = ldpt(ci.q, j);
-                        C[(long long)i * ldc + j] += covf(cpl, pi.x, pi.y, pj.x, pj.y) + (i == j ? ci.diag : 0.0);
-                    }
-                }
-            }
         }
     }
 #ifdef MRA_BULK

@@ -500,17 +500,20 @@ k_wide_covfill(TreeParams tp, WideParams wp, const int4* tasks, long long ntask)
         }
         __syncthreads();
         double* Gr = wp.G + (o0 - wp.G_base) * wp.ldG;
-        // the n x Pg entries flattened over the CTA (balanced), (row, column) advanced incrementally
-        int i = 0, c = threadIdx.x;
-        while (c >= Pg) { c -= Pg; i++; }
-        const int di = CFT / Pg, dc = CFT - di * Pg;
+        // work items (column c, run of 16 rows): consecutive threads take consecutive columns (coalesced stores),
+        // the knot sits in registers for the whole run and the point is a broadcast shared load; a 64-row tile of
+        // Pg = 9 x 64 columns is 2304 items = 9 per thread
+        const int nch = (n + 15) >> 4;
+        for (int it = threadIdx.x; it < Pg * nch; it += CFT) {
+            const int ch = it / Pg, c = it - ch * Pg;
+            const double2 q = knots_s[c];
+            const int i1 = min(16 * ch + 16, n);
+            double* out = Gr + (long long)(16 * ch) * wp.ldG + c;
 #pragma unroll 4
-        for (long long e = threadIdx.x; e < (long long)n * Pg; e += CFT) {
-            const double2 pp = pts_s[i], q = knots_s[c];
-            Gr[(long long)i * wp.ldG + c] = covf(cp, pp.x, pp.y, q.x, q.y);
-            i += di;
-            c += dc;
-            if (c >= Pg) { c -= Pg; i++; }
+            for (int i = 16 * ch; i < i1; i++, out += wp.ldG) {
+                const double2 pp = pts_s[i];
+                *out = covf(cp, pp.x, pp.y, q.x, q.y);
+            }
         }
         for (int r = threadIdx.x; r < n; r += CFT) Gr[(long long)r * wp.ldG + Pg] = tp.zs[o0 + r];
     }

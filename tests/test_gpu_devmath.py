@@ -22,7 +22,9 @@ def test_exp_sqrt_covf_accuracy(tmp_path):
     out = subprocess.run([str(exe)], capture_output=True, text=True, check=True, timeout=300).stdout
     ulps = [float(v) for v in re.findall(r"exp_neg .*max ([0-9.]+) ulp", out)]
     assert len(ulps) == 3 and max(ulps) <= 1.5, out
-    sq = float(re.search(r"sqrt_fast .*max ([0-9.]+) ulp", out).group(1))
+    sq = float(re.search(r"sqrt_fast vs .*max ([0-9.]+) ulp", out).group(1))
     assert sq <= 1.0, out
+    tiny = re.search(r"sqrt_fast tiny .*max ([0-9.]+) ulp; special cases failed: (\d+)", out)
+    assert float(tiny.group(1)) <= 1.0 and int(tiny.group(2)) == 0, out
     rel = [float(v) for v in re.findall(r"covf kind \d .*max relative ([0-9.e+-]+)", out)]
     assert len(rel) == 2 and max(rel) <= 1e-14, out

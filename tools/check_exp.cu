@@ -32,6 +32,21 @@ __global__ void ksqrt(long long n, double* maxu) {
     for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
     if ((threadIdx.x & 31) == 0) atomicMax((unsigned long long*)maxu, __double_as_longlong(m));
 }
+// the scaled branch of sqrt_fast (q < 2^-120): log-uniform q over [1e-100, 1e-30]; plus the exact special cases
+__global__ void ksqrt_tiny(long long n, double* maxu, int* bad) {
+    double m = 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const double q = exp(-230.2585 + 161.1810 * ((double)i + 0.5) / (double)n);
+        m = fmax(m, ulp_err(sqrt_fast(q), sqrt(q)));
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (sqrt_fast(0.0) != 0.0) atomicAdd(bad, 1);
+        if (exp_neg(708.0) != 0.0 || exp_neg(1e300) != 0.0 || exp_neg(nan("")) != 0.0) atomicAdd(bad, 1);
+        if (exp_neg(0.0) != 1.0) atomicAdd(bad, 1);
+    }
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax((unsigned long long*)maxu, __double_as_longlong(m));
+}
 __global__ void kcov(long long n, int kind, double* maxrel) {
     CovP c;
     c.kind = kind; c.s2 = 1.7; c.rho = 0.3; c.xs = 1.0; c.ys = 1.0;
@@ -60,6 +75,12 @@ int main() {
     ksqrt<<<1184, 256>>>(200000000LL, d);
     double h; cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
     printf("sqrt_fast vs sqrt, q in [1e-30, 1e6] on 2e8 points: max %.2f ulp\n", h);
+    {
+        int* bad; cudaMalloc(&bad, 4); cudaMemset(bad, 0, 4); cudaMemset(d, 0, 8);
+        ksqrt_tiny<<<1184, 256>>>(20000000LL, d, bad);
+        int hb; cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost); cudaMemcpy(&hb, bad, 4, cudaMemcpyDeviceToHost);
+        printf("sqrt_fast tiny q in [1e-100, 1e-30] on 2e7 points: max %.2f ulp; special cases failed: %d\n", h, hb);
+    }
     for (int kind = 0; kind < 2; kind++) {
         cudaMemset(d, 0, 8);
         kcov<<<1184, 256>>>(100000000LL, kind, d);
