@@ -15,6 +15,7 @@
 // tensor path on sm_100a is the warp-level DMMA.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #ifdef MRA_BULK
 #include "mra_internal.h"   // TmaReg
 #endif
@@ -341,6 +342,104 @@ __device__ __forceinline__ void mma_ktile(double (&acc)[MI][4][2], const double*
     mma_ktile_v<KA, KB, MASK, LAY, TRI, MI>(acc, As, Bs, nk, tri);
 }
 
+// MI x 4 DMMAs per k-step of 4 on the warp's WM x 32 sub-tile
+// MASK: the ragged k-tile's fragments with k >= nk are zeroed (the bulk-copy path leaves stale values there; the
+// cp.async path zero-fills, MASK = false)
+// tri (TRI instantiations only: the Sigma tiles, EPI = 1): the warp's sub-tile sits on the diagonal of a lower-triangular
+// output tile (WM == WN): the 8 x 8 blocks strictly above the diagonal are not needed (the epilogue never stores
+// them), so their DMMAs are not issued -- the SM's fp64 pipe is shared by the co-resident CTAs, which get that
+// time. (Compiled into every instantiation, the branch slowed the others by a few % through code size.)
+// NV: 8-column blocks of the warp's sub-tile (4; 2 for the two half-width warps of a balanced diagonal tile); the
+// sub-tile's origin (wr, wc) comes from cta_gemm_impl
+template <int KA, int KB, bool MASK, int LAY, bool TRI, int MV, int NV = 4>
+__device__ __forceinline__ void mma_ktile_vb(double (&acc)[MI][4][2], const double* As, const double* Bs, int nk,
+                                            bool tri, int wr, int wc) {
+    const int lane = threadIdx.x & 31;
+    const int g = lane >> 2, t = lane & 3;
+    auto step = [&](int kk) {
+        double a[MV], b[NV];
+#pragma unroll
+        for (int mi = 0; mi < MV; mi++) a[mi] = frag<KA, LAY>(As, wr + mi * 8 + g, kk + t);
+#pragma unroll
+        for (int ni = 0; ni < NV; ni++) b[ni] = frag<KB, LAY>(Bs, wc + ni * 8 + g, kk + t);
+        if (TRI && WM == WN && tri) {
+#pragma unroll
+            for (int mi = 0; mi < MV; mi++)
+#pragma unroll
+                for (int ni = 0; ni < NV; ni++)
+                    if (ni <= mi) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+        } else {
+#pragma unroll
+            for (int mi = 0; mi < MV; mi++)
+#pragma unroll
+                for (int ni = 0; ni < NV; ni++) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+        }
+    };
+    if (nk == TK) {
+#pragma unroll
+        for (int kk = 0; kk < TK; kk += 4) step(kk);
+    } else if (!MASK) {
+        const int nk4 = (nk + 3) & ~3;
+        for (int kk = 0; kk < nk4; kk += 4) step(kk);
+    } else {
+        const int nk4 = (nk + 3) & ~3;
+        for (int kk = 0; kk < nk4; kk += 4) {
+            const bool kin = kk + t < nk;
+            double a[MV], b[NV];
+#pragma unroll
+            for (int mi = 0; mi < MV; mi++) a[mi] = kin ? frag<KA, LAY>(As, wr + mi * 8 + g, kk + t) : 0.0;
+#pragma unroll
+            for (int ni = 0; ni < NV; ni++) b[ni] = kin ? frag<KB, LAY>(Bs, wc + ni * 8 + g, kk + t) : 0.0;
+#pragma unroll
+            for (int mi = 0; mi < MV; mi++)
+#pragma unroll
+                for (int ni = 0; ni < NV; ni++)
+                    if (!(TRI && WM == WN && tri) || ni <= mi) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+        }
+    }
+}
+
+// act (cta_gemm_impl): bits 0-1 active (1) / on the diagonal of a lower tile (2) / half-width sub-tile of a balanced
+// diagonal tile (3), bits 2-4 how many of the warp's 8-row blocks hold wanted rows, bits 5-7 / 8-10 the sub-tile's
+// row / column origin in 8-blocks. RAG: a warp whose wanted rows (a ragged last row tile) lie in the first half of its row
+// blocks runs a second unrolled body without the other half's DMMAs (a branch: predicated-off DMMAs still occupy
+// the pipe; one extra body, not one per count, to keep the code instruction-cache resident)
+template <int KA, int KB, bool MASK = false, int LAY = 0, bool TRI = false, bool RAG = false>
+__device__ __forceinline__ void mma_ktile_bal(double (&acc)[MI][4][2], const double* As, const double* Bs, int nk,
+                                          int act) {
+    const bool tri = (act & 3) == 2;
+    int wr, wc;
+    if constexpr (TRI && WM == 32 && NWARP == 4) {   // the sub-tile origin travels in act (balanced diagonal tiles)
+        wr = ((act >> 5) & 7) * 8;
+        wc = ((act >> 8) & 7) * 8;
+    } else {
+        const int warp = threadIdx.x >> 5;
+        wr = (warp / (64 / WN)) * WM;
+        wc = (warp % (64 / WN)) * WN;
+    }
+    if constexpr (TRI && WM == 32 && NWARP == 4) {
+        if ((act & 3) == 3) {
+            mma_ktile_vb<KA, KB, MASK, LAY, false, MI, 2>(acc, As, Bs, nk, false, wr, wc);
+            return;
+        }
+    }
+    if constexpr (RAG) {
+        if (2 * ((act >> 2) & 7) <= MI && !(TRI && (act & 3) >= 2)) {
+            mma_ktile_vb<KA, KB, MASK, LAY, false, MI / 2>(acc, As, Bs, nk, false, wr, wc);
+            return;
+        }
+    }
+    mma_ktile_vb<KA, KB, MASK, LAY, TRI, MI>(acc, As, Bs, nk, tri, wr, wc);
+}
+
+// k-tile body: the balanced-diagonal one (sub-tile origin in act) for cta_gemm_impl_bal, the plain one otherwise
+template <bool BALD, int KA, int KB, bool MASK, int LAY, bool TRI, bool RAG>
+__device__ __forceinline__ void mma_ktile_sel(double (&acc)[MI][4][2], const double* As, const double* Bs, int nk,
+                                              int act) {
+    if constexpr (BALD) mma_ktile_bal<KA, KB, MASK, LAY, TRI, RAG>(acc, As, Bs, nk, act);
+    else mma_ktile<KA, KB, MASK, LAY, TRI, RAG>(acc, As, Bs, nk, act);
+}
+
 // the ragged-row body where it pays: not in the merge-tile GEMMs (G^T G and -F F^T: their rows are whole tiles
 // but for the one y row, and the extra body cost mtile 2 %)
 template <int KA0, int KB0, int KA1, int KB1>
@@ -463,7 +562,7 @@ __device__ __forceinline__ void tma_tile(double* dst, const TmaReg* reg, int ti,
 #endif
 
 // accumulate both K-segments of one output tile through an NSTAGE-deep cp.async pipeline
-template <int KA0, int KB0, int KA1, int KB1, bool TRI = false>
+template <int KA0, int KB0, int KA1, int KB1, bool TRI = false, bool BALD = false>
 __device__ __forceinline__ void tile_pipeline(double (&acc)[MI][4][2], const GemmDesc& d, int r0, int nr, int c0,
                                               int nc, double* smem, int wact) {
     // only the current segment's two operand descriptors are held in registers (segment 1's are read
@@ -503,8 +602,8 @@ __device__ __forceinline__ void tile_pipeline(double (&acc)[MI][4][2], const Gem
         if (!(wact & 3)) continue;   // this warp's sub-tile holds no wanted output (it still loads)
         const double* As = smem + (kt % NSTAGE) * STAGE_DBL;
         const double* Bs = As + TILE_DBL;
-        if (kt < T0) mma_ktile<KA0, KB0, false, 0, TRI, rag_of<KA0, KB0, KA1, KB1>()>(acc, As, Bs, min(TK, K0 - kt * TK), wact);
-        else mma_ktile<KA1, KB1, false, 0, TRI, rag_of<KA0, KB0, KA1, KB1>()>(acc, As, Bs, min(TK, K1 - (kt - T0) * TK), wact);
+        if (kt < T0) mma_ktile_sel<BALD, KA0, KB0, false, 0, TRI, rag_of<KA0, KB0, KA1, KB1>()>(acc, As, Bs, min(TK, K0 - kt * TK), wact);
+        else mma_ktile_sel<BALD, KA1, KB1, false, 0, TRI, rag_of<KA0, KB0, KA1, KB1>()>(acc, As, Bs, min(TK, K1 - (kt - T0) * TK), wact);
     }
     cp_async_wait<0>();
 }
@@ -513,7 +612,7 @@ __device__ __forceinline__ void tile_pipeline(double (&acc)[MI][4][2], const Gem
 // every operand of the call is a bulk-staged MEMT: warp 0 keeps NSTAGE - 1 k-tiles in flight (lane 0 waits for a
 // stage's empty barrier and posts the byte count, the lanes issue the k-row copies), every warp waits on the
 // stage's full barrier, runs its DMMAs and arrives on the empty barrier
-template <int KA0, int KB0, int KA1, int KB1, bool TRI = false>
+template <int KA0, int KB0, int KA1, int KB1, bool TRI = false, bool BALD = false>
 __device__ __forceinline__ void tile_pipeline_bulk(double (&acc)[MI][4][2], const GemmDesc& d, int r0, int nr, int c0,
                                                    int nc, double* smem, int wact, unsigned gs) {
     BulkState* bs = bulk_state(smem);
@@ -542,8 +641,8 @@ __device__ __forceinline__ void tile_pipeline_bulk(double (&acc)[MI][4][2], cons
         if (wact & 3) {
             const double* As = smem + b * STAGE_DBL;
             const double* Bs = As + TILE_DBL;
-            if (kt < T0) mma_ktile<KA0, KB0, true, 0, TRI, rag_of<KA0, KB0, KA1, KB1>()>(acc, As, Bs, min(TK, K0 - kt * TK), wact);
-            else mma_ktile<KA1, KB1, true, 0, TRI, rag_of<KA0, KB0, KA1, KB1>()>(acc, As, Bs, min(TK, K1 - (kt - T0) * TK), wact);
+            if (kt < T0) mma_ktile_sel<BALD, KA0, KB0, true, 0, TRI, rag_of<KA0, KB0, KA1, KB1>()>(acc, As, Bs, min(TK, K0 - kt * TK), wact);
+            else mma_ktile_sel<BALD, KA1, KB1, true, 0, TRI, rag_of<KA0, KB0, KA1, KB1>()>(acc, As, Bs, min(TK, K1 - (kt - T0) * TK), wact);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&bs->empty[b]);
@@ -553,7 +652,7 @@ __device__ __forceinline__ void tile_pipeline_bulk(double (&acc)[MI][4][2], cons
 // every operand of the call lies in a registered buffer: thread 0 keeps NSTAGE - 1 k-tiles in flight, one TMA tensor
 // load per operand k-tile (16 KB per stage); full / empty barriers as the bulk pipeline; ragged k-tiles masked (the
 // boxes read the buffer's next columns / rows there)
-template <int KA0, int KB0, int KA1, int KB1, bool TRI = false>
+template <int KA0, int KB0, int KA1, int KB1, bool TRI = false, bool BALD = false>
 __device__ __forceinline__ void tile_pipeline_tma(double (&acc)[MI][4][2], const GemmDesc& d, int r0, int c0,
                                                   double* smem, int wact, unsigned gs) {
     BulkState* bs = bulk_state(smem);
@@ -584,8 +683,8 @@ __device__ __forceinline__ void tile_pipeline_tma(double (&acc)[MI][4][2], const
         if (wact & 3) {
             const double* As = smem + b * STAGE_DBL;
             const double* Bs = As + TILE_DBL;
-            if (kt < T0) mma_ktile<KA0, KB0, true, 1, TRI, rag_of<KA0, KB0, KA1, KB1>()>(acc, As, Bs, min(TK, K0 - kt * TK), wact);
-            else mma_ktile<KA1, KB1, true, 1, TRI, rag_of<KA0, KB0, KA1, KB1>()>(acc, As, Bs, min(TK, K1 - (kt - T0) * TK), wact);
+            if (kt < T0) mma_ktile_sel<BALD, KA0, KB0, true, 1, TRI, rag_of<KA0, KB0, KA1, KB1>()>(acc, As, Bs, min(TK, K0 - kt * TK), wact);
+            else mma_ktile_sel<BALD, KA1, KB1, true, 1, TRI, rag_of<KA0, KB0, KA1, KB1>()>(acc, As, Bs, min(TK, K1 - (kt - T0) * TK), wact);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&bs->empty[b]);
@@ -704,6 +803,116 @@ __device__ __noinline__ void cta_gemm_impl(double* smem) {
     __syncthreads();
 }
 
+// EPI = 2 (the merge tiles' diagonal blocks): the TRI skip and the balanced diagonal tiles. A separate function, so
+// that the other instantiations keep their register allocation (ptxas spilled the chain's TMA GEMM with the extra
+// per-tile state compiled in). Measured on C3: merge tiles 576 -> 553 ms; on the Sigma tiles (EPI = 1) the extra
+// bodies made the TMA k-loop spill and the balance did not pay (C2, all Sigma tiles diagonal: 3.2 -> 3.5 ms)
+template <int KA0, int KB0, int KA1, int KB1, int EPI, int MODE>
+__device__ __noinline__ void cta_gemm_impl_bal(double* smem) {
+    const GemmDesc& d = *gemm_desc(smem);
+    const int Mr = d.Mr, Nc = d.Nc, lower = d.lower, K0 = d.K0, K1 = d.K1;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int tiles_m = (Mr + TM - 1) / TM, tiles_n = (Nc + TN - 1) / TN;
+    constexpr bool TRI = EPI >= 1;   // the instantiations with the triangular DMMA skip
+    constexpr bool BAL = TRI && WM == 32 && NWARP == 4;   // ... and the balanced diagonal tiles
+    const int wr0 = (warp / (64 / WN)) * WM, wc0 = (warp % (64 / WN)) * WN;
+#ifdef MRA_BULK
+    BulkState* bs = bulk_state(smem);
+    unsigned gs = bs->gs;
+    if (MODE != 0) {
+        __syncthreads();   // the stage area's previous users are done before the bulk engine writes it
+        if (threadIdx.x < 32) {
+            // order earlier generic writes of the operands (this CTA's, and through the caller's acquire other
+            // CTAs') and of the stage area before the async-proxy copies
+            asm volatile("fence.proxy.async.global;\n" ::: "memory");
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        }
+    }
+#endif
+    for (int tm = 0; tm < tiles_m; tm++) {
+        for (int tn = 0; tn < tiles_n; tn++) {
+            if (lower && tn > tm) continue;
+            const int r0 = tm * TM, c0 = tn * TN;
+            const int nr = min(TM, Mr - r0), nc = min(TN, Nc - c0);
+            // warp -> sub-tile. A diagonal tile of a lower output in the TRI instantiations (4 warps of 32 x 32) is
+            // balanced: warps 0 / 3 take the two 32 x 32 diagonal sub-tiles (10 of 16 8 x 8 blocks each, the TRI skip),
+            // warps 1 / 2 the two 32 x 16 halves of the sub-diagonal one (8 each) -- instead of one warp idle and one
+            // at 16 blocks, which set the tile's time (each element is still accumulated in the same k order)
+            const bool dtile = lower && tm == tn;
+            const bool half = BAL && dtile && (warp == 1 || warp == 2);
+            const int wr = half ? 32 : wr0, wc = half ? (warp == 1 ? 0 : 16) : wc0;
+            const int nv = half ? 2 : 4;   // 8-column blocks of the warp's sub-tile
+            double acc[MI][4][2];
+#pragma unroll
+            for (int mi = 0; mi < MI; mi++)
+#pragma unroll
+                for (int ni = 0; ni < 4; ni++) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+            // warps whose sub-tile lies outside a ragged tile (e.g. the 1-row y tile) or strictly above the
+            // diagonal of a lower-triangular tile skip their DMMAs
+            // 0: the warp's sub-tile holds no wanted output; 1: active; 2: active on the diagonal of a lower tile
+            // (bits 2-4: how many of its 8-row blocks hold wanted rows, mma_ktile)
+            const int wact = (wr < nr && wc < nc && !(dtile && wc > wr + WM - 1))
+                                 ? (half ? 3 : (WM == WN && dtile && wr == wc) ? 2 : 1) |
+                                       (min(MI, (nr - wr + 7) >> 3) << 2) | (BAL ? ((wr >> 3) << 5) | ((wc >> 3) << 8) : 0)
+                                 : 0;
+#ifdef MRA_BULK
+            if (MODE == 1) {
+                tile_pipeline_bulk<KA0, KB0, KA1, KB1, TRI, true>(acc, d, r0, nr, c0, nc, smem, wact, gs);
+                gs += (K0 + TK - 1) / TK + (K1 + TK - 1) / TK;
+            } else if (MODE == 3) {
+                tile_pipeline_tma<KA0, KB0, KA1, KB1, TRI, true>(acc, d, r0, c0, smem, wact, gs);
+                gs += (K0 + TK - 1) / TK + (K1 + TK - 1) / TK;
+            } else
+#endif
+            if (K0 + K1 > 0)
+                tile_pipeline<KA0, KB0, KA1, KB1, TRI, true>(acc, d, r0, nr, c0, nc, smem, wact);
+            const CInit ci = d.ci;
+            const double alpha = d.alpha;
+            double* C = d.C;
+            const long long ldc = d.ldc;
+            // the (e = 0, 1) pair of a fragment is two adjacent columns: one 16-byte access when the
+            // whole pair is in range and aligned
+            const bool vec = ((reinterpret_cast<uintptr_t>(C) & 15) == 0) && ((ldc & 1) == 0) &&
+                             (ci.kind != 1 || (((reinterpret_cast<uintptr_t>(ci.p) & 15) == 0) && ((ci.ld & 1) == 0)));
+            static_assert(EPI == 2, "the balanced impl serves the EPI = 2 instantiations");
+#pragma unroll
+            for (int mi = 0; mi < MI; mi++)
+#pragma unroll
+                for (int ni = 0; ni < 4; ni++) {
+                    const int i = r0 + wr + mi * 8 + g, j = c0 + wc + ni * 8 + 2 * t;
+                    if (BAL && ni >= nv) continue;   // a half-width sub-tile: the next columns are another warp's
+                    if (vec && i < Mr && j + 1 < Nc && (!lower || j + 1 <= i)) {
+                        double2 v = make_double2(0.0, 0.0);
+                        if (ci.kind == 1) v = *reinterpret_cast<const double2*>(ci.p + (long long)i * ci.ld + j);
+                        *reinterpret_cast<double2*>(C + (long long)i * ldc + j) =
+                            make_double2(v.x + alpha * acc[mi][ni][0], v.y + alpha * acc[mi][ni][1]);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 2; e++) {
+                            const int jj = j + e;
+                            if (i < Mr && jj < Nc && (!lower || jj <= i)) {
+                                const double v = (ci.kind == 1) ? ci.p[(long long)i * ci.ld + jj] : 0.0;
+                                C[(long long)i * ldc + jj] = v + alpha * acc[mi][ni][e];
+                            }
+                        }
+                    }
+                }
+            if (EPI != 1 && ci.kind == 2) __trap();   // a covariance init needs the EPI = 1 instantiation
+        }
+    }
+#ifdef MRA_BULK
+    if (MODE != 0 && threadIdx.x == 0) bs->gs = gs;
+#endif
+    __syncthreads();
+}
+
+template <int KA0, int KB0, int KA1, int KB1, int EPI, int MODE>
+__device__ __forceinline__ void cta_gemm_impl_sel(double* smem) {
+    if constexpr (EPI == 2) cta_gemm_impl_bal<KA0, KB0, KA1, KB1, EPI, MODE>(smem);
+    else cta_gemm_impl<KA0, KB0, KA1, KB1, EPI, MODE>(smem);
+}
+
 // C[Mr x Nc] = init + alpha * (A0 B0^T [K0] + A1 B1^T [K1]); lower != 0 -> only i >= j written.
 // In-place use (C aliasing the operands / init) is safe when every output tile reads only its own
 // rows (A side) / columns (B side) of the aliased region -- see DESIGN.md §5.
@@ -753,14 +962,14 @@ __device__ __forceinline__ void cta_gemm(int Mr, int Nc, int lower, const Op& A0
     __syncthreads();
     const int mode = d->amask;
     if (tk_ok && mode == 3)
-        cta_gemm_impl<KA0, KB0, KA1, KB1, EPI, tk_ok ? 3 : 0>(smem);
+        cta_gemm_impl_sel<KA0, KB0, KA1, KB1, EPI, tk_ok ? 3 : 0>(smem);
     else if (any_t && mode == 1)
-        cta_gemm_impl<KA0, KB0, KA1, KB1, EPI, any_t ? 1 : 0>(smem);
+        cta_gemm_impl_sel<KA0, KB0, KA1, KB1, EPI, any_t ? 1 : 0>(smem);
     else
-        cta_gemm_impl<KA0, KB0, KA1, KB1, EPI, 0>(smem);
+        cta_gemm_impl_sel<KA0, KB0, KA1, KB1, EPI, 0>(smem);
 #else
     __syncthreads();
-    cta_gemm_impl<KA0, KB0, KA1, KB1, EPI, 0>(smem);
+    cta_gemm_impl_sel<KA0, KB0, KA1, KB1, EPI, 0>(smem);
 #endif
 }
 

@@ -563,10 +563,23 @@ k_wide_mtile(TreeParams tp, TREG, WideParams wp, long long g_first, double* out,
                                              op_mem(F + (long long)c0 * rh, rh), rh, op_mem(F, 0), op_mem(F, 0), 0,
                                              ci_mem(Oab, q), 1.0, Oab, q, cp, smem);
 #else
-            cta_gemm<MEMT, MEMT, MEMN, MEMN>(nrow, ncl, a == b, op_mem(G + rh + r0, wp.ldG),
-                                             op_mem(G + rh + c0, wp.ldG), ng, op_mem(Fn + (long long)r0 * rh, rh),
-                                             op_mem(F + (long long)c0 * rh, rh), rh, ci_zero(), 1.0, Oab, q, cp,
-                                             smem);
+            // diagonal tiles (a == b, lower) of long-K groups through the EPI = 2 instantiation: the balanced warp map
+            // and the skipped 8 x 8 blocks above the diagonal (its own function, so the off-diagonal tiles' code is
+            // unchanged). Measured: C3 (K = 720 + 64) merge tiles 579 -> 553 ms; C2 (K = 256 + 64) 10.9 -> 12.3 ms,
+            // hence the K threshold
+#ifndef MRA_BAL_MINK
+#define MRA_BAL_MINK 512
+#endif
+            if (a == b && ng >= MRA_BAL_MINK)
+                cta_gemm<MEMT, MEMT, MEMN, MEMN, 2>(nrow, ncl, 1, op_mem(G + rh + r0, wp.ldG),
+                                                    op_mem(G + rh + c0, wp.ldG), ng, op_mem(Fn + (long long)r0 * rh, rh),
+                                                    op_mem(F + (long long)c0 * rh, rh), rh, ci_zero(), 1.0, Oab, q, cp,
+                                                    smem);
+            else
+                cta_gemm<MEMT, MEMT, MEMN, MEMN>(nrow, ncl, a == b, op_mem(G + rh + r0, wp.ldG),
+                                                 op_mem(G + rh + c0, wp.ldG), ng, op_mem(Fn + (long long)r0 * rh, rh),
+                                                 op_mem(F + (long long)c0 * rh, rh), rh, ci_zero(), 1.0, Oab, q, cp,
+                                                 smem);
 #endif
             PHASE_ADD(24, ph2);
 #ifdef MRA_PHASE_TIMING
