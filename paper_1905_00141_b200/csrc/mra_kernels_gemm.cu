@@ -245,28 +245,29 @@ k_wide_trsm(TreeParams tp, TREG, WideParams wp, const int4* tasks, long long nta
         const double* Sl = wp.S + wp.S_off[l];
         if (tk.z == 2) {
             // the y column alone (ncol = 64 k + 1): g = X y by rows, X[i][K] = Sl[K ld + i] (K < block start)
-            // and the inverted diagonal block; row chunks descending so g can overwrite y in place
+            // and the inverted diagonal block. y is first staged in shared memory (g_i needs y_k for k <= i only, so
+            // the snapshot gives the in-place result); each thread's loads of its X row then run back to back
+            // (unrolled; the two accumulators keep their order)
             double* gcol = wp.G + (tp.leaf_off[l] - wp.G_base) * wp.ldG + (ncol - 1);
-            for (int base = ((n - 1) / NT) * NT; base >= 0; base -= NT) {
-                const int i = base + threadIdx.x;
-                double v = 0.0;
-                if (i < n) {
-                    const int bi = i / 64, i0 = 64 * bi;
-                    double s0 = 0.0, s1 = 0.0;
-                    int k = 0;
-                    for (; k + 1 < i0; k += 2) {
-                        s0 += Sl[(long long)k * ld + i] * gcol[(long long)k * wp.ldG];
-                        s1 += Sl[(long long)(k + 1) * ld + i] * gcol[(long long)(k + 1) * wp.ldG];
-                    }
-                    if (k < i0) s0 += Sl[(long long)k * ld + i] * gcol[(long long)k * wp.ldG];
-                    const double* Di = wp.D + wp.D_off[l] + 4096LL * bi + (long long)(i - i0) * 64;
-                    for (int kk = 0; kk <= i - i0; kk++) s1 += Di[kk] * gcol[(long long)(i0 + kk) * wp.ldG];
-                    v = s0 + s1;
+            double* ys = smem;   // n <= ncol doubles: the GEMM stage area is idle between calls
+            for (int i = threadIdx.x; i < n; i += NT) ys[i] = gcol[(long long)i * wp.ldG];
+            __syncthreads();
+            for (int i = threadIdx.x; i < n; i += NT) {
+                const int bi = i / 64, i0 = 64 * bi;
+                double s0 = 0.0, s1 = 0.0;
+                int k = 0;
+#pragma unroll 4
+                for (; k + 1 < i0; k += 2) {
+                    s0 += Sl[(long long)k * ld + i] * ys[k];
+                    s1 += Sl[(long long)(k + 1) * ld + i] * ys[k + 1];
                 }
-                __syncthreads();
-                if (i < n) gcol[(long long)i * wp.ldG] = v;
-                __syncthreads();
+                if (k < i0) s0 += Sl[(long long)k * ld + i] * ys[k];
+                const double* Di = wp.D + wp.D_off[l] + 4096LL * bi + (long long)(i - i0) * 64;
+#pragma unroll 4
+                for (int kk = 0; kk <= i - i0; kk++) s1 += Di[kk] * ys[i0 + kk];
+                gcol[(long long)i * wp.ldG] = s0 + s1;
             }
+            __syncthreads();   // ys is free for the next task
             continue;
         }
         const int c0 = 64 * tk.y, nc = min(64, ncol - c0);
