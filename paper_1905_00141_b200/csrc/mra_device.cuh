@@ -176,6 +176,15 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
+// compile-time loop: f(integral_constant<int, I>) for I in [B, E)
+template <int B, int E, typename F>
+__device__ __forceinline__ void sfor(F&& f) {
+    if constexpr (B < E) {
+        f(std::integral_constant<int, B>());
+        sfor<B + 1, E>(f);
+    }
+}
+
 // ------------------------------------------------------------- async tile staging
 #ifndef MRA_NSTAGE
 #define MRA_NSTAGE 3
@@ -757,20 +766,31 @@ __device__ __noinline__ void cta_gemm_impl(double* smem) {
             if (EPI == 1 && ci.kind == 2) {
                 // covariance initial value (Sigma tiles): C = alpha acc + (C(s_i, s_j) + diag), one store per element;
                 // the covariance chains run unconditionally on clamped (valid) points and only the store is
-                // predicated, so no branch splits the unrolled chains
+                // predicated, so no branch splits the unrolled chains. A warp with nothing to store computes
+                // nothing, and a warp on the diagonal of a diagonal tile only the 8 x 8 blocks on or below it (its
+                // own straight-line body): the generation is a fifth of the Sigma tile's fp64-pipe time
                 const CovP cpl = d.cp;
-#pragma unroll
-                for (int mi = 0; mi < MI; mi++) {
-                    const int i = r0 + wr + mi * 8 + g;
-                    const double2 pi = ldpt(ci.p, min(i, Mr - 1));
-#pragma unroll
-                    for (int q = 0; q < 8; q++) {
-                        const int ni = q >> 1, e = q & 1, j = c0 + wc + ni * 8 + 2 * t + e;
-                        const double2 pj = ldpt(ci.q, min(j, Nc - 1));
-                        const double w = covf(cpl, pi.x, pi.y, pj.x, pj.y) + (i == j ? ci.diag : 0.0);
-                        if (i < Mr && j < Nc && (!lower || j <= i))
-                            C[(long long)i * ldc + j] = __dadd_rn(__dmul_rn(alpha, acc[mi][ni][e]), w);
-                    }
+                auto cov_store = [&](auto diagc) {
+                    constexpr bool DIAG = decltype(diagc)::value;
+                    sfor<0, MI>([&](auto mic) {
+                        constexpr int mi = decltype(mic)::value;
+                        const int i = r0 + wr + mi * 8 + g;
+                        const double2 pi = ldpt(ci.p, min(i, Mr - 1));
+                        sfor<0, 8>([&](auto qc) {
+                            constexpr int q = decltype(qc)::value, ni = q >> 1, e = q & 1;
+                            if constexpr (!(DIAG && ni > mi)) {
+                                const int j = c0 + wc + ni * 8 + 2 * t + e;
+                                const double2 pj = ldpt(ci.q, min(j, Nc - 1));
+                                const double w = covf(cpl, pi.x, pi.y, pj.x, pj.y) + (i == j ? ci.diag : 0.0);
+                                if (i < Mr && j < Nc && (!lower || j <= i))
+                                    C[(long long)i * ldc + j] = __dadd_rn(__dmul_rn(alpha, acc[mi][ni][e]), w);
+                            }
+                        });
+                    });
+                };
+                if (wact & 3) {
+                    if (WM == WN && lower && tm == tn && wr == wc) cov_store(std::true_type());
+                    else cov_store(std::false_type());
                 }
             } else
 #pragma unroll
