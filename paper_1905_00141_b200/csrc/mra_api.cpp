@@ -169,6 +169,7 @@ struct mra_plan {
     struct WideSub {
         long long g0 = 0, gcount = 0;
         long long chain_off = 0, chain_n = 0, sigma_off = 0, sigma_n = 0;
+        long long cs_off = 0, cs_n = 0;   // fused chain + Sigma list (k_wide_chsig), cs_n = 0: separate kernels
         std::vector<long long> upd_off, upd_n, diag_off, diag_n, pf_off, pf_n, tr_off, tr_n;
         long long trsm_off = 0, trsm_n = 0, mt_off = 0, mt_n = 0;
     };
@@ -626,6 +627,17 @@ static mra_status size_device(mra_plan* P, double budget_gb, int stream_opt) {
     return MRA_OK;
 }
 
+// chain + Sigma as one dataflow kernel (MRA_CHSIG=1) and the lag, in leaves, of a leaf's Sigma tiles behind its
+// chain tasks (MRA_CS_LAG)
+static bool chsig_on() {
+    static const bool on = [] { const char* e = getenv("MRA_CHSIG"); return e && atoi(e) != 0; }();
+    return on;
+}
+static long long chsig_lag() {
+    static const long long lag = [] { const char* e = getenv("MRA_CS_LAG"); return e ? std::max(1LL, atoll(e)) : 40LL; }();
+    return lag;
+}
+
 // Wide path: split every posterior chunk's level-(M-1) groups into sub-chunks whose Sigma_j fit the
 // budget, and precompute each sub-chunk's task lists (int4 {leaf, i, k, 0}).
 static mra_status size_wide(mra_plan* P, double budget, bool explicit_budget) {
@@ -692,6 +704,24 @@ static mra_status size_wide(mra_plan* P, double budget, bool explicit_budget) {
                         for (int k = 0; k <= i; k++) tasks.push_back(make_int4((int)l, i, k, 0));
                 }
                 ws.sigma_n = (long long)tasks.size() - ws.sigma_off;
+                // the same chain and Sigma tasks as one dataflow (k_wide_chsig): leaf l's Sigma tiles follow the
+                // chain tasks of leaf l + lag (type in .w)
+                if (chsig_on()) {
+                    const long long L0 = ws.g0 * J, L1 = (ws.g0 + ws.gcount) * J, lag = chsig_lag();
+                    auto push_sig = [&](long long l) {
+                        const int T = (int)((leaf_n(l) + 63) / 64);
+                        for (int i = 0; i < T; i++)
+                            for (int k = 0; k <= i; k++) tasks.push_back(make_int4((int)l, i, k, 1));
+                    };
+                    ws.cs_off = (long long)tasks.size();
+                    for (long long l = L0; l < L1; l++) {
+                        const int T = (int)((leaf_n(l) + 63) / 64);
+                        for (int i = 0; i < T; i++) tasks.push_back(make_int4((int)l, i, 0, 0));
+                        if (l - lag >= L0) push_sig(l - lag);
+                    }
+                    for (long long l = std::max(L0, L1 - lag); l < L1; l++) push_sig(l);
+                    ws.cs_n = (long long)tasks.size() - ws.cs_off;
+                }
                 // super-blocked Cholesky of the leaves' Sigma_j (blocks of 64, super-blocks of NBS blocks):
                 // left-looking inside a super-block, one right-looking trailing update after it, so the
                 // late steps of large leaves (C4: up to 139 blocks) keep every CTA busy with K = 64 NBS
@@ -800,7 +830,7 @@ static mra_status size_wide(mra_plan* P, double budget, bool explicit_budget) {
         P->mring.maxg = maxgc;
         P->mring.stride = round_up(4096 + (long long)rh * rh + 2LL * qm * rh, 32);   // A_oo | Li | F | -F
         if ((s = dalloc(P, (void**)&P->mring.slot, 8 * P->mring.stride * ns, "merge slots"))) return s;
-        if ((s = dalloc(P, (void**)&P->mring.flags, 4 * 3 * maxgc, "merge flags"))) return s;
+        if ((s = dalloc(P, (void**)&P->mring.flags, 4 * (3 + J) * maxgc, "merge flags"))) return s;
         P->mring.chol_done = P->mring.flags;
         P->mring.f_done = P->mring.flags + maxgc;
         P->mring.o_done = P->mring.flags + 2 * maxgc;
@@ -1323,8 +1353,13 @@ static mra_status eval_wide(mra_plan* P, const TreeParams& tp, long long gf, lon
         if (w.g0 != gf + done) return fail(MRA_E_CUDA, "internal: wide sub-chunk schedule out of order");
         wp.G_base = P->leaf_off[w.g0 * P->J];
         LCHK_K(KIND_COVGEN, launch_wide(6, tp, P->treg, wp, 0, P->wtasks + w.chain_off, w.chain_n, P->grid, take_counter(P), st));
-        LCHK_K(KIND_CHAIN, launch_wide(0, tp, P->treg, wp, 0, P->wtasks + w.chain_off, w.chain_n, P->grid, take_counter(P), st));
-        LCHK_K(KIND_SIGMA, launch_wide(1, tp, P->treg, wp, 0, P->wtasks + w.sigma_off, w.sigma_n, P->grid, take_counter(P), st));
+        if (w.cs_n > 0) {
+            LCHK_K(KIND_CHAIN, launch_wide_chsig(tp, P->treg, wp, P->wtasks + w.cs_off, w.cs_n, take_counter(P),
+                                                 P->mring.flags + 3 * P->mring.maxg, w.g0 * P->J, w.gcount * P->J, st));
+        } else {
+            LCHK_K(KIND_CHAIN, launch_wide(0, tp, P->treg, wp, 0, P->wtasks + w.chain_off, w.chain_n, P->grid, take_counter(P), st));
+            LCHK_K(KIND_SIGMA, launch_wide(1, tp, P->treg, wp, 0, P->wtasks + w.sigma_off, w.sigma_n, P->grid, take_counter(P), st));
+        }
         constexpr int NBS = 8;   // as in size_wide
         for (size_t s2 = 0; s2 < w.diag_n.size(); s2++) {
             const int kb0 = (int)s2 / NBS * NBS;

@@ -94,7 +94,7 @@ struct MergeRing {
     long long stride;
     int ns;
     long long maxg;         // groups per launch (counter arrays)
-    int* flags;             // [3 * maxg]: chol_done | f_done | o_done
+    int* flags;             // [(3 + J) * maxg]: chol_done | f_done | o_done | leaf_done (k_wide_chsig, J * maxg)
     int *chol_done, *f_done, *o_done;
     long long* slot_done;   // [ns] groups that have released the slot
 };
@@ -142,6 +142,9 @@ int unit_ctas_per_sm();
 void init_kernel_attrs();   // every kernel's smem attribute / occupancy for the current device (before any capture)
 void phase_cycles_unit(unsigned long long* out32, bool reset);
 int wide_mtile_resident();
+cudaError_t launch_wide_chsig(const TreeParams& tp, const TmaReg& reg, const WideParams& wp, const int4* tasks,
+                              long long ntask, unsigned long long* counter, int* leaf_done, long long l0,
+                              long long nleaf, cudaStream_t st);
 cudaError_t launch_wide_mtile(const TreeParams& tp, const TmaReg& reg, const WideParams& wp, long long g_first,
                               long long g_count,
                               double* out, long long out_first, int q, const int4* tasks, long long ntask, int grid,

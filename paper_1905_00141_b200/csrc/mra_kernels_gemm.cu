@@ -109,6 +109,56 @@ k_wide_sigma(TreeParams tp, TREG, WideParams wp, const int4* tasks, long long nt
     }
 }
 
+// chain and Sigma tasks of one sub-chunk as one dataflow (host-ordered list, int4 {leaf, i, k, type}: type 0 the
+// V chain of row tile i, type 1 the Sigma tile (i, k)); the host puts a leaf's Sigma tiles `lag` leaves after its
+// chain tasks, so they normally run while the leaf's V rows are still in L2 (the phase-separated kernels read them
+// back from DRAM: the whole sub-chunk's chain runs first). A Sigma task waits for its leaf's chain tasks, claimed
+// earlier by co-resident CTAs (the grid is exactly the resident CTA count), so the waits always terminate.
+__global__ void __launch_bounds__(NT, MRA_MINB)
+k_wide_chsig(TreeParams tp, TREG, WideParams wp, const int4* tasks, long long ntask, unsigned long long* counter,
+             int* leaf_done, long long l0) {
+    double* smem = dyn_smem();
+    ENGINE_INIT(smem);
+    const CovP cp = covp_of(tp);
+    const int m = tp.M - 1, Pg = m * tp.rh;
+    for (;;) {
+        const long long it = next_item(counter, smem);
+        if (it >= ntask) break;
+        const int4 tk = tasks[it];
+        const long long l = tk.x;
+        const long long o = tp.leaf_off[l];
+        const int nl = leaf_n(tp, l);
+        if (tk.w == 0) {
+            const int n = min(64, nl - 64 * tk.y);
+            double* Gr = wp.G + (o + 64LL * tk.y - wp.G_base) * wp.ldG;
+            point_chain_pre(tp, m, l >> tp.lj, n, Gr, wp.ldG, cp, smem);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                __threadfence();
+                atomicAdd(leaf_done + (l - l0), 1);
+            }
+        } else {
+            if (threadIdx.x == 0) {
+                const int T = (nl + 63) / 64;
+                while (*(volatile int*)(leaf_done + (l - l0)) < T) __nanosleep(100);
+                __threadfence();
+            }
+            __syncthreads();
+            const int i = tk.y, k = tk.z;
+            const int ld = wp.S_ld[l];
+            double* C = wp.S + wp.S_off[l] + 64LL * i * ld + 64LL * k;
+            const double* Gi = wp.G + (o - wp.G_base + 64LL * i) * wp.ldG;
+            const double* Gk = wp.G + (o - wp.G_base + 64LL * k) * wp.ldG;
+            cta_gemm<MEMN, MEMN, MEMN, MEMN, 1>(min(64, nl - 64 * i), min(64, nl - 64 * k), i == k,
+                                                 op_mem(Gi, wp.ldG), op_mem(Gk, wp.ldG), Pg, op_mem(Gi, 0),
+                                                 op_mem(Gi, 0), 0,
+                                                 ci_cov(tp.pxy + 2 * (o + 64LL * i), tp.pxy + 2 * (o + 64LL * k),
+                                                        i == k ? tau2_of(tp) : 0.0),
+                                                 -1.0, C, ld, cp, smem);
+        }
+    }
+}
+
 // ---- factorization task bodies of the per-step kernels
 // update tile (i, j) of leaf l: A_ij -= A_{i,K} A_{j,K}^T over block columns [k0, k0 + K)
 __device__ __forceinline__ void wide_upd_tile(const TreeParams& tp, const WideParams& wp, long long l, int i, int j,
@@ -759,7 +809,7 @@ k_merge_sum(int J, int qc, long long t_first, long long t_count, double* child_o
 constexpr int MAXDEV = 64;
 struct GemmAttrs {
     bool done = false;
-    int resident[9] = {1, 1, 1, 1, 1, 1, 1, 1, 1};
+    int resident[10] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 1};
     int nsm = 148;
 };
 static GemmAttrs g_gemm_attrs[MAXDEV];
@@ -775,11 +825,12 @@ static const GemmAttrs& gemm_set_attrs() {
     std::lock_guard<std::mutex> lk(g_gemm_mu);
     if (A.done) return A;
     const int b = gemm_smem_bytes();
-    const void* ks[9] = {(const void*)k_wide_chain,   (const void*)k_wide_sigma, (const void*)k_wide_update,
-                         (const void*)k_wide_diag,    (const void*)k_wide_panel_x, (const void*)k_wide_trsm,
-                         (const void*)k_wide_mtile,   (const void*)k_prior,      (const void*)k_merge};
+    const void* ks[10] = {(const void*)k_wide_chain,   (const void*)k_wide_sigma, (const void*)k_wide_update,
+                          (const void*)k_wide_diag,    (const void*)k_wide_panel_x, (const void*)k_wide_trsm,
+                          (const void*)k_wide_mtile,   (const void*)k_prior,      (const void*)k_merge,
+                          (const void*)k_wide_chsig};
     cudaDeviceGetAttribute(&A.nsm, cudaDevAttrMultiProcessorCount, dev);
-    for (int i = 0; i < 9; i++) {
+    for (int i = 0; i < 10; i++) {
         cudaFuncSetAttribute(ks[i], cudaFuncAttributeMaxDynamicSharedMemorySize, b);
         int per = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ks[i], NT, b);
@@ -808,6 +859,21 @@ cudaError_t launch_wide(int phase, const TreeParams& tp, const TmaReg& reg, cons
         case 5: ++g_kernel_launches; k_wide_trsm<<<(int)g, NT, b, st>>>(tp, reg, wp, tasks, ntask, counter); break;
         default: return cudaErrorInvalidValue;
     }
+    return cudaGetLastError();
+}
+
+// chain + Sigma dataflow of one sub-chunk (k_wide_chsig): leaf_done[nleaf] counters zeroed here; the grid is the
+// resident CTA count (Sigma tasks wait on chain tasks claimed earlier by co-resident CTAs)
+cudaError_t launch_wide_chsig(const TreeParams& tp, const TmaReg& reg, const WideParams& wp, const int4* tasks,
+                              long long ntask, unsigned long long* counter, int* leaf_done, long long l0,
+                              long long nleaf, cudaStream_t st) {
+    long long g = gemm_set_attrs().resident[9];
+    if (ntask < g) g = ntask;
+    if (g < 1) return cudaSuccess;
+    cudaError_t e = cudaMemsetAsync(leaf_done, 0, sizeof(int) * nleaf, st);
+    if (e != cudaSuccess) return e;
+    ++g_kernel_launches;
+    k_wide_chsig<<<(int)g, NT, gemm_smem_bytes(), st>>>(tp, reg, wp, tasks, ntask, counter, leaf_done, l0);
     return cudaGetLastError();
 }
 
