@@ -395,3 +395,30 @@ def test_axis_scaled_distance_pins(xs, ys, J, cov):
     if J == 4 and xs == 2.0 and ys == 0.5:
         alt = oracle.run(x * 2.0, y * 0.5, z, 3, J, 9, theta)["loglik"]
         assert abs(got - alt) <= 1e-12 * abs(alt)
+
+
+def test_single_bar_midpoint_R7():
+    """DESIGN R7 / R5 / R6: one bar sits at the box midpoint. Boxes written out by hand from R8 / R9
+    (points {0,1}^2: root [0, 1.01]^2, J = 4 children SW, SE, NW, NE split at 0.505): r = 1 gives r_hat = 1 and
+    one knot at each interior region's centre; r = 2 gives 2 x-bars (R6: lo + off ext, hi - off ext) and 1 y-bar
+    (the midpoint), knots row-major by (y, x). The midpoint is also the mean of R6's bar set for any bar count
+    (R6's bars are symmetric about it), which the last check confirms on the oracle's 6 x 5 example."""
+    x = np.array([0.0, 1.0, 0.0, 1.0]); y = np.array([0.0, 0.0, 1.0, 1.0])
+    e = 1.01
+    h = e / 2
+    boxes = [(0.0, e, 0.0, e), (0.0, h, 0.0, h), (h, e, 0.0, h), (0.0, h, h, e), (h, e, h, e)]   # xlo, xhi, ylo, yhi
+    off = oracle.E_OVER_100
+    p1 = oracle.plan(x, y, 3, 4, 1)
+    assert p1["r_hat"] == 1
+    for k, (x0, x1, y0, y1) in enumerate(boxes):
+        assert abs(p1["knots_x"][k, 0] - 0.5 * (x0 + x1)) <= 1e-15
+        assert abs(p1["knots_y"][k, 0] - 0.5 * (y0 + y1)) <= 1e-15
+    p2 = oracle.plan(x, y, 3, 4, 2)
+    assert p2["r_hat"] == 2
+    for k, (x0, x1, y0, y1) in enumerate(boxes):
+        ex = x1 - x0
+        np.testing.assert_allclose(p2["knots_x"][k], [x0 + off * ex, x1 - off * ex], rtol=0, atol=1e-15)
+        np.testing.assert_allclose(p2["knots_y"][k], [0.5 * (y0 + y1)] * 2, rtol=0, atol=1e-15)
+    p30 = oracle.plan(x, y, 2, 4, 32)
+    assert abs(np.mean(np.unique(p30["knots_x"][0])) - h) <= 1e-15
+    assert abs(np.mean(np.unique(p30["knots_y"][0])) - h) <= 1e-15
